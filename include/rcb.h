@@ -1,0 +1,159 @@
+/*
+ * rcb.h — C ABI of the B200-native Region Competition hot path
+ * (librcseg_b200.so, built for sm_100a).
+ *
+ * The reference (rcseg, /root/reference/pkg/src/rcseg) is pure Python on
+ * numpy arrays; it has no FFI.  Each entry point below replaces one reference
+ * function and is what a maintainer would bind with ctypes.
+ * All arrays are plain C-order host pointers; sizes are explicit; no torch
+ * types.  Lattices are described by (ndim, dims[ndim]); flat indices are
+ * C-order over dims, exactly as in the reference (grid.py:1-8).
+ *
+ * Every function returns RCB_OK (0) or a negative status; the message of the
+ * last failure on the calling thread is rcb_last_error().  The Python shim
+ * maps statuses to the reference's exception types (ValueError,
+ * RuntimeError, DegenerateStatsError, StaleParticleError).
+ */
+#ifndef RCB_H
+#define RCB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCB_OK 0
+#define RCB_ERR_VALUE -1      /* bad argument            -> ValueError */
+#define RCB_ERR_CUDA -2       /* CUDA runtime failure     -> RuntimeError */
+#define RCB_ERR_CAPACITY -3   /* output buffer too small; *n holds the size needed */
+#define RCB_ERR_DEGENERATE -4 /* empty region mean        -> DegenerateStatsError */
+#define RCB_ERR_NODEVICE -5   /* no CUDA device           -> RuntimeError */
+
+/* energy.py:37-50  EnergyConfig */
+typedef struct {
+    int32_t region_model;   /* 0 = "pc", 1 = "ps" */
+    int32_t noise_model;    /* 0 = "gauss", 1 = "poisson" */
+    double lam;
+    int32_t smooth_radius;
+} rcb_energy_cfg;
+
+/* sobolev.py:18-31 SobolevParams, plus the host-evaluated kernel table
+ * w[d2] = kernel_eval(sqrt(d2)) for every integer d2 < (E/2)^2
+ * (sobolev.py:34-49, 121). */
+typedef struct {
+    double length_scale;
+    double epsilon;
+    const double *weights;  /* n_weights entries, copied at create time */
+    int32_t n_weights;
+} rcb_sobolev_cfg;
+
+/* optimizer.py:36-56 OptimizerConfig (the fields the device iteration uses;
+ * oscillation/resync/drift policy stays in the host driver). */
+typedef struct {
+    int32_t gradient;       /* 0 = "l2", 1 = "sobolev" */
+    double move_budget;
+    uint64_t seed;
+    int32_t allow_fusion;
+    int32_t allow_vanish;
+    int32_t vanish_grace;
+    int32_t full_fg;        /* Connectivity: 1 = default (8/26 fg), 0 = (4/6 fg) */
+} rcb_opt_cfg;
+
+/* optimizer.py:58-65 IterationRecord (device part). */
+typedef struct {
+    int64_t iteration;
+    double energy;          /* incremental ledger after the iteration */
+    int64_t moves;
+    int64_t particles;      /* len(contour) after the iteration */
+    int64_t candidates;     /* particles scored this iteration */
+    int64_t negative;       /* candidates with rank < 0 */
+    int64_t pairs;          /* Sobolev particle interactions (0 in l2 mode) */
+    int32_t mode;           /* 0 = l2, 1 = sobolev */
+} rcb_iter_record;
+
+typedef struct rcb_engine rcb_engine;
+
+int32_t rcb_version(void);
+const char *rcb_last_error(void);
+int32_t rcb_device_count(int32_t *n);
+
+/* ---- function-level drop-ins ------------------------------------------ */
+
+/* sobolev.py:137-174 sobolev_filter(coords, owners, competitors, raw, params)
+ * coords: n x ndim int64 (non-negative); out: n doubles.  *n_pairs receives
+ * the interaction count len(CellList.pairs(cutoff)[0]) (sobolev.py:99-122). */
+int32_t rcb_sobolev_filter(const int64_t *coords, int64_t n, int32_t ndim,
+                           const int64_t *owners, const int64_t *competitors,
+                           const double *raw, const rcb_sobolev_cfg *params,
+                           double *out, int64_t *n_pairs);
+
+/* contour.py:84-116 scan_contour(labels, conn) + as_arrays: particles sorted
+ * by (x, competitor).  If cap < count, returns RCB_ERR_CAPACITY with *n set. */
+int32_t rcb_scan_contour(const int32_t *labels, int32_t ndim, const int64_t *dims,
+                         int32_t full_fg, int64_t *xs, int64_t *owners,
+                         int64_t *competitors, int64_t cap, int64_t *n);
+
+/* energy.py:111-126 delta_internal_batch(labels, pixels, owners, competitors) */
+int32_t rcb_delta_internal_batch(const int32_t *labels, int32_t ndim, const int64_t *dims,
+                                 const int64_t *xs, const int64_t *owners,
+                                 const int64_t *competitors, int64_t n, int64_t *out);
+
+/* energy.py:302-372 EnergyModel.delta_external_batch.  PC reads the caller's
+ * region statistics (count/total/total_sq, n_labels entries — the model's
+ * StatsTable, grid.py:142-188); PS rebuilds the ball fields from labels. */
+int32_t rcb_delta_external_batch(const double *image, const int32_t *labels, int32_t ndim,
+                                 const int64_t *dims, const rcb_energy_cfg *cfg,
+                                 int32_t n_labels, const int64_t *count, const double *total,
+                                 const double *total_sq, const int64_t *xs,
+                                 const int64_t *owners, const int64_t *competitors, int64_t n,
+                                 double *out);
+
+/* grid.py:155-169 StatsTable.from_labels (raster-order sequential sums). */
+int32_t rcb_stats_from_labels(const double *image, const int32_t *labels, int64_t size,
+                              int32_t n_labels, int64_t *count, double *total,
+                              double *total_sq);
+
+/* energy.py:233-257 evaluate_total -> (external, internal); the external
+ * sum is correctly rounded like math.fsum. */
+int32_t rcb_evaluate_total(const double *image, const int32_t *labels, int32_t ndim,
+                           const int64_t *dims, const rcb_energy_cfg *cfg, double *external,
+                           int64_t *internal);
+
+/* ---- the engine: RegionCompetition (optimizer.py:90-230) --------------- */
+
+/* image: float64 C-order (optimizer.py:102); labels: int32 (copied).
+ * stream: a cudaStream_t to launch on (NULL = a private stream). */
+int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t ndim,
+                          const int64_t *dims, const rcb_energy_cfg *ecfg,
+                          const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg,
+                          int32_t device, void *stream, rcb_engine **out);
+void rcb_engine_destroy(rcb_engine *eng);
+/* optimizer.py:122-160 iterate(): extraction, ΔE, Sobolev, rank, acceptance. */
+int32_t rcb_engine_iterate(rcb_engine *eng, rcb_iter_record *rec);
+int32_t rcb_engine_get_labels(rcb_engine *eng, int32_t *out);
+int32_t rcb_engine_set_labels(rcb_engine *eng, const int32_t *labels);
+/* last_candidates (optimizer.py:140-142): (x, owner, competitor, rank). */
+int32_t rcb_engine_get_candidates(rcb_engine *eng, int64_t *xs, int64_t *owners,
+                                  int64_t *competitors, double *rank, int64_t cap, int64_t *n);
+/* accepted moves of the last iteration in acceptance order, as (x, a, b). */
+int32_t rcb_engine_get_accepted(rcb_engine *eng, int64_t *xab, int64_t cap, int64_t *n);
+int32_t rcb_engine_get_stats(rcb_engine *eng, int64_t *count, double *total, double *total_sq,
+                             int32_t n_labels);
+int32_t rcb_engine_n_labels(rcb_engine *eng, int32_t *n_labels);
+int32_t rcb_engine_set_mode(rcb_engine *eng, int32_t gradient);
+int32_t rcb_engine_set_energy(rcb_engine *eng, double energy);
+/* EnergyModel.refresh (energy.py:285-291): rebuild stats and PS fields. */
+int32_t rcb_engine_refresh(rcb_engine *eng);
+/* evaluate_total on the engine's current device state. */
+int32_t rcb_engine_evaluate(rcb_engine *eng, double *external, int64_t *internal);
+int32_t rcb_engine_stream(rcb_engine *eng, void **stream);
+/* Device time (ms) of the last iterate() phases, CUDA events on the engine
+ * stream: [0] extract, [1] energy, [2] sobolev, [3] rank/sort, [4] accept,
+ * [5] whole iteration.  Also the kernel launch count of the last iterate. */
+int32_t rcb_engine_timings(rcb_engine *eng, float *ms6, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCB_H */
