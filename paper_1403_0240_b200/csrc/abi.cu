@@ -1,0 +1,811 @@
+// C ABI of librcseg_b200 (include/rcb.h): the device engine that replaces
+// RegionCompetition.iterate (optimizer.py:122-160) and the function-level
+// drop-ins.  Each entry point cites the reference function it replaces.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace rcb {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+int32_t fail(int32_t code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+std::vector<Off> ball_table(int ndim, int r) {
+  // energy.py:60-70 ball_offsets: |o|^2 <= r^2, |o|^2 ascending, stable over
+  // lexicographic order, centre first.
+  std::vector<Off> out;
+  for (int dz = (ndim == 3 ? -r : 0); dz <= (ndim == 3 ? r : 0); ++dz)
+    for (int dy = -r; dy <= r; ++dy)
+      for (int dx = -r; dx <= r; ++dx) {
+        int d2 = dz * dz + dy * dy + dx * dx;
+        if (d2 <= r * r) out.push_back(Off{(int8_t)dz, (int8_t)dy, (int8_t)dx, (uint8_t)d2});
+      }
+  std::stable_sort(out.begin(), out.end(), [](const Off &a, const Off &b) { return a.aux < b.aux; });
+  return out;
+}
+
+template <typename T>
+static int32_t upload(DBuf<T> &d, const T *h, size_t n, cudaStream_t s) {
+  RCB_TRY(d.reserve(n ? n : 1, s));
+  if (n) RCB_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  return RCB_OK;
+}
+
+static int32_t check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(RCB_ERR_NODEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  return RCB_OK;
+}
+
+static int32_t check_lattice(int32_t ndim, const int64_t *dims) {
+  if (ndim != 2 && ndim != 3) return fail(RCB_ERR_VALUE, "raster must be 2-D or 3-D");
+  int64_t V = 1;
+  for (int k = 0; k < ndim; ++k) {
+    if (dims[k] < 1) return fail(RCB_ERR_VALUE, "raster dimensions must be positive");
+    V *= dims[k];
+  }
+  if (V >= (int64_t)0xffffffffll) return fail(RCB_ERR_VALUE, "raster larger than 2^32-1 sites");
+  return RCB_OK;
+}
+
+// small device-side scalar block, mirrored into pinned host memory once per
+// iteration (the only D2H traffic of iterate()).
+struct Scalars {
+  double energy;
+  int64_t moves;
+  uint32_t epoch;
+  uint32_t pad;
+  unsigned long long pairs;
+  unsigned long long nneg;
+  unsigned long long perim;
+  uint32_t n_next;
+  uint32_t pad2;
+  long long limbs[kLimbs];
+};
+
+}  // namespace rcb
+
+using namespace rcb;
+
+struct rcb_engine {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  bool own_stream = false;
+  Lat lat{};
+  int32_t nl = 0;
+  rcb_energy_cfg ecfg{};
+  rcb_opt_cfg ocfg{};
+  int64_t iteration = 0;
+  int mode = 1;
+  bool prepared = false;
+  int64_t N = 0;  // particles of the current raster (valid when prepared)
+  int64_t n_scored = 0, last_moves = 0;
+
+  DBuf<int32_t> L;
+  DBuf<double> I;
+  DBuf<int64_t> cnt;
+  DBuf<double> tot, tsq;
+  DBuf<int32_t> Cown;
+  DBuf<double> Sown;
+  DBuf<Off> ball, ball_full, st;
+  int nball = 0, nball_full = 0, nst = 0;
+  DBuf<double> wt;
+  DBuf<int32_t> ncomp;
+  DBuf<uint32_t> vis, queue;
+  DBuf<uint32_t> site_off, px, order;
+  DBuf<int32_t> pown, pcomp, dint;
+  DBuf<double> raw, smooth, rank;
+  DBuf<int64_t> acc;
+  DBuf<Scalars> sc;
+  DBuf<uint8_t> tmp;
+  StatsScratch ssc;
+  RankScratch rsc;
+  Scalars *hsc = nullptr;  // pinned
+  cudaEvent_t ev[6] = {};
+  float times[6] = {};
+  int32_t launches = 0;
+
+  ~rcb_engine() {
+    if (s) {
+      cudaSetDevice(device);
+      L.release(s); I.release(s); cnt.release(s); tot.release(s); tsq.release(s);
+      Cown.release(s); Sown.release(s); ball.release(s); ball_full.release(s); st.release(s);
+      wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
+      px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
+      raw.release(s); smooth.release(s); rank.release(s); acc.release(s); sc.release(s);
+      tmp.release(s); ssc.release(s); rsc.release(s);
+      cudaStreamSynchronize(s);
+      for (auto &e : ev)
+        if (e) cudaEventDestroy(e);
+      if (own_stream) cudaStreamDestroy(s);
+    }
+    if (hsc) cudaFreeHost(hsc);
+  }
+
+  int32_t prepare() {  // K1 pass 1 + scan on the current raster
+    RCB_TRY(contour_scan(L.p, lat, ocfg.full_fg, site_off.p, tmp, s));
+    RCB_CUDA(cudaMemcpyAsync(&hsc->n_next, site_off.p + lat.V, sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    N = hsc->n_next;
+    prepared = true;
+    return RCB_OK;
+  }
+
+  int32_t refresh() {  // energy.py:285-291
+    RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
+    if (ecfg.region_model == 1)
+      RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s));
+    return RCB_OK;
+  }
+
+  int32_t components() {
+    return label_components(L.p, lat, ocfg.full_fg, nl, queue.p, ncomp.p, s);
+  }
+};
+
+extern "C" {
+
+int32_t rcb_version(void) { return 100; }
+const char *rcb_last_error(void) { return g_err.c_str(); }
+int32_t rcb_device_count(int32_t *n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  *n = e == cudaSuccess ? c : 0;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t ndim,
+                          const int64_t *dims, const rcb_energy_cfg *ecfg,
+                          const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg, int32_t device,
+                          void *stream, rcb_engine **out) {
+  *out = nullptr;
+  RCB_TRY(check_device());
+  RCB_TRY(check_lattice(ndim, dims));
+  if (ecfg->region_model == 1 && (ecfg->smooth_radius < 1 || ecfg->smooth_radius > 15))
+    return fail(RCB_ERR_VALUE, "smooth_radius must be in [1, 15]");
+  if (!(scfg->length_scale > 0) || scfg->length_scale > 30.0)
+    return fail(RCB_ERR_VALUE, "length_scale must be in (0, 30]");
+  auto *e = new rcb_engine();
+  e->device = device;
+  RCB_CUDA(cudaSetDevice(device));
+  if (stream) {
+    e->s = (cudaStream_t)stream;
+  } else {
+    RCB_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+    e->own_stream = true;
+  }
+  auto bail = [&](int32_t rc) {
+    delete e;
+    return rc;
+  };
+  cudaStream_t s = e->s;
+  e->lat = make_lat(ndim, dims);
+  e->ecfg = *ecfg;
+  e->ocfg = *ocfg;
+  e->mode = ocfg->gradient;
+  const int64_t V = e->lat.V;
+  int32_t mx = 0;
+  for (int64_t i = 0; i < V; ++i) {
+    if (labels[i] < 0) return bail(fail(RCB_ERR_VALUE, "label raster contains negative labels"));
+    mx = std::max(mx, labels[i]);
+  }
+  e->nl = mx + 1;
+  int32_t rc;
+#define TRYB(x)                 \
+  if ((rc = (x)) != RCB_OK) {   \
+    return bail(rc);            \
+  }
+  TRYB(upload(e->L, labels, V, s));
+  TRYB(upload(e->I, image, V, s));
+  TRYB(e->cnt.reserve(e->nl, s));
+  TRYB(e->tot.reserve(e->nl, s));
+  TRYB(e->tsq.reserve(e->nl, s));
+  TRYB(e->ncomp.reserve(e->nl, s));
+  TRYB(e->vis.reserve(V, s));
+  TRYB(e->queue.reserve(V, s));
+  TRYB(e->site_off.reserve(V + 1, s));
+  TRYB(e->sc.reserve(1, s));
+  if (cudaMallocHost((void **)&e->hsc, sizeof(Scalars)) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
+  memset(e->hsc, 0, sizeof(Scalars));
+  if (cudaMemsetAsync(e->sc.p, 0, sizeof(Scalars), s) != cudaSuccess ||
+      cudaMemsetAsync(e->vis.p, 0, sizeof(uint32_t) * V, s) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "memset failed"));
+  e->hsc->epoch = 32;
+  cudaMemcpyAsync(&e->sc.p->epoch, &e->hsc->epoch, sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+  if (ecfg->region_model == 1) {
+    auto full = ball_table(ndim, ecfg->smooth_radius);
+    e->nball_full = (int)full.size();
+    e->nball = e->nball_full - 1;
+    TRYB(upload(e->ball_full, full.data(), full.size(), s));
+    TRYB(upload(e->ball, full.data() + 1, full.size() - 1, s));
+    TRYB(e->Cown.reserve(V, s));
+    TRYB(e->Sown.reserve(V, s));
+  }
+  auto st = sobolev_stencil(ndim, scfg->length_scale);
+  int maxd2 = 0;
+  for (auto &o : st) maxd2 = std::max(maxd2, (int)o.aux);
+  if (scfg->n_weights <= maxd2)
+    return bail(fail(RCB_ERR_VALUE, "Sobolev weight table shorter than the stencil needs"));
+  e->nst = (int)st.size();
+  TRYB(upload(e->st, st.data(), st.size(), s));
+  TRYB(upload(e->wt, scfg->weights, (size_t)scfg->n_weights, s));
+  for (auto &ev : e->ev) cudaEventCreate(&ev);
+  TRYB(e->refresh());
+  TRYB(e->components());
+  TRYB(e->prepare());
+#undef TRYB
+  *out = e;
+  return RCB_OK;
+}
+
+void rcb_engine_destroy(rcb_engine *e) { delete e; }
+
+int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  cudaStream_t s = e->s;
+  e->iteration += 1;
+  e->launches = 0;
+  cudaEventRecord(e->ev[0], s);
+  if (!e->prepared) RCB_TRY(e->prepare());
+  const int64_t n = e->N;
+  const Lat &lat = e->lat;
+  Scalars *d = e->sc.p;
+  RCB_CUDA(cudaMemsetAsync(&d->pairs, 0, sizeof(unsigned long long), s));
+  RCB_CUDA(cudaMemsetAsync(&d->moves, 0, sizeof(int64_t), s));
+  int launches = 2;
+  if (n > 0) {
+    RCB_TRY(e->px.reserve(n, s));
+    RCB_TRY(e->pown.reserve(n, s));
+    RCB_TRY(e->pcomp.reserve(n, s));
+    RCB_TRY(e->dint.reserve(n, s));
+    RCB_TRY(e->raw.reserve(n, s));
+    RCB_TRY(e->smooth.reserve(n, s));
+    RCB_TRY(e->rank.reserve(n, s));
+    RCB_TRY(e->order.reserve(n, s));
+    RCB_TRY(e->acc.reserve(3 * n, s));
+    RCB_TRY(contour_emit(e->L.p, lat, e->ocfg.full_fg, e->site_off.p, e->px.p, e->pown.p,
+                         e->pcomp.p, s));
+    cudaEventRecord(e->ev[1], s);
+    RCB_TRY(delta_int_batch(e->L.p, lat, e->px.p, e->pown.p, e->pcomp.p, n, e->dint.p, s));
+    const int poisson = e->ecfg.noise_model == 1;
+    if (e->ecfg.region_model == 0)
+      RCB_TRY(delta_pc_batch(e->I.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
+                             e->tsq.p, poisson, e->raw.p, s));
+    else
+      RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
+                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s));
+    cudaEventRecord(e->ev[2], s);
+    const double *base = e->raw.p;
+    if (e->mode == 1) {
+      RCB_TRY(sobolev_lattice(e->site_off.p, e->L.p, e->px.p, e->pcomp.p, e->raw.p, lat, e->st.p,
+                              e->nst, e->wt.p, n, e->smooth.p, &d->pairs, s));
+      base = e->smooth.p;
+      launches += 1;
+    }
+    cudaEventRecord(e->ev[3], s);
+    RCB_TRY(rank_order(base, e->dint.p, e->ecfg.lam, n, e->px.p, e->pcomp.p, e->ocfg.seed,
+                       e->rank.p, e->rsc, e->order.p, &d->nneg, s));
+    cudaEventRecord(e->ev[4], s);
+    AcceptArgs A{};
+    A.lat = lat;
+    A.full_fg = e->ocfg.full_fg;
+    A.region_ps = e->ecfg.region_model == 1;
+    A.poisson = poisson;
+    A.mode_l2 = e->mode == 0;
+    A.allow_fusion = e->ocfg.allow_fusion;
+    A.vanish_ok = e->ocfg.allow_vanish && e->iteration > e->ocfg.vanish_grace;
+    A.lam = e->ecfg.lam;
+    A.budget = (int64_t)ceil(e->ocfg.move_budget * (double)n);
+    A.n = n;
+    A.order = e->order.p;
+    A.rank = e->rank.p;
+    A.px = e->px.p;
+    A.pown = e->pown.p;
+    A.pcomp = e->pcomp.p;
+    A.L = e->L.p;
+    A.I = e->I.p;
+    A.cnt = e->cnt.p;
+    A.tot = e->tot.p;
+    A.tsq = e->tsq.p;
+    A.Cown = e->Cown.p;
+    A.Sown = e->Sown.p;
+    A.ball = e->ball.p;
+    A.nball = e->nball;
+    A.ncomp = e->ncomp.p;
+    A.vis = e->vis.p;
+    A.queue = e->queue.p;
+    A.epoch = &d->epoch;
+    A.acc = e->acc.p;
+    A.moves = &d->moves;
+    A.energy = &d->energy;
+    RCB_TRY(accept_seq(A, s));
+    launches += 1 + 4 + 1 + 3 * 8;  // emit, dint, dE, rank, 2 radix sorts (~8 passes)
+  } else {
+    for (int k = 1; k < 5; ++k) cudaEventRecord(e->ev[k], s);
+  }
+  // K1 pass 1 on the updated raster: the particle count of the record and the
+  // lattice index map of the next iteration
+  RCB_TRY(contour_scan(e->L.p, lat, e->ocfg.full_fg, e->site_off.p, e->tmp, s));
+  RCB_CUDA(cudaMemcpyAsync(&d->n_next, e->site_off.p + lat.V, sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, s));
+  cudaEventRecord(e->ev[5], s);
+  RCB_CUDA(cudaMemcpyAsync(e->hsc, d, offsetof(Scalars, limbs), cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  e->n_scored = n;
+  e->N = e->hsc->n_next;
+  e->prepared = true;
+  e->last_moves = e->hsc->moves;
+  if (e->hsc->epoch > 0x80000000u) {  // BFS stamps near wrap: clear
+    RCB_CUDA(cudaMemsetAsync(e->vis.p, 0, sizeof(uint32_t) * lat.V, s));
+    e->hsc->epoch = 32;
+    RCB_CUDA(cudaMemcpyAsync(&d->epoch, &e->hsc->epoch, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  }
+  const int nev = 6;
+  float t[nev] = {};
+  for (int k = 1; k < nev; ++k) cudaEventElapsedTime(&t[k], e->ev[k - 1], e->ev[k]);
+  e->times[0] = t[1];
+  e->times[1] = t[2];
+  e->times[2] = t[3];
+  e->times[3] = t[4];
+  e->times[4] = t[5];
+  cudaEventElapsedTime(&e->times[5], e->ev[0], e->ev[5]);
+  e->launches = launches + 2;
+  rec->iteration = e->iteration;
+  rec->energy = e->hsc->energy;
+  rec->moves = e->hsc->moves;
+  rec->particles = e->N;
+  rec->candidates = n;
+  rec->negative = (int64_t)e->hsc->nneg;
+  rec->pairs = (int64_t)e->hsc->pairs;
+  rec->mode = e->mode;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_get_labels(rcb_engine *e, int32_t *out) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  RCB_CUDA(cudaMemcpyAsync(out, e->L.p, sizeof(int32_t) * e->lat.V, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+int32_t rcb_engine_set_labels(rcb_engine *e, const int32_t *labels) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  for (int64_t i = 0; i < e->lat.V; ++i)
+    if (labels[i] < 0 || labels[i] >= e->nl)
+      return fail(RCB_ERR_VALUE, "labels outside the engine's label table");
+  RCB_CUDA(cudaMemcpyAsync(e->L.p, labels, sizeof(int32_t) * e->lat.V, cudaMemcpyHostToDevice, e->s));
+  RCB_TRY(e->components());
+  RCB_TRY(e->prepare());
+  return RCB_OK;
+}
+
+int32_t rcb_engine_get_candidates(rcb_engine *e, int64_t *xs, int64_t *owners, int64_t *comps,
+                                  double *rank, int64_t cap, int64_t *n) {
+  *n = e->n_scored;
+  if (cap < e->n_scored) return fail(RCB_ERR_CAPACITY, "candidate buffer too small");
+  const int64_t m = e->n_scored;
+  if (m == 0) return RCB_OK;
+  RCB_CUDA(cudaSetDevice(e->device));
+  std::vector<uint32_t> hx(m);
+  std::vector<int32_t> ho(m), hc(m);
+  RCB_CUDA(cudaMemcpyAsync(hx.data(), e->px.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(ho.data(), e->pown.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(hc.data(), e->pcomp.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(rank, e->rank.p, 8 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  for (int64_t i = 0; i < m; ++i) {
+    xs[i] = hx[i];
+    owners[i] = ho[i];
+    comps[i] = hc[i];
+  }
+  return RCB_OK;
+}
+
+int32_t rcb_engine_get_accepted(rcb_engine *e, int64_t *xab, int64_t cap, int64_t *n) {
+  *n = e->last_moves;
+  if (cap < e->last_moves) return fail(RCB_ERR_CAPACITY, "accepted-move buffer too small");
+  if (e->last_moves == 0) return RCB_OK;
+  RCB_CUDA(cudaSetDevice(e->device));
+  RCB_CUDA(cudaMemcpyAsync(xab, e->acc.p, sizeof(int64_t) * 3 * e->last_moves,
+                           cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+int32_t rcb_engine_get_stats(rcb_engine *e, int64_t *count, double *total, double *total_sq,
+                             int32_t n_labels) {
+  if (n_labels < e->nl) return fail(RCB_ERR_CAPACITY, "stats buffers too small");
+  RCB_CUDA(cudaSetDevice(e->device));
+  RCB_CUDA(cudaMemcpyAsync(count, e->cnt.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(total, e->tot.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(total_sq, e->tsq.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+int32_t rcb_engine_n_labels(rcb_engine *e, int32_t *n_labels) {
+  *n_labels = e->nl;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_set_mode(rcb_engine *e, int32_t gradient) {
+  if (gradient != 0 && gradient != 1) return fail(RCB_ERR_VALUE, "gradient must be 0 or 1");
+  e->mode = gradient;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_set_energy(rcb_engine *e, double energy) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  e->hsc->energy = energy;
+  RCB_CUDA(cudaMemcpyAsync(&e->sc.p->energy, &e->hsc->energy, sizeof(double),
+                           cudaMemcpyHostToDevice, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+int32_t rcb_engine_refresh(rcb_engine *e) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  RCB_TRY(e->refresh());
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+static int32_t evaluate_on(const int32_t *L, const double *I, const Lat &lat,
+                           const rcb_energy_cfg *cfg, int32_t nl, double *external,
+                           int64_t *internal, cudaStream_t s) {
+  DBuf<long long> limbs;
+  DBuf<unsigned long long> per;
+  RCB_TRY(limbs.reserve(kLimbs, s));
+  RCB_TRY(per.reserve(1, s));
+  const int poisson = cfg->noise_model == 1;
+  int32_t rc = RCB_OK;
+  if (cfg->region_model == 0) {
+    DBuf<int64_t> c;
+    DBuf<double> t, q;
+    StatsScratch ss;
+    if ((rc = c.reserve(nl, s)) == RCB_OK && (rc = t.reserve(nl, s)) == RCB_OK &&
+        (rc = q.reserve(nl, s)) == RCB_OK &&
+        (rc = stats_rebuild(L, I, lat.V, nl, c.p, t.p, q.p, ss, s)) == RCB_OK)
+      rc = pc_terms_exact(c.p, t.p, q.p, nl, poisson, limbs.p, s);
+    cudaStreamSynchronize(s);
+    c.release(s);
+    t.release(s);
+    q.release(s);
+    ss.release(s);
+  } else {
+    DBuf<int32_t> C;
+    DBuf<double> S;
+    DBuf<Off> b;
+    auto full = ball_table(lat.ndim, cfg->smooth_radius);
+    if ((rc = C.reserve(lat.V, s)) == RCB_OK && (rc = S.reserve(lat.V, s)) == RCB_OK &&
+        (rc = upload(b, full.data(), full.size(), s)) == RCB_OK &&
+        (rc = ps_fields(L, I, lat, b.p, (int)full.size(), C.p, S.p, s)) == RCB_OK)
+      rc = ps_terms_exact(C.p, S.p, I, lat.V, poisson, limbs.p, s);
+    cudaStreamSynchronize(s);
+    C.release(s);
+    S.release(s);
+    b.release(s);
+  }
+  if (rc == RCB_OK) rc = perimeter(L, lat, per.p, s);
+  long long hl[kLimbs];
+  unsigned long long hp = 0;
+  if (rc == RCB_OK) {
+    cudaMemcpyAsync(hl, limbs.p, sizeof(hl), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hp, per.p, sizeof(hp), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) rc = fail(RCB_ERR_CUDA, "evaluate sync failed");
+  }
+  limbs.release(s);
+  per.release(s);
+  if (rc != RCB_OK) return rc;
+  *external = limbs_to_double(hl);
+  *internal = (int64_t)hp;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_evaluate(rcb_engine *e, double *external, int64_t *internal) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  return evaluate_on(e->L.p, e->I.p, e->lat, &e->ecfg, e->nl, external, internal, e->s);
+}
+
+int32_t rcb_engine_stream(rcb_engine *e, void **stream) {
+  *stream = (void *)e->s;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_timings(rcb_engine *e, float *ms6, int32_t *launches) {
+  for (int k = 0; k < 6; ++k) ms6[k] = e->times[k];
+  *launches = e->launches;
+  return RCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// function-level drop-ins (stateless: upload, compute, download)
+// ---------------------------------------------------------------------------
+
+struct TmpStream {
+  cudaStream_t s = nullptr;
+  TmpStream() { cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking); }
+  ~TmpStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+int32_t rcb_sobolev_filter(const int64_t *coords, int64_t n, int32_t ndim, const int64_t *owners,
+                           const int64_t *competitors, const double *raw,
+                           const rcb_sobolev_cfg *params, double *out, int64_t *n_pairs) {
+  *n_pairs = 0;
+  if (ndim != 2 && ndim != 3) return fail(RCB_ERR_VALUE, "coords must be (n, 2) or (n, 3)");
+  if (!(params->length_scale > 0) || params->length_scale > 30.0)
+    return fail(RCB_ERR_VALUE, "length_scale must be in (0, 30]");
+  if (n == 0) return RCB_OK;
+  RCB_TRY(check_device());
+  int64_t dims[3] = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < ndim; ++k) {
+      int64_t c = coords[i * ndim + k];
+      if (c < 0) return fail(RCB_ERR_VALUE, "coordinates must be non-negative");
+      dims[k] = std::max(dims[k], c + 1);
+    }
+  for (int64_t i = 0; i < n; ++i) {
+    if (competitors[i] < 0 || competitors[i] > 0x7fffffff || owners[i] < -0x7fffffffll ||
+        owners[i] > 0x7fffffff)
+      return fail(RCB_ERR_VALUE, "owner/competitor labels outside [0, 2^31)");
+  }
+  RCB_TRY(check_lattice(ndim, dims));
+  Lat lat = make_lat(ndim, dims);
+  auto st = sobolev_stencil(ndim, params->length_scale);
+  int maxd2 = 0;
+  for (auto &o : st) maxd2 = std::max(maxd2, (int)o.aux);
+  if (params->n_weights <= maxd2)
+    return fail(RCB_ERR_VALUE, "Sobolev weight table shorter than the stencil needs");
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int64_t> dc, dow, dcm;
+  DBuf<double> draw, dout, dwt;
+  DBuf<Off> dst;
+  DBuf<unsigned long long> dp;
+  int32_t rc = RCB_OK;
+  auto go = [&]() -> int32_t {
+    RCB_TRY(upload(dc, coords, (size_t)n * ndim, s));
+    RCB_TRY(upload(dow, owners, n, s));
+    RCB_TRY(upload(dcm, competitors, n, s));
+    RCB_TRY(upload(draw, raw, n, s));
+    RCB_TRY(upload(dwt, params->weights, params->n_weights, s));
+    RCB_TRY(upload(dst, st.data(), st.size(), s));
+    RCB_TRY(dout.reserve(n, s));
+    RCB_TRY(dp.reserve(1, s));
+    RCB_CUDA(cudaMemsetAsync(dp.p, 0, sizeof(unsigned long long), s));
+    RCB_TRY(sobolev_coords(dc.p, n, ndim, lat, dow.p, dcm.p, draw.p, dst.p, (int)st.size(), dwt.p,
+                           dout.p, dp.p, s));
+    unsigned long long hp = 0;
+    RCB_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaMemcpyAsync(&hp, dp.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    *n_pairs = (int64_t)hp;
+    return RCB_OK;
+  };
+  rc = go();
+  dc.release(s); dow.release(s); dcm.release(s); draw.release(s); dout.release(s);
+  dwt.release(s); dst.release(s); dp.release(s);
+  return rc;
+}
+
+int32_t rcb_scan_contour(const int32_t *labels, int32_t ndim, const int64_t *dims, int32_t full_fg,
+                         int64_t *xs, int64_t *owners, int64_t *competitors, int64_t cap,
+                         int64_t *n) {
+  *n = 0;
+  RCB_TRY(check_lattice(ndim, dims));
+  RCB_TRY(check_device());
+  Lat lat = make_lat(ndim, dims);
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int32_t> L, po, pc;
+  DBuf<uint32_t> off, px;
+  DBuf<uint8_t> tmp;
+  int32_t rc = RCB_OK;
+  auto go = [&]() -> int32_t {
+    RCB_TRY(upload(L, labels, lat.V, s));
+    RCB_TRY(off.reserve(lat.V + 1, s));
+    RCB_TRY(contour_scan(L.p, lat, full_fg, off.p, tmp, s));
+    uint32_t total = 0;
+    RCB_CUDA(cudaMemcpyAsync(&total, off.p + lat.V, 4, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    *n = total;
+    if (cap < (int64_t)total) return fail(RCB_ERR_CAPACITY, "particle buffer too small");
+    if (total == 0) return RCB_OK;
+    RCB_TRY(px.reserve(total, s));
+    RCB_TRY(po.reserve(total, s));
+    RCB_TRY(pc.reserve(total, s));
+    RCB_TRY(contour_emit(L.p, lat, full_fg, off.p, px.p, po.p, pc.p, s));
+    std::vector<uint32_t> hx(total);
+    std::vector<int32_t> ho(total), hc(total);
+    RCB_CUDA(cudaMemcpyAsync(hx.data(), px.p, 4ull * total, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaMemcpyAsync(ho.data(), po.p, 4ull * total, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaMemcpyAsync(hc.data(), pc.p, 4ull * total, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t i = 0; i < total; ++i) {
+      xs[i] = hx[i];
+      owners[i] = ho[i];
+      competitors[i] = hc[i];
+    }
+    return RCB_OK;
+  };
+  rc = go();
+  L.release(s); po.release(s); pc.release(s); off.release(s); px.release(s); tmp.release(s);
+  return rc;
+}
+
+static int32_t upload_particles(const int64_t *xs, const int64_t *owners, const int64_t *comps,
+                                int64_t n, int64_t V, DBuf<uint32_t> &px, DBuf<int32_t> &po,
+                                DBuf<int32_t> &pc, cudaStream_t s) {
+  std::vector<uint32_t> hx(n);
+  std::vector<int32_t> ho(n), hc(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (xs[i] < 0 || xs[i] >= V) return fail(RCB_ERR_VALUE, "pixel index out of range");
+    if (owners[i] < 0 || owners[i] > 0x7fffffff || comps[i] < 0 || comps[i] > 0x7fffffff)
+      return fail(RCB_ERR_VALUE, "labels must be non-negative int32");
+    hx[i] = (uint32_t)xs[i];
+    ho[i] = (int32_t)owners[i];
+    hc[i] = (int32_t)comps[i];
+  }
+  RCB_TRY(upload(px, hx.data(), n, s));
+  RCB_TRY(upload(po, ho.data(), n, s));
+  RCB_TRY(upload(pc, hc.data(), n, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  return RCB_OK;
+}
+
+int32_t rcb_delta_internal_batch(const int32_t *labels, int32_t ndim, const int64_t *dims,
+                                 const int64_t *xs, const int64_t *owners,
+                                 const int64_t *competitors, int64_t n, int64_t *out) {
+  RCB_TRY(check_lattice(ndim, dims));
+  if (n == 0) return RCB_OK;
+  RCB_TRY(check_device());
+  Lat lat = make_lat(ndim, dims);
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int32_t> L, po, pc, d;
+  DBuf<uint32_t> px;
+  auto go = [&]() -> int32_t {
+    RCB_TRY(upload(L, labels, lat.V, s));
+    RCB_TRY(upload_particles(xs, owners, competitors, n, lat.V, px, po, pc, s));
+    RCB_TRY(d.reserve(n, s));
+    RCB_TRY(delta_int_batch(L.p, lat, px.p, po.p, pc.p, n, d.p, s));
+    std::vector<int32_t> h(n);
+    RCB_CUDA(cudaMemcpyAsync(h.data(), d.p, 4 * n, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n; ++i) out[i] = h[i];
+    return RCB_OK;
+  };
+  int32_t rc = go();
+  L.release(s); po.release(s); pc.release(s); d.release(s); px.release(s);
+  return rc;
+}
+
+int32_t rcb_delta_external_batch(const double *image, const int32_t *labels, int32_t ndim,
+                                 const int64_t *dims, const rcb_energy_cfg *cfg,
+                                 int32_t n_labels, const int64_t *count, const double *total,
+                                 const double *total_sq, const int64_t *xs,
+                                 const int64_t *owners, const int64_t *competitors, int64_t n,
+                                 double *out) {
+  RCB_TRY(check_lattice(ndim, dims));
+  if (n == 0) return RCB_OK;
+  RCB_TRY(check_device());
+  Lat lat = make_lat(ndim, dims);
+  for (int64_t i = 0; i < n; ++i)
+    if (owners[i] >= n_labels || competitors[i] >= n_labels)
+      return fail(RCB_ERR_VALUE, "label outside the statistics table");
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int32_t> L, po, pc, C;
+  DBuf<uint32_t> px;
+  DBuf<double> I, d, S, t, q;
+  DBuf<int64_t> c;
+  DBuf<Off> b;
+  const int poisson = cfg->noise_model == 1;
+  auto go = [&]() -> int32_t {
+    RCB_TRY(upload(L, labels, lat.V, s));
+    RCB_TRY(upload(I, image, lat.V, s));
+    RCB_TRY(upload_particles(xs, owners, competitors, n, lat.V, px, po, pc, s));
+    RCB_TRY(d.reserve(n, s));
+    if (cfg->region_model == 0) {
+      RCB_TRY(upload(c, count, n_labels, s));
+      RCB_TRY(upload(t, total, n_labels, s));
+      RCB_TRY(upload(q, total_sq, n_labels, s));
+      RCB_TRY(delta_pc_batch(I.p, px.p, po.p, pc.p, n, c.p, t.p, q.p, poisson, d.p, s));
+    } else {
+      if (cfg->smooth_radius < 1 || cfg->smooth_radius > 15)
+        return fail(RCB_ERR_VALUE, "smooth_radius must be in [1, 15]");
+      auto full = ball_table(ndim, cfg->smooth_radius);
+      RCB_TRY(upload(b, full.data(), full.size(), s));
+      RCB_TRY(C.reserve(lat.V, s));
+      RCB_TRY(S.reserve(lat.V, s));
+      RCB_TRY(ps_fields(L.p, I.p, lat, b.p, (int)full.size(), C.p, S.p, s));
+      RCB_TRY(delta_ps_batch(L.p, I.p, C.p, S.p, lat, b.p + 1, (int)full.size() - 1, px.p, po.p,
+                             pc.p, n, poisson, d.p, s));
+    }
+    RCB_CUDA(cudaMemcpyAsync(out, d.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    return RCB_OK;
+  };
+  int32_t rc = go();
+  L.release(s); po.release(s); pc.release(s); C.release(s); px.release(s); I.release(s);
+  d.release(s); S.release(s); t.release(s); q.release(s); c.release(s); b.release(s);
+  return rc;
+}
+
+int32_t rcb_stats_from_labels(const double *image, const int32_t *labels, int64_t size,
+                              int32_t n_labels, int64_t *count, double *total, double *total_sq) {
+  if (size < 0 || n_labels < 1) return fail(RCB_ERR_VALUE, "bad sizes");
+  RCB_TRY(check_device());
+  for (int64_t i = 0; i < size; ++i)
+    if (labels[i] < 0 || labels[i] >= n_labels)
+      return fail(RCB_ERR_VALUE, "label outside [0, n_labels)");
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int32_t> L;
+  DBuf<double> I, t, q;
+  DBuf<int64_t> c;
+  StatsScratch ss;
+  auto go = [&]() -> int32_t {
+    RCB_TRY(upload(L, labels, size, s));
+    RCB_TRY(upload(I, image, size, s));
+    RCB_TRY(c.reserve(n_labels, s));
+    RCB_TRY(t.reserve(n_labels, s));
+    RCB_TRY(q.reserve(n_labels, s));
+    RCB_TRY(stats_rebuild(L.p, I.p, size, n_labels, c.p, t.p, q.p, ss, s));
+    RCB_CUDA(cudaMemcpyAsync(count, c.p, 8 * n_labels, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaMemcpyAsync(total, t.p, 8 * n_labels, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaMemcpyAsync(total_sq, q.p, 8 * n_labels, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    return RCB_OK;
+  };
+  int32_t rc = go();
+  L.release(s); I.release(s); t.release(s); q.release(s); c.release(s); ss.release(s);
+  return rc;
+}
+
+int32_t rcb_evaluate_total(const double *image, const int32_t *labels, int32_t ndim,
+                           const int64_t *dims, const rcb_energy_cfg *cfg, double *external,
+                           int64_t *internal) {
+  RCB_TRY(check_lattice(ndim, dims));
+  RCB_TRY(check_device());
+  Lat lat = make_lat(ndim, dims);
+  int32_t mx = 0;
+  for (int64_t i = 0; i < lat.V; ++i) {
+    if (labels[i] < 0) return fail(RCB_ERR_VALUE, "label raster contains negative labels");
+    mx = std::max(mx, labels[i]);
+  }
+  if (cfg->region_model == 1 && (cfg->smooth_radius < 1 || cfg->smooth_radius > 15))
+    return fail(RCB_ERR_VALUE, "smooth_radius must be in [1, 15]");
+  TmpStream ts;
+  cudaStream_t s = ts.s;
+  DBuf<int32_t> L;
+  DBuf<double> I;
+  int32_t rc = upload(L, labels, lat.V, s);
+  if (rc == RCB_OK) rc = upload(I, image, lat.V, s);
+  if (rc == RCB_OK) rc = evaluate_on(L.p, I.p, lat, cfg, mx + 1, external, internal, s);
+  L.release(s);
+  I.release(s);
+  return rc;
+}
+
+}  // extern "C"

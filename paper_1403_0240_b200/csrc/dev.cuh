@@ -1,0 +1,226 @@
+// Device functions shared by the kernels (header-only; every TU that uses
+// them is compiled with -fmad=false).
+#pragma once
+
+#include "common.cuh"
+
+namespace rcb {
+
+static constexpr double kPoissonFloor = 1e-8;  // energy.py:30
+
+// ---------------------------------------------------------------------------
+// neighbourhoods (grid.py:42-96)
+// ---------------------------------------------------------------------------
+
+// Distinct labels != own among the background-adjacency neighbours of a site,
+// sorted ascending (contour.py:66-125; Appendix B1).  Background adjacency is
+// the 2d faces for the default connectivity (full_fg) and the full box
+// otherwise.  Returns the count; out has room for 26.
+__device__ __forceinline__ int site_competitors(const int32_t *__restrict__ L, const Lat &lat,
+                                                int full_fg, int64_t z, int64_t y, int64_t x,
+                                                int32_t own, int32_t *out) {
+  int n = 0;
+  const int zlo = lat.ndim == 3 ? -1 : 0, zhi = lat.ndim == 3 ? 1 : 0;
+  for (int dz = zlo; dz <= zhi; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        int m = abs(dz) + abs(dy) + abs(dx);
+        if (m == 0) continue;
+        if (full_fg && m != 1) continue;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (!lat.inb(zz, yy, xx)) continue;
+        int32_t l = __ldg(&L[lat.flat(zz, yy, xx)]);
+        if (l == own) continue;
+        // insertion into a sorted distinct list
+        int k = n;
+        bool dup = false;
+        for (int j = 0; j < n; ++j)
+          if (out[j] == l) {
+            dup = true;
+            break;
+          }
+        if (dup) continue;
+        while (k > 0 && out[k - 1] > l) {
+          out[k] = out[k - 1];
+          --k;
+        }
+        out[k] = l;
+        ++n;
+      }
+  return n;
+}
+
+// Bit index of a box cell (dz, dy, dx) in [-1, 1]^3.
+__host__ __device__ __forceinline__ int box_bit(int dz, int dy, int dx) {
+  return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+}
+
+// Foreground adjacency among the 27 box cells: bit i of adj[j] set when
+// cells i and j are fg-adjacent (Chebyshev 1 for full_fg, Manhattan 1 else).
+__device__ __forceinline__ uint32_t box_adj(int j, int full_fg) {
+  int jz = j / 9 - 1, jy = (j / 3) % 3 - 1, jx = j % 3 - 1;
+  uint32_t m = 0;
+  for (int i = 0; i < 27; ++i) {
+    int iz = i / 9 - 1, iy = (i / 3) % 3 - 1, ix = i % 3 - 1;
+    int dz = abs(iz - jz), dy = abs(iy - jy), dx = abs(ix - jx);
+    int cheb = max(dz, max(dy, dx)), man = dz + dy + dx;
+    if (cheb == 0) continue;
+    if (full_fg ? cheb == 1 : man == 1) m |= 1u << i;
+  }
+  return m;
+}
+
+// Local component count of label a in the punctured 3^d box around a site
+// (contour.py:128-162): 0 = no same-label cell, 1 = all fg-adjacent
+// same-label cells connected inside the box, 2 = inconclusive.
+__device__ __forceinline__ int local_component_count(const int32_t *__restrict__ L,
+                                                     const Lat &lat, int full_fg, int64_t z,
+                                                     int64_t y, int64_t x, int32_t a) {
+  uint32_t cells = 0, seeds = 0;
+  const int zlo = lat.ndim == 3 ? -1 : 0, zhi = lat.ndim == 3 ? 1 : 0;
+  for (int dz = zlo; dz <= zhi; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        int m = abs(dz) + abs(dy) + abs(dx);
+        if (m == 0) continue;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (!lat.inb(zz, yy, xx)) continue;
+        if (L[lat.flat(zz, yy, xx)] != a) continue;
+        uint32_t bit = 1u << box_bit(dz, dy, dx);
+        cells |= bit;
+        if (full_fg || m == 1) seeds |= bit;
+      }
+  if (!cells) return 0;
+  if (!seeds) return 2;
+  uint32_t reach = seeds & (~seeds + 1);  // lowest seed
+  for (;;) {
+    uint32_t grow = reach;
+    for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, full_fg) & cells;
+    if (grow == reach) break;
+    reach = grow;
+  }
+  return (seeds & ~reach) ? 2 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// energies (energy.py:129-143, 226-230)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double g_gauss(double n, double s, double q) {
+  return n > 0.0 ? q - s * s / n : 0.0;
+}
+
+__device__ __forceinline__ double g_poisson(double n, double s) {
+  if (!(n > 0.0)) return 0.0;
+  double m = s / n;
+  m = m < kPoissonFloor ? kPoissonFloor : m;
+  return s - s * log(m);
+}
+
+__device__ __forceinline__ double rho(double i, double theta, int poisson) {
+  if (!poisson) {
+    double r = i - theta;
+    return r * r;
+  }
+  double t = theta < kPoissonFloor ? kPoissonFloor : theta;
+  return theta - i * log(t);
+}
+
+// PC increment from the region statistics (energy.py:308-324; Appendix B3).
+__device__ __forceinline__ double delta_pc(double v, int64_t ca, double sa, double qa, int64_t cb,
+                                           double sb, double qb, int poisson) {
+  double na = (double)ca, nb = (double)cb;
+  if (!poisson) {
+    double before = g_gauss(na, sa, qa) + g_gauss(nb, sb, qb);
+    double after = g_gauss(na - 1.0, sa - v, qa - v * v) + g_gauss(nb + 1.0, sb + v, qb + v * v);
+    return after - before;
+  }
+  double before = g_poisson(na, sa) + g_poisson(nb, sb);
+  double after = g_poisson(na - 1.0, sa - v) + g_poisson(nb + 1.0, sb + v);
+  return after - before;
+}
+
+// Face-count perimeter change (energy.py:91-126).
+__device__ __forceinline__ int delta_internal(const int32_t *__restrict__ L, const Lat &lat,
+                                              int64_t z, int64_t y, int64_t x, int32_t a,
+                                              int32_t b) {
+  int d = 0;
+  const int64_t c[3] = {z, y, x};
+  const int64_t n[3] = {lat.nz, lat.ny, lat.nx};
+  const int64_t st[3] = {lat.ny * lat.nx, lat.nx, 1};
+  const int64_t f = lat.flat(z, y, x);
+  for (int ax = 3 - lat.ndim; ax < 3; ++ax)
+    for (int s = -1; s <= 1; s += 2) {
+      int64_t cc = c[ax] + s;
+      if (cc < 0 || cc >= n[ax]) continue;
+      int32_t l = L[f + s * st[ax]];
+      d += (int)(l != b) - (int)(l != a);
+    }
+  return d;
+}
+
+// PS increment of one particle (energy.py:337-372; Appendix B4), with the
+// dense per-label fields replaced by own-label fields Cown/Sown and the
+// competitor's ball count/sum at x gathered during the walk.  ball holds the
+// non-centre ball offsets in ball_offsets order.  Returns the increment and,
+// through cb/sb, the competitor's ball count and sum at x.
+__device__ __forceinline__ double delta_ps(const int32_t *__restrict__ L,
+                                           const double *__restrict__ I,
+                                           const int32_t *__restrict__ Cown,
+                                           const double *__restrict__ Sown, const Lat &lat,
+                                           const Off *__restrict__ ball, int nball, int64_t z,
+                                           int64_t y, int64_t x, int32_t a, int32_t b, int poisson,
+                                           int32_t *cb_out, double *sb_out) {
+  const int64_t f = lat.flat(z, y, x);
+  const double v = I[f];
+  double acc_a = 0.0;
+  for (int k = 0; k < nball; ++k) {
+    Off o = ball[k];
+    int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+    if (!lat.inb(zz, yy, xx)) continue;
+    int64_t g = lat.flat(zz, yy, xx);
+    if (L[g] != a) continue;
+    double cy = (double)Cown[g], sy = Sown[g], iy = I[g];
+    acc_a += rho(iy, (sy - v) / (cy - 1.0), poisson) - rho(iy, sy / cy, poisson);
+  }
+  double acc_b = 0.0, sb = 0.0;
+  int32_t cb = 0;
+  for (int k = 0; k < nball; ++k) {
+    Off o = ball[k];
+    int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+    if (!lat.inb(zz, yy, xx)) continue;
+    int64_t g = lat.flat(zz, yy, xx);
+    if (L[g] != b) continue;
+    double cy = (double)Cown[g], sy = Sown[g], iy = I[g];
+    acc_b += rho(iy, (sy + v) / (cy + 1.0), poisson) - rho(iy, sy / cy, poisson);
+    cb += 1;
+    sb += iy;
+  }
+  double d = 0.0 + acc_a;
+  d = d + acc_b;
+  d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
+  d -= rho(v, Sown[f] / (double)Cown[f], poisson);
+  if (cb_out) *cb_out = cb;
+  if (sb_out) *sb_out = sb;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// ranking (optimizer.py:80-87)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t tie_key(uint64_t x, uint64_t c, uint64_t seed) {
+  uint64_t z = x * 0x9E3779B97F4A7C15ull;
+  z ^= c * 0xBF58476D1CE4E5B9ull;
+  z ^= seed;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Order-preserving map of a double to uint64 (ascending), for radix sort.
+__device__ __forceinline__ uint64_t double_key(double d) {
+  uint64_t u = (uint64_t)__double_as_longlong(d);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+}  // namespace rcb

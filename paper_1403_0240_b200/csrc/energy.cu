@@ -1,0 +1,343 @@
+// Energy kernels: K2 region statistics, K3 PC increment + perimeter change,
+// K4 own-label PS ball fields, K5 PS increment, K9 exact energy totals.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace rcb {
+
+// ---------------------------------------------------------------------------
+// K3 (energy.py:111-126, 308-324)
+// ---------------------------------------------------------------------------
+__global__ void k_delta_int(const int32_t *__restrict__ L, Lat lat, const uint32_t *__restrict__ px,
+                            const int32_t *__restrict__ pown, const int32_t *__restrict__ pcomp,
+                            int64_t n, int32_t *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t z, y, x;
+  lat.coord(px[i], z, y, x);
+  out[i] = delta_internal(L, lat, z, y, x, pown[i], pcomp[i]);
+}
+
+__global__ void k_delta_pc(const double *__restrict__ I, const uint32_t *__restrict__ px,
+                           const int32_t *__restrict__ pown, const int32_t *__restrict__ pcomp,
+                           int64_t n, const int64_t *__restrict__ cnt,
+                           const double *__restrict__ tot, const double *__restrict__ tsq,
+                           int poisson, double *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t a = pown[i], b = pcomp[i];
+  out[i] = delta_pc(__ldg(&I[px[i]]), cnt[a], tot[a], tsq[a], cnt[b], tot[b], tsq[b], poisson);
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5 (energy.py:196-223, 337-372)
+// ---------------------------------------------------------------------------
+__global__ void k_ps_fields(const int32_t *__restrict__ L, const double *__restrict__ I, Lat lat,
+                            const Off *__restrict__ ball, int nball, int32_t *__restrict__ Cown,
+                            double *__restrict__ Sown) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < lat.V; f += stride) {
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    int32_t own = __ldg(&L[f]);
+    int32_t c = 0;
+    double s = 0.0;
+    for (int k = 0; k < nball; ++k) {
+      Off o = ball[k];
+      int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+      if (!lat.inb(zz, yy, xx)) continue;
+      int64_t g = lat.flat(zz, yy, xx);
+      if (__ldg(&L[g]) != own) continue;
+      c += 1;
+      s += __ldg(&I[g]);
+    }
+    Cown[f] = c;
+    Sown[f] = s;
+  }
+}
+
+__global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restrict__ I,
+                           const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
+                           Lat lat, const Off *__restrict__ ball, int nball,
+                           const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+                           const int32_t *__restrict__ pcomp, int64_t n, int poisson,
+                           double *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t z, y, x;
+  lat.coord(px[i], z, y, x);
+  out[i] = delta_ps(L, I, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i], poisson,
+                    nullptr, nullptr);
+}
+
+int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, const int32_t *pown,
+                        const int32_t *pcomp, int64_t n, int32_t *out, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_delta_int<<<grid_for(n, 256), 256, 0, s>>>(L, lat, px, pown, pcomp, n, out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
+                       const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
+                       const double *tsq, int poisson, double *out, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_delta_pc<<<grid_for(n, 256), 256, 0, s>>>(I, px, pown, pcomp, n, cnt, tot, tsq, poisson, out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s) {
+  k_ps_fields<<<grid_for(lat.V, 256), 256, 0, s>>>(L, I, lat, ball_full, nball_full, Cown, Sown);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
+                       const Lat &lat, const Off *ball, int nball, const uint32_t *px,
+                       const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
+                       double *out, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown, pcomp,
+                                              n, poisson, out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2 — region statistics in raster order (grid.py:155-169; Appendix B8).
+// np.bincount accumulates sequentially in raster order, so each label's sum
+// is one ordered fp64 chain.  A stable radix sort by label gives every
+// label's sites in raster order; one warp per label then gathers 32 values
+// at a time and all lanes replay the ordered chain on broadcast values.
+// ---------------------------------------------------------------------------
+__global__ void k_iota(uint32_t *__restrict__ v, int64_t n) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    v[i] = (uint32_t)i;
+}
+
+__global__ void k_seg_bounds(const uint32_t *__restrict__ keys, int64_t n,
+                             int64_t *__restrict__ start, int64_t *__restrict__ end) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) start[k] = i;
+    if (i == n - 1 || keys[i + 1] != k) end[k] = i + 1;
+  }
+}
+
+__global__ void k_seq_sums(const uint32_t *__restrict__ sites, const double *__restrict__ I,
+                           const int64_t *__restrict__ start, const int64_t *__restrict__ end,
+                           int32_t nl, int64_t *__restrict__ cnt, double *__restrict__ tot,
+                           double *__restrict__ tsq) {
+  int lane = threadIdx.x & 31;
+  int32_t l = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (l >= nl) return;
+  int64_t s = start[l], e = end[l];
+  double t = 0.0, q = 0.0;
+  for (int64_t base = s; base < e; base += 32) {
+    int64_t i = base + lane;
+    double v = i < e ? __ldg(&I[sites[i]]) : 0.0;
+    int m = (e - base) < 32 ? (int)(e - base) : 32;
+    for (int j = 0; j < m; ++j) {
+      double w = __shfl_sync(0xffffffffu, v, j);
+      t += w;
+      q += w * w;
+    }
+  }
+  if (lane == 0) {
+    cnt[l] = e - s;
+    tot[l] = t;
+    tsq[l] = q;
+  }
+}
+
+int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
+                      double *tot, double *tsq, StatsScratch &sc, cudaStream_t s) {
+  RCB_TRY(sc.keys.reserve(V, s));
+  RCB_TRY(sc.vals_in.reserve(V, s));
+  RCB_TRY(sc.vals.reserve(V, s));
+  RCB_TRY(sc.bounds.reserve(2 * (size_t)nl, s));
+  k_iota<<<grid_for(V, 256), 256, 0, s>>>(sc.vals_in.p, V);
+  RCB_CUDA(cudaGetLastError());
+  int end_bit = 1;
+  while (end_bit < 32 && ((int64_t)1 << end_bit) < nl) ++end_bit;
+  size_t bytes = 0;
+  const uint32_t *keys_in = reinterpret_cast<const uint32_t *>(L);
+  RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sc.keys.p, sc.vals_in.p,
+                                           sc.vals.p, V, 0, end_bit, s));
+  RCB_TRY(sc.tmp.reserve(bytes, s));
+  RCB_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp.p, bytes, keys_in, sc.keys.p, sc.vals_in.p,
+                                           sc.vals.p, V, 0, end_bit, s));
+  int64_t *start = sc.bounds.p, *end = sc.bounds.p + nl;
+  RCB_CUDA(cudaMemsetAsync(start, 0, sizeof(int64_t) * nl, s));
+  RCB_CUDA(cudaMemsetAsync(end, 0, sizeof(int64_t) * nl, s));
+  if (V > 0) {
+    k_seg_bounds<<<grid_for(V, 256), 256, 0, s>>>(sc.keys.p, V, start, end);
+    RCB_CUDA(cudaGetLastError());
+  }
+  k_seq_sums<<<grid_for((int64_t)nl * 32, 128), 128, 0, s>>>(sc.vals.p, I, start, end, nl, cnt,
+                                                             tot, tsq);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K9 — exact sums (math.fsum semantics) with a fixed-point superaccumulator.
+// A double m*2^e (e >= -1074) is split into three 32-bit chunks added to
+// int64 limbs of weight 2^(32k-1074); the host rounds the exact total once.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void acc_add(long long *limbs, double d) {
+  if (d == 0.0) return;
+  uint64_t u = (uint64_t)__double_as_longlong(d);
+  int ex = (int)((u >> 52) & 0x7ff);
+  uint64_t m = u & ((1ull << 52) - 1);
+  int e;
+  if (ex == 0) {
+    e = -1074;
+  } else {
+    m |= 1ull << 52;
+    e = ex - 1075;
+  }
+  int pos = e + 1074;
+  int k0 = pos >> 5, sh = pos & 31;
+  uint64_t lo = m << sh;
+  uint64_t hi = sh ? (m >> (64 - sh)) : 0;
+  long long c0 = (long long)(lo & 0xffffffffull), c1 = (long long)(lo >> 32), c2 = (long long)hi;
+  if (u >> 63) {
+    c0 = -c0;
+    c1 = -c1;
+    c2 = -c2;
+  }
+  if (c0) atomicAdd((unsigned long long *)&limbs[k0], (unsigned long long)c0);
+  if (c1) atomicAdd((unsigned long long *)&limbs[k0 + 1], (unsigned long long)c1);
+  if (c2) atomicAdd((unsigned long long *)&limbs[k0 + 2], (unsigned long long)c2);
+}
+
+__device__ __forceinline__ void acc_flush(long long *sm, long long *gl) {
+  __syncthreads();
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x)
+    if (sm[k]) atomicAdd((unsigned long long *)&gl[k], (unsigned long long)sm[k]);
+}
+
+__global__ void k_pc_terms(const int64_t *__restrict__ cnt, const double *__restrict__ tot,
+                           const double *__restrict__ tsq, int32_t nl, int poisson,
+                           long long *__restrict__ limbs) {
+  __shared__ long long sm[kLimbs];
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  __syncthreads();
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nl; l += gridDim.x * blockDim.x) {
+    double n = (double)cnt[l];
+    double g = poisson ? g_poisson(n, tot[l]) : g_gauss(n, tot[l], tsq[l]);
+    acc_add(sm, g);
+  }
+  acc_flush(sm, limbs);
+}
+
+__global__ void k_ps_terms(const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
+                           const double *__restrict__ I, int64_t V, int poisson,
+                           long long *__restrict__ limbs) {
+  __shared__ long long sm[kLimbs];
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  __syncthreads();
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < V; f += stride)
+    acc_add(sm, rho(I[f], Sown[f] / (double)Cown[f], poisson));
+  acc_flush(sm, limbs);
+}
+
+__global__ void k_perimeter(const int32_t *__restrict__ L, Lat lat,
+                            unsigned long long *__restrict__ out) {
+  unsigned long long c = 0;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < lat.V; f += stride) {
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    int32_t l = L[f];
+    if (x + 1 < lat.nx) c += L[f + 1] != l;
+    if (y + 1 < lat.ny) c += L[f + lat.nx] != l;
+    if (z + 1 < lat.nz) c += L[f + lat.nx * lat.ny] != l;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,
+                       int poisson, long long *limbs, cudaStream_t s) {
+  RCB_CUDA(cudaMemsetAsync(limbs, 0, sizeof(long long) * kLimbs, s));
+  k_pc_terms<<<grid_for(nl, 256), 256, 0, s>>>(cnt, tot, tsq, nl, poisson, limbs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t ps_terms_exact(const int32_t *Cown, const double *Sown, const double *I, int64_t V,
+                       int poisson, long long *limbs, cudaStream_t s) {
+  RCB_CUDA(cudaMemsetAsync(limbs, 0, sizeof(long long) * kLimbs, s));
+  unsigned g = grid_for(V, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  k_ps_terms<<<g, 256, 0, s>>>(Cown, Sown, I, V, poisson, limbs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t perimeter(const int32_t *L, const Lat &lat, unsigned long long *out, cudaStream_t s) {
+  RCB_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
+  unsigned g = grid_for(lat.V, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  k_perimeter<<<g, 256, 0, s>>>(L, lat, out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+// Correctly rounded (nearest-even) value of the limb total, as math.fsum.
+double limbs_to_double(const long long *limbs) {
+  // carry-normalise into 32-bit digits (two's complement), then take |.|
+  const int ND = kLimbs + 3;
+  uint32_t dig[ND];
+  long long carry = 0;
+  for (int k = 0; k < ND; ++k) {
+    long long t = (k < kLimbs ? limbs[k] : 0) + carry;
+    dig[k] = (uint32_t)(t & 0xffffffffll);
+    carry = t >> 32;  // arithmetic shift
+  }
+  bool neg = carry < 0;
+  if (neg) {  // negate the ND-digit two's complement number
+    uint64_t c = 1;
+    for (int k = 0; k < ND; ++k) {
+      uint64_t t = (uint64_t)(uint32_t)~dig[k] + c;
+      dig[k] = (uint32_t)t;
+      c = t >> 32;
+    }
+  }
+  int top = -1;
+  for (int k = ND - 1; k >= 0; --k)
+    if (dig[k]) {
+      top = k * 32 + (31 - __builtin_clz(dig[k]));
+      break;
+    }
+  if (top < 0) return 0.0;
+  auto bit = [&](int p) -> uint64_t { return p < 0 ? 0 : (dig[p >> 5] >> (p & 31)) & 1u; };
+  uint64_t m = 0;
+  int shift = top >= 52 ? top - 52 : 0;
+  for (int p = top; p >= shift; --p) m = (m << 1) | bit(p);
+  if (shift > 0) {
+    uint64_t g = bit(shift - 1);
+    bool sticky = false;
+    for (int p = shift - 2; p >= 0 && !sticky; --p) sticky = bit(p) != 0;
+    if (g && (sticky || (m & 1))) {
+      ++m;
+      if (m == (1ull << 53)) {
+        m >>= 1;
+        ++shift;
+      }
+    }
+  }
+  double r = ldexp((double)m, shift - 1074);
+  return neg ? -r : r;
+}
+
+}  // namespace rcb

@@ -1,0 +1,112 @@
+// Host-side launch wrappers of the kernels (internal to librcseg_b200).
+#pragma once
+
+#include "common.cuh"
+
+namespace rcb {
+
+static constexpr int kLimbs = 68;  // superaccumulator limbs of 32 bits from 2^-1074
+
+struct StatsScratch {
+  DBuf<uint32_t> keys, vals_in, vals;
+  DBuf<int64_t> bounds;
+  DBuf<uint8_t> tmp;
+  void release(cudaStream_t s) {
+    keys.release(s);
+    vals_in.release(s);
+    vals.release(s);
+    bounds.release(s);
+    tmp.release(s);
+  }
+};
+
+struct RankScratch {
+  DBuf<uint64_t> tie, tie2, rkey, rkey2;
+  DBuf<uint32_t> idx, idx2;
+  DBuf<uint8_t> tmp;
+  void release(cudaStream_t s) {
+    tie.release(s);
+    tie2.release(s);
+    rkey.release(s);
+    rkey2.release(s);
+    idx.release(s);
+    idx2.release(s);
+    tmp.release(s);
+  }
+};
+
+struct AcceptArgs {
+  Lat lat;
+  int full_fg, region_ps, poisson, mode_l2, allow_fusion, vanish_ok;
+  double lam;
+  int64_t budget;
+  int64_t n;
+  const uint32_t *order;
+  const double *rank;
+  const uint32_t *px;
+  const int32_t *pown, *pcomp;
+  int32_t *L;
+  const double *I;
+  int64_t *cnt;
+  double *tot, *tsq;
+  int32_t *Cown;
+  double *Sown;
+  const Off *ball;
+  int nball;
+  int32_t *ncomp;
+  uint32_t *vis, *queue, *epoch;
+  int64_t *acc;
+  int64_t *moves;
+  double *energy;
+};
+
+// contour.cu
+int32_t contour_scan(const int32_t *L, const Lat &lat, int full_fg, uint32_t *site_off,
+                     DBuf<uint8_t> &tmp, cudaStream_t s);
+int32_t contour_emit(const int32_t *L, const Lat &lat, int full_fg, const uint32_t *site_off,
+                     uint32_t *px, int32_t *pown, int32_t *pcomp, cudaStream_t s);
+// energy.cu
+int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, const int32_t *pown,
+                        const int32_t *pcomp, int64_t n, int32_t *out, cudaStream_t s);
+int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
+                       const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
+                       const double *tsq, int poisson, double *out, cudaStream_t s);
+int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s);
+int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
+                       const Lat &lat, const Off *ball, int nball, const uint32_t *px,
+                       const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
+                       double *out, cudaStream_t s);
+int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
+                      double *tot, double *tsq, StatsScratch &sc, cudaStream_t s);
+int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,
+                       int poisson, long long *limbs, cudaStream_t s);
+int32_t ps_terms_exact(const int32_t *Cown, const double *Sown, const double *I, int64_t V,
+                       int poisson, long long *limbs, cudaStream_t s);
+int32_t perimeter(const int32_t *L, const Lat &lat, unsigned long long *out, cudaStream_t s);
+double limbs_to_double(const long long *limbs);
+// sobolev.cu
+std::vector<Off> sobolev_stencil(int ndim, double length_scale);
+int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *L, const uint32_t *px,
+                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *st,
+                        int nst, const double *wt, int64_t n, double *out,
+                        unsigned long long *pairs, cudaStream_t s);
+int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &lat,
+                       const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,
+                       const Off *st, int nst, const double *wt, double *d_out,
+                       unsigned long long *d_pairs, cudaStream_t s);
+// rank.cu
+int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t n,
+                   const uint32_t *px, const int32_t *pcomp, uint64_t seed, double *rank,
+                   RankScratch &sc, uint32_t *order, unsigned long long *nneg, cudaStream_t s);
+void gather_u64(const uint64_t *src, const uint32_t *idx, int64_t n, uint64_t *dst,
+                cudaStream_t s);
+// accept.cu
+int32_t accept_seq(const AcceptArgs &args, cudaStream_t s);
+int32_t label_components(const int32_t *L, const Lat &lat, int full_fg, int32_t nl,
+                         uint32_t *par_scratch, int32_t *ncomp, cudaStream_t s);
+
+// tables (abi.cu)
+std::vector<Off> ball_table(int ndim, int r);  // ball_offsets order, centre first
+
+}  // namespace rcb

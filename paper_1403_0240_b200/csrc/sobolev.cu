@@ -1,0 +1,179 @@
+// K6 — the Sobolev particle-particle interaction (Eq. 6) as a masked lattice
+// stencil over the contour set (replaces sobolev.py:137-174 sobolev_filter,
+// :52-134 CellList/pairs and the per-pair kernel_eval).
+//
+// Particles are kept sorted by (site, competitor) with the CSR lattice index
+// site_off, so for particle p the partners q with |x_q - x_p|^2 < (E/2)^2 are
+// the particles of the stencil sites x_p + o.  Visiting the stencil offsets in
+// lexicographic order and each site's particles in competitor order is the
+// reference's canonical pair order (flat q, comp q, index q) (sobolev.py:
+// 155-161), and the weight of a pair is the host table
+// w[|o|^2] = kernel_eval(sqrt(|o|^2)), so the fp64 sums are bit-identical.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace rcb {
+
+// qown == nullptr: every particle at site g is owned by L[g] (engine layout).
+// oidx != nullptr: write the result of sorted particle p to out[oidx[p]].
+__global__ void __launch_bounds__(128) k_sobolev(
+    const uint32_t *__restrict__ site_off, const int32_t *__restrict__ L,
+    const int32_t *__restrict__ qown, const int32_t *__restrict__ pcomp,
+    const uint32_t *__restrict__ px, const double *__restrict__ raw, Lat lat,
+    const Off *__restrict__ st, int nst, const double *__restrict__ wt, int64_t n,
+    double *__restrict__ out, const uint32_t *__restrict__ oidx,
+    unsigned long long *__restrict__ pairs) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long np = 0;
+  if (p < n) {
+    const int64_t f = px[p];
+    const int32_t own = qown ? qown[p] : __ldg(&L[f]);
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    double same = 0.0, opp = 0.0;
+    int64_t cs = 0, co = 0;
+    for (int k = 0; k < nst; ++k) {
+      const Off o = st[k];
+      const int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+      if (!lat.inb(zz, yy, xx)) continue;
+      const int64_t g = lat.flat(zz, yy, xx);
+      const uint32_t q0 = __ldg(&site_off[g]), q1 = __ldg(&site_off[g + 1]);
+      if (q0 == q1) continue;
+      const double w = __ldg(&wt[o.aux]);
+      const int32_t lq = qown ? 0 : __ldg(&L[g]);
+      np += q1 - q0;
+      for (uint32_t q = q0; q < q1; ++q) {
+        const double c = w * __ldg(&raw[q]);
+        const int32_t oq = qown ? __ldg(&qown[q]) : lq;
+        if (oq == own) {
+          same += c;
+          ++cs;
+        }
+        if (__ldg(&pcomp[q]) == own) {
+          opp += c;
+          ++co;
+        }
+      }
+    }
+    const double a = cs > 0 ? same / (double)cs : 0.0;
+    const double b = co > 0 ? opp / (double)co : 0.0;
+    out[oidx ? oidx[p] : p] = a - b;
+  }
+  if (pairs) {
+    for (int s = 16; s; s >>= 1) np += __shfl_down_sync(0xffffffffu, np, s);
+    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
+  }
+}
+
+// Stencil of the cutoff: offsets with |o|^2 < (E/2)^2 in lexicographic order,
+// aux = |o|^2 (index into the weight table).
+std::vector<Off> sobolev_stencil(int ndim, double length_scale) {
+  double c2 = (length_scale / 2.0) * (length_scale / 2.0);
+  int r = (int)ceil(length_scale / 2.0);
+  std::vector<Off> out;
+  for (int dz = (ndim == 3 ? -r : 0); dz <= (ndim == 3 ? r : 0); ++dz)
+    for (int dy = -r; dy <= r; ++dy)
+      for (int dx = -r; dx <= r; ++dx) {
+        int d2 = dz * dz + dy * dy + dx * dx;
+        if ((double)d2 < c2) out.push_back(Off{(int8_t)dz, (int8_t)dy, (int8_t)dx, (uint8_t)d2});
+      }
+  return out;
+}
+
+int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *L, const uint32_t *px,
+                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *st,
+                        int nst, const double *wt, int64_t n, double *out,
+                        unsigned long long *pairs, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off, L, nullptr, pcomp, px, raw, lat, st, nst,
+                                             wt, n, out, nullptr, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+// ---- function-level path: arbitrary coordinates ---------------------------
+__global__ void k_canon_keys(const int64_t *__restrict__ coords, int64_t n, int ndim, Lat lat,
+                             const int64_t *__restrict__ comps, uint64_t *__restrict__ keys,
+                             uint32_t *__restrict__ idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t z = ndim == 3 ? coords[i * 3] : 0;
+  int64_t y = coords[i * ndim + ndim - 2], x = coords[i * ndim + ndim - 1];
+  uint64_t f = (uint64_t)lat.flat(z, y, x);
+  keys[i] = (f << 32) | (uint64_t)(uint32_t)comps[i];
+  idx[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_sorted(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx,
+                                int64_t n, const int64_t *__restrict__ owners,
+                                const double *__restrict__ raw, uint32_t *__restrict__ px,
+                                int32_t *__restrict__ own, int32_t *__restrict__ comp,
+                                double *__restrict__ rraw, uint32_t *__restrict__ site_cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = keys[i];
+  uint32_t j = idx[i];
+  px[i] = (uint32_t)(k >> 32);
+  comp[i] = (int32_t)(uint32_t)(k & 0xffffffffu);
+  own[i] = (int32_t)owners[j];
+  rraw[i] = raw[j];
+  atomicAdd(&site_cnt[k >> 32], 1u);
+}
+
+int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &lat,
+                       const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,
+                       const Off *st, int nst, const double *wt, double *d_out,
+                       unsigned long long *d_pairs, cudaStream_t s) {
+  DBuf<uint64_t> keys, keys2;
+  DBuf<uint32_t> idx, idx2, px, site_off;
+  DBuf<int32_t> own, comp;
+  DBuf<double> rraw;
+  DBuf<uint8_t> tmp;
+  int32_t rc = RCB_OK;
+  auto run = [&]() -> int32_t {
+    RCB_TRY(keys.reserve(n, s));
+    RCB_TRY(keys2.reserve(n, s));
+    RCB_TRY(idx.reserve(n, s));
+    RCB_TRY(idx2.reserve(n, s));
+    RCB_TRY(px.reserve(n, s));
+    RCB_TRY(own.reserve(n, s));
+    RCB_TRY(comp.reserve(n, s));
+    RCB_TRY(rraw.reserve(n, s));
+    RCB_TRY(site_off.reserve(lat.V + 1, s));
+    k_canon_keys<<<grid_for(n, 256), 256, 0, s>>>(d_coords, n, ndim, lat, d_comps, keys.p, idx.p);
+    RCB_CUDA(cudaGetLastError());
+    size_t b1 = 0, b2 = 0;
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, keys.p, keys2.p, idx.p, idx2.p, n, 0,
+                                             64, s));
+    RCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, site_off.p, site_off.p, lat.V + 1, s));
+    RCB_TRY(tmp.reserve(b1 > b2 ? b1 : b2, s));
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, b1, keys.p, keys2.p, idx.p, idx2.p, n, 0, 64,
+                                             s));
+    RCB_CUDA(cudaMemsetAsync(site_off.p, 0, sizeof(uint32_t) * (lat.V + 1), s));
+    k_gather_sorted<<<grid_for(n, 256), 256, 0, s>>>(keys2.p, idx2.p, n, d_owners, d_raw, px.p,
+                                                     own.p, comp.p, rraw.p, site_off.p);
+    RCB_CUDA(cudaGetLastError());
+    RCB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, b2, site_off.p, site_off.p, lat.V + 1, s));
+    k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off.p, nullptr, own.p, comp.p, px.p, rraw.p,
+                                               lat, st, nst, wt, n, d_out, idx2.p, d_pairs);
+    RCB_CUDA(cudaGetLastError());
+    return RCB_OK;
+  };
+  rc = run();
+  keys.release(s);
+  keys2.release(s);
+  idx.release(s);
+  idx2.release(s);
+  px.release(s);
+  own.release(s);
+  comp.release(s);
+  rraw.release(s);
+  site_off.release(s);
+  tmp.release(s);
+  return rc;
+}
+
+}  // namespace rcb
