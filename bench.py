@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the Region Competition iteration on B200 (driver contract).
+
+Workload (BASELINE.json configs[1]): 2-D 1024x1024
+PS/Poisson, local-mean radius 4, Sobolev width 3 (E = 6), bubbles 16x16 r=10
+init, vanish_grace 5.  A step is one ``RegionCompetition.iterate()`` — particle
+extraction, ΔE, Sobolev filter, ranking and acceptance, plus the resync on
+every 10th iteration — on the device.  Inputs are seeded synthetic images
+(scenes.py); the reference's CPU path is timed beside it.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+Under torchrun each rank runs an independent image (seed 2 + rank): weak
+scaling, no data-path collective (the batched configs shard by image).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Sobolev particle-interactions/s and iterations/s; % of HBM roofline"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def loop():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([v.strip() for v in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def scene_for(rank: int, small: bool = False):
+    import scenes
+    if small:
+        return scenes.cfg2_small(seed=2 + rank)
+    return scenes.cfg2(seed=2 + rank)
+
+
+def ball_band_sites(labels, xs, radius):
+    """B_R: lattice sites within distance R of a particle."""
+    from scipy import ndimage
+    mask = np.zeros(labels.size, bool)
+    mask[xs] = True
+    mask = mask.reshape(labels.shape)
+    g = np.meshgrid(*([np.arange(-radius, radius + 1)] * labels.ndim), indexing="ij")
+    fp = sum(a * a for a in g) <= radius * radius
+    return int(ndimage.binary_dilation(mask, structure=fp).sum())
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1403_0240_b200 as P
+
+    sc = scene_for(rank, args.small)
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    scfg = P.SobolevParams(sc.length_scale)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    eng = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.iterate()
+    barrier()
+    ms_total = 0.0
+    phase = np.zeros(6)
+    launches = 0
+    pairs = 0
+    particles = 0
+    alg_bytes = 0.0
+    energy_sob_ms = 0.0
+    records = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (126 MB L2 < 512 MB)
+            torch.cuda.synchronize()
+            lab_before = eng.labels if args.roofline else None
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rec = eng.iterate()
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            ms_total += ms
+            t, nl = eng.timings()
+            phase += np.array(t)
+            launches += nl
+            pairs += eng.last_pairs
+            n = len(eng.last_candidates[0]) if args.roofline else 0
+            particles += n
+            if args.roofline and n:
+                xs = eng.last_candidates[0]
+                B = ball_band_sites(lab_before, xs, sc.smooth_radius)
+                alg_bytes += 29 * n + 24 * B + 28 * n
+                energy_sob_ms += t[1] + t[2]
+            records.append((rec.iteration, rec.moves, rec.particles, ms))
+    barrier()
+    tmax = ms_total
+    if ws > 1:
+        tt = torch.tensor([ms_total], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        tmax = float(tt.item())
+    value = args.steps * ws / (tmax / 1e3)
+
+    # end-to-end through the public API from host buffers: construct from
+    # pinned host arrays (H2D), iterate K times (each reads back its record),
+    # read the labels back (D2H); wall clock, max over ranks.
+    img_h = torch.from_numpy(np.ascontiguousarray(sc.image, np.float64)).pin_memory().numpy()
+    lab_h = torch.from_numpy(np.ascontiguousarray(sc.labels, np.int32)).pin_memory().numpy()
+    barrier()
+    t0 = time.perf_counter()
+    e2 = P.RegionCompetition(img_h, lab_h, ecfg, scfg, ocfg, device=local)
+    for _ in range(args.warmup + args.steps):
+        e2.iterate()
+    out_labels = e2.labels
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    n_e2e = args.warmup + args.steps
+    del e2
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "iterations/s",
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": tmax / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (scenes.cfg2: seeded ellipses, blur 1.5, Poisson peak 50)",
+            "config": {"workload": "cfg2: 2-D 1024x1024 PS/Poisson R=4, Sobolev w=3 (E=6), "
+                                   "bubbles 16x16 r=10, iterations continue from warm-up",
+                       "l2": "flushed between timed iterations (512 MB write)",
+                       "parallelism": f"{ws} independent images (one per GPU)"},
+            "particle_interactions_per_s": pairs / max(1e-9, phase[2] / 1e3),
+            "interactions_per_iteration": pairs / args.steps,
+            "particles_per_iteration": particles / args.steps if particles else None,
+            "phase_ms_per_iteration": dict(zip(["extract", "energy", "sobolev", "rank",
+                                                "accept+rescan", "iterate"],
+                                               (phase / args.steps).round(4).tolist())),
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": {"value": n_e2e * ws / e2e_s, "unit": "iterations/s",
+                    "h2d_bytes_per_step": (img_h.nbytes + lab_h.nbytes) / n_e2e,
+                    "d2h_bytes_per_step": (out_labels.nbytes + 64 * n_e2e) / n_e2e,
+                    "what": "RegionCompetition(host image, host labels) + K iterate() + labels, "
+                            "wall clock"},
+        }
+        if args.roofline and energy_sob_ms > 0:
+            ach = alg_bytes / (energy_sob_ms / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak,
+                                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                                "peak_kind": peak_kind,
+                                "kernels": "K5 PS energy + K6 Sobolev (SURVEY §8d bytes: "
+                                           "29N + 24B_R + 28N per iteration)"}
+        if args.cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(args, steps=None, budget_s=25.0):
+    """The oracle port (oracle/rc_oracle.py, a numpy restatement of the
+    reference; single-threaded like the reference) on the host cores, on a
+    bounded sample of the same workload: the first iterations of cfg2."""
+    from oracle import rc_oracle as O
+    sc = scene_for(0, args.small)
+    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    t0 = time.perf_counter()
+    eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
+                         sc.length_scale, config=cfg)
+    t_init = time.perf_counter() - t0
+    done = 0
+    t1 = time.perf_counter()
+    while True:
+        eng.iterate()
+        done += 1
+        el = time.perf_counter() - t1
+        if (steps is not None and done >= steps) or (steps is None and el > budget_s):
+            break
+    el = time.perf_counter() - t1
+    return {"value": done / el, "unit": "iterations/s", "cores": 1, "kind": "port",
+            "sample": f"first {done} iterations of cfg2 (after a {t_init:.1f} s constructor), "
+                      f"oracle port of the reference, 1 thread"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cap_s = 150.0
+    from oracle import rc_oracle as O
+    sc = scene_for(0, args.small)
+    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
+                         sc.length_scale, config=cfg)
+    t_all = time.perf_counter()
+    for _ in range(min(args.warmup, 1)):
+        eng.iterate()
+    done = 0
+    t0 = time.perf_counter()
+    while done < args.steps:
+        eng.iterate()
+        done += 1
+        if time.perf_counter() - t_all > cap_s:
+            break
+    el = time.perf_counter() - t0
+    v = done / el
+    line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": ws, "steps": done,
+            "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * el / done,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (scenes.cfg2)", "impl": "reference",
+            "config": {"workload": "cfg2: 2-D 1024x1024 PS/Poisson R=4, Sobolev w=3 (E=6), "
+                                   "bubbles 16x16 r=10"},
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
+                             "sample": f"{done} iterations of cfg2 after {min(args.warmup, 1)} "
+                                       f"warm-up (capped at {cap_s:.0f} s), oracle port of "
+                                       "the reference, single-threaded like the reference"},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--small", action="store_true", help="256^2 crop (debug)")
+    ap.add_argument("--no-roofline", dest="roofline", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -2,6 +2,7 @@
 // RegionCompetition.iterate (optimizer.py:122-160) and the function-level
 // drop-ins.  Each entry point cites the reference function it replaces.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -109,6 +110,14 @@ struct rcb_engine {
   DBuf<int32_t> pown, pcomp, dint;
   DBuf<double> raw, smooth, rank;
   DBuf<int64_t> acc;
+  // parallel acceptance state (accept_par.cu)
+  DBuf<int32_t> newlab, wpos, pend, dround, lab_pend, nown, bfs_list, ctl, dint_acc;
+  DBuf<uint8_t> dec, small, dirty;
+  DBuf<int64_t> cnt0;
+  DBuf<uint32_t> gq1, slot;
+  DBuf<double> dtot;
+  bool simple_topology = false;
+  bool force_sequential = false;
   DBuf<Scalars> sc;
   DBuf<uint8_t> tmp;
   StatsScratch ssc;
@@ -126,6 +135,10 @@ struct rcb_engine {
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
       raw.release(s); smooth.release(s); rank.release(s); acc.release(s); sc.release(s);
+      newlab.release(s); wpos.release(s); pend.release(s); dround.release(s); lab_pend.release(s);
+      nown.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
+      small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
+      dtot.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
       for (auto &e : ev)
@@ -153,7 +166,14 @@ struct rcb_engine {
   }
 
   int32_t components() {
-    return label_components(L.p, lat, ocfg.full_fg, nl, queue.p, ncomp.p, s);
+    RCB_TRY(label_components(L.p, lat, ocfg.full_fg, nl, queue.p, ncomp.p, s));
+    std::vector<int32_t> h(nl);
+    RCB_CUDA(cudaMemcpyAsync(h.data(), ncomp.p, 4 * nl, cudaMemcpyDeviceToHost, s));
+    RCB_CUDA(cudaStreamSynchronize(s));
+    simple_topology = true;
+    for (int32_t l = 1; l < nl; ++l)
+      if (h[l] > 1) simple_topology = false;
+    return RCB_OK;
   }
 };
 
@@ -197,6 +217,10 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   e->ecfg = *ecfg;
   e->ocfg = *ocfg;
   e->mode = ocfg->gradient;
+  {
+    const char *fs = getenv("RCB_FORCE_SEQUENTIAL");  // testing: exact single-thread acceptance
+    e->force_sequential = fs && fs[0] == '1';
+  }
   const int64_t V = e->lat.V;
   int32_t mx = 0;
   for (int64_t i = 0; i < V; ++i) {
@@ -244,6 +268,24 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   e->nst = (int)st.size();
   TRYB(upload(e->st, st.data(), st.size(), s));
   TRYB(upload(e->wt, scfg->weights, (size_t)scfg->n_weights, s));
+  TRYB(e->newlab.reserve(V, s));
+  TRYB(e->wpos.reserve(V, s));
+  TRYB(e->pend.reserve(V, s));
+  TRYB(e->gq1.reserve(V, s));
+  TRYB(e->lab_pend.reserve(e->nl, s));
+  TRYB(e->nown.reserve(e->nl, s));
+  TRYB(e->small.reserve(e->nl, s));
+  TRYB(e->cnt0.reserve(e->nl, s));
+  TRYB(e->ctl.reserve(16, s));
+  if (cudaMemsetAsync(e->wpos.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
+      cudaMemsetAsync(e->pend.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
+      cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "memset failed"));
+  if (ecfg->region_model == 1) {
+    TRYB(e->dirty.reserve(V, s));
+    if (cudaMemsetAsync(e->dirty.p, 0, V, s) != cudaSuccess)
+      return bail(fail(RCB_ERR_CUDA, "memset failed"));
+  }
   for (auto &ev : e->ev) cudaEventCreate(&ev);
   TRYB(e->refresh());
   TRYB(e->components());
@@ -301,40 +343,107 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     RCB_TRY(rank_order(base, e->dint.p, e->ecfg.lam, n, e->px.p, e->pcomp.p, e->ocfg.seed,
                        e->rank.p, e->rsc, e->order.p, &d->nneg, s));
     cudaEventRecord(e->ev[4], s);
-    AcceptArgs A{};
-    A.lat = lat;
-    A.full_fg = e->ocfg.full_fg;
-    A.region_ps = e->ecfg.region_model == 1;
-    A.poisson = poisson;
-    A.mode_l2 = e->mode == 0;
-    A.allow_fusion = e->ocfg.allow_fusion;
-    A.vanish_ok = e->ocfg.allow_vanish && e->iteration > e->ocfg.vanish_grace;
-    A.lam = e->ecfg.lam;
-    A.budget = (int64_t)ceil(e->ocfg.move_budget * (double)n);
-    A.n = n;
-    A.order = e->order.p;
-    A.rank = e->rank.p;
-    A.px = e->px.p;
-    A.pown = e->pown.p;
-    A.pcomp = e->pcomp.p;
-    A.L = e->L.p;
-    A.I = e->I.p;
-    A.cnt = e->cnt.p;
-    A.tot = e->tot.p;
-    A.tsq = e->tsq.p;
-    A.Cown = e->Cown.p;
-    A.Sown = e->Sown.p;
-    A.ball = e->ball.p;
-    A.nball = e->nball;
-    A.ncomp = e->ncomp.p;
-    A.vis = e->vis.p;
-    A.queue = e->queue.p;
-    A.epoch = &d->epoch;
-    A.acc = e->acc.p;
-    A.moves = &d->moves;
-    A.energy = &d->energy;
-    RCB_TRY(accept_seq(A, s));
-    launches += 1 + 4 + 1 + 3 * 8;  // emit, dint, dE, rank, 2 radix sorts (~8 passes)
+    const bool par = e->mode == 1 && e->ocfg.full_fg && e->simple_topology && !e->force_sequential;
+    const int64_t budget = (int64_t)ceil(e->ocfg.move_budget * (double)n);
+    if (par) {
+      RCB_TRY(e->dec.reserve(n, s));
+      RCB_TRY(e->dround.reserve(n, s));
+      RCB_TRY(e->bfs_list.reserve(n, s));
+      RCB_TRY(e->slot.reserve(n + 1, s));
+      RCB_TRY(e->dint_acc.reserve(n, s));
+      RCB_TRY(e->dtot.reserve(n, s));
+      ParArgs P{};
+      P.lat = lat;
+      P.allow_fusion = e->ocfg.allow_fusion;
+      P.vanish_ok = e->ocfg.allow_vanish && e->iteration > e->ocfg.vanish_grace;
+      P.nl = e->nl;
+      P.nneg = &d->nneg;
+      P.order = e->order.p;
+      P.px = e->px.p;
+      P.pown = e->pown.p;
+      P.pcomp = e->pcomp.p;
+      P.L = e->L.p;
+      P.newlab = e->newlab.p;
+      P.w = e->wpos.p;
+      P.pend = e->pend.p;
+      P.dec = e->dec.p;
+      P.dround = e->dround.p;
+      P.small = e->small.p;
+      P.lab_pend = e->lab_pend.p;
+      P.nown = e->nown.p;
+      P.cnt = e->cnt.p;
+      P.cnt0 = e->cnt0.p;
+      P.bfs_list = e->bfs_list.p;
+      P.ctl = e->ctl.p;
+      P.vis = e->vis.p;
+      P.epoch = &d->epoch;
+      P.gq[0] = e->queue.p;
+      P.gq[1] = e->gq1.p;
+      P.dint_acc = e->dint_acc.p;
+      ParExtra X{};
+      X.n_particles = n;
+      X.budget = budget;
+      X.slot = e->slot.p;
+      X.tmp = &e->tmp;
+      X.acc = e->acc.p;
+      X.moves = &d->moves;
+      X.I = e->I.p;
+      X.tot = e->tot.p;
+      X.tsq = e->tsq.p;
+      X.energy = &d->energy;
+      X.dtot = e->dtot.p;
+      X.ncomp = e->ncomp.p;
+      X.Lmut = e->L.p;
+      X.region_ps = e->ecfg.region_model == 1;
+      X.poisson = poisson;
+      X.lam = e->ecfg.lam;
+      X.ball = e->ball.p;
+      X.ball_full = e->ball_full.p;
+      X.nball = e->nball;
+      X.nball_full = e->nball_full;
+      X.dirty = e->dirty.p;
+      X.Cown = e->Cown.p;
+      X.Sown = e->Sown.p;
+      int nla = 0;
+      RCB_TRY(accept_par(P, X, s, &nla));
+      launches += nla;
+    } else {
+      AcceptArgs A{};
+      A.lat = lat;
+      A.full_fg = e->ocfg.full_fg;
+      A.region_ps = e->ecfg.region_model == 1;
+      A.poisson = poisson;
+      A.mode_l2 = e->mode == 0;
+      A.allow_fusion = e->ocfg.allow_fusion;
+      A.vanish_ok = e->ocfg.allow_vanish && e->iteration > e->ocfg.vanish_grace;
+      A.lam = e->ecfg.lam;
+      A.budget = budget;
+      A.n = n;
+      A.order = e->order.p;
+      A.rank = e->rank.p;
+      A.px = e->px.p;
+      A.pown = e->pown.p;
+      A.pcomp = e->pcomp.p;
+      A.L = e->L.p;
+      A.I = e->I.p;
+      A.cnt = e->cnt.p;
+      A.tot = e->tot.p;
+      A.tsq = e->tsq.p;
+      A.Cown = e->Cown.p;
+      A.Sown = e->Sown.p;
+      A.ball = e->ball.p;
+      A.nball = e->nball;
+      A.ncomp = e->ncomp.p;
+      A.vis = e->vis.p;
+      A.queue = e->queue.p;
+      A.epoch = &d->epoch;
+      A.acc = e->acc.p;
+      A.moves = &d->moves;
+      A.energy = &d->energy;
+      RCB_TRY(accept_seq(A, s));
+  launches += 1;
+    }
+    launches += 4 + 1 + 3 * 8;  // emit, dint, dE, rank, 2 radix sorts (~8 passes each)
   } else {
     for (int k = 1; k < 5; ++k) cudaEventRecord(e->ev[k], s);
   }

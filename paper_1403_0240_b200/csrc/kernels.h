@@ -60,6 +60,43 @@ struct AcceptArgs {
   double *energy;
 };
 
+struct ParArgs {
+  Lat lat;
+  int allow_fusion, vanish_ok;
+  int32_t nl;
+  const unsigned long long *nneg;
+  const uint32_t *order, *px;
+  const int32_t *pown, *pcomp;
+  const int32_t *L;  // iteration-start raster (read-only during the rounds)
+  int32_t *newlab, *w, *pend;
+  uint8_t *dec;
+  int32_t *dround;
+  uint8_t *small;
+  int32_t *lab_pend, *nown;
+  int64_t *cnt, *cnt0;
+  int32_t *bfs_list, *ctl;
+  uint32_t *vis, *epoch;
+  uint32_t *gq[2];
+  int32_t *dint_acc;
+};
+
+struct ParExtra {
+  int64_t n_particles, budget;
+  uint32_t *slot;
+  DBuf<uint8_t> *tmp;
+  int64_t *acc, *moves;
+  const double *I;
+  double *tot, *tsq, *energy, *dtot;
+  int32_t *ncomp, *Lmut;
+  int region_ps, poisson;
+  double lam;
+  const Off *ball, *ball_full;
+  int nball, nball_full;
+  uint8_t *dirty;
+  int32_t *Cown;
+  double *Sown;
+};
+
 // contour.cu
 int32_t contour_scan(const int32_t *L, const Lat &lat, int full_fg, uint32_t *site_off,
                      DBuf<uint8_t> &tmp, cudaStream_t s);
@@ -105,6 +142,10 @@ void gather_u64(const uint64_t *src, const uint32_t *idx, int64_t n, uint64_t *d
 int32_t accept_seq(const AcceptArgs &args, cudaStream_t s);
 int32_t label_components(const int32_t *L, const Lat &lat, int full_fg, int32_t nl,
                          uint32_t *par_scratch, int32_t *ncomp, cudaStream_t s);
+
+// accept_par.cu
+int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches);
+size_t accept_par_smem();
 
 // tables (abi.cu)
 std::vector<Off> ball_table(int ndim, int r);  // ball_offsets order, centre first

@@ -241,3 +241,33 @@ def test_engine_invariants_at_full_cfg2_size(P):
     for l in np.unique(lab):
         if l > 0:
             assert ndimage.label(lab == l, structure=conn.fg_structure)[1] == 1
+
+
+@pytest.mark.parametrize("which", ["cfg2", "cfg1", "cfg3_small"])
+def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
+    """K8 v2 (cooperative rounds) against K8 v1 (one thread, the literal
+    sequential greedy) on the same inputs: accepted moves in order, labels and
+    ledger must be identical."""
+    import scenes
+    if which == "cfg2":
+        sc, iters = scenes.cfg2(), 3
+    elif which == "cfg1":
+        sc, iters = scenes.cfg1(), 6
+    else:
+        sc, iters = scenes.cfg3(n=48), 3
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    runs = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("RCB_FORCE_SEQUENTIAL", force)
+        eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
+        out = []
+        for _ in range(iters):
+            rec = eng.iterate()
+            out.append((rec.moves, rec.energy, eng.last_accepted.copy(), eng.labels))
+        runs.append(out)
+    for it, (a, b) in enumerate(zip(*runs)):
+        assert a[0] == b[0], (which, it)
+        assert np.array_equal(a[2], b[2]), (which, it)
+        assert np.array_equal(a[3], b[3]), (which, it)
+        assert a[1] == b[1], (which, it, a[1], b[1])
