@@ -145,6 +145,7 @@ def run_ours(args):
     alg_bytes = 0.0
     energy_sob_ms = 0.0
     records = []
+    ctr_sum = {}
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (126 MB L2 < 512 MB)
@@ -170,6 +171,8 @@ def run_ours(args):
                 alg_bytes += 29 * n + 24 * B + 28 * n
                 energy_sob_ms += t[1] + t[2]
             records.append((rec.iteration, rec.moves, rec.particles, ms))
+            for k, v in eng.counters().items():
+                ctr_sum[k] = ctr_sum.get(k, 0) + v
     barrier()
     tmax = ms_total
     if ws > 1:
@@ -224,6 +227,7 @@ def run_ours(args):
                                                 "accept+rescan", "iterate"],
                                                (phase / args.steps).round(4).tolist())),
             "gpu_launches": int(launches),
+            "acceptance_per_iteration": {k: v / args.steps for k, v in ctr_sum.items()},
             "clocks": clk.summary(),
             "e2e": {"value": n_e2e * ws / e2e_s, "unit": "iterations/s",
                     "h2d_bytes_per_step": (img_h.nbytes + lab_h.nbytes) / n_e2e,

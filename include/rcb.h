@@ -152,6 +152,12 @@ int32_t rcb_engine_stream(rcb_engine *eng, void **stream);
  * stream: [0] extract, [1] energy, [2] sobolev, [3] rank/sort, [4] accept,
  * [5] whole iteration.  Also the kernel launch count of the last iterate. */
 int32_t rcb_engine_timings(rcb_engine *eng, float *ms6, int32_t *launches);
+/* Acceptance diagnostics of the last iterate(): [0] rounds, [1] block BFS
+ * runs, [2] deferred to the global BFS, [3] BFS aborted on a pending site,
+ * [4] candidates with rank < 0, [5] accepted moves, [6] 1 if the parallel
+ * acceptance ran (0 = sequential), [7] device us of the acceptance kernels,
+ * [8] total BFS levels, [9] deepest BFS (levels). */
+int32_t rcb_engine_counters(rcb_engine *eng, int64_t *out10);
 
 #ifdef __cplusplus
 }

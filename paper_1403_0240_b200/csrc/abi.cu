@@ -111,11 +111,13 @@ struct rcb_engine {
   DBuf<double> raw, smooth, rank;
   DBuf<int64_t> acc;
   // parallel acceptance state (accept_par.cu)
-  DBuf<int32_t> newlab, wpos, pend, dround, lab_pend, nown, bfs_list, ctl, dint_acc;
+  DBuf<int32_t> newlab, wpos, pend, dround, lab_pend, nown, bfs_list, ctl, dint_acc, blocker;
   DBuf<uint8_t> dec, small, dirty;
   DBuf<int64_t> cnt0;
   DBuf<uint32_t> gq1, slot;
-  DBuf<double> dtot;
+  DBuf<double> dtot, snap, evv;
+  DBuf<uint32_t> evkey, evkey2, evval, evval2;
+  DBuf<int64_t> evbounds;
   bool simple_topology = false;
   bool force_sequential = false;
   DBuf<Scalars> sc;
@@ -124,6 +126,10 @@ struct rcb_engine {
   RankScratch rsc;
   Scalars *hsc = nullptr;  // pinned
   cudaEvent_t ev[6] = {};
+  cudaEvent_t ev_acc[2] = {};
+  int32_t hctl[16] = {};
+  int64_t counters[10] = {};
+  bool last_par = false;
   float times[6] = {};
   int32_t launches = 0;
 
@@ -136,12 +142,15 @@ struct rcb_engine {
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
       raw.release(s); smooth.release(s); rank.release(s); acc.release(s); sc.release(s);
       newlab.release(s); wpos.release(s); pend.release(s); dround.release(s); lab_pend.release(s);
-      nown.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
+      nown.release(s); blocker.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
-      dtot.release(s);
+      dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
+      evval2.release(s); evbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
       for (auto &e : ev)
+        if (e) cudaEventDestroy(e);
+      for (auto &e : ev_acc)
         if (e) cudaEventDestroy(e);
       if (own_stream) cudaStreamDestroy(s);
     }
@@ -287,6 +296,7 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
       return bail(fail(RCB_ERR_CUDA, "memset failed"));
   }
   for (auto &ev : e->ev) cudaEventCreate(&ev);
+  for (auto &ev : e->ev_acc) cudaEventCreate(&ev);
   TRYB(e->refresh());
   TRYB(e->components());
   TRYB(e->prepare());
@@ -351,6 +361,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       RCB_TRY(e->bfs_list.reserve(n, s));
       RCB_TRY(e->slot.reserve(n + 1, s));
       RCB_TRY(e->dint_acc.reserve(n, s));
+      RCB_TRY(e->blocker.reserve(n, s));
       RCB_TRY(e->dtot.reserve(n, s));
       ParArgs P{};
       P.lat = lat;
@@ -380,6 +391,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       P.gq[0] = e->queue.p;
       P.gq[1] = e->gq1.p;
       P.dint_acc = e->dint_acc.p;
+      P.blocker = e->blocker.p;
       ParExtra X{};
       X.n_particles = n;
       X.budget = budget;
@@ -401,11 +413,23 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.ball_full = e->ball_full.p;
       X.nball = e->nball;
       X.nball_full = e->nball_full;
+      X.radius = e->ecfg.smooth_radius;
       X.dirty = e->dirty.p;
       X.Cown = e->Cown.p;
       X.Sown = e->Sown.p;
+      X.evkey = &e->evkey;
+      X.evkey2 = &e->evkey2;
+      X.evval = &e->evval;
+      X.evval2 = &e->evval2;
+      X.bounds = &e->evbounds;
+      X.snap = &e->snap;
+      X.evv = &e->evv;
       int nla = 0;
+      RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));
+      cudaEventRecord(e->ev_acc[0], s);
       RCB_TRY(accept_par(P, X, s, &nla));
+      cudaEventRecord(e->ev_acc[1], s);
+      RCB_CUDA(cudaMemcpyAsync(e->hctl, e->ctl.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, s));
       launches += nla;
     } else {
       AcceptArgs A{};
@@ -456,6 +480,22 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
   RCB_CUDA(cudaMemcpyAsync(e->hsc, d, offsetof(Scalars, limbs), cudaMemcpyDeviceToHost, s));
   RCB_CUDA(cudaStreamSynchronize(s));
   e->n_scored = n;
+  e->last_par = n > 0 && e->mode == 1 && e->ocfg.full_fg && e->simple_topology &&
+                !e->force_sequential;
+  {
+    float acc_ms = 0.f;
+    if (e->last_par) cudaEventElapsedTime(&acc_ms, e->ev_acc[0], e->ev_acc[1]);
+    e->counters[0] = e->last_par ? e->hctl[5] : 0;
+    e->counters[1] = e->last_par ? e->hctl[6] : 0;
+    e->counters[2] = e->last_par ? e->hctl[7] : 0;
+    e->counters[3] = e->last_par ? e->hctl[8] : 0;
+    e->counters[4] = (int64_t)e->hsc->nneg;
+    e->counters[5] = e->hsc->moves;
+    e->counters[6] = e->last_par ? 1 : 0;
+    e->counters[7] = (int64_t)(acc_ms * 1000.f);
+    e->counters[8] = e->last_par ? e->hctl[9] : 0;
+    e->counters[9] = e->last_par ? e->hctl[10] : 0;
+  }
   e->N = e->hsc->n_next;
   e->prepared = true;
   e->last_moves = e->hsc->moves;
@@ -633,6 +673,11 @@ int32_t rcb_engine_evaluate(rcb_engine *e, double *external, int64_t *internal) 
 
 int32_t rcb_engine_stream(rcb_engine *e, void **stream) {
   *stream = (void *)e->s;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_counters(rcb_engine *e, int64_t *out8) {
+  for (int k = 0; k < 10; ++k) out8[k] = e->counters[k];
   return RCB_OK;
 }
 

@@ -25,10 +25,12 @@
 // single component at iteration start (so components(a\{x}) == pieces).
 #include <cooperative_groups.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "dev.cuh"
 #include "kernels.h"
+#include "ordered_sum.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -41,7 +43,8 @@ static constexpr int kMaxInsert = kHC * 5 / 8;
 static constexpr unsigned long long kEmpty = ~0ull;
 
 enum : uint8_t { UNDEC = 0, ACC = 1, REJ = 2, DEFER = 3 };
-enum { C_NUND0 = 0, C_NUND1, C_MIN0, C_MIN1, C_BFS, C_ROUNDS, C_BFSRUNS, C_DEFER, C_BLOCKED, C_N };
+enum { C_NUND0 = 0, C_NUND1, C_MIN0, C_MIN1, C_BFS, C_ROUNDS, C_BFSRUNS, C_DEFER, C_BLOCKED,
+       C_LEVELS, C_MAXLEV, C_N };
 
 __device__ __forceinline__ int32_t ld(const int32_t *p) { return __ldcg(p); }
 
@@ -49,8 +52,16 @@ struct View {
   const ParArgs &A;
   int32_t pos;
   __device__ __forceinline__ int32_t lab(int64_t y) const {
-    int32_t wy = ld(A.w + y);
-    return wy < pos ? ld(A.newlab + y) : __ldg(A.L + y);
+    const int32_t wy = ld(A.w + y);
+    const int32_t l0 = __ldg(A.L + y);
+    return wy < pos ? ld(A.newlab + y) : l0;
+  }
+  // label and pending flag with the three loads issued together
+  __device__ __forceinline__ int32_t lab_pend(int64_t y, int32_t &pmin) const {
+    const int32_t wy = ld(A.w + y);
+    const int32_t l0 = __ldg(A.L + y);
+    pmin = ld(A.pend + y);
+    return wy < pos ? ld(A.newlab + y) : l0;
   }
   __device__ __forceinline__ bool pending(int64_t y) const { return ld(A.pend + y) < pos; }
 };
@@ -101,6 +112,123 @@ __device__ __forceinline__ bool box_fusion_bad(const int32_t *lab, int32_t a, in
   return false;
 }
 
+// ---------------------------------------------------------------------------
+// Second-tier exact local test on a (2r+1)^d window (r = 3 in 2-D, 2 in 3-D),
+// used when the reference's 3^d test is inconclusive.  Components of the
+// donor label inside the window (x removed) are flooded bit-parallel.
+// Returns 1 if every seed (same-label fg-neighbour of x) lies in one window
+// component (=> one piece globally), 2 if a seed component is closed inside
+// the window while another seed lies outside it (=> >= 2 pieces globally),
+// 0 if inconclusive, -2 if a window site still has an earlier undecided
+// candidate.  Both verdicts are exact consequences of the global question,
+// so results stay identical to the reference's flood fill.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int window_pieces_2d(const View &v, const Lat &lat, int64_t y,
+                                                int64_t x, int32_t a) {
+  constexpr int R = 3, W = 7;
+  constexpr uint64_t FULL = (1ull << 49) - 1;
+  uint64_t col0 = 0, col6 = 0, border = 0;
+  for (int r = 0; r < W; ++r) {
+    col0 |= 1ull << (r * W);
+    col6 |= 1ull << (r * W + W - 1);
+  }
+  border = col0 | col6 | 0x7full | (0x7full << 42);
+  uint64_t cells = 0;
+  for (int dy = -R; dy <= R; ++dy)
+    for (int dx = -R; dx <= R; ++dx) {
+      if (dy == 0 && dx == 0) continue;
+      int64_t yy = y + dy, xx = x + dx;
+      if (!lat.inb(0, yy, xx)) continue;
+      int64_t g = lat.flat(0, yy, xx);
+      if (v.pending(g)) return -2;
+      if (v.lab(g) == a) cells |= 1ull << ((dy + R) * W + dx + R);
+    }
+  uint64_t seeds = 0;
+  for (int dy = -1; dy <= 1; ++dy)
+    for (int dx = -1; dx <= 1; ++dx)
+      if (dy || dx) seeds |= 1ull << ((dy + R) * W + dx + R);
+  seeds &= cells;
+  auto flood = [&](uint64_t r) {
+    for (;;) {
+      uint64_t l = r & ~col0, h = r & ~col6;
+      uint64_t n = r | (h << 1) | (l >> 1) | (r << W) | (r >> W) | (h << (W + 1)) |
+                   (l << (W - 1)) | (h >> (W - 1)) | (l >> (W + 1));
+      n &= cells & FULL;
+      if (n == r) return r;
+      r = n;
+    }
+  };
+  uint64_t c0 = flood(seeds & (~seeds + 1));
+  if ((seeds & ~c0) == 0) return 1;
+  if ((c0 & border) == 0) return 2;
+  for (uint64_t rest = seeds & ~c0; rest;) {
+    uint64_t c = flood(rest & (~rest + 1));
+    if ((c & border) == 0) return 2;
+    rest &= ~c;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ int window_pieces_3d(const View &v, const Lat &lat, int64_t z,
+                                                int64_t y, int64_t x, int32_t a) {
+  typedef unsigned __int128 u128;
+  constexpr int R = 2, W = 5;
+  u128 one = 1, cells = 0, seeds = 0, border = 0, nx0 = 0, nx4 = 0, ny0 = 0, ny4 = 0;
+  for (int k = 0; k < W * W * W; ++k) {
+    int cz = k / 25, cy = (k / 5) % 5, cx = k % 5;
+    u128 bit = one << k;
+    if (cz == 0 || cz == 4 || cy == 0 || cy == 4 || cx == 0 || cx == 4) border |= bit;
+    if (cx != 0) nx0 |= bit;
+    if (cx != 4) nx4 |= bit;
+    if (cy != 0) ny0 |= bit;
+    if (cy != 4) ny4 |= bit;
+  }
+  const u128 FULL = (one << 125) - 1;
+  for (int dz = -R; dz <= R; ++dz)
+    for (int dy = -R; dy <= R; ++dy)
+      for (int dx = -R; dx <= R; ++dx) {
+        if (!dz && !dy && !dx) continue;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (!lat.inb(zz, yy, xx)) continue;
+        int64_t g = lat.flat(zz, yy, xx);
+        if (v.pending(g)) return -2;
+        if (v.lab(g) == a) {
+          u128 bit = one << ((dz + R) * 25 + (dy + R) * 5 + dx + R);
+          cells |= bit;
+          if (abs(dz) <= 1 && abs(dy) <= 1 && abs(dx) <= 1) seeds |= bit;
+        }
+      }
+  auto flood = [&](u128 r) {
+    for (;;) {
+      u128 n = r;
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            if (!dz && !dy && !dx) continue;
+            u128 m = r;
+            if (dx == 1) m &= nx4;
+            if (dx == -1) m &= nx0;
+            if (dy == 1) m &= ny4;
+            if (dy == -1) m &= ny0;
+            int sh = dz * 25 + dy * 5 + dx;
+            n |= sh > 0 ? (m << sh) : (m >> (-sh));
+          }
+      n &= cells & FULL;
+      if (n == r) return r;
+      r = n;
+    }
+  };
+  u128 c0 = flood(seeds & (~seeds + 1));
+  if ((seeds & ~c0) == 0) return 1;
+  if ((c0 & border) == 0) return 2;
+  for (u128 rest = seeds & ~c0; rest != 0;) {
+    u128 c = flood(rest & (~rest + 1));
+    if ((c & border) == 0) return 2;
+    rest &= ~c;
+  }
+  return 0;
+}
+
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
   x *= 0x7feb352dU;
@@ -120,7 +248,7 @@ struct BfsShared {
   uint32_t unions[27];
   int nseed;
   int ninsert;
-  int blocked, overflow, result;
+  int blocked, overflow, result, levels, blocker;
   int32_t pos, a, b;
   int64_t x;
 };
@@ -171,6 +299,8 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
     S.b = A.pcomp[p];
     S.ninsert = 0;
     S.blocked = S.overflow = 0;
+    S.levels = 0;
+    S.blocker = 0x7fffffff;
     S.result = -1;
     S.nfr[0] = S.nfr[1] = 0;
   }
@@ -223,11 +353,14 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
         if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
         int64_t t = lat.flat(zz, yy, xx);
         if (t == xc) continue;
-        if (v.pending(t)) {
+        int32_t pm;
+        const int32_t lt = v.lab_pend(t, pm);
+        if (pm < v.pos) {
           S.blocked = 1;
+          atomicMin(&S.blocker, pm);
           continue;
         }
-        if (v.lab(t) != a) continue;
+        if (lt != a) continue;
         uint32_t h = hash32((uint32_t)t) & (kHC - 1);
         for (;;) {
           unsigned long long cv = S.key[h];
@@ -261,6 +394,7 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
     if (threadIdx.x == 0) {
       S.result = bfs_level_verdict(S, nxt);
       S.nfr[cur] = 0;
+      S.levels += 1;
     }
     __syncthreads();
     if (S.result >= 0) break;
@@ -395,6 +529,7 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
   for (int64_t pos = tid; pos < M; pos += nth) {
     A.dec[pos] = UNDEC;
     A.dround[pos] = -1;
+    A.blocker[pos] = -1;
   }
   grid.sync();
   for (int64_t pos = tid; pos < M; pos += nth) {
@@ -424,6 +559,13 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
     // ---- phase D: local decisions of ready candidates
     for (int64_t pos = tid; pos < M; pos += nth) {
       if (__ldcg(A.dec + pos) != UNDEC) continue;
+      {
+        const int32_t bl = A.blocker[pos];
+        if (bl >= 0) {
+          const uint8_t db = __ldcg(A.dec + bl);
+          if (db == UNDEC || db == DEFER) continue;  // BFS would hit the same pending site
+        }
+      }
       const uint32_t p = A.order[pos];
       const int64_t f = A.px[p];
       const int32_t a = A.pown[p], b = A.pcomp[p];
@@ -451,9 +593,16 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
           if (k == 0) {
             d = REJ;  // a \ {x} would keep only the other components: != 1
           } else if (k != 1) {
-            int e = atomicAdd(ctl + C_BFS, 1);
-            A.bfs_list[e] = (int32_t)pos;
-            continue;
+            const int wv = lat.ndim == 2 ? window_pieces_2d(v, lat, y, x, a)
+                                         : window_pieces_3d(v, lat, z, y, x, a);
+            if (wv == -2) continue;  // a window site is still pending
+            if (wv == 2) {
+              d = REJ;
+            } else if (wv == 0) {
+              int e = atomicAdd(ctl + C_BFS, 1);
+              A.bfs_list[e] = (int32_t)pos;
+              continue;
+            }
           }
         }
       }
@@ -470,7 +619,12 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
         int r = block_bfs(A, S, pos);
         if (threadIdx.x == 0) {
           atomicAdd(ctl + C_BFSRUNS, 1);
-          if (r == 0) atomicAdd(ctl + C_BLOCKED, 1);
+          if (r == 0) {
+            atomicAdd(ctl + C_BLOCKED, 1);
+            A.blocker[pos] = S.blocker;
+          }
+          atomicAdd(ctl + C_LEVELS, S.levels);
+          atomicMax(ctl + C_MAXLEV, S.levels);
           if (r == 3) {
             A.dec[pos] = DEFER;
             atomicAdd(ctl + C_DEFER, 1);
@@ -575,17 +729,37 @@ __device__ __forceinline__ int delta_internal_view(const ParArgs &A, const View 
   return d;
 }
 
-// PS ledger terms: the exact increment of each kept move in the view V_i,
-// with the own-label fields at the ball sites recomputed from that view.
-__global__ void k_ps_dtot(const ParArgs A, const int64_t *__restrict__ acc,
-                          const int64_t *__restrict__ moves, const double *__restrict__ I,
-                          const Off *__restrict__ ball, int nball, int poisson, double lam,
-                          double *__restrict__ dtot) {
+// PS ledger terms: the exact increment of each kept move in its view V_i
+// (energy.py:337-372).  The own-label ball fields "as of position i" are the
+// iteration-start fields Cown/Sown plus the corrections of the sites flipped
+// earlier in this iteration within 2R of x, which one warp gathers into a
+// short shared-memory list; a ball site that itself flipped earlier is
+// recounted directly.  Exact for integer-valued (Poisson) data.
+static constexpr int kFlipCap = 256;
+struct FlipList {
+  int8_t dz[kFlipCap], dy[kFlipCap], dx[kFlipCap];
+  int32_t oldl[kFlipCap], newl[kFlipCap];
+  double val[kFlipCap];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t *__restrict__ acc,
+                                                 const int64_t *__restrict__ moves,
+                                                 const double *__restrict__ I,
+                                                 const int32_t *__restrict__ Cown,
+                                                 const double *__restrict__ Sown,
+                                                 const Off *__restrict__ ball, int nball, int R,
+                                                 int poisson, double lam,
+                                                 double *__restrict__ dtot) {
+  __shared__ FlipList fls[8];
   const int64_t n = *moves;
   const int lane = threadIdx.x & 31;
+  FlipList &F = fls[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const Lat &lat = A.lat;
+  const int R2 = R * R, W = 4 * R + 1;
+  const int wz_lo = lat.ndim == 3 ? -2 * R : 0, wz_n = lat.ndim == 3 ? W : 1;
   for (int64_t k = warp; k < n; k += nwarps) {
     const int64_t f = acc[3 * k];
     const int32_t a = (int32_t)acc[3 * k + 1], b = (int32_t)acc[3 * k + 2];
@@ -594,173 +768,270 @@ __global__ void k_ps_dtot(const ParArgs A, const int64_t *__restrict__ acc,
     int64_t z, y, x;
     lat.coord(f, z, y, x);
     const double vx = I[f];
-    // own-label fields at x (label a) and competitor count/sum at x
-    // lanes take ball offsets; each computes its own site's term
-    double ta = 0.0, tb = 0.0;  // per-lane terms are summed in offset order below
+    // 1. sites flipped before pos within the (4R+1)^d window around x
+    if (lane == 0) F.n = 0;
+    __syncwarp();
+    const int nwin = wz_n * W * W;
+    for (int base = 0; base < nwin; base += 32) {
+      const int q = base + lane;
+      bool hit = false;
+      int ddz = 0, ddy = 0, ddx = 0;
+      int64_t g = 0;
+      if (q < nwin) {
+        ddz = wz_lo + q / (W * W);
+        ddy = (q / W) % W - 2 * R;
+        ddx = q % W - 2 * R;
+        const int64_t zz = z + ddz, yy = y + ddy, xx = x + ddx;
+        if (lat.inb(zz, yy, xx)) {
+          g = lat.flat(zz, yy, xx);
+          hit = ld(A.w + g) < pos;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const int slot = F.n + __popc(m & ((1u << lane) - 1));
+        if (slot < kFlipCap) {
+          F.dz[slot] = (int8_t)ddz;
+          F.dy[slot] = (int8_t)ddy;
+          F.dx[slot] = (int8_t)ddx;
+          F.oldl[slot] = __ldg(A.L + g);
+          F.newl[slot] = ld(A.newlab + g);
+          F.val[slot] = I[g];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) F.n += __popc(m);
+      __syncwarp();
+    }
+    const int nf = F.n;
+    const bool list_ok = nf <= kFlipCap;
+    // own-label count/sum of the label at (dz,dy,dx) relative to x, at pos
+    auto own_field = [&](int oz, int oy, int ox, int64_t g, int32_t lg, int32_t &c, double &s) {
+      if (list_ok && !(ld(A.w + g) < pos)) {
+        c = Cown[g];
+        s = Sown[g];
+        for (int e = 0; e < nf; ++e) {
+          const int ez = F.dz[e] - oz, ey = F.dy[e] - oy, ex = F.dx[e] - ox;
+          if (ez * ez + ey * ey + ex * ex > R2) continue;
+          if (F.newl[e] == lg) {
+            c += 1;
+            s += F.val[e];
+          }
+          if (F.oldl[e] == lg) {
+            c -= 1;
+            s -= F.val[e];
+          }
+        }
+        return;
+      }
+      int64_t gz, gy, gx;
+      lat.coord(g, gz, gy, gx);
+      c = 0;
+      s = 0.0;
+      for (int q = 0; q <= nball; ++q) {
+        const Off o2 = q == 0 ? Off{0, 0, 0, 0} : ball[q - 1];
+        const int64_t z2 = gz + o2.dz, y2 = gy + o2.dy, x2 = gx + o2.dx;
+        if (!lat.inb(z2, y2, x2)) continue;
+        const int64_t h = lat.flat(z2, y2, x2);
+        if (v.lab(h) != lg) continue;
+        c += 1;
+        s += I[h];
+      }
+    };
+    // 2. per ball site terms (lanes over offsets), ordered sums, competitor ball
+    double ta = 0.0, tb = 0.0, sb = 0.0;
+    int cb = 0;
     for (int base = 0; base < nball; base += 32) {
-      int kk = base + lane;
-      double term_a = 0.0, term_b = 0.0;
+      const int kk = base + lane;
+      double term_a = 0.0, term_b = 0.0, ib = 0.0;
       int hit_a = 0, hit_b = 0;
       if (kk < nball) {
-        Off o = ball[kk];
-        int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+        const Off o = ball[kk];
+        const int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
         if (lat.inb(zz, yy, xx)) {
-          int64_t g = lat.flat(zz, yy, xx);
-          int32_t lg = v.lab(g);
+          const int64_t g = lat.flat(zz, yy, xx);
+          const int32_t lg = v.lab(g);
           if (lg == a || lg == b) {
-            // own-label ball count/sum at g in view V_pos (centre first)
-            int32_t c = 0;
-            double s = 0.0;
-            int64_t gz, gy, gx;
-            lat.coord(g, gz, gy, gx);
-            for (int q = 0; q <= nball; ++q) {
-              Off o2 = q == 0 ? Off{0, 0, 0, 0} : ball[q - 1];
-              int64_t z2 = gz + o2.dz, y2 = gy + o2.dy, x2 = gx + o2.dx;
-              if (!lat.inb(z2, y2, x2)) continue;
-              int64_t h = lat.flat(z2, y2, x2);
-              if (v.lab(h) != lg) continue;
-              c += 1;
-              s += I[h];
-            }
-            double cy = (double)c, iy = I[g];
+            int32_t c;
+            double s;
+            own_field(o.dz, o.dy, o.dx, g, lg, c, s);
+            const double cy = (double)c, iy = I[g];
             if (lg == a) {
               term_a = rho(iy, (s - vx) / (cy - 1.0), poisson) - rho(iy, s / cy, poisson);
               hit_a = 1;
             } else {
               term_b = rho(iy, (s + vx) / (cy + 1.0), poisson) - rho(iy, s / cy, poisson);
               hit_b = 1;
+              ib = iy;
             }
           }
         }
       }
-      // ordered accumulation (offset order) replayed by every lane
-      for (int j = 0; j < 32; ++j) {
-        if (base + j >= nball) break;
-        int ha = __shfl_sync(0xffffffffu, hit_a, j);
-        double da = __shfl_sync(0xffffffffu, term_a, j);
+      const int m = (nball - base) < 32 ? nball - base : 32;
+      for (int j = 0; j < m; ++j) {
+        const int ha = __shfl_sync(0xffffffffu, hit_a, j);
+        const double da = __shfl_sync(0xffffffffu, term_a, j);
         if (ha) ta += da;
       }
-      for (int j = 0; j < 32; ++j) {
-        if (base + j >= nball) break;
-        int hb = __shfl_sync(0xffffffffu, hit_b, j);
-        double db = __shfl_sync(0xffffffffu, term_b, j);
-        if (hb) tb += db;
-      }
-    }
-    // competitor count/sum at x and own fields at x, in view V_pos
-    if (lane == 0) {
-      int32_t cb = 0, ca = 0;
-      double sb = 0.0, sa = 0.0;
-      for (int q = 0; q <= nball; ++q) {
-        Off o2 = q == 0 ? Off{0, 0, 0, 0} : ball[q - 1];
-        int64_t z2 = z + o2.dz, y2 = y + o2.dy, x2 = x + o2.dx;
-        if (!lat.inb(z2, y2, x2)) continue;
-        int64_t h = lat.flat(z2, y2, x2);
-        int32_t lh = v.lab(h);
-        if (lh == a) {
-          ca += 1;
-          sa += I[h];
-        } else if (lh == b) {
+      for (int j = 0; j < m; ++j) {
+        const int hb = __shfl_sync(0xffffffffu, hit_b, j);
+        const double db = __shfl_sync(0xffffffffu, term_b, j);
+        const double vb = __shfl_sync(0xffffffffu, ib, j);
+        if (hb) {
+          tb += db;
           cb += 1;
-          sb += I[h];
+          sb += vb;
         }
       }
+    }
+    // 3. centre terms: own field of a at x, competitor count/sum at x
+    if (lane == 0) {
+      int32_t ca;
+      double sa;
+      own_field(0, 0, 0, f, a, ca, sa);
       double d = 0.0 + ta;
       d = d + tb;
       d += rho(vx, (sb + vx) / ((double)cb + 1.0), poisson);
       d -= rho(vx, sa / (double)ca, poisson);
-      int di = delta_internal_view(A, v, z, y, x, a, b);
+      const int di = delta_internal_view(A, v, z, y, x, a, b);
       dtot[k] = d + lam * (double)di;
+    }
+    __syncwarp();
+  }
+}
+
+// Region statistics and ledger in acceptance order (grid.py:171-181,
+// optimizer.py:197).  The fp64 chains are ordered per label only, so each
+// label replays its own events (remove/add in acceptance order) in one warp;
+// every lane keeps the pre-event statistics of its event, which gives each
+// move the exact statistics the sequential loop would see.  The PC
+// increments are then evaluated in parallel and summed into the ledger in
+// acceptance order by one warp.
+__global__ void k_events(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                         int64_t cap, int32_t nl, uint32_t *__restrict__ key,
+                         uint32_t *__restrict__ val) {
+  const int64_t n = *moves;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += stride) {
+    if (k < n) {
+      key[2 * k] = (uint32_t)acc[3 * k + 1];
+      val[2 * k] = (uint32_t)(k << 1);
+      key[2 * k + 1] = (uint32_t)acc[3 * k + 2];
+      val[2 * k + 1] = (uint32_t)((k << 1) | 1);
+    } else {
+      key[2 * k] = key[2 * k + 1] = (uint32_t)nl;
+      val[2 * k] = val[2 * k + 1] = 0xffffffffu;
     }
   }
 }
 
-// Sequential region statistics and ledger in acceptance order (grid.py:171-181,
-// optimizer.py:197).  One warp: lanes prefetch 32 moves, lane 0 replays the
-// fp64 chains in order and snapshots the pre-move statistics; the PC
-// increments of the 32 moves are then evaluated in parallel and added to the
-// ledger in order.  Per-label state lives in shared memory.
-__global__ void k_chain(const ParArgs A, const int64_t *__restrict__ acc,
-                        const int64_t *__restrict__ moves, const double *__restrict__ I,
-                        double *__restrict__ tot, double *__restrict__ tsq,
-                        const double *__restrict__ dtot_ps, int region_ps, int poisson,
-                        double lam, double *__restrict__ energy, int32_t *__restrict__ ncomp) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  const int32_t nl = A.nl;
-  int64_t *scnt = reinterpret_cast<int64_t *>(sm);
-  double *stot = reinterpret_cast<double *>(scnt + nl);
-  double *stsq = stot + nl;
-  __shared__ double snap[32][6];
-  const int lane = threadIdx.x;
-  for (int l = lane; l < nl; l += 32) {
-    scnt[l] = A.cnt0[l];
-    stot[l] = tot[l];
-    stsq[l] = tsq[l];
+__global__ void k_label_bounds(const uint32_t *__restrict__ key, int64_t n, int32_t nl,
+                               int64_t *__restrict__ start, int64_t *__restrict__ end) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t k = key[i];
+    if (k >= (uint32_t)nl) continue;
+    if (i == 0 || key[i - 1] != k) start[k] = i;
+    if (i == n - 1 || key[i + 1] != k) end[k] = i + 1;
   }
-  __syncwarp();
+}
+
+__global__ void k_event_vals(const int64_t *__restrict__ acc, const uint32_t *__restrict__ evval,
+                             const uint32_t *__restrict__ evkey, int64_t n, int32_t nl,
+                             const double *__restrict__ I, double *__restrict__ evv) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    evv[i] = evkey[i] < (uint32_t)nl ? I[acc[3 * (evval[i] >> 1)]] : 0.0;
+}
+
+// blockIdx.x = 3 * label + which: 0 count, 1 total, 2 total_sq.  Each block
+// replays its label's events exactly (OrderedSum) and records, per event, the
+// statistic before the event into snap[6 k + 3 side + which].
+__global__ void __launch_bounds__(512) k_label_chain(
+    const ParArgs A, const uint32_t *__restrict__ evval, const double *__restrict__ evv,
+    const int64_t *__restrict__ start, const int64_t *__restrict__ end, double *__restrict__ tot,
+    double *__restrict__ tsq, double *__restrict__ snap, int32_t *__restrict__ ncomp) {
+  typedef OrderedSum<512> OS;
+  __shared__ typename OS::Temp T;
+  const int64_t l = blockIdx.x / 3;
+  const int which = blockIdx.x % 3;
+  const int64_t s0 = start[l], n = end[l] - s0;
+  if (which == 0) {
+    typedef cub::BlockScan<long long, 512> Scan;
+    __shared__ typename Scan::TempStorage sc;
+    __shared__ long long carry;
+    if (threadIdx.x == 0) carry = A.cnt0[l];
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += 512) {
+      const int64_t i = base + threadIdx.x;
+      long long d = 0;
+      uint32_t ev = 0;
+      if (i < n) {
+        ev = evval[s0 + i];
+        d = (ev & 1u) ? 1 : -1;
+      }
+      long long excl, agg;
+      Scan(sc).ExclusiveSum(d, excl, agg);
+      const long long c0 = carry;
+      if (i < n) snap[6 * (int64_t)(ev >> 1) + 3 * (ev & 1u)] = (double)(c0 + excl);
+      __syncthreads();
+      if (threadIdx.x == 0) carry = c0 + agg;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      A.cnt[l] = carry;
+      if (l > 0 && carry == 0) ncomp[l] = 0;
+    }
+    return;
+  }
+  double *dst = which == 1 ? tot : tsq;
+  const double init = dst[l];
+  auto val = [&](long long i) -> double {
+    const uint32_t ev = evval[s0 + i];
+    const double v = evv[s0 + i];
+    const double w = which == 1 ? v : v * v;
+    return (ev & 1u) ? w : -w;
+  };
+  auto pre = [&](long long i, double before) {
+    const uint32_t ev = evval[s0 + i];
+    snap[6 * (int64_t)(ev >> 1) + 3 * (ev & 1u) + which] = before;
+  };
+  const double fin = OS::run(T, init, n, val, pre);
+  if (threadIdx.x == 0) dst[l] = fin;
+}
+
+__global__ void k_pc_dtot(const ParArgs A, const int64_t *__restrict__ acc,
+                          const int64_t *__restrict__ moves, const double *__restrict__ I,
+                          const double *__restrict__ snap, int poisson, double lam,
+                          double *__restrict__ dtot) {
   const int64_t n = *moves;
-  double e = *energy;
-  for (int64_t base = 0; base < n; base += 32) {
-    const int64_t k = base + lane;
-    int64_t f = 0;
-    int32_t a = 0, b = 0;
-    double v = 0.0, dps = 0.0;
-    if (k < n) {
-      f = acc[3 * k];
-      a = (int32_t)acc[3 * k + 1];
-      b = (int32_t)acc[3 * k + 2];
-      v = I[f];
-      if (region_ps) dps = dtot_ps[k];
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const double v = I[acc[3 * k]];
+    const double *s = snap + 6 * k;
+    double dext;
+    if (!poisson) {
+      double before = g_gauss(s[0], s[1], s[2]) + g_gauss(s[3], s[4], s[5]);
+      double after = g_gauss(s[0] - 1.0, s[1] - v, s[2] - v * v) +
+                     g_gauss(s[3] + 1.0, s[4] + v, s[5] + v * v);
+      dext = after - before;
+    } else {
+      double before = g_poisson(s[0], s[1]) + g_poisson(s[3], s[4]);
+      double after = g_poisson(s[0] - 1.0, s[1] - v) + g_poisson(s[3] + 1.0, s[4] + v);
+      dext = after - before;
     }
-    const int m = (n - base) < 32 ? (int)(n - base) : 32;
-    for (int j = 0; j < m; ++j) {
-      const int32_t aj = __shfl_sync(0xffffffffu, a, j);
-      const int32_t bj = __shfl_sync(0xffffffffu, b, j);
-      const double vj = __shfl_sync(0xffffffffu, v, j);
-      if (lane == 0) {
-        snap[j][0] = (double)scnt[aj];
-        snap[j][1] = stot[aj];
-        snap[j][2] = stsq[aj];
-        snap[j][3] = (double)scnt[bj];
-        snap[j][4] = stot[bj];
-        snap[j][5] = stsq[bj];
-        scnt[aj] -= 1;
-        stot[aj] -= vj;
-        stsq[aj] -= vj * vj;
-        scnt[bj] += 1;
-        stot[bj] += vj;
-        stsq[bj] += vj * vj;
-      }
-    }
-    __syncwarp();
-    double d = dps;
-    if (!region_ps && k < n) {
-      const double na = snap[lane][0], nb = snap[lane][3];
-      // delta_pc of the pre-move statistics (energy.py:308-324) + lam * dE_int
-      double dext;
-      if (!poisson) {
-        double before = g_gauss(na, snap[lane][1], snap[lane][2]) +
-                        g_gauss(nb, snap[lane][4], snap[lane][5]);
-        double after = g_gauss(na - 1.0, snap[lane][1] - v, snap[lane][2] - v * v) +
-                       g_gauss(nb + 1.0, snap[lane][4] + v, snap[lane][5] + v * v);
-        dext = after - before;
-      } else {
-        double before = g_poisson(na, snap[lane][1]) + g_poisson(nb, snap[lane][4]);
-        double after = g_poisson(na - 1.0, snap[lane][1] - v) + g_poisson(nb + 1.0, snap[lane][4] + v);
-        dext = after - before;
-      }
-      d = dext + lam * (double)A.dint_acc[k];
-    }
-    for (int j = 0; j < m; ++j) e += __shfl_sync(0xffffffffu, d, j);
-    __syncwarp();
+    dtot[k] = dext + lam * (double)A.dint_acc[k];
   }
-  for (int l = lane; l < nl; l += 32) {
-    A.cnt[l] = scnt[l];
-    tot[l] = stot[l];
-    tsq[l] = stsq[l];
-    if (l > 0 && scnt[l] == 0) ncomp[l] = 0;
-  }
-  if (lane == 0) *energy = e;
+}
+
+__global__ void __launch_bounds__(1024) k_ledger(const double *__restrict__ dtot,
+                                                 const int64_t *__restrict__ moves,
+                                                 double *__restrict__ energy) {
+  typedef OrderedSum<1024> OS;
+  __shared__ typename OS::Temp T;
+  const double fin = OS::run(T, *energy, (long long)*moves,
+                             [&](long long i) { return dtot[i]; }, [](long long, double) {});
+  if (threadIdx.x == 0) *energy = fin;
 }
 
 __global__ void k_final_labels(const ParArgs A, const uint32_t *__restrict__ slot, int64_t budget,
@@ -865,16 +1136,43 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
   int nl = 6;
   if (X.region_ps) {
-    k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.ball, X.nball, X.poisson, X.lam,
-                                      X.dtot);
+    k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
+                                      X.radius, X.poisson, X.lam, X.dtot);
     ++nl;
   }
-  size_t csm = (size_t)A.nl * 24;
-  if (csm > 200 * 1024) return fail(RCB_ERR_VALUE, "too many labels for the ledger chain");
-  if (csm > 48 * 1024)
-    RCB_CUDA(cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-  k_chain<<<1, 32, csm, s>>>(A, X.acc, X.moves, X.I, X.tot, X.tsq, X.dtot, X.region_ps, X.poisson,
-                             X.lam, X.energy, X.ncomp);
+  // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger
+  {
+    const int64_t cap = N;
+    RCB_TRY(X.evkey->reserve(2 * cap, s));
+    RCB_TRY(X.evkey2->reserve(2 * cap, s));
+    RCB_TRY(X.evval->reserve(2 * cap, s));
+    RCB_TRY(X.evval2->reserve(2 * cap, s));
+    RCB_TRY(X.bounds->reserve(2 * (size_t)A.nl, s));
+    RCB_TRY(X.snap->reserve(6 * cap, s));
+    k_events<<<grid_for(cap, 256), 256, 0, s>>>(X.acc, X.moves, cap, A.nl, X.evkey->p, X.evval->p);
+    int end_bit = 1;
+    while (end_bit < 32 && ((int64_t)1 << end_bit) <= A.nl) ++end_bit;
+    size_t b2 = 0;
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, X.evkey->p, X.evkey2->p, X.evval->p,
+                                             X.evval2->p, 2 * cap, 0, end_bit, s));
+    RCB_TRY(X.tmp->reserve(b2, s));
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b2, X.evkey->p, X.evkey2->p, X.evval->p,
+                                             X.evval2->p, 2 * cap, 0, end_bit, s));
+    int64_t *st = X.bounds->p, *en = X.bounds->p + A.nl;
+    RCB_CUDA(cudaMemsetAsync(st, 0, sizeof(int64_t) * A.nl, s));
+    RCB_CUDA(cudaMemsetAsync(en, 0, sizeof(int64_t) * A.nl, s));
+    k_label_bounds<<<grid_for(2 * cap, 256), 256, 0, s>>>(X.evkey2->p, 2 * cap, A.nl, st, en);
+    RCB_TRY(X.evv->reserve(2 * cap, s));
+    k_event_vals<<<grid_for(2 * cap, 256), 256, 0, s>>>(X.acc, X.evval2->p, X.evkey2->p, 2 * cap,
+                                                        A.nl, X.I, X.evv->p);
+    k_label_chain<<<3 * A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq,
+                                           X.snap->p, X.ncomp);
+    if (!X.region_ps)
+      k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
+                                                   X.lam, X.dtot);
+    k_ledger<<<1, 1024, 0, s>>>(X.dtot, X.moves, X.energy);
+    nl += 12;
+  }
   k_final_labels<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.Lmut);
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);

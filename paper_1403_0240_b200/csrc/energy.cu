@@ -4,6 +4,7 @@
 
 #include "dev.cuh"
 #include "kernels.h"
+#include "ordered_sum.cuh"
 
 namespace rcb {
 
@@ -130,29 +131,41 @@ __global__ void k_seg_bounds(const uint32_t *__restrict__ keys, int64_t n,
   }
 }
 
-__global__ void k_seq_sums(const uint32_t *__restrict__ sites, const double *__restrict__ I,
-                           const int64_t *__restrict__ start, const int64_t *__restrict__ end,
-                           int32_t nl, int64_t *__restrict__ cnt, double *__restrict__ tot,
-                           double *__restrict__ tsq) {
-  int lane = threadIdx.x & 31;
-  int32_t l = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (l >= nl) return;
-  int64_t s = start[l], e = end[l];
-  double t = 0.0, q = 0.0;
-  for (int64_t base = s; base < e; base += 32) {
-    int64_t i = base + lane;
-    double v = i < e ? __ldg(&I[sites[i]]) : 0.0;
-    int m = (e - base) < 32 ? (int)(e - base) : 32;
-    for (int j = 0; j < m; ++j) {
-      double w = __shfl_sync(0xffffffffu, v, j);
-      t += w;
-      q += w * w;
+__global__ void k_gather_vals(const uint32_t *__restrict__ sites, const double *__restrict__ I,
+                              int64_t n, double *__restrict__ out) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __ldg(&I[sites[i]]);
+}
+
+// Per label (blockIdx.x = 2 * label + which): the raster-order fp64 sum of the
+// label's values (which = 0) or of their squares (which = 1), replayed exactly
+// by OrderedSum; the count is the segment length.
+__global__ void __launch_bounds__(512) k_seq_sums(const double *__restrict__ vals,
+                                                  const int64_t *__restrict__ start,
+                                                  const int64_t *__restrict__ end, int32_t nl,
+                                                  int64_t *__restrict__ cnt,
+                                                  double *__restrict__ tot,
+                                                  double *__restrict__ tsq) {
+  typedef OrderedSum<512> OS;
+  __shared__ typename OS::Temp T;
+  const int32_t l = blockIdx.x >> 1;
+  const int which = blockIdx.x & 1;
+  const int64_t s = start[l], n = end[l] - s;
+  const double fin = OS::run(
+      T, 0.0, (long long)n,
+      [&](long long i) {
+        const double v = vals[s + i];
+        return which ? v * v : v;
+      },
+      [](long long, double) {});
+  if (threadIdx.x == 0) {
+    if (which) {
+      tsq[l] = fin;
+    } else {
+      tot[l] = fin;
+      cnt[l] = n;
     }
-  }
-  if (lane == 0) {
-    cnt[l] = e - s;
-    tot[l] = t;
-    tsq[l] = q;
   }
 }
 
@@ -180,8 +193,9 @@ int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, 
     k_seg_bounds<<<grid_for(V, 256), 256, 0, s>>>(sc.keys.p, V, start, end);
     RCB_CUDA(cudaGetLastError());
   }
-  k_seq_sums<<<grid_for((int64_t)nl * 32, 128), 128, 0, s>>>(sc.vals.p, I, start, end, nl, cnt,
-                                                             tot, tsq);
+  RCB_TRY(sc.gathered.reserve(V, s));
+  k_gather_vals<<<grid_for(V, 256), 256, 0, s>>>(sc.vals.p, I, V, sc.gathered.p);
+  k_seq_sums<<<2 * nl, 512, 0, s>>>(sc.gathered.p, start, end, nl, cnt, tot, tsq);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

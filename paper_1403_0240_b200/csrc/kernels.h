@@ -11,7 +11,9 @@ struct StatsScratch {
   DBuf<uint32_t> keys, vals_in, vals;
   DBuf<int64_t> bounds;
   DBuf<uint8_t> tmp;
+  DBuf<double> gathered;
   void release(cudaStream_t s) {
+    gathered.release(s);
     keys.release(s);
     vals_in.release(s);
     vals.release(s);
@@ -78,6 +80,7 @@ struct ParArgs {
   uint32_t *vis, *epoch;
   uint32_t *gq[2];
   int32_t *dint_acc;
+  int32_t *blocker;
 };
 
 struct ParExtra {
@@ -91,10 +94,13 @@ struct ParExtra {
   int region_ps, poisson;
   double lam;
   const Off *ball, *ball_full;
-  int nball, nball_full;
+  int nball, nball_full, radius;
   uint8_t *dirty;
   int32_t *Cown;
   double *Sown;
+  DBuf<uint32_t> *evkey, *evkey2, *evval, *evval2;
+  DBuf<int64_t> *bounds;
+  DBuf<double> *snap, *evv;
 };
 
 // contour.cu

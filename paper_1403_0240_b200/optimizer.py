@@ -204,6 +204,14 @@ class RegionCompetition:
         _lib.check(_lib.lib.rcb_engine_timings(self._h, t, C.byref(n)))
         return list(t), n.value
 
+    def counters(self) -> dict:
+        """Acceptance diagnostics of the last iterate() (rcb_engine_counters)."""
+        out = np.zeros(10, np.int64)
+        _lib.check(_lib.lib.rcb_engine_counters(self._h, _lib.ptr(out)))
+        keys = ["rounds", "bfs_runs", "deferred", "bfs_blocked", "negative", "moves",
+                "parallel", "accept_us", "bfs_levels", "bfs_max_levels"]
+        return dict(zip(keys, out.tolist()))
+
     @property
     def stream(self) -> int:
         s = C.c_void_p()

@@ -271,3 +271,32 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
         assert np.array_equal(a[2], b[2]), (which, it)
         assert np.array_equal(a[3], b[3]), (which, it)
         assert a[1] == b[1], (which, it, a[1], b[1])
+
+
+def _adversarial_sequences():
+    rng = np.random.default_rng(77)
+    seqs = [
+        rng.normal(size=20000),                                  # sign changes, small binades
+        rng.poisson(6.0, size=30000).astype(np.float64),          # integers (exact)
+        np.concatenate([[2.0 ** 53], np.ones(3000), [3.0] * 500, [-1.0] * 700]),  # ties at u=2
+        np.concatenate([[2.0 ** 52 + 1.0], np.full(2000, 0.5), np.full(2000, 1.5)]),  # ties, u=1
+        np.cumprod(np.full(600, 1.07)) * rng.choice([-1, 1], 600),  # binade sweeps
+        np.concatenate([[-0.0, 0.0, -0.0], rng.normal(size=50), [1e300, -1e300], rng.normal(size=50)]),
+        np.tile([1e16, 1.0, -1e16, 2.0 ** -30], 2000),
+        rng.normal(size=5000) * 10.0 ** rng.integers(-20, 20, size=5000),
+    ]
+    return seqs
+
+
+def test_ordered_sum_exact_vs_sequential(P):
+    """The parallel replay of s = fl(s + v) (stats rebuild, label chains,
+    ledger) must equal numpy's sequential bincount accumulation bit for bit."""
+    for k, seq in enumerate(_adversarial_sequences()):
+        img = np.ascontiguousarray(seq, np.float64).reshape(1, -1)
+        lab = np.zeros(img.shape, np.int32)
+        lab[0, ::7] = 1  # a second interleaved label
+        t = P.StatsTable.from_labels(lab, img)
+        o = O.Stats(lab, img, 2)
+        assert np.array_equal(t.count, o.count), k
+        assert np.array_equal(t.total, o.total, equal_nan=True), (k, t.total, o.total)
+        assert np.array_equal(t.total_sq, o.total_sq, equal_nan=True), (k, t.total_sq, o.total_sq)
