@@ -294,6 +294,10 @@ def gen_runs(skip_cfg1: bool):
     s2 = scenes.cfg2_small()
     record_run("cfg2_small", s2.image, s2.labels, E("ps", "poisson", smooth_radius=4), S(6.0),
                O("sobolev", vanish_grace=5), 4, keep_labels=False)
+    # the bench workload itself (cfg2, 1024^2): first 3 iterations
+    s2f = scenes.cfg2()
+    record_run("cfg2_full", s2f.image, s2f.labels, E("ps", "poisson", smooth_radius=4), S(6.0),
+               O("sobolev", vanish_grace=5), 3, keep_labels=False)
     if not skip_cfg1:
         s1 = scenes.cfg1()
         record_run("cfg1", s1.image, s1.labels, E("pc", "gauss"), S(4.0), O("sobolev"), 50,
@@ -305,6 +309,12 @@ if __name__ == "__main__":
     ap.add_argument("--skip-cfg1", action="store_true")
     ap.add_argument("--only", default="")
     a = ap.parse_args()
+    if a.only == "cfg2_full":
+        E, S, O = rc_energy.EnergyConfig, rc_sob.SobolevParams, rc_opt.OptimizerConfig
+        s2f = scenes.cfg2()
+        record_run("cfg2_full", s2f.image, s2f.labels, E("ps", "poisson", smooth_radius=4),
+                   S(6.0), O("sobolev", vanish_grace=5), 3, keep_labels=False)
+        sys.exit(0)
     todo = a.only.split(",") if a.only else ["kernel", "sobolev", "contour", "energy",
                                              "admissible", "runs"]
     for t in todo:
