@@ -29,6 +29,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Sobolev particle-interactions/s and iterations/s; % of HBM roofline"
+# The reference's drift check is absolute (1e-6, optimizer.py:45).  On cfg2
+# |E| ~ 4.8e7 (ulp 7.5e-9) and ~3e5 ledger additions happen per 10 iterations,
+# so the reference's own ledger drifts past 1e-6 by iteration 20 (measured:
+# 1.07e-6, identical on the oracle and on the GPU).  Both arms use 1e-3.
+DRIFT_TOL = 1e-3
 
 
 def _dist():
@@ -123,7 +128,8 @@ def run_ours(args):
     sc = scene_for(rank, args.small)
     ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
     scfg = P.SobolevParams(sc.length_scale)
-    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace,
+                             drift_tolerance=DRIFT_TOL)
     eng = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
@@ -218,6 +224,7 @@ def run_ours(args):
             "data": "synthetic (scenes.cfg2: seeded ellipses, blur 1.5, Poisson peak 50)",
             "config": {"workload": "cfg2: 2-D 1024x1024 PS/Poisson R=4, Sobolev w=3 (E=6), "
                                    "bubbles 16x16 r=10, iterations continue from warm-up",
+                       "drift_tolerance": DRIFT_TOL,
                        "l2": "flushed between timed iterations (512 MB write)",
                        "parallelism": f"{ws} independent images (one per GPU)"},
             "particle_interactions_per_s": pairs / max(1e-9, phase[2] / 1e3),
@@ -255,7 +262,7 @@ def cpu_baseline(args, steps=None, budget_s=25.0):
     bounded sample of the same workload: the first iterations of cfg2."""
     from oracle import rc_oracle as O
     sc = scene_for(0, args.small)
-    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
     t0 = time.perf_counter()
     eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
                          sc.length_scale, config=cfg)
@@ -282,7 +289,7 @@ def run_reference(args):
     cap_s = 150.0
     from oracle import rc_oracle as O
     sc = scene_for(0, args.small)
-    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
     eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
                          sc.length_scale, config=cfg)
     t_all = time.perf_counter()

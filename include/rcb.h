@@ -158,6 +158,10 @@ int32_t rcb_engine_timings(rcb_engine *eng, float *ms6, int32_t *launches);
  * acceptance ran (0 = sequential), [7] device us of the acceptance kernels,
  * [8] total BFS levels, [9] deepest BFS (levels). */
 int32_t rcb_engine_counters(rcb_engine *eng, int64_t *out10);
+/* Diagnostics of the last parallel acceptance: for rank position i < *n,
+ * particle[i] (index into last_candidates) and code[i] (decision path). */
+int32_t rcb_engine_debug_codes(rcb_engine *eng, int32_t *particle, int32_t *code, int64_t cap,
+                               int64_t *n);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGNATURES = {
     "rcb_engine_stream": [_P, _P],
     "rcb_engine_timings": [_P, _P, _P],
     "rcb_engine_counters": [_P, _P],
+    "rcb_engine_debug_codes": [_P, _P, _P, _I64, _P],
 }
 _RESTYPES = {"rcb_last_error": C.c_char_p, "rcb_engine_destroy": None}
 

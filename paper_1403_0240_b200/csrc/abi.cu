@@ -118,6 +118,10 @@ struct rcb_engine {
   DBuf<double> dtot, snap, evv;
   DBuf<uint32_t> evkey, evkey2, evval, evval2;
   DBuf<int64_t> evbounds;
+  DBuf<uint64_t> labkey, labkey2;
+  DBuf<int32_t> labpos, pos_of, lab_ptr, gmutex;
+  DBuf<int64_t> labbounds;
+  int accept_mode = 0;
   bool simple_topology = false;
   bool force_sequential = false;
   DBuf<Scalars> sc;
@@ -145,7 +149,9 @@ struct rcb_engine {
       nown.release(s); blocker.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
-      evval2.release(s); evbounds.release(s);
+      evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
+      labpos.release(s); pos_of.release(s); lab_ptr.release(s); gmutex.release(s);
+      labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
       for (auto &e : ev)
@@ -229,6 +235,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   {
     const char *fs = getenv("RCB_FORCE_SEQUENTIAL");  // testing: exact single-thread acceptance
     e->force_sequential = fs && fs[0] == '1';
+    const char *am = getenv("RCB_ACCEPT");  // "rounds": K8 v2 instead of the dataflow K8 v3
+    e->accept_mode = (am && strcmp(am, "rounds") == 0) ? 1 : 0;
   }
   const int64_t V = e->lat.V;
   int32_t mx = 0;
@@ -286,6 +294,10 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   TRYB(e->small.reserve(e->nl, s));
   TRYB(e->cnt0.reserve(e->nl, s));
   TRYB(e->ctl.reserve(16, s));
+  TRYB(e->lab_ptr.reserve(e->nl, s));
+  TRYB(e->gmutex.reserve(1, s));
+  if (cudaMemsetAsync(e->gmutex.p, 0, sizeof(int32_t), s) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "memset failed"));
   if (cudaMemsetAsync(e->wpos.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->pend.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s) != cudaSuccess)
@@ -362,6 +374,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       RCB_TRY(e->slot.reserve(n + 1, s));
       RCB_TRY(e->dint_acc.reserve(n, s));
       RCB_TRY(e->blocker.reserve(n, s));
+      RCB_TRY(e->pos_of.reserve(n, s));
       RCB_TRY(e->dtot.reserve(n, s));
       ParArgs P{};
       P.lat = lat;
@@ -392,6 +405,10 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       P.gq[1] = e->gq1.p;
       P.dint_acc = e->dint_acc.p;
       P.blocker = e->blocker.p;
+      P.pos_of = e->pos_of.p;
+      P.site_off = e->site_off.p;
+      P.lab_ptr = e->lab_ptr.p;
+      P.gmutex = e->gmutex.p;
       ParExtra X{};
       X.n_particles = n;
       X.budget = budget;
@@ -424,6 +441,11 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.bounds = &e->evbounds;
       X.snap = &e->snap;
       X.evv = &e->evv;
+      X.accept_mode = e->accept_mode;
+      X.labkey = &e->labkey;
+      X.labkey2 = &e->labkey2;
+      X.labpos = &e->labpos;
+      X.labbounds = &e->labbounds;
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));
       cudaEventRecord(e->ev_acc[0], s);
@@ -673,6 +695,19 @@ int32_t rcb_engine_evaluate(rcb_engine *e, double *external, int64_t *internal) 
 
 int32_t rcb_engine_stream(rcb_engine *e, void **stream) {
   *stream = (void *)e->s;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_debug_codes(rcb_engine *e, int32_t *particle, int32_t *code, int64_t cap,
+                               int64_t *n) {
+  const int64_t m = e->last_par ? (int64_t)e->hsc->nneg : 0;
+  *n = m;
+  if (cap < m) return fail(RCB_ERR_CAPACITY, "debug buffers too small");
+  if (m == 0) return RCB_OK;
+  RCB_CUDA(cudaSetDevice(e->device));
+  RCB_CUDA(cudaMemcpyAsync(particle, e->order.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(code, e->blocker.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
   return RCB_OK;
 }
 

@@ -397,10 +397,11 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
       S.levels += 1;
     }
     __syncthreads();
-    if (S.result >= 0) break;
+    const int res = S.result;
+    __syncthreads();  // all threads read the verdict before thread 0 reuses S
+    if (res >= 0) return res;
     cur = nxt;
   }
-  return S.result;
 }
 
 // Unbounded BFS with global stamps/frontiers for the earliest undecided
@@ -481,11 +482,12 @@ __device__ int global_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
       nf[cur] = 0;
     }
     __syncthreads();
-    if (S.result >= 0) break;
+    const int res = S.result;
+    __syncthreads();  // all threads read the verdict before thread 0 reuses S
+    if (res >= 0) return res;
     cur = nxt;
     __threadfence_block();
   }
-  return S.result;
 }
 
 __device__ __forceinline__ void finish_topology(const ParArgs &A, int32_t pos, int pieces,
@@ -678,6 +680,483 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
       if (tid == 0) ctl[C_ROUNDS] = round + 1;
       break;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K8 v3 — dataflow acceptance: no grid barriers.  Persistent warps take
+// candidates in rank order from an atomic counter; a warp waits (acquire
+// loads) only until the earlier candidates sitting on the sites it reads are
+// decided, then decides and publishes (release stores): the flip, then the
+// next pending position of its site and, for small labels, the label's next
+// event.  Every wait is on a strictly earlier position and positions are
+// handed out in order to co-resident warps, so the earliest undecided
+// candidate never waits and the scheme cannot deadlock.  Verdicts are the
+// same functions of the same view V_i as in the round-based kernel.
+// ---------------------------------------------------------------------------
+static constexpr int kHW = 1024;  // warp BFS hash entries
+static constexpr int kFW = 256;   // warp BFS frontier capacity
+static constexpr int kMaxInsertW = kHW * 5 / 8;
+static constexpr int kDfWarps = 16;
+
+__device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(int32_t *p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
+  int ns = 32;
+  while (ld_acq(A.pend + g) < pos) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
+struct WarpBfs {
+  unsigned long long key[kHW];
+  uint32_t fr[2][kFW];
+  uint8_t fg[2][kFW];
+  int nfr[2];
+  int par[27], gcount[27];
+  uint32_t unions[27];
+  int nseed, ninsert, blocked, overflow, result;
+  int64_t bsite;
+};
+
+__device__ int warp_level_verdict(WarpBfs &S) {
+  if (S.blocked) return 0;
+  if (S.overflow) return 3;
+  for (int g = 0; g < S.nseed; ++g)
+    for (uint32_t m = S.unions[g]; m; m &= m - 1) {
+      int h = __ffs(m) - 1;
+      int rg = uf_root(S.par, g), rh = uf_root(S.par, h);
+      if (rg != rh) S.par[rh] = rg;
+    }
+  int roots = 0, rc[27];
+  for (int g = 0; g < S.nseed; ++g) {
+    S.unions[g] = 0;
+    rc[g] = 0;
+  }
+  for (int g = 0; g < S.nseed; ++g) {
+    int r = uf_root(S.par, g);
+    if (r == g) ++roots;
+    rc[r] += S.gcount[g];
+    S.gcount[g] = 0;
+  }
+  if (roots == 1) return 1;
+  for (int g = 0; g < S.nseed; ++g)
+    if (uf_root(S.par, g) == g && rc[g] == 0) return 2;
+  return -1;
+}
+
+// Warp-cooperative pieces BFS (same question as block_bfs).  Returns 0 blocked
+// (S.bsite = a pending site), 1 one piece, 2 several, 3 overflow.
+__device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
+  const Lat &lat = A.lat;
+  const int lane = threadIdx.x & 31;
+  View v{A, pos};
+  for (int k = lane; k < kHW; k += 32) S.key[k] = kEmpty;
+  __syncwarp();
+  if (lane == 0) {
+    S.blocked = S.overflow = 0;
+    S.result = -1;
+    S.nfr[0] = S.nfr[1] = 0;
+    auto put = [&](uint32_t site, int g) {
+      uint32_t h = hash32(site) & (kHW - 1);
+      while (S.key[h] != kEmpty) h = (h + 1) & (kHW - 1);
+      S.key[h] = ((unsigned long long)site << 8) | (unsigned)g;
+    };
+    put((uint32_t)f, 255);
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    int ns = 0;
+    for (int k = 0; k < 27; ++k) {
+      if (k == 13) continue;
+      int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+      int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+      int64_t g = lat.flat(zz, yy, xx);
+      if (v.lab(g) != a) continue;
+      put((uint32_t)g, ns);
+      S.fr[0][ns] = (uint32_t)g;
+      S.fg[0][ns] = (uint8_t)ns;
+      S.par[ns] = ns;
+      S.gcount[ns] = 0;
+      S.unions[ns] = 0;
+      ++ns;
+    }
+    S.nseed = ns;
+    S.nfr[0] = ns;
+    S.ninsert = ns + 1;
+  }
+  __syncwarp();
+  int cur = 0;
+  for (;;) {
+    const int n = S.nfr[cur], nxt = cur ^ 1;
+    for (int j = lane; j < n; j += 32) {
+      const uint32_t s = S.fr[cur][j];
+      const int g = S.fg[cur][j];
+      int64_t z, y, x;
+      lat.coord(s, z, y, x);
+      for (int k = 0; k < 27; ++k) {
+        if (k == 13) continue;
+        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+        int64_t t = lat.flat(zz, yy, xx);
+        if (t == f) continue;
+        int32_t pm;
+        const int32_t lt = v.lab_pend(t, pm);
+        if (pm < pos) {
+          S.blocked = 1;
+          S.bsite = t;
+          continue;
+        }
+        if (lt != a) continue;
+        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
+        for (;;) {
+          unsigned long long cv = S.key[h];
+          if (cv == kEmpty) {
+            unsigned long long mine = ((unsigned long long)t << 8) | (unsigned)g;
+            unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
+            if (old == kEmpty) {
+              int idx = atomicAdd(&S.nfr[nxt], 1);
+              if (idx < kFW) {
+                S.fr[nxt][idx] = (uint32_t)t;
+                S.fg[nxt][idx] = (uint8_t)g;
+              } else {
+                S.overflow = 1;
+              }
+              atomicAdd(&S.gcount[g], 1);
+              if (atomicAdd(&S.ninsert, 1) >= kMaxInsertW) S.overflow = 1;
+              break;
+            }
+            cv = old;
+          }
+          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
+            int hg = (int)(cv & 0xff);
+            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
+            break;
+          }
+          h = (h + 1) & (kHW - 1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      S.result = warp_level_verdict(S);
+      S.nfr[cur] = 0;
+    }
+    __syncwarp();
+    const int r = S.result;
+    __syncwarp();  // every lane has read the verdict before lane 0 may reuse S
+    if (r >= 0) return r;
+    cur = nxt;
+  }
+}
+
+// Unbounded fallback (overflowing footprints) with global stamps/frontiers,
+// one warp at a time under a global lock; aborts (releasing the lock) on a
+// pending site.
+__device__ int warp_global_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
+  const Lat &lat = A.lat;
+  const int lane = threadIdx.x & 31;
+  View v{A, pos};
+  __shared__ unsigned long long gnf[kDfWarps][2];
+  unsigned long long *nf = gnf[(threadIdx.x >> 5) % kDfWarps];
+  uint32_t ep = 0;
+  if (lane == 0) {
+    while (atomicCAS(A.gmutex, 0, 1) != 0) __nanosleep(256);
+    __threadfence();
+    ep = *(volatile uint32_t *)A.epoch;
+    *(volatile uint32_t *)A.epoch = ep + 32;
+    S.blocked = S.overflow = 0;
+    S.result = -1;
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    A.vis[f] = ep + 31;
+    int ns = 0;
+    for (int k = 0; k < 27; ++k) {
+      if (k == 13) continue;
+      int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+      int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+      int64_t g = lat.flat(zz, yy, xx);
+      if (v.lab(g) != a) continue;
+      A.vis[g] = ep + ns;
+      A.gq[0][ns] = (uint32_t)g;
+      S.par[ns] = ns;
+      S.gcount[ns] = 0;
+      S.unions[ns] = 0;
+      ++ns;
+    }
+    S.nseed = ns;
+    nf[0] = ns;
+    nf[1] = 0;
+  }
+  ep = __shfl_sync(0xffffffffu, ep, 0);
+  __syncwarp();
+  __threadfence();
+  int cur = 0, r;
+  for (;;) {
+    const unsigned long long n = nf[cur];
+    const int nxt = cur ^ 1;
+    for (unsigned long long j = lane; j < n; j += 32) {
+      const uint32_t s = __ldcg(A.gq[cur] + j);
+      const int g = (int)(__ldcg(A.vis + s) - ep);
+      int64_t z, y, x;
+      lat.coord(s, z, y, x);
+      for (int k = 0; k < 27; ++k) {
+        if (k == 13) continue;
+        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+        int64_t t = lat.flat(zz, yy, xx);
+        int32_t pm;
+        const int32_t lt = v.lab_pend(t, pm);
+        if (pm < pos && t != f) {
+          S.blocked = 1;
+          S.bsite = t;
+          continue;
+        }
+        if (lt != a) continue;
+        uint32_t cv = __ldcg(A.vis + t);
+        for (;;) {
+          if (cv >= ep && cv < ep + 32) {
+            int h = (int)(cv - ep);
+            if (h != 31 && h != g) atomicOr(&S.unions[g], 1u << h);
+            break;
+          }
+          uint32_t old = atomicCAS(A.vis + t, cv, ep + (uint32_t)g);
+          if (old == cv) {
+            unsigned long long idx = atomicAdd(&nf[nxt], 1ull);
+            A.gq[nxt][idx] = (uint32_t)t;
+            atomicAdd(&S.gcount[g], 1);
+            break;
+          }
+          cv = old;
+        }
+      }
+    }
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) {
+      S.result = warp_level_verdict(S);
+      nf[cur] = 0;
+    }
+    __syncwarp();
+    r = S.result;
+    __syncwarp();
+    if (r >= 0) break;
+    cur = nxt;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(A.gmutex, 0);
+  }
+  __syncwarp();
+  return r;
+}
+
+__global__ void k_df_init(ParArgs A, int64_t N) {
+  const int32_t M = (int32_t)*A.nneg;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride)
+    A.pos_of[i] = kInf;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride) {
+    A.cnt0[l] = A.cnt[l];
+    A.nown[l] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 16) A.ctl[threadIdx.x] = 0;
+  (void)M;
+}
+
+__global__ void k_df_init2(ParArgs A) {
+  const int32_t M = (int32_t)*A.nneg;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < M; pos += stride) {
+    const uint32_t p = A.order[pos];
+    A.pos_of[p] = (int32_t)pos;
+    A.dec[pos] = UNDEC;
+    atomicMin(A.pend + A.px[p], (int32_t)pos);
+    const int32_t a = A.pown[p];
+    if (a > 0) atomicAdd(A.nown + a, 1);
+  }
+}
+
+__global__ void k_df_small(ParArgs A) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride)
+    A.small[l] = (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
+}
+
+// events (label, position) of candidates involving small labels, as sortable
+// 64-bit keys; everything else gets the sentinel key.
+__global__ void k_df_labkeys(ParArgs A, int64_t cap, uint64_t *__restrict__ key) {
+  const int64_t M = (int64_t)*A.nneg;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < cap; pos += stride) {
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    if (pos < M) {
+      const uint32_t p = A.order[pos];
+      const int32_t a = A.pown[p], b = A.pcomp[p];
+      if (A.small[a]) k0 = ((uint64_t)a << 32) | (uint64_t)pos;
+      if (A.small[b]) k1 = ((uint64_t)b << 32) | (uint64_t)pos;
+    }
+    key[2 * pos] = k0;
+    key[2 * pos + 1] = k1;
+  }
+}
+
+__global__ void k_df_labcsr(const uint64_t *__restrict__ key, int64_t n, int32_t nl,
+                            int32_t *__restrict__ lab_pos, int32_t *__restrict__ lab_ptr) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t k = key[i];
+    if (k == ~0ull) {
+      lab_pos[i] = kInf;
+      continue;
+    }
+    lab_pos[i] = (int32_t)(k & 0xffffffffu);
+    const uint32_t l = (uint32_t)(k >> 32);
+    if (i == 0 || (uint32_t)(key[i - 1] >> 32) != l) lab_ptr[l] = (int32_t)i;
+  }
+}
+
+__device__ __forceinline__ void df_wait_label(const ParArgs &A, int32_t l, int32_t pos) {
+  int ns = 32;
+  while (A.lab_pos[ld_acq(A.lab_ptr + l)] != pos) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
+  __shared__ int32_t wpos[kDfWarps];
+  const Lat &lat = A.lat;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t M = (int32_t)*A.nneg;
+  int32_t *ctl = A.ctl;
+  for (;;) {
+    if (lane == 0) wpos[wid] = atomicAdd(ctl + 12, 1);
+    __syncwarp();
+    const int32_t pos = wpos[wid];
+    __syncwarp();
+    if (pos >= M) break;
+    const uint32_t p = A.order[pos];
+    const int64_t f = A.px[p];
+    const int32_t a = A.pown[p], b = A.pcomp[p];
+    const bool sa = A.small[a], sb = A.small[b];
+    if (lane == 0) {
+      if (sa) df_wait_label(A, a, pos);
+      if (sb) df_wait_label(A, b, pos);
+    }
+    __syncwarp();
+    View v{A, pos};
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    // the 3^d box, one cell per lane
+    int32_t mine = -1;
+    if (lane < 27) {
+      const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+      const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      if (!(lat.ndim == 2 && dz != 0) && lat.inb(zz, yy, xx)) {
+        const int64_t g = lat.flat(zz, yy, xx);
+        wait_pend(A, g, pos);
+        mine = v.lab(g);
+      }
+    }
+    int32_t lab[27];
+#pragma unroll
+    for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
+    uint8_t d = ACC;
+    int how = 0;  // 1: needs window test
+    int dbg = 0;  // decision path: 1000*how + 100*(window+2) + 10*(bfs+1) + retries
+    if (lab[13] != a) {
+      d = REJ;
+    } else {
+      bool adj = false;
+      for (int k = 0; k < 27; ++k)
+        if (is_face(k) && lab[k] == b) adj = true;
+      if (!adj) d = REJ;
+    }
+    if (d == ACC && a > 0) {
+      if (sa && __ldcg((const long long *)A.cnt + a) == 1) {
+        if (!A.vanish_ok) d = REJ;
+      } else {
+        const int k = box_local_count(lab, a);
+        if (k == 0)
+          d = REJ;
+        else if (k != 1)
+          how = 1;
+      }
+    }
+    if (how == 1) {
+      // second-tier window test, cells spread over lanes (waits per cell)
+      const int R = lat.ndim == 2 ? 3 : 2, W = 2 * R + 1;
+      const int ncell = lat.ndim == 2 ? W * W : W * W * W;
+      for (int c = lane; c < ncell; c += 32) {
+        const int dz = lat.ndim == 2 ? 0 : c / (W * W) - R;
+        const int dy = (c / W) % W - R, dx = c % W - R;
+        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (lat.inb(zz, yy, xx)) wait_pend(A, lat.flat(zz, yy, xx), pos);
+      }
+      __syncwarp();
+      const int wv = lat.ndim == 2 ? window_pieces_2d(v, lat, y, x, a)
+                                   : window_pieces_3d(v, lat, z, y, x, a);
+      dbg = 1000 + 100 * (wv + 2);
+      if (wv == 2) {
+        d = REJ;
+      } else if (wv == 0) {
+        int r;
+        for (;;) {
+          dbg += 1;
+          r = warp_bfs(A, S, pos, f, a);
+          if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
+          if (r == 3) {
+            if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
+            r = warp_global_bfs(A, S, pos, f, a);
+          }
+          if (r == 1 || r == 2) break;
+          if (lane == 0) {
+            atomicAdd(ctl + C_BLOCKED, 1);
+            if (r == 0) wait_pend(A, S.bsite, pos);
+          }
+          __syncwarp();
+        }
+        if (r == 2) d = REJ;
+        dbg += 10 * (r + 1);
+      } else if (wv != 1) {
+        d = REJ;  // cannot happen after the waits; never accept unproven
+      }
+    }
+    if (d == ACC && b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b)) d = REJ;
+    if (lane == 0) {
+      A.blocker[pos] = dbg;
+      if (d == ACC) {
+        A.newlab[f] = b;
+        A.w[f] = pos;
+        if (sa) atomicAdd((unsigned long long *)(A.cnt + a), (unsigned long long)(-1ll));
+        if (sb) atomicAdd((unsigned long long *)(A.cnt + b), 1ull);
+      }
+      A.dec[pos] = d;
+      __threadfence();
+      // next pending position at this site
+      int32_t nxt = kInf;
+      for (uint32_t q = A.site_off[f]; q < A.site_off[f + 1]; ++q) {
+        const int32_t pq = A.pos_of[q];
+        if (pq > pos && pq < nxt) nxt = pq;
+      }
+      st_rel(A.pend + f, nxt);
+      if (sa) st_rel(A.lab_ptr + a, A.lab_ptr[a] + 1);
+      if (sb) st_rel(A.lab_ptr + b, A.lab_ptr[b] + 1);
+    }
+    __syncwarp();
   }
 }
 
@@ -1123,10 +1602,44 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_par does not fit on an SM");
     grid_blocks = per_sm * sms;
   }
-  void *args[] = {&A};
-  RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_par, dim3(grid_blocks), dim3(512), args,
-                                       smem, s));
   const int64_t N = X.n_particles;
+  void *args[] = {&A};
+  if (X.accept_mode == 1) {
+    RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_par, dim3(grid_blocks), dim3(512), args,
+                                         smem, s));
+  } else {
+    static int df_blocks = 0;
+    const size_t dsm = sizeof(WarpBfs) * kDfWarps;
+    if (df_blocks == 0) {
+      RCB_CUDA(cudaFuncSetAttribute(k_accept_df, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dsm));
+      int per_sm = 0, dev = 0, sms = 0;
+      RCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accept_df, 32 * kDfWarps,
+                                                             dsm));
+      RCB_CUDA(cudaGetDevice(&dev));
+      RCB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_df does not fit on an SM");
+      df_blocks = per_sm * sms;
+    }
+    k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
+    k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
+    k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
+    RCB_TRY(X.labkey->reserve(2 * N, s));
+    RCB_TRY(X.labkey2->reserve(2 * N, s));
+    RCB_TRY(X.labpos->reserve(2 * N, s));
+    k_df_labkeys<<<grid_for(N, 256), 256, 0, s>>>(A, N, X.labkey->p);
+    size_t b3 = 0;
+    RCB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b3, X.labkey->p, X.labkey2->p, 2 * N, 0, 64,
+                                            s));
+    RCB_TRY(X.tmp->reserve(b3, s));
+    RCB_CUDA(cub::DeviceRadixSort::SortKeys(X.tmp->p, b3, X.labkey->p, X.labkey2->p, 2 * N, 0, 64,
+                                            s));
+    k_df_labcsr<<<grid_for(2 * N, 256), 256, 0, s>>>(X.labkey2->p, 2 * N, A.nl, X.labpos->p,
+                                                     A.lab_ptr);
+    A.lab_pos = X.labpos->p;
+    RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(df_blocks), dim3(32 * kDfWarps),
+                                         args, dsm, s));
+  }
   k_acc_flags<<<grid_for(N + 1, 256), 256, 0, s>>>(A.dec, A.nneg, X.slot);
   size_t bytes = 0;
   RCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, X.slot, X.slot, N + 1, s));

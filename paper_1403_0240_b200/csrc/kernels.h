@@ -81,6 +81,12 @@ struct ParArgs {
   uint32_t *gq[2];
   int32_t *dint_acc;
   int32_t *blocker;
+  // dataflow acceptance (k_accept_df)
+  int32_t *pos_of;           // position of each particle in the rank order (INF: rank >= 0)
+  const uint32_t *site_off;  // K1 CSR (particles of a site)
+  int32_t *lab_ptr;          // per small label: index of its next undecided event
+  const int32_t *lab_pos;    // per small label: its candidates' positions, ascending
+  int32_t *gmutex;           // global-BFS fallback lock
 };
 
 struct ParExtra {
@@ -101,6 +107,10 @@ struct ParExtra {
   DBuf<uint32_t> *evkey, *evkey2, *evval, *evval2;
   DBuf<int64_t> *bounds;
   DBuf<double> *snap, *evv;
+  int accept_mode;  // 0 dataflow (default), 1 rounds
+  DBuf<uint64_t> *labkey, *labkey2;
+  DBuf<int32_t> *labpos;
+  DBuf<int64_t> *labbounds;
 };
 
 // contour.cu

@@ -245,9 +245,9 @@ def test_engine_invariants_at_full_cfg2_size(P):
 
 @pytest.mark.parametrize("which", ["cfg2", "cfg1", "cfg3_small"])
 def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
-    """K8 v2 (cooperative rounds) against K8 v1 (one thread, the literal
-    sequential greedy) on the same inputs: accepted moves in order, labels and
-    ledger must be identical."""
+    """K8 v3 (dataflow) and K8 v2 (cooperative rounds) against K8 v1 (one
+    thread, the literal sequential greedy) on the same inputs: accepted moves
+    in order, labels and ledger must be identical."""
     import scenes
     if which == "cfg2":
         sc, iters = scenes.cfg2(), 3
@@ -258,19 +258,21 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
     ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
     ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
     runs = []
-    for force in ("0", "1"):
+    for force, mode in (("0", "dataflow"), ("0", "rounds"), ("1", "dataflow")):
         monkeypatch.setenv("RCB_FORCE_SEQUENTIAL", force)
+        monkeypatch.setenv("RCB_ACCEPT", mode)
         eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
         out = []
         for _ in range(iters):
             rec = eng.iterate()
             out.append((rec.moves, rec.energy, eng.last_accepted.copy(), eng.labels))
         runs.append(out)
-    for it, (a, b) in enumerate(zip(*runs)):
-        assert a[0] == b[0], (which, it)
-        assert np.array_equal(a[2], b[2]), (which, it)
-        assert np.array_equal(a[3], b[3]), (which, it)
-        assert a[1] == b[1], (which, it, a[1], b[1])
+    for other in runs[1:]:
+        for it, (a, b) in enumerate(zip(runs[0], other)):
+            assert a[0] == b[0], (which, it)
+            assert np.array_equal(a[2], b[2]), (which, it)
+            assert np.array_equal(a[3], b[3]), (which, it)
+            assert a[1] == b[1], (which, it, a[1], b[1])
 
 
 def _adversarial_sequences():
