@@ -993,36 +993,38 @@ __global__ void k_df_small(ParArgs A) {
     A.small[l] = (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
 }
 
-// events (label, position) of candidates involving small labels, as sortable
-// 64-bit keys; everything else gets the sentinel key.
-__global__ void k_df_labkeys(ParArgs A, int64_t cap, uint64_t *__restrict__ key) {
+// events (label, position) of candidates involving small labels, emitted in
+// position order; a stable sort by label then gives each small label its
+// positions ascending.  Other candidates get the sentinel label nl.
+__global__ void k_df_labkeys(ParArgs A, int64_t cap, uint32_t *__restrict__ key,
+                             int32_t *__restrict__ val) {
   const int64_t M = (int64_t)*A.nneg;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < cap; pos += stride) {
-    uint64_t k0 = ~0ull, k1 = ~0ull;
+    uint32_t k0 = (uint32_t)A.nl, k1 = (uint32_t)A.nl;
     if (pos < M) {
       const uint32_t p = A.order[pos];
       const int32_t a = A.pown[p], b = A.pcomp[p];
-      if (A.small[a]) k0 = ((uint64_t)a << 32) | (uint64_t)pos;
-      if (A.small[b]) k1 = ((uint64_t)b << 32) | (uint64_t)pos;
+      if (A.small[a]) k0 = (uint32_t)a;
+      if (A.small[b]) k1 = (uint32_t)b;
     }
     key[2 * pos] = k0;
     key[2 * pos + 1] = k1;
+    val[2 * pos] = (int32_t)pos;
+    val[2 * pos + 1] = (int32_t)pos;
   }
 }
 
-__global__ void k_df_labcsr(const uint64_t *__restrict__ key, int64_t n, int32_t nl,
-                            int32_t *__restrict__ lab_pos, int32_t *__restrict__ lab_ptr) {
+__global__ void k_df_labcsr(const uint32_t *__restrict__ key, int32_t *__restrict__ val, int64_t n,
+                            int32_t nl, int32_t *__restrict__ lab_ptr) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = key[i];
-    if (k == ~0ull) {
-      lab_pos[i] = kInf;
+    const uint32_t l = key[i];
+    if (l >= (uint32_t)nl) {
+      val[i] = kInf;
       continue;
     }
-    lab_pos[i] = (int32_t)(k & 0xffffffffu);
-    const uint32_t l = (uint32_t)(k >> 32);
-    if (i == 0 || (uint32_t)(key[i - 1] >> 32) != l) lab_ptr[l] = (int32_t)i;
+    if (i == 0 || key[i - 1] != l) lab_ptr[l] = (int32_t)i;
   }
 }
 
@@ -1219,6 +1221,7 @@ struct FlipList {
   int8_t dz[kFlipCap], dy[kFlipCap], dx[kFlipCap];
   int32_t oldl[kFlipCap], newl[kFlipCap];
   double val[kFlipCap];
+  double ta[32], tb[32], ib[32];
   int n;
 };
 
@@ -1317,13 +1320,14 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
         s += I[h];
       }
     };
-    // 2. per ball site terms (lanes over offsets), ordered sums, competitor ball
+    // 2. per ball site terms (lanes over offsets); lane 0 replays the ordered
+    // sums from shared memory (offset order, as np.bincount accumulates)
     double ta = 0.0, tb = 0.0, sb = 0.0;
     int cb = 0;
     for (int base = 0; base < nball; base += 32) {
       const int kk = base + lane;
       double term_a = 0.0, term_b = 0.0, ib = 0.0;
-      int hit_a = 0, hit_b = 0;
+      bool hit_a = false, hit_b = false;
       if (kk < nball) {
         const Off o = ball[kk];
         const int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
@@ -1337,31 +1341,31 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
             const double cy = (double)c, iy = I[g];
             if (lg == a) {
               term_a = rho(iy, (s - vx) / (cy - 1.0), poisson) - rho(iy, s / cy, poisson);
-              hit_a = 1;
+              hit_a = true;
             } else {
               term_b = rho(iy, (s + vx) / (cy + 1.0), poisson) - rho(iy, s / cy, poisson);
-              hit_b = 1;
+              hit_b = true;
               ib = iy;
             }
           }
         }
       }
-      const int m = (nball - base) < 32 ? nball - base : 32;
-      for (int j = 0; j < m; ++j) {
-        const int ha = __shfl_sync(0xffffffffu, hit_a, j);
-        const double da = __shfl_sync(0xffffffffu, term_a, j);
-        if (ha) ta += da;
-      }
-      for (int j = 0; j < m; ++j) {
-        const int hb = __shfl_sync(0xffffffffu, hit_b, j);
-        const double db = __shfl_sync(0xffffffffu, term_b, j);
-        const double vb = __shfl_sync(0xffffffffu, ib, j);
-        if (hb) {
-          tb += db;
+      const unsigned ma = __ballot_sync(0xffffffffu, hit_a);
+      const unsigned mb = __ballot_sync(0xffffffffu, hit_b);
+      F.ta[lane] = term_a;
+      F.tb[lane] = term_b;
+      F.ib[lane] = ib;
+      __syncwarp();
+      if (lane == 0) {
+        for (unsigned m = ma; m; m &= m - 1) ta += F.ta[__ffs(m) - 1];
+        for (unsigned m = mb; m; m &= m - 1) {
+          const int j2 = __ffs(m) - 1;
+          tb += F.tb[j2];
           cb += 1;
-          sb += vb;
+          sb += F.ib[j2];
         }
       }
+      __syncwarp();
     }
     // 3. centre terms: own field of a at x, competitor count/sum at x
     if (lane == 0) {
@@ -1503,10 +1507,10 @@ __global__ void k_pc_dtot(const ParArgs A, const int64_t *__restrict__ acc,
   }
 }
 
-__global__ void __launch_bounds__(1024) k_ledger(const double *__restrict__ dtot,
-                                                 const int64_t *__restrict__ moves,
-                                                 double *__restrict__ energy) {
-  typedef OrderedSum<1024> OS;
+__global__ void __launch_bounds__(512) k_ledger(const double *__restrict__ dtot,
+                                                const int64_t *__restrict__ moves,
+                                                double *__restrict__ energy) {
+  typedef OrderedSum<512> OS;
   __shared__ typename OS::Temp T;
   const double fin = OS::run(T, *energy, (long long)*moves,
                              [&](long long i) { return dtot[i]; }, [](long long, double) {});
@@ -1624,17 +1628,20 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
-    RCB_TRY(X.labkey->reserve(2 * N, s));
-    RCB_TRY(X.labkey2->reserve(2 * N, s));
+    RCB_TRY(X.evkey->reserve(2 * N, s));
+    RCB_TRY(X.evkey2->reserve(2 * N, s));
     RCB_TRY(X.labpos->reserve(2 * N, s));
-    k_df_labkeys<<<grid_for(N, 256), 256, 0, s>>>(A, N, X.labkey->p);
+    RCB_TRY(X.labpos2->reserve(2 * N, s));
+    k_df_labkeys<<<grid_for(N, 256), 256, 0, s>>>(A, N, X.evkey->p, X.labpos2->p);
+    int lbits = 1;
+    while (lbits < 32 && ((int64_t)1 << lbits) <= A.nl) ++lbits;
     size_t b3 = 0;
-    RCB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b3, X.labkey->p, X.labkey2->p, 2 * N, 0, 64,
-                                            s));
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b3, X.evkey->p, X.evkey2->p, X.labpos2->p,
+                                             X.labpos->p, 2 * N, 0, lbits, s));
     RCB_TRY(X.tmp->reserve(b3, s));
-    RCB_CUDA(cub::DeviceRadixSort::SortKeys(X.tmp->p, b3, X.labkey->p, X.labkey2->p, 2 * N, 0, 64,
-                                            s));
-    k_df_labcsr<<<grid_for(2 * N, 256), 256, 0, s>>>(X.labkey2->p, 2 * N, A.nl, X.labpos->p,
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b3, X.evkey->p, X.evkey2->p, X.labpos2->p,
+                                             X.labpos->p, 2 * N, 0, lbits, s));
+    k_df_labcsr<<<grid_for(2 * N, 256), 256, 0, s>>>(X.evkey2->p, X.labpos->p, 2 * N, A.nl,
                                                      A.lab_ptr);
     A.lab_pos = X.labpos->p;
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(df_blocks), dim3(32 * kDfWarps),
@@ -1683,7 +1690,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (!X.region_ps)
       k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
                                                    X.lam, X.dtot);
-    k_ledger<<<1, 1024, 0, s>>>(X.dtot, X.moves, X.energy);
+    k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
     nl += 12;
   }
   k_final_labels<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.Lmut);

@@ -48,7 +48,7 @@ __device__ __forceinline__ bool run_step(double v, int e, long long &step) {
   return true;
 }
 
-template <int BT>
+template <int BT, int IT = 8>
 struct OrderedSum {
   typedef cub::BlockScan<long long, BT> Scan;
   typedef cub::BlockReduce<int, BT> Red;
@@ -60,56 +60,84 @@ struct OrderedSum {
     int stop;
   };
 
-  // Replays s = fl(s + val(i)) for i in [0, n) with the whole block; pre(i, s)
-  // receives the running value before step i (optional work per element).
+  // Replays s = fl(s + val(i)) for i in [0, n) with the whole block, BT*IT
+  // elements per step; pre(i, s) receives the running value before step i.
   // Returns the final s (valid in every thread).
   template <class Val, class Pre>
   __device__ static double run(Temp &T, double s, long long n, Val val, Pre pre) {
+    constexpr int W = BT * IT;
     long long pos = 0;
     while (pos < n) {
       const Binade b = binade_of(s);
-      const long long i = pos + threadIdx.x;
-      const bool live = i < n;
-      double v = 0.0;
-      long long step = 0;
-      bool good = true;
-      if (live) {
-        v = val(i);
-        good = b.ok && run_step(v, b.e, step);
-        if (!good) step = 0;
+      const long long i0 = pos + (long long)threadIdx.x * IT;
+      double v[IT];
+      long long loc[IT];
+      bool good[IT];
+      long long acc = 0;
+#pragma unroll
+      for (int k = 0; k < IT; ++k) {
+        const long long i = i0 + k;
+        long long st = 0;
+        good[k] = true;
+        v[k] = 0.0;
+        if (i < n) {
+          v[k] = val(i);
+          good[k] = b.ok && run_step(v[k], b.e, st);
+          if (!good[k]) st = 0;
+        }
+        acc += st;
+        loc[k] = acc;
       }
-      long long incl;
-      Scan(T.scan).InclusiveSum(step, incl);
-      if (live && good) {
-        const long long M = b.M + incl;
-        const long long aM = M < 0 ? -M : M;
-        const bool same_sign = (M < 0) == (b.M < 0);
-        good = same_sign && aM >= (1ll << 52) + 1 && aM <= (1ll << 53) - 1;
+      long long tbase;
+      Scan(T.scan).ExclusiveSum(acc, tbase);
+      int bad = W;
+#pragma unroll
+      for (int k = 0; k < IT; ++k) {
+        const long long i = i0 + k;
+        if (i >= n) continue;
+        bool g = good[k];
+        if (g) {
+          const long long M = b.M + tbase + loc[k];
+          const long long aM = M < 0 ? -M : M;
+          g = ((M < 0) == (b.M < 0)) && aM >= (1ll << 52) + 1 && aM <= (1ll << 53) - 1;
+        }
+        if (!g && bad == W) bad = (int)threadIdx.x * IT + k;
       }
-      const int bad = (live && !good) ? (int)threadIdx.x : BT;
       const int first = Red(T.red).Reduce(bad, cub::Min());
       if (threadIdx.x == 0) T.stop = first;
       __syncthreads();
       const int stop = T.stop;
-      const long long cnt_valid = (n - pos) < (long long)BT ? (long long)(n - pos) : (long long)BT;
-      const int upto = stop < cnt_valid ? stop : (int)cnt_valid;  // steps taken by the run
-      if (live && (int)threadIdx.x < upto) pre(i, ldexp((double)(b.M + incl - step), b.e - 52));
-      if ((int)threadIdx.x == upto - 1) T.base = b.M + incl;
+      const long long avail = (n - pos) < (long long)W ? (n - pos) : (long long)W;
+      const int upto = stop < avail ? stop : (int)avail;
+#pragma unroll
+      for (int k = 0; k < IT; ++k) {
+        const int w = (int)threadIdx.x * IT + k;
+        if (w < upto) {
+          const long long incl = tbase + loc[k];
+          long long st = (k == 0 ? loc[0] : loc[k] - loc[k - 1]);
+          pre(i0 + k, ldexp((double)(b.M + incl - st), b.e - 52));
+          if (w == upto - 1) T.base = b.M + incl;
+        }
+      }
       __syncthreads();
-      double s_run = upto > 0 ? ldexp((double)T.base, b.e - 52) : s;
-      if (stop < cnt_valid) {
-        // one sequential step at the breaking element
+      const double s_run = upto > 0 ? ldexp((double)T.base, b.e - 52) : s;
+      if (stop < avail) {
         const long long j = pos + stop;
-        if ((int)threadIdx.x == stop) {
+        if ((int)threadIdx.x == stop / IT) {
+          const int k = stop % IT;
+          double vj = 0.0;
+#pragma unroll
+          for (int q = 0; q < IT; ++q)
+            if (q == k) vj = v[q];
           pre(j, s_run);
-          T.s = s_run + v;
+          T.s = s_run + vj;
         }
         __syncthreads();
         s = T.s;
         pos = j + 1;
       } else {
         s = s_run;
-        pos += cnt_valid;
+        pos += avail;
       }
       __syncthreads();
     }
