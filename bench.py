@@ -44,7 +44,11 @@ def _dist():
 
 
 class Clocks:
-    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+    """Sample SM clocks and throttle reasons during the timed region, in
+    process through NVML (what nvidia-smi reads), every 20 ms."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
@@ -54,19 +58,21 @@ class Clocks:
 
     def __enter__(self):
         def loop():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            except Exception:
+                return
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([v.strip() for v in out.split(",")])
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, mx, rs))
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.02)
         self._t = threading.Thread(target=loop, daemon=True)
         self._t.start()
         return self
@@ -79,14 +85,10 @@ class Clocks:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(r[1] for r in self.rows)),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML in-process"}
 
 
 def scene_for(rank: int, small: bool = False):
@@ -233,6 +235,7 @@ def run_ours(args):
             "phase_ms_per_iteration": dict(zip(["extract", "energy", "sobolev", "rank",
                                                 "accept+rescan", "iterate"],
                                                (phase / args.steps).round(4).tolist())),
+            "step_ms": [round(r[3], 3) for r in records],
             "gpu_launches": int(launches),
             "acceptance_per_iteration": {k: v / args.steps for k, v in ctr_sum.items()},
             "clocks": clk.summary(),
