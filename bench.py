@@ -247,11 +247,23 @@ def run_ours(args):
         }
         if args.roofline and energy_sob_ms > 0:
             ach = alg_bytes / (energy_sob_ms / 1e3) / 1e9
+            traffic = None
+            try:
+                with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+                    traffic = json.load(f)["energy_plus_sobolev_dram_bytes"]
+            except Exception:
+                pass
+            shares = phase / max(phase[5], 1e-9)
             line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak,
-                                "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                                "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                                 "peak_kind": peak_kind,
+                                "algorithmic_bytes_per_iteration": alg_bytes / args.steps,
                                 "kernels": "K5 PS energy + K6 Sobolev (SURVEY §8d bytes: "
-                                           "29N + 24B_R + 28N per iteration)"}
+                                           "29N + 24B_R + 28N per iteration); traffic = ncu "
+                                           "dram bytes of one iteration (profiles/)",
+                                "dominant": {"phase": "accept (K8 v3 + exact ledger/stats)",
+                                             "share": float(shares[4]),
+                                             "bound": "latency / FP64 issue, DRAM < 1 % (ncu)"}}
         if args.cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
