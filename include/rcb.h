@@ -163,6 +163,21 @@ int32_t rcb_engine_counters(rcb_engine *eng, int64_t *out10);
 int32_t rcb_engine_debug_codes(rcb_engine *eng, int32_t *particle, int32_t *code, int64_t cap,
                                int64_t *n);
 
+/* ---- Sobolev sweep workload (BASELINE configs[4], second part) --------- */
+typedef struct rcb_sweep rcb_sweep;
+/* Paint the union of nsph spheres (z, y, x, r as float, 4 per sphere) into a
+ * zero lattice on the device, extract the contour particles (K1) and draw
+ * raw ~ N(0,1) from a seeded counter hash of (site, competitor). */
+int32_t rcb_sweep_create(int32_t ndim, const int64_t *dims, const float *spheres, int32_t nsph,
+                         uint64_t seed, const rcb_sobolev_cfg *scfg, int32_t device,
+                         rcb_sweep **out);
+void rcb_sweep_destroy(rcb_sweep *sweep);
+int32_t rcb_sweep_info(rcb_sweep *sweep, int64_t *n_particles, int64_t *n_sites, void **stream);
+/* One K6 launch over the resident particles: interactions and device ms. */
+int32_t rcb_sweep_run(rcb_sweep *sweep, int64_t *pairs, float *ms);
+int32_t rcb_sweep_get(rcb_sweep *sweep, int64_t *xs, int64_t *owners, int64_t *comps,
+                      double *raw, double *out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,8 +74,13 @@ SIGNATURES = {
     "rcb_engine_timings": [_P, _P, _P],
     "rcb_engine_counters": [_P, _P],
     "rcb_engine_debug_codes": [_P, _P, _P, _I64, _P],
+    "rcb_sweep_create": [_I32, _P, _P, _I32, C.c_uint64, _P, _I32, _P],
+    "rcb_sweep_destroy": [_P],
+    "rcb_sweep_info": [_P, _P, _P, _P],
+    "rcb_sweep_run": [_P, _P, _P],
+    "rcb_sweep_get": [_P, _P, _P, _P, _P, _P, _I64],
 }
-_RESTYPES = {"rcb_last_error": C.c_char_p, "rcb_engine_destroy": None}
+_RESTYPES = {"rcb_last_error": C.c_char_p, "rcb_engine_destroy": None, "rcb_sweep_destroy": None}
 
 
 def _load():

@@ -277,9 +277,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
     TRYB(e->Cown.reserve(V, s));
     TRYB(e->Sown.reserve(V, s));
   }
-  auto st = sobolev_stencil(ndim, scfg->length_scale);
   int maxd2 = 0;
-  for (auto &o : st) maxd2 = std::max(maxd2, (int)o.aux);
+  auto st = sobolev_rows(ndim, scfg->length_scale, &maxd2);
   if (scfg->n_weights <= maxd2)
     return bail(fail(RCB_ERR_VALUE, "Sobolev weight table shorter than the stencil needs"));
   e->nst = (int)st.size();
@@ -356,7 +355,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     cudaEventRecord(e->ev[2], s);
     const double *base = e->raw.p;
     if (e->mode == 1) {
-      RCB_TRY(sobolev_lattice(e->site_off.p, e->L.p, e->px.p, e->pcomp.p, e->raw.p, lat, e->st.p,
+      RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat, e->st.p,
                               e->nst, e->wt.p, n, e->smooth.p, &d->pairs, s));
       base = e->smooth.p;
       launches += 1;
@@ -761,9 +760,8 @@ int32_t rcb_sobolev_filter(const int64_t *coords, int64_t n, int32_t ndim, const
   }
   RCB_TRY(check_lattice(ndim, dims));
   Lat lat = make_lat(ndim, dims);
-  auto st = sobolev_stencil(ndim, params->length_scale);
   int maxd2 = 0;
-  for (auto &o : st) maxd2 = std::max(maxd2, (int)o.aux);
+  auto st = sobolev_rows(ndim, params->length_scale, &maxd2);
   if (params->n_weights <= maxd2)
     return fail(RCB_ERR_VALUE, "Sobolev weight table shorter than the stencil needs");
   TmpStream ts;

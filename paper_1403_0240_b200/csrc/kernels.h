@@ -140,9 +140,10 @@ int32_t perimeter(const int32_t *L, const Lat &lat, unsigned long long *out, cud
 double limbs_to_double(const long long *limbs);
 // sobolev.cu
 std::vector<Off> sobolev_stencil(int ndim, double length_scale);
-int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *L, const uint32_t *px,
-                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *st,
-                        int nst, const double *wt, int64_t n, double *out,
+std::vector<Off> sobolev_rows(int ndim, double length_scale, int *max_d2);
+int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
+                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *rows,
+                        int nrows, const double *wt, int64_t n, double *out,
                         unsigned long long *pairs, cudaStream_t s);
 int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &lat,
                        const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,

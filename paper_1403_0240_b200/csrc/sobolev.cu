@@ -12,43 +12,50 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "dev.cuh"
 #include "kernels.h"
 
 namespace rcb {
 
-// qown == nullptr: every particle at site g is owned by L[g] (engine layout).
+// One thread per particle p.  The stencil {o : |o|^2 < (E/2)^2} is walked row
+// by row: for each (dz, dy) in lexicographic order the partners are the
+// particles of the contiguous site range [x - h, x + h] of that lattice row,
+// fetched with two CSR lookups and visited in site order, each site's
+// particles in competitor order — exactly the canonical pair order
+// (flat q, comp q, index q) of sobolev.py:155-161.  The pair weight is the
+// host table entry w[dz^2 + dy^2 + dx^2].
 // oidx != nullptr: write the result of sorted particle p to out[oidx[p]].
 __global__ void __launch_bounds__(128) k_sobolev(
-    const uint32_t *__restrict__ site_off, const int32_t *__restrict__ L,
-    const int32_t *__restrict__ qown, const int32_t *__restrict__ pcomp,
-    const uint32_t *__restrict__ px, const double *__restrict__ raw, Lat lat,
-    const Off *__restrict__ st, int nst, const double *__restrict__ wt, int64_t n,
-    double *__restrict__ out, const uint32_t *__restrict__ oidx,
-    unsigned long long *__restrict__ pairs) {
+    const uint32_t *__restrict__ site_off, const int32_t *__restrict__ qown,
+    const int32_t *__restrict__ pcomp, const uint32_t *__restrict__ px,
+    const double *__restrict__ raw, Lat lat, const Off *__restrict__ rows, int nrows,
+    const double *__restrict__ wt, int64_t n, double *__restrict__ out,
+    const uint32_t *__restrict__ oidx, unsigned long long *__restrict__ pairs) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long np = 0;
   if (p < n) {
     const int64_t f = px[p];
-    const int32_t own = qown ? qown[p] : __ldg(&L[f]);
+    const int32_t own = __ldg(&qown[p]);
     int64_t z, y, x;
     lat.coord(f, z, y, x);
     double same = 0.0, opp = 0.0;
-    int64_t cs = 0, co = 0;
-    for (int k = 0; k < nst; ++k) {
-      const Off o = st[k];
-      const int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
-      if (!lat.inb(zz, yy, xx)) continue;
-      const int64_t g = lat.flat(zz, yy, xx);
-      const uint32_t q0 = __ldg(&site_off[g]), q1 = __ldg(&site_off[g + 1]);
-      if (q0 == q1) continue;
-      const double w = __ldg(&wt[o.aux]);
-      const int32_t lq = qown ? 0 : __ldg(&L[g]);
+    int cs = 0, co = 0;
+    for (int k = 0; k < nrows; ++k) {
+      const Off r = rows[k];
+      const int64_t zz = z + r.dz, yy = y + r.dy;
+      if (zz < 0 || zz >= lat.nz || yy < 0 || yy >= lat.ny) continue;
+      const int64_t x0 = x - r.dx < 0 ? 0 : x - r.dx;
+      const int64_t x1 = x + r.dx >= lat.nx ? lat.nx - 1 : x + r.dx;
+      const int64_t rb = lat.flat(zz, yy, 0);
+      const uint32_t q0 = __ldg(&site_off[rb + x0]), q1 = __ldg(&site_off[rb + x1 + 1]);
       np += q1 - q0;
+      const int64_t centre = rb + x;
       for (uint32_t q = q0; q < q1; ++q) {
-        const double c = w * __ldg(&raw[q]);
-        const int32_t oq = qown ? __ldg(&qown[q]) : lq;
-        if (oq == own) {
+        const int dx = (int)((int64_t)__ldg(&px[q]) - centre);
+        const double c = __ldg(&wt[(int)r.aux + dx * dx]) * __ldg(&raw[q]);
+        if (__ldg(&qown[q]) == own) {
           same += c;
           ++cs;
         }
@@ -68,6 +75,27 @@ __global__ void __launch_bounds__(128) k_sobolev(
   }
 }
 
+// Rows of the stencil: (dz, dy) in lexicographic order with half-width
+// h = max{dx : dz^2 + dy^2 + dx^2 < (E/2)^2} in Off.dx and dz^2 + dy^2 in
+// Off.aux.  max_d2 receives the largest |o|^2 (weight-table length check).
+std::vector<Off> sobolev_rows(int ndim, double length_scale, int *max_d2) {
+  const double c2 = (length_scale / 2.0) * (length_scale / 2.0);
+  const int r = (int)ceil(length_scale / 2.0);
+  std::vector<Off> out;
+  int mx = 0;
+  for (int dz = (ndim == 3 ? -r : 0); dz <= (ndim == 3 ? r : 0); ++dz)
+    for (int dy = -r; dy <= r; ++dy) {
+      const int b = dz * dz + dy * dy;
+      if (!((double)b < c2)) continue;
+      int h = 0;
+      while ((double)(b + (h + 1) * (h + 1)) < c2) ++h;
+      out.push_back(Off{(int8_t)dz, (int8_t)dy, (int8_t)h, (uint8_t)b});
+      mx = std::max(mx, b + h * h);
+    }
+  if (max_d2) *max_d2 = mx;
+  return out;
+}
+
 // Stencil of the cutoff: offsets with |o|^2 < (E/2)^2 in lexicographic order,
 // aux = |o|^2 (index into the weight table).
 std::vector<Off> sobolev_stencil(int ndim, double length_scale) {
@@ -83,12 +111,12 @@ std::vector<Off> sobolev_stencil(int ndim, double length_scale) {
   return out;
 }
 
-int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *L, const uint32_t *px,
-                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *st,
-                        int nst, const double *wt, int64_t n, double *out,
+int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
+                        const int32_t *pcomp, const double *raw, const Lat &lat, const Off *rows,
+                        int nrows, const double *wt, int64_t n, double *out,
                         unsigned long long *pairs, cudaStream_t s) {
   if (n == 0) return RCB_OK;
-  k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off, L, nullptr, pcomp, px, raw, lat, st, nst,
+  k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows, nrows,
                                              wt, n, out, nullptr, pairs);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
@@ -157,8 +185,8 @@ int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &
                                                      own.p, comp.p, rraw.p, site_off.p);
     RCB_CUDA(cudaGetLastError());
     RCB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, b2, site_off.p, site_off.p, lat.V + 1, s));
-    k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off.p, nullptr, own.p, comp.p, px.p, rraw.p,
-                                               lat, st, nst, wt, n, d_out, idx2.p, d_pairs);
+    k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off.p, own.p, comp.p, px.p, rraw.p, lat, st,
+                                               nst, wt, n, d_out, idx2.p, d_pairs);
     RCB_CUDA(cudaGetLastError());
     return RCB_OK;
   };

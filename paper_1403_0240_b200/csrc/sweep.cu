@@ -1,0 +1,207 @@
+// Sobolev-kernel sweep workload (BASELINE.json configs[4], second part):
+// contour particles of seeded sphere unions in lattices up to
+// 2048x2048x512, raw increments ~ N(0, 1), K6 alone.  The volume is painted on
+// the device (the host only draws sphere centres and radii), particles come
+// from K1, raw values from a counter-based hash of (site, competitor), so a
+// 2^31-site workload never touches the host.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "dev.cuh"
+#include "kernels.h"
+
+namespace rcb {
+
+__global__ void k_paint_spheres(int32_t *__restrict__ L, Lat lat, const float *__restrict__ sph,
+                                int nsph) {
+  // one block per sphere, threads over its bounding box
+  const int s = blockIdx.x;
+  if (s >= nsph) return;
+  const float cz = sph[4 * s], cy = sph[4 * s + 1], cx = sph[4 * s + 2], r = sph[4 * s + 3];
+  auto clampi = [](int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); };
+  const int64_t z0 = lat.ndim == 3 ? clampi((int64_t)floorf(cz - r), 0, lat.nz - 1) : 0;
+  const int64_t z1 = lat.ndim == 3 ? clampi((int64_t)ceilf(cz + r), 0, lat.nz - 1) : 0;
+  const int64_t y0 = clampi((int64_t)floorf(cy - r), 0, lat.ny - 1);
+  const int64_t y1 = clampi((int64_t)ceilf(cy + r), 0, lat.ny - 1);
+  const int64_t x0 = clampi((int64_t)floorf(cx - r), 0, lat.nx - 1);
+  const int64_t x1 = clampi((int64_t)ceilf(cx + r), 0, lat.nx - 1);
+  const int64_t nzb = z1 - z0 + 1, nyb = y1 - y0 + 1, nxb = x1 - x0 + 1;
+  const int64_t tot = nzb * nyb * nxb;
+  const float r2 = r * r;
+  for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int64_t zz = z0 + i / (nyb * nxb), yy = y0 + (i / nxb) % nyb, xx = x0 + i % nxb;
+    const float dz = lat.ndim == 3 ? (float)zz - cz : 0.f, dy = (float)yy - cy, dx = (float)xx - cx;
+    if (dz * dz + dy * dy + dx * dx <= r2) L[lat.flat(zz, yy, xx)] = 1;
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_raw_normal(const uint32_t *__restrict__ px, const int32_t *__restrict__ pcomp,
+                             int64_t n, uint64_t seed, double *__restrict__ raw) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t h1 = mix64(seed ^ ((uint64_t)px[i] * 0x9E3779B97F4A7C15ull) ^ (uint64_t)pcomp[i]);
+    const uint64_t h2 = mix64(h1 + 0x632BE59BD9B4E019ull);
+    const double u1 = ((double)(h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = (double)(h2 >> 11) * (1.0 / 9007199254740992.0);
+    raw[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+}  // namespace rcb
+
+using namespace rcb;
+
+struct rcb_sweep {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  Lat lat{};
+  int64_t n = 0;
+  DBuf<int32_t> L, pown, pcomp;
+  DBuf<uint32_t> site_off, px;
+  DBuf<double> raw, out, wt;
+  DBuf<Off> st;
+  int nst = 0;
+  DBuf<unsigned long long> pairs;
+  DBuf<uint8_t> tmp;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ~rcb_sweep() {
+    if (s) {
+      cudaSetDevice(device);
+      L.release(s); pown.release(s); pcomp.release(s); site_off.release(s); px.release(s);
+      raw.release(s); out.release(s); wt.release(s); st.release(s); pairs.release(s);
+      tmp.release(s);
+      cudaStreamSynchronize(s);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+extern "C" {
+
+int32_t rcb_sweep_create(int32_t ndim, const int64_t *dims, const float *spheres, int32_t nsph,
+                         uint64_t seed, const rcb_sobolev_cfg *scfg, int32_t device,
+                         rcb_sweep **out) {
+  *out = nullptr;
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) return fail(RCB_ERR_NODEVICE, "no CUDA device");
+  if (ndim != 2 && ndim != 3) return fail(RCB_ERR_VALUE, "sweep lattice must be 2-D or 3-D");
+  auto *w = new rcb_sweep();
+  w->device = device;
+  cudaSetDevice(device);
+  cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking);
+  cudaEventCreate(&w->e0);
+  cudaEventCreate(&w->e1);
+  cudaStream_t s = w->s;
+  w->lat = make_lat(ndim, dims);
+  const Lat &lat = w->lat;
+  auto bail = [&](int32_t rc) {
+    delete w;
+    return rc;
+  };
+  int32_t rc;
+#define TRYB(x)               \
+  if ((rc = (x)) != RCB_OK) { \
+    return bail(rc);          \
+  }
+  TRYB(w->L.reserve(lat.V, s));
+  TRYB(w->site_off.reserve(lat.V + 1, s));
+  if (cudaMemsetAsync(w->L.p, 0, sizeof(int32_t) * lat.V, s) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "memset failed"));
+  DBuf<float> dsph;
+  TRYB(dsph.reserve(4 * (size_t)(nsph > 0 ? nsph : 1), s));
+  if (nsph > 0) {
+    cudaMemcpyAsync(dsph.p, spheres, sizeof(float) * 4 * nsph, cudaMemcpyHostToDevice, s);
+    k_paint_spheres<<<nsph, 256, 0, s>>>(w->L.p, lat, dsph.p, nsph);
+  }
+  TRYB(contour_scan(w->L.p, lat, 1, w->site_off.p, w->tmp, s));
+  uint32_t total = 0;
+  cudaMemcpyAsync(&total, w->site_off.p + lat.V, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return bail(fail(RCB_ERR_CUDA, "sweep setup failed"));
+  dsph.release(s);
+  w->n = total;
+  const int64_t n = w->n > 0 ? w->n : 1;
+  TRYB(w->px.reserve(n, s));
+  TRYB(w->pown.reserve(n, s));
+  TRYB(w->pcomp.reserve(n, s));
+  TRYB(w->raw.reserve(n, s));
+  TRYB(w->out.reserve(n, s));
+  TRYB(w->pairs.reserve(1, s));
+  if (w->n > 0) {
+    TRYB(contour_emit(w->L.p, lat, 1, w->site_off.p, w->px.p, w->pown.p, w->pcomp.p, s));
+    k_raw_normal<<<grid_for(w->n, 256), 256, 0, s>>>(w->px.p, w->pcomp.p, w->n, seed, w->raw.p);
+  }
+  int maxd2 = 0;
+  auto stv = sobolev_rows(ndim, scfg->length_scale, &maxd2);
+  if (scfg->n_weights <= maxd2) return bail(fail(RCB_ERR_VALUE, "weight table too short"));
+  w->nst = (int)stv.size();
+  TRYB(w->st.reserve(stv.size(), s));
+  TRYB(w->wt.reserve(scfg->n_weights, s));
+  cudaMemcpyAsync(w->st.p, stv.data(), sizeof(Off) * stv.size(), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(w->wt.p, scfg->weights, sizeof(double) * scfg->n_weights, cudaMemcpyHostToDevice, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return bail(fail(RCB_ERR_CUDA, "sweep setup failed"));
+#undef TRYB
+  *out = w;
+  return RCB_OK;
+}
+
+void rcb_sweep_destroy(rcb_sweep *w) { delete w; }
+
+int32_t rcb_sweep_info(rcb_sweep *w, int64_t *n_particles, int64_t *n_sites, void **stream) {
+  *n_particles = w->n;
+  *n_sites = w->lat.V;
+  *stream = (void *)w->s;
+  return RCB_OK;
+}
+
+// One K6 launch over the resident particle set; device ms between events on
+// the sweep stream and the interaction count.
+int32_t rcb_sweep_run(rcb_sweep *w, int64_t *pairs, float *ms) {
+  RCB_CUDA(cudaSetDevice(w->device));
+  cudaStream_t s = w->s;
+  RCB_CUDA(cudaMemsetAsync(w->pairs.p, 0, sizeof(unsigned long long), s));
+  RCB_CUDA(cudaEventRecord(w->e0, s));
+  RCB_TRY(sobolev_lattice(w->site_off.p, w->pown.p, w->px.p, w->pcomp.p, w->raw.p, w->lat, w->st.p,
+                          w->nst, w->wt.p, w->n, w->out.p, w->pairs.p, s));
+  RCB_CUDA(cudaEventRecord(w->e1, s));
+  unsigned long long hp = 0;
+  RCB_CUDA(cudaMemcpyAsync(&hp, w->pairs.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  RCB_CUDA(cudaEventElapsedTime(ms, w->e0, w->e1));
+  *pairs = (int64_t)hp;
+  return RCB_OK;
+}
+
+// Host copies of the particle set, raw values and the last K6 output.
+int32_t rcb_sweep_get(rcb_sweep *w, int64_t *xs, int64_t *owners, int64_t *comps, double *raw,
+                      double *out, int64_t cap) {
+  if (cap < w->n) return fail(RCB_ERR_CAPACITY, "sweep buffers too small");
+  RCB_CUDA(cudaSetDevice(w->device));
+  const int64_t n = w->n;
+  std::vector<uint32_t> hx(n);
+  std::vector<int32_t> ho(n), hc(n);
+  cudaStream_t s = w->s;
+  RCB_CUDA(cudaMemcpyAsync(hx.data(), w->px.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaMemcpyAsync(ho.data(), w->pown.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaMemcpyAsync(hc.data(), w->pcomp.p, 4 * n, cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaMemcpyAsync(raw, w->raw.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaMemcpyAsync(out, w->out.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    xs[i] = hx[i];
+    owners[i] = ho[i];
+    comps[i] = hc[i];
+  }
+  return RCB_OK;
+}
+
+}  // extern "C"
