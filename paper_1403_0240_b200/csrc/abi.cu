@@ -440,7 +440,9 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.bounds = &e->evbounds;
       X.snap = &e->snap;
       X.evv = &e->evv;
-      X.accept_mode = e->accept_mode;
+      // 3-D: footprints of inconclusive topology tests often exceed a warp's
+      // hash; the round-based kernel's block BFS handles them
+      X.accept_mode = (e->accept_mode == 1 || lat.ndim == 3) ? 1 : 0;
       X.labkey = &e->labkey;
       X.labkey2 = &e->labkey2;
       X.labpos = &e->labpos;

@@ -858,9 +858,9 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   }
 }
 
-// Unbounded fallback (overflowing footprints) with global stamps/frontiers,
-// one warp at a time under a global lock; aborts (releasing the lock) on a
-// pending site.
+// Unbounded fallback (overflowing footprints) with global stamps/frontiers.
+// Run only by the candidate at the low-water mark (every earlier candidate is
+// decided), so it never meets a pending site and at most one runs at a time.
 __device__ int warp_global_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
   const Lat &lat = A.lat;
   const int lane = threadIdx.x & 31;
@@ -869,7 +869,6 @@ __device__ int warp_global_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_
   unsigned long long *nf = gnf[(threadIdx.x >> 5) % kDfWarps];
   uint32_t ep = 0;
   if (lane == 0) {
-    while (atomicCAS(A.gmutex, 0, 1) != 0) __nanosleep(256);
     __threadfence();
     ep = *(volatile uint32_t *)A.epoch;
     *(volatile uint32_t *)A.epoch = ep + 32;
@@ -953,12 +952,26 @@ __device__ int warp_global_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_
     if (r >= 0) break;
     cur = nxt;
   }
-  if (lane == 0) {
-    __threadfence();
-    atomicExch(A.gmutex, 0);
-  }
   __syncwarp();
   return r;
+}
+
+// Wait until every position before pos is decided (the candidate is the
+// earliest undecided).  Only overflowing BFS candidates wait here, so the scan
+// over dec[] is done lazily by the waiter, starting from a shared hint
+// (ctl[13]) that waiters push forward.
+__device__ __forceinline__ void wait_lowmark(const ParArgs &A, int32_t pos) {
+  int32_t m = ld_acq(A.ctl + 13);
+  int ns = 64;
+  while (m < pos) {
+    while (m < pos && *(volatile uint8_t *)(A.dec + m) != UNDEC) ++m;
+    atomicMax(A.ctl + 13, m);
+    if (m < pos) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+  __threadfence();
 }
 
 __global__ void k_df_init(ParArgs A, int64_t N) {
@@ -1115,21 +1128,29 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
       if (wv == 2) {
         d = REJ;
       } else if (wv == 0) {
+        // blocked: wait for the blocking site and retry (the footprint is at
+        // most kMaxInsertW sites); overflow: wait to become the earliest
+        // undecided candidate, then the unbounded BFS cannot block
         int r;
         for (;;) {
-          dbg += 1;
           r = warp_bfs(A, S, pos, f, a);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
-          if (r == 3) {
-            if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
-            r = warp_global_bfs(A, S, pos, f, a);
-          }
-          if (r == 1 || r == 2) break;
+          if (r != 0) break;
           if (lane == 0) {
             atomicAdd(ctl + C_BLOCKED, 1);
-            if (r == 0) wait_pend(A, S.bsite, pos);
+            wait_pend(A, S.bsite, pos);
           }
           __syncwarp();
+          dbg += 1;
+        }
+        if (r == 3) {
+          if (lane == 0) {
+            atomicAdd(ctl + C_DEFER, 1);
+            wait_lowmark(A, pos);
+          }
+          __syncwarp();
+          r = warp_global_bfs(A, S, pos, f, a);
+          dbg += 2;
         }
         if (r == 2) d = REJ;
         dbg += 10 * (r + 1);
@@ -1146,7 +1167,8 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
         if (sa) atomicAdd((unsigned long long *)(A.cnt + a), (unsigned long long)(-1ll));
         if (sb) atomicAdd((unsigned long long *)(A.cnt + b), 1ull);
       }
-      A.dec[pos] = d;
+      __threadfence();
+      *(volatile uint8_t *)(A.dec + pos) = d;
       __threadfence();
       // next pending position at this site
       int32_t nxt = kInf;

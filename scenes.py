@@ -36,11 +36,24 @@ class Scene:
 
 
 def _ellipse(shape, centre, semi):
-    g = np.ogrid[tuple(slice(0, s) for s in shape)]
+    """Boolean mask of the axis-aligned ellipsoid sum(((x_k - c_k)/a_k)^2) <= 1."""
+    m = np.zeros(shape, bool)
+    _paint(m, centre, semi, True)
+    return m
+
+
+def _paint(arr, centre, semi, value):
+    """Set arr to value inside the ellipsoid, touching only its bounding box."""
+    lo = [max(0, int(np.floor(c - a))) for c, a in zip(centre, semi)]
+    hi = [min(n, int(np.ceil(c + a)) + 1) for c, a, n in zip(centre, semi, arr.shape)]
+    if any(h <= l for l, h in zip(lo, hi)):
+        return
+    g = np.ogrid[tuple(slice(l, h) for l, h in zip(lo, hi))]
     acc = 0.0
     for gi, c, a in zip(g, centre, semi):
         acc = acc + ((gi - c) / a) ** 2
-    return acc <= 1.0
+    sub = arr[tuple(slice(l, h) for l, h in zip(lo, hi))]
+    sub[acc <= 1.0] = value
 
 
 def bubbles(shape, per_axis: int, radius: float) -> np.ndarray:
@@ -48,10 +61,8 @@ def bubbles(shape, per_axis: int, radius: float) -> np.ndarray:
     (the reference's ``bubbles:<n>:<r>`` initialisation, optimizer.py:325-335)."""
     labels = np.zeros(shape, np.int32)
     centres = [[(i + 0.5) * d / per_axis for i in range(per_axis)] for d in shape]
-    g = np.ogrid[tuple(slice(0, s) for s in shape)]
     for lab, c in enumerate(itertools.product(*centres), start=1):
-        d2 = sum((gi - ci) ** 2 for gi, ci in zip(g, c))
-        labels[d2 <= radius * radius] = lab
+        _paint(labels, c, [radius] * len(shape), lab)
     return labels
 
 
@@ -83,7 +94,7 @@ def _cfg2_image(n: int, seed: int) -> np.ndarray:
         c = rng.uniform(0, n, size=2)
         a = rng.uniform(15, 60, size=2)
         val = rng.uniform(0.6, 1.0)
-        img[_ellipse(shape, c, a)] = val
+        _paint(img, c, a, val)
     img = _blur(img, 1.5)
     return _poisson(img, 50.0, rng)
 
@@ -110,7 +121,7 @@ def cfg3(seed: int = 3, n: int = 128) -> Scene:
     for _ in range(8):
         r = rng.uniform(10, 25) * n / 128
         c = rng.uniform(r, n - r, size=3)
-        img[_ellipse(shape, c, (r, r, r))] = 1.0
+        _paint(img, c, (r, r, r), 1.0)
     img = _blur(img, (2.0, 1.0, 1.0))
     img += rng.normal(0.0, 0.25, size=shape)
     lab = np.zeros(shape, np.int32)
@@ -128,7 +139,7 @@ def cfg4(seed: int = 4, n: int = 512, n_obj: int = 64, per_axis: int = 8) -> Sce
         c = rng.uniform(0, n, size=3)
         a = rng.uniform(10, 50, size=3) * n / 512
         val = rng.uniform(0.5, 1.0)
-        img[_ellipse(shape, c, a)] = val
+        _paint(img, c, a, val)
     img = _blur(img, 1.5)
     img = _poisson(img, 30.0, rng)
     lab = bubbles(shape, per_axis, 15.0 * n / 512 if n < 512 else 15.0)
@@ -149,26 +160,12 @@ def cfg5_image(i: int, n: int = 512) -> Scene:
     for _ in range(int(rng.integers(4, 13))):
         c = rng.uniform(0, n, size=2)
         a = rng.uniform(15, 60, size=2)
-        img[_ellipse(shape, c, a)] = 1.0
+        _paint(img, c, a, 1.0)
     img += rng.normal(0.0, 0.3, size=shape)
     lab = np.zeros(shape, np.int32)
     m = int(round(56 * n / 512))
     lab[m:n - m, m:n - m] = 1
     return Scene(f"cfg5[{i}]", img.astype(np.float32), lab, "pc", "gauss", 4.0, iterations=50)
-
-
-def sphere_union_particles(shape, n_spheres: int, seed: int, rmin=6.0, rmax=20.0):
-    """Sweep input: contour particles of a union of random balls.
-    Returns (labels, xs, owners, comps, raw) with raw ~ N(0, 1)."""
-    rng = np.random.default_rng(seed)
-    labels = np.zeros(shape, np.int32)
-    g = np.ogrid[tuple(slice(0, s) for s in shape)]
-    for _ in range(n_spheres):
-        r = rng.uniform(rmin, rmax)
-        c = [rng.uniform(0, s) for s in shape]
-        d2 = sum((gi - ci) ** 2 for gi, ci in zip(g, c))
-        labels[d2 <= r * r] = 1
-    return labels, rng
 
 
 def two_region_small(shape=(48, 48), seed: int = 0) -> Scene:
