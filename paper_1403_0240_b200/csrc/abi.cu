@@ -120,6 +120,9 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, gmutex;
+  DBuf<unsigned long long> bigkey;
+  DBuf<uint32_t> bigfr, bigtag;
+  DBuf<uint8_t> bigfg;
   DBuf<int64_t> labbounds;
   int accept_mode = 0;
   bool simple_topology = false;
@@ -150,7 +153,8 @@ struct rcb_engine {
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
-      labpos.release(s); labpos2.release(s); pos_of.release(s); lab_ptr.release(s); gmutex.release(s);
+      labpos.release(s); labpos2.release(s); pos_of.release(s); bigkey.release(s);
+      bigfr.release(s); bigtag.release(s); bigfg.release(s); lab_ptr.release(s); gmutex.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -408,6 +412,22 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       P.site_off = e->site_off.p;
       P.lab_ptr = e->lab_ptr.p;
       P.gmutex = e->gmutex.p;
+      if (lat.ndim == 3 || e->accept_mode == 1) {
+        // slots for the round-based kernel's large-footprint BFS (<= 160 blocks)
+        const size_t nb = 160;
+        if (!e->bigkey.p) {
+          RCB_TRY(e->bigkey.reserve(nb * (1u << 19), s));
+          RCB_TRY(e->bigfr.reserve(nb * 2 * (1u << 17), s));
+          RCB_TRY(e->bigfg.reserve(nb * 2 * (1u << 17), s));
+          RCB_TRY(e->bigtag.reserve(nb, s));
+          RCB_CUDA(cudaMemsetAsync(e->bigkey.p, 0, sizeof(unsigned long long) * nb * (1u << 19), s));
+          RCB_CUDA(cudaMemsetAsync(e->bigtag.p, 0, sizeof(uint32_t) * nb, s));
+        }
+        P.bigkey = e->bigkey.p;
+        P.bigfr = e->bigfr.p;
+        P.bigfg = e->bigfg.p;
+        P.bigtag = e->bigtag.p;
+      }
       ParExtra X{};
       X.n_particles = n;
       X.budget = budget;

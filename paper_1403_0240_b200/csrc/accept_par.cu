@@ -229,6 +229,96 @@ __device__ __forceinline__ int window_pieces_3d(const View &v, const Lat &lat, i
   return 0;
 }
 
+// Third-tier exact window test, radius R (3-D: 9^3 cells for R = 4; 2-D:
+// 11^2 for R = 5).  Each z-plane of the window is one 128-bit mask
+// (W^2 <= 121 bits); 26-connectivity dilation is the in-plane 8-neighbour
+// dilation of planes k-1, k, k+1.  Same verdicts as window_pieces_2d/3d.
+template <int R>
+__device__ __noinline__ int window_pieces_big(const View &v, const Lat &lat, int64_t z, int64_t y,
+                                              int64_t x, int32_t a) {
+  typedef unsigned __int128 u128;
+  constexpr int W = 2 * R + 1, PL = W * W;
+  const int NZ = lat.ndim == 3 ? W : 1;
+  const u128 one = 1;
+  const u128 full = (one << PL) - 1;
+  u128 col0 = 0, colW = 0, rim = 0;
+  for (int r = 0; r < W; ++r) {
+    col0 |= one << (r * W);
+    colW |= one << (r * W + W - 1);
+  }
+  rim = col0 | colW | ((one << W) - 1) | (((one << W) - 1) << (PL - W));
+  u128 cells[W], seeds[W];
+  for (int k = 0; k < W; ++k) cells[k] = seeds[k] = 0;
+  for (int k = 0; k < NZ; ++k)
+    for (int i = 0; i < W; ++i)
+      for (int j = 0; j < W; ++j) {
+        const int dz = lat.ndim == 3 ? k - R : 0, dy = i - R, dx = j - R;
+        if (!dz && !dy && !dx) continue;
+        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (!lat.inb(zz, yy, xx)) continue;
+        const int64_t g = lat.flat(zz, yy, xx);
+        if (v.pending(g)) return -2;
+        if (v.lab(g) != a) continue;
+        const u128 bit = one << (i * W + j);
+        cells[k] |= bit;
+        if (abs(dz) <= 1 && abs(dy) <= 1 && abs(dx) <= 1) seeds[k] |= bit;
+      }
+  auto d2 = [&](u128 p) -> u128 {
+    const u128 l = p & ~col0, h = p & ~colW;
+    return (p | (h << 1) | (l >> 1) | (p << W) | (p >> W) | (h << (W + 1)) | (l << (W - 1)) |
+            (h >> (W - 1)) | (l >> (W + 1))) &
+           full;
+  };
+  auto flood = [&](u128 *r) {
+    for (;;) {
+      bool grew = false;
+      u128 dn[W];
+      for (int k = 0; k < NZ; ++k) dn[k] = d2(r[k]);
+      for (int k = 0; k < NZ; ++k) {
+        u128 n = dn[k];
+        if (k > 0) n |= dn[k - 1];
+        if (k + 1 < NZ) n |= dn[k + 1];
+        n &= cells[k];
+        if (n != r[k]) grew = true;
+        r[k] = n;
+      }
+      if (!grew) return;
+    }
+  };
+  auto touches_border = [&](const u128 *r) {
+    for (int k = 0; k < NZ; ++k) {
+      if (r[k] == 0) continue;
+      if (NZ > 1 && (k == 0 || k == NZ - 1)) return true;
+      if (r[k] & rim) return true;
+    }
+    return false;
+  };
+  u128 rest[W], comp[W];
+  bool any = false;
+  for (int k = 0; k < NZ; ++k) {
+    rest[k] = seeds[k];
+    any |= seeds[k] != 0;
+  }
+  if (!any) return 0;
+  bool first = true;
+  for (;;) {
+    int k0 = 0;
+    while (k0 < NZ && rest[k0] == 0) ++k0;
+    if (k0 == NZ) return 0;  // every seed component reaches the window rim
+    for (int k = 0; k < NZ; ++k) comp[k] = 0;
+    comp[k0] = rest[k0] & (~rest[k0] + 1);
+    flood(comp);
+    bool all = true;
+    for (int k = 0; k < NZ; ++k) {
+      if (rest[k] & ~comp[k]) all = false;
+      rest[k] &= ~comp[k];
+    }
+    if (first && all) return 1;
+    first = false;
+    if (!touches_border(comp)) return 2;
+  }
+}
+
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
   x *= 0x7feb352dU;
@@ -399,6 +489,148 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
     __syncthreads();
     const int res = S.result;
     __syncthreads();  // all threads read the verdict before thread 0 reuses S
+    if (res >= 0) return res;
+    cur = nxt;
+  }
+}
+
+// Large-footprint BFS (after the shared-memory BFS overflowed): same
+// algorithm on the block's private slot of global memory — a 2^19-entry hash
+// whose keys carry a per-BFS tag (stale keys count as empty, so nothing is
+// cleared) and 2^17-entry frontiers.  Disconnection proofs of tubes between
+// large blobs (3-D) need to flood a whole piece; they run here concurrently
+// in every block instead of through the one-per-round escape.
+static constexpr int kBigHC = 1 << 19;
+static constexpr int kBigFC = 1 << 17;
+static constexpr int kBigMaxInsert = kBigHC / 8 * 5;
+
+__device__ int block_bfs_big(const ParArgs &A, BfsShared &S, int32_t pos) {
+  const Lat &lat = A.lat;
+  View v{A, pos};
+  unsigned long long *key = A.bigkey + (size_t)blockIdx.x * kBigHC;
+  uint32_t *fr0 = A.bigfr + (size_t)blockIdx.x * 2 * kBigFC;
+  uint8_t *fg0 = A.bigfg + (size_t)blockIdx.x * 2 * kBigFC;
+  __shared__ unsigned long long tag;
+  if (threadIdx.x == 0) {
+    uint32_t t = A.bigtag[blockIdx.x] + 1;
+    if (t >= (1u << 24)) t = 1;  // (wrap: stale tags are cleared below)
+    A.bigtag[blockIdx.x] = t;
+    tag = (unsigned long long)t;
+    uint32_t p = A.order[pos];
+    S.pos = pos;
+    S.x = A.px[p];
+    S.a = A.pown[p];
+    S.b = A.pcomp[p];
+    S.blocked = S.overflow = 0;
+    S.levels = 0;
+    S.blocker = 0x7fffffff;
+    S.result = -1;
+    S.nfr[0] = S.nfr[1] = 0;
+  }
+  __syncthreads();
+  if (tag == 1)
+    for (int k = threadIdx.x; k < kBigHC; k += blockDim.x) key[k] = 0;
+  __syncthreads();
+  const unsigned long long T = tag;
+  auto make = [&](uint32_t site, int g) { return (T << 40) | ((unsigned long long)site << 8) | (unsigned)g; };
+  if (threadIdx.x == 0) {
+    int64_t z, y, x;
+    lat.coord(S.x, z, y, x);
+    auto put = [&](uint32_t site, int g) {
+      uint32_t h = hash32(site) & (kBigHC - 1);
+      while ((key[h] >> 40) == T) h = (h + 1) & (kBigHC - 1);
+      key[h] = make(site, g);
+    };
+    put((uint32_t)S.x, 255);
+    int ns = 0;
+    for (int k = 0; k < 27; ++k) {
+      if (k == 13) continue;
+      int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+      int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+      int64_t g = lat.flat(zz, yy, xx);
+      if (v.lab(g) != S.a) continue;
+      put((uint32_t)g, ns);
+      fr0[ns] = (uint32_t)g;
+      fg0[ns] = (uint8_t)ns;
+      S.par[ns] = ns;
+      S.gcount[ns] = 0;
+      S.unions[ns] = 0;
+      ++ns;
+    }
+    S.nseed = ns;
+    S.nfr[0] = ns;
+    S.ninsert = ns + 1;
+  }
+  __syncthreads();
+  __threadfence_block();
+  int cur = 0;
+  for (;;) {
+    const int n = S.nfr[cur], nxt = cur ^ 1;
+    const int32_t a = S.a;
+    const int64_t xc = S.x;
+    uint32_t *frc = fr0 + cur * kBigFC, *frn = fr0 + nxt * kBigFC;
+    uint8_t *fgc = fg0 + cur * kBigFC, *fgn = fg0 + nxt * kBigFC;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint32_t s = __ldcg(frc + j);
+      const int g = __ldcg(fgc + j);
+      int64_t z, y, x;
+      lat.coord(s, z, y, x);
+      for (int k = 0; k < 27; ++k) {
+        if (k == 13) continue;
+        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+        int64_t t = lat.flat(zz, yy, xx);
+        if (t == xc) continue;
+        int32_t pm;
+        const int32_t lt = v.lab_pend(t, pm);
+        if (pm < v.pos) {
+          S.blocked = 1;
+          atomicMin(&S.blocker, pm);
+          continue;
+        }
+        if (lt != a) continue;
+        uint32_t h = hash32((uint32_t)t) & (kBigHC - 1);
+        const unsigned long long mine = make((uint32_t)t, g);
+        for (;;) {
+          unsigned long long cv = __ldcg(key + h);
+          if ((cv >> 40) != T) {
+            const unsigned long long old = atomicCAS(key + h, cv, mine);
+            if (old == cv) {
+              const int idx = atomicAdd(&S.nfr[nxt], 1);
+              if (idx < kBigFC) {
+                frn[idx] = (uint32_t)t;
+                fgn[idx] = (uint8_t)g;
+              } else {
+                S.overflow = 1;
+              }
+              atomicAdd(&S.gcount[g], 1);
+              if (atomicAdd(&S.ninsert, 1) >= kBigMaxInsert) S.overflow = 1;
+              break;
+            }
+            cv = old;
+            if ((cv >> 40) != T) continue;  // replaced by another stale value: retry the slot
+          }
+          if ((uint32_t)((cv >> 8) & 0xffffffffu) == (uint32_t)t) {
+            const int hg = (int)(cv & 0xff);
+            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
+            break;
+          }
+          h = (h + 1) & (kBigHC - 1);
+        }
+      }
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.result = bfs_level_verdict(S, nxt);
+      S.nfr[cur] = 0;
+      S.levels += 1;
+    }
+    __syncthreads();
+    const int res = S.result;
+    __syncthreads();
     if (res >= 0) return res;
     cur = nxt;
   }
@@ -598,9 +830,14 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
             const int wv = lat.ndim == 2 ? window_pieces_2d(v, lat, y, x, a)
                                          : window_pieces_3d(v, lat, z, y, x, a);
             if (wv == -2) continue;  // a window site is still pending
-            if (wv == 2) {
+            int wb = wv;
+            if (wv == 0)
+              wb = lat.ndim == 2 ? window_pieces_big<5>(v, lat, z, y, x, a)
+                                 : window_pieces_big<4>(v, lat, z, y, x, a);
+            if (wb == -2) continue;
+            if (wb == 2) {
               d = REJ;
-            } else if (wv == 0) {
+            } else if (wb == 0) {
               int e = atomicAdd(ctl + C_BFS, 1);
               A.bfs_list[e] = (int32_t)pos;
               continue;
@@ -619,6 +856,7 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
       for (int e = blockIdx.x; e < nb; e += gridDim.x) {
         const int32_t pos = A.bfs_list[e];
         int r = block_bfs(A, S, pos);
+        if (r == 3 && A.bigkey) r = block_bfs_big(A, S, pos);
         if (threadIdx.x == 0) {
           atomicAdd(ctl + C_BFSRUNS, 1);
           if (r == 0) {
@@ -1125,9 +1363,24 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
       const int wv = lat.ndim == 2 ? window_pieces_2d(v, lat, y, x, a)
                                    : window_pieces_3d(v, lat, z, y, x, a);
       dbg = 1000 + 100 * (wv + 2);
-      if (wv == 2) {
+      int wb = wv;
+      if (wv == 0) {
+        // larger window: wait on its extra cells, then test
+        const int RB = lat.ndim == 2 ? 5 : 4, WB = 2 * RB + 1;
+        const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
+        for (int c = lane; c < nb; c += 32) {
+          const int dz = lat.ndim == 2 ? 0 : c / (WB * WB) - RB;
+          const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
+          const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+          if (lat.inb(zz, yy, xx)) wait_pend(A, lat.flat(zz, yy, xx), pos);
+        }
+        __syncwarp();
+        wb = lat.ndim == 2 ? window_pieces_big<5>(v, lat, z, y, x, a)
+                           : window_pieces_big<4>(v, lat, z, y, x, a);
+      }
+      if (wb == 2) {
         d = REJ;
-      } else if (wv == 0) {
+      } else if (wb == 0) {
         // blocked: wait for the blocking site and retry (the footprint is at
         // most kMaxInsertW sites); overflow: wait to become the earliest
         // undecided candidate, then the unbounded BFS cannot block
@@ -1154,7 +1407,7 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
         }
         if (r == 2) d = REJ;
         dbg += 10 * (r + 1);
-      } else if (wv != 1) {
+      } else if (wb != 1) {
         d = REJ;  // cannot happen after the waits; never accept unproven
       }
     }
@@ -1627,6 +1880,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_par does not fit on an SM");
     grid_blocks = per_sm * sms;
+    if (grid_blocks > 160) grid_blocks = 160;  // large-BFS slots
   }
   const int64_t N = X.n_particles;
   void *args[] = {&A};

@@ -87,6 +87,10 @@ struct ParArgs {
   int32_t *lab_ptr;          // per small label: index of its next undecided event
   const int32_t *lab_pos;    // per small label: its candidates' positions, ascending
   int32_t *gmutex;           // global-BFS fallback lock
+  // large-footprint block BFS slots (one per block of k_accept_par)
+  unsigned long long *bigkey;
+  uint32_t *bigfr, *bigtag;
+  uint8_t *bigfg;
 };
 
 struct ParExtra {
