@@ -119,7 +119,7 @@ struct rcb_engine {
   DBuf<uint32_t> evkey, evkey2, evval, evval2;
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
-  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, gmutex;
+  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, gmutex, flrows;
   DBuf<unsigned long long> bigkey;
   DBuf<uint32_t> bigfr, bigtag;
   DBuf<uint8_t> bigfg;
@@ -153,7 +153,7 @@ struct rcb_engine {
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
-      labpos.release(s); labpos2.release(s); pos_of.release(s); bigkey.release(s);
+      labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); lab_ptr.release(s); gmutex.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -467,6 +467,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.labkey2 = &e->labkey2;
       X.labpos = &e->labpos;
       X.labpos2 = &e->labpos2;
+      X.flrows = &e->flrows;
       X.labbounds = &e->labbounds;
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));

@@ -233,36 +233,34 @@ __device__ __forceinline__ int window_pieces_3d(const View &v, const Lat &lat, i
 // 11^2 for R = 5).  Each z-plane of the window is one 128-bit mask
 // (W^2 <= 121 bits); 26-connectivity dilation is the in-plane 8-neighbour
 // dilation of planes k-1, k, k+1.  Same verdicts as window_pieces_2d/3d.
+// Verdict of the window test from the window's bit vector (cell c = (k*W + i)
+// * W + j is bit c; k plane, i row, j column; centre excluded by the caller).
 template <int R>
-__device__ __noinline__ int window_pieces_big(const View &v, const Lat &lat, int64_t z, int64_t y,
-                                              int64_t x, int32_t a) {
+__device__ __noinline__ int window_verdict_bits(const uint32_t *bits, int NZ) {
   typedef unsigned __int128 u128;
   constexpr int W = 2 * R + 1, PL = W * W;
-  const int NZ = lat.ndim == 3 ? W : 1;
   const u128 one = 1;
   const u128 full = (one << PL) - 1;
-  u128 col0 = 0, colW = 0, rim = 0;
+  u128 col0 = 0, colW = 0;
   for (int r = 0; r < W; ++r) {
     col0 |= one << (r * W);
     colW |= one << (r * W + W - 1);
   }
-  rim = col0 | colW | ((one << W) - 1) | (((one << W) - 1) << (PL - W));
+  const u128 rim = col0 | colW | ((one << W) - 1) | (((one << W) - 1) << (PL - W));
   u128 cells[W], seeds[W];
-  for (int k = 0; k < W; ++k) cells[k] = seeds[k] = 0;
-  for (int k = 0; k < NZ; ++k)
-    for (int i = 0; i < W; ++i)
-      for (int j = 0; j < W; ++j) {
-        const int dz = lat.ndim == 3 ? k - R : 0, dy = i - R, dx = j - R;
-        if (!dz && !dy && !dx) continue;
-        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if (!lat.inb(zz, yy, xx)) continue;
-        const int64_t g = lat.flat(zz, yy, xx);
-        if (v.pending(g)) return -2;
-        if (v.lab(g) != a) continue;
-        const u128 bit = one << (i * W + j);
-        cells[k] |= bit;
-        if (abs(dz) <= 1 && abs(dy) <= 1 && abs(dx) <= 1) seeds[k] |= bit;
-      }
+  for (int k = 0; k < W; ++k) {
+    cells[k] = seeds[k] = 0;
+    if (k >= NZ) continue;
+    for (int q = 0; q < PL; ++q) {
+      const int c = k * PL + q;
+      if ((bits[c >> 5] >> (c & 31)) & 1u) cells[k] |= one << q;
+    }
+    const int kc = NZ == 1 ? 0 : R;
+    if (k >= kc - 1 && k <= kc + 1)
+      for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj) seeds[k] |= one << ((R + di) * W + R + dj);
+    seeds[k] &= cells[k];
+  }
   auto d2 = [&](u128 p) -> u128 {
     const u128 l = p & ~col0, h = p & ~colW;
     return (p | (h << 1) | (l >> 1) | (p << W) | (p >> W) | (h << (W + 1)) | (l << (W - 1)) |
@@ -304,7 +302,7 @@ __device__ __noinline__ int window_pieces_big(const View &v, const Lat &lat, int
   for (;;) {
     int k0 = 0;
     while (k0 < NZ && rest[k0] == 0) ++k0;
-    if (k0 == NZ) return 0;  // every seed component reaches the window rim
+    if (k0 == NZ) return 0;
     for (int k = 0; k < NZ; ++k) comp[k] = 0;
     comp[k0] = rest[k0] & (~rest[k0] + 1);
     flood(comp);
@@ -317,6 +315,32 @@ __device__ __noinline__ int window_pieces_big(const View &v, const Lat &lat, int
     first = false;
     if (!touches_border(comp)) return 2;
   }
+}
+
+// Third-tier exact window test, radius R (3-D: 9^3 cells for R = 4; 2-D:
+// 11^2 for R = 5), one thread: gathers the window's donor-label bits through
+// the view (-2 if a cell is still pending), then window_verdict_bits.
+template <int R>
+__device__ __noinline__ int window_pieces_big(const View &v, const Lat &lat, int64_t z, int64_t y,
+                                              int64_t x, int32_t a) {
+  constexpr int W = 2 * R + 1;
+  const int NZ = lat.ndim == 3 ? W : 1;
+  uint32_t bits[(W * W * W + 31) / 32];
+  for (int q = 0; q < (W * W * W + 31) / 32; ++q) bits[q] = 0;
+  for (int k = 0; k < NZ; ++k)
+    for (int i = 0; i < W; ++i)
+      for (int j = 0; j < W; ++j) {
+        const int dz = lat.ndim == 3 ? k - R : 0, dy = i - R, dx = j - R;
+        if (!dz && !dy && !dx) continue;
+        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+        if (!lat.inb(zz, yy, xx)) continue;
+        const int64_t g = lat.flat(zz, yy, xx);
+        if (v.pending(g)) return -2;
+        if (v.lab(g) != a) continue;
+        const int c = (k * W + i) * W + j;
+        bits[c >> 5] |= 1u << (c & 31);
+      }
+  return window_verdict_bits<R>(bits, NZ);
 }
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -1287,7 +1311,7 @@ __device__ __forceinline__ void df_wait_label(const ParArgs &A, int32_t l, int32
   }
 }
 
-__global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
+__global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
   __shared__ int32_t wpos[kDfWarps];
@@ -1350,34 +1374,35 @@ __global__ void __launch_bounds__(32 * kDfWarps) k_accept_df(ParArgs A) {
       }
     }
     if (how == 1) {
-      // second-tier window test, cells spread over lanes (waits per cell)
-      const int R = lat.ndim == 2 ? 3 : 2, W = 2 * R + 1;
-      const int ncell = lat.ndim == 2 ? W * W : W * W * W;
-      for (int c = lane; c < ncell; c += 32) {
-        const int dz = lat.ndim == 2 ? 0 : c / (W * W) - R;
-        const int dy = (c / W) % W - R, dx = c % W - R;
-        const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if (lat.inb(zz, yy, xx)) wait_pend(A, lat.flat(zz, yy, xx), pos);
-      }
-      __syncwarp();
-      const int wv = lat.ndim == 2 ? window_pieces_2d(v, lat, y, x, a)
-                                   : window_pieces_3d(v, lat, z, y, x, a);
-      dbg = 1000 + 100 * (wv + 2);
-      int wb = wv;
-      if (wv == 0) {
-        // larger window: wait on its extra cells, then test
-        const int RB = lat.ndim == 2 ? 5 : 4, WB = 2 * RB + 1;
-        const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
-        for (int c = lane; c < nb; c += 32) {
+      // exact window test (radius 5 in 2-D, 4 in 3-D), warp-cooperative:
+      // lanes wait on and read disjoint cells, ballots collect the donor-label
+      // bits, lane 0 floods and broadcasts the verdict
+      const int RB = lat.ndim == 2 ? 5 : 4, WB = 2 * RB + 1;
+      const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
+      uint32_t *bits = S.fr[0];
+      for (int base = 0; base < nb; base += 32) {
+        const int c = base + lane;
+        bool bit = false;
+        if (c < nb) {
           const int dz = lat.ndim == 2 ? 0 : c / (WB * WB) - RB;
           const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
           const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-          if (lat.inb(zz, yy, xx)) wait_pend(A, lat.flat(zz, yy, xx), pos);
+          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) {
+            const int64_t g = lat.flat(zz, yy, xx);
+            wait_pend(A, g, pos);
+            bit = v.lab(g) == a;
+          }
         }
-        __syncwarp();
-        wb = lat.ndim == 2 ? window_pieces_big<5>(v, lat, z, y, x, a)
-                           : window_pieces_big<4>(v, lat, z, y, x, a);
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) bits[base >> 5] = m;
       }
+      __syncwarp();
+      if (lane == 0)
+        S.result = lat.ndim == 2 ? window_verdict_bits<5>(bits, 1) : window_verdict_bits<4>(bits, WB);
+      __syncwarp();
+      const int wb = S.result;
+      __syncwarp();
+      dbg = 1000 + 100 * (wb + 2);
       if (wb == 2) {
         d = REJ;
       } else if (wb == 0) {
@@ -1507,7 +1532,11 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
                                                  const double *__restrict__ Sown,
                                                  const Off *__restrict__ ball, int nball, int R,
                                                  int poisson, double lam,
-                                                 double *__restrict__ dtot) {
+                                                 double *__restrict__ dtot,
+                                                 const uint32_t *__restrict__ fl_site,
+                                                 const int32_t *__restrict__ fl_k,
+                                                 const int32_t *__restrict__ fl_start,
+                                                 const int32_t *__restrict__ fl_end) {
   __shared__ FlipList fls[8];
   const int64_t n = *moves;
   const int lane = threadIdx.x & 31;
@@ -1525,28 +1554,27 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
     int64_t z, y, x;
     lat.coord(f, z, y, x);
     const double vx = I[f];
-    // 1. sites flipped before pos within the (4R+1)^d window around x
+    // 1. sites flipped earlier this iteration within 2R of x: walk the
+    // window rows (dz, dy) with dz^2 + dy^2 <= (2R)^2 and their sorted flips
     if (lane == 0) F.n = 0;
     __syncwarp();
-    const int nwin = wz_n * W * W;
-    for (int base = 0; base < nwin; base += 32) {
-      const int q = base + lane;
-      bool hit = false;
-      int ddz = 0, ddy = 0, ddx = 0;
-      int64_t g = 0;
-      if (q < nwin) {
-        ddz = wz_lo + q / (W * W);
-        ddy = (q / W) % W - 2 * R;
-        ddx = q % W - 2 * R;
-        const int64_t zz = z + ddz, yy = y + ddy, xx = x + ddx;
-        if (lat.inb(zz, yy, xx)) {
-          g = lat.flat(zz, yy, xx);
-          hit = ld(A.w + g) < pos;
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        const int slot = F.n + __popc(m & ((1u << lane) - 1));
+    const int R2w = 4 * R2, side = 4 * R + 1;
+    const int nrow = wz_n * side;
+    for (int q = lane; q < nrow; q += 32) {
+      const int ddz = lat.ndim == 3 ? q / side - 2 * R : 0;
+      const int ddy = q % side - 2 * R;
+      if (ddz * ddz + ddy * ddy > R2w) continue;
+      const int64_t zz = z + ddz, yy = y + ddy;
+      if (zz < 0 || zz >= lat.nz || yy < 0 || yy >= lat.ny) continue;
+      const int64_t row = zz * lat.ny + yy;
+      const int32_t lo = fl_start[row], hi = fl_end[row];
+      const int64_t centre = row * lat.nx + x;
+      for (int32_t e = lo; e < hi; ++e) {
+        const int64_t g = fl_site[e];
+        const int ddx = (int)(g - centre);
+        if (ddx < -2 * R || ddx > 2 * R || fl_k[e] >= k) continue;
+        if (ddz * ddz + ddy * ddy + ddx * ddx > R2w) continue;
+        const int slot = atomicAdd(&F.n, 1);
         if (slot < kFlipCap) {
           F.dz[slot] = (int8_t)ddz;
           F.dy[slot] = (int8_t)ddy;
@@ -1556,10 +1584,8 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
           F.val[slot] = I[g];
         }
       }
-      __syncwarp();
-      if (lane == 0) F.n += __popc(m);
-      __syncwarp();
     }
+    __syncwarp();
     const int nf = F.n;
     const bool list_ok = nf <= kFlipCap;
     // own-label count/sum of the label at (dz,dy,dx) relative to x, at pos
@@ -1655,6 +1681,31 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
       dtot[k] = d + lam * (double)di;
     }
     __syncwarp();
+  }
+}
+
+// Flip index of the kept moves: sites sorted ascending (row-major), per
+// lattice row [start, end) into the sorted list; used by k_ps_dtot.
+__global__ void k_flip_keys(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                            int64_t cap, uint32_t *__restrict__ key, int32_t *__restrict__ val) {
+  const int64_t n = *moves;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += stride) {
+    key[k] = k < n ? (uint32_t)acc[3 * k] : 0xffffffffu;
+    val[k] = (int32_t)k;
+  }
+}
+
+__global__ void k_flip_rows(const uint32_t *__restrict__ key, int64_t cap, int64_t nx,
+                            int32_t *__restrict__ start, int32_t *__restrict__ end) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
+    const uint32_t sgl = key[i];
+    if (sgl == 0xffffffffu) continue;
+    const int64_t r = (int64_t)sgl / nx;
+    if (i == 0 || (int64_t)key[i - 1] / nx != r) start[r] = (int32_t)i;
+    if (i == cap - 1 || key[i + 1] == 0xffffffffu || (int64_t)key[i + 1] / nx != r)
+      end[r] = (int32_t)(i + 1);
   }
 }
 
@@ -1932,8 +1983,25 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
   int nl = 6;
   if (X.region_ps) {
+    const int64_t rows = A.lat.nz * A.lat.ny;
+    RCB_TRY(X.evkey->reserve(N, s));
+    RCB_TRY(X.evkey2->reserve(N, s));
+    RCB_TRY(X.labpos->reserve(N, s));
+    RCB_TRY(X.labpos2->reserve(N, s));
+    RCB_TRY(X.flrows->reserve(2 * rows, s));
+    k_flip_keys<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.evkey->p, X.labpos2->p);
+    size_t b4 = 0;
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
+                                             X.labpos->p, N, 0, 32, s));
+    RCB_TRY(X.tmp->reserve(b4, s));
+    RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
+                                             X.labpos->p, N, 0, 32, s));
+    RCB_CUDA(cudaMemsetAsync(X.flrows->p, 0, sizeof(int32_t) * 2 * rows, s));
+    k_flip_rows<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, N, A.lat.nx, X.flrows->p,
+                                                 X.flrows->p + rows);
     k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
-                                      X.radius, X.poisson, X.lam, X.dtot);
+                                      X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
+                                      X.labpos->p, X.flrows->p, X.flrows->p + rows);
     ++nl;
   }
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger

@@ -113,7 +113,7 @@ struct ParExtra {
   DBuf<double> *snap, *evv;
   int accept_mode;  // 0 dataflow (default), 1 rounds
   DBuf<uint64_t> *labkey, *labkey2;
-  DBuf<int32_t> *labpos, *labpos2;
+  DBuf<int32_t> *labpos, *labpos2, *flrows;
   DBuf<int64_t> *labbounds;
 };
 
