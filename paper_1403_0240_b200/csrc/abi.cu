@@ -100,7 +100,7 @@ struct rcb_engine {
   DBuf<int64_t> cnt;
   DBuf<double> tot, tsq;
   DBuf<int32_t> Cown;
-  DBuf<double> Sown;
+  DBuf<double> Sown, rho0;
   DBuf<Off> ball, ball_full, st;
   int nball = 0, nball_full = 0, nst = 0;
   DBuf<double> wt;
@@ -144,7 +144,7 @@ struct rcb_engine {
     if (s) {
       cudaSetDevice(device);
       L.release(s); I.release(s); cnt.release(s); tot.release(s); tsq.release(s);
-      Cown.release(s); Sown.release(s); ball.release(s); ball_full.release(s); st.release(s);
+      Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
       raw.release(s); smooth.release(s); rank.release(s); acc.release(s); sc.release(s);
@@ -180,7 +180,8 @@ struct rcb_engine {
   int32_t refresh() {  // energy.py:285-291
     RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
     if (ecfg.region_model == 1)
-      RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s));
+      RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s, rho0.p,
+                        ecfg.noise_model == 1));
     return RCB_OK;
   }
 
@@ -280,6 +281,7 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
     TRYB(upload(e->ball, full.data() + 1, full.size() - 1, s));
     TRYB(e->Cown.reserve(V, s));
     TRYB(e->Sown.reserve(V, s));
+    TRYB(e->rho0.reserve(V, s));
   }
   int maxd2 = 0;
   auto st = sobolev_rows(ndim, scfg->length_scale, &maxd2);
@@ -355,7 +357,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
                              e->tsq.p, poisson, e->raw.p, s));
     else
       RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s));
+                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s, e->rho0.p));
     cudaEventRecord(e->ev[2], s);
     const double *base = e->raw.p;
     if (e->mode == 1) {
@@ -453,6 +455,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.dirty = e->dirty.p;
       X.Cown = e->Cown.p;
       X.Sown = e->Sown.p;
+      X.rho0 = e->rho0.p;
       X.evkey = &e->evkey;
       X.evkey2 = &e->evkey2;
       X.evval = &e->evval;
@@ -500,6 +503,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       A.tsq = e->tsq.p;
       A.Cown = e->Cown.p;
       A.Sown = e->Sown.p;
+      A.rho0 = e->rho0.p;
       A.ball = e->ball.p;
       A.nball = e->nball;
       A.ncomp = e->ncomp.p;

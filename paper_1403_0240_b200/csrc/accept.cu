@@ -174,7 +174,7 @@ __global__ void k_accept_seq(AcceptArgs A) {
     double dext;
     if (A.region_ps)
       dext = delta_ps(A.L, A.I, A.Cown, A.Sown, lat, A.ball, A.nball, z, y, x, a, b, A.poisson,
-                      &cb, &sb);
+                      &cb, &sb, A.rho0);
     else
       dext = delta_pc(v, A.cnt[a], A.tot[a], A.tsq[a], A.cnt[b], A.tot[b], A.tsq[b], A.poisson);
     const double dtot = dext + A.lam * (double)delta_internal(A.L, lat, z, y, x, a, b);
@@ -204,10 +204,14 @@ __global__ void k_accept_seq(AcceptArgs A) {
         } else if (l == b) {
           A.Cown[g] += 1;
           A.Sown[g] += v;
+        } else {
+          continue;
         }
+        if (A.rho0) A.rho0[g] = rho(A.I[g], A.Sown[g] / (double)A.Cown[g], A.poisson);
       }
       A.Cown[f] = cb + 1;
       A.Sown[f] = sb + v;
+      if (A.rho0) A.rho0[f] = rho(v, A.Sown[f] / (double)A.Cown[f], A.poisson);
     }
     A.L[f] = b;
     A.cnt[a] -= 1;

@@ -1536,7 +1536,8 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
                                                  const uint32_t *__restrict__ fl_site,
                                                  const int32_t *__restrict__ fl_k,
                                                  const int32_t *__restrict__ fl_start,
-                                                 const int32_t *__restrict__ fl_end) {
+                                                 const int32_t *__restrict__ fl_end,
+                                                 const double *__restrict__ rho0) {
   __shared__ FlipList fls[8];
   const int64_t n = *moves;
   const int lane = threadIdx.x & 31;
@@ -1589,23 +1590,26 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
     const int nf = F.n;
     const bool list_ok = nf <= kFlipCap;
     // own-label count/sum of the label at (dz,dy,dx) relative to x, at pos
-    auto own_field = [&](int oz, int oy, int ox, int64_t g, int32_t lg, int32_t &c, double &s) {
+    auto own_field = [&](int oz, int oy, int ox, int64_t g, int32_t lg, int32_t &c, double &s) -> bool {
       if (list_ok && !(ld(A.w + g) < pos)) {
         c = Cown[g];
         s = Sown[g];
+        bool touched = false;
         for (int e = 0; e < nf; ++e) {
           const int ez = F.dz[e] - oz, ey = F.dy[e] - oy, ex = F.dx[e] - ox;
           if (ez * ez + ey * ey + ex * ex > R2) continue;
           if (F.newl[e] == lg) {
             c += 1;
             s += F.val[e];
+            touched = true;
           }
           if (F.oldl[e] == lg) {
             c -= 1;
             s -= F.val[e];
+            touched = true;
           }
         }
-        return;
+        return !touched;  // true: the iteration-start field (and rho0) still hold
       }
       int64_t gz, gy, gx;
       lat.coord(g, gz, gy, gx);
@@ -1620,6 +1624,7 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
         c += 1;
         s += I[h];
       }
+      return false;
     };
     // 2. per ball site terms (lanes over offsets); lane 0 replays the ordered
     // sums from shared memory (offset order, as np.bincount accumulates)
@@ -1638,13 +1643,14 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
           if (lg == a || lg == b) {
             int32_t c;
             double s;
-            own_field(o.dz, o.dy, o.dx, g, lg, c, s);
+            const bool clean = own_field(o.dz, o.dy, o.dx, g, lg, c, s);
             const double cy = (double)c, iy = I[g];
+            const double r_old = (clean && rho0) ? rho0[g] : rho(iy, s / cy, poisson);
             if (lg == a) {
-              term_a = rho(iy, (s - vx) / (cy - 1.0), poisson) - rho(iy, s / cy, poisson);
+              term_a = rho(iy, (s - vx) / (cy - 1.0), poisson) - r_old;
               hit_a = true;
             } else {
-              term_b = rho(iy, (s + vx) / (cy + 1.0), poisson) - rho(iy, s / cy, poisson);
+              term_b = rho(iy, (s + vx) / (cy + 1.0), poisson) - r_old;
               hit_b = true;
               ib = iy;
             }
@@ -1672,11 +1678,11 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
     if (lane == 0) {
       int32_t ca;
       double sa;
-      own_field(0, 0, 0, f, a, ca, sa);
+      const bool clean = own_field(0, 0, 0, f, a, ca, sa);
       double d = 0.0 + ta;
       d = d + tb;
       d += rho(vx, (sb + vx) / ((double)cb + 1.0), poisson);
-      d -= rho(vx, sa / (double)ca, poisson);
+      d -= (clean && rho0) ? rho0[f] : rho(vx, sa / (double)ca, poisson);
       const int di = delta_internal_view(A, v, z, y, x, a, b);
       dtot[k] = d + lam * (double)di;
     }
@@ -1893,7 +1899,7 @@ __global__ void k_mark_band(const int64_t *__restrict__ acc, const int64_t *__re
 __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__restrict__ I, Lat lat,
                                const Off *__restrict__ ball_full, int nball_full,
                                uint8_t *__restrict__ dirty, int32_t *__restrict__ Cown,
-                               double *__restrict__ Sown) {
+                               double *__restrict__ Sown, double *__restrict__ rho0, int poisson) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < lat.V; f += stride) {
     if (!dirty[f]) continue;
@@ -1914,6 +1920,7 @@ __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__re
     }
     Cown[f] = c;
     Sown[f] = s;
+    if (rho0) rho0[f] = rho(I[f], s / (double)c, poisson);
   }
 }
 
@@ -2001,7 +2008,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
                                                  X.flrows->p + rows);
     k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
                                       X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
-                                      X.labpos->p, X.flrows->p, X.flrows->p + rows);
+                                      X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0);
     ++nl;
   }
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger
@@ -2041,7 +2048,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(X.Lmut, X.I, A.lat, X.ball_full,
-                                                          X.nball_full, X.dirty, X.Cown, X.Sown);
+                                                          X.nball_full, X.dirty, X.Cown, X.Sown,
+                                                          X.rho0, X.poisson);
     nl += 2;
   }
   RCB_CUDA(cudaGetLastError());

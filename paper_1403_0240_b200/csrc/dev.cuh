@@ -159,7 +159,9 @@ __device__ __forceinline__ int delta_internal(const int32_t *__restrict__ L, con
   return d;
 }
 
-// PS increment of one particle (energy.py:337-372; Appendix B4), with the
+// PS increment of one particle (energy.py:337-372; Appendix B4).  rho0, when
+// given, holds rho(I[y], Sown[y]/Cown[y]) for the current fields — the same
+// function of the same inputs, so results are unchanged.  Also: with the
 // dense per-label fields replaced by own-label fields Cown/Sown and the
 // competitor's ball count/sum at x gathered during the walk.  ball holds the
 // non-centre ball offsets in ball_offsets order.  Returns the increment and,
@@ -170,7 +172,8 @@ __device__ __forceinline__ double delta_ps(const int32_t *__restrict__ L,
                                            const double *__restrict__ Sown, const Lat &lat,
                                            const Off *__restrict__ ball, int nball, int64_t z,
                                            int64_t y, int64_t x, int32_t a, int32_t b, int poisson,
-                                           int32_t *cb_out, double *sb_out) {
+                                           int32_t *cb_out, double *sb_out,
+                                           const double *__restrict__ rho0 = nullptr) {
   const int64_t f = lat.flat(z, y, x);
   const double v = I[f];
   double acc_a = 0.0;
@@ -181,7 +184,7 @@ __device__ __forceinline__ double delta_ps(const int32_t *__restrict__ L,
     int64_t g = lat.flat(zz, yy, xx);
     if (L[g] != a) continue;
     double cy = (double)Cown[g], sy = Sown[g], iy = I[g];
-    acc_a += rho(iy, (sy - v) / (cy - 1.0), poisson) - rho(iy, sy / cy, poisson);
+    acc_a += rho(iy, (sy - v) / (cy - 1.0), poisson) - (rho0 ? rho0[g] : rho(iy, sy / cy, poisson));
   }
   double acc_b = 0.0, sb = 0.0;
   int32_t cb = 0;
@@ -192,14 +195,14 @@ __device__ __forceinline__ double delta_ps(const int32_t *__restrict__ L,
     int64_t g = lat.flat(zz, yy, xx);
     if (L[g] != b) continue;
     double cy = (double)Cown[g], sy = Sown[g], iy = I[g];
-    acc_b += rho(iy, (sy + v) / (cy + 1.0), poisson) - rho(iy, sy / cy, poisson);
+    acc_b += rho(iy, (sy + v) / (cy + 1.0), poisson) - (rho0 ? rho0[g] : rho(iy, sy / cy, poisson));
     cb += 1;
     sb += iy;
   }
   double d = 0.0 + acc_a;
   d = d + acc_b;
   d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
-  d -= rho(v, Sown[f] / (double)Cown[f], poisson);
+  d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
   if (cb_out) *cb_out = cb;
   if (sb_out) *sb_out = sb;
   return d;

@@ -59,18 +59,26 @@ __global__ void k_ps_fields(const int32_t *__restrict__ L, const double *__restr
   }
 }
 
+__global__ void k_rho0(const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
+                       const double *__restrict__ I, int64_t V, int poisson,
+                       double *__restrict__ rho0) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < V; f += stride)
+    rho0[f] = rho(I[f], Sown[f] / (double)Cown[f], poisson);
+}
+
 __global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restrict__ I,
                            const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
                            Lat lat, const Off *__restrict__ ball, int nball,
                            const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
                            const int32_t *__restrict__ pcomp, int64_t n, int poisson,
-                           double *__restrict__ out) {
+                           double *__restrict__ out, const double *__restrict__ rho0) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t z, y, x;
   lat.coord(px[i], z, y, x);
   out[i] = delta_ps(L, I, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i], poisson,
-                    nullptr, nullptr);
+                    nullptr, nullptr, rho0);
 }
 
 int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, const int32_t *pown,
@@ -91,8 +99,10 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
 }
 
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
-                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s) {
+                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s, double *rho0,
+                  int poisson) {
   k_ps_fields<<<grid_for(lat.V, 256), 256, 0, s>>>(L, I, lat, ball_full, nball_full, Cown, Sown);
+  if (rho0) k_rho0<<<grid_for(lat.V, 256), 256, 0, s>>>(Cown, Sown, I, lat.V, poisson, rho0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -100,10 +110,10 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
-                       double *out, cudaStream_t s) {
+                       double *out, cudaStream_t s, const double *rho0) {
   if (n == 0) return RCB_OK;
   k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown, pcomp,
-                                              n, poisson, out);
+                                              n, poisson, out, rho0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

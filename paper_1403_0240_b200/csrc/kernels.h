@@ -53,6 +53,7 @@ struct AcceptArgs {
   double *tot, *tsq;
   int32_t *Cown;
   double *Sown;
+  double *rho0;
   const Off *ball;
   int nball;
   int32_t *ncomp;
@@ -108,6 +109,7 @@ struct ParExtra {
   uint8_t *dirty;
   int32_t *Cown;
   double *Sown;
+  double *rho0;
   DBuf<uint32_t> *evkey, *evkey2, *evval, *evval2;
   DBuf<int64_t> *bounds;
   DBuf<double> *snap, *evv;
@@ -129,11 +131,12 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
                        const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
                        const double *tsq, int poisson, double *out, cudaStream_t s);
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
-                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s);
+                  int nball_full, int32_t *Cown, double *Sown, cudaStream_t s,
+                  double *rho0 = nullptr, int poisson = 0);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
-                       double *out, cudaStream_t s);
+                       double *out, cudaStream_t s, const double *rho0 = nullptr);
 int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
                       double *tot, double *tsq, StatsScratch &sc, cudaStream_t s);
 int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,
