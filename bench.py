@@ -189,6 +189,29 @@ def run_ours(args):
         tmax = float(tt.item())
     value = args.steps * ws / (tmax / 1e3)
 
+    # fp32 mode (same workload, gradient path in fp32): device-timed steps
+    fp32_value = None
+    if args.fp32:
+        o32 = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL,
+                                precision="fp32")
+        e32 = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, o32, device=local)
+        st32 = torch.cuda.ExternalStream(e32.stream, device=torch.device("cuda", local))
+        for _ in range(args.warmup):
+            e32.iterate()
+        t32 = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(st32)
+            e32.iterate()
+            a1.record(st32)
+            a1.synchronize()
+            t32 += a0.elapsed_time(a1)
+        fp32_value = args.steps * ws / (t32 / 1e3)
+        del e32
+
     # end-to-end through the public API from host buffers: construct from
     # pinned host arrays (H2D), iterate K times (each reads back its record),
     # read the labels back (D2H); wall clock, max over ranks.
@@ -236,6 +259,9 @@ def run_ours(args):
                                                 "accept+rescan", "iterate"],
                                                (phase / args.steps).round(4).tolist())),
             "step_ms": [round(r[3], 3) for r in records],
+            "fp32_mode": {"value": fp32_value, "unit": "iterations/s",
+                          "what": "same workload, raw increments + Sobolev filter in fp32 "
+                                  "(gradients rtol 1e-4, Dice >= 0.999: tests/test_gpu_fp32.py)"},
             "gpu_launches": int(launches),
             "acceptance_per_iteration": {k: v / args.steps for k, v in ctr_sum.items()},
             "clocks": clk.summary(),
@@ -343,6 +369,7 @@ def main():
     ap.add_argument("--small", action="store_true", help="256^2 crop (debug)")
     ap.add_argument("--no-roofline", dest="roofline", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-fp32", dest="fp32", action="store_false")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -58,6 +58,8 @@ typedef struct {
     int32_t allow_vanish;
     int32_t vanish_grace;
     int32_t full_fg;        /* Connectivity: 1 = default (8/26 fg), 0 = (4/6 fg) */
+    int32_t fp32;           /* 1: fp32 gradient path (raw increments, Sobolev filter);
+                               statistics, fields, ledger and totals stay fp64 */
 } rcb_opt_cfg;
 
 /* optimizer.py:58-65 IterationRecord (device part). */

@@ -34,7 +34,7 @@ class SobolevCfg(C.Structure):
 class OptCfg(C.Structure):
     _fields_ = [("gradient", C.c_int32), ("move_budget", C.c_double), ("seed", C.c_uint64),
                 ("allow_fusion", C.c_int32), ("allow_vanish", C.c_int32),
-                ("vanish_grace", C.c_int32), ("full_fg", C.c_int32)]
+                ("vanish_grace", C.c_int32), ("full_fg", C.c_int32), ("fp32", C.c_int32)]
 
 
 class IterRecord(C.Structure):

@@ -97,6 +97,7 @@ struct rcb_engine {
 
   DBuf<int32_t> L;
   DBuf<double> I;
+  DBuf<float> I32, raw32, wt32;  // fp32 mode
   DBuf<int64_t> cnt;
   DBuf<double> tot, tsq;
   DBuf<int32_t> Cown;
@@ -143,7 +144,7 @@ struct rcb_engine {
   ~rcb_engine() {
     if (s) {
       cudaSetDevice(device);
-      L.release(s); I.release(s); cnt.release(s); tot.release(s); tsq.release(s);
+      L.release(s); I.release(s); I32.release(s); raw32.release(s); wt32.release(s); cnt.release(s); tot.release(s); tsq.release(s);
       Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
@@ -290,6 +291,12 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   e->nst = (int)st.size();
   TRYB(upload(e->st, st.data(), st.size(), s));
   TRYB(upload(e->wt, scfg->weights, (size_t)scfg->n_weights, s));
+  if (ocfg->fp32) {
+    TRYB(e->I32.reserve(V, s));
+    TRYB(e->wt32.reserve(scfg->n_weights, s));
+    TRYB(to_float(e->I.p, V, e->I32.p, s));
+    TRYB(to_float(e->wt.p, scfg->n_weights, e->wt32.p, s));
+  }
   TRYB(e->newlab.reserve(V, s));
   TRYB(e->wpos.reserve(V, s));
   TRYB(e->pend.reserve(V, s));
@@ -352,7 +359,16 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     cudaEventRecord(e->ev[1], s);
     RCB_TRY(delta_int_batch(e->L.p, lat, e->px.p, e->pown.p, e->pcomp.p, n, e->dint.p, s));
     const int poisson = e->ecfg.noise_model == 1;
-    if (e->ecfg.region_model == 0)
+    const bool fp32 = e->ocfg.fp32 != 0;
+    if (fp32) RCB_TRY(e->raw32.reserve(n, s));
+    if (fp32 && e->ecfg.region_model == 0)
+      RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
+                               poisson, e->raw32.p, e->raw.p, s));
+    else if (fp32)
+      RCB_TRY(delta_ps32_batch(e->L.p, e->I32.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
+                               e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw32.p, e->raw.p,
+                               s));
+    else if (e->ecfg.region_model == 0)
       RCB_TRY(delta_pc_batch(e->I.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
                              e->tsq.p, poisson, e->raw.p, s));
     else
@@ -361,8 +377,12 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     cudaEventRecord(e->ev[2], s);
     const double *base = e->raw.p;
     if (e->mode == 1) {
-      RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat, e->st.p,
-                              e->nst, e->wt.p, n, e->smooth.p, &d->pairs, s));
+      if (fp32)
+        RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
+                                  e->st.p, e->nst, e->wt32.p, n, e->smooth.p, &d->pairs, s));
+      else
+        RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat,
+                                e->st.p, e->nst, e->wt.p, n, e->smooth.p, &d->pairs, s));
       base = e->smooth.p;
       launches += 1;
     }
@@ -1015,6 +1035,7 @@ int32_t rcb_evaluate_total(const double *image, const int32_t *labels, int32_t n
   cudaStream_t s = ts.s;
   DBuf<int32_t> L;
   DBuf<double> I;
+  DBuf<float> I32, raw32, wt32;  // fp32 mode
   int32_t rc = upload(L, labels, lat.V, s);
   if (rc == RCB_OK) rc = upload(I, image, lat.V, s);
   if (rc == RCB_OK) rc = evaluate_on(L.p, I.p, lat, cfg, mx + 1, external, internal, s);

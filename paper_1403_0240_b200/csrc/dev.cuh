@@ -227,3 +227,87 @@ __device__ __forceinline__ uint64_t double_key(double d) {
 }
 
 }  // namespace rcb
+
+namespace rcb {
+
+// ---------------------------------------------------------------------------
+// fp32 mode: the gradient path (raw increments, Sobolev filter) in single
+// precision with cancellation-free difference forms (SURVEY Appendix B,
+// "fp32 mode"); statistics, fields, ledger and totals stay fp64.
+// ---------------------------------------------------------------------------
+
+// PC increment, stable forms.  Gauss: n_b/(n_b+1)(v-mu_b)^2 - n_a/(n_a-1)(v-mu_a)^2
+// (the a-term is 0 when a vanishes).  Poisson: p(n+-1, s+-v) - p(n, s)
+// = +-v(1 - log mu) - (s+-v) log1p(+-(v-mu)/((n+-1) mu)).
+__device__ __forceinline__ float delta_pc32(float v, int64_t ca, double sa, int64_t cb, double sb,
+                                            int poisson) {
+  const float na = (float)ca, nb = (float)cb;
+  const float mua = ca > 0 ? (float)(sa / (double)ca) : 0.f;
+  const float mub = cb > 0 ? (float)(sb / (double)cb) : 0.f;
+  if (!poisson) {
+    float da = 0.f, db;
+    if (ca > 1) {
+      const float r = v - mua;
+      da = na / (na - 1.f) * r * r;
+    }
+    const float r = v - mub;
+    db = cb > 0 ? nb / (nb + 1.f) * r * r : 0.f;  // empty b: g(b') = 0 too
+    return db - da;
+  }
+  // Poisson: fall back to the direct fp64 form near the mean floor
+  if (!(mua > 1e-6f) || !(mub > 1e-6f) || ca < 2 || cb < 1) {
+    const double vd = (double)v;
+    return (float)delta_pc(vd, ca, sa, 0.0, cb, sb, 0.0, 1);
+  }
+  const float sa_f = (float)sa, sb_f = (float)sb;
+  // removal from a: n -> n-1, s -> s-v ; addition to b: n -> n+1, s -> s+v
+  const float ta = -v * (1.f - logf(mua)) - (sa_f - v) * log1pf(-(v - mua) / ((na - 1.f) * mua));
+  const float tb = v * (1.f - logf(mub)) - (sb_f + v) * log1pf((v - mub) / ((nb + 1.f) * mub));
+  return ta + tb;
+}
+
+// rho(i, theta + d) - rho(i, theta), cancellation-free.
+__device__ __forceinline__ float drho32(float i, float theta, float d, int poisson) {
+  if (!poisson) return d * (d - 2.f * (i - theta));
+  if (!(theta > 1e-6f) || !(theta + d > 1e-6f)) {
+    return (float)(rho((double)i, (double)theta + (double)d, 1) - rho((double)i, (double)theta, 1));
+  }
+  return d - i * log1pf(d / theta);
+}
+
+// PS increment in fp32 (ball terms as stable differences; the two centre
+// terms are full rho values, evaluated in fp64).
+__device__ __forceinline__ float delta_ps32(const int32_t *__restrict__ L, const float *__restrict__ I32,
+                                            const int32_t *__restrict__ Cown,
+                                            const double *__restrict__ Sown, const Lat &lat,
+                                            const Off *__restrict__ ball, int nball, int64_t z,
+                                            int64_t y, int64_t x, int32_t a, int32_t b,
+                                            int poisson) {
+  const int64_t f = lat.flat(z, y, x);
+  const float v = I32[f];
+  float acc_a = 0.f, acc_b = 0.f;
+  double sb = 0.0;
+  int32_t cb = 0;
+  for (int k = 0; k < nball; ++k) {
+    const Off o = ball[k];
+    const int64_t zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+    if (!lat.inb(zz, yy, xx)) continue;
+    const int64_t g = lat.flat(zz, yy, xx);
+    const int32_t l = L[g];
+    if (l != a && l != b) continue;
+    const float cy = (float)Cown[g], th = (float)(Sown[g] / (double)Cown[g]), iy = I32[g];
+    if (l == a) {
+      acc_a += drho32(iy, th, (th - v) / (cy - 1.f), poisson);
+    } else {
+      acc_b += drho32(iy, th, (v - th) / (cy + 1.f), poisson);
+      cb += 1;
+      sb += (double)iy;
+    }
+  }
+  const double vd = (double)v;
+  const double centre = rho(vd, (sb + vd) / ((double)cb + 1.0), poisson) -
+                        rho(vd, Sown[f] / (double)Cown[f], poisson);
+  return (acc_a + acc_b) + (float)centre;
+}
+
+}  // namespace rcb

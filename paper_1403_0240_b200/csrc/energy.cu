@@ -81,6 +81,70 @@ __global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restri
                     nullptr, nullptr, rho0);
 }
 
+// fp32 gradient path (dev.cuh: delta_pc32 / delta_ps32); outputs in float
+// (for K6) and double (rank composition in l2 mode).
+__global__ void k_delta_pc32(const float *__restrict__ I32, const uint32_t *__restrict__ px,
+                             const int32_t *__restrict__ pown, const int32_t *__restrict__ pcomp,
+                             int64_t n, const int64_t *__restrict__ cnt,
+                             const double *__restrict__ tot, int poisson,
+                             float *__restrict__ out32, double *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t a = pown[i], b = pcomp[i];
+  const float d = delta_pc32(__ldg(&I32[px[i]]), cnt[a], tot[a], cnt[b], tot[b], poisson);
+  out32[i] = d;
+  out[i] = (double)d;
+}
+
+__global__ void k_delta_ps32(const int32_t *__restrict__ L, const float *__restrict__ I32,
+                             const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
+                             Lat lat, const Off *__restrict__ ball, int nball,
+                             const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+                             const int32_t *__restrict__ pcomp, int64_t n, int poisson,
+                             float *__restrict__ out32, double *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t z, y, x;
+  lat.coord(px[i], z, y, x);
+  const float d = delta_ps32(L, I32, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i],
+                             poisson);
+  out32[i] = d;
+  out[i] = (double)d;
+}
+
+__global__ void k_to_float(const double *__restrict__ src, int64_t n, float *__restrict__ dst) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = (float)src[i];
+}
+
+int32_t to_float(const double *src, int64_t n, float *dst, cudaStream_t s) {
+  k_to_float<<<grid_for(n, 256), 256, 0, s>>>(src, n, dst);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t delta_pc32_batch(const float *I32, const uint32_t *px, const int32_t *pown,
+                         const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
+                         int poisson, float *out32, double *out, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_delta_pc32<<<grid_for(n, 256), 256, 0, s>>>(I32, px, pown, pcomp, n, cnt, tot, poisson, out32,
+                                                out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t delta_ps32_batch(const int32_t *L, const float *I32, const int32_t *Cown,
+                         const double *Sown, const Lat &lat, const Off *ball, int nball,
+                         const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
+                         int poisson, float *out32, double *out, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_delta_ps32<<<grid_for(n, 128), 128, 0, s>>>(L, I32, Cown, Sown, lat, ball, nball, px, pown,
+                                                pcomp, n, poisson, out32, out);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, const int32_t *pown,
                         const int32_t *pcomp, int64_t n, int32_t *out, cudaStream_t s) {
   if (n == 0) return RCB_OK;

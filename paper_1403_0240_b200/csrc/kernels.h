@@ -156,6 +156,19 @@ int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &
                        const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,
                        const Off *st, int nst, const double *wt, double *d_out,
                        unsigned long long *d_pairs, cudaStream_t s);
+// fp32 gradient path
+int32_t to_float(const double *src, int64_t n, float *dst, cudaStream_t s);
+int32_t delta_pc32_batch(const float *I32, const uint32_t *px, const int32_t *pown,
+                         const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
+                         int poisson, float *out32, double *out, cudaStream_t s);
+int32_t delta_ps32_batch(const int32_t *L, const float *I32, const int32_t *Cown,
+                         const double *Sown, const Lat &lat, const Off *ball, int nball,
+                         const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
+                         int poisson, float *out32, double *out, cudaStream_t s);
+int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
+                          const int32_t *pcomp, const float *raw, const Lat &lat, const Off *rows,
+                          int nrows, const float *wt, int64_t n, double *out,
+                          unsigned long long *pairs, cudaStream_t s);
 // rank.cu
 int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t n,
                    const uint32_t *px, const int32_t *pcomp, uint64_t seed, double *rank,

@@ -75,6 +75,66 @@ __global__ void __launch_bounds__(128) k_sobolev(
   }
 }
 
+// fp32 variant of K6 (fp32 mode): float increments, weights and sums.
+__global__ void __launch_bounds__(128) k_sobolev32(
+    const uint32_t *__restrict__ site_off, const int32_t *__restrict__ qown,
+    const int32_t *__restrict__ pcomp, const uint32_t *__restrict__ px,
+    const float *__restrict__ raw, Lat lat, const Off *__restrict__ rows, int nrows,
+    const float *__restrict__ wt, int64_t n, double *__restrict__ out,
+    unsigned long long *__restrict__ pairs) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long np = 0;
+  if (p < n) {
+    const int64_t f = px[p];
+    const int32_t own = __ldg(&qown[p]);
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    float same = 0.f, opp = 0.f;
+    int cs = 0, co = 0;
+    for (int k = 0; k < nrows; ++k) {
+      const Off r = rows[k];
+      const int64_t zz = z + r.dz, yy = y + r.dy;
+      if (zz < 0 || zz >= lat.nz || yy < 0 || yy >= lat.ny) continue;
+      const int64_t x0 = x - r.dx < 0 ? 0 : x - r.dx;
+      const int64_t x1 = x + r.dx >= lat.nx ? lat.nx - 1 : x + r.dx;
+      const int64_t rb = lat.flat(zz, yy, 0);
+      const uint32_t q0 = __ldg(&site_off[rb + x0]), q1 = __ldg(&site_off[rb + x1 + 1]);
+      np += q1 - q0;
+      const int64_t centre = rb + x;
+      for (uint32_t q = q0; q < q1; ++q) {
+        const int dx = (int)((int64_t)__ldg(&px[q]) - centre);
+        const float c = __ldg(&wt[(int)r.aux + dx * dx]) * __ldg(&raw[q]);
+        if (__ldg(&qown[q]) == own) {
+          same += c;
+          ++cs;
+        }
+        if (__ldg(&pcomp[q]) == own) {
+          opp += c;
+          ++co;
+        }
+      }
+    }
+    const float a = cs > 0 ? same / (float)cs : 0.f;
+    const float b = co > 0 ? opp / (float)co : 0.f;
+    out[p] = (double)(a - b);
+  }
+  if (pairs) {
+    for (int s = 16; s; s >>= 1) np += __shfl_down_sync(0xffffffffu, np, s);
+    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
+  }
+}
+
+int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
+                          const int32_t *pcomp, const float *raw, const Lat &lat, const Off *rows,
+                          int nrows, const float *wt, int64_t n, double *out,
+                          unsigned long long *pairs, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  k_sobolev32<<<grid_for(n, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows, nrows,
+                                               wt, n, out, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 // Rows of the stencil: (dz, dy) in lexicographic order with half-width
 // h = max{dx : dz^2 + dy^2 + dx^2 < (E/2)^2} in Off.dx and dz^2 + dy^2 in
 // Off.aux.  max_d2 receives the largest |o|^2 (weight-table length check).

@@ -38,8 +38,11 @@ class OptimizerConfig:
     resync_every: int = 10
     drift_tolerance: float = 1e-6
     debug_check_rate: float = 0.0
+    precision: str = "fp64"         # "fp64" (reference-exact) | "fp32" (gradient path in fp32)
 
     def __post_init__(self):
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError(f"unknown precision {self.precision!r}")
         if self.gradient not in ("l2", "sobolev"):
             raise ValueError(f"unknown gradient mode {self.gradient!r}")
         if not 0.0 < self.move_budget <= 1.0:
@@ -115,7 +118,7 @@ class RegionCompetition:
         self._ocfg = _lib.OptCfg(int(self.mode == "sobolev"), float(cfg.move_budget),
                                  int(cfg.seed) & 0xFFFFFFFFFFFFFFFF, int(cfg.allow_fusion),
                                  int(cfg.allow_vanish), int(cfg.vanish_grace),
-                                 int(self.conn.full_fg))
+                                 int(self.conn.full_fg), int(cfg.precision == "fp32"))
         dims = _lib.dims_arr(self.shape)
         h = C.c_void_p()
         _lib.check(_lib.lib.rcb_engine_create(
