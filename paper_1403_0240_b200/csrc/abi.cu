@@ -98,6 +98,8 @@ struct rcb_engine {
   DBuf<int32_t> L;
   DBuf<double> I;
   DBuf<float> I32, raw32, wt32;  // fp32 mode
+  DBuf<int32_t> cb0;             // PS: competitor ball count/sum per particle (K5)
+  DBuf<double> sb0;
   DBuf<int64_t> cnt;
   DBuf<double> tot, tsq;
   DBuf<int32_t> Cown;
@@ -136,7 +138,7 @@ struct rcb_engine {
   cudaEvent_t ev[6] = {};
   cudaEvent_t ev_acc[2] = {};
   int32_t hctl[16] = {};
-  int64_t counters[10] = {};
+  int64_t counters[12] = {};
   bool last_par = false;
   float times[6] = {};
   int32_t launches = 0;
@@ -144,7 +146,8 @@ struct rcb_engine {
   ~rcb_engine() {
     if (s) {
       cudaSetDevice(device);
-      L.release(s); I.release(s); I32.release(s); raw32.release(s); wt32.release(s); cnt.release(s); tot.release(s); tsq.release(s);
+      L.release(s); I.release(s); I32.release(s); raw32.release(s); wt32.release(s);
+      cb0.release(s); sb0.release(s); cnt.release(s); tot.release(s); tsq.release(s);
       Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
@@ -361,19 +364,24 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     const int poisson = e->ecfg.noise_model == 1;
     const bool fp32 = e->ocfg.fp32 != 0;
     if (fp32) RCB_TRY(e->raw32.reserve(n, s));
+    if (e->ecfg.region_model == 1) {
+      RCB_TRY(e->cb0.reserve(n, s));
+      RCB_TRY(e->sb0.reserve(n, s));
+    }
     if (fp32 && e->ecfg.region_model == 0)
       RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
                                poisson, e->raw32.p, e->raw.p, s));
     else if (fp32)
       RCB_TRY(delta_ps32_batch(e->L.p, e->I32.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
                                e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw32.p, e->raw.p,
-                               s));
+                               s, e->cb0.p, e->sb0.p));
     else if (e->ecfg.region_model == 0)
       RCB_TRY(delta_pc_batch(e->I.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
                              e->tsq.p, poisson, e->raw.p, s));
     else
       RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s, e->rho0.p));
+                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s, e->rho0.p,
+                             e->cb0.p, e->sb0.p));
     cudaEventRecord(e->ev[2], s);
     const double *base = e->raw.p;
     if (e->mode == 1) {
@@ -476,6 +484,8 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.Cown = e->Cown.p;
       X.Sown = e->Sown.p;
       X.rho0 = e->rho0.p;
+      X.cb0 = e->cb0.p;
+      X.sb0 = e->sb0.p;
       X.evkey = &e->evkey;
       X.evkey2 = &e->evkey2;
       X.evval = &e->evval;
@@ -564,6 +574,8 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     e->counters[7] = (int64_t)(acc_ms * 1000.f);
     e->counters[8] = e->last_par ? e->hctl[9] : 0;
     e->counters[9] = e->last_par ? e->hctl[10] : 0;
+    e->counters[10] = e->last_par ? e->hctl[14] : 0;
+    e->counters[11] = e->last_par ? e->hctl[15] : 0;
   }
   e->N = e->hsc->n_next;
   e->prepared = true;
@@ -759,7 +771,7 @@ int32_t rcb_engine_debug_codes(rcb_engine *e, int32_t *particle, int32_t *code, 
 }
 
 int32_t rcb_engine_counters(rcb_engine *e, int64_t *out8) {
-  for (int k = 0; k < 10; ++k) out8[k] = e->counters[k];
+  for (int k = 0; k < 12; ++k) out8[k] = e->counters[k];
   return RCB_OK;
 }
 
@@ -1036,6 +1048,8 @@ int32_t rcb_evaluate_total(const double *image, const int32_t *labels, int32_t n
   DBuf<int32_t> L;
   DBuf<double> I;
   DBuf<float> I32, raw32, wt32;  // fp32 mode
+  DBuf<int32_t> cb0;             // PS: competitor ball count/sum per particle (K5)
+  DBuf<double> sb0;
   int32_t rc = upload(L, labels, lat.V, s);
   if (rc == RCB_OK) rc = upload(I, image, lat.V, s);
   if (rc == RCB_OK) rc = evaluate_on(L.p, I.p, lat, cfg, mx + 1, external, internal, s);

@@ -1537,7 +1537,9 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
                                                  const int32_t *__restrict__ fl_k,
                                                  const int32_t *__restrict__ fl_start,
                                                  const int32_t *__restrict__ fl_end,
-                                                 const double *__restrict__ rho0) {
+                                                 const double *__restrict__ rho0,
+                                                 const int32_t *__restrict__ cb0,
+                                                 const double *__restrict__ sb0) {
   __shared__ FlipList fls[8];
   const int64_t n = *moves;
   const int lane = threadIdx.x & 31;
@@ -1589,6 +1591,7 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
     __syncwarp();
     const int nf = F.n;
     const bool list_ok = nf <= kFlipCap;
+    if (lane == 0) atomicAdd(A.ctl + 15, nf);  // diagnostics: flips per move
     // own-label count/sum of the label at (dz,dy,dx) relative to x, at pos
     auto own_field = [&](int oz, int oy, int ox, int64_t g, int32_t lg, int32_t &c, double &s) -> bool {
       if (list_ok && !(ld(A.w + g) < pos)) {
@@ -1611,8 +1614,30 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
         }
         return !touched;  // true: the iteration-start field (and rho0) still hold
       }
+      if (list_ok && cb0) {
+        // g flipped earlier to lg: its iteration-start ball count/sum of lg is
+        // the competitor count/sum K5 computed for g's accepted particle; the
+        // flip list (which contains g's own flip) brings it to position pos
+        const uint32_t pg = A.order[ld(A.w + g)];
+        c = cb0[pg];
+        s = sb0[pg];
+        for (int e = 0; e < nf; ++e) {
+          const int ez = F.dz[e] - oz, ey = F.dy[e] - oy, ex = F.dx[e] - ox;
+          if (ez * ez + ey * ey + ex * ex > R2) continue;
+          if (F.newl[e] == lg) {
+            c += 1;
+            s += F.val[e];
+          }
+          if (F.oldl[e] == lg) {
+            c -= 1;
+            s -= F.val[e];
+          }
+        }
+        return false;
+      }
       int64_t gz, gy, gx;
       lat.coord(g, gz, gy, gx);
+      atomicAdd(A.ctl + 14, 1);  // diagnostics: slow-path recounts
       c = 0;
       s = 0.0;
       for (int q = 0; q <= nball; ++q) {
@@ -2008,7 +2033,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
                                                  X.flrows->p + rows);
     k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
                                       X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
-                                      X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0);
+                                      X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0, X.cb0,
+                                      X.sb0);
     ++nl;
   }
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger

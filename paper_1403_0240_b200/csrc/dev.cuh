@@ -282,7 +282,7 @@ __device__ __forceinline__ float delta_ps32(const int32_t *__restrict__ L, const
                                             const double *__restrict__ Sown, const Lat &lat,
                                             const Off *__restrict__ ball, int nball, int64_t z,
                                             int64_t y, int64_t x, int32_t a, int32_t b,
-                                            int poisson) {
+                                            int poisson, int32_t *cb_out, double *sb_out) {
   const int64_t f = lat.flat(z, y, x);
   const float v = I32[f];
   float acc_a = 0.f, acc_b = 0.f;
@@ -307,6 +307,8 @@ __device__ __forceinline__ float delta_ps32(const int32_t *__restrict__ L, const
   const double vd = (double)v;
   const double centre = rho(vd, (sb + vd) / ((double)cb + 1.0), poisson) -
                         rho(vd, Sown[f] / (double)Cown[f], poisson);
+  *cb_out = cb;
+  *sb_out = sb;
   return (acc_a + acc_b) + (float)centre;
 }
 

@@ -72,13 +72,20 @@ __global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restri
                            Lat lat, const Off *__restrict__ ball, int nball,
                            const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
                            const int32_t *__restrict__ pcomp, int64_t n, int poisson,
-                           double *__restrict__ out, const double *__restrict__ rho0) {
+                           double *__restrict__ out, const double *__restrict__ rho0,
+                           int32_t *__restrict__ cb0, double *__restrict__ sb0) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t z, y, x;
   lat.coord(px[i], z, y, x);
-  out[i] = delta_ps(L, I, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i], poisson,
-                    nullptr, nullptr, rho0);
+  int32_t cb;
+  double sb;
+  out[i] = delta_ps(L, I, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i], poisson, &cb,
+                    &sb, rho0);
+  if (cb0) {  // the competitor's iteration-start ball count/sum at x (PS ledger terms)
+    cb0[i] = cb;
+    sb0[i] = sb;
+  }
 }
 
 // fp32 gradient path (dev.cuh: delta_pc32 / delta_ps32); outputs in float
@@ -101,13 +108,20 @@ __global__ void k_delta_ps32(const int32_t *__restrict__ L, const float *__restr
                              Lat lat, const Off *__restrict__ ball, int nball,
                              const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
                              const int32_t *__restrict__ pcomp, int64_t n, int poisson,
-                             float *__restrict__ out32, double *__restrict__ out) {
+                             float *__restrict__ out32, double *__restrict__ out,
+                             int32_t *__restrict__ cb0, double *__restrict__ sb0) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t z, y, x;
   lat.coord(px[i], z, y, x);
+  int32_t cb;
+  double sb;
   const float d = delta_ps32(L, I32, Cown, Sown, lat, ball, nball, z, y, x, pown[i], pcomp[i],
-                             poisson);
+                             poisson, &cb, &sb);
+  if (cb0) {
+    cb0[i] = cb;
+    sb0[i] = sb;
+  }
   out32[i] = d;
   out[i] = (double)d;
 }
@@ -137,10 +151,11 @@ int32_t delta_pc32_batch(const float *I32, const uint32_t *px, const int32_t *po
 int32_t delta_ps32_batch(const int32_t *L, const float *I32, const int32_t *Cown,
                          const double *Sown, const Lat &lat, const Off *ball, int nball,
                          const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
-                         int poisson, float *out32, double *out, cudaStream_t s) {
+                         int poisson, float *out32, double *out, cudaStream_t s, int32_t *cb0,
+                         double *sb0) {
   if (n == 0) return RCB_OK;
   k_delta_ps32<<<grid_for(n, 128), 128, 0, s>>>(L, I32, Cown, Sown, lat, ball, nball, px, pown,
-                                                pcomp, n, poisson, out32, out);
+                                                pcomp, n, poisson, out32, out, cb0, sb0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -174,10 +189,11 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
-                       double *out, cudaStream_t s, const double *rho0) {
+                       double *out, cudaStream_t s, const double *rho0, int32_t *cb0,
+                       double *sb0) {
   if (n == 0) return RCB_OK;
   k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown, pcomp,
-                                              n, poisson, out, rho0);
+                                              n, poisson, out, rho0, cb0, sb0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

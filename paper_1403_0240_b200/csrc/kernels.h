@@ -110,6 +110,8 @@ struct ParExtra {
   int32_t *Cown;
   double *Sown;
   double *rho0;
+  const int32_t *cb0;   // per particle: competitor's iteration-start ball count at x (K5)
+  const double *sb0;    // ... and ball sum
   DBuf<uint32_t> *evkey, *evkey2, *evval, *evval2;
   DBuf<int64_t> *bounds;
   DBuf<double> *snap, *evv;
@@ -136,7 +138,8 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
-                       double *out, cudaStream_t s, const double *rho0 = nullptr);
+                       double *out, cudaStream_t s, const double *rho0 = nullptr,
+                       int32_t *cb0 = nullptr, double *sb0 = nullptr);
 int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
                       double *tot, double *tsq, StatsScratch &sc, cudaStream_t s);
 int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,
@@ -164,7 +167,8 @@ int32_t delta_pc32_batch(const float *I32, const uint32_t *px, const int32_t *po
 int32_t delta_ps32_batch(const int32_t *L, const float *I32, const int32_t *Cown,
                          const double *Sown, const Lat &lat, const Off *ball, int nball,
                          const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
-                         int poisson, float *out32, double *out, cudaStream_t s);
+                         int poisson, float *out32, double *out, cudaStream_t s,
+                         int32_t *cb0 = nullptr, double *sb0 = nullptr);
 int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
                           const int32_t *pcomp, const float *raw, const Lat &lat, const Off *rows,
                           int nrows, const float *wt, int64_t n, double *out,

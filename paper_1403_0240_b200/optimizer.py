@@ -209,10 +209,11 @@ class RegionCompetition:
 
     def counters(self) -> dict:
         """Acceptance diagnostics of the last iterate() (rcb_engine_counters)."""
-        out = np.zeros(10, np.int64)
+        out = np.zeros(12, np.int64)
         _lib.check(_lib.lib.rcb_engine_counters(self._h, _lib.ptr(out)))
         keys = ["rounds", "bfs_runs", "deferred", "bfs_blocked", "negative", "moves",
-                "parallel", "accept_us", "bfs_levels", "bfs_max_levels"]
+                "parallel", "accept_us", "bfs_levels", "bfs_max_levels", "ps_recounts",
+                "ps_flips"]
         return dict(zip(keys, out.tolist()))
 
     @property
