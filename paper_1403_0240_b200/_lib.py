@@ -74,6 +74,7 @@ SIGNATURES = {
     "rcb_engine_timings": [_P, _P, _P],
     "rcb_engine_counters": [_P, _P],
     "rcb_engine_debug_codes": [_P, _P, _P, _I64, _P],
+    "rcb_engine_debug_times": [_P, _P, _I64, _P],
     "rcb_sweep_create": [_I32, _P, _P, _I32, C.c_uint64, _P, _I32, _P],
     "rcb_sweep_destroy": [_P],
     "rcb_sweep_info": [_P, _P, _P, _P],

@@ -124,6 +124,8 @@ struct rcb_engine {
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, gmutex, flrows;
   DBuf<unsigned long long> bigkey;
+  DBuf<long long> tdbg;
+  bool profile = false;
   DBuf<uint32_t> bigfr, bigtag;
   DBuf<uint8_t> bigfg;
   DBuf<int64_t> labbounds;
@@ -158,7 +160,7 @@ struct rcb_engine {
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
-      bigfr.release(s); bigtag.release(s); bigfg.release(s); lab_ptr.release(s); gmutex.release(s);
+      bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); gmutex.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -246,6 +248,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
     e->force_sequential = fs && fs[0] == '1';
     const char *am = getenv("RCB_ACCEPT");  // "rounds": K8 v2 instead of the dataflow K8 v3
     e->accept_mode = (am && strcmp(am, "rounds") == 0) ? 1 : 0;
+    const char *pf = getenv("RCB_PROFILE");
+    e->profile = pf && pf[0] == '1';
   }
   const int64_t V = e->lat.V;
   int32_t mx = 0;
@@ -442,6 +446,10 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       P.site_off = e->site_off.p;
       P.lab_ptr = e->lab_ptr.p;
       P.gmutex = e->gmutex.p;
+      if (e->profile) {
+        RCB_TRY(e->tdbg.reserve(2 * n, s));
+        P.tdbg = e->tdbg.p;
+      }
       if (lat.ndim == 3 || e->accept_mode == 1) {
         // slots for the round-based kernel's large-footprint BFS (<= 160 blocks)
         const size_t nb = 160;
@@ -766,6 +774,16 @@ int32_t rcb_engine_debug_codes(rcb_engine *e, int32_t *particle, int32_t *code, 
   RCB_CUDA(cudaSetDevice(e->device));
   RCB_CUDA(cudaMemcpyAsync(particle, e->order.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaMemcpyAsync(code, e->blocker.p, 4 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  return RCB_OK;
+}
+
+int32_t rcb_engine_debug_times(rcb_engine *e, int64_t *t2, int64_t cap, int64_t *n) {
+  const int64_t m = (e->last_par && e->profile) ? (int64_t)e->hsc->nneg : 0;
+  *n = m;
+  if (cap < m) return fail(RCB_ERR_CAPACITY, "debug buffers too small");
+  if (m == 0) return RCB_OK;
+  RCB_CUDA(cudaMemcpyAsync(t2, e->tdbg.p, 16 * m, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaStreamSynchronize(e->s));
   return RCB_OK;
 }

@@ -32,6 +32,9 @@
 #include "kernels.h"
 #include "ordered_sum.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace cg = cooperative_groups;
 
 namespace rcb {
@@ -83,6 +86,41 @@ __device__ __forceinline__ bool read_box(const View &v, const Lat &lat, int64_t 
     lab[k] = v.lab(g);
   }
   return ok;
+}
+
+// Neighbour scan of a BFS frontier site: the fg-neighbours (full box) are
+// visited one dz-plane at a time with all nine sites' loads (flip position,
+// snapshot label, pending position) issued before any is used, so a BFS level
+// costs one or three memory round trips instead of 8 / 26 dependent ones.
+// fn(t, label in the view, min pending position at t).
+template <class F>
+__device__ __forceinline__ void scan_nbrs(const View &v, const Lat &lat, uint32_t s, int64_t skip,
+                                          F &&fn) {
+  int64_t z, y, x;
+  lat.coord(s, z, y, x);
+  const int zlo = lat.ndim == 3 ? -1 : 0, zhi = lat.ndim == 3 ? 1 : 0;
+  for (int dz = zlo; dz <= zhi; ++dz) {
+    int64_t t[9];
+    int32_t wv[9], l0[9], pm[9];
+    bool ok[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int dy = k / 3 - 1, dx = k % 3 - 1;
+      const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      ok[k] = !(dz == 0 && dy == 0 && dx == 0) && lat.inb(zz, yy, xx);
+      t[k] = ok[k] ? lat.flat(zz, yy, xx) : 0;
+      ok[k] = ok[k] && t[k] != skip;
+      wv[k] = ok[k] ? ld(v.A.w + t[k]) : 0x7fffffff;
+      l0[k] = ok[k] ? __ldg(v.A.L + t[k]) : -1;
+      pm[k] = ok[k] ? ld(v.A.pend + t[k]) : 0x7fffffff;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      if (!ok[k]) continue;
+      const int32_t lab = wv[k] < v.pos ? ld(v.A.newlab + t[k]) : l0[k];
+      fn(t[k], lab, pm[k]);
+    }
+  }
 }
 
 __device__ __forceinline__ bool is_face(int k) {
@@ -458,23 +496,13 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const uint32_t s = S.fr[cur][j];
       const int g = S.fg[cur][j];
-      int64_t z, y, x;
-      lat.coord(s, z, y, x);
-      for (int k = 0; k < 27; ++k) {
-        if (k == 13) continue;
-        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-        int64_t t = lat.flat(zz, yy, xx);
-        if (t == xc) continue;
-        int32_t pm;
-        const int32_t lt = v.lab_pend(t, pm);
+      scan_nbrs(v, lat, s, xc, [&](int64_t t, int32_t lt, int32_t pm) {
         if (pm < v.pos) {
           S.blocked = 1;
           atomicMin(&S.blocker, pm);
-          continue;
+          return;
         }
-        if (lt != a) continue;
+        if (lt != a) return;
         uint32_t h = hash32((uint32_t)t) & (kHC - 1);
         for (;;) {
           unsigned long long cv = S.key[h];
@@ -502,7 +530,7 @@ __device__ int block_bfs(const ParArgs &A, BfsShared &S, int32_t pos) {
           }
           h = (h + 1) & (kHC - 1);
         }
-      }
+      });
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -598,23 +626,13 @@ __device__ int block_bfs_big(const ParArgs &A, BfsShared &S, int32_t pos) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const uint32_t s = __ldcg(frc + j);
       const int g = __ldcg(fgc + j);
-      int64_t z, y, x;
-      lat.coord(s, z, y, x);
-      for (int k = 0; k < 27; ++k) {
-        if (k == 13) continue;
-        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-        int64_t t = lat.flat(zz, yy, xx);
-        if (t == xc) continue;
-        int32_t pm;
-        const int32_t lt = v.lab_pend(t, pm);
+      scan_nbrs(v, lat, s, xc, [&](int64_t t, int32_t lt, int32_t pm) {
         if (pm < v.pos) {
           S.blocked = 1;
           atomicMin(&S.blocker, pm);
-          continue;
+          return;
         }
-        if (lt != a) continue;
+        if (lt != a) return;
         uint32_t h = hash32((uint32_t)t) & (kBigHC - 1);
         const unsigned long long mine = make((uint32_t)t, g);
         for (;;) {
@@ -643,7 +661,7 @@ __device__ int block_bfs_big(const ParArgs &A, BfsShared &S, int32_t pos) {
           }
           h = (h + 1) & (kBigHC - 1);
         }
-      }
+      });
     }
     __threadfence_block();
     __syncthreads();
@@ -969,11 +987,14 @@ __device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
 __device__ __forceinline__ void st_rel(int32_t *p, int32_t v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_rel_u8(uint8_t *p, uint8_t v) {
+  asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
   int ns = 32;
   while (ld_acq(A.pend + g) < pos) {
     __nanosleep(ns);
-    if (ns < 512) ns <<= 1;
+    if (ns < 256) ns <<= 1;
   }
 }
 
@@ -1061,23 +1082,13 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
     for (int j = lane; j < n; j += 32) {
       const uint32_t s = S.fr[cur][j];
       const int g = S.fg[cur][j];
-      int64_t z, y, x;
-      lat.coord(s, z, y, x);
-      for (int k = 0; k < 27; ++k) {
-        if (k == 13) continue;
-        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-        int64_t t = lat.flat(zz, yy, xx);
-        if (t == f) continue;
-        int32_t pm;
-        const int32_t lt = v.lab_pend(t, pm);
+      scan_nbrs(v, lat, s, f, [&](int64_t t, int32_t lt, int32_t pm) {
         if (pm < pos) {
           S.blocked = 1;
           S.bsite = t;
-          continue;
+          return;
         }
-        if (lt != a) continue;
+        if (lt != a) return;
         uint32_t h = hash32((uint32_t)t) & (kHW - 1);
         for (;;) {
           unsigned long long cv = S.key[h];
@@ -1105,7 +1116,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
           }
           h = (h + 1) & (kHW - 1);
         }
-      }
+      });
     }
     __syncwarp();
     if (lane == 0) {
@@ -1325,6 +1336,11 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     const int32_t pos = wpos[wid];
     __syncwarp();
     if (pos >= M) break;
+    if (A.tdbg && lane == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      A.tdbg[2 * pos] = (long long)t;
+    }
     const uint32_t p = A.order[pos];
     const int64_t f = A.px[p];
     const int32_t a = A.pown[p], b = A.pcomp[p];
@@ -1445,9 +1461,14 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         if (sa) atomicAdd((unsigned long long *)(A.cnt + a), (unsigned long long)(-1ll));
         if (sb) atomicAdd((unsigned long long *)(A.cnt + b), 1ull);
       }
-      __threadfence();
-      *(volatile uint8_t *)(A.dec + pos) = d;
-      __threadfence();
+      if (A.tdbg) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        A.tdbg[2 * pos + 1] = (long long)t;
+      }
+      // release: the flip (newlab, w) and counts are visible before the
+      // decision, the decision before the site's next pending position
+      st_rel_u8(A.dec + pos, d);
       // next pending position at this site
       int32_t nxt = kInf;
       for (uint32_t q = A.site_off[f]; q < A.site_off[f + 1]; ++q) {
@@ -1951,7 +1972,39 @@ __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__re
 
 size_t accept_par_smem() { return sizeof(BfsShared); }
 
+// RCB_PROFILE=1: warm per-stage device times of the acceptance (stderr).
+struct StageTimer {
+  bool on = false;
+  cudaStream_t s;
+  cudaEvent_t ev[16];
+  const char *name[16];
+  int n = 0;
+  explicit StageTimer(cudaStream_t st) : s(st) {
+    const char *e = getenv("RCB_PROFILE");
+    on = e && e[0] == '1';
+    if (on)
+      for (auto &x : ev) cudaEventCreate(&x);
+  }
+  void mark(const char *nm) {
+    if (!on || n >= 16) return;
+    name[n] = nm;
+    cudaEventRecord(ev[n++], s);
+  }
+  ~StageTimer() {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int k = 1; k < n; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[k - 1], ev[k]);
+      fprintf(stderr, "[rcb] %-12s %8.3f ms\n", name[k], ms);
+    }
+    for (auto &x : ev) cudaEventDestroy(x);
+  }
+};
+
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) {
+  StageTimer T(s);
+  T.mark("start");
   static int grid_blocks = 0;
   const size_t smem = sizeof(BfsShared);
   if (grid_blocks == 0) {
@@ -2003,9 +2056,11 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     k_df_labcsr<<<grid_for(2 * N, 256), 256, 0, s>>>(X.evkey2->p, X.labpos->p, 2 * N, A.nl,
                                                      A.lab_ptr);
     A.lab_pos = X.labpos->p;
+    T.mark("df-setup");
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(df_blocks), dim3(32 * kDfWarps),
                                          args, dsm, s));
   }
+  T.mark("decide");
   k_acc_flags<<<grid_for(N + 1, 256), 256, 0, s>>>(A.dec, A.nneg, X.slot);
   size_t bytes = 0;
   RCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, X.slot, X.slot, N + 1, s));
@@ -2013,6 +2068,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   RCB_CUDA(cub::DeviceScan::ExclusiveSum(X.tmp->p, bytes, X.slot, X.slot, N + 1, s));
   k_acc_write<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.acc, X.moves);
   k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
+  T.mark("compact");
   int nl = 6;
   if (X.region_ps) {
     const int64_t rows = A.lat.nz * A.lat.ny;
@@ -2031,12 +2087,14 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaMemsetAsync(X.flrows->p, 0, sizeof(int32_t) * 2 * rows, s));
     k_flip_rows<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, N, A.lat.nx, X.flrows->p,
                                                  X.flrows->p + rows);
+    T.mark("flip-index");
     k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
                                       X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
                                       X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0, X.cb0,
                                       X.sb0);
     ++nl;
   }
+  T.mark("ps-dtot");
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger
   {
     const int64_t cap = N;
@@ -2067,10 +2125,13 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (!X.region_ps)
       k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
                                                    X.lam, X.dtot);
+    T.mark("chains");
     k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
+    T.mark("ledger");
     nl += 12;
   }
   k_final_labels<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.Lmut);
+  T.mark("labels");
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(X.Lmut, X.I, A.lat, X.ball_full,
@@ -2078,6 +2139,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
                                                           X.rho0, X.poisson);
     nl += 2;
   }
+  T.mark("band");
   RCB_CUDA(cudaGetLastError());
   *launches = nl + 8;
   return RCB_OK;

@@ -92,6 +92,7 @@ struct ParArgs {
   unsigned long long *bigkey;
   uint32_t *bigfr, *bigtag;
   uint8_t *bigfg;
+  long long *tdbg;  // RCB_PROFILE: per position (fetch, decide) globaltimer ns
 };
 
 struct ParExtra {
