@@ -1591,12 +1591,23 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
       const int64_t zz = z + ddz, yy = y + ddy;
       if (zz < 0 || zz >= lat.nz || yy < 0 || yy >= lat.ny) continue;
       const int64_t row = zz * lat.ny + yy;
-      const int32_t lo = fl_start[row], hi = fl_end[row];
+      int32_t lo = fl_start[row], hi = fl_end[row];
       const int64_t centre = row * lat.nx + x;
+      // the row's flips are sorted by site: binary search to x - 2R
+      const uint32_t first = (uint32_t)(centre - 2 * R < row * lat.nx ? row * lat.nx : centre - 2 * R);
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (fl_site[mid] < first)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      hi = fl_end[row];
       for (int32_t e = lo; e < hi; ++e) {
         const int64_t g = fl_site[e];
         const int ddx = (int)(g - centre);
-        if (ddx < -2 * R || ddx > 2 * R || fl_k[e] >= k) continue;
+        if (ddx > 2 * R) break;
+        if (fl_k[e] >= k) continue;
         if (ddz * ddz + ddy * ddy + ddx * ddx > R2w) continue;
         const int slot = atomicAdd(&F.n, 1);
         if (slot < kFlipCap) {
