@@ -165,9 +165,9 @@ int32_t rcb_engine_counters(rcb_engine *eng, int64_t *out12);
  * particle[i] (index into last_candidates) and code[i] (decision path). */
 int32_t rcb_engine_debug_codes(rcb_engine *eng, int32_t *particle, int32_t *code, int64_t cap,
                                int64_t *n);
-/* RCB_PROFILE=1: (fetch, decide) globaltimer ns per rank position of the last
- * dataflow acceptance. */
-int32_t rcb_engine_debug_times(rcb_engine *eng, int64_t *t2, int64_t cap, int64_t *n);
+/* RCB_PROFILE=1: (fetch, decide, box done, window done) globaltimer ns per
+ * rank position of the last dataflow acceptance (t4 holds 4 * cap values). */
+int32_t rcb_engine_debug_times(rcb_engine *eng, int64_t *t4, int64_t cap, int64_t *n);
 
 /* ---- Sobolev sweep workload (BASELINE configs[4], second part) --------- */
 typedef struct rcb_sweep rcb_sweep;

@@ -122,7 +122,8 @@ struct rcb_engine {
   DBuf<uint32_t> evkey, evkey2, evval, evval2;
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
-  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, gmutex, flrows;
+  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows;
+  DBuf<unsigned long long> ufp, job;
   DBuf<unsigned long long> bigkey;
   DBuf<long long> tdbg;
   bool profile = false;
@@ -160,7 +161,8 @@ struct rcb_engine {
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
-      bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); gmutex.release(s);
+      bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s);
+      ufp.release(s); job.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -314,9 +316,7 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   TRYB(e->cnt0.reserve(e->nl, s));
   TRYB(e->ctl.reserve(16, s));
   TRYB(e->lab_ptr.reserve(e->nl, s));
-  TRYB(e->gmutex.reserve(1, s));
-  if (cudaMemsetAsync(e->gmutex.p, 0, sizeof(int32_t), s) != cudaSuccess)
-    return bail(fail(RCB_ERR_CUDA, "memset failed"));
+  TRYB(e->lbox.reserve(4 * e->nl, s));
   if (cudaMemsetAsync(e->wpos.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->pend.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s) != cudaSuccess)
@@ -445,10 +445,28 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       P.pos_of = e->pos_of.p;
       P.site_off = e->site_off.p;
       P.lab_ptr = e->lab_ptr.p;
-      P.gmutex = e->gmutex.p;
+      P.lbox = e->lbox.p;
+      {
+        const char *wr = getenv("RCB_DF_WINDOW");
+        P.win_r = wr ? atoi(wr) : 0;
+        const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs
+        P.max_insert = mi ? atoi(mi) : 0;
+        const char *bc = getenv("RCB_DF_BOXCAP");  // tests: 0 sends overflows to assist jobs
+        P.box_cap = bc ? atoi(bc) : -1;
+      }
       if (e->profile) {
-        RCB_TRY(e->tdbg.reserve(2 * n, s));
+        RCB_TRY(e->tdbg.reserve(4 * n, s));
         P.tdbg = e->tdbg.p;
+      }
+      if (lat.ndim == 2 && e->accept_mode != 1) {
+        if (!e->ufp.p) {
+          RCB_TRY(e->ufp.reserve(lat.V, s));
+          RCB_TRY(e->job.reserve(64, s));
+          RCB_CUDA(cudaMemsetAsync(e->ufp.p, 0xff, sizeof(unsigned long long) * lat.V, s));
+          RCB_CUDA(cudaMemsetAsync(e->job.p, 0, sizeof(unsigned long long) * 64, s));
+        }
+        P.ufp = e->ufp.p;
+        P.job = e->job.p;
       }
       if (lat.ndim == 3 || e->accept_mode == 1) {
         // slots for the round-based kernel's large-footprint BFS (<= 160 blocks)
@@ -783,7 +801,7 @@ int32_t rcb_engine_debug_times(rcb_engine *e, int64_t *t2, int64_t cap, int64_t 
   *n = m;
   if (cap < m) return fail(RCB_ERR_CAPACITY, "debug buffers too small");
   if (m == 0) return RCB_OK;
-  RCB_CUDA(cudaMemcpyAsync(t2, e->tdbg.p, 16 * m, cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaMemcpyAsync(t2, e->tdbg.p, 32 * m, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaStreamSynchronize(e->s));
   return RCB_OK;
 }

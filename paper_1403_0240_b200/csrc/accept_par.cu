@@ -990,11 +990,199 @@ __device__ __forceinline__ void st_rel(int32_t *p, int32_t v) {
 __device__ __forceinline__ void st_rel_u8(uint8_t *p, uint8_t v) {
   asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
 }
-__device__ __forceinline__ void wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
+__device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Assist jobs.  A candidate whose BFS footprint overflows the warp's shared
+// hash waits to become the earliest undecided candidate; its topology test is
+// then answered by a union-find connected-components pass over label a in its
+// view V_pos (minus x), run by every warp of the grid that is waiting anyway:
+// all wait loops below call warp_help() instead of sleeping.  The seeds (the
+// a-sites of x's box) are one piece iff they share a root -- the same verdict
+// as the unbounded BFS of block_bfs/global_bfs, at grid-wide parallelism.
+// The pass covers a's iteration-start bounding box grown by one site: a site
+// can only flip into a this iteration if it was face-adjacent to a.
+//   job[0]  = (tag << 32) | next chunk to claim
+//   job[1]  = last tag issued (owner only)
+//   job[8 + 8 * (tag & 3) + k], k = 0..6: x, a, pos, chunks done, first row,
+//            first column | (box width << 32), chunk count
+//   ufp[y] = (~tag << 32) | parent for the current tag; entries of older
+//            tags are larger, so they read as roots and atomicMin replaces them.
+// ---------------------------------------------------------------------------
+static constexpr int kJobChunk = 64;  // sites per claimed chunk (2 per lane)
+
+__device__ __forceinline__ unsigned long long *job_desc(const ParArgs &A, uint32_t tag) {
+  return A.job + 8 + 8 * (tag & 3);
+}
+
+// Root of x with path halving.  Parents always have smaller indices than
+// their children (hooks go to the smaller root), so pointing x at its
+// grandparent with atomicMin is monotone and commutes with concurrent hooks.
+__device__ __forceinline__ uint32_t job_find(unsigned long long *ufp, uint32_t hi, uint32_t x) {
+  for (;;) {
+    const unsigned long long v = __ldcg(ufp + x);
+    if ((uint32_t)(v >> 32) != hi) return x;
+    const uint32_t p = (uint32_t)v;
+    const unsigned long long w = __ldcg(ufp + p);
+    if ((uint32_t)(w >> 32) != hi) return p;
+    atomicMin(ufp + x, w);
+    x = (uint32_t)w;
+  }
+}
+
+__device__ void job_union(unsigned long long *ufp, uint32_t hi, uint32_t a, uint32_t b) {
+  for (;;) {
+    a = job_find(ufp, hi, a);
+    b = job_find(ufp, hi, b);
+    if (a == b) return;
+    if (a > b) {
+      const uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    const unsigned long long old = atomicMin(ufp + b, ((unsigned long long)hi << 32) | a);
+    if ((uint32_t)(old >> 32) != hi) return;  // b was a root: hooked under a
+    b = (uint32_t)old;  // b already had a parent: merge that one with a too
+  }
+}
+
+// Claim and process one chunk of the current job (whole warp).  Returns false
+// when there is nothing to claim.  Claims are fetch-and-add (a failed CAS
+// storm from thousands of waiting warps would serialise on job[0]); claims
+// past the last chunk are harmless no-ops.
+__device__ bool warp_help(const ParArgs &A) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long c = 0, desc[6] = {0, 0, 0, 0, 0, 0};
+  int got = 0;
+  if (lane == 0) {
+    c = ld_acq64(A.job);
+    if ((c >> 32) != 0 && (uint32_t)c < (uint32_t)__ldcg(A.job + 2)) {  // tag 0: none yet
+      asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], 1;" : "=l"(c) : "l"(A.job) : "memory");
+      const unsigned long long *d = job_desc(A, (uint32_t)(c >> 32));
+      if ((uint32_t)c < (uint32_t)__ldcg(d + 6)) {
+        desc[0] = __ldcg(d);
+        desc[1] = __ldcg(d + 1);
+        desc[2] = __ldcg(d + 2);
+        desc[4] = __ldcg(d + 4);
+        desc[5] = __ldcg(d + 5);
+        got = 1;
+      }
+    }
+  }
+  got = __shfl_sync(0xffffffffu, got, 0);
+  if (!got) return false;
+  c = __shfl_sync(0xffffffffu, c, 0);
+  const int64_t f = (int64_t)__shfl_sync(0xffffffffu, desc[0], 0);
+  const int32_t a = (int32_t)__shfl_sync(0xffffffffu, desc[1], 0);
+  const int32_t pos = (int32_t)__shfl_sync(0xffffffffu, desc[2], 0);
+  const int64_t r0 = (int64_t)__shfl_sync(0xffffffffu, desc[4], 0);
+  const unsigned long long cw = __shfl_sync(0xffffffffu, desc[5], 0);
+  const int64_t c0 = (int64_t)(uint32_t)cw, bw = (int64_t)(cw >> 32);
+  const uint32_t tag = (uint32_t)(c >> 32), hi = ~tag;
+  const Lat &lat = A.lat;
+  View v{A, pos};
+  const int64_t i0 = (int64_t)(uint32_t)c * kJobChunk, nbox = (int64_t)__ldcg(job_desc(A, tag) + 7);
+#pragma unroll
+  for (int i = 0; i < kJobChunk / 32; ++i) {
+    const int64_t li = i0 + i * 32 + lane;
+    if (li >= nbox) continue;
+    const int64_t yy = r0 + li / bw, x = c0 + li % bw, y = yy * lat.nx + x;
+    if (y == f || v.lab(y) != a) continue;
+    // backward half of the 8-neighbourhood: every edge once (the job box
+    // contains every a-site, so edges to sites outside it never join a-sites)
+    const int dys[4] = {-1, -1, -1, 0}, dxs[4] = {-1, 0, 1, -1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t y2 = yy + dys[k], xx = x + dxs[k];
+      if (!lat.inb(0, y2, xx)) continue;
+      const int64_t g = y2 * lat.nx + xx;
+      if (g != f && v.lab(g) == a) job_union(A.ufp, hi, (uint32_t)y, (uint32_t)g);
+    }
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicAdd(job_desc(A, tag) + 3, 1ull);
+  return true;
+}
+
+// Run the job of candidate pos (the earliest undecided; whole warp).
+// Returns 1 (one piece) or 2 (several pieces).
+__device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
+  const int lane = threadIdx.x & 31;
+  uint32_t tag = 0;
+  unsigned long long nch = 0;
+  if (lane == 0) {
+    const Lat &lat = A.lat;
+    const int32_t *bx = A.lbox + 4 * a;
+    const int64_t r0 = bx[0] > 0 ? bx[0] - 1 : 0, r1 = bx[1] + 1 < lat.ny ? bx[1] + 1 : lat.ny - 1;
+    const int64_t c0 = bx[2] > 0 ? bx[2] - 1 : 0, c1 = bx[3] + 1 < lat.nx ? bx[3] + 1 : lat.nx - 1;
+    const int64_t bw = c1 - c0 + 1, nbox = (r1 - r0 + 1) * bw;
+    nch = (unsigned long long)((nbox + kJobChunk - 1) / kJobChunk);
+    tag = (uint32_t)A.job[1] + 1;
+    A.job[1] = tag;
+    unsigned long long *d = job_desc(A, tag);
+    d[0] = (unsigned long long)f;
+    d[1] = (unsigned long long)(uint32_t)a;
+    d[2] = (unsigned long long)(uint32_t)pos;
+    d[3] = 0;
+    d[4] = (unsigned long long)r0;
+    d[5] = (unsigned long long)c0 | ((unsigned long long)bw << 32);
+    d[6] = nch;
+    d[7] = (unsigned long long)nbox;
+    A.job[2] = nch;
+    __threadfence();
+    st_rel64(A.job, (unsigned long long)tag << 32);
+  }
+  tag = __shfl_sync(0xffffffffu, tag, 0);
+  nch = __shfl_sync(0xffffffffu, nch, 0);
+  __syncwarp();
+  while (warp_help(A)) {
+  }
+  int r = 2;
+  if (lane == 0) {
+    const unsigned long long *done = job_desc(A, tag) + 3;
+    while (ld_acq64(done) < nch) __nanosleep(64);
+    __threadfence();
+    const Lat &lat = A.lat;
+    View v{A, pos};
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    const uint32_t hi = ~tag;
+    int64_t root = -1;
+    r = 1;
+    for (int k = 0; k < 27; ++k) {
+      if (k == 13) continue;
+      const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+      const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+      const int64_t g = lat.flat(zz, yy, xx);
+      if (v.lab(g) != a) continue;
+      const int64_t rg = job_find(A.ufp, hi, (uint32_t)g);
+      if (root < 0) root = rg;
+      else if (rg != root) r = 2;
+    }
+  }
+  return __shfl_sync(0xffffffffu, r, 0);
+}
+
+// Warp-level wait until every lane's site g (or -1) has no candidate before
+// pos pending; helps the current job meanwhile.
+__device__ __forceinline__ void warp_wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
   int ns = 32;
-  while (ld_acq(A.pend + g) < pos) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+  for (;;) {
+    const bool p = g >= 0 && ld_acq(A.pend + g) < pos;
+    if (!__any_sync(0xffffffffu, p)) break;
+    if (!warp_help(A)) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+    }
   }
 }
 
@@ -1005,7 +1193,7 @@ struct WarpBfs {
   int nfr[2];
   int par[27], gcount[27];
   uint32_t unions[27];
-  int nseed, ninsert, blocked, overflow, result;
+  int nseed, ninsert, blocked, overflow, result, levels;
   int64_t bsite;
 };
 
@@ -1046,6 +1234,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   if (lane == 0) {
     S.blocked = S.overflow = 0;
     S.result = -1;
+    S.levels = 0;
     S.nfr[0] = S.nfr[1] = 0;
     auto put = [&](uint32_t site, int g) {
       uint32_t h = hash32(site) & (kHW - 1);
@@ -1104,7 +1293,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
                 S.overflow = 1;
               }
               atomicAdd(&S.gcount[g], 1);
-              if (atomicAdd(&S.ninsert, 1) >= kMaxInsertW) S.overflow = 1;
+              if (atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
               break;
             }
             cv = old;
@@ -1122,6 +1311,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
     if (lane == 0) {
       S.result = warp_level_verdict(S);
       S.nfr[cur] = 0;
+      S.levels += 1;
     }
     __syncwarp();
     const int r = S.result;
@@ -1131,120 +1321,174 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   }
 }
 
-// Unbounded fallback (overflowing footprints) with global stamps/frontiers.
-// Run only by the candidate at the low-water mark (every earlier candidate is
-// decided), so it never meets a pending site and at most one runs at a time.
-__device__ int warp_global_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
+// Second tier for footprints beyond the hash (2-D): the same multi-source
+// BFS with the visited set as a 4-bit group map over label a's bounding box
+// (grown by one site; every a-site of any view V_i lies inside it), held in
+// the hash's shared memory: up to 2 * 8 * kHW sites.  Unbounded in footprint
+// within the box, so it needs no low-water mark; only frontiers wider than
+// kFW or boxes beyond capacity fall through (3) to the assist job.
+__device__ int warp_bfs_box(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
   const Lat &lat = A.lat;
   const int lane = threadIdx.x & 31;
+  if (lat.ndim != 2) return 3;
+  const int32_t *bx = A.lbox + 4 * a;
+  const int64_t r0 = bx[0] > 0 ? bx[0] - 1 : 0, r1 = bx[1] + 1 < lat.ny ? bx[1] + 1 : lat.ny - 1;
+  const int64_t c0 = bx[2] > 0 ? bx[2] - 1 : 0, c1 = bx[3] + 1 < lat.nx ? bx[3] + 1 : lat.nx - 1;
+  const int64_t bw = c1 - c0 + 1, nbox = (r1 - r0 + 1) * bw;
+  if (nbox > (int64_t)A.box_cap) return 3;
+  uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
+  const int nw = (int)((nbox + 7) >> 3);
+  for (int k = lane; k < nw; k += 32) nib[k] = 0;
   View v{A, pos};
-  __shared__ unsigned long long gnf[kDfWarps][2];
-  unsigned long long *nf = gnf[(threadIdx.x >> 5) % kDfWarps];
-  uint32_t ep = 0;
+  auto idx = [&](int64_t t) -> int64_t {
+    const int64_t r = t / lat.nx - r0, c = t % lat.nx - c0;
+    return (r < 0 || c < 0 || c >= bw || r > r1 - r0) ? -1 : r * bw + c;
+  };
+  __syncwarp();
   if (lane == 0) {
-    __threadfence();
-    ep = *(volatile uint32_t *)A.epoch;
-    *(volatile uint32_t *)A.epoch = ep + 32;
     S.blocked = S.overflow = 0;
     S.result = -1;
+    S.levels = 0;
+    S.nfr[0] = S.nfr[1] = 0;
     int64_t z, y, x;
     lat.coord(f, z, y, x);
-    A.vis[f] = ep + 31;
     int ns = 0;
-    for (int k = 0; k < 27; ++k) {
+    for (int k = 9; k < 18; ++k) {
       if (k == 13) continue;
-      int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-      int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-      int64_t g = lat.flat(zz, yy, xx);
+      const int dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
+      const int64_t yy = y + dy, xx = x + dx;
+      if (!lat.inb(0, yy, xx)) continue;
+      const int64_t g = lat.flat(0, yy, xx);
       if (v.lab(g) != a) continue;
-      A.vis[g] = ep + ns;
-      A.gq[0][ns] = (uint32_t)g;
+      const int64_t li = idx(g);
+      if (li < 0) {
+        S.overflow = 1;  // cannot happen: a-sites lie in the box
+        continue;
+      }
+      nib[li >> 3] |= (uint32_t)(ns + 1) << (4 * (li & 7));
+      S.fr[0][ns] = (uint32_t)g;
+      S.fg[0][ns] = (uint8_t)ns;
       S.par[ns] = ns;
       S.gcount[ns] = 0;
       S.unions[ns] = 0;
       ++ns;
     }
     S.nseed = ns;
-    nf[0] = ns;
-    nf[1] = 0;
+    S.nfr[0] = ns;
   }
-  ep = __shfl_sync(0xffffffffu, ep, 0);
   __syncwarp();
-  __threadfence();
-  int cur = 0, r;
+  int cur = 0;
   for (;;) {
-    const unsigned long long n = nf[cur];
-    const int nxt = cur ^ 1;
-    for (unsigned long long j = lane; j < n; j += 32) {
-      const uint32_t s = __ldcg(A.gq[cur] + j);
-      const int g = (int)(__ldcg(A.vis + s) - ep);
-      int64_t z, y, x;
-      lat.coord(s, z, y, x);
-      for (int k = 0; k < 27; ++k) {
-        if (k == 13) continue;
-        int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-        int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-        if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-        int64_t t = lat.flat(zz, yy, xx);
-        int32_t pm;
-        const int32_t lt = v.lab_pend(t, pm);
-        if (pm < pos && t != f) {
+    const int n = S.nfr[cur], nxt = cur ^ 1;
+    for (int j = lane; j < n; j += 32) {
+      const uint32_t s = S.fr[cur][j];
+      const int g = S.fg[cur][j];
+      scan_nbrs(v, lat, s, f, [&](int64_t t, int32_t lt, int32_t pm) {
+        if (pm < pos) {
           S.blocked = 1;
           S.bsite = t;
-          continue;
+          return;
         }
-        if (lt != a) continue;
-        uint32_t cv = __ldcg(A.vis + t);
+        if (lt != a) return;
+        const int64_t li = idx(t);
+        if (li < 0) {
+          S.overflow = 1;
+          return;
+        }
+        uint32_t *wp = nib + (li >> 3);
+        const int sh = 4 * (int)(li & 7);
+        uint32_t w = *(volatile uint32_t *)wp;
         for (;;) {
-          if (cv >= ep && cv < ep + 32) {
-            int h = (int)(cv - ep);
-            if (h != 31 && h != g) atomicOr(&S.unions[g], 1u << h);
+          const int cg = (int)((w >> sh) & 15u);
+          if (cg != 0) {
+            if (cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
             break;
           }
-          uint32_t old = atomicCAS(A.vis + t, cv, ep + (uint32_t)g);
-          if (old == cv) {
-            unsigned long long idx = atomicAdd(&nf[nxt], 1ull);
-            A.gq[nxt][idx] = (uint32_t)t;
+          const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
+          if (old == w) {
+            const int k = atomicAdd(&S.nfr[nxt], 1);
+            if (k < kFW) {
+              S.fr[nxt][k] = (uint32_t)t;
+              S.fg[nxt][k] = (uint8_t)g;
+            } else {
+              S.overflow = 1;
+            }
             atomicAdd(&S.gcount[g], 1);
             break;
           }
-          cv = old;
+          w = old;
         }
-      }
+      });
     }
     __syncwarp();
-    __threadfence();
     if (lane == 0) {
       S.result = warp_level_verdict(S);
-      nf[cur] = 0;
+      S.nfr[cur] = 0;
+      S.levels += 1;
     }
     __syncwarp();
-    r = S.result;
+    const int r = S.result;
     __syncwarp();
-    if (r >= 0) break;
+    if (r >= 0) return r;
     cur = nxt;
   }
-  __syncwarp();
-  return r;
+}
+
+__device__ __forceinline__ int first_zero_byte(uint32_t w) {
+  const uint32_t z = (w - 0x01010101u) & ~w & 0x80808080u;  // exact for the lowest zero byte
+  return z ? (__ffs(z) - 1) >> 3 : 4;
 }
 
 // Wait until every position before pos is decided (the candidate is the
-// earliest undecided).  Only overflowing BFS candidates wait here, so the scan
-// over dec[] is done lazily by the waiter, starting from a shared hint
-// (ctl[13]) that waiters push forward.
-__device__ __forceinline__ void wait_lowmark(const ParArgs &A, int32_t pos) {
-  int32_t m = ld_acq(A.ctl + 13);
+// earliest undecided; whole warp), helping assist jobs meanwhile.  The scan
+// of dec[] starts from a shared low-water hint (ctl[13]) that waiters push
+// forward; each step reads 512 decisions, 16 per lane.
+__device__ __forceinline__ void warp_wait_lowmark(const ParArgs &A, int32_t pos) {
+  const int lane = threadIdx.x & 31;
   int ns = 64;
-  while (m < pos) {
-    while (m < pos && *(volatile uint8_t *)(A.dec + m) != UNDEC) ++m;
-    atomicMax(A.ctl + 13, m);
-    if (m < pos) {
+  int32_t m = __shfl_sync(0xffffffffu, lane == 0 ? ld_acq(A.ctl + 13) : 0, 0);
+  for (;;) {
+    while (m < pos) {
+      const int32_t base = m & ~15;
+      const int32_t lo = base + 16 * lane;
+      int first = 16;  // first undecided offset in this lane's 16 positions
+      if (lo + 16 <= pos) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(A.dec + lo));
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 3; k >= 0; --k) {
+          const int b = first_zero_byte(w4[k]);
+          if (b < 4) first = 4 * k + b;
+        }
+      } else {
+        for (int k = 0; k < 16 && lo + k < pos; ++k)
+          if (*(volatile uint8_t *)(A.dec + lo + k) == UNDEC) {
+            first = k;
+            break;
+          }
+      }
+      // positions below m are known decided
+      if (lo + first < m) first = 16;
+      const unsigned bal = __ballot_sync(0xffffffffu, first < 16);
+      if (bal) {
+        const int l = __ffs(bal) - 1;
+        m = __shfl_sync(0xffffffffu, lo + first, l);
+        break;
+      }
+      m = base + 512;
+    }
+    if (m > pos) m = pos;
+    if (lane == 0) atomicMax(A.ctl + 13, m);
+    if (m >= pos) break;
+    if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 1024) ns <<= 1;
     }
+    const int32_t h = __shfl_sync(0xffffffffu, lane == 0 ? ld_acq(A.ctl + 13) : 0, 0);
+    if (h > m) m = h;
   }
   __threadfence();
+  __syncwarp();
 }
 
 __global__ void k_df_init(ParArgs A, int64_t N) {
@@ -1255,6 +1499,8 @@ __global__ void k_df_init(ParArgs A, int64_t N) {
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride) {
     A.cnt0[l] = A.cnt[l];
     A.nown[l] = 0;
+    A.lbox[4 * l + 0] = A.lbox[4 * l + 2] = kInf;
+    A.lbox[4 * l + 1] = A.lbox[4 * l + 3] = -1;
   }
   if (blockIdx.x == 0 && threadIdx.x < 16) A.ctl[threadIdx.x] = 0;
   (void)M;
@@ -1270,6 +1516,40 @@ __global__ void k_df_init2(ParArgs A) {
     atomicMin(A.pend + A.px[p], (int32_t)pos);
     const int32_t a = A.pown[p];
     if (a > 0) atomicAdd(A.nown + a, 1);
+  }
+}
+
+// Per-label bounding boxes of the iteration-start raster (2-D).  A region's
+// extreme rows/columns are attained at sites that are either on the image
+// border or have a face neighbour of another label, i.e. are particles, so
+// the particle list plus the border sites give the exact box.
+__device__ __forceinline__ void bbox_add(const ParArgs &A, int32_t l, int64_t y) {
+  if (l <= 0) return;
+  const int32_t r = (int32_t)(y / A.lat.nx), c = (int32_t)(y % A.lat.nx);
+  int32_t *b = A.lbox + 4 * l;
+  atomicMin(b + 0, r);
+  atomicMax(b + 1, r);
+  atomicMin(b + 2, c);
+  atomicMax(b + 3, c);
+}
+
+__global__ void k_df_bbox(ParArgs A, int64_t N) {
+  const int64_t nx = A.lat.nx, ny = A.lat.ny, nb = 2 * (nx + ny);
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N + nb; i += stride) {
+    if (i < N) {
+      // one update per site: the first particle of the site
+      const int64_t y = A.px[i];
+      if (A.site_off[y] == (uint32_t)i) bbox_add(A, A.pown[i], y);
+      continue;
+    }
+    const int64_t j = i - N;
+    int64_t y;
+    if (j < nx) y = j;                                   // top row
+    else if (j < 2 * nx) y = (ny - 1) * nx + (j - nx);   // bottom row
+    else if (j < 2 * nx + ny) y = (j - 2 * nx) * nx;     // left column
+    else y = (j - 2 * nx - ny) * nx + nx - 1;            // right column
+    bbox_add(A, A.L[y], y);
   }
 }
 
@@ -1314,12 +1594,20 @@ __global__ void k_df_labcsr(const uint32_t *__restrict__ key, int32_t *__restric
   }
 }
 
-__device__ __forceinline__ void df_wait_label(const ParArgs &A, int32_t l, int32_t pos) {
+// Wait (whole warp) until small label l's next event is position pos.
+__device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int32_t pos) {
+  const int lane = threadIdx.x & 31;
   int ns = 32;
-  while (A.lab_pos[ld_acq(A.lab_ptr + l)] != pos) {
-    __nanosleep(ns);
-    if (ns < 512) ns <<= 1;
+  for (;;) {
+    int ok = 0;
+    if (lane == 0) ok = A.lab_pos[ld_acq(A.lab_ptr + l)] == pos;
+    if (__shfl_sync(0xffffffffu, ok, 0)) break;
+    if (!warp_help(A)) {
+      __nanosleep(ns);
+      if (ns < 512) ns <<= 1;
+    }
   }
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
@@ -1335,35 +1623,35 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     __syncwarp();
     const int32_t pos = wpos[wid];
     __syncwarp();
-    if (pos >= M) break;
+    if (pos >= M) {
+      // keep helping assist jobs until every candidate is decided
+      warp_wait_lowmark(A, M);
+      break;
+    }
     if (A.tdbg && lane == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      A.tdbg[2 * pos] = (long long)t;
+      A.tdbg[4 * pos] = (long long)t;
     }
     const uint32_t p = A.order[pos];
     const int64_t f = A.px[p];
     const int32_t a = A.pown[p], b = A.pcomp[p];
     const bool sa = A.small[a], sb = A.small[b];
-    if (lane == 0) {
-      if (sa) df_wait_label(A, a, pos);
-      if (sb) df_wait_label(A, b, pos);
-    }
-    __syncwarp();
+    if (sa) warp_wait_label(A, a, pos);
+    if (sb) warp_wait_label(A, b, pos);
     View v{A, pos};
     int64_t z, y, x;
     lat.coord(f, z, y, x);
     // the 3^d box, one cell per lane
     int32_t mine = -1;
+    int64_t gb = -1;
     if (lane < 27) {
       const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
       const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-      if (!(lat.ndim == 2 && dz != 0) && lat.inb(zz, yy, xx)) {
-        const int64_t g = lat.flat(zz, yy, xx);
-        wait_pend(A, g, pos);
-        mine = v.lab(g);
-      }
+      if (!(lat.ndim == 2 && dz != 0) && lat.inb(zz, yy, xx)) gb = lat.flat(zz, yy, xx);
     }
+    warp_wait_pend(A, gb, pos);
+    if (gb >= 0) mine = v.lab(gb);
     int32_t lab[27];
 #pragma unroll
     for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
@@ -1389,36 +1677,48 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
           how = 1;
       }
     }
+    if (A.tdbg && lane == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      A.tdbg[4 * pos + 2] = (long long)t;
+      A.tdbg[4 * pos + 3] = (long long)t;
+    }
     if (how == 1) {
       // exact window test (radius 5 in 2-D, 4 in 3-D), warp-cooperative:
       // lanes wait on and read disjoint cells, ballots collect the donor-label
       // bits, lane 0 floods and broadcasts the verdict
-      const int RB = lat.ndim == 2 ? 5 : 4, WB = 2 * RB + 1;
+      const int RB = lat.ndim == 2 ? (A.win_r ? A.win_r : 5) : 4, WB = 2 * RB + 1;
       const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
       uint32_t *bits = S.fr[0];
       for (int base = 0; base < nb; base += 32) {
         const int c = base + lane;
-        bool bit = false;
+        int64_t gw = -1;
         if (c < nb) {
           const int dz = lat.ndim == 2 ? 0 : c / (WB * WB) - RB;
           const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
           const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) {
-            const int64_t g = lat.flat(zz, yy, xx);
-            wait_pend(A, g, pos);
-            bit = v.lab(g) == a;
-          }
+          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) gw = lat.flat(zz, yy, xx);
         }
+        warp_wait_pend(A, gw, pos);
+        const bool bit = gw >= 0 && v.lab(gw) == a;
         const unsigned m = __ballot_sync(0xffffffffu, bit);
         if (lane == 0) bits[base >> 5] = m;
       }
       __syncwarp();
       if (lane == 0)
-        S.result = lat.ndim == 2 ? window_verdict_bits<5>(bits, 1) : window_verdict_bits<4>(bits, WB);
+        S.result = lat.ndim == 3 ? window_verdict_bits<4>(bits, WB)
+                   : RB == 3     ? window_verdict_bits<3>(bits, 1)
+                   : RB == 1     ? 0
+                                 : window_verdict_bits<5>(bits, 1);
       __syncwarp();
       const int wb = S.result;
       __syncwarp();
       dbg = 1000 + 100 * (wb + 2);
+      if (A.tdbg && lane == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        A.tdbg[4 * pos + 3] = (long long)t;
+      }
       if (wb == 2) {
         d = REJ;
       } else if (wb == 0) {
@@ -1430,24 +1730,40 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
           r = warp_bfs(A, S, pos, f, a);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
           if (r != 0) break;
-          if (lane == 0) {
-            atomicAdd(ctl + C_BLOCKED, 1);
-            wait_pend(A, S.bsite, pos);
-          }
-          __syncwarp();
+          if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
+          warp_wait_pend(A, lane == 0 ? S.bsite : -1, pos);
           dbg += 1;
         }
         if (r == 3) {
-          if (lane == 0) {
-            atomicAdd(ctl + C_DEFER, 1);
-            wait_lowmark(A, pos);
+          // footprint beyond the hash: the box-map tier, same retry rule
+          for (;;) {
+            r = warp_bfs_box(A, S, pos, f, a);
+            if (r != 0) break;
+            if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
+            warp_wait_pend(A, lane == 0 ? S.bsite : -1, pos);
+            dbg += 1;
           }
-          __syncwarp();
-          r = warp_global_bfs(A, S, pos, f, a);
+          dbg += 100000000;
+        }
+        if (r == 3) {
+          if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
+          warp_wait_lowmark(A, pos);
+          if (A.tdbg && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            A.tdbg[4 * pos + 2] = (long long)t;  // deferred: low-water mark reached
+          }
+          r = warp_job_owner(A, pos, f, a);
+          if (A.tdbg && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            A.tdbg[4 * pos + 3] = (long long)t;  // deferred: job answered
+          }
+          dbg += 1000000000;
           dbg += 2;
         }
         if (r == 2) d = REJ;
-        dbg += 10 * (r + 1);
+        dbg += 10 * (r + 1) + 10000 * (S.levels < 9999 ? S.levels : 9999);  // +1e8 box tier, +1e9 job
       } else if (wb != 1) {
         d = REJ;  // cannot happen after the waits; never accept unproven
       }
@@ -1464,7 +1780,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       if (A.tdbg) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        A.tdbg[2 * pos + 1] = (long long)t;
+        A.tdbg[4 * pos + 1] = (long long)t;
       }
       // release: the flip (newlab, w) and counts are visible before the
       // decision, the decision before the site's next pending position
@@ -2030,6 +2346,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (grid_blocks > 160) grid_blocks = 160;  // large-BFS slots
   }
   const int64_t N = X.n_particles;
+  if (A.max_insert <= 0 || A.max_insert > kMaxInsertW) A.max_insert = kMaxInsertW;
+  if (A.box_cap < 0 || A.box_cap > 16 * kHW) A.box_cap = 16 * kHW;
   void *args[] = {&A};
   if (X.accept_mode == 1) {
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_par, dim3(grid_blocks), dim3(512), args,
@@ -2051,6 +2369,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
+    k_df_bbox<<<grid_for(N + 2 * (A.lat.nx + A.lat.ny), 256), 256, 0, s>>>(A, N);
     RCB_TRY(X.evkey->reserve(2 * N, s));
     RCB_TRY(X.evkey2->reserve(2 * N, s));
     RCB_TRY(X.labpos->reserve(2 * N, s));

@@ -87,12 +87,16 @@ struct ParArgs {
   const uint32_t *site_off;  // K1 CSR (particles of a site)
   int32_t *lab_ptr;          // per small label: index of its next undecided event
   const int32_t *lab_pos;    // per small label: its candidates' positions, ascending
-  int32_t *gmutex;           // global-BFS fallback lock
+  int32_t *lbox;             // 2-D: per label (row min, row max, col min, col max)
   // large-footprint block BFS slots (one per block of k_accept_par)
   unsigned long long *bigkey;
   uint32_t *bigfr, *bigtag;
   uint8_t *bigfg;
-  long long *tdbg;  // RCB_PROFILE: per position (fetch, decide) globaltimer ns
+  long long *tdbg;  // RCB_PROFILE: per position (fetch, decide, box, window) globaltimer ns
+  int win_r;        // dataflow window radius in 2-D (0: default 5; 1: none)
+  int max_insert;   // dataflow warp-BFS footprint cap (0: default)
+  int box_cap;      // dataflow box-map BFS capacity in sites (-1: default, 0: off)
+  unsigned long long *job, *ufp;  // dataflow assist jobs (accept_par.cu)
 };
 
 struct ParExtra {

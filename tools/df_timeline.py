@@ -15,20 +15,21 @@ it_target = int(sys.argv[1]) if len(sys.argv) > 1 else 19
 sc = scenes.cfg2()
 eng = P.RegionCompetition(sc.image, sc.labels, P.EnergyConfig("ps", "poisson", smooth_radius=4),
                           P.SobolevParams(6.0), P.OptimizerConfig("sobolev", vanish_grace=5, drift_tolerance=1e-3))
-for _ in range(it_target):
+for _ in range(it_target - 1):
     eng.iterate()
+cnt0 = eng.model.stats.count.copy()
+eng.iterate()
 n = C.c_int64()
 cap = 400000
-t = np.zeros(2 * cap, np.int64)
+t = np.zeros(4 * cap, np.int64)
 part = np.zeros(cap, np.int32)
 code = np.zeros(cap, np.int32)
 P._lib.check(P._lib.lib.rcb_engine_debug_times(eng._h, P._lib.ptr(t), cap, C.byref(n)))
 P._lib.check(P._lib.lib.rcb_engine_debug_codes(eng._h, P._lib.ptr(part), P._lib.ptr(code), cap, C.byref(n)))
 m = n.value
-f, d = t[0:2 * m:2], t[1:2 * m:2]
+f, d, tb, tw = (t[k:4 * m:4] for k in range(4))
 t0 = f.min()
-f = (f - t0) / 1e3
-d = (d - t0) / 1e3
+f, d, tb, tw = ((u - t0) / 1e3 for u in (f, d, tb, tw))
 print("candidates", m, "span us", d.max(), "counters", eng.counters())
 lat = d - f
 print("decide-latency us: p50 %.1f p90 %.1f p99 %.1f max %.1f" % tuple(np.percentile(lat, [50, 90, 99, 100])))
@@ -40,3 +41,60 @@ print("slowest (pos, code, fetch, latency):")
 for p in slow:
     print(int(p), int(code[p]), round(f[p], 1), round(lat[p], 1))
 # how many candidates are decided after 50% of the span
+defer = code >= 1000000000
+code = code % 1000000000
+boxt = code >= 100000000
+print('box-tier candidates', int(boxt.sum()), 'deferred', int(defer.sum()))
+code = code % 100000000
+lv = code // 10000
+bfs = lv > 0
+print("BFS candidates", int(bfs.sum()), "levels p50/p90/p99/max", np.percentile(lv[bfs], [50, 90, 99, 100]) if bfs.any() else None)
+big = np.argsort(-lat)[:8]
+print("slowest: levels", [int(lv[p]) for p in big], "latency", [round(float(lat[p]), 1) for p in big])
+print("slowest phases (box wait, window wait, bfs):")
+for p in np.argsort(-lat)[:12]:
+    print("  pos", int(p), "box %.1f win %.1f bfs %.1f" % (tb[p] - f[p], tw[p] - tb[p], d[p] - tw[p]), "code", int(code[p]))
+late = np.argsort(-d)[:200]
+print("latest 200 mean phases: box %.1f win %.1f bfs %.1f" % ((tb - f)[late].mean(), (tw - tb)[late].mean(), (d - tw)[late].mean()))
+
+xs, ow, cm, rk = eng.last_candidates
+neg = rk < 0
+nown = np.bincount(ow[neg], minlength=len(cnt0))
+small = (np.arange(len(cnt0)) > 0) & (cnt0 - nown[:len(cnt0)] <= 1)
+pa, pb = ow[part[:m]], cm[part[:m]]
+inv = small[pa] | small[pb]
+print("small labels", int(small.sum()), "candidates involving them", int(inv.sum()))
+slow = np.argsort(-lat)[:40]
+print("slowest 40: involve small label:", int(inv[slow].sum()), " owner small:", int(small[pa][slow].sum()))
+late = d > np.quantile(d, 0.99)
+print("last 1%: involve small label", int(inv[late].sum()), "of", int(late.sum()))
+
+# inherent dependency depth: position p waits on every earlier position whose
+# pixel lies in p's 3x3 box (the minimum read set of the simple-point test)
+W = sc.image.shape[1]
+px = xs[part[:m]]
+best = {}
+depth = np.zeros(m, np.int32)
+for p in range(m):
+    x = int(px[p]); r, c = divmod(x, W)
+    dmax = 0
+    for dr in (-1, 0, 1):
+        for dc in (-1, 0, 1):
+            v = best.get((r + dr) * W + c + dc, 0)
+            if v > dmax:
+                dmax = v
+    depth[p] = dmax + 1
+    if depth[p] > best.get(x, 0):
+        best[x] = depth[p]
+print("box-dependency critical path", int(depth.max()), "p99", np.percentile(depth, 99))
+for q in (0.5, 0.9, 0.99, 1.0):
+    sel = d >= np.quantile(d, q) - 1e-9
+    print(f"decided at >= q{q}: mean depth {depth[sel].mean():.1f}")
+late = np.argsort(-d)[:10]
+print("latest decided: depth", [int(depth[p]) for p in late], "time", [round(float(d[p]), 1) for p in late])
+cc = np.corrcoef(depth, d)[0, 1]
+print("corr(depth, decide time)", round(float(cc), 3), " us per depth level", round(float(d.max() / depth.max()), 2))
+
+for p in np.nonzero(defer)[0]:
+    print("deferred pos %d fetch %.1f lowmark %.1f job %.1f decided %.1f (job us %.1f)" %
+          (p, f[p], tb[p], tw[p], d[p], tw[p] - tb[p]))
