@@ -458,7 +458,9 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
         RCB_TRY(e->tdbg.reserve(4 * n, s));
         P.tdbg = e->tdbg.p;
       }
-      if (lat.ndim == 2 && e->accept_mode != 1) {
+      // dataflow kernel: 2-D with sides < 2^16 (packed BFS coordinates)
+      const bool use_df = lat.ndim == 2 && e->accept_mode != 1 && lat.nx < 65536 && lat.ny < 65536;
+      if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufp.reserve(lat.V, s));
           RCB_TRY(e->job.reserve(64, s));
@@ -468,7 +470,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
         P.ufp = e->ufp.p;
         P.job = e->job.p;
       }
-      if (lat.ndim == 3 || e->accept_mode == 1) {
+      if (!use_df) {
         // slots for the round-based kernel's large-footprint BFS (<= 160 blocks)
         const size_t nb = 160;
         if (!e->bigkey.p) {
@@ -521,7 +523,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.evv = &e->evv;
       // 3-D: footprints of inconclusive topology tests often exceed a warp's
       // hash; the round-based kernel's block BFS handles them
-      X.accept_mode = (e->accept_mode == 1 || lat.ndim == 3) ? 1 : 0;
+      X.accept_mode = use_df ? 0 : 1;
       X.labkey = &e->labkey;
       X.labkey2 = &e->labkey2;
       X.labpos = &e->labpos;

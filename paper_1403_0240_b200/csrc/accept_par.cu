@@ -979,6 +979,16 @@ static constexpr int kFW = 256;   // warp BFS frontier capacity
 static constexpr int kMaxInsertW = kHW * 5 / 8;
 static constexpr int kDfWarps = 16;
 
+// Polls use relaxed L2 loads; the waiter orders its later reads with one
+// acquire fence once the condition holds (fence-based synchronisation with the
+// publisher's release store).  An acquire load per poll would hit L2 with
+// ordering traffic from thousands of spinning warps.
+__device__ __forceinline__ int32_t ld_rlx(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1062,7 +1072,7 @@ __device__ bool warp_help(const ParArgs &A) {
   unsigned long long c = 0, desc[6] = {0, 0, 0, 0, 0, 0};
   int got = 0;
   if (lane == 0) {
-    c = ld_acq64(A.job);
+    c = __ldcg(A.job);  // relaxed peek; the claim below is an acquire RMW
     if ((c >> 32) != 0 && (uint32_t)c < (uint32_t)__ldcg(A.job + 2)) {  // tag 0: none yet
       asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], 1;" : "=l"(c) : "l"(A.job) : "memory");
       const unsigned long long *d = job_desc(A, (uint32_t)(c >> 32));
@@ -1177,89 +1187,143 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
 __device__ __forceinline__ void warp_wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
   int ns = 32;
   for (;;) {
-    const bool p = g >= 0 && ld_acq(A.pend + g) < pos;
+    const bool p = g >= 0 && ld_rlx(A.pend + g) < pos;
     if (!__any_sync(0xffffffffu, p)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
-      if (ns < 256) ns <<= 1;
+      if (ns < 512) ns <<= 1;
     }
   }
+  fence_acq();
 }
 
 struct WarpBfs {
-  unsigned long long key[kHW];
-  uint32_t fr[2][kFW];
-  uint8_t fg[2][kFW];
+  unsigned long long key[kHW];  // hash tier: (site << 8 | group); box tier: 4-bit map
+  uint32_t fr[2][kFW];          // frontier sites, packed (y << 16 | x)
+  uint8_t fg[2][kFW];           // their seed groups
   int nfr[2];
-  int par[27], gcount[27];
-  uint32_t unions[27];
-  int nseed, ninsert, blocked, overflow, result, levels;
+  uint32_t unions[8];           // groups met by each group this level
+  uint32_t alive;               // groups that inserted a site this level
+  uint32_t gblk;                // groups that met a pending site (sticky)
+  int nseed, ninsert, overflow, result, levels;
+  unsigned long long comp;      // byte g = component mask of group g
   int64_t bsite;
 };
 
-__device__ int warp_level_verdict(WarpBfs &S) {
-  if (S.blocked) return 0;
-  if (S.overflow) return 3;
-  for (int g = 0; g < S.nseed; ++g)
-    for (uint32_t m = S.unions[g]; m; m &= m - 1) {
-      int h = __ffs(m) - 1;
-      int rg = uf_root(S.par, g), rh = uf_root(S.par, h);
-      if (rg != rh) S.par[rh] = rg;
-    }
-  int roots = 0, rc[27];
-  for (int g = 0; g < S.nseed; ++g) {
-    S.unions[g] = 0;
-    rc[g] = 0;
-  }
-  for (int g = 0; g < S.nseed; ++g) {
-    int r = uf_root(S.par, g);
-    if (r == g) ++roots;
-    rc[r] += S.gcount[g];
-    S.gcount[g] = 0;
-  }
-  if (roots == 1) return 1;
-  for (int g = 0; g < S.nseed; ++g)
-    if (uf_root(S.par, g) == g && rc[g] == 0) return 2;
-  return -1;
+// ---------------------------------------------------------------------------
+// Warp BFS of the dataflow kernel (2-D, sides < 2^16): the pieces question
+// of block_bfs -- do the a-sites of x's box (the seed groups, <= 8) stay in
+// one 8-connected piece of a \ {x} in the view V_pos? -- answered by a
+// multi-source BFS, one frontier site per lane, 32-bit neighbour arithmetic.
+// Pending sites (an earlier candidate there is undecided) are skipped as if
+// not in a, and each group that met one is flagged in gblk: seeds joined
+// through settled a-sites are joined in every completion of the view, so one
+// component is final (1); a component that ran out of sites without meeting
+// a pending site is final too (2); one that ran out but met one waits (0).
+// The visited set is either
+//   kBox:  a 4-bit group map over a's bounding box grown by one site (every
+//          a-site of any V_i lies in it: a site can only flip into a if it
+//          was face-adjacent to a), direct index, up to 16 * kHW sites; or
+//   hash:  open addressing on the site index, at most max_insert sites.
+// Returns 0 wait (S.bsite pending), 1 one piece, 2 several, 3 overflow.
+// ---------------------------------------------------------------------------
+struct BfsBox {
+  int r0, c0, bh, bw;  // grown bounding box of a
+};
+
+__device__ __forceinline__ int comp_of(unsigned long long C, int g) {
+  return (int)((C >> (8 * g)) & 0xffu);
 }
 
-// Warp-cooperative pieces BFS (same question as block_bfs).  Returns 0 blocked
-// (S.bsite = a pending site), 1 one piece, 2 several, 3 overflow.
-__device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
-  const Lat &lat = A.lat;
+// lane 0: fold this level's unions into the components and decide
+__device__ int warp_verdict8(WarpBfs &S) {
+  if (S.overflow) return 3;
+  unsigned long long C = S.comp;
+  const int ns = S.nseed;
+  for (int g = 0; g < ns; ++g) {
+    uint32_t m = S.unions[g];
+    S.unions[g] = 0;
+    while (m) {
+      const int h = __ffs(m) - 1;
+      m &= m - 1;
+      const int mg = comp_of(C, g), mh = comp_of(C, h);
+      if (mg & (1 << h)) continue;
+      const int u = mg | mh;
+      for (int q = u; q; q &= q - 1) {
+        const int i = __ffs(q) - 1;
+        C = (C & ~(0xffull << (8 * i))) | ((unsigned long long)u << (8 * i));
+      }
+    }
+  }
+  S.comp = C;
+  const int all = (1 << ns) - 1;
+  if (comp_of(C, 0) == all) return 1;
+  const uint32_t alive = S.alive;
+  S.alive = 0;
+  int res = -1, seen = 0;
+  for (int g = 0; g < ns; ++g) {
+    if (seen & (1 << g)) continue;
+    const int m = comp_of(C, g);
+    seen |= m;
+    if ((m & alive) == 0) {
+      if ((m & S.gblk) == 0) return 2;
+      res = 0;
+    }
+  }
+  return res;
+}
+
+template <bool kBox>
+__device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
+                          uint32_t seedmask, const BfsBox bb) {
   const int lane = threadIdx.x & 31;
-  View v{A, pos};
-  for (int k = lane; k < kHW; k += 32) S.key[k] = kEmpty;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
+  const int fy = (int)(f / nx), fx = (int)(f % nx);
+  const int32_t *__restrict__ Wp = A.w, *__restrict__ Lp = A.L, *__restrict__ Pp = A.pend,
+                              *__restrict__ Np = A.newlab;
+  uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
+  if (kBox) {
+    const int nw = (bb.bh * bb.bw + 7) >> 3;
+    for (int k = lane; k < nw; k += 32) nib[k] = 0;
+  } else {
+    for (int k = lane; k < kHW; k += 32) S.key[k] = kEmpty;
+  }
   __syncwarp();
   if (lane == 0) {
-    S.blocked = S.overflow = 0;
+    S.gblk = 0;
+    S.alive = 0;
+    S.overflow = 0;
     S.result = -1;
     S.levels = 0;
-    S.nfr[0] = S.nfr[1] = 0;
-    auto put = [&](uint32_t site, int g) {
-      uint32_t h = hash32(site) & (kHW - 1);
-      while (S.key[h] != kEmpty) h = (h + 1) & (kHW - 1);
-      S.key[h] = ((unsigned long long)site << 8) | (unsigned)g;
-    };
-    put((uint32_t)f, 255);
-    int64_t z, y, x;
-    lat.coord(f, z, y, x);
+    S.nfr[1] = 0;
+    if (kBox) {
+      const int li = (fy - bb.r0) * bb.bw + (fx - bb.c0);
+      nib[li >> 3] |= 15u << (4 * (li & 7));  // x itself: never entered
+    } else {
+      uint32_t h = hash32((uint32_t)f) & (kHW - 1);
+      S.key[h] = ((unsigned long long)(uint32_t)f << 8) | 255u;
+    }
     int ns = 0;
-    for (int k = 0; k < 27; ++k) {
-      if (k == 13) continue;
-      int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-      int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
-      int64_t g = lat.flat(zz, yy, xx);
-      if (v.lab(g) != a) continue;
-      put((uint32_t)g, ns);
-      S.fr[0][ns] = (uint32_t)g;
+    unsigned long long C = 0;
+    for (int k = 0; k < 9; ++k) {
+      if (!((seedmask >> k) & 1u)) continue;
+      const int yy = fy + k / 3 - 1, xx = fx + k % 3 - 1;
+      if (kBox) {
+        const int li = (yy - bb.r0) * bb.bw + (xx - bb.c0);
+        nib[li >> 3] |= (uint32_t)(ns + 1) << (4 * (li & 7));
+      } else {
+        const uint32_t site = (uint32_t)(yy * nx + xx);
+        uint32_t h = hash32(site) & (kHW - 1);
+        while (S.key[h] != kEmpty) h = (h + 1) & (kHW - 1);
+        S.key[h] = ((unsigned long long)site << 8) | (unsigned)ns;
+      }
+      S.fr[0][ns] = ((uint32_t)yy << 16) | (uint32_t)xx;
       S.fg[0][ns] = (uint8_t)ns;
-      S.par[ns] = ns;
-      S.gcount[ns] = 0;
       S.unions[ns] = 0;
+      C |= (unsigned long long)(1u << ns) << (8 * ns);
       ++ns;
     }
+    S.comp = C;
     S.nseed = ns;
     S.nfr[0] = ns;
     S.ninsert = ns + 1;
@@ -1269,47 +1333,126 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   for (;;) {
     const int n = S.nfr[cur], nxt = cur ^ 1;
     for (int j = lane; j < n; j += 32) {
-      const uint32_t s = S.fr[cur][j];
+      const uint32_t e = S.fr[cur][j];
       const int g = S.fg[cur][j];
-      scan_nbrs(v, lat, s, f, [&](int64_t t, int32_t lt, int32_t pm) {
-        if (pm < pos) {
-          S.blocked = 1;
-          S.bsite = t;
-          return;
-        }
-        if (lt != a) return;
-        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
-        for (;;) {
-          unsigned long long cv = S.key[h];
-          if (cv == kEmpty) {
-            unsigned long long mine = ((unsigned long long)t << 8) | (unsigned)g;
-            unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
-            if (old == kEmpty) {
-              int idx = atomicAdd(&S.nfr[nxt], 1);
-              if (idx < kFW) {
-                S.fr[nxt][idx] = (uint32_t)t;
-                S.fg[nxt][idx] = (uint8_t)g;
-              } else {
-                S.overflow = 1;
-              }
-              atomicAdd(&S.gcount[g], 1);
-              if (atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
+      const int y = (int)(e >> 16), x = (int)(e & 0xffffu);
+      uint32_t met = 0;  // groups met (unions)
+      bool blk = false, grew = false;
+      int t[8], li[8];
+      bool ok[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int dy = k < 3 ? -1 : (k < 5 ? 0 : 1);
+        const int dx = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
+        const int yy = y + dy, xx = x + dx;
+        ok[k] = (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+        t[k] = yy * nx + xx;
+        li[k] = 0;
+        if (kBox) {
+          const int ry = yy - bb.r0, rx = xx - bb.c0;
+          // outside the grown box: never an a-site
+          ok[k] = ok[k] && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
+          li[k] = ry * bb.bw + rx;
+          if (ok[k]) {
+            const int cg = (int)((nib[li[k] >> 3] >> (4 * (li[k] & 7))) & 15u);
+            if (cg) {
+              if (cg != 15 && cg - 1 != g) met |= 1u << (cg - 1);
+              ok[k] = false;
+            }
+          }
+        } else if (ok[k]) {
+          uint32_t h = hash32((uint32_t)t[k]) & (kHW - 1);
+          for (;;) {
+            const unsigned long long cv = S.key[h];
+            if (cv == kEmpty) break;
+            if ((uint32_t)(cv >> 8) == (uint32_t)t[k]) {
+              const int hg = (int)(cv & 0xff);
+              if (hg != 255 && hg != g) met |= 1u << hg;
+              ok[k] = false;
               break;
             }
-            cv = old;
+            h = (h + 1) & (kHW - 1);
           }
-          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
-            int hg = (int)(cv & 0xff);
-            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
-            break;
-          }
-          h = (h + 1) & (kHW - 1);
         }
-      });
+      }
+      int32_t wv[8], l0[8], pm[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wv[k] = ok[k] ? __ldcg(Wp + t[k]) : 0x7fffffff;
+        l0[k] = ok[k] ? __ldg(Lp + t[k]) : -1;
+        pm[k] = ok[k] ? __ldcg(Pp + t[k]) : 0x7fffffff;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (!ok[k]) continue;
+        if (pm[k] < pos) {
+          blk = true;
+          S.bsite = t[k];
+          continue;
+        }
+        const int32_t lab = wv[k] < pos ? __ldcg(Np + t[k]) : l0[k];
+        if (lab != a) continue;
+        const int dy = k < 3 ? -1 : (k < 5 ? 0 : 1);
+        const int dx = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
+        const uint32_t pk = ((uint32_t)(y + dy) << 16) | (uint32_t)(x + dx);
+        bool ins = false;
+        if (kBox) {
+          uint32_t *wp = nib + (li[k] >> 3);
+          const int sh = 4 * (li[k] & 7);
+          uint32_t w = *(volatile uint32_t *)wp;
+          for (;;) {
+            const int cg = (int)((w >> sh) & 15u);
+            if (cg) {
+              if (cg != 15 && cg - 1 != g) met |= 1u << (cg - 1);
+              break;
+            }
+            const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
+            if (old == w) {
+              ins = true;
+              break;
+            }
+            w = old;
+          }
+        } else {
+          uint32_t h = hash32((uint32_t)t[k]) & (kHW - 1);
+          const unsigned long long mine = ((unsigned long long)(uint32_t)t[k] << 8) | (unsigned)g;
+          for (;;) {
+            unsigned long long cv = S.key[h];
+            if (cv == kEmpty) {
+              const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
+              if (old == kEmpty) {
+                ins = true;
+                break;
+              }
+              cv = old;
+            }
+            if ((uint32_t)(cv >> 8) == (uint32_t)t[k]) {
+              const int hg = (int)(cv & 0xff);
+              if (hg != 255 && hg != g) met |= 1u << hg;
+              break;
+            }
+            h = (h + 1) & (kHW - 1);
+          }
+          if (ins && atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
+        }
+        if (ins) {
+          grew = true;
+          const int q = atomicAdd(&S.nfr[nxt], 1);
+          if (q < kFW) {
+            S.fr[nxt][q] = pk;
+            S.fg[nxt][q] = (uint8_t)g;
+          } else {
+            S.overflow = 1;
+          }
+        }
+      }
+      if (met) atomicOr(&S.unions[g], met);
+      if (grew) atomicOr(&S.alive, 1u << g);
+      if (blk) atomicOr(&S.gblk, 1u << g);
     }
     __syncwarp();
     if (lane == 0) {
-      S.result = warp_level_verdict(S);
+      S.result = warp_verdict8(S);
       S.nfr[cur] = 0;
       S.levels += 1;
     }
@@ -1321,118 +1464,6 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   }
 }
 
-// Second tier for footprints beyond the hash (2-D): the same multi-source
-// BFS with the visited set as a 4-bit group map over label a's bounding box
-// (grown by one site; every a-site of any view V_i lies inside it), held in
-// the hash's shared memory: up to 2 * 8 * kHW sites.  Unbounded in footprint
-// within the box, so it needs no low-water mark; only frontiers wider than
-// kFW or boxes beyond capacity fall through (3) to the assist job.
-__device__ int warp_bfs_box(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a) {
-  const Lat &lat = A.lat;
-  const int lane = threadIdx.x & 31;
-  if (lat.ndim != 2) return 3;
-  const int32_t *bx = A.lbox + 4 * a;
-  const int64_t r0 = bx[0] > 0 ? bx[0] - 1 : 0, r1 = bx[1] + 1 < lat.ny ? bx[1] + 1 : lat.ny - 1;
-  const int64_t c0 = bx[2] > 0 ? bx[2] - 1 : 0, c1 = bx[3] + 1 < lat.nx ? bx[3] + 1 : lat.nx - 1;
-  const int64_t bw = c1 - c0 + 1, nbox = (r1 - r0 + 1) * bw;
-  if (nbox > (int64_t)A.box_cap) return 3;
-  uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
-  const int nw = (int)((nbox + 7) >> 3);
-  for (int k = lane; k < nw; k += 32) nib[k] = 0;
-  View v{A, pos};
-  auto idx = [&](int64_t t) -> int64_t {
-    const int64_t r = t / lat.nx - r0, c = t % lat.nx - c0;
-    return (r < 0 || c < 0 || c >= bw || r > r1 - r0) ? -1 : r * bw + c;
-  };
-  __syncwarp();
-  if (lane == 0) {
-    S.blocked = S.overflow = 0;
-    S.result = -1;
-    S.levels = 0;
-    S.nfr[0] = S.nfr[1] = 0;
-    int64_t z, y, x;
-    lat.coord(f, z, y, x);
-    int ns = 0;
-    for (int k = 9; k < 18; ++k) {
-      if (k == 13) continue;
-      const int dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-      const int64_t yy = y + dy, xx = x + dx;
-      if (!lat.inb(0, yy, xx)) continue;
-      const int64_t g = lat.flat(0, yy, xx);
-      if (v.lab(g) != a) continue;
-      const int64_t li = idx(g);
-      if (li < 0) {
-        S.overflow = 1;  // cannot happen: a-sites lie in the box
-        continue;
-      }
-      nib[li >> 3] |= (uint32_t)(ns + 1) << (4 * (li & 7));
-      S.fr[0][ns] = (uint32_t)g;
-      S.fg[0][ns] = (uint8_t)ns;
-      S.par[ns] = ns;
-      S.gcount[ns] = 0;
-      S.unions[ns] = 0;
-      ++ns;
-    }
-    S.nseed = ns;
-    S.nfr[0] = ns;
-  }
-  __syncwarp();
-  int cur = 0;
-  for (;;) {
-    const int n = S.nfr[cur], nxt = cur ^ 1;
-    for (int j = lane; j < n; j += 32) {
-      const uint32_t s = S.fr[cur][j];
-      const int g = S.fg[cur][j];
-      scan_nbrs(v, lat, s, f, [&](int64_t t, int32_t lt, int32_t pm) {
-        if (pm < pos) {
-          S.blocked = 1;
-          S.bsite = t;
-          return;
-        }
-        if (lt != a) return;
-        const int64_t li = idx(t);
-        if (li < 0) {
-          S.overflow = 1;
-          return;
-        }
-        uint32_t *wp = nib + (li >> 3);
-        const int sh = 4 * (int)(li & 7);
-        uint32_t w = *(volatile uint32_t *)wp;
-        for (;;) {
-          const int cg = (int)((w >> sh) & 15u);
-          if (cg != 0) {
-            if (cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
-            break;
-          }
-          const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
-          if (old == w) {
-            const int k = atomicAdd(&S.nfr[nxt], 1);
-            if (k < kFW) {
-              S.fr[nxt][k] = (uint32_t)t;
-              S.fg[nxt][k] = (uint8_t)g;
-            } else {
-              S.overflow = 1;
-            }
-            atomicAdd(&S.gcount[g], 1);
-            break;
-          }
-          w = old;
-        }
-      });
-    }
-    __syncwarp();
-    if (lane == 0) {
-      S.result = warp_level_verdict(S);
-      S.nfr[cur] = 0;
-      S.levels += 1;
-    }
-    __syncwarp();
-    const int r = S.result;
-    __syncwarp();
-    if (r >= 0) return r;
-    cur = nxt;
-  }
-}
 
 __device__ __forceinline__ int first_zero_byte(uint32_t w) {
   const uint32_t z = (w - 0x01010101u) & ~w & 0x80808080u;  // exact for the lowest zero byte
@@ -1600,13 +1631,14 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
   int ns = 32;
   for (;;) {
     int ok = 0;
-    if (lane == 0) ok = A.lab_pos[ld_acq(A.lab_ptr + l)] == pos;
+    if (lane == 0) ok = A.lab_pos[ld_rlx(A.lab_ptr + l)] == pos;
     if (__shfl_sync(0xffffffffu, ok, 0)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 512) ns <<= 1;
     }
   }
+  fence_acq();
   __syncwarp();
 }
 
@@ -1624,8 +1656,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     const int32_t pos = wpos[wid];
     __syncwarp();
     if (pos >= M) {
-      // keep helping assist jobs until every candidate is decided
-      warp_wait_lowmark(A, M);
+      // drain an active assist job, then leave: spinning finished warps
+      // would flood L2 with polls while the last candidates decide
+      while (warp_help(A)) {
+      }
       break;
     }
     if (A.tdbg && lane == 0) {
@@ -1685,31 +1719,52 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     }
     if (how == 1) {
       // exact window test (radius 5 in 2-D, 4 in 3-D), warp-cooperative:
-      // lanes wait on and read disjoint cells, ballots collect the donor-label
-      // bits, lane 0 floods and broadcasts the verdict
+      // lanes read disjoint cells without waiting, ballots collect the
+      // settled donor-label bits P and the pending cells U.  Window
+      // connectivity only grows with more a-cells, and a seed piece that
+      // cannot reach the rim stays so with fewer, so the verdict is exact
+      // if P alone joins the seeds (1) or P|U leaves a piece enclosed (2);
+      // otherwise the BFS (which skips pending sites the same way) decides.
       const int RB = lat.ndim == 2 ? (A.win_r ? A.win_r : 5) : 4, WB = 2 * RB + 1;
       const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
-      uint32_t *bits = S.fr[0];
+      uint32_t *bits = S.fr[0], *unk = S.fr[1];
       for (int base = 0; base < nb; base += 32) {
         const int c = base + lane;
-        int64_t gw = -1;
+        bool bit = false, u = false;
         if (c < nb) {
           const int dz = lat.ndim == 2 ? 0 : c / (WB * WB) - RB;
           const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
           const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) gw = lat.flat(zz, yy, xx);
+          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) {
+            const int64_t gw = lat.flat(zz, yy, xx);
+            u = ld_rlx(A.pend + gw) < pos;
+            if (!u) fence_acq();
+            bit = !u && v.lab(gw) == a;
+          }
         }
-        warp_wait_pend(A, gw, pos);
-        const bool bit = gw >= 0 && v.lab(gw) == a;
-        const unsigned m = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) bits[base >> 5] = m;
+        const unsigned m = __ballot_sync(0xffffffffu, bit), mu = __ballot_sync(0xffffffffu, u);
+        if (lane == 0) {
+          bits[base >> 5] = m;
+          unk[base >> 5] = mu;
+        }
       }
       __syncwarp();
-      if (lane == 0)
-        S.result = lat.ndim == 3 ? window_verdict_bits<4>(bits, WB)
-                   : RB == 3     ? window_verdict_bits<3>(bits, 1)
-                   : RB == 1     ? 0
-                                 : window_verdict_bits<5>(bits, 1);
+      if (lane == 0) {
+        auto verdict = [&](const uint32_t *b) {
+          return lat.ndim == 3 ? window_verdict_bits<4>(b, WB)
+                 : RB == 3     ? window_verdict_bits<3>(b, 1)
+                 : RB == 1     ? 0
+                               : window_verdict_bits<5>(b, 1);
+        };
+        uint32_t any_u = 0;
+        for (int q = 0; q < (nb + 31) / 32; ++q) any_u |= unk[q];
+        int r = verdict(bits);
+        if (r != 1 && any_u) {
+          for (int q = 0; q < (nb + 31) / 32; ++q) bits[q] |= unk[q];
+          r = verdict(bits) == 2 ? 2 : 0;
+        }
+        S.result = r;
+      }
       __syncwarp();
       const int wb = S.result;
       __syncwarp();
@@ -1722,29 +1777,34 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       if (wb == 2) {
         d = REJ;
       } else if (wb == 0) {
-        // blocked: wait for the blocking site and retry (the footprint is at
-        // most kMaxInsertW sites); overflow: wait to become the earliest
-        // undecided candidate, then the unbounded BFS cannot block
+        // BFS tiers: the bounding-box map when a's grown box fits, else the
+        // hash (<= max_insert sites); overflow of either goes to the assist
+        // job at the low-water mark.  A BFS whose verdict depends on a
+        // pending site (0) waits for it and runs again.
+        BfsBox bb;
+        {
+          const int32_t *bx = A.lbox + 4 * a;
+          const int ny = (int)lat.ny, nx = (int)lat.nx;
+          bb.r0 = bx[0] > 0 ? bx[0] - 1 : 0;
+          bb.c0 = bx[2] > 0 ? bx[2] - 1 : 0;
+          bb.bh = (bx[1] + 1 < ny ? bx[1] + 1 : ny - 1) - bb.r0 + 1;
+          bb.bw = (bx[3] + 1 < nx ? bx[3] + 1 : nx - 1) - bb.c0 + 1;
+        }
+        const bool use_box = (int64_t)bb.bh * bb.bw <= (int64_t)A.box_cap;
+        uint32_t seeds = 0;
+        for (int k = 9; k < 18; ++k)
+          if (k != 13 && lab[k] == a) seeds |= 1u << (k - 9);
         int r;
         for (;;) {
-          r = warp_bfs(A, S, pos, f, a);
+          r = use_box ? warp_bfs2d<true>(A, S, pos, f, a, seeds, bb)
+                      : warp_bfs2d<false>(A, S, pos, f, a, seeds, bb);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
           if (r != 0) break;
           if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
           warp_wait_pend(A, lane == 0 ? S.bsite : -1, pos);
           dbg += 1;
         }
-        if (r == 3) {
-          // footprint beyond the hash: the box-map tier, same retry rule
-          for (;;) {
-            r = warp_bfs_box(A, S, pos, f, a);
-            if (r != 0) break;
-            if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
-            warp_wait_pend(A, lane == 0 ? S.bsite : -1, pos);
-            dbg += 1;
-          }
-          dbg += 100000000;
-        }
+        if (use_box) dbg += 100000000;
         if (r == 3) {
           if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
           warp_wait_lowmark(A, pos);

@@ -247,10 +247,10 @@ def test_engine_invariants_at_full_cfg2_size(P):
 def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
     """K8 v3 (dataflow) and K8 v2 (cooperative rounds) against K8 v1 (one
     thread, the literal sequential greedy) on the same inputs: accepted moves
-    in order, labels and ledger must be identical.  The last two runs cap
-    the dataflow warp BFS at 8 sites so most inconclusive topology tests go
-    through the bounding-box BFS tier, or (box tier off) through the
-    grid-wide union-find assist job."""
+    in order, labels and ledger must be identical.  The dataflow runs cover
+    each topology-test tier: the bounding-box map BFS (default), the hash
+    BFS (box tier off), and the grid-wide union-find assist job (box tier
+    off, hash capped at 8 sites)."""
     import scenes
     if which == "cfg2":
         sc, iters = scenes.cfg2(), 3
@@ -262,7 +262,7 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
     ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
     runs = []
     for force, mode, cap, box in (("0", "dataflow", "0", "-1"), ("0", "rounds", "0", "-1"),
-                                  ("1", "dataflow", "0", "-1"), ("0", "dataflow", "8", "-1"),
+                                  ("1", "dataflow", "0", "-1"), ("0", "dataflow", "0", "0"),
                                   ("0", "dataflow", "8", "0")):
         monkeypatch.setenv("RCB_FORCE_SEQUENTIAL", force)
         monkeypatch.setenv("RCB_ACCEPT", mode)

@@ -45,7 +45,8 @@ def main():
         print(json.dumps({"it": rec.iteration, "ms": round(t[5], 3), "host_s": round(rec.seconds, 4),
                           "moves": rec.moves, "particles": rec.particles, "energy": rec.energy,
                           "mode": rec.mode, "negative": c["negative"], "pairs": e.last_pairs,
-                          "bfs": c["bfs_runs"], "deferred": c["deferred"]}), flush=True)
+                          "bfs": c["bfs_runs"], "deferred": c["deferred"],
+                          "phases": [round(x, 3) for x in t[:5]]}), flush=True)
 
     res = eng.run(on_iteration=cb)
     wall = time.time() - t_wall

@@ -98,3 +98,18 @@ print("corr(depth, decide time)", round(float(cc), 3), " us per depth level", ro
 for p in np.nonzero(defer)[0]:
     print("deferred pos %d fetch %.1f lowmark %.1f job %.1f decided %.1f (job us %.1f)" %
           (p, f[p], tb[p], tw[p], d[p], tw[p] - tb[p]))
+bt = d - tw
+code = code[:m]
+retries = code % 10
+isb = (code // 10) % 10 > 0
+lvl = code // 10000
+sel0 = isb & (retries == 0) & (lvl > 0)
+if sel0.any():
+    per = bt[sel0] / lvl[sel0]
+    print("BFS no-retry: n %d, us/level p50 %.2f p90 %.2f, bfs us p50 %.1f p90 %.1f max %.1f" %
+          (sel0.sum(), np.median(per), np.percentile(per, 90), np.median(bt[sel0]),
+           np.percentile(bt[sel0], 90), bt[sel0].max()))
+sel1 = isb & (retries > 0)
+print("BFS with retries: n %d, retries mean %.2f, bfs us p50 %.1f max %.1f" %
+      (sel1.sum(), retries[sel1].mean() if sel1.any() else 0, np.median(bt[sel1]) if sel1.any() else 0,
+       bt[sel1].max() if sel1.any() else 0))
