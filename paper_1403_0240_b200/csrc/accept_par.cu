@@ -1331,124 +1331,103 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
   __syncwarp();
   int cur = 0;
   for (;;) {
+    // one (frontier site, neighbour) pair per lane: eight lanes share a
+    // site, so its neighbours' loads coalesce and the code is straight-line
     const int n = S.nfr[cur], nxt = cur ^ 1;
-    for (int j = lane; j < n; j += 32) {
+    for (int p = lane; p < 8 * n; p += 32) {
+      const int j = p >> 3, k = p & 7;
       const uint32_t e = S.fr[cur][j];
       const int g = S.fg[cur][j];
-      const int y = (int)(e >> 16), x = (int)(e & 0xffffu);
-      uint32_t met = 0;  // groups met (unions)
-      bool blk = false, grew = false;
-      int t[8], li[8];
-      bool ok[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int dy = k < 3 ? -1 : (k < 5 ? 0 : 1);
-        const int dx = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
-        const int yy = y + dy, xx = x + dx;
-        ok[k] = (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
-        t[k] = yy * nx + xx;
-        li[k] = 0;
-        if (kBox) {
-          const int ry = yy - bb.r0, rx = xx - bb.c0;
-          // outside the grown box: never an a-site
-          ok[k] = ok[k] && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
-          li[k] = ry * bb.bw + rx;
-          if (ok[k]) {
-            const int cg = (int)((nib[li[k] >> 3] >> (4 * (li[k] & 7))) & 15u);
-            if (cg) {
-              if (cg != 15 && cg - 1 != g) met |= 1u << (cg - 1);
-              ok[k] = false;
-            }
-          }
-        } else if (ok[k]) {
-          uint32_t h = hash32((uint32_t)t[k]) & (kHW - 1);
-          for (;;) {
-            const unsigned long long cv = S.key[h];
-            if (cv == kEmpty) break;
-            if ((uint32_t)(cv >> 8) == (uint32_t)t[k]) {
-              const int hg = (int)(cv & 0xff);
-              if (hg != 255 && hg != g) met |= 1u << hg;
-              ok[k] = false;
-              break;
-            }
-            h = (h + 1) & (kHW - 1);
+      const int kk = k + (k >= 4);  // skip the centre of the 3x3
+      const int yy = (int)(e >> 16) + kk / 3 - 1, xx = (int)(e & 0xffffu) + kk % 3 - 1;
+      bool ok = (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+      const int t = yy * nx + xx;
+      int li = 0;
+      if (kBox) {
+        const int ry = yy - bb.r0, rx = xx - bb.c0;
+        // outside the grown box: never an a-site
+        ok = ok && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
+        li = ry * bb.bw + rx;
+        if (ok) {
+          const int cg = (int)((nib[li >> 3] >> (4 * (li & 7))) & 15u);
+          if (cg) {
+            if (cg != 15 && cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
+            ok = false;
           }
         }
-      }
-      int32_t wv[8], l0[8], pm[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        wv[k] = ok[k] ? __ldcg(Wp + t[k]) : 0x7fffffff;
-        l0[k] = ok[k] ? __ldg(Lp + t[k]) : -1;
-        pm[k] = ok[k] ? __ldcg(Pp + t[k]) : 0x7fffffff;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (!ok[k]) continue;
-        if (pm[k] < pos) {
-          blk = true;
-          S.bsite = t[k];
-          continue;
+      } else if (ok) {
+        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
+        for (;;) {
+          const unsigned long long cv = S.key[h];
+          if (cv == kEmpty) break;
+          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
+            const int hg = (int)(cv & 0xff);
+            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
+            ok = false;
+            break;
+          }
+          h = (h + 1) & (kHW - 1);
         }
-        const int32_t lab = wv[k] < pos ? __ldcg(Np + t[k]) : l0[k];
-        if (lab != a) continue;
-        const int dy = k < 3 ? -1 : (k < 5 ? 0 : 1);
-        const int dx = k < 3 ? k - 1 : (k < 5 ? (k == 3 ? -1 : 1) : k - 6);
-        const uint32_t pk = ((uint32_t)(y + dy) << 16) | (uint32_t)(x + dx);
-        bool ins = false;
-        if (kBox) {
-          uint32_t *wp = nib + (li[k] >> 3);
-          const int sh = 4 * (li[k] & 7);
-          uint32_t w = *(volatile uint32_t *)wp;
-          for (;;) {
-            const int cg = (int)((w >> sh) & 15u);
-            if (cg) {
-              if (cg != 15 && cg - 1 != g) met |= 1u << (cg - 1);
-              break;
-            }
-            const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
-            if (old == w) {
+      }
+      if (!ok) continue;
+      const int32_t wv = __ldcg(Wp + t), l0 = __ldg(Lp + t), pm = __ldcg(Pp + t);
+      if (pm < pos) {
+        atomicOr(&S.gblk, 1u << g);
+        S.bsite = t;
+        continue;
+      }
+      const int32_t lab = wv < pos ? __ldcg(Np + t) : l0;
+      if (lab != a) continue;
+      bool ins = false;
+      if (kBox) {
+        uint32_t *wp = nib + (li >> 3);
+        const int sh = 4 * (li & 7);
+        uint32_t w = *(volatile uint32_t *)wp;
+        for (;;) {
+          const int cg = (int)((w >> sh) & 15u);
+          if (cg) {
+            if (cg != 15 && cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
+            break;
+          }
+          const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
+          if (old == w) {
+            ins = true;
+            break;
+          }
+          w = old;
+        }
+      } else {
+        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
+        const unsigned long long mine = ((unsigned long long)(uint32_t)t << 8) | (unsigned)g;
+        for (;;) {
+          unsigned long long cv = S.key[h];
+          if (cv == kEmpty) {
+            const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
+            if (old == kEmpty) {
               ins = true;
               break;
             }
-            w = old;
+            cv = old;
           }
-        } else {
-          uint32_t h = hash32((uint32_t)t[k]) & (kHW - 1);
-          const unsigned long long mine = ((unsigned long long)(uint32_t)t[k] << 8) | (unsigned)g;
-          for (;;) {
-            unsigned long long cv = S.key[h];
-            if (cv == kEmpty) {
-              const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
-              if (old == kEmpty) {
-                ins = true;
-                break;
-              }
-              cv = old;
-            }
-            if ((uint32_t)(cv >> 8) == (uint32_t)t[k]) {
-              const int hg = (int)(cv & 0xff);
-              if (hg != 255 && hg != g) met |= 1u << hg;
-              break;
-            }
-            h = (h + 1) & (kHW - 1);
+          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
+            const int hg = (int)(cv & 0xff);
+            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
+            break;
           }
-          if (ins && atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
+          h = (h + 1) & (kHW - 1);
         }
-        if (ins) {
-          grew = true;
-          const int q = atomicAdd(&S.nfr[nxt], 1);
-          if (q < kFW) {
-            S.fr[nxt][q] = pk;
-            S.fg[nxt][q] = (uint8_t)g;
-          } else {
-            S.overflow = 1;
-          }
+        if (ins && atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
+      }
+      if (ins) {
+        atomicOr(&S.alive, 1u << g);
+        const int q = atomicAdd(&S.nfr[nxt], 1);
+        if (q < kFW) {
+          S.fr[nxt][q] = ((uint32_t)yy << 16) | (uint32_t)xx;
+          S.fg[nxt][q] = (uint8_t)g;
+        } else {
+          S.overflow = 1;
         }
       }
-      if (met) atomicOr(&S.unions[g], met);
-      if (grew) atomicOr(&S.alive, 1u << g);
-      if (blk) atomicOr(&S.gblk, 1u << g);
     }
     __syncwarp();
     if (lane == 0) {
