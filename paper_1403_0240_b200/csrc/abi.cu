@@ -123,7 +123,8 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows;
-  DBuf<unsigned long long> ufp, job;
+  DBuf<unsigned long long> ufp, job, wpk;
+  DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
   DBuf<long long> tdbg;
   bool profile = false;
@@ -162,7 +163,7 @@ struct rcb_engine {
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s);
-      ufp.release(s); job.release(s);
+      ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -459,16 +460,20 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
         P.tdbg = e->tdbg.p;
       }
       // dataflow kernel: 2-D with sides < 2^16 (packed BFS coordinates)
-      const bool use_df = lat.ndim == 2 && e->accept_mode != 1 && lat.nx < 65536 && lat.ny < 65536;
+      const bool use_df = lat.ndim == 2 && e->accept_mode != 1 && lat.nx < 65536 &&
+                          lat.ny < 65536 && n < 0xffffff && e->nl <= 65536;
       if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufp.reserve(lat.V, s));
+          RCB_TRY(e->wpk.reserve(lat.V, s));
+          RCB_CUDA(cudaMemsetAsync(e->wpk.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_TRY(e->job.reserve(64, s));
           RCB_CUDA(cudaMemsetAsync(e->ufp.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->job.p, 0, sizeof(unsigned long long) * 64, s));
         }
         P.ufp = e->ufp.p;
         P.job = e->job.p;
+        P.wp = e->wpk.p;
       }
       if (!use_df) {
         // slots for the round-based kernel's large-footprint BFS (<= 160 blocks)
@@ -529,6 +534,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.labpos = &e->labpos;
       X.labpos2 = &e->labpos2;
       X.flrows = &e->flrows;
+      X.rec = &e->rec;
       X.labbounds = &e->labbounds;
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));

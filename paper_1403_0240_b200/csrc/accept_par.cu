@@ -989,6 +989,30 @@ __device__ __forceinline__ int32_t ld_rlx(const int32_t *p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_rlx64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Dataflow site word wp[y] = newlab << 48 | w << 24 | pend: the earliest
+// undecided position at y, the position that flipped y and its new label
+// (all-ones fields: none), published together by one release store.  One
+// relaxed load therefore gives a consistent triple: a reader that finds
+// pend >= pos has y settled for V_pos, with V_pos(y) = w < pos ? newlab : L[y]
+// and no further memory access.  The host keeps this kernel to particle
+// counts < 2^24 - 1 and labels < 2^16.
+static constexpr uint32_t kWpInf = 0xffffffu;
+__device__ __forceinline__ int32_t wp_pend(unsigned long long v) { return (int32_t)(v & kWpInf); }
+__device__ __forceinline__ int32_t wp_w(unsigned long long v) { return (int32_t)((v >> 24) & kWpInf); }
+__device__ __forceinline__ int32_t wp_lab(unsigned long long v) { return (int32_t)(v >> 48); }
+__device__ __forceinline__ unsigned long long wp_pack(int32_t pend, int32_t w, int32_t lab) {
+  const uint32_t p = pend < (int32_t)kWpInf ? (uint32_t)pend : kWpInf;
+  const uint32_t q = w < (int32_t)kWpInf ? (uint32_t)w : kWpInf;
+  return ((unsigned long long)(uint32_t)lab << 48) | ((unsigned long long)q << 24) | p;
+}
+__device__ __forceinline__ int32_t df_lab(unsigned long long v, int32_t l0, int32_t pos) {
+  return wp_w(v) < pos ? wp_lab(v) : l0;
+}
 __device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
   int32_t v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1182,19 +1206,23 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
   return __shfl_sync(0xffffffffu, r, 0);
 }
 
-// Warp-level wait until every lane's site g (or -1) has no candidate before
-// pos pending; helps the current job meanwhile.
-__device__ __forceinline__ void warp_wait_pend(const ParArgs &A, int64_t g, int32_t pos) {
+// Warp-level wait until every lane's site g (or -1) is settled for V_pos (no
+// candidate before pos pending there); helps the current job meanwhile.
+// Returns this lane's packed site word.
+__device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A, int64_t g,
+                                                                int32_t pos) {
   int ns = 32;
+  unsigned long long v = 0;
   for (;;) {
-    const bool p = g >= 0 && ld_rlx(A.pend + g) < pos;
+    if (g >= 0) v = ld_rlx64(A.wp + g);
+    const bool p = g >= 0 && wp_pend(v) < pos;
     if (!__any_sync(0xffffffffu, p)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 512) ns <<= 1;
     }
   }
-  fence_acq();
+  return v;
 }
 
 struct WarpBfs {
@@ -1279,8 +1307,7 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
   const int lane = threadIdx.x & 31;
   const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
   const int fy = (int)(f / nx), fx = (int)(f % nx);
-  const int32_t *__restrict__ Wp = A.w, *__restrict__ Lp = A.L, *__restrict__ Pp = A.pend,
-                              *__restrict__ Np = A.newlab;
+  const int32_t *__restrict__ Lp = A.L;
   uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
   if (kBox) {
     const int nw = (bb.bh * bb.bw + 7) >> 3;
@@ -1370,13 +1397,14 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
         }
       }
       if (!ok) continue;
-      const int32_t wv = __ldcg(Wp + t), l0 = __ldg(Lp + t), pm = __ldcg(Pp + t);
-      if (pm < pos) {
+      const unsigned long long pk = ld_rlx64(A.wp + t);
+      const int32_t l0 = __ldg(Lp + t);
+      if (wp_pend(pk) < pos) {
         atomicOr(&S.gblk, 1u << g);
         S.bsite = t;
         continue;
       }
-      const int32_t lab = wv < pos ? __ldcg(Np + t) : l0;
+      const int32_t lab = df_lab(pk, l0, pos);
       if (lab != a) continue;
       bool ins = false;
       if (kBox) {
@@ -1443,6 +1471,93 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 31x31 window test, warp-parallel (2-D): lane r holds row r of the window
+// around x as a bit mask (built by ballots, one row of cells per load round),
+// and components flood by shuffles: one iteration grows them by one cell.
+// Same verdict rules as window_verdict_bits (1: the seeds -- the a-cells of
+// x's box -- share a component; 2: a seed component cannot reach the rim;
+// 0: inconclusive), evaluated on the settled a-cells (pessimistic, exact for
+// 1) and on settled | pending (optimistic, exact for 2).
+// ---------------------------------------------------------------------------
+static constexpr int kW31 = 31, kR31 = 15;
+
+__device__ __forceinline__ uint32_t flood31(uint32_t cur, uint32_t cells) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t up = __shfl_up_sync(0xffffffffu, cur, 1), dn = __shfl_down_sync(0xffffffffu, cur, 1);
+    if (lane == 0) up = 0;
+    if (lane == 31) dn = 0;
+    uint32_t v = cur | up | dn;
+    v = (v | (v << 1) | (v >> 1)) & cells;
+    if (!__any_sync(0xffffffffu, v != cur)) return cur;
+    cur = v;
+  }
+}
+
+// verdict on one cell plane (whole warp)
+__device__ __forceinline__ int verdict31(uint32_t cells, uint32_t seeds) {
+  const int lane = threadIdx.x & 31;
+  uint32_t rest = seeds;
+  bool first = true;
+  for (;;) {
+    const unsigned rows = __ballot_sync(0xffffffffu, rest != 0);
+    if (!rows) return 0;
+    const int r0 = __ffs(rows) - 1;
+    const uint32_t low = __shfl_sync(0xffffffffu, rest & (~rest + 1), r0);
+    const uint32_t comp = flood31(lane == r0 ? low : 0u, cells);
+    const bool all = !__any_sync(0xffffffffu, (rest & ~comp) != 0);
+    rest &= ~comp;
+    if (first && all) return 1;
+    first = false;
+    const uint32_t rim = (lane == 0 || lane == kW31 - 1) ? comp : (comp & (1u | (1u << (kW31 - 1))));
+    if (!__any_sync(0xffffffffu, rim != 0)) return 2;
+  }
+}
+
+__device__ int window31(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
+  const int lane = threadIdx.x & 31;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
+  const int fy = (int)(f / nx), fx = (int)(f % nx);
+  uint32_t P = 0, U = 0;  // this lane's row: settled a-cells, pending cells
+  const int xx = fx - kR31 + lane;
+  const bool colok = lane < kW31 && (unsigned)xx < (unsigned)nx;
+  for (int rb = 0; rb < kW31; rb += 8) {
+    int t[8];
+    bool in[8];
+    unsigned long long pk[8];
+    int32_t l0[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = rb + i, yy = fy - kR31 + r;
+      in[i] = colok && r < kW31 && (unsigned)yy < (unsigned)ny && !(r == kR31 && lane == kR31);
+      t[i] = yy * nx + xx;
+      pk[i] = in[i] ? ld_rlx64(A.wp + t[i]) : ~0ull;
+      l0[i] = in[i] ? __ldg(A.L + t[i]) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool st = in[i] && wp_pend(pk[i]) >= pos;
+      const int32_t lab = st ? df_lab(pk[i], l0[i], pos) : -1;
+      const unsigned mp = __ballot_sync(0xffffffffu, st && lab == a);
+      const unsigned mu = __ballot_sync(0xffffffffu, in[i] && !st);
+      if (lane == rb + i) {
+        P = mp;
+        U = mu;
+      }
+    }
+  }
+  // seeds: the settled a-cells of x's box (the box was waited on)
+  const uint32_t boxm = (lane >= kR31 - 1 && lane <= kR31 + 1)
+                            ? ((7u << (kR31 - 1)) & ~(lane == kR31 ? (1u << kR31) : 0u))
+                            : 0u;
+  const uint32_t seeds = P & boxm;
+  const bool anyU = __any_sync(0xffffffffu, U != 0);
+  const int rp = verdict31(P, seeds);
+  if (rp == 1 || !anyU) return rp;
+  return verdict31(P | U, seeds) == 2 ? 2 : 0;
+}
 
 __device__ __forceinline__ int first_zero_byte(uint32_t w) {
   const uint32_t z = (w - 0x01010101u) & ~w & 0x80808080u;  // exact for the lowest zero byte
@@ -1523,7 +1638,7 @@ __global__ void k_df_init2(ParArgs A) {
     const uint32_t p = A.order[pos];
     A.pos_of[p] = (int32_t)pos;
     A.dec[pos] = UNDEC;
-    atomicMin(A.pend + A.px[p], (int32_t)pos);
+    atomicMin(A.wp + A.px[p], ~(unsigned long long)kWpInf | (unsigned)pos);  // pend field
     const int32_t a = A.pown[p];
     if (a > 0) atomicAdd(A.nown + a, 1);
   }
@@ -1560,6 +1675,26 @@ __global__ void k_df_bbox(ParArgs A, int64_t N) {
     else if (j < 2 * nx + ny) y = (j - 2 * nx) * nx;     // left column
     else y = (j - 2 * nx - ny) * nx + nx - 1;            // right column
     bbox_add(A, A.L[y], y);
+  }
+}
+
+// Per rank position: (site, owner | small << 31, competitor | small << 31,
+// next position at the same site), so a warp needs one load per candidate
+// and publishes the site's next pending position without a CSR scan.
+__global__ void k_df_records(ParArgs A, int4 *__restrict__ rec) {
+  const int32_t M = (int32_t)*A.nneg;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < M; pos += stride) {
+    const uint32_t p = A.order[pos];
+    const int64_t f = A.px[p];
+    const int32_t a = A.pown[p], b = A.pcomp[p];
+    int32_t nxt = kInf;
+    for (uint32_t q = A.site_off[f]; q < A.site_off[f + 1]; ++q) {
+      const int32_t pq = A.pos_of[q];
+      if (pq > pos && pq < nxt) nxt = pq;
+    }
+    rec[pos] = make_int4((int32_t)f, (int32_t)((uint32_t)a | (A.small[a] ? 0x80000000u : 0u)),
+                         (int32_t)((uint32_t)b | (A.small[b] ? 0x80000000u : 0u)), nxt);
   }
 }
 
@@ -1621,19 +1756,27 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
   __syncwarp();
 }
 
+__device__ __forceinline__ void df_stamp(const ParArgs &A, int32_t pos, int k) {
+  if (A.tdbg && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tdbg[4 * pos + k] = (long long)t;
+  }
+}
+
+// 2-D only (the host routes 3-D lattices to the round-based kernel).
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
-  __shared__ int32_t wpos[kDfWarps];
   const Lat &lat = A.lat;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int32_t M = (int32_t)*A.nneg;
+  const int nx = (int)lat.nx, ny = (int)lat.ny;
   int32_t *ctl = A.ctl;
+  // positions come from an atomic counter one at a time: a position held
+  // ahead by a warp stuck in a long BFS would stall its dependants
   for (;;) {
-    if (lane == 0) wpos[wid] = atomicAdd(ctl + 12, 1);
-    __syncwarp();
-    const int32_t pos = wpos[wid];
-    __syncwarp();
+    const int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
     if (pos >= M) {
       // drain an active assist job, then leave: spinning finished warps
       // would flood L2 with polls while the last candidates decide
@@ -1641,36 +1784,31 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       }
       break;
     }
-    if (A.tdbg && lane == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      A.tdbg[4 * pos] = (long long)t;
-    }
-    const uint32_t p = A.order[pos];
-    const int64_t f = A.px[p];
-    const int32_t a = A.pown[p], b = A.pcomp[p];
-    const bool sa = A.small[a], sb = A.small[b];
+    const int4 rc = __ldg(A.rec + pos);
+    df_stamp(A, pos, 0);
+    const int32_t f = rc.x, next = rc.w;
+    const int32_t a = rc.y & 0x7fffffff, b = rc.z & 0x7fffffff;
+    const bool sa = rc.y < 0, sb = rc.z < 0;
     if (sa) warp_wait_label(A, a, pos);
     if (sb) warp_wait_label(A, b, pos);
-    View v{A, pos};
-    int64_t z, y, x;
-    lat.coord(f, z, y, x);
-    // the 3^d box, one cell per lane
-    int32_t mine = -1;
+    const int y = f / nx, x = f - y * nx;
+    // the 3x3 box, lanes 9..17 in the 3^3 layout of lab[] (13 = x itself)
     int64_t gb = -1;
-    if (lane < 27) {
-      const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
-      const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-      if (!(lat.ndim == 2 && dz != 0) && lat.inb(zz, yy, xx)) gb = lat.flat(zz, yy, xx);
+    if (lane >= 9 && lane < 18) {
+      const int yy = y + lane / 3 - 4, xx = x + lane % 3 - 1;
+      if ((unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx) gb = yy * nx + xx;
     }
-    warp_wait_pend(A, gb, pos);
-    if (gb >= 0) mine = v.lab(gb);
+    const int32_t l0 = gb >= 0 ? __ldg(A.L + gb) : -1;
+    const unsigned long long pk = warp_wait_settled(A, gb, pos);
+    const int32_t mine = gb >= 0 ? df_lab(pk, l0, pos) : -1;
+    const unsigned long long pkc = __shfl_sync(0xffffffffu, pk, 13);  // x's own word
+    const int32_t wold = wp_w(pkc), lold = wp_lab(pkc);
     int32_t lab[27];
 #pragma unroll
-    for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
+    for (int k = 0; k < 27; ++k) lab[k] = (k >= 9 && k < 18) ? __shfl_sync(0xffffffffu, mine, k) : -1;
     uint8_t d = ACC;
-    int how = 0;  // 1: needs window test
-    int dbg = 0;  // decision path: 1000*how + 100*(window+2) + 10*(bfs+1) + retries
+    int how = 0;  // 1: needs the window test
+    int dbg = 0;  // decision path (tools/df_timeline.py decodes it)
     if (lab[13] != a) {
       d = REJ;
     } else {
@@ -1690,35 +1828,29 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
           how = 1;
       }
     }
-    if (A.tdbg && lane == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      A.tdbg[4 * pos + 2] = (long long)t;
-      A.tdbg[4 * pos + 3] = (long long)t;
-    }
+    df_stamp(A, pos, 2);
+    df_stamp(A, pos, 3);
     if (how == 1) {
-      // exact window test (radius 5 in 2-D, 4 in 3-D), warp-cooperative:
-      // lanes read disjoint cells without waiting, ballots collect the
-      // settled donor-label bits P and the pending cells U.  Window
-      // connectivity only grows with more a-cells, and a seed piece that
-      // cannot reach the rim stays so with fewer, so the verdict is exact
-      // if P alone joins the seeds (1) or P|U leaves a piece enclosed (2);
-      // otherwise the BFS (which skips pending sites the same way) decides.
-      const int RB = lat.ndim == 2 ? (A.win_r ? A.win_r : 5) : 4, WB = 2 * RB + 1;
-      const int nb = lat.ndim == 2 ? WB * WB : WB * WB * WB;
+      // exact window test (radius 5), warp-cooperative: lanes read disjoint
+      // cells without waiting, ballots collect the settled donor-label bits
+      // P and the pending cells U.  Window connectivity only grows with more
+      // a-cells, and a seed piece that cannot reach the rim stays so with
+      // fewer, so the verdict is exact if P alone joins the seeds (1) or P|U
+      // leaves a piece enclosed (2); otherwise the 31x31 window and then the
+      // BFS (which skip pending sites the same way) decide.
+      const int RB = A.win_r ? A.win_r : 5, WB = 2 * RB + 1, nb = WB * WB;
       uint32_t *bits = S.fr[0], *unk = S.fr[1];
       for (int base = 0; base < nb; base += 32) {
         const int c = base + lane;
         bool bit = false, u = false;
         if (c < nb) {
-          const int dz = lat.ndim == 2 ? 0 : c / (WB * WB) - RB;
-          const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
-          const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-          if ((dz || dy || dx) && lat.inb(zz, yy, xx)) {
-            const int64_t gw = lat.flat(zz, yy, xx);
-            u = ld_rlx(A.pend + gw) < pos;
-            if (!u) fence_acq();
-            bit = !u && v.lab(gw) == a;
+          const int yy = y + c / WB - RB, xx = x + c % WB - RB;
+          if ((yy != y || xx != x) && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx) {
+            const int gw = yy * nx + xx;
+            const unsigned long long wv = ld_rlx64(A.wp + gw);
+            const int32_t lw = __ldg(A.L + gw);
+            u = wp_pend(wv) < pos;
+            bit = !u && df_lab(wv, lw, pos) == a;
           }
         }
         const unsigned m = __ballot_sync(0xffffffffu, bit), mu = __ballot_sync(0xffffffffu, u);
@@ -1729,11 +1861,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       }
       __syncwarp();
       if (lane == 0) {
-        auto verdict = [&](const uint32_t *b) {
-          return lat.ndim == 3 ? window_verdict_bits<4>(b, WB)
-                 : RB == 3     ? window_verdict_bits<3>(b, 1)
-                 : RB == 1     ? 0
-                               : window_verdict_bits<5>(b, 1);
+        auto verdict = [&](const uint32_t *bb) {
+          return RB == 3 ? window_verdict_bits<3>(bb, 1)
+                 : RB == 1 ? 0
+                           : window_verdict_bits<5>(bb, 1);
         };
         uint32_t any_u = 0;
         for (int q = 0; q < (nb + 31) / 32; ++q) any_u |= unk[q];
@@ -1745,13 +1876,13 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         S.result = r;
       }
       __syncwarp();
-      const int wb = S.result;
+      int wb = S.result;
       __syncwarp();
       dbg = 1000 + 100 * (wb + 2);
-      if (A.tdbg && lane == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        A.tdbg[4 * pos + 3] = (long long)t;
+      df_stamp(A, pos, 3);
+      if (wb == 0) {
+        wb = window31(A, pos, f, a);
+        dbg += 10000000 * (wb + 1);
       }
       if (wb == 2) {
         d = REJ;
@@ -1763,7 +1894,6 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         BfsBox bb;
         {
           const int32_t *bx = A.lbox + 4 * a;
-          const int ny = (int)lat.ny, nx = (int)lat.nx;
           bb.r0 = bx[0] > 0 ? bx[0] - 1 : 0;
           bb.c0 = bx[2] > 0 ? bx[2] - 1 : 0;
           bb.bh = (bx[1] + 1 < ny ? bx[1] + 1 : ny - 1) - bb.r0 + 1;
@@ -1780,31 +1910,20 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
           if (r != 0) break;
           if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
-          warp_wait_pend(A, lane == 0 ? S.bsite : -1, pos);
+          warp_wait_settled(A, lane == 0 ? S.bsite : -1, pos);
           dbg += 1;
         }
         if (use_box) dbg += 100000000;
         if (r == 3) {
           if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
           warp_wait_lowmark(A, pos);
-          if (A.tdbg && lane == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            A.tdbg[4 * pos + 2] = (long long)t;  // deferred: low-water mark reached
-          }
+          df_stamp(A, pos, 2);  // deferred: low-water mark reached
           r = warp_job_owner(A, pos, f, a);
-          if (A.tdbg && lane == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            A.tdbg[4 * pos + 3] = (long long)t;  // deferred: job answered
-          }
-          dbg += 1000000000;
-          dbg += 2;
+          df_stamp(A, pos, 3);  // deferred: job answered
+          dbg += 1000000000 + 2;
         }
         if (r == 2) d = REJ;
-        dbg += 10 * (r + 1) + 10000 * (S.levels < 9999 ? S.levels : 9999);  // +1e8 box tier, +1e9 job
-      } else if (wb != 1) {
-        d = REJ;  // cannot happen after the waits; never accept unproven
+        dbg += 10 * (r + 1) + 10000 * (S.levels < 999 ? S.levels : 999);  // +1e7 w31, +1e8 box, +1e9 job
       }
     }
     if (d == ACC && b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b)) d = REJ;
@@ -1816,21 +1935,11 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         if (sa) atomicAdd((unsigned long long *)(A.cnt + a), (unsigned long long)(-1ll));
         if (sb) atomicAdd((unsigned long long *)(A.cnt + b), 1ull);
       }
-      if (A.tdbg) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        A.tdbg[4 * pos + 1] = (long long)t;
-      }
+      df_stamp(A, pos, 1);
       // release: the flip (newlab, w) and counts are visible before the
-      // decision, the decision before the site's next pending position
+      // decision, the decision before the site word with its next position
       st_rel_u8(A.dec + pos, d);
-      // next pending position at this site
-      int32_t nxt = kInf;
-      for (uint32_t q = A.site_off[f]; q < A.site_off[f + 1]; ++q) {
-        const int32_t pq = A.pos_of[q];
-        if (pq > pos && pq < nxt) nxt = pq;
-      }
-      st_rel(A.pend + f, nxt);
+      st_rel64(A.wp + f, d == ACC ? wp_pack(next, pos, b) : wp_pack(next, wold, lold));
       if (sa) st_rel(A.lab_ptr + a, A.lab_ptr[a] + 1);
       if (sb) st_rel(A.lab_ptr + b, A.lab_ptr[b] + 1);
     }
@@ -2270,6 +2379,7 @@ __global__ void k_final_labels(const ParArgs A, const uint32_t *__restrict__ slo
     uint32_t p = A.order[i];
     int64_t f = A.px[p];
     A.w[f] = kInf;
+    if (A.wp) A.wp[f] = ~0ull;
     if ((int64_t)slot[i] < budget) L[f] = A.pcomp[p];
   }
 }
@@ -2409,6 +2519,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
     k_df_bbox<<<grid_for(N + 2 * (A.lat.nx + A.lat.ny), 256), 256, 0, s>>>(A, N);
+    RCB_TRY(X.rec->reserve(N, s));
+    k_df_records<<<grid_for(N, 256), 256, 0, s>>>(A, X.rec->p);
+    A.rec = X.rec->p;
     RCB_TRY(X.evkey->reserve(2 * N, s));
     RCB_TRY(X.evkey2->reserve(2 * N, s));
     RCB_TRY(X.labpos->reserve(2 * N, s));

@@ -97,6 +97,8 @@ struct ParArgs {
   int max_insert;   // dataflow warp-BFS footprint cap (0: default)
   int box_cap;      // dataflow box-map BFS capacity in sites (-1: default, 0: off)
   unsigned long long *job, *ufp;  // dataflow assist jobs (accept_par.cu)
+  unsigned long long *wp;         // dataflow site words (pend << 32 | w)
+  const int4 *rec;                // dataflow per-position records
 };
 
 struct ParExtra {
@@ -123,6 +125,7 @@ struct ParExtra {
   int accept_mode;  // 0 dataflow (default), 1 rounds
   DBuf<uint64_t> *labkey, *labkey2;
   DBuf<int32_t> *labpos, *labpos2, *flrows;
+  DBuf<int4> *rec;
   DBuf<int64_t> *labbounds;
 };
 

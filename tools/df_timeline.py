@@ -46,6 +46,9 @@ code = code % 1000000000
 boxt = code >= 100000000
 print('box-tier candidates', int(boxt.sum()), 'deferred', int(defer.sum()))
 code = code % 100000000
+w31 = code // 10000000 - 1
+print('window31 runs', int((w31 >= 0).sum()), 'verdicts 1/2/0:', int((w31 == 1).sum()), int((w31 == 2).sum()), int((w31 == 0).sum()))
+code = code % 10000000
 lv = code // 10000
 bfs = lv > 0
 print("BFS candidates", int(bfs.sum()), "levels p50/p90/p99/max", np.percentile(lv[bfs], [50, 90, 99, 100]) if bfs.any() else None)
@@ -113,3 +116,11 @@ sel1 = isb & (retries > 0)
 print("BFS with retries: n %d, retries mean %.2f, bfs us p50 %.1f max %.1f" %
       (sel1.sum(), retries[sel1].mean() if sel1.any() else 0, np.median(bt[sel1]) if sel1.any() else 0,
        bt[sel1].max() if sel1.any() else 0))
+how = (code % 10000) // 1000
+wbv = (code % 1000) // 100 - 2
+print("candidates needing the window test:", int((how == 1).sum()), "of", m,
+      " window verdicts 1/2/0:", int(((how == 1) & (wbv == 1)).sum()), int(((how == 1) & (wbv == 2)).sum()),
+      int(((how == 1) & (wbv == 0)).sum()))
+bl = lvl[isb]
+for R in (7, 10, 15, 20):
+    print(f"  BFS with <= {R} levels: {int((bl <= R).sum())} of {len(bl)}")
