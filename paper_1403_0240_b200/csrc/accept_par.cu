@@ -1236,7 +1236,12 @@ struct WarpBfs {
   int nseed, ninsert, overflow, result, levels;
   unsigned long long comp;      // byte g = component mask of group g
   int64_t bsite;
+  int npq;                      // skipped pending sites (site, group), for resuming
+  uint32_t pq[64];
+  uint8_t pqg[64];
+  uint32_t lastalive;
 };
+static constexpr int kPQ = 64;
 
 // ---------------------------------------------------------------------------
 // Warp BFS of the dataflow kernel (2-D, sides < 2^16): the pieces question
@@ -1263,8 +1268,9 @@ __device__ __forceinline__ int comp_of(unsigned long long C, int g) {
   return (int)((C >> (8 * g)) & 0xffu);
 }
 
-// lane 0: fold this level's unions into the components and decide
-__device__ int warp_verdict8(WarpBfs &S) {
+// lane 0: fold this level's unions into the components and decide; alive =
+// groups that inserted a site this level
+__device__ int warp_verdict8(WarpBfs &S, uint32_t alive) {
   if (S.overflow) return 3;
   unsigned long long C = S.comp;
   const int ns = S.nseed;
@@ -1286,8 +1292,6 @@ __device__ int warp_verdict8(WarpBfs &S) {
   S.comp = C;
   const int all = (1 << ns) - 1;
   if (comp_of(C, 0) == all) return 1;
-  const uint32_t alive = S.alive;
-  S.alive = 0;
   int res = -1, seen = 0;
   for (int g = 0; g < ns; ++g) {
     if (seen & (1 << g)) continue;
@@ -1301,13 +1305,71 @@ __device__ int warp_verdict8(WarpBfs &S) {
   return res;
 }
 
+// Visit site t (settled, label lab) from group g: insert it or record the
+// union with the group that owns it.  Returns true if newly inserted.
+template <bool kBox>
+__device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t *nib, int li,
+                                          int t, int g) {
+  bool ins = false;
+  if (kBox) {
+    uint32_t *wp = nib + (li >> 3);
+    const int sh = 4 * (li & 7);
+    uint32_t w = *(volatile uint32_t *)wp;
+    for (;;) {
+      const int cg = (int)((w >> sh) & 15u);
+      if (cg) {
+        if (cg != 15 && cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
+        break;
+      }
+      const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
+      if (old == w) {
+        ins = true;
+        break;
+      }
+      w = old;
+    }
+  } else {
+    uint32_t h = hash32((uint32_t)t) & (kHW - 1);
+    const unsigned long long mine = ((unsigned long long)(uint32_t)t << 8) | (unsigned)g;
+    for (;;) {
+      unsigned long long cv = S.key[h];
+      if (cv == kEmpty) {
+        const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
+        if (old == kEmpty) {
+          ins = true;
+          break;
+        }
+        cv = old;
+      }
+      if ((uint32_t)(cv >> 8) == (uint32_t)t) {
+        const int hg = (int)(cv & 0xff);
+        if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
+        break;
+      }
+      h = (h + 1) & (kHW - 1);
+    }
+    if (ins && atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
+  }
+  return ins;
+}
+
+__device__ __forceinline__ void bfs_push(WarpBfs &S, int nxt, int yy, int xx, int g) {
+  atomicOr(&S.alive, 1u << g);
+  const int q = atomicAdd(&S.nfr[nxt], 1);
+  if (q < kFW) {
+    S.fr[nxt][q] = ((uint32_t)yy << 16) | (uint32_t)xx;
+    S.fg[nxt][q] = (uint8_t)g;
+  } else {
+    S.overflow = 1;
+  }
+}
+
 template <bool kBox>
 __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
                           uint32_t seedmask, const BfsBox bb) {
   const int lane = threadIdx.x & 31;
   const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
   const int fy = (int)(f / nx), fx = (int)(f % nx);
-  const int32_t *__restrict__ Lp = A.L;
   uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
   if (kBox) {
     const int nw = (bb.bh * bb.bw + 7) >> 3;
@@ -1322,6 +1384,7 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
     S.overflow = 0;
     S.result = -1;
     S.levels = 0;
+    S.npq = 0;
     S.nfr[1] = 0;
     if (kBox) {
       const int li = (fy - bb.r0) * bb.bw + (fx - bb.c0);
@@ -1356,120 +1419,132 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
     S.ninsert = ns + 1;
   }
   __syncwarp();
+  auto box_index = [&](int yy, int xx, bool &ok) -> int {
+    if (!kBox) return 0;
+    const int ry = yy - bb.r0, rx = xx - bb.c0;
+    // outside the grown box: never an a-site
+    ok = ok && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
+    return ry * bb.bw + rx;
+  };
   int cur = 0;
   for (;;) {
-    // one (frontier site, neighbour) pair per lane: eight lanes share a
-    // site, so its neighbours' loads coalesce and the code is straight-line
+    // (frontier site, neighbour) pairs, three per lane with all their loads
+    // issued before any is used; eight lanes share a site so its
+    // neighbours' loads coalesce
     const int n = S.nfr[cur], nxt = cur ^ 1;
-    for (int p = lane; p < 8 * n; p += 32) {
-      const int j = p >> 3, k = p & 7;
-      const uint32_t e = S.fr[cur][j];
-      const int g = S.fg[cur][j];
-      const int kk = k + (k >= 4);  // skip the centre of the 3x3
-      const int yy = (int)(e >> 16) + kk / 3 - 1, xx = (int)(e & 0xffffu) + kk % 3 - 1;
-      bool ok = (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
-      const int t = yy * nx + xx;
-      int li = 0;
-      if (kBox) {
-        const int ry = yy - bb.r0, rx = xx - bb.c0;
-        // outside the grown box: never an a-site
-        ok = ok && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
-        li = ry * bb.bw + rx;
-        if (ok) {
-          const int cg = (int)((nib[li >> 3] >> (4 * (li & 7))) & 15u);
-          if (cg) {
-            if (cg != 15 && cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
-            ok = false;
-          }
-        }
-      } else if (ok) {
-        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
-        for (;;) {
-          const unsigned long long cv = S.key[h];
-          if (cv == kEmpty) break;
-          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
-            const int hg = (int)(cv & 0xff);
-            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
-            ok = false;
-            break;
-          }
-          h = (h + 1) & (kHW - 1);
-        }
-      }
-      if (!ok) continue;
-      const unsigned long long pk = ld_rlx64(A.wp + t);
-      const int32_t l0 = __ldg(Lp + t);
-      if (wp_pend(pk) < pos) {
-        atomicOr(&S.gblk, 1u << g);
-        S.bsite = t;
-        continue;
-      }
-      const int32_t lab = df_lab(pk, l0, pos);
-      if (lab != a) continue;
-      bool ins = false;
-      if (kBox) {
-        uint32_t *wp = nib + (li >> 3);
-        const int sh = 4 * (li & 7);
-        uint32_t w = *(volatile uint32_t *)wp;
-        for (;;) {
-          const int cg = (int)((w >> sh) & 15u);
-          if (cg) {
-            if (cg != 15 && cg - 1 != g) atomicOr(&S.unions[g], 1u << (cg - 1));
-            break;
-          }
-          const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
-          if (old == w) {
-            ins = true;
-            break;
-          }
-          w = old;
-        }
-      } else {
-        uint32_t h = hash32((uint32_t)t) & (kHW - 1);
-        const unsigned long long mine = ((unsigned long long)(uint32_t)t << 8) | (unsigned)g;
-        for (;;) {
-          unsigned long long cv = S.key[h];
-          if (cv == kEmpty) {
-            const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
-            if (old == kEmpty) {
-              ins = true;
-              break;
+    for (int base = 0; base < 8 * n; base += 96) {
+      int t[3], li[3], g[3], yy[3], xx[3];
+      bool ok[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int p = base + 32 * u + lane;
+        ok[u] = p < 8 * n;
+        const int j = ok[u] ? p >> 3 : 0, k = p & 7;
+        const uint32_t e = S.fr[cur][j];
+        g[u] = S.fg[cur][j];
+        const int kk = k + (k >= 4);  // skip the centre of the 3x3
+        yy[u] = (int)(e >> 16) + kk / 3 - 1;
+        xx[u] = (int)(e & 0xffffu) + kk % 3 - 1;
+        ok[u] = ok[u] && (unsigned)yy[u] < (unsigned)ny && (unsigned)xx[u] < (unsigned)nx;
+        t[u] = yy[u] * nx + xx[u];
+        li[u] = box_index(yy[u], xx[u], ok[u]);
+        if (ok[u]) {
+          if (kBox) {
+            const int cg = (int)((nib[li[u] >> 3] >> (4 * (li[u] & 7))) & 15u);
+            if (cg) {
+              if (cg != 15 && cg - 1 != g[u]) atomicOr(&S.unions[g[u]], 1u << (cg - 1));
+              ok[u] = false;
             }
-            cv = old;
+          } else {
+            uint32_t h = hash32((uint32_t)t[u]) & (kHW - 1);
+            for (;;) {
+              const unsigned long long cv = S.key[h];
+              if (cv == kEmpty) break;
+              if ((uint32_t)(cv >> 8) == (uint32_t)t[u]) {
+                const int hg = (int)(cv & 0xff);
+                if (hg != 255 && hg != g[u]) atomicOr(&S.unions[g[u]], 1u << hg);
+                ok[u] = false;
+                break;
+              }
+              h = (h + 1) & (kHW - 1);
+            }
           }
-          if ((uint32_t)(cv >> 8) == (uint32_t)t) {
-            const int hg = (int)(cv & 0xff);
-            if (hg != 255 && hg != g) atomicOr(&S.unions[g], 1u << hg);
-            break;
-          }
-          h = (h + 1) & (kHW - 1);
         }
-        if (ins && atomicAdd(&S.ninsert, 1) >= A.max_insert) S.overflow = 1;
       }
-      if (ins) {
-        atomicOr(&S.alive, 1u << g);
-        const int q = atomicAdd(&S.nfr[nxt], 1);
-        if (q < kFW) {
-          S.fr[nxt][q] = ((uint32_t)yy << 16) | (uint32_t)xx;
-          S.fg[nxt][q] = (uint8_t)g;
-        } else {
-          S.overflow = 1;
+      unsigned long long pk[3];
+      int32_t l0[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        pk[u] = ok[u] ? ld_rlx64(A.wp + t[u]) : ~0ull;
+        l0[u] = ok[u] ? __ldg(A.L + t[u]) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if (!ok[u]) continue;
+        if (wp_pend(pk[u]) < pos) {
+          // skipped as not-a for now; remembered for resuming
+          atomicOr(&S.gblk, 1u << g[u]);
+          S.bsite = t[u];
+          const int q = atomicAdd(&S.npq, 1);
+          if (q < kPQ) {
+            S.pq[q] = (uint32_t)t[u];
+            S.pqg[q] = (uint8_t)g[u];
+          }
+          continue;
         }
+        if (df_lab(pk[u], l0[u], pos) != a) continue;
+        if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u])) bfs_push(S, nxt, yy[u], xx[u], g[u]);
       }
     }
     __syncwarp();
     if (lane == 0) {
-      S.result = warp_verdict8(S);
-      S.nfr[cur] = 0;
+      const uint32_t alive = S.alive;
+      S.alive = 0;
+      S.lastalive = alive;
+      S.result = warp_verdict8(S, alive);
       S.levels += 1;
     }
     __syncwarp();
-    const int r = S.result;
-    __syncwarp();  // every lane has read the verdict before lane 0 may reuse S
+    int r = S.result;
+    __syncwarp();
+    if (r == 0 && S.npq <= kPQ) {
+      // a finished piece met pending sites: wait for them, then visit the
+      // settled ones from the groups that reached them and go on (the
+      // visited set and frontier stay valid: they hold settled sites only)
+      const int np = S.npq;
+      for (int q0 = 0; q0 < np; q0 += 32) {
+        const int q = q0 + lane;
+        const int64_t tq = q < np ? (int64_t)S.pq[q] : -1;
+        const unsigned long long v = warp_wait_settled(A, tq, pos);
+        if (tq >= 0) {
+          const int gq = S.pqg[q];
+          const int yq = (int)(tq / nx), xq = (int)(tq - (int64_t)yq * nx);
+          bool okq = true;
+          const int lq = box_index(yq, xq, okq);
+          if (okq && df_lab(v, __ldg(A.L + tq), pos) == a &&
+              bfs_visit<kBox>(A, S, nib, lq, (int)tq, gq))
+            bfs_push(S, nxt, yq, xq, gq);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        S.npq = 0;
+        S.gblk = 0;
+        const uint32_t alive = S.alive | S.lastalive;
+        S.alive = 0;
+        S.result = warp_verdict8(S, alive);
+      }
+      __syncwarp();
+      r = S.result;
+      __syncwarp();
+    }
+    if (lane == 0) S.nfr[cur] = 0;
+    __syncwarp();
     if (r >= 0) return r;
     cur = nxt;
   }
 }
+
 
 
 // ---------------------------------------------------------------------------
