@@ -1,9 +1,10 @@
 // K7 — rank composition, tie keys and the acceptance order
 // (optimizer.py:80-87 _tie_keys, :135-147 rank + np.lexsort).
 //
-// lexsort((comps, xs, ties, rank)) == a stable sort by tie followed by a
-// stable sort by rank, starting from the (x, comp) particle order that K1
-// already produces.  Non-negative ranks are never executed
+// lexsort((comps, xs, ties, rank)) orders by rank, then tie, then particle
+// (x, comp) order, which K1 already produces: one stable radix sort by rank
+// from particle order, then each run of equal ranks (exact ties are rare) is
+// ordered by (tie, particle).  Non-negative ranks are never executed
 // (optimizer.py:170-171), so they are keyed to the end and the acceptance
 // walk stops at the first of them.
 #include <cub/device/device_radix_sort.cuh>
@@ -32,31 +33,124 @@ __global__ void k_rank(const double *__restrict__ base, const int32_t *__restric
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(nneg, (unsigned long long)__popc(m));
 }
 
+// Runs of equal rank keys (rare: exact ties of the rank value) are put in
+// (tie key, particle index) order after the single stable sort by rank key,
+// which leaves each run in particle order.  Short runs: insertion sort by the
+// thread that finds the run; long runs (degenerate inputs): a block bitonic
+// sort in shared memory, or for runs beyond its capacity a serial sort.
+static constexpr int kShortRun = 32, kBitonic = 4096;
+
+__device__ __forceinline__ bool tie_less(const uint64_t *tie, uint32_t p, uint32_t q) {
+  const uint64_t a = tie[p], b = tie[q];
+  return a < b || (a == b && p < q);
+}
+
+__device__ void insertion_by_tie(uint32_t *o, int64_t len, const uint64_t *tie) {
+  for (int64_t i = 1; i < len; ++i) {
+    const uint32_t v = o[i];
+    int64_t j = i - 1;
+    while (j >= 0 && tie_less(tie, v, o[j])) {
+      o[j + 1] = o[j];
+      --j;
+    }
+    o[j + 1] = v;
+  }
+}
+
+__global__ void k_tie_runs(const uint64_t *__restrict__ key, int64_t n, uint32_t *__restrict__ order,
+                           const uint64_t *__restrict__ tie, int64_t *__restrict__ longs,
+                           unsigned long long *__restrict__ nlong) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = key[i];
+  if (k == ~0ull) return;                     // non-negative ranks: never executed
+  if (i > 0 && key[i - 1] == k) return;       // not a run start
+  if (i + 1 >= n || key[i + 1] != k) return;  // run of one
+  int64_t e = i + 1;
+  while (e < n && key[e] == k) ++e;
+  const int64_t len = e - i;
+  if (len <= kShortRun) {
+    insertion_by_tie(order + i, len, tie);
+  } else {
+    const unsigned long long slot = atomicAdd(nlong, 1ull);
+    longs[2 * slot] = i;
+    longs[2 * slot + 1] = len;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order,
+                                                    const uint64_t *__restrict__ tie,
+                                                    const int64_t *__restrict__ longs,
+                                                    const unsigned long long *__restrict__ nlong) {
+  __shared__ uint64_t sk[kBitonic];
+  __shared__ uint32_t sv[kBitonic];
+  const unsigned long long nr = *nlong;
+  for (unsigned long long r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int64_t start = longs[2 * r], len = longs[2 * r + 1];
+    uint32_t *o = order + start;
+    if (len > kBitonic) {
+      if (threadIdx.x == 0) insertion_by_tie(o, len, tie);
+      __syncthreads();
+      continue;
+    }
+    int m = 1;
+    while (m < len) m <<= 1;
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+      sv[t] = t < len ? o[t] : 0xffffffffu;
+      sk[t] = t < len ? tie[sv[t]] : ~0ull;
+    }
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < m; t += blockDim.x) {
+          const int u = t ^ stride;
+          if (u > t) {
+            const bool up = (t & size) == 0;
+            const bool gt = sk[t] > sk[u] || (sk[t] == sk[u] && sv[t] > sv[u]);
+            if (gt == up) {
+              const uint64_t tk = sk[t];
+              sk[t] = sk[u];
+              sk[u] = tk;
+              const uint32_t tv = sv[t];
+              sv[t] = sv[u];
+              sv[u] = tv;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int t = threadIdx.x; t < len; t += blockDim.x) o[t] = sv[t];
+    __syncthreads();
+  }
+}
+
 int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t n,
                    const uint32_t *px, const int32_t *pcomp, uint64_t seed, double *rank,
                    RankScratch &sc, uint32_t *order, unsigned long long *nneg, cudaStream_t s) {
   RCB_CUDA(cudaMemsetAsync(nneg, 0, sizeof(unsigned long long), s));
   if (n == 0) return RCB_OK;
   RCB_TRY(sc.tie.reserve(n, s));
-  RCB_TRY(sc.tie2.reserve(n, s));
   RCB_TRY(sc.rkey.reserve(n, s));
   RCB_TRY(sc.rkey2.reserve(n, s));
   RCB_TRY(sc.idx.reserve(n, s));
-  RCB_TRY(sc.idx2.reserve(n, s));
+  RCB_TRY(sc.tie2.reserve(n + 2, s));  // long-run list (start, length) + its count
   k_rank<<<grid_for(n, 256), 256, 0, s>>>(base, dint, lam, n, px, pcomp, seed, rank, sc.tie.p,
                                           sc.rkey.p, sc.idx.p, nneg);
   RCB_CUDA(cudaGetLastError());
-  // pass 1: stable by tie (carry the rank key along as the value's payload)
+  // one stable sort by rank key from particle (x, comp) order
   size_t b = 0;
-  RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, sc.tie.p, sc.tie2.p, sc.idx.p, sc.idx2.p, n,
+  RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, sc.rkey.p, sc.rkey2.p, sc.idx.p, order, n,
                                            0, 64, s));
   RCB_TRY(sc.tmp.reserve(b, s));
-  RCB_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp.p, b, sc.tie.p, sc.tie2.p, sc.idx.p, sc.idx2.p,
-                                           n, 0, 64, s));
-  // pass 2: stable by rank key of the tie-ordered particles
-  gather_u64(sc.rkey.p, sc.idx2.p, n, sc.rkey2.p, s);
-  RCB_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp.p, b, sc.rkey2.p, sc.rkey.p, sc.idx2.p, order, n,
+  RCB_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp.p, b, sc.rkey.p, sc.rkey2.p, sc.idx.p, order, n,
                                            0, 64, s));
+  // equal rank values: (tie key, particle) order, as lexsort's next keys
+  unsigned long long *nlong = reinterpret_cast<unsigned long long *>(sc.tie2.p + n);
+  RCB_CUDA(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), s));
+  int64_t *longs = reinterpret_cast<int64_t *>(sc.tie2.p);
+  k_tie_runs<<<grid_for(n, 256), 256, 0, s>>>(sc.rkey2.p, n, order, sc.tie.p, longs, nlong);
+  k_long_runs<<<64, 1024, 0, s>>>(order, sc.tie.p, longs, nlong);
+  RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
 

@@ -218,6 +218,36 @@ def test_engine_candidates_match_oracle(P):
         assert np.array_equal(rk, orank)
 
 
+@pytest.mark.parametrize("mode", ["dataflow", "rounds"])
+def test_rank_ties_noiseless_vs_oracle(P, mode, monkeypatch):
+    """A noiseless piecewise-constant image with straight edges gives long
+    runs of exactly equal rank values, so the acceptance order inside each
+    run comes from the tie keys and particle order alone (lexsort's later
+    keys): accepted moves and labels must match the oracle exactly."""
+    monkeypatch.setenv("RCB_ACCEPT", mode)
+    img = np.zeros((96, 96))
+    img[20:70, 16:60] = 1.0
+    img[50:90, 50:92] = 0.5
+    lab = np.zeros((96, 96), np.int32)
+    lab[8:88, 8:88] = 1
+    lab[40:60, 40:60] = 2
+    cfg = P.OptimizerConfig("sobolev")
+    eng = P.RegionCompetition(img, lab, P.EnergyConfig("pc", "gauss"), P.SobolevParams(4.0), cfg)
+    o = O.OracleEngine(img, lab, "pc", "gauss", 0.0, 8, 4.0)
+    longest = 0
+    for it in range(8):
+        rec = eng.iterate()
+        orec = o.iterate()
+        rk = eng.last_candidates[3]
+        _, cnt = np.unique(rk[rk < 0], return_counts=True)
+        longest = max(longest, int(cnt.max()) if cnt.size else 0)
+        want = np.asarray(orec.accepted, np.int64).reshape(-1, 3)
+        assert np.array_equal(eng.last_accepted, want), (mode, it)
+        assert np.array_equal(eng.labels, o.labels), (mode, it)
+        assert rec.energy == orec.energy, (mode, it)
+    assert longest > 32  # exercises the long-run (block bitonic) fix-up too
+
+
 def test_engine_invariants_at_full_cfg2_size(P):
     """Size-independent properties on the 1024^2 PS-Poisson config: the
     device contour equals a fresh scan, the ledger agrees with the from-scratch
