@@ -92,6 +92,7 @@ struct rcb_engine {
   int64_t iteration = 0;
   int mode = 1;
   bool prepared = false;
+  bool fields_fresh = false;  // stats/fields were just rebuilt from the raster (refresh)
   int64_t N = 0;  // particles of the current raster (valid when prepared)
   int64_t n_scored = 0, last_moves = 0;
 
@@ -123,7 +124,8 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows;
-  DBuf<unsigned long long> ufp, job, wpk;
+  DBuf<unsigned long long> ufp, job, wpk, eval_per;
+  DBuf<long long> eval_limbs;
   DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
   DBuf<long long> tdbg;
@@ -164,6 +166,7 @@ struct rcb_engine {
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
+      eval_per.release(s); eval_limbs.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -231,6 +234,16 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   auto *e = new rcb_engine();
   e->device = device;
   RCB_CUDA(cudaSetDevice(device));
+  {
+    // keep freed stream-ordered allocations cached in the device pool: the
+    // default release threshold (0) hands them back to the driver at every
+    // synchronisation, and re-mapping them costs milliseconds per resync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (stream) {
     e->s = (cudaStream_t)stream;
   } else {
@@ -344,6 +357,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
   cudaStream_t s = e->s;
   e->iteration += 1;
   e->launches = 0;
+  e->fields_fresh = false;
   cudaEventRecord(e->ev[0], s);
   if (!e->prepared) RCB_TRY(e->prepare());
   const int64_t n = e->N;
@@ -652,6 +666,7 @@ int32_t rcb_engine_set_labels(rcb_engine *e, const int32_t *labels) {
   for (int64_t i = 0; i < e->lat.V; ++i)
     if (labels[i] < 0 || labels[i] >= e->nl)
       return fail(RCB_ERR_VALUE, "labels outside the engine's label table");
+  e->fields_fresh = false;
   RCB_CUDA(cudaMemcpyAsync(e->L.p, labels, sizeof(int32_t) * e->lat.V, cudaMemcpyHostToDevice, e->s));
   RCB_TRY(e->components());
   RCB_TRY(e->prepare());
@@ -726,6 +741,7 @@ int32_t rcb_engine_refresh(rcb_engine *e) {
   RCB_CUDA(cudaSetDevice(e->device));
   RCB_TRY(e->refresh());
   RCB_CUDA(cudaStreamSynchronize(e->s));
+  e->fields_fresh = true;
   return RCB_OK;
 }
 
@@ -783,7 +799,28 @@ static int32_t evaluate_on(const int32_t *L, const double *I, const Lat &lat,
 
 int32_t rcb_engine_evaluate(rcb_engine *e, double *external, int64_t *internal) {
   RCB_CUDA(cudaSetDevice(e->device));
-  return evaluate_on(e->L.p, e->I.p, e->lat, &e->ecfg, e->nl, external, internal, e->s);
+  if (!e->fields_fresh)
+    return evaluate_on(e->L.p, e->I.p, e->lat, &e->ecfg, e->nl, external, internal, e->s);
+  // right after refresh(): the engine's statistics / own-label fields are the
+  // from-scratch ones of the current raster (same kernels as evaluate_on), so
+  // only the exact term sums and the perimeter remain
+  cudaStream_t s = e->s;
+  RCB_TRY(e->eval_limbs.reserve(kLimbs, s));
+  RCB_TRY(e->eval_per.reserve(1, s));
+  const int poisson = e->ecfg.noise_model == 1;
+  if (e->ecfg.region_model == 0)
+    RCB_TRY(pc_terms_exact(e->cnt.p, e->tot.p, e->tsq.p, e->nl, poisson, e->eval_limbs.p, s));
+  else
+    RCB_TRY(ps_terms_exact(e->Cown.p, e->Sown.p, e->I.p, e->lat.V, poisson, e->eval_limbs.p, s));
+  RCB_TRY(perimeter(e->L.p, e->lat, e->eval_per.p, s));
+  long long hl[kLimbs];
+  unsigned long long hp = 0;
+  RCB_CUDA(cudaMemcpyAsync(hl, e->eval_limbs.p, sizeof(hl), cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaMemcpyAsync(&hp, e->eval_per.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  *external = limbs_to_double(hl);
+  *internal = (int64_t)hp;
+  return RCB_OK;
 }
 
 int32_t rcb_engine_stream(rcb_engine *e, void **stream) {
