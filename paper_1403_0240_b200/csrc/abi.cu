@@ -243,6 +243,12 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
       uint64_t keep = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
+    // reserve the acceptance kernels' per-thread stack once: otherwise the
+    // local-memory reservation is re-grown (milliseconds) whenever a launch
+    // needs more than the previous one left in place
+    size_t stack = 0;
+    if (cudaDeviceGetLimit(&stack, cudaLimitStackSize) == cudaSuccess && stack < 2048)
+      cudaDeviceSetLimit(cudaLimitStackSize, 2048);
   }
   if (stream) {
     e->s = (cudaStream_t)stream;
@@ -256,6 +262,15 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   };
   cudaStream_t s = e->s;
   e->lat = make_lat(ndim, dims);
+  {
+    // prime the device pool with about the engine's footprint (~160 B per
+    // site): later stream-ordered allocations are then served from cached
+    // memory instead of blocking the host while new memory is mapped
+    void *prime = nullptr;
+    if (cudaMallocAsync(&prime, (size_t)160 * (size_t)e->lat.V + ((size_t)64 << 20), s) == cudaSuccess)
+      cudaFreeAsync(prime, s);
+    cudaGetLastError();
+  }
   e->ecfg = *ecfg;
   e->ocfg = *ocfg;
   e->mode = ocfg->gradient;

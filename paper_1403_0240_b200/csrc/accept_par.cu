@@ -1634,6 +1634,116 @@ __device__ int window31(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
   return verdict31(P | U, seeds) == 2 ? 2 : 0;
 }
 
+// ---------------------------------------------------------------------------
+// 63x63 window test, same rules as window31: lane l holds rows l (a) and
+// l + 32 (b) as 64-bit masks; rows above 62 are empty.
+// ---------------------------------------------------------------------------
+static constexpr int kW63 = 63, kR63 = 31;
+
+__device__ __forceinline__ void flood63(uint64_t &a, uint64_t &b, uint64_t ca, uint64_t cb) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    uint64_t ua = __shfl_up_sync(0xffffffffu, a, 1), da = __shfl_down_sync(0xffffffffu, a, 1);
+    uint64_t ub = __shfl_up_sync(0xffffffffu, b, 1), db = __shfl_down_sync(0xffffffffu, b, 1);
+    const uint64_t a31 = __shfl_sync(0xffffffffu, a, 31), b0 = __shfl_sync(0xffffffffu, b, 0);
+    if (lane == 0) {
+      ua = 0;    // row -1
+      ub = a31;  // row 31 above row 32
+    }
+    if (lane == 31) {
+      da = b0;   // row 32 below row 31
+      db = 0;    // row 64
+    }
+    uint64_t va = a | ua | da, vb = b | ub | db;
+    va = (va | (va << 1) | (va >> 1)) & ca;
+    vb = (vb | (vb << 1) | (vb >> 1)) & cb;
+    if (!__any_sync(0xffffffffu, va != a || vb != b)) return;
+    a = va;
+    b = vb;
+  }
+}
+
+__device__ __noinline__ int verdict63(uint64_t ca, uint64_t cb, uint64_t sa, uint64_t sb) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t rimc = 1ull | (1ull << (kW63 - 1));
+  uint64_t ra = sa, rb = sb;
+  bool first = true;
+  for (;;) {
+    const unsigned ba = __ballot_sync(0xffffffffu, ra != 0), bb = __ballot_sync(0xffffffffu, rb != 0);
+    if (!ba && !bb) return 0;
+    uint64_t xa = 0, xb = 0;
+    if (ba) {
+      const int l = __ffs(ba) - 1;
+      const uint64_t low = __shfl_sync(0xffffffffu, ra & (~ra + 1), l);
+      if (lane == l) xa = low;
+    } else {
+      const int l = __ffs(bb) - 1;
+      const uint64_t low = __shfl_sync(0xffffffffu, rb & (~rb + 1), l);
+      if (lane == l) xb = low;
+    }
+    flood63(xa, xb, ca, cb);
+    const bool all = !__any_sync(0xffffffffu, ((ra & ~xa) | (rb & ~xb)) != 0);
+    ra &= ~xa;
+    rb &= ~xb;
+    if (first && all) return 1;
+    first = false;
+    // rim: rows 0 and 62 (lane 0's a, lane 30's b), columns 0 and 62
+    const bool rim = (xa & rimc) || (xb & rimc) || (lane == 0 && xa) || (lane == 30 && xb);
+    if (!__any_sync(0xffffffffu, rim)) return 2;
+  }
+}
+
+__device__ __noinline__ int window63(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
+  const int lane = threadIdx.x & 31;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
+  const int fy = (int)(f / nx), fx = (int)(f % nx);
+  uint64_t Pa = 0, Pb = 0, Ua = 0, Ub = 0;  // rows lane / lane + 32: settled a-cells, pending
+  for (int rb = 0; rb < kW63; rb += 4) {
+    int t[8];
+    bool in[8];
+    unsigned long long pk[8];
+    int32_t l0[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = rb + (i >> 1), c = (i & 1) * 32 + lane;
+      const int yy = fy - kR63 + r, xx = fx - kR63 + c;
+      in[i] = r < kW63 && c < kW63 && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx &&
+              !(r == kR63 && c == kR63);
+      t[i] = yy * nx + xx;
+      pk[i] = in[i] ? ld_rlx64(A.wp + t[i]) : ~0ull;
+      l0[i] = in[i] ? __ldg(A.L + t[i]) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      uint64_t mp = 0, mu = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool st = in[i + h] && wp_pend(pk[i + h]) >= pos;
+        const int32_t lab = st ? df_lab(pk[i + h], l0[i + h], pos) : -1;
+        mp |= (uint64_t)__ballot_sync(0xffffffffu, st && lab == a) << (32 * h);
+        mu |= (uint64_t)__ballot_sync(0xffffffffu, in[i + h] && !st) << (32 * h);
+      }
+      const int r = rb + (i >> 1);
+      if (r < 32 && lane == r) {
+        Pa = mp;
+        Ua = mu;
+      } else if (r >= 32 && lane == r - 32) {
+        Pb = mp;
+        Ub = mu;
+      }
+    }
+  }
+  // seeds: the settled a-cells of x's box: rows 30, 31 (lanes 30, 31, a) and
+  // 32 (lane 0, b), columns 30..32 without the centre
+  const uint64_t c3 = 7ull << (kR63 - 1);
+  const uint64_t sa = Pa & ((lane == 30) ? c3 : (lane == 31) ? (c3 & ~(1ull << kR63)) : 0ull);
+  const uint64_t sb = Pb & (lane == 0 ? c3 : 0ull);
+  const bool anyU = __any_sync(0xffffffffu, (Ua | Ub) != 0);
+  const int rp = verdict63(Pa, Pb, sa, sb);
+  if (rp == 1 || !anyU) return rp;
+  return verdict63(Pa | Ua, Pb | Ub, sa, sb) == 2 ? 2 : 0;
+}
+
 __device__ __forceinline__ int first_zero_byte(uint32_t w) {
   const uint32_t z = (w - 0x01010101u) & ~w & 0x80808080u;  // exact for the lowest zero byte
   return z ? (__ffs(z) - 1) >> 3 : 4;
@@ -1959,6 +2069,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         wb = window31(A, pos, f, a);
         dbg += 10000000 * (wb + 1);
       }
+      if (wb == 0) {
+        wb = window63(A, pos, f, a);
+        dbg += 1000000 * (wb + 1);
+      }
       if (wb == 2) {
         d = REJ;
       } else if (wb == 0) {
@@ -1998,7 +2112,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
           dbg += 1000000000 + 2;
         }
         if (r == 2) d = REJ;
-        dbg += 10 * (r + 1) + 10000 * (S.levels < 999 ? S.levels : 999);  // +1e7 w31, +1e8 box, +1e9 job
+        dbg += 10 * (r + 1) + 10000 * (S.levels < 99 ? S.levels : 99);  // +1e6 w63, +1e7 w31, +1e8 box, +1e9 job
       }
     }
     if (d == ACC && b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b)) d = REJ;

@@ -8,6 +8,9 @@
 // fp64 parity: every translation unit is compiled with -fmad=false, so
 // a*b+c is two IEEE roundings exactly as numpy evaluates it.
 #pragma once
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -84,9 +87,14 @@ struct DBuf {
   size_t cap = 0;  // elements
   int32_t reserve(size_t n, cudaStream_t s) {
     if (n <= cap) return RCB_OK;
+    const auto t0 = std::chrono::steady_clock::now();
     if (p) cudaFreeAsync(p, s);
-    size_t want = n + n / 4 + 64;
+    size_t want = 2 * n + 64;  // geometric growth: particle counts climb for tens of iterations
     cudaError_t e = cudaMallocAsync((void **)&p, want * sizeof(T), s);
+    if (getenv("RCB_ALLOC_LOG")) {
+      const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+      fprintf(stderr, "[rcb-alloc] %zu bytes %.1f us\n", want * sizeof(T), us);
+    }
     if (e != cudaSuccess) {
       p = nullptr;
       cap = 0;

@@ -49,6 +49,9 @@ code = code % 100000000
 w31 = code // 10000000 - 1
 print('window31 runs', int((w31 >= 0).sum()), 'verdicts 1/2/0:', int((w31 == 1).sum()), int((w31 == 2).sum()), int((w31 == 0).sum()))
 code = code % 10000000
+w63 = code // 1000000 - 1
+print('window63 runs', int((w63 >= 0).sum()), 'verdicts 1/2/0:', int((w63 == 1).sum()), int((w63 == 2).sum()), int((w63 == 0).sum()))
+code = code % 1000000
 lv = code // 10000
 bfs = lv > 0
 print("BFS candidates", int(bfs.sum()), "levels p50/p90/p99/max", np.percentile(lv[bfs], [50, 90, 99, 100]) if bfs.any() else None)
