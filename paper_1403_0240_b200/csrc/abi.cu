@@ -123,7 +123,7 @@ struct rcb_engine {
   DBuf<uint32_t> evkey, evkey2, evval, evval2;
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
-  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows;
+  DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
   DBuf<unsigned long long> ufp, job, wpk, eval_per;
   DBuf<long long> eval_limbs;
   DBuf<int4> rec;
@@ -164,7 +164,7 @@ struct rcb_engine {
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
-      bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s);
+      bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       eval_per.release(s); eval_limbs.release(s);
       labbounds.release(s);
@@ -564,6 +564,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.labpos2 = &e->labpos2;
       X.flrows = &e->flrows;
       X.rec = &e->rec;
+      X.colb = &e->colb;
       X.labbounds = &e->labbounds;
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));

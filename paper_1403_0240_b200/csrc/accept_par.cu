@@ -2400,6 +2400,264 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// PS ledger terms, 2-D: the same quantities as k_ps_dtot with the latency
+// taken out.  Each kept flip has a packed record (site, move index, old and
+// new label) and its value in flip-index order, and every row has a column
+// bucket index (16 columns per bucket), so the flips near a move come from
+// two loads per window row and are fetched by all lanes at once.  The ball
+// sites and the centre are items (IPL per lane) whose loads are all issued
+// in one round; the ordered sums are replayed by lane 0 in offset order as
+// before, so every fp64 expression is the one of k_ps_dtot.
+// ---------------------------------------------------------------------------
+static constexpr int kColB = 16;  // columns per flip bucket
+
+__global__ void k_flip_recs(const uint32_t *__restrict__ fsite, const int32_t *__restrict__ fk,
+                            const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                            const double *__restrict__ I, int4 *__restrict__ frec,
+                            double *__restrict__ fval) {
+  const int64_t n = *moves;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    const uint32_t g = fsite[e];
+    const int32_t k = fk[e];
+    frec[e] = make_int4((int32_t)g, k, (int32_t)acc[3 * (int64_t)k + 1], (int32_t)acc[3 * (int64_t)k + 2]);
+    fval[e] = I[g];
+  }
+}
+
+// colb[r * nbk + c] = first flip of row r with column >= kColB * c
+__global__ void k_flip_cols(const uint32_t *__restrict__ fsite, const int32_t *__restrict__ rstart,
+                            const int32_t *__restrict__ rend, int64_t rows, int64_t nx, int nbk,
+                            int32_t *__restrict__ colb) {
+  const int64_t tot = rows * nbk;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += stride) {
+    const int64_t r = i / nbk;
+    const int c = (int)(i - r * nbk);
+    int32_t lo = rstart[r], hi = rend[r];
+    const uint32_t first = (uint32_t)(r * nx + (int64_t)c * kColB);
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (fsite[mid] < first)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    colb[i] = lo;
+  }
+}
+
+struct FlipList2 {
+  int8_t dy[kFlipCap], dx[kFlipCap];
+  int32_t oldl[kFlipCap], newl[kFlipCap];
+  double val[kFlipCap];
+  int n;
+};
+static constexpr int kPsWarps = 4;
+
+template <int IPL>
+__global__ void __launch_bounds__(32 * kPsWarps) k_ps_dtot2d(
+    const ParArgs A, const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+    const double *__restrict__ I, const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
+    const Off *__restrict__ ball, int nball, int R, int poisson, double lam,
+    double *__restrict__ dtot, const int4 *__restrict__ frec, const double *__restrict__ fval,
+    const int32_t *__restrict__ colb, int nbk, const double *__restrict__ rho0,
+    const int32_t *__restrict__ cb0, const double *__restrict__ sb0) {
+  __shared__ FlipList2 fls[kPsWarps];
+  __shared__ double tta[kPsWarps][32 * IPL], ttb[kPsWarps][32 * IPL], tib[kPsWarps][32 * IPL];
+  const int64_t n = *moves;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  FlipList2 &F = fls[wl];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
+  const int R2 = R * R, R2w = 4 * R2, nit = nball + 1;  // items: ball offsets, then the centre
+  for (int64_t k = warp; k < n; k += nwarps) {
+    const int32_t f = (int32_t)acc[3 * k];
+    const int32_t a = (int32_t)acc[3 * k + 1], b = (int32_t)acc[3 * k + 2];
+    const int y = f / nx, x = f - y * nx;
+    // 1. every item's loads, one round
+    int t[IPL], oy[IPL], ox[IPL];
+    bool in[IPL];
+    int32_t wv[IPL], l0[IPL], nl[IPL], cw[IPL];
+    double sw[IPL], iv[IPL], r0[IPL];
+#pragma unroll
+    for (int u = 0; u < IPL; ++u) {
+      const int it = u * 32 + lane;
+      oy[u] = 0;
+      ox[u] = 0;
+      if (it < nball) {
+        const Off o = ball[it];
+        oy[u] = o.dy;
+        ox[u] = o.dx;
+      }
+      const int yy = y + oy[u], xx = x + ox[u];
+      in[u] = it < nit && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+      t[u] = in[u] ? yy * nx + xx : f;
+      wv[u] = in[u] ? ld(A.w + t[u]) : kInf;
+      l0[u] = in[u] ? __ldg(A.L + t[u]) : -1;
+      nl[u] = in[u] ? ld(A.newlab + t[u]) : -1;
+      cw[u] = in[u] ? Cown[t[u]] : 0;
+      sw[u] = in[u] ? Sown[t[u]] : 0.0;
+      iv[u] = in[u] ? I[t[u]] : 0.0;
+      r0[u] = (in[u] && rho0) ? rho0[t[u]] : 0.0;
+    }
+    // the move's own position: w at the centre item
+    const int cl = nball & 31, cu = nball >> 5;
+    int32_t wc = 0;
+#pragma unroll
+    for (int u = 0; u < IPL; ++u)
+      if (u == cu) wc = wv[u];
+    const int32_t pos = __shfl_sync(0xffffffffu, wc, cl);
+    // 2. flips of earlier moves within 2R: bucket ranges of the window rows
+    if (lane == 0) F.n = 0;
+    __syncwarp();
+    if (lane <= 4 * R) {
+      const int ddy = lane - 2 * R, yy = y + ddy;
+      if ((unsigned)yy < (unsigned)ny) {
+        const int c0 = (x - 2 * R) < 0 ? 0 : (x - 2 * R) / kColB;
+        int c1 = (x + 2 * R) / kColB + 1;
+        if (c1 > nbk - 1) c1 = nbk - 1;
+        const int32_t lo = colb[(int64_t)yy * nbk + c0], hi = colb[(int64_t)yy * nbk + c1];
+        const int rowbase = yy * nx;
+        for (int32_t e = lo; e < hi; ++e) {
+          const int4 rc = __ldg(frec + e);
+          const int ddx = rc.x - rowbase - x;
+          if (rc.y >= k || ddx < -2 * R || ddx > 2 * R || ddy * ddy + ddx * ddx > R2w) continue;
+          const int slot = atomicAdd(&F.n, 1);
+          if (slot < kFlipCap) {
+            F.dy[slot] = (int8_t)ddy;
+            F.dx[slot] = (int8_t)ddx;
+            F.oldl[slot] = rc.z;
+            F.newl[slot] = rc.w;
+            F.val[slot] = __ldg(fval + e);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const int nf = F.n;
+    const bool list_ok = nf <= kFlipCap;
+    if (lane == 0) atomicAdd(A.ctl + 15, nf);  // diagnostics: flips per move
+    const double vx = I[f];
+    // 3. per item: label in the view, own field at pos, its term
+    int di = 0;
+    double ra_c = 0.0;  // centre: r_old of a at x
+    unsigned ma[IPL], mb[IPL];
+#pragma unroll
+    for (int u = 0; u < IPL; ++u) {
+      const int it = u * 32 + lane;
+      double term_a = 0.0, term_b = 0.0, ib = 0.0;
+      bool hit_a = false, hit_b = false;
+      if (in[u]) {
+        const bool flipped = wv[u] < pos;
+        const int32_t lg = flipped ? nl[u] : l0[u];
+        const bool centre = it == nball;
+        if (!centre && (oy[u] == 0) != (ox[u] == 0) && (oy[u] * oy[u] + ox[u] * ox[u] == 1))
+          di += (int)(lg != b) - (int)(lg != a);
+        if (centre || lg == a || lg == b) {
+          const int32_t lgx = centre ? a : lg;
+          int32_t c = 0;
+          double sv = 0.0;
+          bool clean = false;
+          if (list_ok && !flipped) {
+            c = cw[u];
+            sv = sw[u];
+            bool touched = false;
+            for (int e = 0; e < nf; ++e) {
+              const int ey = F.dy[e] - oy[u], ex = F.dx[e] - ox[u];
+              if (ey * ey + ex * ex > R2) continue;
+              if (F.newl[e] == lgx) {
+                c += 1;
+                sv += F.val[e];
+                touched = true;
+              }
+              if (F.oldl[e] == lgx) {
+                c -= 1;
+                sv -= F.val[e];
+                touched = true;
+              }
+            }
+            clean = !touched;
+          } else if (list_ok && cb0) {
+            const uint32_t pg = A.order[wv[u]];
+            c = cb0[pg];
+            sv = sb0[pg];
+            for (int e = 0; e < nf; ++e) {
+              const int ey = F.dy[e] - oy[u], ex = F.dx[e] - ox[u];
+              if (ey * ey + ex * ex > R2) continue;
+              if (F.newl[e] == lgx) {
+                c += 1;
+                sv += F.val[e];
+              }
+              if (F.oldl[e] == lgx) {
+                c -= 1;
+                sv -= F.val[e];
+              }
+            }
+          } else {
+            // slow path: recount the ball of the item's site in the view
+            atomicAdd(A.ctl + 14, 1);
+            View v{A, pos};
+            const int gy = y + oy[u], gx = x + ox[u];
+            for (int q = 0; q <= nball; ++q) {
+              const int y2 = gy + (q == 0 ? 0 : ball[q - 1].dy), x2 = gx + (q == 0 ? 0 : ball[q - 1].dx);
+              if ((unsigned)y2 >= (unsigned)ny || (unsigned)x2 >= (unsigned)nx) continue;
+              const int h = y2 * nx + x2;
+              if (v.lab(h) != lgx) continue;
+              c += 1;
+              sv += I[h];
+            }
+          }
+          const double cy = (double)c, iy = iv[u];
+          const double r_old = (clean && rho0) ? r0[u] : rho(iy, sv / cy, poisson);
+          if (centre) {
+            ra_c = r_old;
+          } else if (lg == a) {
+            term_a = rho(iy, (sv - vx) / (cy - 1.0), poisson) - r_old;
+            hit_a = true;
+          } else {
+            term_b = rho(iy, (sv + vx) / (cy + 1.0), poisson) - r_old;
+            hit_b = true;
+            ib = iy;
+          }
+        }
+      }
+      tta[wl][it] = term_a;
+      ttb[wl][it] = term_b;
+      tib[wl][it] = ib;
+      ma[u] = __ballot_sync(0xffffffffu, hit_a);
+      mb[u] = __ballot_sync(0xffffffffu, hit_b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) di += __shfl_xor_sync(0xffffffffu, di, o);
+    const double rac = __shfl_sync(0xffffffffu, ra_c, cl);
+    __syncwarp();
+    // 4. ordered sums in offset order (np.bincount order), lane 0
+    if (lane == 0) {
+      double ta = 0.0, tb = 0.0, sb = 0.0;
+      int cb = 0;
+#pragma unroll
+      for (int u = 0; u < IPL; ++u) {
+        for (unsigned m = ma[u]; m; m &= m - 1) ta += tta[wl][u * 32 + __ffs(m) - 1];
+        for (unsigned m = mb[u]; m; m &= m - 1) {
+          const int it = u * 32 + __ffs(m) - 1;
+          tb += ttb[wl][it];
+          cb += 1;
+          sb += tib[wl][it];
+        }
+      }
+      double d = 0.0 + ta;
+      d = d + tb;
+      d += rho(vx, (sb + vx) / ((double)cb + 1.0), poisson);
+      d -= rac;
+      dtot[k] = d + lam * (double)di;
+    }
+    __syncwarp();
+  }
+}
+
 // Flip index of the kept moves: sites sorted ascending (row-major), per
 // lattice row [start, end) into the sorted list; used by k_ps_dtot.
 __global__ void k_flip_keys(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
@@ -2758,12 +3016,37 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaMemsetAsync(X.flrows->p, 0, sizeof(int32_t) * 2 * rows, s));
     k_flip_rows<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, N, A.lat.nx, X.flrows->p,
                                                  X.flrows->p + rows);
-    T.mark("flip-index");
-    k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
-                                      X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
-                                      X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0, X.cb0,
-                                      X.sb0);
-    ++nl;
+    const int ipl = (X.nball + 1 + 31) / 32;
+    if (A.lat.ndim == 2 && ipl <= 4) {
+      const int nbk = (int)((A.lat.nx + kColB - 1) / kColB) + 1;
+      RCB_TRY(X.rec->reserve(N, s));
+      RCB_TRY(X.snap->reserve(N, s));
+      RCB_TRY(X.colb->reserve(rows * nbk, s));
+      int4 *frec = X.rec->p;  // the dataflow records are no longer needed here
+      double *fval = X.snap->p;
+      k_flip_recs<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, X.labpos->p, X.acc, X.moves, X.I,
+                                                   frec, fval);
+      k_flip_cols<<<grid_for(rows * nbk, 256), 256, 0, s>>>(X.evkey2->p, X.flrows->p,
+                                                            X.flrows->p + rows, rows, A.lat.nx,
+                                                            nbk, X.colb->p);
+      T.mark("flip-index");
+      if (ipl <= 2)
+        k_ps_dtot2d<2><<<148 * 16, 32 * kPsWarps, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball,
+                                               X.nball, X.radius, X.poisson, X.lam, X.dtot, frec,
+                                               fval, X.colb->p, nbk, X.rho0, X.cb0, X.sb0);
+      else
+        k_ps_dtot2d<4><<<148 * 16, 32 * kPsWarps, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball,
+                                               X.nball, X.radius, X.poisson, X.lam, X.dtot, frec,
+                                               fval, X.colb->p, nbk, X.rho0, X.cb0, X.sb0);
+      nl += 3;
+    } else {
+      T.mark("flip-index");
+      k_ps_dtot<<<148 * 8, 256, 0, s>>>(A, X.acc, X.moves, X.I, X.Cown, X.Sown, X.ball, X.nball,
+                                        X.radius, X.poisson, X.lam, X.dtot, X.evkey2->p,
+                                        X.labpos->p, X.flrows->p, X.flrows->p + rows, X.rho0, X.cb0,
+                                        X.sb0);
+      ++nl;
+    }
   }
   T.mark("ps-dtot");
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger

@@ -126,6 +126,7 @@ struct ParExtra {
   DBuf<uint64_t> *labkey, *labkey2;
   DBuf<int32_t> *labpos, *labpos2, *flrows;
   DBuf<int4> *rec;
+  DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
 };
 
