@@ -263,12 +263,14 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   cudaStream_t s = e->s;
   e->lat = make_lat(ndim, dims);
   {
-    // prime the device pool with about the engine's footprint (~160 B per
-    // site): later stream-ordered allocations are then served from cached
-    // memory instead of blocking the host while new memory is mapped
+    // prime the device pool with the engine's footprint plus room for the
+    // particle buffers to double a few times (~320 B per site + 256 MB,
+    // at most 16 GB): later stream-ordered allocations are then served
+    // from cached memory instead of blocking the host while memory is mapped
+    size_t want = (size_t)320 * (size_t)e->lat.V + ((size_t)256 << 20);
+    if (want > ((size_t)16 << 30)) want = (size_t)16 << 30;
     void *prime = nullptr;
-    if (cudaMallocAsync(&prime, (size_t)160 * (size_t)e->lat.V + ((size_t)64 << 20), s) == cudaSuccess)
-      cudaFreeAsync(prime, s);
+    if (cudaMallocAsync(&prime, want, s) == cudaSuccess) cudaFreeAsync(prime, s);
     cudaGetLastError();
   }
   e->ecfg = *ecfg;

@@ -88,6 +88,77 @@ __global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restri
   }
 }
 
+// K5 for 2-D lattices (the common case): one pass over the ball per particle
+// with 32-bit coordinates and the offsets staged in shared memory; loads for
+// kChunk offsets are issued before any is used.  The a-terms and b-terms are
+// still two separate sequential sums in ball-offset order, so the result is
+// bit-identical to delta_ps (dev.cuh).
+static constexpr int kPsChunk = 8, kPsMaxBall = 1024;
+
+__global__ void __launch_bounds__(128) k_delta_ps2d(
+    const int32_t *__restrict__ L, const double *__restrict__ I, const int32_t *__restrict__ Cown,
+    const double *__restrict__ Sown, int nx, int ny, const Off *__restrict__ ball, int nball,
+    const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+    const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
+    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0) {
+  __shared__ int8_t sdy[kPsMaxBall], sdx[kPsMaxBall];
+  for (int k = threadIdx.x; k < nball; k += blockDim.x) {
+    sdy[k] = ball[k].dy;
+    sdx[k] = ball[k].dx;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int f = (int)px[i];
+  const int y = f / nx, x = f - y * nx;
+  const int32_t a = pown[i], b = pcomp[i];
+  const double v = I[f];
+  double acc_a = 0.0, acc_b = 0.0, sb = 0.0;
+  int32_t cb = 0;
+  for (int k0 = 0; k0 < nball; k0 += kPsChunk) {
+    int g[kPsChunk];
+    int32_t lab[kPsChunk];
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      const int k = k0 + u;
+      const int yy = y + (k < nball ? sdy[k] : 0), xx = x + (k < nball ? sdx[k] : 0);
+      const bool ok = k < nball && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+      g[u] = ok ? yy * nx + xx : f;
+      lab[u] = ok ? __ldg(L + g[u]) : -1;
+    }
+    double cy[kPsChunk], sy[kPsChunk], iy[kPsChunk], r0[kPsChunk];
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      const bool need = lab[u] == a || lab[u] == b;
+      cy[u] = need ? (double)__ldg(Cown + g[u]) : 1.0;
+      sy[u] = need ? __ldg(Sown + g[u]) : 0.0;
+      iy[u] = need ? __ldg(I + g[u]) : 0.0;
+      r0[u] = (need && rho0) ? __ldg(rho0 + g[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      if (lab[u] == a) {
+        acc_a += rho(iy[u], (sy[u] - v) / (cy[u] - 1.0), poisson) -
+                 (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+      } else if (lab[u] == b) {
+        acc_b += rho(iy[u], (sy[u] + v) / (cy[u] + 1.0), poisson) -
+                 (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+        cb += 1;
+        sb += iy[u];
+      }
+    }
+  }
+  double d = 0.0 + acc_a;
+  d = d + acc_b;
+  d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
+  d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
+  out[i] = d;
+  if (cb0) {  // the competitor's iteration-start ball count/sum at x (PS ledger terms)
+    cb0[i] = cb;
+    sb0[i] = sb;
+  }
+}
+
 // fp32 gradient path (dev.cuh: delta_pc32 / delta_ps32); outputs in float
 // (for K6) and double (rank composition in l2 mode).
 __global__ void k_delta_pc32(const float *__restrict__ I32, const uint32_t *__restrict__ px,
@@ -192,8 +263,13 @@ int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, c
                        double *out, cudaStream_t s, const double *rho0, int32_t *cb0,
                        double *sb0) {
   if (n == 0) return RCB_OK;
-  k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown, pcomp,
-                                              n, poisson, out, rho0, cb0, sb0);
+  if (lat.ndim == 2 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
+    k_delta_ps2d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny, ball,
+                                                  nball, px, pown, pcomp, n, poisson, out, rho0,
+                                                  cb0, sb0);
+  else
+    k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown,
+                                                pcomp, n, poisson, out, rho0, cb0, sb0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
