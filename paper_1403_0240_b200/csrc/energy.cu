@@ -93,9 +93,9 @@ __global__ void k_delta_ps(const int32_t *__restrict__ L, const double *__restri
 // kChunk offsets are issued before any is used.  The a-terms and b-terms are
 // still two separate sequential sums in ball-offset order, so the result is
 // bit-identical to delta_ps (dev.cuh).
-static constexpr int kPsChunk = 8, kPsMaxBall = 1024;
+static constexpr int kPsChunk = 4, kPsMaxBall = 1024;
 
-__global__ void __launch_bounds__(128) k_delta_ps2d(
+__global__ void __launch_bounds__(128, 6) k_delta_ps2d(
     const int32_t *__restrict__ L, const double *__restrict__ I, const int32_t *__restrict__ Cown,
     const double *__restrict__ Sown, int nx, int ny, const Off *__restrict__ ball, int nball,
     const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
