@@ -125,7 +125,7 @@ struct rcb_engine {
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
   DBuf<unsigned long long> ufp, job, wpk, eval_per;
-  DBuf<long long> eval_limbs;
+  DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
   DBuf<long long> tdbg;
@@ -166,7 +166,7 @@ struct rcb_engine {
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
-      eval_per.release(s); eval_limbs.release(s);
+      eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       cudaStreamSynchronize(s);
@@ -347,7 +347,7 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   TRYB(e->cnt0.reserve(e->nl, s));
   TRYB(e->ctl.reserve(16, s));
   TRYB(e->lab_ptr.reserve(e->nl, s));
-  TRYB(e->lbox.reserve(4 * e->nl, s));
+  TRYB(e->lbox.reserve(6 * e->nl, s));
   if (cudaMemsetAsync(e->wpos.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->pend.p, 0x7f, sizeof(int32_t) * V, s) != cudaSuccess ||
       cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s) != cudaSuccess)
@@ -490,9 +490,12 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
         RCB_TRY(e->tdbg.reserve(4 * n, s));
         P.tdbg = e->tdbg.p;
       }
-      // dataflow kernel: 2-D with sides < 2^16 (packed BFS coordinates)
-      const bool use_df = lat.ndim == 2 && e->accept_mode != 1 && lat.nx < 65536 &&
-                          lat.ny < 65536 && n < 0xffffff && e->nl <= 65536;
+      // dataflow kernel (K8 v3): packed BFS coordinates need sides < 2^16 in
+      // 2-D and < 2^11 (x, y), < 2^10 (z) in 3-D; site words hold 24-bit
+      // positions and 16-bit labels
+      const bool fits = lat.ndim == 2 ? (lat.nx < 65536 && lat.ny < 65536)
+                                      : (lat.nx < 2048 && lat.ny < 2048 && lat.nz < 1024);
+      const bool use_df = fits && e->accept_mode != 1 && n < 0xffffff && e->nl <= 65536;
       if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufp.reserve(lat.V, s));
@@ -566,6 +569,8 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       X.labpos2 = &e->labpos2;
       X.flrows = &e->flrows;
       X.rec = &e->rec;
+      RCB_TRY(e->band.reserve(kLimbs + 2, s));
+      X.band = e->band.p;
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
       int nla = 0;

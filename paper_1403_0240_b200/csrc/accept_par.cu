@@ -144,6 +144,30 @@ __device__ __forceinline__ int box_local_count(const int32_t *lab, int32_t a) {
   return (cells & ~reach) ? 2 : 1;
 }
 
+// Seed groups for the BFS tiers: the a-cells of x's box (x excluded), one
+// group per box-local component (<= 4 in 2-D, <= 8 in 3-D); returns the
+// cell mask, fills grp[k] and the group count.
+__device__ __forceinline__ uint32_t box_groups(const int32_t *lab, int32_t a, uint8_t *grp,
+                                               int &ngrp) {
+  uint32_t cells = 0;
+  for (int k = 0; k < 27; ++k)
+    if (k != 13 && lab[k] == a) cells |= 1u << k;
+  ngrp = 0;
+  for (uint32_t rest = cells; rest;) {
+    uint32_t reach = rest & (~rest + 1);
+    for (;;) {
+      uint32_t grow = reach;
+      for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, 1) & cells;
+      if (grow == reach) break;
+      reach = grow;
+    }
+    for (uint32_t r = reach; r; r &= r - 1) grp[__ffs(r) - 1] = (uint8_t)ngrp;
+    ++ngrp;
+    rest &= ~reach;
+  }
+  return cells;
+}
+
 __device__ __forceinline__ bool box_fusion_bad(const int32_t *lab, int32_t a, int32_t b) {
   for (int k = 0; k < 27; ++k)
     if (k != 13 && lab[k] > 0 && lab[k] != a && lab[k] != b) return true;
@@ -1033,6 +1057,24 @@ __device__ __forceinline__ void st_rel64(unsigned long long *p, unsigned long lo
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Grown bounding box of label a (every a-site of any view V_i lies in it: a
+// site can only flip into a if it was adjacent to a at iteration start).
+struct LabBox {
+  int z0, y0, x0, bd, bh, bw;
+};
+__device__ __forceinline__ LabBox grown_box(const ParArgs &A, int32_t a) {
+  const int32_t *bx = A.lbox + 6 * a;
+  const int nz = (int)A.lat.nz, ny = (int)A.lat.ny, nx = (int)A.lat.nx;
+  LabBox b;
+  b.z0 = bx[0] > 0 ? bx[0] - 1 : 0;
+  b.y0 = bx[2] > 0 ? bx[2] - 1 : 0;
+  b.x0 = bx[4] > 0 ? bx[4] - 1 : 0;
+  b.bd = (bx[1] + 1 < nz ? bx[1] + 1 : nz - 1) - b.z0 + 1;
+  b.bh = (bx[3] + 1 < ny ? bx[3] + 1 : ny - 1) - b.y0 + 1;
+  b.bw = (bx[5] + 1 < nx ? bx[5] + 1 : nx - 1) - b.x0 + 1;
+  return b;
+}
+
 // ---------------------------------------------------------------------------
 // Assist jobs.  A candidate whose BFS footprint overflows the warp's shared
 // hash waits to become the earliest undecided candidate; its topology test is
@@ -1116,9 +1158,11 @@ __device__ bool warp_help(const ParArgs &A) {
   const int64_t f = (int64_t)__shfl_sync(0xffffffffu, desc[0], 0);
   const int32_t a = (int32_t)__shfl_sync(0xffffffffu, desc[1], 0);
   const int32_t pos = (int32_t)__shfl_sync(0xffffffffu, desc[2], 0);
-  const int64_t r0 = (int64_t)__shfl_sync(0xffffffffu, desc[4], 0);
-  const unsigned long long cw = __shfl_sync(0xffffffffu, desc[5], 0);
-  const int64_t c0 = (int64_t)(uint32_t)cw, bw = (int64_t)(cw >> 32);
+  const unsigned long long o4 = __shfl_sync(0xffffffffu, desc[4], 0);
+  const unsigned long long o5 = __shfl_sync(0xffffffffu, desc[5], 0);
+  const int64_t z0 = (int64_t)(o4 & 0x1fffff), y0 = (int64_t)((o4 >> 21) & 0x1fffff),
+                x0 = (int64_t)(o4 >> 42);
+  const int64_t bw = (int64_t)(o5 & 0x1fffff), bh = (int64_t)((o5 >> 21) & 0x1fffff);
   const uint32_t tag = (uint32_t)(c >> 32), hi = ~tag;
   const Lat &lat = A.lat;
   View v{A, pos};
@@ -1127,16 +1171,17 @@ __device__ bool warp_help(const ParArgs &A) {
   for (int i = 0; i < kJobChunk / 32; ++i) {
     const int64_t li = i0 + i * 32 + lane;
     if (li >= nbox) continue;
-    const int64_t yy = r0 + li / bw, x = c0 + li % bw, y = yy * lat.nx + x;
+    const int64_t zz = z0 + li / (bw * bh), yy = y0 + (li / bw) % bh, x = x0 + li % bw;
+    const int64_t y = (zz * lat.ny + yy) * lat.nx + x;
     if (y == f || v.lab(y) != a) continue;
-    // backward half of the 8-neighbourhood: every edge once (the job box
+    // backward half of the full neighbourhood: every edge once (the job box
     // contains every a-site, so edges to sites outside it never join a-sites)
-    const int dys[4] = {-1, -1, -1, 0}, dxs[4] = {-1, 0, 1, -1};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t y2 = yy + dys[k], xx = x + dxs[k];
-      if (!lat.inb(0, y2, xx)) continue;
-      const int64_t g = y2 * lat.nx + xx;
+    for (int k = 0; k < 13; ++k) {
+      const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;  // lexicographically < 0
+      if (lat.ndim == 2 && dz != 0) continue;
+      const int64_t z2 = zz + dz, y2 = yy + dy, x2 = x + dx;
+      if (!lat.inb(z2, y2, x2)) continue;
+      const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
       if (g != f && v.lab(g) == a) job_union(A.ufp, hi, (uint32_t)y, (uint32_t)g);
     }
   }
@@ -1153,11 +1198,8 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
   uint32_t tag = 0;
   unsigned long long nch = 0;
   if (lane == 0) {
-    const Lat &lat = A.lat;
-    const int32_t *bx = A.lbox + 4 * a;
-    const int64_t r0 = bx[0] > 0 ? bx[0] - 1 : 0, r1 = bx[1] + 1 < lat.ny ? bx[1] + 1 : lat.ny - 1;
-    const int64_t c0 = bx[2] > 0 ? bx[2] - 1 : 0, c1 = bx[3] + 1 < lat.nx ? bx[3] + 1 : lat.nx - 1;
-    const int64_t bw = c1 - c0 + 1, nbox = (r1 - r0 + 1) * bw;
+    const LabBox bx = grown_box(A, a);
+    const int64_t nbox = (int64_t)bx.bd * bx.bh * bx.bw;
     nch = (unsigned long long)((nbox + kJobChunk - 1) / kJobChunk);
     tag = (uint32_t)A.job[1] + 1;
     A.job[1] = tag;
@@ -1166,8 +1208,10 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
     d[1] = (unsigned long long)(uint32_t)a;
     d[2] = (unsigned long long)(uint32_t)pos;
     d[3] = 0;
-    d[4] = (unsigned long long)r0;
-    d[5] = (unsigned long long)c0 | ((unsigned long long)bw << 32);
+    d[4] = (unsigned long long)bx.z0 | ((unsigned long long)bx.y0 << 21) |
+           ((unsigned long long)bx.x0 << 42);
+    d[5] = (unsigned long long)bx.bw | ((unsigned long long)bx.bh << 21) |
+           ((unsigned long long)bx.bd << 42);
     d[6] = nch;
     d[7] = (unsigned long long)nbox;
     A.job[2] = nch;
@@ -1260,10 +1304,6 @@ static constexpr int kPQ = 64;
 //   hash:  open addressing on the site index, at most max_insert sites.
 // Returns 0 wait (S.bsite pending), 1 one piece, 2 several, 3 overflow.
 // ---------------------------------------------------------------------------
-struct BfsBox {
-  int r0, c0, bh, bw;  // grown bounding box of a
-};
-
 __device__ __forceinline__ int comp_of(unsigned long long C, int g) {
   return (int)((C >> (8 * g)) & 0xffu);
 }
@@ -1329,9 +1369,19 @@ __device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t
       w = old;
     }
   } else {
+    // the insert cap is checked before inserting (a 3-D level can offer
+    // thousands of sites) and probing is bounded, so the table never fills
+    if (*(volatile int *)&S.ninsert >= A.max_insert) {
+      S.overflow = 1;
+      return false;
+    }
     uint32_t h = hash32((uint32_t)t) & (kHW - 1);
     const unsigned long long mine = ((unsigned long long)(uint32_t)t << 8) | (unsigned)g;
-    for (;;) {
+    for (int probe = 0;; ++probe) {
+      if (probe == kHW) {
+        S.overflow = 1;
+        return false;
+      }
       unsigned long long cv = S.key[h];
       if (cv == kEmpty) {
         const unsigned long long old = atomicCAS(&S.key[h], kEmpty, mine);
@@ -1353,26 +1403,58 @@ __device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t
   return ins;
 }
 
-__device__ __forceinline__ void bfs_push(WarpBfs &S, int nxt, int yy, int xx, int g) {
+__device__ __forceinline__ void bfs_push(WarpBfs &S, int nxt, uint32_t packed, int g) {
   atomicOr(&S.alive, 1u << g);
   const int q = atomicAdd(&S.nfr[nxt], 1);
   if (q < kFW) {
-    S.fr[nxt][q] = ((uint32_t)yy << 16) | (uint32_t)xx;
+    S.fr[nxt][q] = packed;
     S.fg[nxt][q] = (uint8_t)g;
   } else {
     S.overflow = 1;
   }
 }
 
-template <bool kBox>
-__device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
-                          uint32_t seedmask, const BfsBox bb) {
+// Packed frontier coordinates: 2-D (y << 16 | x), 3-D (z << 22 | y << 11 | x).
+template <bool k3D>
+__device__ __forceinline__ uint32_t pack_c(int z, int y, int x) {
+  return k3D ? ((uint32_t)z << 22) | ((uint32_t)y << 11) | (uint32_t)x
+             : ((uint32_t)y << 16) | (uint32_t)x;
+}
+template <bool k3D>
+__device__ __forceinline__ void unpack_c(uint32_t e, int &z, int &y, int &x) {
+  if (k3D) {
+    z = (int)(e >> 22);
+    y = (int)((e >> 11) & 0x7ff);
+    x = (int)(e & 0x7ff);
+  } else {
+    z = 0;
+    y = (int)(e >> 16);
+    x = (int)(e & 0xffff);
+  }
+}
+
+// seeds: bit k of seedmask (3^3 layout, k != 13) is an a-cell of x's box;
+// sgrp[k] its group (box-local component, < 8)
+template <bool kBox, bool k3D>
+__device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
+                        uint32_t seedmask, const uint8_t *sgrp, int ngrp, const LabBox bb) {
   const int lane = threadIdx.x & 31;
-  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny;
-  const int fy = (int)(f / nx), fx = (int)(f % nx);
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny, nz = (int)A.lat.nz;
+  const int nxy = nx * ny;
+  const int fz = k3D ? (int)(f / nxy) : 0, frem = (int)(f - (int64_t)fz * nxy);
+  const int fy = frem / nx, fx = frem - fy * nx;
+  constexpr int kNb = k3D ? 26 : 8;
   uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
+  auto box_index = [&](int zz, int yy, int xx, bool &ok) -> int {
+    if (!kBox) return 0;
+    const int rz = zz - bb.z0, ry = yy - bb.y0, rx = xx - bb.x0;
+    // outside the grown box: never an a-site
+    ok = ok && (unsigned)rz < (unsigned)bb.bd && (unsigned)ry < (unsigned)bb.bh &&
+         (unsigned)rx < (unsigned)bb.bw;
+    return (rz * bb.bh + ry) * bb.bw + rx;
+  };
   if (kBox) {
-    const int nw = (bb.bh * bb.bw + 7) >> 3;
+    const int nw = (bb.bd * bb.bh * bb.bw + 7) >> 3;
     for (int k = lane; k < nw; k += 32) nib[k] = 0;
   } else {
     for (int k = lane; k < kHW; k += 32) S.key[k] = kEmpty;
@@ -1387,67 +1469,74 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
     S.npq = 0;
     S.nfr[1] = 0;
     if (kBox) {
-      const int li = (fy - bb.r0) * bb.bw + (fx - bb.c0);
+      bool ok = true;
+      const int li = box_index(fz, fy, fx, ok);
       nib[li >> 3] |= 15u << (4 * (li & 7));  // x itself: never entered
     } else {
       uint32_t h = hash32((uint32_t)f) & (kHW - 1);
       S.key[h] = ((unsigned long long)(uint32_t)f << 8) | 255u;
     }
-    int ns = 0;
+    int nfr = 0;
     unsigned long long C = 0;
-    for (int k = 0; k < 9; ++k) {
+    for (int g = 0; g < ngrp; ++g) {
+      S.unions[g] = 0;
+      C |= (unsigned long long)(1u << g) << (8 * g);
+    }
+    for (int k = 0; k < 27; ++k) {
       if (!((seedmask >> k) & 1u)) continue;
-      const int yy = fy + k / 3 - 1, xx = fx + k % 3 - 1;
+      const int zz = fz + k / 9 - 1, yy = fy + (k / 3) % 3 - 1, xx = fx + k % 3 - 1;
+      const int g = sgrp[k];
       if (kBox) {
-        const int li = (yy - bb.r0) * bb.bw + (xx - bb.c0);
-        nib[li >> 3] |= (uint32_t)(ns + 1) << (4 * (li & 7));
+        bool ok = true;
+        const int li = box_index(zz, yy, xx, ok);
+        nib[li >> 3] |= (uint32_t)(g + 1) << (4 * (li & 7));
       } else {
-        const uint32_t site = (uint32_t)(yy * nx + xx);
+        const uint32_t site = (uint32_t)((zz * ny + yy) * nx + xx);
         uint32_t h = hash32(site) & (kHW - 1);
         while (S.key[h] != kEmpty) h = (h + 1) & (kHW - 1);
-        S.key[h] = ((unsigned long long)site << 8) | (unsigned)ns;
+        S.key[h] = ((unsigned long long)site << 8) | (unsigned)g;
       }
-      S.fr[0][ns] = ((uint32_t)yy << 16) | (uint32_t)xx;
-      S.fg[0][ns] = (uint8_t)ns;
-      S.unions[ns] = 0;
-      C |= (unsigned long long)(1u << ns) << (8 * ns);
-      ++ns;
+      S.fr[0][nfr] = pack_c<k3D>(zz, yy, xx);
+      S.fg[0][nfr] = (uint8_t)g;
+      ++nfr;
     }
     S.comp = C;
-    S.nseed = ns;
-    S.nfr[0] = ns;
-    S.ninsert = ns + 1;
+    S.nseed = ngrp;
+    S.nfr[0] = nfr;
+    S.ninsert = nfr + 1;
   }
   __syncwarp();
-  auto box_index = [&](int yy, int xx, bool &ok) -> int {
-    if (!kBox) return 0;
-    const int ry = yy - bb.r0, rx = xx - bb.c0;
-    // outside the grown box: never an a-site
-    ok = ok && (unsigned)ry < (unsigned)bb.bh && (unsigned)rx < (unsigned)bb.bw;
-    return ry * bb.bw + rx;
-  };
   int cur = 0;
   for (;;) {
     // (frontier site, neighbour) pairs, three per lane with all their loads
-    // issued before any is used; eight lanes share a site so its
-    // neighbours' loads coalesce
+    // issued before any is used; lanes sharing a site coalesce
     const int n = S.nfr[cur], nxt = cur ^ 1;
-    for (int base = 0; base < 8 * n; base += 96) {
-      int t[3], li[3], g[3], yy[3], xx[3];
+    for (int base = 0; base < kNb * n; base += 96) {
+      int t[3], li[3], g[3], zq[3], yq[3], xq[3];
       bool ok[3];
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
         const int p = base + 32 * u + lane;
-        ok[u] = p < 8 * n;
-        const int j = ok[u] ? p >> 3 : 0, k = p & 7;
-        const uint32_t e = S.fr[cur][j];
+        ok[u] = p < kNb * n;
+        const int j = ok[u] ? p / kNb : 0, k = p - j * kNb;
+        int ez, ey, ex;
+        unpack_c<k3D>(S.fr[cur][j], ez, ey, ex);
         g[u] = S.fg[cur][j];
-        const int kk = k + (k >= 4);  // skip the centre of the 3x3
-        yy[u] = (int)(e >> 16) + kk / 3 - 1;
-        xx[u] = (int)(e & 0xffffu) + kk % 3 - 1;
-        ok[u] = ok[u] && (unsigned)yy[u] < (unsigned)ny && (unsigned)xx[u] < (unsigned)nx;
-        t[u] = yy[u] * nx + xx[u];
-        li[u] = box_index(yy[u], xx[u], ok[u]);
+        if (k3D) {
+          const int kk = k + (k >= 13);  // skip the centre of the 3^3
+          zq[u] = ez + kk / 9 - 1;
+          yq[u] = ey + (kk / 3) % 3 - 1;
+          xq[u] = ex + kk % 3 - 1;
+        } else {
+          const int kk = k + (k >= 4);  // skip the centre of the 3^2
+          zq[u] = 0;
+          yq[u] = ey + kk / 3 - 1;
+          xq[u] = ex + kk % 3 - 1;
+        }
+        ok[u] = ok[u] && (unsigned)zq[u] < (unsigned)nz && (unsigned)yq[u] < (unsigned)ny &&
+                (unsigned)xq[u] < (unsigned)nx;
+        t[u] = (zq[u] * ny + yq[u]) * nx + xq[u];
+        li[u] = box_index(zq[u], yq[u], xq[u], ok[u]);
         if (ok[u]) {
           if (kBox) {
             const int cg = (int)((nib[li[u] >> 3] >> (4 * (li[u] & 7))) & 15u);
@@ -1457,7 +1546,7 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
             }
           } else {
             uint32_t h = hash32((uint32_t)t[u]) & (kHW - 1);
-            for (;;) {
+            for (int probe = 0; probe < kHW; ++probe) {
               const unsigned long long cv = S.key[h];
               if (cv == kEmpty) break;
               if ((uint32_t)(cv >> 8) == (uint32_t)t[u]) {
@@ -1493,7 +1582,8 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
           continue;
         }
         if (df_lab(pk[u], l0[u], pos) != a) continue;
-        if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u])) bfs_push(S, nxt, yy[u], xx[u], g[u]);
+        if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u]))
+          bfs_push(S, nxt, pack_c<k3D>(zq[u], yq[u], xq[u]), g[u]);
       }
     }
     __syncwarp();
@@ -1518,12 +1608,13 @@ __device__ int warp_bfs2d(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, 
         const unsigned long long v = warp_wait_settled(A, tq, pos);
         if (tq >= 0) {
           const int gq = S.pqg[q];
-          const int yq = (int)(tq / nx), xq = (int)(tq - (int64_t)yq * nx);
+          const int zq = (int)(tq / nxy), rq = (int)(tq - (int64_t)zq * nxy);
+          const int yq = rq / nx, xq = rq - yq * nx;
           bool okq = true;
-          const int lq = box_index(yq, xq, okq);
+          const int lq = box_index(zq, yq, xq, okq);
           if (okq && df_lab(v, __ldg(A.L + tq), pos) == a &&
               bfs_visit<kBox>(A, S, nib, lq, (int)tq, gq))
-            bfs_push(S, nxt, yq, xq, gq);
+            bfs_push(S, nxt, pack_c<k3D>(zq, yq, xq), gq);
         }
       }
       __syncwarp();
@@ -1809,8 +1900,8 @@ __global__ void k_df_init(ParArgs A, int64_t N) {
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride) {
     A.cnt0[l] = A.cnt[l];
     A.nown[l] = 0;
-    A.lbox[4 * l + 0] = A.lbox[4 * l + 2] = kInf;
-    A.lbox[4 * l + 1] = A.lbox[4 * l + 3] = -1;
+    A.lbox[6 * l + 0] = A.lbox[6 * l + 2] = A.lbox[6 * l + 4] = kInf;
+    A.lbox[6 * l + 1] = A.lbox[6 * l + 3] = A.lbox[6 * l + 5] = -1;
   }
   if (blockIdx.x == 0 && threadIdx.x < 16) A.ctl[threadIdx.x] = 0;
   (void)M;
@@ -1829,22 +1920,29 @@ __global__ void k_df_init2(ParArgs A) {
   }
 }
 
-// Per-label bounding boxes of the iteration-start raster (2-D).  A region's
-// extreme rows/columns are attained at sites that are either on the image
+// Per-label bounding boxes of the iteration-start raster.  A region's
+// extreme coordinates are attained at sites that are either on the lattice
 // border or have a face neighbour of another label, i.e. are particles, so
 // the particle list plus the border sites give the exact box.
 __device__ __forceinline__ void bbox_add(const ParArgs &A, int32_t l, int64_t y) {
   if (l <= 0) return;
-  const int32_t r = (int32_t)(y / A.lat.nx), c = (int32_t)(y % A.lat.nx);
-  int32_t *b = A.lbox + 4 * l;
-  atomicMin(b + 0, r);
-  atomicMax(b + 1, r);
-  atomicMin(b + 2, c);
-  atomicMax(b + 3, c);
+  const int64_t nxy = A.lat.nx * A.lat.ny;
+  const int32_t zc = (int32_t)(y / nxy), rem = (int32_t)(y - (int64_t)zc * nxy);
+  const int32_t r = rem / (int32_t)A.lat.nx, c = rem - r * (int32_t)A.lat.nx;
+  int32_t *b = A.lbox + 6 * l;
+  atomicMin(b + 0, zc);
+  atomicMax(b + 1, zc);
+  atomicMin(b + 2, r);
+  atomicMax(b + 3, r);
+  atomicMin(b + 4, c);
+  atomicMax(b + 5, c);
 }
 
 __global__ void k_df_bbox(ParArgs A, int64_t N) {
-  const int64_t nx = A.lat.nx, ny = A.lat.ny, nb = 2 * (nx + ny);
+  const int64_t nx = A.lat.nx, ny = A.lat.ny, nz = A.lat.nz;
+  // border sites: the y and x faces of every z-plane, plus the z faces in 3-D
+  const int64_t fy = 2 * nz * nx, fx = 2 * nz * ny, fz = A.lat.ndim == 3 ? 2 * nx * ny : 0;
+  const int64_t nb = fy + fx + fz;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N + nb; i += stride) {
     if (i < N) {
@@ -1853,12 +1951,25 @@ __global__ void k_df_bbox(ParArgs A, int64_t N) {
       if (A.site_off[y] == (uint32_t)i) bbox_add(A, A.pown[i], y);
       continue;
     }
-    const int64_t j = i - N;
-    int64_t y;
-    if (j < nx) y = j;                                   // top row
-    else if (j < 2 * nx) y = (ny - 1) * nx + (j - nx);   // bottom row
-    else if (j < 2 * nx + ny) y = (j - 2 * nx) * nx;     // left column
-    else y = (j - 2 * nx - ny) * nx + nx - 1;            // right column
+    int64_t j = i - N, z, r, c;
+    if (j < fy) {
+      z = j / (2 * nx);
+      const int64_t q = j % (2 * nx);
+      r = q < nx ? 0 : ny - 1;
+      c = q % nx;
+    } else if ((j -= fy) < fx) {
+      z = j / (2 * ny);
+      const int64_t q = j % (2 * ny);
+      c = q < ny ? 0 : nx - 1;
+      r = q % ny;
+    } else {
+      j -= fx;
+      const int64_t q = j / (nx * ny);
+      z = q == 0 ? 0 : nz - 1;
+      r = (j % (nx * ny)) / nx;
+      c = j % nx;
+    }
+    const int64_t y = (z * ny + r) * nx + c;
     bbox_add(A, A.L[y], y);
   }
 }
@@ -1924,6 +2035,22 @@ __global__ void k_df_labcsr(const uint32_t *__restrict__ key, int32_t *__restric
   }
 }
 
+// Finished warps: help assist jobs until every warp has finished (ctl[11]
+// counts finished warps; a warp still deciding may yet start a job).  Polls
+// the job word every ~2 us: a tight spin of thousands of finished warps would
+// flood L2 while the last candidates decide.
+__device__ void warp_idle_help(const ParArgs &A) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+  if (lane == 0) atomicAdd(A.ctl + 11, 1);
+  for (;;) {
+    if (warp_help(A)) continue;
+    const int idle = __shfl_sync(0xffffffffu, lane == 0 ? ld_rlx(A.ctl + 11) : 0, 0);
+    if (idle >= nwarps) return;
+    __nanosleep(2000);
+  }
+}
+
 // Wait (whole warp) until small label l's next event is position pos.
 __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int32_t pos) {
   const int lane = threadIdx.x & 31;
@@ -1949,24 +2076,23 @@ __device__ __forceinline__ void df_stamp(const ParArgs &A, int32_t pos, int k) {
   }
 }
 
-// 2-D only (the host routes 3-D lattices to the round-based kernel).
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
   const Lat &lat = A.lat;
   const int lane = threadIdx.x & 31;
   const int32_t M = (int32_t)*A.nneg;
-  const int nx = (int)lat.nx, ny = (int)lat.ny;
+  const int nx = (int)lat.nx, ny = (int)lat.ny, nz = (int)lat.nz;
   int32_t *ctl = A.ctl;
   // positions come from an atomic counter one at a time: a position held
   // ahead by a warp stuck in a long BFS would stall its dependants
   for (;;) {
     const int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
     if (pos >= M) {
-      // drain an active assist job, then leave: spinning finished warps
-      // would flood L2 with polls while the last candidates decide
-      while (warp_help(A)) {
-      }
+      // stay as a helper for assist jobs until every position is decided,
+      // polling slowly (a tight spin of thousands of finished warps would
+      // flood L2 while the last candidates decide)
+      warp_idle_help(A);
       break;
     }
     const int4 rc = __ldg(A.rec + pos);
@@ -1976,12 +2102,17 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     const bool sa = rc.y < 0, sb = rc.z < 0;
     if (sa) warp_wait_label(A, a, pos);
     if (sb) warp_wait_label(A, b, pos);
-    const int y = f / nx, x = f - y * nx;
-    // the 3x3 box, lanes 9..17 in the 3^3 layout of lab[] (13 = x itself)
+    const bool is3 = lat.ndim == 3;
+    const int nxy = nx * ny;
+    const int z = is3 ? f / nxy : 0, frem = f - z * nxy;
+    const int y = frem / nx, x = frem - y * nx;
+    // the 3^d box, one cell per lane in the 3^3 layout of lab[] (13 = x)
     int64_t gb = -1;
-    if (lane >= 9 && lane < 18) {
-      const int yy = y + lane / 3 - 4, xx = x + lane % 3 - 1;
-      if ((unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx) gb = yy * nx + xx;
+    if (lane < 27) {
+      const int dz = lane / 9 - 1, zz = z + dz, yy = y + (lane / 3) % 3 - 1, xx = x + lane % 3 - 1;
+      if ((is3 || dz == 0) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+          (unsigned)xx < (unsigned)nx)
+        gb = ((int64_t)zz * ny + yy) * nx + xx;
     }
     const int32_t l0 = gb >= 0 ? __ldg(A.L + gb) : -1;
     const unsigned long long pk = warp_wait_settled(A, gb, pos);
@@ -1990,7 +2121,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     const int32_t wold = wp_w(pkc), lold = wp_lab(pkc);
     int32_t lab[27];
 #pragma unroll
-    for (int k = 0; k < 27; ++k) lab[k] = (k >= 9 && k < 18) ? __shfl_sync(0xffffffffu, mine, k) : -1;
+    for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
     uint8_t d = ACC;
     int how = 0;  // 1: needs the window test
     int dbg = 0;  // decision path (tools/df_timeline.py decodes it)
@@ -2016,22 +2147,27 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     df_stamp(A, pos, 2);
     df_stamp(A, pos, 3);
     if (how == 1) {
-      // exact window test (radius 5), warp-cooperative: lanes read disjoint
-      // cells without waiting, ballots collect the settled donor-label bits
-      // P and the pending cells U.  Window connectivity only grows with more
-      // a-cells, and a seed piece that cannot reach the rim stays so with
-      // fewer, so the verdict is exact if P alone joins the seeds (1) or P|U
-      // leaves a piece enclosed (2); otherwise the 31x31 window and then the
-      // BFS (which skip pending sites the same way) decide.
-      const int RB = A.win_r ? A.win_r : 5, WB = 2 * RB + 1, nb = WB * WB;
+      // exact window test (radius 5 in 2-D, 4 in 3-D), warp-cooperative:
+      // lanes read disjoint cells without waiting, ballots collect the
+      // settled donor-label bits P and the pending cells U.  Window
+      // connectivity only grows with more a-cells, and a seed piece that
+      // cannot reach the rim stays so with fewer, so the verdict is exact
+      // if P alone joins the seeds (1) or P|U leaves a piece enclosed (2);
+      // otherwise the larger windows (2-D) and the BFS (which skip pending
+      // sites the same way) decide.
+      const int RB = is3 ? 4 : (A.win_r ? A.win_r : 5), WB = 2 * RB + 1;
+      const int nb = is3 ? WB * WB * WB : WB * WB;
       uint32_t *bits = S.fr[0], *unk = S.fr[1];
       for (int base = 0; base < nb; base += 32) {
         const int c = base + lane;
         bool bit = false, u = false;
         if (c < nb) {
-          const int yy = y + c / WB - RB, xx = x + c % WB - RB;
-          if ((yy != y || xx != x) && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx) {
-            const int gw = yy * nx + xx;
+          const int dz = is3 ? c / (WB * WB) - RB : 0;
+          const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
+          const int zz = z + dz, yy = y + dy, xx = x + dx;
+          if ((dz || dy || dx) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+              (unsigned)xx < (unsigned)nx) {
+            const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
             const unsigned long long wv = ld_rlx64(A.wp + gw);
             const int32_t lw = __ldg(A.L + gw);
             u = wp_pend(wv) < pos;
@@ -2047,7 +2183,8 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       __syncwarp();
       if (lane == 0) {
         auto verdict = [&](const uint32_t *bb) {
-          return RB == 3 ? window_verdict_bits<3>(bb, 1)
+          return is3 ? window_verdict_bits<4>(bb, WB)
+                 : RB == 3 ? window_verdict_bits<3>(bb, 1)
                  : RB == 1 ? 0
                            : window_verdict_bits<5>(bb, 1);
         };
@@ -2065,13 +2202,13 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       __syncwarp();
       dbg = 1000 + 100 * (wb + 2);
       df_stamp(A, pos, 3);
-      if (wb == 0) {
+      if (wb == 0 && !is3) {
         wb = window31(A, pos, f, a);
         dbg += 10000000 * (wb + 1);
-      }
-      if (wb == 0) {
-        wb = window63(A, pos, f, a);
-        dbg += 1000000 * (wb + 1);
+        if (wb == 0) {
+          wb = window63(A, pos, f, a);
+          dbg += 1000000 * (wb + 1);
+        }
       }
       if (wb == 2) {
         d = REJ;
@@ -2079,23 +2216,20 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         // BFS tiers: the bounding-box map when a's grown box fits, else the
         // hash (<= max_insert sites); overflow of either goes to the assist
         // job at the low-water mark.  A BFS whose verdict depends on a
-        // pending site (0) waits for it and runs again.
-        BfsBox bb;
-        {
-          const int32_t *bx = A.lbox + 4 * a;
-          bb.r0 = bx[0] > 0 ? bx[0] - 1 : 0;
-          bb.c0 = bx[2] > 0 ? bx[2] - 1 : 0;
-          bb.bh = (bx[1] + 1 < ny ? bx[1] + 1 : ny - 1) - bb.r0 + 1;
-          bb.bw = (bx[3] + 1 < nx ? bx[3] + 1 : nx - 1) - bb.c0 + 1;
-        }
-        const bool use_box = (int64_t)bb.bh * bb.bw <= (int64_t)A.box_cap;
-        uint32_t seeds = 0;
-        for (int k = 9; k < 18; ++k)
-          if (k != 13 && lab[k] == a) seeds |= 1u << (k - 9);
+        // pending site it could not resolve (0) waits for it and runs again.
+        const LabBox bb = grown_box(A, a);
+        const bool use_box = (int64_t)bb.bd * bb.bh * bb.bw <= (int64_t)A.box_cap;
+        uint8_t sgrp[27];
+        int ngrp = 0;
+        const uint32_t seeds = box_groups(lab, a, sgrp, ngrp);
         int r;
         for (;;) {
-          r = use_box ? warp_bfs2d<true>(A, S, pos, f, a, seeds, bb)
-                      : warp_bfs2d<false>(A, S, pos, f, a, seeds, bb);
+          if (is3)
+            r = use_box ? warp_bfs<true, true>(A, S, pos, f, a, seeds, sgrp, ngrp, bb)
+                        : warp_bfs<false, true>(A, S, pos, f, a, seeds, sgrp, ngrp, bb);
+          else
+            r = use_box ? warp_bfs<true, false>(A, S, pos, f, a, seeds, sgrp, ngrp, bb)
+                        : warp_bfs<false, false>(A, S, pos, f, a, seeds, sgrp, ngrp, bb);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
           if (r != 0) break;
           if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
@@ -2865,13 +2999,23 @@ __global__ void k_mark_band(const int64_t *__restrict__ acc, const int64_t *__re
   }
 }
 
+// band != nullptr (band ledger): also accumulate sum(rho_new - rho_old) over the
+// dirty sites into the superaccumulator band[0..kLimbs) -- the exact change
+// of the external energy, since clean sites keep their own-label field.
 __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__restrict__ I, Lat lat,
                                const Off *__restrict__ ball_full, int nball_full,
                                uint8_t *__restrict__ dirty, int32_t *__restrict__ Cown,
-                               double *__restrict__ Sown, double *__restrict__ rho0, int poisson) {
+                               double *__restrict__ Sown, double *__restrict__ rho0, int poisson,
+                               long long *__restrict__ band) {
+  __shared__ long long sm[kLimbs];
+  if (band) {
+    for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+    __syncthreads();
+  }
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < lat.V; f += stride) {
     if (!dirty[f]) continue;
+    if (band) acc_add(sm, -rho0[f]);
     dirty[f] = 0;
     int64_t z, y, x;
     lat.coord(f, z, y, x);
@@ -2890,7 +3034,29 @@ __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__re
     Cown[f] = c;
     Sown[f] = s;
     if (rho0) rho0[f] = rho(I[f], s / (double)c, poisson);
+    if (band) acc_add(sm, rho0[f]);
   }
+  if (band) acc_flush(sm, band);
+}
+
+// Band ledger: sum of dE_int over the kept moves (band[kLimbs]) ...
+__global__ void k_dint_sum(const ParArgs A, const int64_t *__restrict__ moves,
+                           long long *__restrict__ band) {
+  const int64_t n = *moves;
+  long long c = 0;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+    c += A.dint_acc[k];
+  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)(band + kLimbs), (unsigned long long)c);
+}
+
+// ... and the iteration's energy change, exact external part rounded once
+__global__ void k_band_ledger(const long long *__restrict__ band, double lam,
+                              double *__restrict__ energy) {
+  if (threadIdx.x != 0) return;
+  const double dext = limbs_round_dev(band);
+  *energy = *energy + (dext + lam * (double)band[kLimbs]);
 }
 
 size_t accept_par_smem() { return sizeof(BfsShared); }
@@ -2965,7 +3131,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
-    k_df_bbox<<<grid_for(N + 2 * (A.lat.nx + A.lat.ny), 256), 256, 0, s>>>(A, N);
+    k_df_bbox<<<grid_for(N + 2 * (A.lat.nz * (A.lat.nx + A.lat.ny) + A.lat.nx * A.lat.ny), 256), 256,
+                0, s>>>(A, N);
     RCB_TRY(X.rec->reserve(N, s));
     k_df_records<<<grid_for(N, 256), 256, 0, s>>>(A, X.rec->p);
     A.rec = X.rec->p;
@@ -2999,7 +3166,11 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
   T.mark("compact");
   int nl = 6;
-  if (X.region_ps) {
+  // 3-D PS: the per-move exact ledger terms cost moves x ball x nearby flips,
+  // so the ledger takes the iteration's exact band change instead (see
+  // k_refield_band); 2-D keeps the per-move terms of the reference's ledger
+  const bool band_ledger = X.region_ps && A.lat.ndim == 3 && X.rho0 && X.band;
+  if (X.region_ps && !band_ledger) {
     const int64_t rows = A.lat.nz * A.lat.ny;
     RCB_TRY(X.evkey->reserve(N, s));
     RCB_TRY(X.evkey2->reserve(N, s));
@@ -3080,7 +3251,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
                                                    X.lam, X.dtot);
     T.mark("chains");
-    k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
+    if (!band_ledger) k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
     T.mark("ledger");
     nl += 12;
   }
@@ -3088,10 +3259,16 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   T.mark("labels");
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
-    k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(X.Lmut, X.I, A.lat, X.ball_full,
-                                                          X.nball_full, X.dirty, X.Cown, X.Sown,
-                                                          X.rho0, X.poisson);
+    if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
+    k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
+        X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.dirty, X.Cown, X.Sown, X.rho0, X.poisson,
+        band_ledger ? X.band : nullptr);
     nl += 2;
+    if (band_ledger) {
+      if (X.lam != 0.0) k_dint_sum<<<grid_for(N, 256), 256, 0, s>>>(A, X.moves, X.band);
+      k_band_ledger<<<1, 32, 0, s>>>(X.band, X.lam, X.energy);
+      nl += 2;
+    }
   }
   T.mark("band");
   RCB_CUDA(cudaGetLastError());

@@ -80,6 +80,8 @@ int32_t fail(int32_t code, const std::string &msg);
     if (_s != RCB_OK) return _s;   \
   } while (0)
 
+static constexpr int kLimbs = 68;  // superaccumulator limbs of 32 bits from 2^-1074
+
 // ---- device memory: stream-ordered buffers --------------------------------
 template <typename T>
 struct DBuf {

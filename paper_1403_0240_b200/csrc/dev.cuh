@@ -208,6 +208,88 @@ __device__ __forceinline__ double delta_ps(const int32_t *__restrict__ L,
   return d;
 }
 
+// Superaccumulator (K9): exact fp64 sums in int64 limbs.
+__device__ __forceinline__ void acc_add(long long *limbs, double d) {
+  if (d == 0.0) return;
+  uint64_t u = (uint64_t)__double_as_longlong(d);
+  int ex = (int)((u >> 52) & 0x7ff);
+  uint64_t m = u & ((1ull << 52) - 1);
+  int e;
+  if (ex == 0) {
+    e = -1074;
+  } else {
+    m |= 1ull << 52;
+    e = ex - 1075;
+  }
+  int pos = e + 1074;
+  int k0 = pos >> 5, sh = pos & 31;
+  uint64_t lo = m << sh;
+  uint64_t hi = sh ? (m >> (64 - sh)) : 0;
+  long long c0 = (long long)(lo & 0xffffffffull), c1 = (long long)(lo >> 32), c2 = (long long)hi;
+  if (u >> 63) {
+    c0 = -c0;
+    c1 = -c1;
+    c2 = -c2;
+  }
+  if (c0) atomicAdd((unsigned long long *)&limbs[k0], (unsigned long long)c0);
+  if (c1) atomicAdd((unsigned long long *)&limbs[k0 + 1], (unsigned long long)c1);
+  if (c2) atomicAdd((unsigned long long *)&limbs[k0 + 2], (unsigned long long)c2);
+}
+
+__device__ __forceinline__ void acc_flush(long long *sm, long long *gl) {
+  __syncthreads();
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x)
+    if (sm[k]) atomicAdd((unsigned long long *)&gl[k], (unsigned long long)sm[k]);
+}
+
+
+// Exact sum rounded once to the nearest double, on the device (the host's
+// limbs_to_double, energy.cu); one thread.
+__device__ inline double limbs_round_dev(const long long *limbs) {
+  constexpr int ND = kLimbs + 3;
+  uint32_t dig[ND];
+  long long carry = 0;
+  for (int k = 0; k < ND; ++k) {
+    const long long t = (k < kLimbs ? limbs[k] : 0) + carry;
+    dig[k] = (uint32_t)(t & 0xffffffffll);
+    carry = t >> 32;
+  }
+  const bool neg = carry < 0;
+  if (neg) {
+    uint64_t c = 1;
+    for (int k = 0; k < ND; ++k) {
+      const uint64_t t = (uint64_t)(uint32_t)~dig[k] + c;
+      dig[k] = (uint32_t)t;
+      c = t >> 32;
+    }
+  }
+  int top = -1;
+  for (int k = ND - 1; k >= 0; --k)
+    if (dig[k]) {
+      top = k * 32 + (31 - __clz(dig[k]));
+      break;
+    }
+  if (top < 0) return 0.0;
+  auto bit = [&](int p) -> uint64_t { return p < 0 ? 0 : (dig[p >> 5] >> (p & 31)) & 1u; };
+  uint64_t m = 0;
+  int shift = top >= 52 ? top - 52 : 0;
+  for (int p = top; p >= shift; --p) m = (m << 1) | bit(p);
+  if (shift > 0) {
+    const uint64_t g = bit(shift - 1);
+    bool sticky = false;
+    for (int p = shift - 2; p >= 0 && !sticky; --p) sticky = bit(p) != 0;
+    if (g && (sticky || (m & 1))) {
+      ++m;
+      if (m == (1ull << 53)) {
+        m >>= 1;
+        ++shift;
+      }
+    }
+  }
+  const double r = ldexp((double)m, shift - 1074);
+  return neg ? -r : r;
+}
+
 // ---------------------------------------------------------------------------
 // ranking (optimizer.py:80-87)
 // ---------------------------------------------------------------------------

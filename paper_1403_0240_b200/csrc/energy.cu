@@ -417,39 +417,6 @@ int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, 
 // A double m*2^e (e >= -1074) is split into three 32-bit chunks added to
 // int64 limbs of weight 2^(32k-1074); the host rounds the exact total once.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void acc_add(long long *limbs, double d) {
-  if (d == 0.0) return;
-  uint64_t u = (uint64_t)__double_as_longlong(d);
-  int ex = (int)((u >> 52) & 0x7ff);
-  uint64_t m = u & ((1ull << 52) - 1);
-  int e;
-  if (ex == 0) {
-    e = -1074;
-  } else {
-    m |= 1ull << 52;
-    e = ex - 1075;
-  }
-  int pos = e + 1074;
-  int k0 = pos >> 5, sh = pos & 31;
-  uint64_t lo = m << sh;
-  uint64_t hi = sh ? (m >> (64 - sh)) : 0;
-  long long c0 = (long long)(lo & 0xffffffffull), c1 = (long long)(lo >> 32), c2 = (long long)hi;
-  if (u >> 63) {
-    c0 = -c0;
-    c1 = -c1;
-    c2 = -c2;
-  }
-  if (c0) atomicAdd((unsigned long long *)&limbs[k0], (unsigned long long)c0);
-  if (c1) atomicAdd((unsigned long long *)&limbs[k0 + 1], (unsigned long long)c1);
-  if (c2) atomicAdd((unsigned long long *)&limbs[k0 + 2], (unsigned long long)c2);
-}
-
-__device__ __forceinline__ void acc_flush(long long *sm, long long *gl) {
-  __syncthreads();
-  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x)
-    if (sm[k]) atomicAdd((unsigned long long *)&gl[k], (unsigned long long)sm[k]);
-}
-
 __global__ void k_pc_terms(const int64_t *__restrict__ cnt, const double *__restrict__ tot,
                            const double *__restrict__ tsq, int32_t nl, int poisson,
                            long long *__restrict__ limbs) {

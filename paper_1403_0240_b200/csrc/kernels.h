@@ -5,7 +5,6 @@
 
 namespace rcb {
 
-static constexpr int kLimbs = 68;  // superaccumulator limbs of 32 bits from 2^-1074
 
 struct StatsScratch {
   DBuf<uint32_t> keys, vals_in, vals;
@@ -126,6 +125,7 @@ struct ParExtra {
   DBuf<uint64_t> *labkey, *labkey2;
   DBuf<int32_t> *labpos, *labpos2, *flrows;
   DBuf<int4> *rec;
+  long long *band;  // band ledger: kLimbs superaccumulator limbs + dE_int sum
   DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
 };

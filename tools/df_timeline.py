@@ -12,9 +12,10 @@ import paper_1403_0240_b200 as P  # noqa: E402
 import scenes  # noqa: E402
 
 it_target = int(sys.argv[1]) if len(sys.argv) > 1 else 19
-sc = scenes.cfg2()
-eng = P.RegionCompetition(sc.image, sc.labels, P.EnergyConfig("ps", "poisson", smooth_radius=4),
-                          P.SobolevParams(6.0), P.OptimizerConfig("sobolev", vanish_grace=5, drift_tolerance=1e-3))
+sc = scenes.CONFIGS[sys.argv[2]]() if len(sys.argv) > 2 else scenes.cfg2()
+eng = P.RegionCompetition(sc.image, sc.labels, P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius),
+                          P.SobolevParams(sc.length_scale),
+                          P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=1e-3))
 for _ in range(it_target - 1):
     eng.iterate()
 cnt0 = eng.model.stats.count.copy()
@@ -77,7 +78,7 @@ print("last 1%: involve small label", int(inv[late].sum()), "of", int(late.sum()
 
 # inherent dependency depth: position p waits on every earlier position whose
 # pixel lies in p's 3x3 box (the minimum read set of the simple-point test)
-W = sc.image.shape[1]
+W = sc.image.shape[-1]
 px = xs[part[:m]]
 best = {}
 depth = np.zeros(m, np.int32)
