@@ -169,6 +169,36 @@ int32_t rcb_engine_debug_codes(rcb_engine *eng, int32_t *particle, int32_t *code
  * rank position of the last dataflow acceptance (t4 holds 4 * cap values). */
 int32_t rcb_engine_debug_times(rcb_engine *eng, int64_t *t4, int64_t cap, int64_t *n);
 
+/* ---- z-slab sharding: one engine per GPU ------------- *
+ * Every rank holds the whole raster (512^3 needs ~12 GB with the own-label
+ * field layout, against 180 GB per B200) and runs the identical rank order and
+ * acceptance on it, so decisions agree bit for bit without exchanging them.
+ * The scoring kernels are split by outer planes (z in 3-D, rows in 2-D):
+ * rank r computes ΔE (K3/K5) for its slab plus the Sobolev stencil's halo and
+ * the Sobolev filter (K6) for its slab; the exchange step is an all-gather of
+ * each slab's scores (base, and for PS the competitor ball terms cb0/sb0)
+ * into the same offsets on every rank.  iterate() == score() + finish(). */
+typedef struct {
+    int64_t n_particles;    /* particles scored this iteration (all slabs) */
+    int64_t p0, p1;         /* this slab's particle range [p0, p1) */
+    void *base;             /* device double[n]: smoothed (sobolev) or raw (l2) ΔE */
+    void *cb0;              /* device int32[n] (PS only, else NULL) */
+    void *sb0;              /* device double[n] (PS only, else NULL) */
+    void *stream;           /* cudaStream_t the scores were computed on */
+} rcb_slab_info;
+
+/* Outer planes [lo, hi) this engine scores; hi <= lo = the whole lattice. */
+int32_t rcb_engine_set_slab(rcb_engine *eng, int64_t lo, int64_t hi);
+/* First half of iterate(): K1 emit, ΔE_int, ΔE, Sobolev over the slab. */
+int32_t rcb_engine_score(rcb_engine *eng, rcb_slab_info *info);
+/* Second half, after every slab's [p0, p1) of base/cb0/sb0 is in place:
+ * rank order, acceptance and bookkeeping (replicated on every rank). */
+int32_t rcb_engine_finish(rcb_engine *eng, rcb_iter_record *rec);
+/* Particle index of the first site of each outer plane planes[i] (clamped
+ * to [0, planes]); a slab [lo, hi) owns [out(lo), out(hi)). */
+int32_t rcb_engine_particle_ranges(rcb_engine *eng, const int64_t *planes, int32_t k,
+                                   int64_t *out);
+
 /* ---- Sobolev sweep workload (BASELINE configs[4], second part) --------- */
 typedef struct rcb_sweep rcb_sweep;
 /* Paint the union of nsph spheres (z, y, x, r as float, 4 per sphere) into a

@@ -37,6 +37,12 @@ class OptCfg(C.Structure):
                 ("vanish_grace", C.c_int32), ("full_fg", C.c_int32), ("fp32", C.c_int32)]
 
 
+class SlabInfo(C.Structure):
+    _fields_ = [("n_particles", C.c_int64), ("p0", C.c_int64), ("p1", C.c_int64),
+                ("base", C.c_void_p), ("cb0", C.c_void_p), ("sb0", C.c_void_p),
+                ("stream", C.c_void_p)]
+
+
 class IterRecord(C.Structure):
     _fields_ = [("iteration", C.c_int64), ("energy", C.c_double), ("moves", C.c_int64),
                 ("particles", C.c_int64), ("candidates", C.c_int64), ("negative", C.c_int64),
@@ -75,6 +81,10 @@ SIGNATURES = {
     "rcb_engine_counters": [_P, _P],
     "rcb_engine_debug_codes": [_P, _P, _P, _I64, _P],
     "rcb_engine_debug_times": [_P, _P, _I64, _P],
+    "rcb_engine_set_slab": [_P, _I64, _I64],
+    "rcb_engine_score": [_P, _P],
+    "rcb_engine_finish": [_P, _P],
+    "rcb_engine_particle_ranges": [_P, _P, _I32, _P],
     "rcb_sweep_create": [_I32, _P, _P, _I32, C.c_uint64, _P, _I32, _P],
     "rcb_sweep_destroy": [_P],
     "rcb_sweep_info": [_P, _P, _P, _P],

@@ -148,6 +148,12 @@ struct rcb_engine {
   bool last_par = false;
   float times[6] = {};
   int32_t launches = 0;
+  // z-slab sharding (rcb_engine_set_slab): outer planes [slab_lo, slab_hi)
+  int64_t slab_lo = 0, slab_hi = 0, stencil_reach = 0;
+  int64_t p0 = 0, p1 = 0;  // own particle range of the last score
+  bool scored = false;
+  int score_launches = 0;
+  uint32_t *hoff = nullptr;  // pinned: site_off reads
 
   ~rcb_engine() {
     if (s) {
@@ -177,6 +183,7 @@ struct rcb_engine {
       if (own_stream) cudaStreamDestroy(s);
     }
     if (hsc) cudaFreeHost(hsc);
+    if (hoff) cudaFreeHost(hoff);
   }
 
   int32_t prepare() {  // K1 pass 1 + scan on the current raster
@@ -309,6 +316,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   if (cudaMallocHost((void **)&e->hsc, sizeof(Scalars)) != cudaSuccess)
     return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
   memset(e->hsc, 0, sizeof(Scalars));
+  if (cudaMallocHost((void **)&e->hoff, 16 * sizeof(uint32_t)) != cudaSuccess)
+    return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
   if (cudaMemsetAsync(e->sc.p, 0, sizeof(Scalars), s) != cudaSuccess ||
       cudaMemsetAsync(e->vis.p, 0, sizeof(uint32_t) * V, s) != cudaSuccess)
     return bail(fail(RCB_ERR_CUDA, "memset failed"));
@@ -329,6 +338,10 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   if (scfg->n_weights <= maxd2)
     return bail(fail(RCB_ERR_VALUE, "Sobolev weight table shorter than the stencil needs"));
   e->nst = (int)st.size();
+  for (const Off &o : st) {  // outer-axis reach of the stencil (dz in 3-D, dy in 2-D)
+    const int64_t r = std::abs(ndim == 3 ? (int)o.dz : (int)o.dy);
+    e->stencil_reach = std::max(e->stencil_reach, r);
+  }
   TRYB(upload(e->st, st.data(), st.size(), s));
   TRYB(upload(e->wt, scfg->weights, (size_t)scfg->n_weights, s));
   if (ocfg->fp32) {
@@ -369,7 +382,27 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
 
 void rcb_engine_destroy(rcb_engine *e) { delete e; }
 
-int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
+// Particle range [p(lo), p(hi)) of the sites in outer planes [lo, hi) (z in
+// 3-D, rows in 2-D): particles are sorted by site, so a slab of planes is one
+// contiguous range of the particle list (read from the K1 index site_off).
+static int32_t plane_ranges(rcb_engine *e, const int64_t *planes, int k, int64_t *out) {
+  const int64_t plane = e->lat.ndim == 3 ? e->lat.ny * e->lat.nx : e->lat.nx;
+  const int64_t np = e->lat.ndim == 3 ? e->lat.nz : e->lat.ny;
+  for (int i = 0; i < k; ++i) {
+    const int64_t pl = std::min(std::max(planes[i], (int64_t)0), np);
+    RCB_CUDA(cudaMemcpyAsync(&e->hoff[i], e->site_off.p + pl * plane, sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, e->s));
+  }
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  for (int i = 0; i < k; ++i) out[i] = e->hoff[i];
+  return RCB_OK;
+}
+
+// Scoring half of iterate(): K1 emit, ΔE_int, ΔE (K3/K5) and the Sobolev
+// filter (K6).  With a slab [slab_lo, slab_hi) set, ΔE is computed for the
+// slab's particles plus a halo of the stencil's reach (the particles K6 reads)
+// and K6 for the slab's particles only; every other array stays replicated.
+static int32_t engine_score(rcb_engine *e) {
   RCB_CUDA(cudaSetDevice(e->device));
   cudaStream_t s = e->s;
   e->iteration += 1;
@@ -383,6 +416,20 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
   RCB_CUDA(cudaMemsetAsync(&d->pairs, 0, sizeof(unsigned long long), s));
   RCB_CUDA(cudaMemsetAsync(&d->moves, 0, sizeof(int64_t), s));
   int launches = 2;
+  // particle ranges: [p0, p1) own slab, [h0, h1) slab + stencil halo
+  int64_t p0 = 0, p1 = n, h0 = 0, h1 = n;
+  if (e->slab_hi > e->slab_lo && n > 0) {
+    const int64_t reach = e->mode == 1 ? e->stencil_reach : 0;
+    const int64_t pl[4] = {e->slab_lo, e->slab_hi, e->slab_lo - reach, e->slab_hi + reach};
+    int64_t r[4];
+    RCB_TRY(plane_ranges(e, pl, 4, r));
+    p0 = r[0];
+    p1 = r[1];
+    h0 = r[2];
+    h1 = r[3];
+  }
+  e->p0 = p0;
+  e->p1 = p1;
   if (n > 0) {
     RCB_TRY(e->px.reserve(n, s));
     RCB_TRY(e->pown.reserve(n, s));
@@ -404,33 +451,54 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
       RCB_TRY(e->cb0.reserve(n, s));
       RCB_TRY(e->sb0.reserve(n, s));
     }
+    const int64_t m = h1 - h0;
     if (fp32 && e->ecfg.region_model == 0)
-      RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
-                               poisson, e->raw32.p, e->raw.p, s));
+      RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m,
+                               e->cnt.p, e->tot.p, poisson, e->raw32.p + h0, e->raw.p + h0, s));
     else if (fp32)
       RCB_TRY(delta_ps32_batch(e->L.p, e->I32.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                               e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw32.p, e->raw.p,
-                               s, e->cb0.p, e->sb0.p));
+                               e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
+                               e->raw32.p + h0, e->raw.p + h0, s, e->cb0.p + h0, e->sb0.p + h0));
     else if (e->ecfg.region_model == 0)
-      RCB_TRY(delta_pc_batch(e->I.p, e->px.p, e->pown.p, e->pcomp.p, n, e->cnt.p, e->tot.p,
-                             e->tsq.p, poisson, e->raw.p, s));
+      RCB_TRY(delta_pc_batch(e->I.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, e->cnt.p,
+                             e->tot.p, e->tsq.p, poisson, e->raw.p + h0, s));
     else
       RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                             e->px.p, e->pown.p, e->pcomp.p, n, poisson, e->raw.p, s, e->rho0.p,
-                             e->cb0.p, e->sb0.p));
+                             e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
+                             e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0));
     cudaEventRecord(e->ev[2], s);
-    const double *base = e->raw.p;
     if (e->mode == 1) {
       if (fp32)
         RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
-                                  e->st.p, e->nst, e->wt32.p, n, e->smooth.p, &d->pairs, s));
+                                  e->st.p, e->nst, e->wt32.p, p1, e->smooth.p, &d->pairs, s, p0));
       else
         RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat,
-                                e->st.p, e->nst, e->wt.p, n, e->smooth.p, &d->pairs, s));
-      base = e->smooth.p;
+                                e->st.p, e->nst, e->wt.p, p1, e->smooth.p, &d->pairs, s, p0));
       launches += 1;
     }
     cudaEventRecord(e->ev[3], s);
+  } else {
+    for (int k = 1; k < 4; ++k) cudaEventRecord(e->ev[k], s);
+  }
+  e->score_launches = launches;
+  e->scored = true;
+  return RCB_OK;
+}
+
+// Decision half of iterate(): rank order (K7), acceptance (K8) and its
+// bookkeeping, K1 pass 1 of the next raster, the iteration record.
+static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
+  if (!e->scored) return fail(RCB_ERR_VALUE, "rcb_engine_finish without rcb_engine_score");
+  e->scored = false;
+  RCB_CUDA(cudaSetDevice(e->device));
+  cudaStream_t s = e->s;
+  const int64_t n = e->N;
+  const Lat &lat = e->lat;
+  Scalars *d = e->sc.p;
+  int launches = e->score_launches;
+  const int poisson = e->ecfg.noise_model == 1;
+  if (n > 0) {
+    const double *base = e->mode == 1 ? e->smooth.p : e->raw.p;
     RCB_TRY(rank_order(base, e->dint.p, e->ecfg.lam, n, e->px.p, e->pcomp.p, e->ocfg.seed,
                        e->rank.p, e->rsc, e->order.p, &d->nneg, s));
     cudaEventRecord(e->ev[4], s);
@@ -619,7 +687,7 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
     }
     launches += 4 + 1 + 3 * 8;  // emit, dint, dE, rank, 2 radix sorts (~8 passes each)
   } else {
-    for (int k = 1; k < 5; ++k) cudaEventRecord(e->ev[k], s);
+    cudaEventRecord(e->ev[4], s);
   }
   // K1 pass 1 on the updated raster: the particle count of the record and the
   // lattice index map of the next iteration
@@ -674,6 +742,43 @@ int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
   rec->negative = (int64_t)e->hsc->nneg;
   rec->pairs = (int64_t)e->hsc->pairs;
   rec->mode = e->mode;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
+  if (e->scored) return fail(RCB_ERR_VALUE, "rcb_engine_iterate between score and finish");
+  RCB_TRY(engine_score(e));
+  return engine_finish(e, rec);
+}
+
+int32_t rcb_engine_set_slab(rcb_engine *e, int64_t lo, int64_t hi) {
+  const int64_t np = e->lat.ndim == 3 ? e->lat.nz : e->lat.ny;
+  if (hi > lo && (lo < 0 || hi > np)) return fail(RCB_ERR_VALUE, "slab outside the lattice");
+  if (e->scored) return fail(RCB_ERR_VALUE, "slab change between score and finish");
+  e->slab_lo = hi > lo ? lo : 0;
+  e->slab_hi = hi > lo ? hi : 0;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_score(rcb_engine *e, rcb_slab_info *info) {
+  if (e->scored) return fail(RCB_ERR_VALUE, "rcb_engine_score called twice");
+  RCB_TRY(engine_score(e));
+  info->n_particles = e->N;
+  info->p0 = e->p0;
+  info->p1 = e->p1;
+  info->base = e->mode == 1 ? (void *)e->smooth.p : (void *)e->raw.p;
+  const bool ps = e->ecfg.region_model == 1 && e->N > 0;
+  info->cb0 = ps ? (void *)e->cb0.p : nullptr;
+  info->sb0 = ps ? (void *)e->sb0.p : nullptr;
+  info->stream = (void *)e->s;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_finish(rcb_engine *e, rcb_iter_record *rec) { return engine_finish(e, rec); }
+
+int32_t rcb_engine_particle_ranges(rcb_engine *e, const int64_t *planes, int32_t k, int64_t *out) {
+  RCB_CUDA(cudaSetDevice(e->device));
+  for (int32_t i = 0; i < k; i += 4) RCB_TRY(plane_ranges(e, planes + i, std::min(4, k - i), out + i));
   return RCB_OK;
 }
 

@@ -163,7 +163,7 @@ std::vector<Off> sobolev_rows(int ndim, double length_scale, int *max_d2);
 int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
                         const int32_t *pcomp, const double *raw, const Lat &lat, const Off *rows,
                         int nrows, const double *wt, int64_t n, double *out,
-                        unsigned long long *pairs, cudaStream_t s);
+                        unsigned long long *pairs, cudaStream_t s, int64_t p0 = 0);
 int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &lat,
                        const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,
                        const Off *st, int nst, const double *wt, double *d_out,
@@ -181,7 +181,7 @@ int32_t delta_ps32_batch(const int32_t *L, const float *I32, const int32_t *Cown
 int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
                           const int32_t *pcomp, const float *raw, const Lat &lat, const Off *rows,
                           int nrows, const float *wt, int64_t n, double *out,
-                          unsigned long long *pairs, cudaStream_t s);
+                          unsigned long long *pairs, cudaStream_t s, int64_t p0 = 0);
 // rank.cu
 int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t n,
                    const uint32_t *px, const int32_t *pcomp, uint64_t seed, double *rank,

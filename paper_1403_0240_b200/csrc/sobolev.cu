@@ -32,8 +32,8 @@ __global__ void __launch_bounds__(128) k_sobolev(
     const int32_t *__restrict__ pcomp, const uint32_t *__restrict__ px,
     const double *__restrict__ raw, Lat lat, const Off *__restrict__ rows, int nrows,
     const double *__restrict__ wt, int64_t n, double *__restrict__ out,
-    const uint32_t *__restrict__ oidx, unsigned long long *__restrict__ pairs) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t *__restrict__ oidx, unsigned long long *__restrict__ pairs, int64_t p0 = 0) {
+  int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long np = 0;
   if (p < n) {
     const int64_t f = px[p];
@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(128) k_sobolev32(
     const int32_t *__restrict__ pcomp, const uint32_t *__restrict__ px,
     const float *__restrict__ raw, Lat lat, const Off *__restrict__ rows, int nrows,
     const float *__restrict__ wt, int64_t n, double *__restrict__ out,
-    unsigned long long *__restrict__ pairs) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long *__restrict__ pairs, int64_t p0 = 0) {
+  int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long np = 0;
   if (p < n) {
     const int64_t f = px[p];
@@ -127,10 +127,10 @@ __global__ void __launch_bounds__(128) k_sobolev32(
 int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
                           const int32_t *pcomp, const float *raw, const Lat &lat, const Off *rows,
                           int nrows, const float *wt, int64_t n, double *out,
-                          unsigned long long *pairs, cudaStream_t s) {
-  if (n == 0) return RCB_OK;
-  k_sobolev32<<<grid_for(n, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows, nrows,
-                                               wt, n, out, pairs);
+                          unsigned long long *pairs, cudaStream_t s, int64_t p0) {
+  if (n <= p0) return RCB_OK;
+  k_sobolev32<<<grid_for(n - p0, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows,
+                                                    nrows, wt, n, out, pairs, p0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -174,10 +174,10 @@ std::vector<Off> sobolev_stencil(int ndim, double length_scale) {
 int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
                         const int32_t *pcomp, const double *raw, const Lat &lat, const Off *rows,
                         int nrows, const double *wt, int64_t n, double *out,
-                        unsigned long long *pairs, cudaStream_t s) {
-  if (n == 0) return RCB_OK;
-  k_sobolev<<<grid_for(n, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows, nrows,
-                                             wt, n, out, nullptr, pairs);
+                        unsigned long long *pairs, cudaStream_t s, int64_t p0) {
+  if (n <= p0) return RCB_OK;
+  k_sobolev<<<grid_for(n - p0, 128), 128, 0, s>>>(site_off, pown, pcomp, px, raw, lat, rows,
+                                                  nrows, wt, n, out, nullptr, pairs, p0);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

@@ -104,6 +104,9 @@ class RegionCompetition:
         if energy_config.noise_model == "poisson" and image.size and np.min(image) < 0:
             raise ValueError("Poisson noise model requires nonnegative intensities")
         _lib.require_device()
+        self.device = int(device)
+        self._slab = None
+        self._exchange = None
         self.image = np.ascontiguousarray(image, dtype=np.float64)
         self.shape = self.image.shape
         self.conn = conn if conn is not None else Connectivity.default(self.image.ndim)
@@ -224,13 +227,31 @@ class RegionCompetition:
 
     # -- single iteration (optimizer.py:122-160) -------------------------------
     def iterate(self) -> IterationRecord:
+        t0 = self._pre_iterate()
+        if self._slab is None:
+            rec = _lib.IterRecord()
+            _lib.check(_lib.lib.rcb_engine_iterate(self._h, C.byref(rec)))
+        else:  # z-slab sharded (shard.py): score, all-gather the slabs' scores, finish
+            info = self._slab.score()
+            self._exchange.gather(self._slab.buffers(info, self.device), self._slab.ranges(),
+                                  stream=info.stream)
+            rec = self._slab.finish()
+        return self._post_iterate(rec, t0)
+
+    def attach_slab(self, slab, exchange) -> None:
+        """Shard the scoring kernels by outer planes (shard.slab_engine)."""
+        self._slab = slab
+        self._exchange = exchange
+
+    def _pre_iterate(self) -> float:
         t0 = time.perf_counter()
-        cfg = self.config
-        if cfg.debug_check_rate > 0.0:
+        if self.config.debug_check_rate > 0.0:
             self._debug_check()
         _lib.check(_lib.lib.rcb_engine_set_mode(self._h, int(self.mode == "sobolev")))
-        rec = _lib.IterRecord()
-        _lib.check(_lib.lib.rcb_engine_iterate(self._h, C.byref(rec)))
+        return t0
+
+    def _post_iterate(self, rec, t0: float) -> IterationRecord:
+        cfg = self.config
         self.iteration = int(rec.iteration)
         self._cand = None
         self._last_n = int(rec.candidates)
