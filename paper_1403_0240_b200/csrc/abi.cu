@@ -271,11 +271,14 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   e->lat = make_lat(ndim, dims);
   {
     // prime the device pool with the engine's footprint plus room for the
-    // particle buffers to double a few times (~320 B per site + 256 MB,
-    // at most 16 GB): later stream-ordered allocations are then served
+    // particle buffers to double a few times (~320 B per site + 256 MB, at
+    // most max(16 GB, half the free memory)): later stream-ordered allocations are then served
     // from cached memory instead of blocking the host while memory is mapped
     size_t want = (size_t)320 * (size_t)e->lat.V + ((size_t)256 << 20);
-    if (want > ((size_t)16 << 30)) want = (size_t)16 << 30;
+    size_t free_b = 0, total_b = 0;
+    size_t cap = (size_t)16 << 30;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
+    if (want > cap) want = cap;
     void *prime = nullptr;
     if (cudaMallocAsync(&prime, want, s) == cudaSuccess) cudaFreeAsync(prime, s);
     cudaGetLastError();

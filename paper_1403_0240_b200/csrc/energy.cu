@@ -137,14 +137,21 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
     }
 #pragma unroll
     for (int u = 0; u < kPsChunk; ++u) {
-      if (lab[u] == a) {
-        acc_a += rho(iy[u], (sy[u] - v) / (cy[u] - 1.0), poisson) -
-                 (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
-      } else if (lab[u] == b) {
-        acc_b += rho(iy[u], (sy[u] + v) / (cy[u] + 1.0), poisson) -
-                 (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
-        cb += 1;
-        sb += iy[u];
+      // one rho evaluation for either side (no divergent a/b paths): the
+      // a-term's (sy - v)/(cy - 1) is computed as (sy + (-v))/(cy + (-1)),
+      // which IEEE arithmetic rounds identically
+      const bool isa = lab[u] == a;
+      if (isa || lab[u] == b) {
+        const double t = rho(iy[u], (sy[u] + (isa ? -v : v)) / (cy[u] + (isa ? -1.0 : 1.0)),
+                             poisson) -
+                         (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+        if (isa) {
+          acc_a += t;
+        } else {
+          acc_b += t;
+          cb += 1;
+          sb += iy[u];
+        }
       }
     }
   }
@@ -154,6 +161,85 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
   d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
   out[i] = d;
   if (cb0) {  // the competitor's iteration-start ball count/sum at x (PS ledger terms)
+    cb0[i] = cb;
+    sb0[i] = sb;
+  }
+}
+
+// K5 for 3-D lattices below 2^31 sites: the 2-D kernel's scheme (one pass
+// over the ball, 32-bit coordinates, offsets in shared memory, kPsChunk
+// offsets' loads in flight) with (dz, dy, dx) offsets.  The a- and b-terms are
+// two sequential sums in ball-offset order: bit-identical to delta_ps.
+__global__ void __launch_bounds__(128, 6) k_delta_ps3d(
+    const int32_t *__restrict__ L, const double *__restrict__ I, const int32_t *__restrict__ Cown,
+    const double *__restrict__ Sown, int nx, int ny, int nz, const Off *__restrict__ ball,
+    int nball, const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+    const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
+    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0) {
+  __shared__ int sofs[kPsMaxBall];  // dz:8 | dy:8 | dx:8, signed, packed
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = ((int)(uint8_t)ball[k].dz << 16) | ((int)(uint8_t)ball[k].dy << 8) |
+              (int)(uint8_t)ball[k].dx;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int f = (int)px[i];
+  const int plane = nx * ny;
+  const int z = f / plane, r = f - z * plane;
+  const int y = r / nx, x = r - y * nx;
+  const int32_t a = pown[i], b = pcomp[i];
+  const double v = I[f];
+  double acc_a = 0.0, acc_b = 0.0, sb = 0.0;
+  int32_t cb = 0;
+  for (int k0 = 0; k0 < nball; k0 += kPsChunk) {
+    int g[kPsChunk];
+    int32_t lab[kPsChunk];
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      const int k = k0 + u;
+      const int o = k < nball ? sofs[k] : 0;
+      const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
+                xx = x + (int)(int8_t)o;
+      const bool ok = k < nball && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+                      (unsigned)xx < (unsigned)nx;
+      g[u] = ok ? zz * plane + yy * nx + xx : f;
+      lab[u] = ok ? __ldg(L + g[u]) : -1;
+    }
+    double cy[kPsChunk], sy[kPsChunk], iy[kPsChunk], r0[kPsChunk];
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      const bool need = lab[u] == a || lab[u] == b;
+      cy[u] = need ? (double)__ldg(Cown + g[u]) : 1.0;
+      sy[u] = need ? __ldg(Sown + g[u]) : 0.0;
+      iy[u] = need ? __ldg(I + g[u]) : 0.0;
+      r0[u] = (need && rho0) ? __ldg(rho0 + g[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPsChunk; ++u) {
+      // one rho evaluation for either side (no divergent a/b paths): the
+      // a-term's (sy - v)/(cy - 1) is computed as (sy + (-v))/(cy + (-1)),
+      // which IEEE arithmetic rounds identically
+      const bool isa = lab[u] == a;
+      if (isa || lab[u] == b) {
+        const double t = rho(iy[u], (sy[u] + (isa ? -v : v)) / (cy[u] + (isa ? -1.0 : 1.0)),
+                             poisson) -
+                         (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+        if (isa) {
+          acc_a += t;
+        } else {
+          acc_b += t;
+          cb += 1;
+          sb += iy[u];
+        }
+      }
+    }
+  }
+  double d = 0.0 + acc_a;
+  d = d + acc_b;
+  d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
+  d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
+  out[i] = d;
+  if (cb0) {
     cb0[i] = cb;
     sb0[i] = sb;
   }
@@ -267,6 +353,10 @@ int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, c
     k_delta_ps2d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny, ball,
                                                   nball, px, pown, pcomp, n, poisson, out, rho0,
                                                   cb0, sb0);
+  else if (lat.ndim == 3 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
+    k_delta_ps3d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny,
+                                                  (int)lat.nz, ball, nball, px, pown, pcomp, n,
+                                                  poisson, out, rho0, cb0, sb0);
   else
     k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown,
                                                 pcomp, n, poisson, out, rho0, cb0, sb0);
