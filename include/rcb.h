@@ -158,7 +158,9 @@ int32_t rcb_engine_timings(rcb_engine *eng, float *ms6, int32_t *launches);
  * runs, [2] deferred to the global BFS, [3] BFS aborted on a pending site,
  * [4] candidates with rank < 0, [5] accepted moves, [6] 1 if the parallel
  * acceptance ran (0 = sequential), [7] device us of the acceptance kernels,
- * [8] total BFS levels, [9] deepest BFS (levels), [10] PS ledger recounts of
+ * [8] total BFS levels (dataflow: union-find rebuilds of the deferred-candidate
+ * jobs), [9] deepest BFS (dataflow: rebuilds forced by a non-simple removal),
+ * [10] PS ledger recounts of
  * flipped ball sites, [11] flips gathered by the PS ledger terms. */
 int32_t rcb_engine_counters(rcb_engine *eng, int64_t *out12);
 /* Diagnostics of the last parallel acceptance: for rank position i < *n,

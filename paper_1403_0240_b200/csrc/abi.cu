@@ -113,6 +113,9 @@ struct rcb_engine {
   DBuf<uint32_t> site_off, px, order;
   DBuf<int32_t> pown, pcomp, dint;
   DBuf<double> raw, smooth, rank;
+  DBuf<int4> pk;  // K6 packed partner records
+  bool sob_packed = false;
+  int nwt = 0;
   DBuf<int64_t> acc;
   // parallel acceptance state (accept_par.cu)
   DBuf<int32_t> newlab, wpos, pend, dround, lab_pend, nown, bfs_list, ctl, dint_acc, blocker;
@@ -124,7 +127,8 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
-  DBuf<unsigned long long> ufp, job, wpk, eval_per;
+  DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark;
+  DBuf<uint32_t> qlist, qscr;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
@@ -163,7 +167,7 @@ struct rcb_engine {
       Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
-      raw.release(s); smooth.release(s); rank.release(s); acc.release(s); sc.release(s);
+      raw.release(s); smooth.release(s); rank.release(s); pk.release(s); acc.release(s); sc.release(s);
       newlab.release(s); wpos.release(s); pend.release(s); dround.release(s); lab_pend.release(s);
       nown.release(s); blocker.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
@@ -172,6 +176,7 @@ struct rcb_engine {
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
+      ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -347,6 +352,11 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   }
   TRYB(upload(e->st, st.data(), st.size(), s));
   TRYB(upload(e->wt, scfg->weights, (size_t)scfg->n_weights, s));
+  e->nwt = scfg->n_weights;
+  {
+    const char *ks = getenv("RCB_K6");  // "scalar": the unpacked K6 (comparison runs)
+    e->sob_packed = sobolev_packable(e->nl, e->nst, maxd2) && !(ks && strcmp(ks, "scalar") == 0);
+  }
   if (ocfg->fp32) {
     TRYB(e->I32.reserve(V, s));
     TRYB(e->wt32.reserve(scfg->n_weights, s));
@@ -471,12 +481,21 @@ static int32_t engine_score(rcb_engine *e) {
                              e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0));
     cudaEventRecord(e->ev[2], s);
     if (e->mode == 1) {
-      if (fp32)
+      if (fp32) {
         RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
                                   e->st.p, e->nst, e->wt32.p, p1, e->smooth.p, &d->pairs, s, p0));
-      else
+      } else if (e->sob_packed && e->nst > 1) {
+        // packed records of the partners K6 reads ([h0, h1) covers the halo);
+        // with one stencil row (w = 1) the unpacked kernel reads less
+        RCB_TRY(e->pk.reserve(n, s));
+        RCB_TRY(sobolev_pack(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, h0, h1, e->pk.p, s));
+        RCB_TRY(sobolev_packed(e->site_off.p, e->pk.p, lat, e->st.p, e->nst, e->wt.p, e->nwt, p0,
+                               p1, e->smooth.p, &d->pairs, s));
+        launches += 1;
+      } else {
         RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat,
                                 e->st.p, e->nst, e->wt.p, p1, e->smooth.p, &d->pairs, s, p0));
+      }
       launches += 1;
     }
     cudaEventRecord(e->ev[3], s);
@@ -556,6 +575,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.max_insert = mi ? atoi(mi) : 0;
         const char *bc = getenv("RCB_DF_BOXCAP");  // tests: 0 sends overflows to assist jobs
         P.box_cap = bc ? atoi(bc) : -1;
+        const char *qj = getenv("RCB_DF_QJOB");  // "0": a full union-find per deferred candidate
+        P.qjob = !(qj && qj[0] == '0');
       }
       if (e->profile) {
         RCB_TRY(e->tdbg.reserve(4 * n, s));
@@ -569,6 +590,10 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       const bool use_df = fits && e->accept_mode != 1 && n < 0xffffff && e->nl <= 65536;
       if (use_df) {
         if (!e->ufp.p) {
+          RCB_TRY(e->ufq.reserve(lat.V, s));
+          RCB_TRY(e->qmark.reserve(lat.V, s));
+          RCB_CUDA(cudaMemsetAsync(e->ufq.p, 0xff, sizeof(unsigned long long) * lat.V, s));
+          RCB_CUDA(cudaMemsetAsync(e->qmark.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_TRY(e->ufp.reserve(lat.V, s));
           RCB_TRY(e->wpk.reserve(lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->wpk.p, 0xff, sizeof(unsigned long long) * lat.V, s));
@@ -576,6 +601,13 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
           RCB_CUDA(cudaMemsetAsync(e->ufp.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->job.p, 0, sizeof(unsigned long long) * 64, s));
         }
+        // registry of deferred candidates (cleared after each run by k_q_reset)
+        RCB_TRY(e->qlist.reserve(n, s));
+        RCB_TRY(e->qscr.reserve(n, s));
+        P.ufq = e->ufq.p;
+        P.qmark = e->qmark.p;
+        P.qlist = e->qlist.p;
+        P.qscr = e->qscr.p;
         P.ufp = e->ufp.p;
         P.job = e->job.p;
         P.wp = e->wpk.p;

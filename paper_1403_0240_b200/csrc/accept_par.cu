@@ -1092,7 +1092,7 @@ __device__ __forceinline__ LabBox grown_box(const ParArgs &A, int32_t a) {
 //   ufp[y] = (~tag << 32) | parent for the current tag; entries of older
 //            tags are larger, so they read as roots and atomicMin replaces them.
 // ---------------------------------------------------------------------------
-static constexpr int kJobChunk = 64;  // sites per claimed chunk (2 per lane)
+static constexpr int kJobChunk = 64;  // items per claimed chunk (2 per lane)
 
 __device__ __forceinline__ unsigned long long *job_desc(const ParArgs &A, uint32_t tag) {
   return A.job + 8 + 8 * (tag & 3);
@@ -1129,25 +1129,67 @@ __device__ void job_union(unsigned long long *ufp, uint32_t hi, uint32_t a, uint
   }
 }
 
+__device__ __forceinline__ void df_stamp(const ParArgs &A, int32_t pos, int k) {
+  if (A.tdbg && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tdbg[4 * pos + k] = (long long)t;
+  }
+}
+
+// Deferred-candidate registry (Q) and job types.  A candidate whose BFS
+// overflows registers its site in Q before waiting for the low-water mark:
+//   qmark[y] = (registration sequence << 32) | owner label (min over the
+//              candidates at y; all-ones = none), qlist[seq] = site.
+// Jobs of the low-water owner (sequential by construction: one at a time):
+//   kJobUF    union-find of a's grown box in V_pos, Q sites (seq < S) and x
+//             excluded: the components of a \ Q ("Q-UF", tag T);
+//   kJobScan  bring the Q-UF from V_lo to V_hi: for the accepted moves at
+//             positions [lo, hi), a site that joined a (still a in V_hi) is
+//             united with its a \ Q neighbours; a UF member that left a must
+//             have been box-simple in a \ Q in its own view V_p (then every
+//             component stays connected), otherwise the Q-UF is invalidated;
+//   kJobQuery the contracted graph for candidate x in Q: Q nodes of label a
+//             (in a in V_pos, != x) united with their a-neighbours (Q nodes,
+//             or the Q-UF roots of the others) in a second union-find (ufq).
+// x's seeds share a ufq root iff a \ {x} keeps them in one piece: the Q-UF
+// components are connected without any Q site, and every other connection
+// runs through Q nodes, whose adjacency the query adds.  One full union-find
+// then serves every later deferred candidate of the label until a non-simple
+// removal (or a candidate registered after it) forces a new one.
+// Job state (lane 0 of the owner only; jobs are serialised):
+//   job[40] registrations issued, job[41] registrations published,
+//   job[42] Q-UF tag T (0: none), job[43] its label, job[44] its S,
+//   job[45] position its view has reached, job[46] invalid flag (scan).
+static constexpr int kJobUF = 0, kJobScan = 1, kJobQuery = 2;
+
+__device__ __forceinline__ bool is_q(const ParArgs &A, int64_t y, int32_t a, uint32_t S) {
+  const unsigned long long m = __ldcg(A.qmark + y);
+  return (uint32_t)m == (uint32_t)a && (uint32_t)(m >> 32) < S;
+}
+
 // Claim and process one chunk of the current job (whole warp).  Returns false
 // when there is nothing to claim.  Claims are fetch-and-add (a failed CAS
 // storm from thousands of waiting warps would serialise on job[0]); claims
-// past the last chunk are harmless no-ops.
+// past the last chunk are harmless no-ops, and so is a claim whose
+// descriptor slot already holds a later job (its tag is checked).
 __device__ bool warp_help(const ParArgs &A) {
   const int lane = threadIdx.x & 31;
-  unsigned long long c = 0, desc[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long c = 0, desc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int got = 0;
   if (lane == 0) {
     c = __ldcg(A.job);  // relaxed peek; the claim below is an acquire RMW
     if ((c >> 32) != 0 && (uint32_t)c < (uint32_t)__ldcg(A.job + 2)) {  // tag 0: none yet
       asm volatile("atom.add.acquire.gpu.global.u64 %0, [%1], 1;" : "=l"(c) : "l"(A.job) : "memory");
       const unsigned long long *d = job_desc(A, (uint32_t)(c >> 32));
-      if ((uint32_t)c < (uint32_t)__ldcg(d + 6)) {
+      const unsigned long long d6 = ld_acq64(d + 6);
+      if ((uint32_t)(d6 >> 32) == (uint32_t)(c >> 32) && (uint32_t)c < (uint32_t)d6) {
         desc[0] = __ldcg(d);
         desc[1] = __ldcg(d + 1);
         desc[2] = __ldcg(d + 2);
         desc[4] = __ldcg(d + 4);
         desc[5] = __ldcg(d + 5);
+        desc[7] = __ldcg(d + 7);
         got = 1;
       }
     }
@@ -1156,33 +1198,92 @@ __device__ bool warp_help(const ParArgs &A) {
   if (!got) return false;
   c = __shfl_sync(0xffffffffu, c, 0);
   const int64_t f = (int64_t)__shfl_sync(0xffffffffu, desc[0], 0);
-  const int32_t a = (int32_t)__shfl_sync(0xffffffffu, desc[1], 0);
-  const int32_t pos = (int32_t)__shfl_sync(0xffffffffu, desc[2], 0);
+  const unsigned long long d1 = __shfl_sync(0xffffffffu, desc[1], 0);
+  const unsigned long long d2 = __shfl_sync(0xffffffffu, desc[2], 0);
   const unsigned long long o4 = __shfl_sync(0xffffffffu, desc[4], 0);
   const unsigned long long o5 = __shfl_sync(0xffffffffu, desc[5], 0);
-  const int64_t z0 = (int64_t)(o4 & 0x1fffff), y0 = (int64_t)((o4 >> 21) & 0x1fffff),
-                x0 = (int64_t)(o4 >> 42);
-  const int64_t bw = (int64_t)(o5 & 0x1fffff), bh = (int64_t)((o5 >> 21) & 0x1fffff);
+  const int64_t nitems = (int64_t)__shfl_sync(0xffffffffu, desc[7], 0);
+  const int32_t a = (int32_t)(uint32_t)d1;
+  const uint32_t S = (uint32_t)(d1 >> 32);
+  const int32_t pos = (int32_t)(uint32_t)d2;
+  const int type = (int)(d2 >> 32);
   const uint32_t tag = (uint32_t)(c >> 32), hi = ~tag;
   const Lat &lat = A.lat;
   View v{A, pos};
-  const int64_t i0 = (int64_t)(uint32_t)c * kJobChunk, nbox = (int64_t)__ldcg(job_desc(A, tag) + 7);
+  const int64_t i0 = (int64_t)(uint32_t)c * kJobChunk;
+  if (type == kJobUF) {
+    const int64_t z0 = (int64_t)(o4 & 0x1fffff), y0 = (int64_t)((o4 >> 21) & 0x1fffff),
+                  x0 = (int64_t)(o4 >> 42);
+    const int64_t bw = (int64_t)(o5 & 0x1fffff), bh = (int64_t)((o5 >> 21) & 0x1fffff);
 #pragma unroll
-  for (int i = 0; i < kJobChunk / 32; ++i) {
-    const int64_t li = i0 + i * 32 + lane;
-    if (li >= nbox) continue;
-    const int64_t zz = z0 + li / (bw * bh), yy = y0 + (li / bw) % bh, x = x0 + li % bw;
-    const int64_t y = (zz * lat.ny + yy) * lat.nx + x;
-    if (y == f || v.lab(y) != a) continue;
-    // backward half of the full neighbourhood: every edge once (the job box
-    // contains every a-site, so edges to sites outside it never join a-sites)
-    for (int k = 0; k < 13; ++k) {
-      const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;  // lexicographically < 0
-      if (lat.ndim == 2 && dz != 0) continue;
-      const int64_t z2 = zz + dz, y2 = yy + dy, x2 = x + dx;
+    for (int i = 0; i < kJobChunk / 32; ++i) {
+      const int64_t li = i0 + i * 32 + lane;
+      if (li >= nitems) continue;
+      const int64_t zz = z0 + li / (bw * bh), yy = y0 + (li / bw) % bh, x = x0 + li % bw;
+      const int64_t y = (zz * lat.ny + yy) * lat.nx + x;
+      if (y == f || v.lab(y) != a || (S && is_q(A, y, a, S))) continue;
+      // backward half of the full neighbourhood: every edge once (the job box
+      // contains every a-site, so edges to sites outside it never join a-sites)
+      for (int k = 0; k < 13; ++k) {
+        const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;  // lexicographically < 0
+        if (lat.ndim == 2 && dz != 0) continue;
+        const int64_t z2 = zz + dz, y2 = yy + dy, x2 = x + dx;
+        if (!lat.inb(z2, y2, x2)) continue;
+        const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
+        if (g != f && v.lab(g) == a && !(S && is_q(A, g, a, S)))
+          job_union(A.ufp, hi, (uint32_t)y, (uint32_t)g);
+      }
+    }
+  } else if (type == kJobScan) {
+    // one item per (position, neighbour): a site that joined a (and is still
+    // a in V_pos) is united with that neighbour if it is in a \ Q; for a UF
+    // member that left a, bit k of qscr[p - lo] records whether neighbour k
+    // was in a \ Q in the mover's view V_p (the owner tests the boxes)
+    const uint32_t hiT = ~(uint32_t)o5;
+    const int32_t lo = (int32_t)o4;
+#pragma unroll
+    for (int i = 0; i < kJobChunk / 32; ++i) {
+      const int64_t li = i0 + i * 32 + lane;
+      if (li >= nitems) continue;
+      const int32_t p = lo + (int32_t)(li / 26);
+      const int k = (int)(li % 26), kk = k < 13 ? k : k + 1;
+      if (*(volatile uint8_t *)(A.dec + p) != ACC) continue;
+      const int4 rc = __ldg(A.rec + p);
+      const int64_t y = rc.x;
+      const int32_t ap = rc.y & 0x7fffffff, bp = rc.z & 0x7fffffff;
+      if (bp != a && ap != a) continue;
+      int64_t zz, yy, xx;
+      lat.coord(y, zz, yy, xx);
+      const int64_t z2 = zz + kk / 9 - 1, y2 = yy + (kk / 3) % 3 - 1, x2 = xx + kk % 3 - 1;
       if (!lat.inb(z2, y2, x2)) continue;
       const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
-      if (g != f && v.lab(g) == a) job_union(A.ufp, hi, (uint32_t)y, (uint32_t)g);
+      if (bp == a) {
+        if (v.lab(y) == a && v.lab(g) == a && !is_q(A, g, a, S))
+          job_union(A.ufp, hiT, (uint32_t)y, (uint32_t)g);
+      } else {
+        const View vp{A, p};
+        if (vp.lab(g) == a && !is_q(A, g, a, S)) atomicOr(A.qscr + (p - lo), 1u << kk);
+      }
+    }
+  } else {  // kJobQuery: one item per (registered site, neighbour)
+    const uint32_t hiT = ~(uint32_t)o5;
+#pragma unroll
+    for (int i = 0; i < kJobChunk / 32; ++i) {
+      const int64_t li = i0 + i * 32 + lane;
+      if (li >= nitems) continue;
+      const int64_t sqi = li / 26;
+      const int k = (int)(li - sqi * 26), kk = k < 13 ? k : k + 1;
+      const uint32_t sq = A.qlist[sqi];
+      const unsigned long long m = __ldcg(A.qmark + sq);
+      if ((uint32_t)m != (uint32_t)a || (uint32_t)(m >> 32) != (uint32_t)sqi) continue;
+      int64_t zz, yy, xx;
+      lat.coord(sq, zz, yy, xx);
+      const int64_t z2 = zz + kk / 9 - 1, y2 = yy + (kk / 3) % 3 - 1, x2 = xx + kk % 3 - 1;
+      if (!lat.inb(z2, y2, x2)) continue;
+      const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
+      if ((int64_t)sq == f || g == f || v.lab(sq) != a || v.lab(g) != a) continue;
+      const uint32_t t = is_q(A, g, a, S) ? (uint32_t)g : job_find(A.ufp, hiT, (uint32_t)g);
+      job_union(A.ufq, hi, sq, t);
     }
   }
   __threadfence();
@@ -1191,63 +1292,239 @@ __device__ bool warp_help(const ParArgs &A) {
   return true;
 }
 
-// Run the job of candidate pos (the earliest undecided; whole warp).
-// Returns 1 (one piece) or 2 (several pieces).
-__device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
+// Publish a job (owner lane 0) and return its tag.
+__device__ uint32_t job_publish(const ParArgs &A, int type, int64_t f, int32_t a, uint32_t S,
+                                int32_t pos, unsigned long long d4, unsigned long long d5,
+                                int64_t nitems) {
+  const unsigned long long nch = (unsigned long long)((nitems + kJobChunk - 1) / kJobChunk);
+  const uint32_t tag = (uint32_t)A.job[1] + 1;
+  A.job[1] = tag;
+  unsigned long long *d = job_desc(A, tag);
+  d[0] = (unsigned long long)f;
+  d[1] = (unsigned long long)(uint32_t)a | ((unsigned long long)S << 32);
+  d[2] = (unsigned long long)(uint32_t)pos | ((unsigned long long)type << 32);
+  d[3] = 0;
+  d[4] = d4;
+  d[5] = d5;
+  d[7] = (unsigned long long)nitems;
+  __threadfence();
+  st_rel64(d + 6, nch | ((unsigned long long)tag << 32));
+  A.job[2] = nch;
+  __threadfence();
+  st_rel64(A.job, (unsigned long long)tag << 32);
+  return tag;
+}
+
+// Run a published job to completion (whole warp; lane 0 holds tag and nch).
+__device__ void job_run(const ParArgs &A, uint32_t tag, unsigned long long nch) {
   const int lane = threadIdx.x & 31;
-  uint32_t tag = 0;
-  unsigned long long nch = 0;
-  if (lane == 0) {
-    const LabBox bx = grown_box(A, a);
-    const int64_t nbox = (int64_t)bx.bd * bx.bh * bx.bw;
-    nch = (unsigned long long)((nbox + kJobChunk - 1) / kJobChunk);
-    tag = (uint32_t)A.job[1] + 1;
-    A.job[1] = tag;
-    unsigned long long *d = job_desc(A, tag);
-    d[0] = (unsigned long long)f;
-    d[1] = (unsigned long long)(uint32_t)a;
-    d[2] = (unsigned long long)(uint32_t)pos;
-    d[3] = 0;
-    d[4] = (unsigned long long)bx.z0 | ((unsigned long long)bx.y0 << 21) |
-           ((unsigned long long)bx.x0 << 42);
-    d[5] = (unsigned long long)bx.bw | ((unsigned long long)bx.bh << 21) |
-           ((unsigned long long)bx.bd << 42);
-    d[6] = nch;
-    d[7] = (unsigned long long)nbox;
-    A.job[2] = nch;
-    __threadfence();
-    st_rel64(A.job, (unsigned long long)tag << 32);
-  }
   tag = __shfl_sync(0xffffffffu, tag, 0);
   nch = __shfl_sync(0xffffffffu, nch, 0);
   __syncwarp();
   while (warp_help(A)) {
   }
-  int r = 2;
   if (lane == 0) {
     const unsigned long long *done = job_desc(A, tag) + 3;
     while (ld_acq64(done) < nch) __nanosleep(64);
     __threadfence();
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned long long job_chunks(int64_t n) {
+  return (unsigned long long)((n + kJobChunk - 1) / kJobChunk);
+}
+
+// Run the topology job of candidate pos (the earliest undecided; whole warp;
+// x registered in Q).  Returns 1 (one piece) or 2 (several pieces).
+__device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t a,
+                               uint32_t *qbits) {
+  const int lane = threadIdx.x & 31;
+  // 1. bring the Q-UF of label a up to V_pos, or rebuild it
+  int need_uf = 0;
+  uint32_t tag = 0, T = 0, S = 0;
+  unsigned long long nch = 0;
+  if (lane == 0) {
+    T = (uint32_t)A.job[42];
+    S = (uint32_t)A.job[44];
+    const uint32_t seqx = (uint32_t)(__ldcg(A.qmark + f) >> 32);
+    need_uf = !(T != 0 && (int32_t)A.job[43] == a && seqx < S);
+    if (!need_uf) {
+      const int32_t lo = (int32_t)A.job[45];
+      if (pos > lo) nch = 1;
+    }
+  }
+  if (!__shfl_sync(0xffffffffu, need_uf, 0) && __shfl_sync(0xffffffffu, nch, 0)) {
+    const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.job[45] : 0ull, 0);
+    for (int32_t q = lane; q < pos - lo; q += 32) A.qscr[q] = 0;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      A.job[46] = 0;
+      tag = job_publish(A, kJobScan, f, a, S, pos, (unsigned long long)(uint32_t)lo, T,
+                        26 * (int64_t)(pos - lo));
+      nch = job_chunks(26 * (int64_t)(pos - lo));
+    }
+  }
+  need_uf = __shfl_sync(0xffffffffu, need_uf, 0);
+  S = __shfl_sync(0xffffffffu, S, 0);
+  T = __shfl_sync(0xffffffffu, T, 0);
+  if (!need_uf && __shfl_sync(0xffffffffu, nch, 0)) {
+    job_run(A, tag, nch);
+    // removals of UF members: box-simple in a \ Q (in their view) keeps every
+    // component connected; the others are listed for the window test
+    {
+      const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.job[45] : 0ull, 0);
+      if (lane == 0) A.job[47] = 0;
+      __threadfence();
+      __syncwarp();
+      for (int32_t q = lane; q < pos - lo; q += 32) {
+        const int32_t p = lo + q;
+        if (*(volatile uint8_t *)(A.dec + p) != ACC) continue;
+        const int4 rc = __ldg(A.rec + p);
+        if ((rc.y & 0x7fffffff) != a || is_q(A, rc.x, a, S)) continue;
+        const uint32_t cells = __ldcg(A.qscr + q);
+        if (!cells) continue;
+        uint32_t reach = cells & (~cells + 1);
+        for (;;) {
+          uint32_t grow = reach;
+          for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, 1) & cells;
+          if (grow == reach) break;
+          reach = grow;
+        }
+        if (cells & ~reach) {
+          const unsigned long long w = atomicAdd(A.job + 47, 1ull);
+          if (w < 16) A.job[48 + w] = (unsigned long long)(uint32_t)p;
+          else atomicExch(A.job + 46, 1ull);
+        }
+      }
+      __threadfence();
+      __syncwarp();
+    }
+    // removals that were not box-simple in a \ Q: safe if the removed site's
+    // a \ Q neighbours stay connected inside its 9^3 window in its view V_p
+    // (window_verdict_bits == 1; then every path through it reroutes)
+    int nw = 0;
+    if (lane == 0) {
+      need_uf = __ldcg(A.job + 46) != 0;
+      nw = (int)__ldcg(A.job + 47);
+    }
+    need_uf = __shfl_sync(0xffffffffu, need_uf, 0);
+    nw = __shfl_sync(0xffffffffu, nw, 0);
+    const Lat &lat = A.lat;
+    const int nx = (int)lat.nx, ny = (int)lat.ny, nz = (int)lat.nz;
+    const bool is3 = lat.ndim == 3;
+    const int RB = is3 ? 4 : 5, WB = 2 * RB + 1, ncell = is3 ? WB * WB * WB : WB * WB;
+    for (int w = 0; w < nw && !need_uf; ++w) {
+      const int32_t p = (int32_t)__ldcg(A.job + 48 + w);
+      const int4 rc = __ldg(A.rec + p);
+      const int nxy = nx * ny;
+      const int zc = is3 ? rc.x / nxy : 0, rem = rc.x - zc * nxy;
+      const int yc = rem / nx, xc = rem - yc * nx;
+      const View vp{A, p};
+      for (int base = 0; base < ncell; base += 32) {
+        const int c = base + lane;
+        bool bit = false;
+        if (c < ncell) {
+          const int dz = is3 ? c / (WB * WB) - RB : 0;
+          const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
+          const int zz = zc + dz, yy = yc + dy, xx = xc + dx;
+          if ((dz || dy || dx) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+              (unsigned)xx < (unsigned)nx) {
+            const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
+            bit = vp.lab(gw) == a && !is_q(A, gw, a, S);
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) qbits[base >> 5] = m;
+      }
+      __syncwarp();
+      int ok = 0;
+      if (lane == 0) ok = (is3 ? window_verdict_bits<4>(qbits, WB) : window_verdict_bits<5>(qbits, 1)) == 1;
+      need_uf = !__shfl_sync(0xffffffffu, ok, 0);
+      __syncwarp();
+    }
+    if (lane == 0 && need_uf) atomicAdd(A.ctl + C_MAXLEV, 1);  // diagnostics: scan invalidations
+  }
+  if (need_uf) {
+    if (lane == 0) {
+      atomicAdd(A.ctl + C_LEVELS, 1);  // diagnostics: union-find rebuilds
+      // every registration issued so far is in Q; wait until all are published
+      S = (uint32_t)atomicAdd((unsigned long long *)(A.job + 40), 0ull);
+      while (ld_acq64(A.job + 41) < S) __nanosleep(32);
+      const LabBox bx = grown_box(A, a);
+      const int64_t nbox = (int64_t)bx.bd * bx.bh * bx.bw;
+      tag = job_publish(A, kJobUF, f, a, S, pos,
+                        (unsigned long long)bx.z0 | ((unsigned long long)bx.y0 << 21) |
+                            ((unsigned long long)bx.x0 << 42),
+                        (unsigned long long)bx.bw | ((unsigned long long)bx.bh << 21) |
+                            ((unsigned long long)bx.bd << 42),
+                        nbox);
+      nch = job_chunks(nbox);
+      T = tag;
+    }
+    job_run(A, tag, nch);
+    if (lane == 0) {
+      A.job[42] = T;
+      A.job[43] = (unsigned long long)(uint32_t)a;
+      A.job[44] = S;
+    }
+  }
+  // 2. the contracted graph of x over Q
+  df_stamp(A, pos, 0);  // RCB_PROFILE: deferred positions reuse slot 0 for "Q-UF ready"
+  if (lane == 0) {
+    A.job[45] = (unsigned long long)(uint32_t)pos;
+    tag = job_publish(A, kJobQuery, f, a, S, pos, 0, T, 26 * (int64_t)S);
+    nch = job_chunks(26 * (int64_t)S);
+  }
+  job_run(A, tag, nch);
+  // seeds (the a-cells of x's box), one per lane: one ufq root for all?
+  tag = __shfl_sync(0xffffffffu, tag, 0);
+  T = __shfl_sync(0xffffffffu, T, 0);
+  S = __shfl_sync(0xffffffffu, S, 0);
+  long long rg = -1;
+  if (lane < 27 && lane != 13) {
     const Lat &lat = A.lat;
     View v{A, pos};
     int64_t z, y, x;
     lat.coord(f, z, y, x);
-    const uint32_t hi = ~tag;
-    int64_t root = -1;
-    r = 1;
-    for (int k = 0; k < 27; ++k) {
-      if (k == 13) continue;
-      const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;
-      const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
-      if ((lat.ndim == 2 && dz != 0) || !lat.inb(zz, yy, xx)) continue;
+    const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+    const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
+    if ((lat.ndim == 3 || dz == 0) && lat.inb(zz, yy, xx)) {
       const int64_t g = lat.flat(zz, yy, xx);
-      if (v.lab(g) != a) continue;
-      const int64_t rg = job_find(A.ufp, hi, (uint32_t)g);
-      if (root < 0) root = rg;
-      else if (rg != root) r = 2;
+      if (v.lab(g) == a) {
+        const uint32_t t = is_q(A, g, a, S) ? (uint32_t)g : job_find(A.ufp, ~T, (uint32_t)g);
+        rg = job_find(A.ufq, ~tag, t);
+      }
     }
   }
-  return __shfl_sync(0xffffffffu, r, 0);
+  long long r0 = rg;
+  for (int l = 0; l < 27; ++l) {  // first seed's root
+    const long long v0 = __shfl_sync(0xffffffffu, rg, l);
+    if (v0 >= 0) {
+      r0 = v0;
+      break;
+    }
+  }
+  const bool split = __any_sync(0xffffffffu, rg >= 0 && rg != r0);
+  return split ? 2 : 1;
+}
+
+// Register deferred candidate x (owner a) in Q (lane 0).
+__device__ __forceinline__ void q_register(const ParArgs &A, int64_t f, int32_t a) {
+  const uint32_t seq = (uint32_t)atomicAdd((unsigned long long *)(A.job + 40), 1ull);
+  A.qlist[seq] = (uint32_t)f;
+  atomicMin(A.qmark + f, ((unsigned long long)seq << 32) | (uint32_t)a);
+  __threadfence();
+  atomicAdd((unsigned long long *)(A.job + 41), 1ull);
+}
+
+__global__ void k_q_reset(ParArgs A) {
+  // clear last run's registrations, then the job state (one block)
+  const uint32_t n = (uint32_t)A.job[40];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) A.qmark[A.qlist[i]] = ~0ull;
+  __syncthreads();
+  if (threadIdx.x < 8) A.job[40 + threadIdx.x] = 0;
 }
 
 // Warp-level wait until every lane's site g (or -1) is settled for V_pos (no
@@ -2068,13 +2345,6 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
   __syncwarp();
 }
 
-__device__ __forceinline__ void df_stamp(const ParArgs &A, int32_t pos, int k) {
-  if (A.tdbg && (threadIdx.x & 31) == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    A.tdbg[4 * pos + k] = (long long)t;
-  }
-}
 
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -2238,10 +2508,14 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         }
         if (use_box) dbg += 100000000;
         if (r == 3) {
-          if (lane == 0) atomicAdd(ctl + C_DEFER, 1);
+          if (lane == 0) {
+            atomicAdd(ctl + C_DEFER, 1);
+            if (A.qjob) q_register(A, f, a);
+          }
+          __syncwarp();
           warp_wait_lowmark(A, pos);
           df_stamp(A, pos, 2);  // deferred: low-water mark reached
-          r = warp_job_owner(A, pos, f, a);
+          r = warp_job_owner(A, pos, f, a, S.fr[0]);
           df_stamp(A, pos, 3);  // deferred: job answered
           dbg += 1000000000 + 2;
         }
@@ -3128,6 +3402,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_df does not fit on an SM");
       df_blocks = per_sm * sms;
     }
+    k_q_reset<<<1, 1024, 0, s>>>(A);
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
@@ -3155,6 +3430,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     T.mark("df-setup");
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(df_blocks), dim3(32 * kDfWarps),
                                          args, dsm, s));
+    k_q_reset<<<1, 1024, 0, s>>>(A);  // clear this run's deferred registry
   }
   T.mark("decide");
   k_acc_flags<<<grid_for(N + 1, 256), 256, 0, s>>>(A.dec, A.nneg, X.slot);

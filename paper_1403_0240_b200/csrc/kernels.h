@@ -97,6 +97,11 @@ struct ParArgs {
   int box_cap;      // dataflow box-map BFS capacity in sites (-1: default, 0: off)
   unsigned long long *job, *ufp;  // dataflow assist jobs (accept_par.cu)
   unsigned long long *wp;         // dataflow site words (pend << 32 | w)
+  unsigned long long *ufq;        // dataflow assist jobs: contracted-graph union-find
+  unsigned long long *qmark;      // deferred-candidate registry: (seq << 32 | label) per site
+  uint32_t *qlist;                // registered sites by sequence
+  uint32_t *qscr;                 // assist-job scans: per-position neighbour masks
+  int qjob;                       // 0: no registry (one full union-find per deferred candidate)
   const int4 *rec;                // dataflow per-position records
 };
 
@@ -164,6 +169,12 @@ int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uin
                         const int32_t *pcomp, const double *raw, const Lat &lat, const Off *rows,
                         int nrows, const double *wt, int64_t n, double *out,
                         unsigned long long *pairs, cudaStream_t s, int64_t p0 = 0);
+bool sobolev_packable(int32_t n_labels, int nrows, int max_d2);
+int32_t sobolev_pack(const uint32_t *px, const int32_t *pown, const int32_t *pcomp,
+                     const double *raw, int64_t lo, int64_t hi, int4 *pk, cudaStream_t s);
+int32_t sobolev_packed(const uint32_t *site_off, const int4 *pk, const Lat &lat, const Off *rows,
+                       int nrows, const double *wt, int nwt, int64_t p0, int64_t p1, double *out,
+                       unsigned long long *pairs, cudaStream_t s);
 int32_t sobolev_coords(const int64_t *d_coords, int64_t n, int ndim, const Lat &lat,
                        const int64_t *d_owners, const int64_t *d_comps, const double *d_raw,
                        const Off *st, int nst, const double *wt, double *d_out,

@@ -135,6 +135,117 @@ int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const u
   return RCB_OK;
 }
 
+// ---- K6 on packed particle records (engine and sweep) ----------------------
+// One 16-byte record per particle {raw (fp64), site, owner | competitor << 16}
+// (labels < 2^16): a partner costs one vector load instead of four scalar
+// ones.  Coordinates and CSR indices are 32-bit (sites < 2^32), the stencil
+// rows and the weight table sit in shared memory, and each row's partners are
+// fetched kSobU records at a time before any is used.  The products and the
+// two sums are formed exactly as in k_sobolev, in the same canonical order,
+// so the results are bit-identical.
+static constexpr int kSobRows = 1024, kSobW = 256, kSobU = 4;
+
+__global__ void k_sob_pack(const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+                           const int32_t *__restrict__ pcomp, const double *__restrict__ raw,
+                           int64_t lo, int64_t hi, int4 *__restrict__ pk) {
+  const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
+  const unsigned long long u = (unsigned long long)__double_as_longlong(raw[i]);
+  pk[i] = make_int4((int)(uint32_t)u, (int)(uint32_t)(u >> 32), (int)px[i],
+                    (int)((uint32_t)pown[i] | ((uint32_t)pcomp[i] << 16)));
+}
+
+__global__ void __launch_bounds__(128) k_sobolev_pk(
+    const uint32_t *__restrict__ site_off, const int4 *__restrict__ pk, uint32_t nx, uint32_t ny,
+    uint32_t nz, const Off *__restrict__ rows, int nrows, const double *__restrict__ wt, int nwt,
+    int64_t p0, int64_t p1, double *__restrict__ out, unsigned long long *__restrict__ pairs) {
+  __shared__ int srow[kSobRows];  // dz:8 | dy:8 | h:8 | aux:8
+  __shared__ double sw[kSobW];
+  for (int k = threadIdx.x; k < nrows; k += blockDim.x) {
+    const Off r = rows[k];
+    srow[k] = ((int)(uint8_t)r.dz << 24) | ((int)(uint8_t)r.dy << 16) | ((int)(uint8_t)r.dx << 8) |
+              (int)r.aux;
+  }
+  for (int k = threadIdx.x; k < nwt; k += blockDim.x) sw[k] = wt[k];
+  __syncthreads();
+  const int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long np = 0;
+  if (p < p1) {
+    const int4 me = pk[p];
+    const uint32_t f = (uint32_t)me.z, own = (uint32_t)me.w & 0xffffu;
+    const uint32_t plane = nx * ny;
+    const uint32_t z = f / plane, rem = f - z * plane;
+    const uint32_t y = rem / nx, x = rem - y * nx;
+    double same = 0.0, opp = 0.0;
+    int cs = 0, co = 0;
+    for (int k = 0; k < nrows; ++k) {
+      const int r = srow[k];
+      const int zz = (int)z + (int)(int8_t)(r >> 24), yy = (int)y + (int)(int8_t)(r >> 16);
+      if ((unsigned)zz >= nz || (unsigned)yy >= ny) continue;
+      const int h = (r >> 8) & 0xff, aux = r & 0xff;
+      const uint32_t x0 = (int)x - h < 0 ? 0u : x - h;
+      const uint32_t x1 = x + h >= nx ? nx - 1 : x + h;
+      const uint32_t rb = ((uint32_t)zz * ny + (uint32_t)yy) * nx;
+      const uint32_t q0 = __ldg(&site_off[rb + x0]), q1 = __ldg(&site_off[rb + x1 + 1]);
+      np += q1 - q0;
+      const uint32_t centre = rb + x;
+      for (uint32_t q = q0; q < q1; q += kSobU) {
+        int4 v[kSobU];
+#pragma unroll
+        for (int u = 0; u < kSobU; ++u)
+          v[u] = q + u < q1 ? __ldg(&pk[q + u]) : make_int4(0, 0, (int)centre, -1);
+#pragma unroll
+        for (int u = 0; u < kSobU; ++u) {
+          if (q + u >= q1) break;
+          const int dx = (int)((uint32_t)v[u].z - centre);
+          const double rq = __longlong_as_double(((long long)(uint32_t)v[u].y << 32) |
+                                                 (long long)(uint32_t)v[u].x);
+          const double c = sw[aux + dx * dx] * rq;
+          const uint32_t oc = (uint32_t)v[u].w;
+          if ((oc & 0xffffu) == own) {
+            same += c;
+            ++cs;
+          }
+          if ((oc >> 16) == own) {
+            opp += c;
+            ++co;
+          }
+        }
+      }
+    }
+    const double a = cs > 0 ? same / (double)cs : 0.0;
+    const double b = co > 0 ? opp / (double)co : 0.0;
+    out[p] = a - b;
+  }
+  if (pairs) {
+    for (int sh = 16; sh; sh >>= 1) np += __shfl_down_sync(0xffffffffu, np, sh);
+    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
+  }
+}
+
+bool sobolev_packable(int32_t n_labels, int nrows, int max_d2) {
+  return n_labels <= 65536 && nrows <= kSobRows && max_d2 < kSobW;
+}
+
+int32_t sobolev_pack(const uint32_t *px, const int32_t *pown, const int32_t *pcomp,
+                     const double *raw, int64_t lo, int64_t hi, int4 *pk, cudaStream_t s) {
+  if (hi <= lo) return RCB_OK;
+  k_sob_pack<<<grid_for(hi - lo, 256), 256, 0, s>>>(px, pown, pcomp, raw, lo, hi, pk);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t sobolev_packed(const uint32_t *site_off, const int4 *pk, const Lat &lat, const Off *rows,
+                       int nrows, const double *wt, int nwt, int64_t p0, int64_t p1, double *out,
+                       unsigned long long *pairs, cudaStream_t s) {
+  if (p1 <= p0) return RCB_OK;
+  k_sobolev_pk<<<grid_for(p1 - p0, 128), 128, 0, s>>>(
+      site_off, pk, (uint32_t)lat.nx, (uint32_t)lat.ny, (uint32_t)lat.nz, rows, nrows, wt,
+      nwt < kSobW ? nwt : kSobW, p0, p1, out, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 // Rows of the stencil: (dz, dy) in lexicographic order with half-width
 // h = max{dx : dz^2 + dy^2 + dx^2 < (E/2)^2} in Off.dx and dz^2 + dy^2 in
 // Off.aux.  max_d2 receives the largest |o|^2 (weight-table length check).

@@ -11,6 +11,7 @@
 
 #include "dev.cuh"
 #include "kernels.h"
+#include <cstring>
 
 namespace rcb {
 
@@ -68,7 +69,9 @@ struct rcb_sweep {
   DBuf<uint32_t> site_off, px;
   DBuf<double> raw, out, wt;
   DBuf<Off> st;
-  int nst = 0;
+  int nst = 0, nwt = 0;
+  bool packed = false;
+  DBuf<int4> pk;  // K6 packed partner records
   DBuf<unsigned long long> pairs;
   DBuf<uint8_t> tmp;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -77,7 +80,7 @@ struct rcb_sweep {
       cudaSetDevice(device);
       L.release(s); pown.release(s); pcomp.release(s); site_off.release(s); px.release(s);
       raw.release(s); out.release(s); wt.release(s); st.release(s); pairs.release(s);
-      tmp.release(s);
+      tmp.release(s); pk.release(s);
       cudaStreamSynchronize(s);
       if (e0) cudaEventDestroy(e0);
       if (e1) cudaEventDestroy(e1);
@@ -144,6 +147,14 @@ int32_t rcb_sweep_create(int32_t ndim, const int64_t *dims, const float *spheres
   auto stv = sobolev_rows(ndim, scfg->length_scale, &maxd2);
   if (scfg->n_weights <= maxd2) return bail(fail(RCB_ERR_VALUE, "weight table too short"));
   w->nst = (int)stv.size();
+  w->nwt = scfg->n_weights;
+  {
+    const char *ks = getenv("RCB_K6");  // "scalar": the unpacked K6 (comparison runs)
+    // one stencil row (w = 1): the unpacked kernel reads less (no packing pass)
+    w->packed = sobolev_packable(2, w->nst, maxd2) && w->nst > 1 &&
+                !(ks && strcmp(ks, "scalar") == 0);
+  }
+  if (w->packed) TRYB(w->pk.reserve(n, s));
   TRYB(w->st.reserve(stv.size(), s));
   TRYB(w->wt.reserve(scfg->n_weights, s));
   cudaMemcpyAsync(w->st.p, stv.data(), sizeof(Off) * stv.size(), cudaMemcpyHostToDevice, s);
@@ -170,8 +181,14 @@ int32_t rcb_sweep_run(rcb_sweep *w, int64_t *pairs, float *ms) {
   cudaStream_t s = w->s;
   RCB_CUDA(cudaMemsetAsync(w->pairs.p, 0, sizeof(unsigned long long), s));
   RCB_CUDA(cudaEventRecord(w->e0, s));
-  RCB_TRY(sobolev_lattice(w->site_off.p, w->pown.p, w->px.p, w->pcomp.p, w->raw.p, w->lat, w->st.p,
-                          w->nst, w->wt.p, w->n, w->out.p, w->pairs.p, s));
+  if (w->packed) {  // the record packing is part of K6's cost: timed with it
+    RCB_TRY(sobolev_pack(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, 0, w->n, w->pk.p, s));
+    RCB_TRY(sobolev_packed(w->site_off.p, w->pk.p, w->lat, w->st.p, w->nst, w->wt.p, w->nwt, 0,
+                           w->n, w->out.p, w->pairs.p, s));
+  } else {
+    RCB_TRY(sobolev_lattice(w->site_off.p, w->pown.p, w->px.p, w->pcomp.p, w->raw.p, w->lat,
+                            w->st.p, w->nst, w->wt.p, w->n, w->out.p, w->pairs.p, s));
+  }
   RCB_CUDA(cudaEventRecord(w->e1, s));
   unsigned long long hp = 0;
   RCB_CUDA(cudaMemcpyAsync(&hp, w->pairs.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
