@@ -112,7 +112,8 @@ struct rcb_engine {
   DBuf<uint32_t> vis, queue;
   DBuf<uint32_t> site_off, px, order;
   DBuf<int32_t> pown, pcomp, dint;
-  DBuf<double> raw, smooth, rank;
+  DBuf<double> raw, smooth, rank, tot_run, tsq_run;
+  bool cur_par = false;
   DBuf<int4> pk;  // K6 packed partner records
   bool sob_packed = false;
   int nwt = 0;
@@ -158,6 +159,7 @@ struct rcb_engine {
   bool scored = false;
   int score_launches = 0;
   uint32_t *hoff = nullptr;  // pinned: site_off reads
+  unsigned long long *hwatch = nullptr;  // pinned: dataflow watchdog words (job[56..61])
 
   ~rcb_engine() {
     if (s) {
@@ -167,7 +169,8 @@ struct rcb_engine {
       Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
-      raw.release(s); smooth.release(s); rank.release(s); pk.release(s); acc.release(s); sc.release(s);
+      raw.release(s); smooth.release(s); rank.release(s); pk.release(s); tot_run.release(s);
+      tsq_run.release(s); acc.release(s); sc.release(s);
       newlab.release(s); wpos.release(s); pend.release(s); dround.release(s); lab_pend.release(s);
       nown.release(s); blocker.release(s); bfs_list.release(s); ctl.release(s); dint_acc.release(s); dec.release(s);
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
@@ -189,6 +192,7 @@ struct rcb_engine {
     }
     if (hsc) cudaFreeHost(hsc);
     if (hoff) cudaFreeHost(hoff);
+    if (hwatch) cudaFreeHost(hwatch);
   }
 
   int32_t prepare() {  // K1 pass 1 + scan on the current raster
@@ -324,8 +328,10 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   if (cudaMallocHost((void **)&e->hsc, sizeof(Scalars)) != cudaSuccess)
     return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
   memset(e->hsc, 0, sizeof(Scalars));
-  if (cudaMallocHost((void **)&e->hoff, 16 * sizeof(uint32_t)) != cudaSuccess)
+  if (cudaMallocHost((void **)&e->hoff, 16 * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMallocHost((void **)&e->hwatch, 8 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
+  memset(e->hwatch, 0, 8 * sizeof(unsigned long long));
   if (cudaMemsetAsync(e->sc.p, 0, sizeof(Scalars), s) != cudaSuccess ||
       cudaMemsetAsync(e->vis.p, 0, sizeof(uint32_t) * V, s) != cudaSuccess)
     return bail(fail(RCB_ERR_CUDA, "memset failed"));
@@ -524,7 +530,18 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
     RCB_TRY(rank_order(base, e->dint.p, e->ecfg.lam, n, e->px.p, e->pcomp.p, e->ocfg.seed,
                        e->rank.p, e->rsc, e->order.p, &d->nneg, s));
     cudaEventRecord(e->ev[4], s);
-    const bool par = e->mode == 1 && e->ocfg.full_fg && e->simple_topology && !e->force_sequential;
+    // dataflow kernel (K8 v3): packed BFS coordinates need sides < 2^16 in
+    // 2-D and < 2^11 (x, y), < 2^10 (z) in 3-D; site words hold 24-bit
+    // positions and 16-bit labels
+    const bool fits = lat.ndim == 2 ? (lat.nx < 65536 && lat.ny < 65536)
+                                    : (lat.nx < 2048 && lat.ny < 2048 && lat.nz < 1024);
+    const bool use_df = fits && e->accept_mode != 1 && n < 0xffffff && e->nl <= 65536;
+    // l2 mode runs in parallel for PC through the dataflow kernel (every label
+    // sequenced, the d_tot < 0 gate on running statistics); PS keeps K8 v1
+    const bool l2par = e->mode == 0 && e->ecfg.region_model == 0 && use_df;
+    const bool par = (e->mode == 1 || l2par) && e->ocfg.full_fg && e->simple_topology &&
+                     !e->force_sequential;
+    e->cur_par = par;
     const int64_t budget = (int64_t)ceil(e->ocfg.move_budget * (double)n);
     if (par) {
       RCB_TRY(e->dec.reserve(n, s));
@@ -577,17 +594,27 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.box_cap = bc ? atoi(bc) : -1;
         const char *qj = getenv("RCB_DF_QJOB");  // "0": a full union-find per deferred candidate
         P.qjob = !(qj && qj[0] == '0');
+        const char *ws = getenv("RCB_DF_WATCH_S");  // watchdog seconds (default 60)
+        P.watch_ns = (unsigned long long)((ws ? atof(ws) : 60.0) * 1e9);
       }
       if (e->profile) {
         RCB_TRY(e->tdbg.reserve(4 * n, s));
         P.tdbg = e->tdbg.p;
       }
-      // dataflow kernel (K8 v3): packed BFS coordinates need sides < 2^16 in
-      // 2-D and < 2^11 (x, y), < 2^10 (z) in 3-D; site words hold 24-bit
-      // positions and 16-bit labels
-      const bool fits = lat.ndim == 2 ? (lat.nx < 65536 && lat.ny < 65536)
-                                      : (lat.nx < 2048 && lat.ny < 2048 && lat.nz < 1024);
-      const bool use_df = fits && e->accept_mode != 1 && n < 0xffffff && e->nl <= 65536;
+      P.l2 = e->mode == 0;
+      P.poisson = poisson;
+      P.lam = e->ecfg.lam;
+      P.I = e->I.p;
+      if (P.l2) {
+        RCB_TRY(e->tot_run.reserve(e->nl, s));
+        RCB_TRY(e->tsq_run.reserve(e->nl, s));
+        RCB_CUDA(cudaMemcpyAsync(e->tot_run.p, e->tot.p, sizeof(double) * e->nl,
+                                 cudaMemcpyDeviceToDevice, s));
+        RCB_CUDA(cudaMemcpyAsync(e->tsq_run.p, e->tsq.p, sizeof(double) * e->nl,
+                                 cudaMemcpyDeviceToDevice, s));
+        P.tot_run = e->tot_run.p;
+        P.tsq_run = e->tsq_run.p;
+      }
       if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufq.reserve(lat.V, s));
@@ -679,7 +706,11 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));
       cudaEventRecord(e->ev_acc[0], s);
+      if (use_df) RCB_CUDA(cudaMemsetAsync(e->job.p + 56, 0, 8 * sizeof(unsigned long long), s));
       RCB_TRY(accept_par(P, X, s, &nla));
+      if (use_df)
+        RCB_CUDA(cudaMemcpyAsync(e->hwatch, e->job.p + 56, 6 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s));
       cudaEventRecord(e->ev_acc[1], s);
       RCB_CUDA(cudaMemcpyAsync(e->hctl, e->ctl.p, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, s));
       launches += nla;
@@ -732,9 +763,19 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
   cudaEventRecord(e->ev[5], s);
   RCB_CUDA(cudaMemcpyAsync(e->hsc, d, offsetof(Scalars, limbs), cudaMemcpyDeviceToHost, s));
   RCB_CUDA(cudaStreamSynchronize(s));
+  if (e->hwatch[0]) {  // the dataflow acceptance's watchdog fired (accept_par.cu)
+    const unsigned long long w0 = e->hwatch[0];
+    char msg[256];
+    snprintf(msg, sizeof msg,
+             "dataflow acceptance watchdog: wait kind %llu at position %llu (aux %lld), "
+             "low-water %llu, fetched %llu; iteration %lld results discarded",
+             w0, e->hwatch[2], (long long)e->hwatch[3], e->hwatch[4], e->hwatch[5],
+             (long long)e->iteration);
+    memset(e->hwatch, 0, 8 * sizeof(unsigned long long));
+    return fail(RCB_ERR_CUDA, msg);
+  }
   e->n_scored = n;
-  e->last_par = n > 0 && e->mode == 1 && e->ocfg.full_fg && e->simple_topology &&
-                !e->force_sequential;
+  e->last_par = n > 0 && e->cur_par;
   {
     float acc_ms = 0.f;
     if (e->last_par) cudaEventElapsedTime(&acc_ms, e->ev_acc[0], e->ev_acc[1]);

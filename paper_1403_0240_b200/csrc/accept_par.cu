@@ -1137,6 +1137,38 @@ __device__ __forceinline__ void df_stamp(const ParArgs &A, int32_t pos, int k) {
   }
 }
 
+// Watchdog of the dataflow waits: a wait that lasts longer than A.watch_ns
+// (the whole acceptance normally takes milliseconds to seconds) records what
+// it waited for in job[56..61] and raises job[56]; every wait loop then
+// gives up, the kernel ends and the host reports the diagnostics instead of
+// hanging the GPU.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool df_aborted(const ParArgs &A) {
+  return *(volatile unsigned long long *)(A.job + 56) != 0;
+}
+// lane-0 check; returns true (on every lane) when the kernel must give up
+__device__ __forceinline__ bool df_watch(const ParArgs &A, unsigned long long t0, int32_t pos,
+                                         int what, long long aux) {
+  int stop = 0;
+  if ((threadIdx.x & 31) == 0) {
+    stop = df_aborted(A);
+    if (!stop && gtimer() - t0 > A.watch_ns) {
+      if (atomicCAS(A.job + 56, 0ull, (unsigned long long)what) == 0ull) {
+        A.job[58] = (unsigned long long)(uint32_t)pos;
+        A.job[59] = (unsigned long long)aux;
+        A.job[60] = (unsigned long long)(uint32_t)ld_rlx(A.ctl + 13);
+        A.job[61] = (unsigned long long)(uint32_t)ld_rlx(A.ctl + 12);
+      }
+      stop = 1;
+    }
+  }
+  return __shfl_sync(0xffffffffu, stop, 0) != 0;
+}
+
 // Deferred-candidate registry (Q) and job types.  A candidate whose BFS
 // overflows registers its site in Q before waiting for the low-water mark:
 //   qmark[y] = (registration sequence << 32) | owner label (min over the
@@ -1325,7 +1357,15 @@ __device__ void job_run(const ParArgs &A, uint32_t tag, unsigned long long nch) 
   }
   if (lane == 0) {
     const unsigned long long *done = job_desc(A, tag) + 3;
-    while (ld_acq64(done) < nch) __nanosleep(64);
+    const unsigned long long t0 = gtimer();
+    while (ld_acq64(done) < nch) {
+      __nanosleep(64);
+      if (df_aborted(A)) break;
+      if (gtimer() - t0 > A.watch_ns) {
+        if (atomicCAS(A.job + 56, 0ull, 5ull) == 0ull) A.job[59] = tag;
+        break;
+      }
+    }
     __threadfence();
   }
   __syncwarp();
@@ -1394,7 +1434,7 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
         }
         if (cells & ~reach) {
           const unsigned long long w = atomicAdd(A.job + 47, 1ull);
-          if (w < 16) A.job[48 + w] = (unsigned long long)(uint32_t)p;
+          if (w < 8) A.job[48 + w] = (unsigned long long)(uint32_t)p;
           else atomicExch(A.job + 46, 1ull);
         }
       }
@@ -1451,7 +1491,7 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
       atomicAdd(A.ctl + C_LEVELS, 1);  // diagnostics: union-find rebuilds
       // every registration issued so far is in Q; wait until all are published
       S = (uint32_t)atomicAdd((unsigned long long *)(A.job + 40), 0ull);
-      while (ld_acq64(A.job + 41) < S) __nanosleep(32);
+      while (ld_acq64(A.job + 41) < S && !df_aborted(A)) __nanosleep(32);
       const LabBox bx = grown_box(A, a);
       const int64_t nbox = (int64_t)bx.bd * bx.bh * bx.bw;
       tag = job_publish(A, kJobUF, f, a, S, pos,
@@ -1534,6 +1574,7 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
                                                                 int32_t pos) {
   int ns = 32;
   unsigned long long v = 0;
+  const unsigned long long t0 = gtimer();
   for (;;) {
     if (g >= 0) v = ld_rlx64(A.wp + g);
     const bool p = g >= 0 && wp_pend(v) < pos;
@@ -1541,6 +1582,9 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
     if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 512) ns <<= 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, p);
+      const long long gs = __shfl_sync(0xffffffffu, g, bal ? __ffs(bal) - 1 : 0);
+      if (df_watch(A, t0, pos, 1, gs)) break;
     }
   }
   return v;
@@ -2124,6 +2168,7 @@ __device__ __forceinline__ int first_zero_byte(uint32_t w) {
 __device__ __forceinline__ void warp_wait_lowmark(const ParArgs &A, int32_t pos) {
   const int lane = threadIdx.x & 31;
   int ns = 64;
+  const unsigned long long t0 = gtimer();
   int32_t m = __shfl_sync(0xffffffffu, lane == 0 ? ld_acq(A.ctl + 13) : 0, 0);
   for (;;) {
     while (m < pos) {
@@ -2161,6 +2206,7 @@ __device__ __forceinline__ void warp_wait_lowmark(const ParArgs &A, int32_t pos)
     if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 1024) ns <<= 1;
+      if (df_watch(A, t0, pos, 2, m)) break;
     }
     const int32_t h = __shfl_sync(0xffffffffu, lane == 0 ? ld_acq(A.ctl + 13) : 0, 0);
     if (h > m) m = h;
@@ -2274,7 +2320,7 @@ __global__ void k_df_records(ParArgs A, int4 *__restrict__ rec) {
 __global__ void k_df_small(ParArgs A) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride)
-    A.small[l] = (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
+    A.small[l] = A.l2 || (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
 }
 
 // events (label, position) of candidates involving small labels, emitted in
@@ -2323,7 +2369,7 @@ __device__ void warp_idle_help(const ParArgs &A) {
   for (;;) {
     if (warp_help(A)) continue;
     const int idle = __shfl_sync(0xffffffffu, lane == 0 ? ld_rlx(A.ctl + 11) : 0, 0);
-    if (idle >= nwarps) return;
+    if (idle >= nwarps || df_aborted(A)) return;
     __nanosleep(2000);
   }
 }
@@ -2332,6 +2378,7 @@ __device__ void warp_idle_help(const ParArgs &A) {
 __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int32_t pos) {
   const int lane = threadIdx.x & 31;
   int ns = 32;
+  const unsigned long long t0 = gtimer();
   for (;;) {
     int ok = 0;
     if (lane == 0) ok = A.lab_pos[ld_rlx(A.lab_ptr + l)] == pos;
@@ -2339,6 +2386,7 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
     if (!warp_help(A)) {
       __nanosleep(ns);
       if (ns < 512) ns <<= 1;
+      if (df_watch(A, t0, pos, 3, l)) break;
     }
   }
   fence_acq();
@@ -2357,6 +2405,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   // positions come from an atomic counter one at a time: a position held
   // ahead by a warp stuck in a long BFS would stall its dependants
   for (;;) {
+    if (__shfl_sync(0xffffffffu, lane == 0 ? (int)df_aborted(A) : 0, 0)) break;  // watchdog
     const int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
     if (pos >= M) {
       // stay as a helper for assist jobs until every position is decided,
@@ -2370,8 +2419,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     const int32_t f = rc.x, next = rc.w;
     const int32_t a = rc.y & 0x7fffffff, b = rc.z & 0x7fffffff;
     const bool sa = rc.y < 0, sb = rc.z < 0;
-    if (sa) warp_wait_label(A, a, pos);
-    if (sb) warp_wait_label(A, b, pos);
+    // l2 mode sequences every label, but waits for its predecessors only after
+    // the topology tests (those need settled footprints, not the statistics)
+    if (sa && !A.l2) warp_wait_label(A, a, pos);
+    if (sb && !A.l2) warp_wait_label(A, b, pos);
     const bool is3 = lat.ndim == 3;
     const int nxy = nx * ny;
     const int z = is3 ? f / nxy : 0, frem = f - z * nxy;
@@ -2403,8 +2454,9 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         if (is_face(k) && lab[k] == b) adj = true;
       if (!adj) d = REJ;
     }
+    const uint8_t d_base = d;  // stale / adjacency verdict (l2: vanish override below)
     if (d == ACC && a > 0) {
-      if (sa && __ldcg((const long long *)A.cnt + a) == 1) {
+      if (sa && !A.l2 && __ldcg((const long long *)A.cnt + a) == 1) {
         if (!A.vanish_ok) d = REJ;
       } else {
         const int k = box_local_count(lab, a);
@@ -2502,6 +2554,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
                         : warp_bfs<false, false>(A, S, pos, f, a, seeds, sgrp, ngrp, bb);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
           if (r != 0) break;
+          if (__shfl_sync(0xffffffffu, lane == 0 ? (int)df_aborted(A) : 0, 0)) {
+            r = 2;  // watchdog: the host discards this run
+            break;
+          }
           if (lane == 0) atomicAdd(ctl + C_BLOCKED, 1);
           warp_wait_settled(A, lane == 0 ? S.bsite : -1, pos);
           dbg += 1;
@@ -2523,7 +2579,35 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         dbg += 10 * (r + 1) + 10000 * (S.levels < 99 ? S.levels : 99);  // +1e6 w63, +1e7 w31, +1e8 box, +1e9 job
       }
     }
-    if (d == ACC && b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b)) d = REJ;
+    const bool fus_bad = b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b);
+    if (d == ACC && fus_bad) d = REJ;
+    if (A.l2) {
+      // l2 mode (optimizer.py:190-191, PC): admissible and d_tot < 0 with the
+      // statistics after every earlier accepted move of labels a and b
+      if (sa) warp_wait_label(A, a, pos);
+      if (sb) warp_wait_label(A, b, pos);
+      if (a > 0 && __ldcg((const long long *)A.cnt + a) == 1)
+        d = (d_base == ACC && A.vanish_ok && !fus_bad) ? ACC : REJ;
+      if (d == ACC) {
+        const double v = __ldg(A.I + f);
+        const long long ca = __ldcg((const long long *)A.cnt + a);
+        const long long cb = __ldcg((const long long *)A.cnt + b);
+        const double ta = __ldcg(A.tot_run + a), qa = __ldcg(A.tsq_run + a);
+        const double tb = __ldcg(A.tot_run + b), qb = __ldcg(A.tsq_run + b);
+        int di = 0;
+        for (int k = 0; k < 27; ++k)
+          if (is_face(k) && lab[k] >= 0) di += (int)(lab[k] != b) - (int)(lab[k] != a);
+        const double dt = delta_pc(v, ca, ta, qa, cb, tb, qb, A.poisson) + A.lam * (double)di;
+        if (!(dt < 0.0)) {
+          d = REJ;
+        } else if (lane == 0) {  // StatsTable.move (grid.py:171-181) on the running copy
+          __stcg(A.tot_run + a, ta - v);
+          __stcg(A.tsq_run + a, qa - v * v);
+          __stcg(A.tot_run + b, tb + v);
+          __stcg(A.tsq_run + b, qb + v * v);
+        }
+      }
+    }
     if (lane == 0) {
       A.blocker[pos] = dbg;
       if (d == ACC) {

@@ -102,6 +102,11 @@ struct ParArgs {
   uint32_t *qlist;                // registered sites by sequence
   uint32_t *qscr;                 // assist-job scans: per-position neighbour masks
   int qjob;                       // 0: no registry (one full union-find per deferred candidate)
+  unsigned long long watch_ns;    // dataflow watchdog: longest single wait
+  int l2, poisson;                // l2 mode (PC): every label sequenced, d_tot < 0 gate
+  double lam;
+  const double *I;
+  double *tot_run, *tsq_run;      // l2 mode: running region sums in acceptance order
   const int4 *rec;                // dataflow per-position records
 };
 

@@ -428,3 +428,30 @@ def test_deferred_registry_equals_full_union_find(P, monkeypatch, cap, box, iter
         assert a[0] == b[0] and a[1] == b[1], it
         assert np.array_equal(a[2], b[2]), it
     assert np.array_equal(runs[0][-1], runs[1][-1])
+
+
+@pytest.mark.parametrize("which,iters", [("cfg1", 8), ("cfg3_small", 5), ("cfg5_0", 6)])
+def test_l2_dataflow_equals_sequential(P, monkeypatch, which, iters):
+    """l2 mode (PC): the dataflow kernel with every label sequenced and the
+    d_tot < 0 gate on running statistics against K8 v1 (one thread, the
+    literal sequential greedy): moves in order, labels and ledger identical."""
+    import scenes
+    sc = {"cfg1": scenes.cfg1, "cfg3_small": lambda: scenes.cfg3(n=48),
+          "cfg5_0": lambda: scenes.cfg5_image(0)}[which]()
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("l2")
+    runs = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("RCB_FORCE_SEQUENTIAL", force)
+        eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
+        out = []
+        for _ in range(iters):
+            rec = eng.iterate()
+            out.append((rec.moves, rec.energy, eng.last_accepted.copy(), eng.counters()["parallel"]))
+        out.append(eng.labels)
+        runs.append(out)
+    assert all(r[3] == 1 for r in runs[0][:-1]) and all(r[3] == 0 for r in runs[1][:-1])
+    for it, (a, b) in enumerate(zip(runs[0][:-1], runs[1][:-1])):
+        assert a[0] == b[0] and a[1] == b[1], (which, it, a[0], b[0])
+        assert np.array_equal(a[2], b[2]), (which, it)
+    assert np.array_equal(runs[0][-1], runs[1][-1])
