@@ -109,6 +109,78 @@ def ball_band_sites(labels, xs, radius):
     return int(ndimage.binary_dilation(mask, structure=fp).sum())
 
 
+def band_sites_device(labels_shape, xs, radius, device):
+    """B_R on the device (bookkeeping for the large-config roofline): sites
+    within Euclidean distance R of a particle, by a ball convolution."""
+    import torch
+    n = int(np.prod(labels_shape))
+    m = torch.zeros(n, dtype=torch.float16, device=device)
+    m[torch.as_tensor(xs, device=device)] = 1
+    m = m.view(1, 1, *labels_shape)
+    r = radius
+    g = torch.arange(-r, r + 1, device=device)
+    if len(labels_shape) == 3:
+        zz, yy, xx = torch.meshgrid(g, g, g, indexing="ij")
+        ball = ((zz * zz + yy * yy + xx * xx) <= r * r).to(torch.float16)[None, None]
+        out = torch.nn.functional.conv3d(m, ball, padding=r)
+    else:
+        yy, xx = torch.meshgrid(g, g, indexing="ij")
+        ball = ((yy * yy + xx * xx) <= r * r).to(torch.float16)[None, None]
+        out = torch.nn.functional.conv2d(m, ball, padding=r)
+    return int((out > 0.5).sum().item())
+
+
+def large_config(P, local, peak):
+    """BASELINE configs[3] (cfg4: 512^3 PS/Poisson, R = 4, Sobolev w = 3) on
+    this GPU: the energy (K5) + Sobolev (K6) kernels at N ~ 10^7 particles,
+    where their HBM roofline is the meaningful bound.  Iterations 4-5 from the
+    bubbles init, CUDA-event phase times on the engine stream; bytes per
+    SURVEY §8(d) (29N + 24B_R for K5, 28N for K6)."""
+    import torch
+    import scenes
+    sc = scenes.cfg4()
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
+    eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg,
+                              device=local)
+    for _ in range(3):
+        eng.iterate()
+    k5 = k6 = it_ms = 0.0
+    b5 = b6 = 0.0
+    n_tot = pairs = 0
+    steps = 2
+    for _ in range(steps):
+        eng.iterate()
+        t, _ = eng.timings()
+        k5 += t[1]
+        k6 += t[2]
+        it_ms += t[5]
+        xs = eng.last_candidates[0]
+        n = len(xs)
+        n_tot += n
+        pairs += eng.last_pairs
+        # the band of this iteration's particles on its start raster: the
+        # particle sites are that raster's contour, so the ball band is the
+        # same set whichever raster the labels come from
+        B = band_sites_device(sc.image.shape, xs, sc.smooth_radius, f"cuda:{local}")
+        b5 += 29 * n + 24 * B
+        b6 += 28 * n
+    del eng
+    torch.cuda.empty_cache()
+    a5 = b5 / (k5 / 1e3) / 1e9
+    a6 = b6 / (k6 / 1e3) / 1e9
+    a56 = (b5 + b6) / ((k5 + k6) / 1e3) / 1e9
+    return {"workload": "cfg4: 3-D 512^3 PS/Poisson R=4, Sobolev w=3 (E=6), bubbles 8x8x8 "
+                        "r=15, iterations 4-5", "particles_per_iteration": n_tot / steps,
+            "iteration_ms": it_ms / steps, "k5_ms": k5 / steps, "k6_ms": k6 / steps,
+            "particle_interactions_per_s": pairs / (k6 / 1e3),
+            "roofline_k5_k6": {"bound": "hbm", "achieved": a56, "peak": peak, "unit": "GB/s",
+                               "frac": a56 / peak, "k5_GBs": a5, "k6_GBs": a6,
+                               "algorithmic_bytes_per_iteration": (b5 + b6) / steps,
+                               "note": "K5 is fp64-log/issue bound (ncu: FP64 pipe ~50 %, "
+                                       "issue ~78 %), K6 issue bound at w=3"}}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -326,6 +398,8 @@ def run_ours(args):
                                 "dominant": {"phase": "accept (K8 v3 + exact ledger/stats)",
                                              "share": float(shares[4]),
                                              "bound": "latency / FP64 issue, DRAM < 1 % (ncu)"}}
+        if args.large:
+            line["large_config"] = large_config(P, local, peak)
         if args.cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
@@ -407,6 +481,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-fp32", dest="fp32", action="store_false")
     ap.add_argument("--no-full-run", dest="full_run", action="store_false")
+    ap.add_argument("--no-large", dest="large", action="store_false",
+                    help="skip the cfg4 (512^3) energy + Sobolev roofline block")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
