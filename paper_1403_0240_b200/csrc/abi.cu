@@ -535,7 +535,11 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
     // positions and 16-bit labels
     const bool fits = lat.ndim == 2 ? (lat.nx < 65536 && lat.ny < 65536)
                                     : (lat.nx < 2048 && lat.ny < 2048 && lat.nz < 1024);
-    const bool use_df = fits && e->accept_mode != 1 && n < 0xffffff && e->nl <= 65536;
+    // site words: 24-bit positions with 16-bit labels, or 27-bit positions with
+    // 10-bit labels (more than 2^24 - 1 candidates, at most 1024 labels)
+    const bool df24 = n < 0xffffff && e->nl <= 65536;
+    const bool df27 = n < 0x7ffffff && e->nl <= 1024;
+    const bool use_df = fits && e->accept_mode != 1 && (df24 || df27);
     // l2 mode runs in parallel for PC through the dataflow kernel (every label
     // sequenced, the d_tot < 0 gate on running statistics); PS keeps K8 v1
     const bool l2par = e->mode == 0 && e->ecfg.region_model == 0 && use_df;
@@ -602,6 +606,10 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.tdbg = e->tdbg.p;
       }
       P.l2 = e->mode == 0;
+      {
+        const char *w27 = getenv("RCB_DF_WP27");  // tests: the wide layout on small inputs
+        P.wp_bits = (df24 && !(w27 && w27[0] == '1' && df27)) ? 24 : 27;
+      }
       P.poisson = poisson;
       P.lam = e->ecfg.lam;
       P.I = e->I.p;

@@ -1025,14 +1025,22 @@ __device__ __forceinline__ unsigned long long ld_rlx64(const unsigned long long 
 // pend >= pos has y settled for V_pos, with V_pos(y) = w < pos ? newlab : L[y]
 // and no further memory access.  The host keeps this kernel to particle
 // counts < 2^24 - 1 and labels < 2^16.
-static constexpr uint32_t kWpInf = 0xffffffu;
-__device__ __forceinline__ int32_t wp_pend(unsigned long long v) { return (int32_t)(v & kWpInf); }
-__device__ __forceinline__ int32_t wp_w(unsigned long long v) { return (int32_t)((v >> 24) & kWpInf); }
-__device__ __forceinline__ int32_t wp_lab(unsigned long long v) { return (int32_t)(v >> 48); }
+// Two layouts, chosen per run by the host (ParArgs.wp_bits): 24-bit positions
+// with 16-bit labels, or 27-bit positions with 10-bit labels (more than 2^24
+// candidates, at most 1024 labels: cfg4's late iterations).
+__constant__ uint32_t c_wp_bits;
+__device__ __forceinline__ uint32_t wp_inf() { return (1u << c_wp_bits) - 1u; }
+__device__ __forceinline__ int32_t wp_pend(unsigned long long v) { return (int32_t)(v & wp_inf()); }
+__device__ __forceinline__ int32_t wp_w(unsigned long long v) {
+  return (int32_t)((v >> c_wp_bits) & wp_inf());
+}
+__device__ __forceinline__ int32_t wp_lab(unsigned long long v) { return (int32_t)(v >> (2 * c_wp_bits)); }
 __device__ __forceinline__ unsigned long long wp_pack(int32_t pend, int32_t w, int32_t lab) {
-  const uint32_t p = pend < (int32_t)kWpInf ? (uint32_t)pend : kWpInf;
-  const uint32_t q = w < (int32_t)kWpInf ? (uint32_t)w : kWpInf;
-  return ((unsigned long long)(uint32_t)lab << 48) | ((unsigned long long)q << 24) | p;
+  const uint32_t inf = wp_inf();
+  const uint32_t p = pend < (int32_t)inf ? (uint32_t)pend : inf;
+  const uint32_t q = w < (int32_t)inf ? (uint32_t)w : inf;
+  return ((unsigned long long)(uint32_t)lab << (2 * c_wp_bits)) |
+         ((unsigned long long)q << c_wp_bits) | p;
 }
 __device__ __forceinline__ int32_t df_lab(unsigned long long v, int32_t l0, int32_t pos) {
   return wp_w(v) < pos ? wp_lab(v) : l0;
@@ -2237,7 +2245,7 @@ __global__ void k_df_init2(ParArgs A) {
     const uint32_t p = A.order[pos];
     A.pos_of[p] = (int32_t)pos;
     A.dec[pos] = UNDEC;
-    atomicMin(A.wp + A.px[p], ~(unsigned long long)kWpInf | (unsigned)pos);  // pend field
+    atomicMin(A.wp + A.px[p], ~(unsigned long long)wp_inf() | (unsigned)pos);  // pend field
     const int32_t a = A.pown[p];
     if (a > 0) atomicAdd(A.nown + a, 1);
   }
@@ -3487,6 +3495,10 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       df_blocks = per_sm * sms;
     }
     k_q_reset<<<1, 1024, 0, s>>>(A);
+    {
+      const uint32_t bits = (uint32_t)A.wp_bits;
+      RCB_CUDA(cudaMemcpyToSymbolAsync(c_wp_bits, &bits, sizeof(bits), 0, cudaMemcpyHostToDevice, s));
+    }
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);

@@ -107,6 +107,7 @@ struct ParArgs {
   double lam;
   const double *I;
   double *tot_run, *tsq_run;      // l2 mode: running region sums in acceptance order
+  int wp_bits;                    // dataflow site-word layout: 24 (16-bit labels) or 27 (10-bit)
   const int4 *rec;                // dataflow per-position records
 };
 

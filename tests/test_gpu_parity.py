@@ -455,3 +455,22 @@ def test_l2_dataflow_equals_sequential(P, monkeypatch, which, iters):
         assert a[0] == b[0] and a[1] == b[1], (which, it, a[0], b[0])
         assert np.array_equal(a[2], b[2]), (which, it)
     assert np.array_equal(runs[0][-1], runs[1][-1])
+
+
+@pytest.mark.parametrize("which", ["cfg1", "cfg4_small"])
+def test_dataflow_wide_site_words(P, monkeypatch, which):
+    """The 27-bit-position / 10-bit-label site-word layout (used above 2^24
+    candidates) decides exactly like the default layout."""
+    import scenes
+    sc = scenes.cfg1() if which == "cfg1" else scenes.cfg4(n=64, n_obj=8, per_axis=2)
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
+    runs = []
+    for wide in ("0", "1"):
+        monkeypatch.setenv("RCB_DF_WP27", wide)
+        eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
+        out = [(r.moves, r.energy, eng.last_accepted.copy()) for r in (eng.iterate() for _ in range(6))]
+        runs.append((out, eng.labels))
+    for (a, b) in zip(runs[0][0], runs[1][0]):
+        assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2])
+    assert np.array_equal(runs[0][1], runs[1][1])
