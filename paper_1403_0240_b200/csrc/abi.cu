@@ -128,7 +128,7 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
-  DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark;
+  DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark, qstate;
   DBuf<uint32_t> qlist, qscr;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
@@ -179,7 +179,7 @@ struct rcb_engine {
       labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
-      ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s);
+      ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -626,6 +626,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufq.reserve(lat.V, s));
+          RCB_TRY(e->qstate.reserve(2 * (size_t)e->nl, s));
+          RCB_CUDA(cudaMemsetAsync(e->qstate.p, 0, sizeof(unsigned long long) * 2 * e->nl, s));
           RCB_TRY(e->qmark.reserve(lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->ufq.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->qmark.p, 0xff, sizeof(unsigned long long) * lat.V, s));
@@ -643,6 +645,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.qmark = e->qmark.p;
         P.qlist = e->qlist.p;
         P.qscr = e->qscr.p;
+        P.qstate = e->qstate.p;
         P.ufp = e->ufp.p;
         P.job = e->job.p;
         P.wp = e->wpk.p;

@@ -1199,8 +1199,10 @@ __device__ __forceinline__ bool df_watch(const ParArgs &A, unsigned long long t0
 // removal (or a candidate registered after it) forces a new one.
 // Job state (lane 0 of the owner only; jobs are serialised):
 //   job[40] registrations issued, job[41] registrations published,
-//   job[42] Q-UF tag T (0: none), job[43] its label, job[44] its S,
-//   job[45] position its view has reached, job[46] invalid flag (scan).
+//   job[46] invalid flag (scan), job[47..55] window-test list;
+//   per label a (labels' sites are disjoint, so their Q-UFs coexist in ufp):
+//   qstate[2a] = T | S << 32 (Q-UF tag, 0: none; registrations it excludes),
+//   qstate[2a + 1] = position its view has reached.
 static constexpr int kJobUF = 0, kJobScan = 1, kJobQuery = 2;
 
 __device__ __forceinline__ bool is_q(const ParArgs &A, int64_t y, int32_t a, uint32_t S) {
@@ -1298,8 +1300,15 @@ __device__ bool warp_help(const ParArgs &A) {
       if (!lat.inb(z2, y2, x2)) continue;
       const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
       if (bp == a) {
-        if (v.lab(y) == a && v.lab(g) == a && !is_q(A, g, a, S))
-          job_union(A.ufp, hiT, (uint32_t)y, (uint32_t)g);
+        if (v.lab(y) != a) continue;
+        const uint32_t ty = ~(uint32_t)(__ldcg(A.ufp + y) >> 32);  // tag of y's entry
+        if (ty != ~hiT && ty > ~hiT && ty != 0u) {
+          // written by a newer union-find (of y's former label): an older one
+          // cannot absorb it (hooks are atomicMin on tagged words) -> rebuild
+          atomicExch(A.job + 46, 1ull);
+          continue;
+        }
+        if (v.lab(g) == a && !is_q(A, g, a, S)) job_union(A.ufp, hiT, (uint32_t)y, (uint32_t)g);
       } else {
         const View vp{A, p};
         if (vp.lab(g) == a && !is_q(A, g, a, S)) atomicOr(A.qscr + (p - lo), 1u << kk);
@@ -1393,17 +1402,23 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
   uint32_t tag = 0, T = 0, S = 0;
   unsigned long long nch = 0;
   if (lane == 0) {
-    T = (uint32_t)A.job[42];
-    S = (uint32_t)A.job[44];
+    T = (uint32_t)A.qstate[2 * a];
+    S = (uint32_t)(A.qstate[2 * a] >> 32);
     const uint32_t seqx = (uint32_t)(__ldcg(A.qmark + f) >> 32);
-    need_uf = !(T != 0 && (int32_t)A.job[43] == a && seqx < S);
+    need_uf = !(T != 0 && seqx < S);
     if (!need_uf) {
-      const int32_t lo = (int32_t)A.job[45];
-      if (pos > lo) nch = 1;
+      // a scan costs 26 items per position since the Q-UF's view, a rebuild
+      // ~one item per site of a's grown box: rebuild when that is cheaper
+      // (labels whose last job was long ago)
+      const int32_t lo = (int32_t)A.qstate[2 * a + 1];
+      const LabBox bx = grown_box(A, a);
+      const int64_t nbox = (int64_t)bx.bd * bx.bh * bx.bw;
+      if (26 * (int64_t)(pos - lo) > 2 * nbox) need_uf = 1;
+      else if (pos > lo) nch = 1;
     }
   }
   if (!__shfl_sync(0xffffffffu, need_uf, 0) && __shfl_sync(0xffffffffu, nch, 0)) {
-    const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.job[45] : 0ull, 0);
+    const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.qstate[2 * a + 1] : 0ull, 0);
     for (int32_t q = lane; q < pos - lo; q += 32) A.qscr[q] = 0;
     __threadfence();
     __syncwarp();
@@ -1422,7 +1437,7 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
     // removals of UF members: box-simple in a \ Q (in their view) keeps every
     // component connected; the others are listed for the window test
     {
-      const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.job[45] : 0ull, 0);
+      const int32_t lo = (int32_t)__shfl_sync(0xffffffffu, lane == 0 ? A.qstate[2 * a + 1] : 0ull, 0);
       if (lane == 0) A.job[47] = 0;
       __threadfence();
       __syncwarp();
@@ -1513,15 +1528,13 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
     }
     job_run(A, tag, nch);
     if (lane == 0) {
-      A.job[42] = T;
-      A.job[43] = (unsigned long long)(uint32_t)a;
-      A.job[44] = S;
+      A.qstate[2 * a] = (unsigned long long)T | ((unsigned long long)S << 32);
     }
   }
   // 2. the contracted graph of x over Q
   df_stamp(A, pos, 0);  // RCB_PROFILE: deferred positions reuse slot 0 for "Q-UF ready"
   if (lane == 0) {
-    A.job[45] = (unsigned long long)(uint32_t)pos;
+    A.qstate[2 * a + 1] = (unsigned long long)(uint32_t)pos;
     tag = job_publish(A, kJobQuery, f, a, S, pos, 0, T, 26 * (int64_t)S);
     nch = job_chunks(26 * (int64_t)S);
   }
@@ -1570,7 +1583,12 @@ __device__ __forceinline__ void q_register(const ParArgs &A, int64_t f, int32_t 
 __global__ void k_q_reset(ParArgs A) {
   // clear last run's registrations, then the job state (one block)
   const uint32_t n = (uint32_t)A.job[40];
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) A.qmark[A.qlist[i]] = ~0ull;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t y = A.qlist[i];
+    const uint32_t l = (uint32_t)A.qmark[y];
+    if (l != 0xffffffffu) A.qstate[2 * l] = 0;
+    A.qmark[y] = ~0ull;
+  }
   __syncthreads();
   if (threadIdx.x < 8) A.job[40 + threadIdx.x] = 0;
 }

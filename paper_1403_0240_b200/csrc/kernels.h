@@ -101,6 +101,7 @@ struct ParArgs {
   unsigned long long *qmark;      // deferred-candidate registry: (seq << 32 | label) per site
   uint32_t *qlist;                // registered sites by sequence
   uint32_t *qscr;                 // assist-job scans: per-position neighbour masks
+  unsigned long long *qstate;     // per label: Q-UF tag | S << 32, position reached
   int qjob;                       // 0: no registry (one full union-find per deferred candidate)
   unsigned long long watch_ns;    // dataflow watchdog: longest single wait
   int l2, poisson;                // l2 mode (PC): every label sequenced, d_tot < 0 gate
