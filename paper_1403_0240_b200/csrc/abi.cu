@@ -129,7 +129,8 @@ struct rcb_engine {
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
   DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark, qstate;
-  DBuf<uint32_t> qlist, qscr;
+  DBuf<uint32_t> qlist, qscr, bigmap, bigfr2;
+  DBuf<uint8_t> bigfg2;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
@@ -180,6 +181,7 @@ struct rcb_engine {
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
+      bigmap.release(s); bigfr2.release(s); bigfg2.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -714,6 +716,14 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.band = e->band.p;
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
+      {
+        const char *bt = getenv("RCB_DF_BIGBOX");  // "0": no large box tier (comparison runs)
+        if (!(bt && bt[0] == '0')) {
+          X.bigmap = &e->bigmap;
+          X.bigfr2 = &e->bigfr2;
+          X.bigfg2 = &e->bigfg2;
+        }
+      }
       int nla = 0;
       RCB_CUDA(cudaMemsetAsync(e->ctl.p, 0, sizeof(int32_t) * 16, s));
       cudaEventRecord(e->ev_acc[0], s);

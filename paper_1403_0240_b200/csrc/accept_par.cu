@@ -1750,12 +1750,21 @@ __device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t
   return ins;
 }
 
-__device__ __forceinline__ void bfs_push(WarpBfs &S, int nxt, uint32_t packed, int g) {
+// Frontier storage of a warp BFS: the shared-memory arrays of WarpBfs, or the
+// warp's slot in global memory for the large box tier.
+struct Frontier {
+  uint32_t *fr[2];
+  uint8_t *fg[2];
+  int cap;
+};
+
+__device__ __forceinline__ void bfs_push(WarpBfs &S, const Frontier &F, int nxt, uint32_t packed,
+                                         int g) {
   atomicOr(&S.alive, 1u << g);
   const int q = atomicAdd(&S.nfr[nxt], 1);
-  if (q < kFW) {
-    S.fr[nxt][q] = packed;
-    S.fg[nxt][q] = (uint8_t)g;
+  if (q < F.cap) {
+    F.fr[nxt][q] = packed;
+    F.fg[nxt][q] = (uint8_t)g;
   } else {
     S.overflow = 1;
   }
@@ -1782,16 +1791,37 @@ __device__ __forceinline__ void unpack_c(uint32_t e, int &z, int &y, int &x) {
 
 // seeds: bit k of seedmask (3^3 layout, k != 13) is an a-cell of x's box;
 // sgrp[k] its group (box-local component, < 8)
-template <bool kBox, bool k3D>
+static constexpr int kBigLevels = 32;
+// kBig: the bounding-box map and the frontiers live in the warp's slot of
+// global memory (labels whose grown box exceeds the shared-memory map; run
+// after the hash tier overflowed, before deferring to an assist job).
+template <bool kBox, bool k3D, bool kBig = false>
 __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
                         uint32_t seedmask, const uint8_t *sgrp, int ngrp, const LabBox bb) {
   const int lane = threadIdx.x & 31;
+  Frontier F;
+  if (kBig) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    F.fr[0] = A.bigfr2 + (2 * wid) * A.big_fcap;
+    F.fr[1] = F.fr[0] + A.big_fcap;
+    F.fg[0] = A.bigfg2 + (2 * wid) * A.big_fcap;
+    F.fg[1] = F.fg[0] + A.big_fcap;
+    F.cap = A.big_fcap;
+  } else {
+    F.fr[0] = S.fr[0];
+    F.fr[1] = S.fr[1];
+    F.fg[0] = S.fg[0];
+    F.fg[1] = S.fg[1];
+    F.cap = kFW;
+  }
   const int nx = (int)A.lat.nx, ny = (int)A.lat.ny, nz = (int)A.lat.nz;
   const int nxy = nx * ny;
   const int fz = k3D ? (int)(f / nxy) : 0, frem = (int)(f - (int64_t)fz * nxy);
   const int fy = frem / nx, fx = frem - fy * nx;
   constexpr int kNb = k3D ? 26 : 8;
-  uint32_t *nib = reinterpret_cast<uint32_t *>(S.key);
+  uint32_t *nib = kBig ? A.bigmap + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) *
+                                         (int64_t)A.big_words
+                       : reinterpret_cast<uint32_t *>(S.key);
   auto box_index = [&](int zz, int yy, int xx, bool &ok) -> int {
     if (!kBox) return 0;
     const int rz = zz - bb.z0, ry = yy - bb.y0, rx = xx - bb.x0;
@@ -1802,7 +1832,13 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   };
   if (kBox) {
     const int nw = (bb.bd * bb.bh * bb.bw + 7) >> 3;
-    for (int k = lane; k < nw; k += 32) nib[k] = 0;
+    if (kBig) {
+      uint4 *n4 = reinterpret_cast<uint4 *>(nib);
+      for (int k = lane; k < (nw + 3) / 4; k += 32) n4[k] = make_uint4(0, 0, 0, 0);
+      __threadfence_block();
+    } else {
+      for (int k = lane; k < nw; k += 32) nib[k] = 0;
+    }
   } else {
     for (int k = lane; k < kHW; k += 32) S.key[k] = kEmpty;
   }
@@ -1843,8 +1879,8 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
         while (S.key[h] != kEmpty) h = (h + 1) & (kHW - 1);
         S.key[h] = ((unsigned long long)site << 8) | (unsigned)g;
       }
-      S.fr[0][nfr] = pack_c<k3D>(zz, yy, xx);
-      S.fg[0][nfr] = (uint8_t)g;
+      F.fr[0][nfr] = pack_c<k3D>(zz, yy, xx);
+      F.fg[0][nfr] = (uint8_t)g;
       ++nfr;
     }
     S.comp = C;
@@ -1867,8 +1903,8 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
         ok[u] = p < kNb * n;
         const int j = ok[u] ? p / kNb : 0, k = p - j * kNb;
         int ez, ey, ex;
-        unpack_c<k3D>(S.fr[cur][j], ez, ey, ex);
-        g[u] = S.fg[cur][j];
+        unpack_c<k3D>(F.fr[cur][j], ez, ey, ex);
+        g[u] = F.fg[cur][j];
         if (k3D) {
           const int kk = k + (k >= 13);  // skip the centre of the 3^3
           zq[u] = ez + kk / 9 - 1;
@@ -1886,7 +1922,8 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
         li[u] = box_index(zq[u], yq[u], xq[u], ok[u]);
         if (ok[u]) {
           if (kBox) {
-            const int cg = (int)((nib[li[u] >> 3] >> (4 * (li[u] & 7))) & 15u);
+            const uint32_t nw = kBig ? *(volatile uint32_t *)(nib + (li[u] >> 3)) : nib[li[u] >> 3];
+            const int cg = (int)((nw >> (4 * (li[u] & 7))) & 15u);
             if (cg) {
               if (cg != 15 && cg - 1 != g[u]) atomicOr(&S.unions[g[u]], 1u << (cg - 1));
               ok[u] = false;
@@ -1930,7 +1967,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
         }
         if (df_lab(pk[u], l0[u], pos) != a) continue;
         if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u]))
-          bfs_push(S, nxt, pack_c<k3D>(zq[u], yq[u], xq[u]), g[u]);
+          bfs_push(S, F, nxt, pack_c<k3D>(zq[u], yq[u], xq[u]), g[u]);
       }
     }
     __syncwarp();
@@ -1961,7 +1998,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
           const int lq = box_index(zq, yq, xq, okq);
           if (okq && df_lab(v, __ldg(A.L + tq), pos) == a &&
               bfs_visit<kBox>(A, S, nib, lq, (int)tq, gq))
-            bfs_push(S, nxt, pack_c<k3D>(zq, yq, xq), gq);
+            bfs_push(S, F, nxt, pack_c<k3D>(zq, yq, xq), gq);
         }
       }
       __syncwarp();
@@ -1979,6 +2016,9 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
     if (lane == 0) S.nfr[cur] = 0;
     __syncwarp();
     if (r >= 0) return r;
+    // the large tier is for footprints that resolve within a few dozen
+    // levels; a long flood (a big piece to exhaust) goes to the assist job
+    if (kBig && S.levels >= kBigLevels) return 3;
     cur = nxt;
   }
 }
@@ -2579,6 +2619,36 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
             r = use_box ? warp_bfs<true, false>(A, S, pos, f, a, seeds, sgrp, ngrp, bb)
                         : warp_bfs<false, false>(A, S, pos, f, a, seeds, sgrp, ngrp, bb);
           if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
+          // Adaptive: the tier pays off where overflowing footprints mostly
+          // resolve as one piece within a few dozen levels (cfg4: seeds of
+          // wide 3-D blobs); where they mostly fail (tubes to exhaust, cfg3)
+          // it is switched off for the rest of the run once failures are the
+          // majority (job[62] tries, job[63] failures).
+          const bool big_ok =
+              __shfl_sync(0xffffffffu, lane == 0 ? (int)(2 * __ldcg(A.job + 63) <=
+                                                         __ldcg(A.job + 62) + 8)
+                                                 : 0, 0) != 0;
+          if (r == 3 && !use_box && A.bigmap && big_ok &&
+              (int64_t)bb.bd * bb.bh * bb.bw <= 8 * (int64_t)A.big_words) {
+            // the hash overflowed: flood again with the label box's map and
+            // frontiers in this warp's global slot (concurrent, no job)
+            for (;;) {
+              r = is3 ? warp_bfs<true, true, true>(A, S, pos, f, a, seeds, sgrp, ngrp, bb)
+                      : warp_bfs<true, false, true>(A, S, pos, f, a, seeds, sgrp, ngrp, bb);
+              if (lane == 0) atomicAdd(ctl + C_BFSRUNS, 1);
+              if (r != 0) break;
+              if (__shfl_sync(0xffffffffu, lane == 0 ? (int)df_aborted(A) : 0, 0)) {
+                r = 2;
+                break;
+              }
+              warp_wait_settled(A, lane == 0 ? S.bsite : -1, pos);
+            }
+            if (lane == 0) {
+              atomicAdd(A.job + 62, 1ull);
+              if (r != 1) atomicAdd(A.job + 63, 1ull);
+            }
+            dbg += 100000000;
+          }
           if (r != 0) break;
           if (__shfl_sync(0xffffffffu, lane == 0 ? (int)df_aborted(A) : 0, 0)) {
             r = 2;  // watchdog: the host discards this run
@@ -3512,7 +3582,21 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_df does not fit on an SM");
       df_blocks = per_sm * sms;
     }
-    k_q_reset<<<1, 1024, 0, s>>>(A);
+    if (A.lat.ndim == 3 && X.bigmap) {
+      // large box tier: per warp a 4-bit map of up to 2M sites and two
+      // frontiers of 16K sites (~2.8 GB for 2 368 warps; 3-D only)
+      const size_t warps = (size_t)df_blocks * kDfWarps;
+      A.big_words = 1 << 18;
+      A.big_fcap = 1 << 14;
+      RCB_TRY(X.bigmap->reserve(warps * (size_t)A.big_words, s));
+      RCB_TRY(X.bigfr2->reserve(warps * 2 * (size_t)A.big_fcap, s));
+      RCB_TRY(X.bigfg2->reserve(warps * 2 * (size_t)A.big_fcap, s));
+      A.bigmap = X.bigmap->p;
+      A.bigfr2 = X.bigfr2->p;
+      A.bigfg2 = X.bigfg2->p;
+    } else {
+      A.bigmap = nullptr;
+    }
     {
       const uint32_t bits = (uint32_t)A.wp_bits;
       RCB_CUDA(cudaMemcpyToSymbolAsync(c_wp_bits, &bits, sizeof(bits), 0, cudaMemcpyHostToDevice, s));

@@ -109,6 +109,10 @@ struct ParArgs {
   const double *I;
   double *tot_run, *tsq_run;      // l2 mode: running region sums in acceptance order
   int wp_bits;                    // dataflow site-word layout: 24 (16-bit labels) or 27 (10-bit)
+  uint32_t *bigmap;               // dataflow large box tier: per-warp 4-bit maps (big_words each)
+  uint32_t *bigfr2;               // ... and frontiers (2 x big_fcap per warp)
+  uint8_t *bigfg2;
+  int big_words, big_fcap;
   const int4 *rec;                // dataflow per-position records
 };
 
@@ -140,6 +144,8 @@ struct ParExtra {
   long long *band;  // band ledger: kLimbs superaccumulator limbs + dE_int sum
   DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
+  DBuf<uint32_t> *bigmap = nullptr, *bigfr2 = nullptr;  // dataflow large box tier (3-D)
+  DBuf<uint8_t> *bigfg2 = nullptr;
 };
 
 // contour.cu

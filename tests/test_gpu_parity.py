@@ -279,8 +279,9 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
     thread, the literal sequential greedy) on the same inputs: accepted moves
     in order, labels and ledger must be identical.  The dataflow runs cover
     each topology-test tier: the bounding-box map BFS (default), the hash
-    BFS (box tier off), and the grid-wide union-find assist job (box tier
-    off, hash capped at 8 sites)."""
+    BFS (box tier off), the large global-memory box tier (3-D, hash capped
+    at 8 sites) and the grid-wide union-find assist jobs (hash capped, large
+    tier off)."""
     import scenes
     if which == "cfg2":
         sc, iters = scenes.cfg2(), 3
@@ -293,13 +294,17 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
     ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
     ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
     runs = []
-    for force, mode, cap, box in (("0", "dataflow", "0", "-1"), ("0", "rounds", "0", "-1"),
-                                  ("1", "dataflow", "0", "-1"), ("0", "dataflow", "0", "0"),
-                                  ("0", "dataflow", "8", "0")):
+    for force, mode, cap, box, big in (("0", "dataflow", "0", "-1", "1"),
+                                       ("0", "rounds", "0", "-1", "1"),
+                                       ("1", "dataflow", "0", "-1", "1"),
+                                       ("0", "dataflow", "0", "0", "1"),
+                                       ("0", "dataflow", "8", "0", "1"),
+                                       ("0", "dataflow", "8", "0", "0")):
         monkeypatch.setenv("RCB_FORCE_SEQUENTIAL", force)
         monkeypatch.setenv("RCB_ACCEPT", mode)
         monkeypatch.setenv("RCB_DF_MAXINSERT", cap)
         monkeypatch.setenv("RCB_DF_BOXCAP", box)
+        monkeypatch.setenv("RCB_DF_BIGBOX", big)
         eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
         out = []
         for _ in range(iters):
@@ -411,6 +416,7 @@ def test_deferred_registry_equals_full_union_find(P, monkeypatch, cap, box, iter
     ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace)
     monkeypatch.setenv("RCB_DF_MAXINSERT", cap)
     monkeypatch.setenv("RCB_DF_BOXCAP", box)
+    monkeypatch.setenv("RCB_DF_BIGBOX", "0")  # every overflow defers (exercise the jobs)
     runs, deferred = [], []
     for q in ("1", "0"):
         monkeypatch.setenv("RCB_DF_QJOB", q)
