@@ -201,6 +201,27 @@ int32_t rcb_engine_finish(rcb_engine *eng, rcb_iter_record *rec);
 int32_t rcb_engine_particle_ranges(rcb_engine *eng, const int64_t *planes, int32_t k,
                                    int64_t *out);
 
+/* ---- synthetic-data pipeline (rcseg/synth.py) --------- *
+ * shapes: 15 doubles per shape, in scene order (later shapes overwrite):
+ * [kind (0 disk/ball, 1 rect/box, 2 annulus/shell), intensity, ncenter,
+ *  c0, c1, c2, r2lo, r2hi (disk: -inf, radius**2; annulus: inner**2,
+ *  outer**2), nbox, lo0, lo1, lo2, hi0, hi1, hi2 (rect: origin, origin+size)].
+ * kernel: the normalised Gaussian taps of synth.py:96-99 (klen odd; 0 = no
+ * blur).  psnr2 = psnr**2.  Results are bit-identical to the reference.     */
+/* synth.py:185-192 generate(): render (synth.py:73-84), blur (:87-103) and,
+ * if noise != 0, poissonize (:169-182) on the device; labels / clean / image
+ * may be NULL (not copied back). */
+int32_t rcb_synth_generate(int32_t ndim, const int64_t *dims, double background,
+                           const double *shapes, int32_t nshapes, const double *kernel,
+                           int32_t klen, int32_t noise, double psnr2, uint64_t seed,
+                           int32_t *labels, double *clean, double *image);
+/* synth.py:87-103 blur() of a float64 image. */
+int32_t rcb_synth_blur(const double *image, int32_t ndim, const int64_t *dims,
+                       const double *kernel, int32_t klen, double *out);
+/* synth.py:169-182 poissonize() of n float64 intensities. */
+int32_t rcb_synth_poissonize(const double *image, int64_t n, double psnr2, uint64_t seed,
+                             double *out);
+
 /* ---- Sobolev sweep workload (BASELINE configs[4], second part) --------- */
 typedef struct rcb_sweep rcb_sweep;
 /* Paint the union of nsph spheres (z, y, x, r as float, 4 per sphere) into a

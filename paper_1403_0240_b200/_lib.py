@@ -85,6 +85,9 @@ SIGNATURES = {
     "rcb_engine_score": [_P, _P],
     "rcb_engine_finish": [_P, _P],
     "rcb_engine_particle_ranges": [_P, _P, _I32, _P],
+    "rcb_synth_generate": [_I32, _P, _D, _P, _I32, _P, _I32, _I32, _D, C.c_uint64, _P, _P, _P],
+    "rcb_synth_blur": [_P, _I32, _P, _P, _I32, _P],
+    "rcb_synth_poissonize": [_P, _I64, _D, C.c_uint64, _P],
     "rcb_sweep_create": [_I32, _P, _P, _I32, C.c_uint64, _P, _I32, _P],
     "rcb_sweep_destroy": [_P],
     "rcb_sweep_info": [_P, _P, _P, _P],
