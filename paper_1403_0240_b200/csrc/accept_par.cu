@@ -3583,10 +3583,13 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       df_blocks = per_sm * sms;
     }
     if (A.lat.ndim == 3 && X.bigmap) {
-      // large box tier: per warp a 4-bit map of up to 2M sites and two
-      // frontiers of 16K sites (~2.8 GB for 2 368 warps; 3-D only)
+      // large box tier (3-D; in 2-D the 31x31 / 63x63 window tiers catch wide
+      // footprints and the tier measured slower): per warp a 4-bit map of up
+      // to 2M sites (at most the lattice) and two frontiers of 16K sites
+      // (~2.8 GB for 2 368 warps at full size)
       const size_t warps = (size_t)df_blocks * kDfWarps;
-      A.big_words = 1 << 18;
+      const int64_t vw = (A.lat.V + 7) / 8 + 4;
+      A.big_words = (int)(vw < (1 << 18) ? ((vw + 3) & ~3) : (1 << 18));
       A.big_fcap = 1 << 14;
       RCB_TRY(X.bigmap->reserve(warps * (size_t)A.big_words, s));
       RCB_TRY(X.bigfr2->reserve(warps * 2 * (size_t)A.big_fcap, s));
