@@ -2945,11 +2945,14 @@ __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t 
             const bool clean = own_field(o.dz, o.dy, o.dx, g, lg, c, s);
             const double cy = (double)c, iy = I[g];
             const double r_old = (clean && rho0) ? rho0[g] : rho(iy, s / cy, poisson);
-            if (lg == a) {
-              term_a = rho(iy, (s - vx) / (cy - 1.0), poisson) - r_old;
+            const bool isa = lg == a;  // one rho for either side (see k_ps_dtot2d)
+            const double t = rho(iy, (s + (isa ? -vx : vx)) / (cy + (isa ? -1.0 : 1.0)), poisson) -
+                             r_old;
+            if (isa) {
+              term_a = t;
               hit_a = true;
             } else {
-              term_b = rho(iy, (s + vx) / (cy + 1.0), poisson) - r_old;
+              term_b = t;
               hit_b = true;
               ib = iy;
             }
@@ -3203,13 +3206,21 @@ __global__ void __launch_bounds__(32 * kPsWarps) k_ps_dtot2d(
           const double r_old = (clean && rho0) ? r0[u] : rho(iy, sv / cy, poisson);
           if (centre) {
             ra_c = r_old;
-          } else if (lg == a) {
-            term_a = rho(iy, (sv - vx) / (cy - 1.0), poisson) - r_old;
-            hit_a = true;
           } else {
-            term_b = rho(iy, (sv + vx) / (cy + 1.0), poisson) - r_old;
-            hit_b = true;
-            ib = iy;
+            // one rho for either side (lanes of a warp no longer run the a-
+            // and b-paths one after the other): (sv - vx)/(cy - 1) is
+            // computed as (sv + (-vx))/(cy + (-1)), rounded identically
+            const bool isa = lg == a;
+            const double t = rho(iy, (sv + (isa ? -vx : vx)) / (cy + (isa ? -1.0 : 1.0)), poisson) -
+                             r_old;
+            if (isa) {
+              term_a = t;
+              hit_a = true;
+            } else {
+              term_b = t;
+              hit_b = true;
+              ib = iy;
+            }
           }
         }
       }
