@@ -3505,6 +3505,130 @@ __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__re
   if (band) acc_flush(sm, band);
 }
 
+// Warp-aggregated superaccumulator add (band ledger): lanes whose value
+// falls on the same limb pair sum their 32-bit limb parts in 64-bit
+// registers first (integer sums: exact in any order), then one shared-memory
+// atomic per limb and group instead of one per lane.  All lanes call it.
+__device__ __forceinline__ void acc_add_warp(long long *limbs, double d, bool has) {
+  const int lane = threadIdx.x & 31;
+  int k0 = 0;
+  long long c0 = 0, c1 = 0, c2 = 0;
+  has = has && d != 0.0;
+  if (has) {
+    const uint64_t u = (uint64_t)__double_as_longlong(d);
+    const int ex = (int)((u >> 52) & 0x7ff);
+    uint64_t m = u & ((1ull << 52) - 1);
+    int e;
+    if (ex == 0) {
+      e = -1074;
+    } else {
+      m |= 1ull << 52;
+      e = ex - 1075;
+    }
+    const int pos = e + 1074;
+    k0 = pos >> 5;
+    const int sh = pos & 31;
+    const uint64_t lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0;
+    c0 = (long long)(lo & 0xffffffffull);
+    c1 = (long long)(lo >> 32);
+    c2 = (long long)hi;
+    if (u >> 63) {
+      c0 = -c0;
+      c1 = -c1;
+      c2 = -c2;
+    }
+  }
+  unsigned act = __ballot_sync(0xffffffffu, has);
+  while (act) {
+    const int leader = __ffs(act) - 1;
+    const int k = __shfl_sync(0xffffffffu, k0, leader);
+    const bool mine = has && k0 == k;
+    long long s0 = mine ? c0 : 0, s1 = mine ? c1 : 0, s2 = mine ? c2 : 0;
+    for (int o = 16; o; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == leader) {
+      if (s0) atomicAdd((unsigned long long *)&limbs[k], (unsigned long long)s0);
+      if (s1) atomicAdd((unsigned long long *)&limbs[k + 1], (unsigned long long)s1);
+      if (s2) atomicAdd((unsigned long long *)&limbs[k + 2], (unsigned long long)s2);
+    }
+    if (mine) has = false;
+    act = __ballot_sync(0xffffffffu, has);
+  }
+}
+
+// k_refield_band for lattices below 2^31 sites: 32-bit coordinates, the ball
+// offsets packed in shared memory, four offsets' loads in flight, and the
+// band-ledger adds aggregated per warp.  Same ball order and arithmetic as
+// k_refield_band (bit-identical fields and band sum).  Warp-uniform loop.
+static constexpr int kRfMaxBall = 1024;
+__global__ void __launch_bounds__(256) k_refield_band32(
+    const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny, int nz,
+    const Off *__restrict__ ball_full, int nball_full, uint8_t *__restrict__ dirty,
+    int32_t *__restrict__ Cown, double *__restrict__ Sown, double *__restrict__ rho0, int poisson,
+    long long *__restrict__ band) {
+  __shared__ long long sm[kLimbs];
+  __shared__ int sofs[kRfMaxBall];
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  for (int k = threadIdx.x; k < nball_full; k += blockDim.x)
+    sofs[k] = ((int)(uint8_t)ball_full[k].dz << 16) | ((int)(uint8_t)ball_full[k].dy << 8) |
+              (int)(uint8_t)ball_full[k].dx;
+  __syncthreads();
+  const int plane = nx * ny;
+  const int64_t V = (int64_t)plane * nz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < V; base += stride) {
+    const int64_t f64 = base + threadIdx.x;
+    const bool act = f64 < V && dirty[f64];
+    double oldr = 0.0, newr = 0.0;
+    if (act) {
+      const int f = (int)f64;
+      if (band) oldr = rho0[f];
+      dirty[f] = 0;
+      const int z = f / plane, rem = f - z * plane;
+      const int y = rem / nx, x = rem - y * nx;
+      const int32_t own = L[f];
+      int32_t c = 0;
+      double sv = 0.0;
+      for (int k0 = 0; k0 < nball_full; k0 += 4) {
+        int g[4];
+        int32_t lab[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          const int o = k < nball_full ? sofs[k] : 0;
+          const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
+                    xx = x + (int)(int8_t)o;
+          const bool ok = k < nball_full && (unsigned)zz < (unsigned)nz &&
+                          (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+          g[u] = ok ? zz * plane + yy * nx + xx : f;
+          lab[u] = ok ? __ldg(L + g[u]) : -1;
+        }
+        double iv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) iv[u] = lab[u] == own ? __ldg(I + g[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (lab[u] == own) {
+            c += 1;
+            sv += iv[u];
+          }
+      }
+      Cown[f] = c;
+      Sown[f] = sv;
+      newr = rho(I[f], sv / (double)c, poisson);
+      if (rho0) rho0[f] = newr;
+    }
+    if (band) {  // warp-uniform: every lane reaches both calls
+      acc_add_warp(sm, -oldr, act);
+      acc_add_warp(sm, newr, act);
+    }
+  }
+  if (band) acc_flush(sm, band);
+}
+
 // Band ledger: sum of dE_int over the kept moves (band[kLimbs]) ...
 __global__ void k_dint_sum(const ParArgs A, const int64_t *__restrict__ moves,
                            long long *__restrict__ band) {
@@ -3758,9 +3882,14 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
-    k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
-        X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.dirty, X.Cown, X.Sown, X.rho0, X.poisson,
-        band_ledger ? X.band : nullptr);
+    if (A.lat.V < ((int64_t)1 << 31) && X.nball_full <= kRfMaxBall && (X.rho0 || !band_ledger))
+      k_refield_band32<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
+          X.Lmut, X.I, (int)A.lat.nx, (int)A.lat.ny, (int)A.lat.nz, X.ball_full, X.nball_full,
+          X.dirty, X.Cown, X.Sown, X.rho0, X.poisson, band_ledger ? X.band : nullptr);
+    else
+      k_refield_band<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
+          X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.dirty, X.Cown, X.Sown, X.rho0,
+          X.poisson, band_ledger ? X.band : nullptr);
     nl += 2;
     if (band_ledger) {
       if (X.lam != 0.0) k_dint_sum<<<grid_for(N, 256), 256, 0, s>>>(A, X.moves, X.band);
