@@ -1,3 +1,4 @@
+#include <climits>
 #include <algorithm>
 // K8 v2 — parallel, exact rank-ordered acceptance (sobolev mode).
 //
@@ -2328,6 +2329,75 @@ __device__ __forceinline__ void bbox_add(const ParArgs &A, int32_t l, int64_t y)
   atomicMax(b + 5, c);
 }
 
+// Shared-memory variant for nl <= kBoxSmemLabels: each block reduces its
+// sites' boxes per label in shared memory (fast shared atomics), then merges
+// the labels it touched into the global boxes -- 6 global atomics per
+// (block, label) instead of per site (cfg4: 18 ms -> well under 1 ms).
+static constexpr int kBoxSmemLabels = 2048;
+__device__ __forceinline__ void bbox_add_sm(const ParArgs &A, int32_t *sb, int32_t l, int64_t y) {
+  if (l <= 0) return;
+  const int64_t nxy = A.lat.nx * A.lat.ny;
+  const int32_t zc = (int32_t)(y / nxy), rem = (int32_t)(y - (int64_t)zc * nxy);
+  const int32_t r = rem / (int32_t)A.lat.nx, c = rem - r * (int32_t)A.lat.nx;
+  int32_t *b = sb + 6 * l;
+  atomicMin(b + 0, zc);
+  atomicMax(b + 1, zc);
+  atomicMin(b + 2, r);
+  atomicMax(b + 3, r);
+  atomicMin(b + 4, c);
+  atomicMax(b + 5, c);
+}
+
+__global__ void k_df_bbox_sm(ParArgs A, int64_t N) {
+  __shared__ int32_t sb[6 * kBoxSmemLabels];
+  const int nl = A.nl;
+  for (int k = threadIdx.x; k < 6 * nl; k += blockDim.x) sb[k] = (k & 1) ? INT_MIN : INT_MAX;
+  __syncthreads();
+  const int64_t nx = A.lat.nx, ny = A.lat.ny, nz = A.lat.nz;
+  const int64_t fy = 2 * nz * nx, fx = 2 * nz * ny, fz = A.lat.ndim == 3 ? 2 * nx * ny : 0;
+  const int64_t nb = fy + fx + fz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N + nb; i += stride) {
+    if (i < N) {
+      const int64_t y = A.px[i];
+      if (A.site_off[y] == (uint32_t)i) bbox_add_sm(A, sb, A.pown[i], y);
+      continue;
+    }
+    int64_t j = i - N, z, r, c;
+    if (j < fy) {
+      z = j / (2 * nx);
+      const int64_t q = j % (2 * nx);
+      r = q < nx ? 0 : ny - 1;
+      c = q % nx;
+    } else if ((j -= fy) < fx) {
+      z = j / (2 * ny);
+      const int64_t q = j % (2 * ny);
+      c = q < ny ? 0 : nx - 1;
+      r = q % ny;
+    } else {
+      j -= fx;
+      const int64_t q = j / (nx * ny);
+      z = q == 0 ? 0 : nz - 1;
+      r = (j % (nx * ny)) / nx;
+      c = j % nx;
+    }
+    const int64_t y = (z * ny + r) * nx + c;
+    bbox_add_sm(A, sb, A.L[y], y);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const int32_t *b = sb + 6 * l;
+    if (b[0] == INT_MAX) continue;  // not seen by this block
+    int32_t *g = A.lbox + 6 * l;
+    atomicMin(g + 0, b[0]);
+    atomicMax(g + 1, b[1]);
+    atomicMin(g + 2, b[2]);
+    atomicMax(g + 3, b[3]);
+    atomicMin(g + 4, b[4]);
+    atomicMax(g + 5, b[5]);
+  }
+}
+
 __global__ void k_df_bbox(ParArgs A, int64_t N) {
   const int64_t nx = A.lat.nx, ny = A.lat.ny, nz = A.lat.nz;
   // border sites: the y and x faces of every z-plane, plus the z faces in 3-D
@@ -2386,8 +2456,11 @@ __global__ void k_df_records(ParArgs A, int4 *__restrict__ rec) {
 
 __global__ void k_df_small(ParArgs A) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride)
-    A.small[l] = A.l2 || (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride) {
+    const uint8_t sm = A.l2 || (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
+    A.small[l] = sm;
+    if (sm) atomicAdd(A.job + 4, 1ull);  // small-label count (host: skip empty event lists)
+  }
 }
 
 // events (label, position) of candidates involving small labels, emitted in
@@ -3742,9 +3815,13 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     }
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
+    RCB_CUDA(cudaMemsetAsync(A.job + 4, 0, sizeof(unsigned long long), s));
     k_df_small<<<grid_for(A.nl, 256), 256, 0, s>>>(A);
-    k_df_bbox<<<grid_for(N + 2 * (A.lat.nz * (A.lat.nx + A.lat.ny) + A.lat.nx * A.lat.ny), 256), 256,
-                0, s>>>(A, N);
+    if (A.nl <= kBoxSmemLabels)
+      k_df_bbox_sm<<<148 * 4, 256, 0, s>>>(A, N);
+    else
+      k_df_bbox<<<grid_for(N + 2 * (A.lat.nz * (A.lat.nx + A.lat.ny) + A.lat.nx * A.lat.ny), 256),
+                  256, 0, s>>>(A, N);
     RCB_TRY(X.rec->reserve(N, s));
     k_df_records<<<grid_for(N, 256), 256, 0, s>>>(A, X.rec->p);
     A.rec = X.rec->p;
@@ -3752,6 +3829,18 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_TRY(X.evkey2->reserve(2 * N, s));
     RCB_TRY(X.labpos->reserve(2 * N, s));
     RCB_TRY(X.labpos2->reserve(2 * N, s));
+    // per-label event lists are only read for small labels; on large inputs
+    // (one host round trip is cheap there) skip building them when none is
+    // small (cfg4: sorting 2N events cost ~20 ms per iteration)
+    bool need_lists = true;
+    if (N > ((int64_t)1 << 20)) {
+      static unsigned long long *hcount = nullptr;
+      if (!hcount) RCB_CUDA(cudaMallocHost((void **)&hcount, sizeof(unsigned long long)));
+      RCB_CUDA(cudaMemcpyAsync(hcount, A.job + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      RCB_CUDA(cudaStreamSynchronize(s));
+      need_lists = *hcount != 0;
+    }
+    if (need_lists) {
     k_df_labkeys<<<grid_for(N, 256), 256, 0, s>>>(A, N, X.evkey->p, X.labpos2->p);
     int lbits = 1;
     while (lbits < 32 && ((int64_t)1 << lbits) <= A.nl) ++lbits;
@@ -3763,6 +3852,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
                                              X.labpos->p, 2 * N, 0, lbits, s));
     k_df_labcsr<<<grid_for(2 * N, 256), 256, 0, s>>>(X.evkey2->p, X.labpos->p, 2 * N, A.nl,
                                                      A.lab_ptr);
+    }
     A.lab_pos = X.labpos->p;
     T.mark("df-setup");
     // persistent grid: one block (16 warps, 16 positions in flight) per 512
