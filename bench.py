@@ -327,11 +327,16 @@ def run_ours(args):
     barrier()
     t0 = time.perf_counter()
     e2 = P.RegionCompetition(img_h, lab_h, ecfg, scfg, ocfg, device=local)
+    t_ctor = time.perf_counter()
     for _ in range(args.warmup + args.steps):
         e2.iterate()
+    t_it = time.perf_counter()
     out_labels = e2.labels
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    e2e_parts = {"construct_ms": round(1e3 * (t_ctor - t0), 3),
+                 "iterate_ms": round(1e3 * (t_it - t_ctor), 3),
+                 "labels_ms": round(1e3 * (time.perf_counter() - t_it), 3)}
     if ws > 1:
         tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -377,7 +382,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": (img_h.nbytes + lab_h.nbytes) / n_e2e,
                     "d2h_bytes_per_step": (out_labels.nbytes + 64 * n_e2e) / n_e2e,
                     "what": "RegionCompetition(host image, host labels) + K iterate() + labels, "
-                            "wall clock"},
+                            "wall clock", "parts": e2e_parts},
         }
         if args.roofline and energy_sob_ms > 0:
             ach = alg_bytes / (energy_sob_ms / 1e3) / 1e9

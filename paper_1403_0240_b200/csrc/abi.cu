@@ -1,3 +1,5 @@
+#include <mutex>
+#include <chrono>
 // C ABI of librcseg_b200 (include/rcb.h): the device engine that replaces
 // RegionCompetition.iterate (optimizer.py:122-160) and the function-level
 // drop-ins.  Each entry point cites the reference function it replaces.
@@ -81,6 +83,33 @@ struct Scalars {
 
 using namespace rcb;
 
+namespace {
+// Pinned host blocks for the engines' small read-back buffers, recycled
+// across engines: cudaMallocHost pins pages and can take milliseconds, which
+// showed up as constructor jitter in the end-to-end timing.
+constexpr size_t kPinnedBlock = 4096;
+std::mutex g_pinned_mu;
+std::vector<void *> g_pinned_free;
+void *pinned_get() {
+  {
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      void *p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  void *p = nullptr;
+  return cudaMallocHost(&p, kPinnedBlock) == cudaSuccess ? p : nullptr;
+}
+void pinned_put(void *p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
+}  // namespace
+
 struct rcb_engine {
   int device = 0;
   cudaStream_t s = nullptr;
@@ -161,6 +190,7 @@ struct rcb_engine {
   int score_launches = 0;
   uint32_t *hoff = nullptr;  // pinned: site_off reads
   unsigned long long *hwatch = nullptr;  // pinned: dataflow watchdog words (job[56..61])
+  void *pinned = nullptr;                // the pinned block hsc / hoff / hwatch live in
 
   ~rcb_engine() {
     if (s) {
@@ -192,9 +222,7 @@ struct rcb_engine {
         if (e) cudaEventDestroy(e);
       if (own_stream) cudaStreamDestroy(s);
     }
-    if (hsc) cudaFreeHost(hsc);
-    if (hoff) cudaFreeHost(hoff);
-    if (hwatch) cudaFreeHost(hwatch);
+    pinned_put(pinned);
   }
 
   int32_t prepare() {  // K1 pass 1 + scan on the current raster
@@ -238,11 +266,29 @@ int32_t rcb_device_count(int32_t *n) {
   return RCB_OK;
 }
 
+namespace {
+struct CtorLog {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  cudaStream_t s = nullptr;
+  CtorLog() : on(getenv("RCB_CTOR_LOG") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char *what) {
+    if (!on) return;
+    if (s) cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rcb-ctor] %-12s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
 int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t ndim,
                           const int64_t *dims, const rcb_energy_cfg *ecfg,
                           const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg, int32_t device,
                           void *stream, rcb_engine **out) {
   *out = nullptr;
+  CtorLog clog;
   RCB_TRY(check_device());
   RCB_TRY(check_lattice(ndim, dims));
   if (ecfg->region_model == 1 && (ecfg->smooth_radius < 1 || ecfg->smooth_radius > 15))
@@ -280,18 +326,36 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   };
   cudaStream_t s = e->s;
   e->lat = make_lat(ndim, dims);
+  clog.s = e->s;
+  clog.mark("stream+pool");
   {
     // prime the device pool with the engine's footprint plus room for the
     // particle buffers to double a few times (~320 B per site + 256 MB, at
     // most max(16 GB, half the free memory)): later stream-ordered allocations are then served
     // from cached memory instead of blocking the host while memory is mapped
     size_t want = (size_t)320 * (size_t)e->lat.V + ((size_t)256 << 20);
-    size_t free_b = 0, total_b = 0;
-    size_t cap = (size_t)16 << 30;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
-    if (want > cap) want = cap;
-    void *prime = nullptr;
-    if (cudaMallocAsync(&prime, want, s) == cudaSuccess) cudaFreeAsync(prime, s);
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    // a pool that already caches that much free memory (engines destroyed
+    // earlier in the process) serves the engine's buffers without priming;
+    // one large priming block would not fit its free chunks and map anew
+    if (clog.on)
+      fprintf(stderr, "[rcb-ctor] pool reserved %.1f MB used %.1f MB want %.1f MB\n", reserved / 1e6,
+              used / 1e6, want / 1e6);
+    if (reserved < used + want) {
+      size_t cap = (size_t)16 << 30;
+      if (want > cap) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
+      }
+      if (want > cap) want = cap;
+      void *prime = nullptr;
+      if (cudaMallocAsync(&prime, want, s) == cudaSuccess) cudaFreeAsync(prime, s);
+    }
     cudaGetLastError();
   }
   e->ecfg = *ecfg;
@@ -306,19 +370,27 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
     e->profile = pf && pf[0] == '1';
   }
   const int64_t V = e->lat.V;
-  int32_t mx = 0;
-  for (int64_t i = 0; i < V; ++i) {
-    if (labels[i] < 0) return bail(fail(RCB_ERR_VALUE, "label raster contains negative labels"));
-    mx = std::max(mx, labels[i]);
-  }
-  e->nl = mx + 1;
   int32_t rc;
 #define TRYB(x)                 \
   if ((rc = (x)) != RCB_OK) {   \
     return bail(rc);            \
   }
+  clog.mark("prime");
   TRYB(upload(e->L, labels, V, s));
   TRYB(upload(e->I, image, V, s));
+  {
+    // input validation on the device (grid.py:24-39; optimizer.py:100-101):
+    // label min / max (-> the label count), non-finite and negative
+    // intensities, one reduction pass and one small read-back
+    InputCheck chk{};
+    TRYB(check_inputs(e->L.p, e->I.p, V, &chk, s));
+    if (chk.nonfinite)
+      return bail(fail(RCB_ERR_VALUE, "intensity raster contains non-finite values"));
+    if (chk.label_min < 0) return bail(fail(RCB_ERR_VALUE, "label raster contains negative labels"));
+    if (ecfg->noise_model == 1 && chk.image_min < 0.0)
+      return bail(fail(RCB_ERR_VALUE, "Poisson noise model requires nonnegative intensities"));
+    e->nl = chk.label_max + 1;
+  }
   TRYB(e->cnt.reserve(e->nl, s));
   TRYB(e->tot.reserve(e->nl, s));
   TRYB(e->tsq.reserve(e->nl, s));
@@ -327,12 +399,15 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   TRYB(e->queue.reserve(V, s));
   TRYB(e->site_off.reserve(V + 1, s));
   TRYB(e->sc.reserve(1, s));
-  if (cudaMallocHost((void **)&e->hsc, sizeof(Scalars)) != cudaSuccess)
-    return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
+  clog.mark("upload");
+  static_assert(sizeof(Scalars) <= 2048, "pinned block layout: Scalars | hoff @2048 | hwatch @3072");
+  e->pinned = pinned_get();
+  if (!e->pinned) return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
+  e->hsc = reinterpret_cast<Scalars *>(e->pinned);
+  e->hoff = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(e->pinned) + 2048);
+  e->hwatch = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(e->pinned) + 3072);
   memset(e->hsc, 0, sizeof(Scalars));
-  if (cudaMallocHost((void **)&e->hoff, 16 * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMallocHost((void **)&e->hwatch, 8 * sizeof(unsigned long long)) != cudaSuccess)
-    return bail(fail(RCB_ERR_CUDA, "cudaMallocHost failed"));
+
   memset(e->hwatch, 0, 8 * sizeof(unsigned long long));
   if (cudaMemsetAsync(e->sc.p, 0, sizeof(Scalars), s) != cudaSuccess ||
       cudaMemsetAsync(e->vis.p, 0, sizeof(uint32_t) * V, s) != cudaSuccess)
@@ -393,9 +468,13 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   }
   for (auto &ev : e->ev) cudaEventCreate(&ev);
   for (auto &ev : e->ev_acc) cudaEventCreate(&ev);
+  clog.mark("buffers");
   TRYB(e->refresh());
+  clog.mark("refresh");
   TRYB(e->components());
+  clog.mark("components");
   TRYB(e->prepare());
+  clog.mark("prepare");
 #undef TRYB
   *out = e;
   return RCB_OK;

@@ -1,3 +1,5 @@
+#include <climits>
+#include <cstring>
 // Energy kernels: K2 region statistics, K3 PC increment + perimeter change,
 // K4 own-label PS ball fields, K5 PS increment, K9 exact energy totals.
 #include <cub/device/device_radix_sort.cuh>
@@ -621,6 +623,81 @@ double limbs_to_double(const long long *limbs) {
   }
   double r = ldexp((double)m, shift - 1074);
   return neg ? -r : r;
+}
+
+
+// ---------------------------------------------------------------------------
+// Input validation of the engine (grid.py:24-39, optimizer.py:100-101): label
+// min / max, intensity min and non-finite count in one reduction pass.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void k_check_inputs(const int32_t *__restrict__ L, const double *__restrict__ I,
+                               int64_t V, int *lmin, int *lmax, unsigned long long *imin,
+                               unsigned long long *nonfin) {
+  int lo = INT_MAX, hi = INT_MIN;
+  unsigned long long dm = ~0ull, nf = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += stride) {
+    const int l = L[i];
+    lo = l < lo ? l : lo;
+    hi = l > hi ? l : hi;
+    const double v = I[i];
+    if (!isfinite(v)) {
+      ++nf;
+    } else {
+      const unsigned long long k = dkey(v);
+      dm = k < dm ? k : dm;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_down_sync(0xffffffffu, hi, o));
+    const unsigned long long d2 = __shfl_down_sync(0xffffffffu, dm, o);
+    dm = d2 < dm ? d2 : dm;
+    nf += __shfl_down_sync(0xffffffffu, nf, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(lmin, lo);
+    atomicMax(lmax, hi);
+    atomicMin(imin, dm);
+    if (nf) atomicAdd(nonfin, nf);
+  }
+}
+
+int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *out,
+                     cudaStream_t s) {
+  struct Dev {
+    int lmin, lmax;
+    unsigned long long imin, nonfin;
+  };
+  static thread_local Dev *hbuf = nullptr;  // pinned, reused
+  if (!hbuf) RCB_CUDA(cudaMallocHost((void **)&hbuf, sizeof(Dev)));
+  Dev *d = nullptr;
+  RCB_CUDA(cudaMallocAsync((void **)&d, sizeof(Dev), s));
+  const Dev init{INT_MAX, INT_MIN, ~0ull, 0ull};
+  *hbuf = init;
+  RCB_CUDA(cudaMemcpyAsync(d, hbuf, sizeof(Dev), cudaMemcpyHostToDevice, s));
+  int64_t g = (V + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  k_check_inputs<<<(unsigned)g, 256, 0, s>>>(L, I, V, &d->lmin, &d->lmax, &d->imin, &d->nonfin);
+  RCB_CUDA(cudaGetLastError());
+  RCB_CUDA(cudaMemcpyAsync(hbuf, d, sizeof(Dev), cudaMemcpyDeviceToHost, s));
+  RCB_CUDA(cudaFreeAsync(d, s));
+  RCB_CUDA(cudaStreamSynchronize(s));
+  out->label_min = V ? hbuf->lmin : 0;
+  out->label_max = V ? hbuf->lmax : 0;
+  out->nonfinite = (int64_t)hbuf->nonfin;
+  const unsigned long long k = hbuf->imin;
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double v;
+  memcpy(&v, &u, sizeof(v));
+  out->image_min = (k == ~0ull) ? 0.0 : v;
+  return RCB_OK;
 }
 
 }  // namespace rcb

@@ -148,6 +148,14 @@ struct ParExtra {
   DBuf<uint8_t> *bigfg2 = nullptr;
 };
 
+// input validation (energy.cu): one pass, one small read-back (synchronises s)
+struct InputCheck {
+  int32_t label_min, label_max;
+  double image_min;
+  int64_t nonfinite;
+};
+int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *out, cudaStream_t s);
+
 // contour.cu
 int32_t contour_scan(const int32_t *L, const Lat &lat, int full_fg, uint32_t *site_off,
                      DBuf<uint8_t> &tmp, cudaStream_t s);

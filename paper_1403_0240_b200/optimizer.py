@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -75,7 +76,16 @@ class _DeviceModel:
     """``engine.model`` view: stats fetched from the device on access."""
 
     def __init__(self, eng: "RegionCompetition"):
-        self._eng = eng
+        # weak: no engine <-> model reference cycle, so dropping the engine
+        # frees its device memory at once instead of at the next GC pass
+        self._ref = weakref.ref(eng)
+
+    @property
+    def _eng(self) -> "RegionCompetition":
+        e = self._ref()
+        if e is None:
+            raise RuntimeError("the engine of this model was destroyed")
+        return e
 
     @property
     def stats(self) -> StatsTable:
@@ -97,12 +107,13 @@ class RegionCompetition:
                  sobolev_params: SobolevParams | None = None,
                  config: OptimizerConfig | None = None, conn: Connectivity | None = None,
                  device: int = 0, stream=None):
-        validate_image(image)
-        validate_labels(init_labels)
+        # grid.py:24-39 / optimizer.py:100-101: rank and dtype here; the value
+        # checks (non-finite intensities, negative labels, negative intensities
+        # under Poisson) run on the device in rcb_engine_create, same messages
+        validate_image(image, values=False)
+        validate_labels(init_labels, values=False)
         if image.shape != init_labels.shape:
             raise ValueError("image and labels differ in shape")
-        if energy_config.noise_model == "poisson" and image.size and np.min(image) < 0:
-            raise ValueError("Poisson noise model requires nonnegative intensities")
         _lib.require_device()
         self.device = int(device)
         self._slab = None

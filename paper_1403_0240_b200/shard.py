@@ -28,6 +28,7 @@ waits on another engine).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 
@@ -125,7 +126,7 @@ class SlabState:
     """Per-engine slab bookkeeping shared by the exchange paths."""
 
     def __init__(self, engine, world: int, rank: int):
-        self.engine = engine
+        self.engine = weakref.proxy(engine)  # the engine holds this state: no cycle
         self.world = world
         self.rank = rank
         n_planes, _ = outer_planes(engine.shape)

@@ -480,3 +480,26 @@ def test_dataflow_wide_site_words(P, monkeypatch, which):
     for (a, b) in zip(runs[0][0], runs[1][0]):
         assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2])
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_engine_input_validation_on_device(P):
+    """grid.py:24-39 / optimizer.py:100-101 semantics, checked on the device
+    in rcb_engine_create: the same ValueErrors, and the label count."""
+    img = np.full((20, 24), 2.0)
+    lab = np.zeros((20, 24), np.int32)
+    lab[5:12, 6:15] = 3
+    ecfg = P.EnergyConfig("pc", "gauss")
+    eng = P.RegionCompetition(img, lab, ecfg)
+    assert eng.n_labels == 4
+    bad = img.copy()
+    bad[3, 4] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        P.RegionCompetition(bad, lab, ecfg)
+    neg = lab.copy()
+    neg[0, 0] = -1
+    with pytest.raises(ValueError, match="negative labels"):
+        P.RegionCompetition(img, neg, ecfg)
+    with pytest.raises(ValueError, match="nonnegative"):
+        P.RegionCompetition(img - 3.0, lab, P.EnergyConfig("pc", "poisson"))
+    with pytest.raises(ValueError):
+        P.RegionCompetition(img, lab.astype(np.float64), ecfg)
