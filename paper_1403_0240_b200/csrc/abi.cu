@@ -215,6 +215,7 @@ struct rcb_engine {
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
+      drop_chains(pending, s);
       cudaStreamSynchronize(s);
       for (auto &e : ev)
         if (e) cudaEventDestroy(e);
@@ -235,7 +236,15 @@ struct rcb_engine {
     return RCB_OK;
   }
 
+  std::vector<PendingChain> pending;  // PS: deferred total / total_sq chains
+
+  int32_t flush_stats() {  // make tot / tsq current (replay deferred chains)
+    if (pending.empty()) return RCB_OK;
+    return replay_chains(pending, nullptr, tot.p, tsq.p, s);
+  }
+
   int32_t refresh() {  // energy.py:285-291
+    drop_chains(pending, s);  // superseded by the rebuild
     RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
     if (ecfg.region_model == 1)
       RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s, rho0.p,
@@ -796,6 +805,10 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
       {
+        const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
+        X.pending = (ds && ds[0] == '0') ? nullptr : &e->pending;
+      }
+      {
         const char *bt = getenv("RCB_DF_BIGBOX");  // "0": no large box tier (comparison runs)
         if (!(bt && bt[0] == '0')) {
           X.bigmap = &e->bigmap;
@@ -848,6 +861,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       A.acc = e->acc.p;
       A.moves = &d->moves;
       A.energy = &d->energy;
+      RCB_TRY(e->flush_stats());  // the sequential kernel reads and updates the sums
       RCB_TRY(accept_seq(A, s));
   launches += 1;
     }
@@ -1014,6 +1028,7 @@ int32_t rcb_engine_get_stats(rcb_engine *e, int64_t *count, double *total, doubl
                              int32_t n_labels) {
   if (n_labels < e->nl) return fail(RCB_ERR_CAPACITY, "stats buffers too small");
   RCB_CUDA(cudaSetDevice(e->device));
+  RCB_TRY(e->flush_stats());
   RCB_CUDA(cudaMemcpyAsync(count, e->cnt.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaMemcpyAsync(total, e->tot.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaMemcpyAsync(total_sq, e->tsq.p, 8 * e->nl, cudaMemcpyDeviceToHost, e->s));

@@ -3406,11 +3406,14 @@ __global__ void k_event_vals(const int64_t *__restrict__ acc, const uint32_t *__
 __global__ void __launch_bounds__(512) k_label_chain(
     const ParArgs A, const uint32_t *__restrict__ evval, const double *__restrict__ evv,
     const int64_t *__restrict__ start, const int64_t *__restrict__ end, double *__restrict__ tot,
-    double *__restrict__ tsq, double *__restrict__ snap, int32_t *__restrict__ ncomp) {
+    double *__restrict__ tsq, double *__restrict__ snap, int32_t *__restrict__ ncomp,
+    int chains = 3) {
   typedef OrderedSum<512> OS;
   __shared__ typename OS::Temp T;
-  const int64_t l = blockIdx.x / 3;
-  const int which = blockIdx.x % 3;
+  // chains: 3 = count, total, total_sq per label; 1 = count only (PS: the
+  // sums are deferred); 2 = total and total_sq only (their replay)
+  const int64_t l = blockIdx.x / chains;
+  const int which = chains == 2 ? 1 + blockIdx.x % 2 : blockIdx.x % chains;
   const int64_t s0 = start[l], n = end[l] - s0;
   if (which == 0) {
     typedef cub::BlockScan<long long, 512> Scan;
@@ -3429,7 +3432,7 @@ __global__ void __launch_bounds__(512) k_label_chain(
       long long excl, agg;
       Scan(sc).ExclusiveSum(d, excl, agg);
       const long long c0 = carry;
-      if (i < n) snap[6 * (int64_t)(ev >> 1) + 3 * (ev & 1u)] = (double)(c0 + excl);
+      if (i < n && snap) snap[6 * (int64_t)(ev >> 1) + 3 * (ev & 1u)] = (double)(c0 + excl);
       __syncthreads();
       if (threadIdx.x == 0) carry = c0 + agg;
       __syncthreads();
@@ -3449,6 +3452,7 @@ __global__ void __launch_bounds__(512) k_label_chain(
     return (ev & 1u) ? w : -w;
   };
   auto pre = [&](long long i, double before) {
+    if (!snap) return;
     const uint32_t ev = evval[s0 + i];
     snap[6 * (int64_t)(ev >> 1) + 3 * (ev & 1u) + which] = before;
   };
@@ -3754,6 +3758,29 @@ struct StageTimer {
   }
 };
 
+int32_t replay_chains(std::vector<PendingChain> &pending, const int64_t *, double *tot,
+                      double *tsq, cudaStream_t s) {
+  ParArgs A{};  // the sum chains read only their event lists
+  for (PendingChain &pc : pending) {
+    const int64_t *st = pc.bounds.p, *en = pc.bounds.p + pc.nl;
+    A.nl = pc.nl;
+    k_label_chain<<<2 * pc.nl, 512, 0, s>>>(A, pc.evval.p, pc.evv.p, st, en, tot, tsq, nullptr,
+                                            nullptr, 2);
+    RCB_CUDA(cudaGetLastError());
+  }
+  drop_chains(pending, s);
+  return RCB_OK;
+}
+
+void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s) {
+  for (PendingChain &pc : pending) {
+    pc.evval.release(s);
+    pc.evv.release(s);
+    pc.bounds.release(s);
+  }
+  pending.clear();
+}
+
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) {
   StageTimer T(s);
   T.mark("start");
@@ -3957,8 +3984,21 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_TRY(X.evv->reserve(2 * cap, s));
     k_event_vals<<<grid_for(2 * cap, 256), 256, 0, s>>>(X.acc, X.evval2->p, X.evkey2->p, 2 * cap,
                                                         A.nl, X.I, X.evv->p);
-    k_label_chain<<<3 * A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq,
-                                           X.snap->p, X.ncomp);
+    if (X.region_ps && X.pending) {
+      // counts now (vanish tests, small labels); the sums when read
+      k_label_chain<<<A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq, nullptr,
+                                         X.ncomp, 1);
+      X.pending->emplace_back();
+      PendingChain &pc = X.pending->back();
+      std::swap(pc.evval, *X.evval2);
+      std::swap(pc.evv, *X.evv);
+      std::swap(pc.bounds, *X.bounds);
+      pc.nl = A.nl;
+      if (X.pending->size() > 16) RCB_TRY(replay_chains(*X.pending, nullptr, X.tot, X.tsq, s));
+    } else {
+      k_label_chain<<<3 * A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq,
+                                             X.snap->p, X.ncomp);
+    }
     if (!X.region_ps)
       k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
                                                    X.lam, X.dtot);

@@ -1,5 +1,6 @@
 // Host-side launch wrappers of the kernels (internal to librcseg_b200).
 #pragma once
+#include <vector>
 
 #include "common.cuh"
 
@@ -116,6 +117,16 @@ struct ParArgs {
   const int4 *rec;                // dataflow per-position records
 };
 
+// PS runs: the per-label total / total_sq chains (only the stats API and the
+// sequential kernel read them; the next resync rebuilds them from the raster)
+// are replayed lazily from the saved event lists, in iteration order.
+struct PendingChain {
+  DBuf<uint32_t> evval;
+  DBuf<double> evv;
+  DBuf<int64_t> bounds;
+  int32_t nl = 0;
+};
+
 struct ParExtra {
   int64_t n_particles, budget;
   uint32_t *slot;
@@ -144,6 +155,7 @@ struct ParExtra {
   long long *band;  // band ledger: kLimbs superaccumulator limbs + dE_int sum
   DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
+  std::vector<PendingChain> *pending = nullptr;  // PS: defer the total / total_sq chains here
   DBuf<uint32_t> *bigmap = nullptr, *bigfr2 = nullptr;  // dataflow large box tier (3-D)
   DBuf<uint8_t> *bigfg2 = nullptr;
 };
@@ -227,6 +239,10 @@ int32_t label_components(const int32_t *L, const Lat &lat, int full_fg, int32_t 
 
 // accept_par.cu
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches);
+// replay (then release) deferred total / total_sq chains in order
+int32_t replay_chains(std::vector<PendingChain> &pending, const int64_t *cnt0_unused, double *tot,
+                      double *tsq, cudaStream_t s);
+void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s);
 size_t accept_par_smem();
 
 // tables (abi.cu)

@@ -503,3 +503,35 @@ def test_engine_input_validation_on_device(P):
         P.RegionCompetition(img - 3.0, lab, P.EnergyConfig("pc", "poisson"))
     with pytest.raises(ValueError):
         P.RegionCompetition(img, lab.astype(np.float64), ecfg)
+
+
+def test_ps_deferred_stats_chains(P, monkeypatch):
+    """PS runs replay the per-label total / total_sq chains when the stats are
+    read: identical to the eager chains before and after a resync, and to
+    the oracle's sequential StatsTable updates."""
+    import scenes
+    sc = scenes.cfg2_small()
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=1e-3)
+    out = []
+    for d in ("1", "0"):
+        monkeypatch.setenv("RCB_DEFER_STATS", d)
+        eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
+        snaps = []
+        for it in range(13):
+            eng.iterate()
+            if it in (0, 6, 8, 12):
+                st = eng.model.stats
+                snaps.append((st.count.copy(), st.total.copy(), st.total_sq.copy()))
+        out.append(snaps)
+    for a, b in zip(out[0], out[1]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    ref = O.OracleEngine(sc.image, sc.labels, "ps", "poisson", 0.0, sc.smooth_radius,
+                         sc.length_scale, config=O.OptimizerConfig(vanish_grace=sc.vanish_grace,
+                                                                   drift_tolerance=1e-3))
+    for _ in range(7):
+        ref.iterate()
+    assert np.array_equal(out[0][1][0], ref.stats.count)
+    assert np.array_equal(out[0][1][1], ref.stats.total)
+    assert np.array_equal(out[0][1][2], ref.stats.total_sq)
