@@ -3582,60 +3582,6 @@ __global__ void k_refield_band(const int32_t *__restrict__ L, const double *__re
   if (band) acc_flush(sm, band);
 }
 
-// Warp-aggregated superaccumulator add (band ledger): lanes whose value
-// falls on the same limb pair sum their 32-bit limb parts in 64-bit
-// registers first (integer sums: exact in any order), then one shared-memory
-// atomic per limb and group instead of one per lane.  All lanes call it.
-__device__ __forceinline__ void acc_add_warp(long long *limbs, double d, bool has) {
-  const int lane = threadIdx.x & 31;
-  int k0 = 0;
-  long long c0 = 0, c1 = 0, c2 = 0;
-  has = has && d != 0.0;
-  if (has) {
-    const uint64_t u = (uint64_t)__double_as_longlong(d);
-    const int ex = (int)((u >> 52) & 0x7ff);
-    uint64_t m = u & ((1ull << 52) - 1);
-    int e;
-    if (ex == 0) {
-      e = -1074;
-    } else {
-      m |= 1ull << 52;
-      e = ex - 1075;
-    }
-    const int pos = e + 1074;
-    k0 = pos >> 5;
-    const int sh = pos & 31;
-    const uint64_t lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0;
-    c0 = (long long)(lo & 0xffffffffull);
-    c1 = (long long)(lo >> 32);
-    c2 = (long long)hi;
-    if (u >> 63) {
-      c0 = -c0;
-      c1 = -c1;
-      c2 = -c2;
-    }
-  }
-  unsigned act = __ballot_sync(0xffffffffu, has);
-  while (act) {
-    const int leader = __ffs(act) - 1;
-    const int k = __shfl_sync(0xffffffffu, k0, leader);
-    const bool mine = has && k0 == k;
-    long long s0 = mine ? c0 : 0, s1 = mine ? c1 : 0, s2 = mine ? c2 : 0;
-    for (int o = 16; o; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    }
-    if (lane == leader) {
-      if (s0) atomicAdd((unsigned long long *)&limbs[k], (unsigned long long)s0);
-      if (s1) atomicAdd((unsigned long long *)&limbs[k + 1], (unsigned long long)s1);
-      if (s2) atomicAdd((unsigned long long *)&limbs[k + 2], (unsigned long long)s2);
-    }
-    if (mine) has = false;
-    act = __ballot_sync(0xffffffffu, has);
-  }
-}
-
 // k_refield_band for lattices below 2^31 sites: 32-bit coordinates, the ball
 // offsets packed in shared memory, four offsets' loads in flight, and the
 // band-ledger adds aggregated per warp.  Same ball order and arithmetic as

@@ -399,17 +399,78 @@ __global__ void k_gather_vals(const uint32_t *__restrict__ sites, const double *
 // Per label (blockIdx.x = 2 * label + which): the raster-order fp64 sum of the
 // label's values (which = 0) or of their squares (which = 1), replayed exactly
 // by OrderedSum; the count is the segment length.
+// Integer fast path of k_seq_sums, for all labels at once (the label-sorted
+// values split over the whole grid instead of one block per label): per
+// (label, which) the int64 sum, the max |addend| and whether every addend is
+// an integer of magnitude <= 2^52.  Warps whose lanes share one label
+// (sorted input: nearly all) reduce first and issue one atomic each.
+__global__ void k_int_sums(const double *__restrict__ vals, const uint32_t *__restrict__ keys,
+                           int64_t V, long long *__restrict__ isum,
+                           unsigned long long *__restrict__ vmax, int *__restrict__ notint) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < V; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < V;
+    const uint32_t l = in ? keys[i] : 0xffffffffu;
+    const double v0 = in ? vals[i] : 0.0;
+    const uint32_t l0 = __shfl_sync(0xffffffffu, l, 0);
+    const bool uni = __all_sync(0xffffffffu, !in || l == l0);
+    for (int which = 0; which < 2; ++which) {
+      const double v = which ? v0 * v0 : v0;
+      const double av = fabs(v);
+      const bool ok = !in || (av <= 4503599627370496.0 && v == rint(v));
+      long long a = (in && ok) ? (long long)v : 0;
+      unsigned long long m = in ? (unsigned long long)__double_as_longlong(av) : 0ull;
+      if (uni) {
+        for (int o = 16; o; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, m, o);
+          m = m2 > m ? m2 : m;
+        }
+        const bool bad = __any_sync(0xffffffffu, !ok);
+        if (lane == 0 && l0 != 0xffffffffu) {
+          atomicAdd((unsigned long long *)&isum[2 * l0 + which], (unsigned long long)a);
+          atomicMax(&vmax[2 * l0 + which], m);
+          if (bad) atomicOr(&notint[2 * l0 + which], 1);
+        }
+      } else if (in) {
+        atomicAdd((unsigned long long *)&isum[2 * l + which], (unsigned long long)a);
+        atomicMax(&vmax[2 * l + which], m);
+        if (!ok) atomicOr(&notint[2 * l + which], 1);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(512) k_seq_sums(const double *__restrict__ vals,
                                                   const int64_t *__restrict__ start,
                                                   const int64_t *__restrict__ end, int32_t nl,
                                                   int64_t *__restrict__ cnt,
                                                   double *__restrict__ tot,
-                                                  double *__restrict__ tsq) {
+                                                  double *__restrict__ tsq,
+                                                  const long long *__restrict__ isum_g,
+                                                  const unsigned long long *__restrict__ vmax_g,
+                                                  const int *__restrict__ notint_g) {
   typedef OrderedSum<512> OS;
   __shared__ typename OS::Temp T;
   const int32_t l = blockIdx.x >> 1;
   const int which = blockIdx.x & 1;
   const int64_t s = start[l], n = end[l] - s;
+  if (isum_g) {  // the grid-wide integer pre-pass (k_int_sums) decided it
+    const double vm = __longlong_as_double((long long)vmax_g[2 * l + which]);
+    if (!notint_g[2 * l + which] && (double)n * vm < 9007199254740992.0) {
+      if (threadIdx.x == 0) {
+        if (which) {
+          tsq[l] = (double)isum_g[2 * l + which];
+        } else {
+          tot[l] = (double)isum_g[2 * l + which];
+          cnt[l] = n;
+        }
+      }
+      return;
+    }
+  }
   // Exact fast path for integer data (Poisson counts): if every addend is an
   // integer and n * max|addend| < 2^53, every partial sum of the sequential
   // chain from 0 is an exactly representable integer, so each fl() is exact
@@ -499,7 +560,21 @@ int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, 
   }
   RCB_TRY(sc.gathered.reserve(V, s));
   k_gather_vals<<<grid_for(V, 256), 256, 0, s>>>(sc.vals.p, I, V, sc.gathered.p);
-  k_seq_sums<<<2 * nl, 512, 0, s>>>(sc.gathered.p, start, end, nl, cnt, tot, tsq);
+  // integer fast path over the whole grid first (Poisson counts)
+  RCB_TRY(sc.isum.reserve(2 * (size_t)nl, s));
+  RCB_TRY(sc.imax.reserve(2 * (size_t)nl, s));
+  RCB_TRY(sc.inot.reserve(2 * (size_t)nl, s));
+  RCB_CUDA(cudaMemsetAsync(sc.isum.p, 0, sizeof(long long) * 2 * nl, s));
+  RCB_CUDA(cudaMemsetAsync(sc.imax.p, 0, sizeof(unsigned long long) * 2 * nl, s));
+  RCB_CUDA(cudaMemsetAsync(sc.inot.p, 0, sizeof(int) * 2 * nl, s));
+  if (V > 0) {
+    int64_t g = (V + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_int_sums<<<(unsigned)g, 256, 0, s>>>(sc.gathered.p, sc.keys.p, V, sc.isum.p, sc.imax.p,
+                                           sc.inot.p);
+  }
+  k_seq_sums<<<2 * nl, 512, 0, s>>>(sc.gathered.p, start, end, nl, cnt, tot, tsq, sc.isum.p,
+                                    sc.imax.p, sc.inot.p);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -529,9 +604,13 @@ __global__ void k_ps_terms(const int32_t *__restrict__ Cown, const double *__res
   __shared__ long long sm[kLimbs];
   for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
   __syncthreads();
+  // warp-uniform loop: the limb adds are aggregated per warp (acc_add_warp)
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < V; f += stride)
-    acc_add(sm, rho(I[f], Sown[f] / (double)Cown[f], poisson));
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < V; base += stride) {
+    const int64_t f = base + threadIdx.x;
+    const bool in = f < V;
+    acc_add_warp(sm, in ? rho(I[f], Sown[f] / (double)Cown[f], poisson) : 0.0, in);
+  }
   acc_flush(sm, limbs);
 }
 

@@ -12,8 +12,14 @@ struct StatsScratch {
   DBuf<int64_t> bounds;
   DBuf<uint8_t> tmp;
   DBuf<double> gathered;
+  DBuf<long long> isum;
+  DBuf<unsigned long long> imax;
+  DBuf<int> inot;
   void release(cudaStream_t s) {
     gathered.release(s);
+    isum.release(s);
+    imax.release(s);
+    inot.release(s);
     keys.release(s);
     vals_in.release(s);
     vals.release(s);
