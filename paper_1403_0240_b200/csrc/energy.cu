@@ -61,6 +61,58 @@ __global__ void k_ps_fields(const int32_t *__restrict__ L, const double *__restr
   }
 }
 
+// k_ps_fields for lattices below 2^31 sites, fused with the rho0 table:
+// 32-bit coordinates, packed ball offsets in shared memory, four offsets'
+// loads in flight; same ball order and sums (bit-identical fields).
+__global__ void __launch_bounds__(256) k_ps_fields32(
+    const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny, int nz,
+    const Off *__restrict__ ball, int nball, int32_t *__restrict__ Cown, double *__restrict__ Sown,
+    double *__restrict__ rho0, int poisson) {
+  __shared__ int sofs[1024];
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = ((int)(uint8_t)ball[k].dz << 16) | ((int)(uint8_t)ball[k].dy << 8) |
+              (int)(uint8_t)ball[k].dx;
+  __syncthreads();
+  const int plane = nx * ny;
+  const int64_t V = (int64_t)plane * nz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f64 < V; f64 += stride) {
+    const int f = (int)f64;
+    const int z = f / plane, rem = f - z * plane;
+    const int y = rem / nx, x = rem - y * nx;
+    const int32_t own = __ldg(&L[f]);
+    int32_t c = 0;
+    double sv = 0.0;
+    for (int k0 = 0; k0 < nball; k0 += 4) {
+      int g[4];
+      int32_t lab[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u;
+        const int o = k < nball ? sofs[k] : 0;
+        const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
+                  xx = x + (int)(int8_t)o;
+        const bool ok = k < nball && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+                        (unsigned)xx < (unsigned)nx;
+        g[u] = ok ? zz * plane + yy * nx + xx : f;
+        lab[u] = ok ? __ldg(L + g[u]) : -1;
+      }
+      double iv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) iv[u] = lab[u] == own ? __ldg(I + g[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lab[u] == own) {
+          c += 1;
+          sv += iv[u];
+        }
+    }
+    Cown[f] = c;
+    Sown[f] = sv;
+    if (rho0) rho0[f] = rho(__ldg(&I[f]), sv / (double)c, poisson);
+  }
+}
+
 __global__ void k_rho0(const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
                        const double *__restrict__ I, int64_t V, int poisson,
                        double *__restrict__ rho0) {
@@ -339,8 +391,16 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s, double *rho0,
                   int poisson) {
-  k_ps_fields<<<grid_for(lat.V, 256), 256, 0, s>>>(L, I, lat, ball_full, nball_full, Cown, Sown);
-  if (rho0) k_rho0<<<grid_for(lat.V, 256), 256, 0, s>>>(Cown, Sown, I, lat.V, poisson, rho0);
+  if (lat.V < ((int64_t)1 << 31) && nball_full <= 1024) {
+    int64_t g = (lat.V + 255) / 256;
+    if (g > 148 * 64) g = 148 * 64;
+    k_ps_fields32<<<(unsigned)(g < 1 ? 1 : g), 256, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny,
+                                                          (int)lat.nz, ball_full, nball_full, Cown,
+                                                          Sown, rho0, poisson);
+  } else {
+    k_ps_fields<<<grid_for(lat.V, 256), 256, 0, s>>>(L, I, lat, ball_full, nball_full, Cown, Sown);
+    if (rho0) k_rho0<<<grid_for(lat.V, 256), 256, 0, s>>>(Cown, Sown, I, lat.V, poisson, rho0);
+  }
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
