@@ -33,23 +33,32 @@ __global__ void k_rank(const double *__restrict__ base, const int32_t *__restric
   if ((threadIdx.x & 31) == 0 && m) atomicAdd(nneg, (unsigned long long)__popc(m));
 }
 
-// Runs of equal rank keys (rare: exact ties of the rank value) are put in
-// (tie key, particle index) order after the single stable sort by rank key,
-// which leaves each run in particle order.  Short runs: insertion sort by the
-// thread that finds the run; long runs (degenerate inputs): a block bitonic
-// sort in shared memory, or for runs beyond its capacity a serial sort.
+// The radix sort orders by the top 32 bits of the rank key only (4 digit
+// passes instead of 8: sign, exponent and 20 mantissa bits, so keys that
+// share them are rare -- equal to ~1e-6 relative).  Each run of equal top
+// halves, left in particle order by the stable sort, is then put in (full
+// rank key, tie key, particle index) order -- the complete lexsort order.
+// Short runs: insertion sort by the thread that finds the run; long runs
+// (degenerate inputs, e.g. exact ties): a block bitonic sort in shared
+// memory, or for runs beyond its capacity a serial sort.
 static constexpr int kShortRun = 32, kBitonic = 4096;
 
 __device__ __forceinline__ bool tie_less(const uint64_t *tie, uint32_t p, uint32_t q) {
   const uint64_t a = tie[p], b = tie[q];
   return a < b || (a == b && p < q);
 }
+__device__ __forceinline__ bool rank_less(const uint64_t *rkey, const uint64_t *tie, uint32_t p,
+                                          uint32_t q) {
+  const uint64_t a = rkey[p], b = rkey[q];
+  return a < b || (a == b && tie_less(tie, p, q));
+}
 
-__device__ void insertion_by_tie(uint32_t *o, int64_t len, const uint64_t *tie) {
+__device__ void insertion_by_tie(uint32_t *o, int64_t len, const uint64_t *rkey,
+                                 const uint64_t *tie) {
   for (int64_t i = 1; i < len; ++i) {
     const uint32_t v = o[i];
     int64_t j = i - 1;
-    while (j >= 0 && tie_less(tie, v, o[j])) {
+    while (j >= 0 && rank_less(rkey, tie, v, o[j])) {
       o[j + 1] = o[j];
       --j;
     }
@@ -58,19 +67,19 @@ __device__ void insertion_by_tie(uint32_t *o, int64_t len, const uint64_t *tie) 
 }
 
 __global__ void k_tie_runs(const uint64_t *__restrict__ key, int64_t n, uint32_t *__restrict__ order,
-                           const uint64_t *__restrict__ tie, int64_t *__restrict__ longs,
-                           unsigned long long *__restrict__ nlong) {
+                           const uint64_t *__restrict__ rkey, const uint64_t *__restrict__ tie,
+                           int64_t *__restrict__ longs, unsigned long long *__restrict__ nlong) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t k = key[i];
-  if (k == ~0ull) return;                     // non-negative ranks: never executed
-  if (i > 0 && key[i - 1] == k) return;       // not a run start
-  if (i + 1 >= n || key[i + 1] != k) return;  // run of one
+  const uint32_t k = (uint32_t)(key[i] >> 32);  // the sorted half
+  if (k == 0xffffffffu) return;                          // non-negative ranks: never executed
+  if (i > 0 && (uint32_t)(key[i - 1] >> 32) == k) return;  // not a run start
+  if (i + 1 >= n || (uint32_t)(key[i + 1] >> 32) != k) return;  // run of one
   int64_t e = i + 1;
-  while (e < n && key[e] == k) ++e;
+  while (e < n && (uint32_t)(key[e] >> 32) == k) ++e;
   const int64_t len = e - i;
   if (len <= kShortRun) {
-    insertion_by_tie(order + i, len, tie);
+    insertion_by_tie(order + i, len, rkey, tie);
   } else {
     const unsigned long long slot = atomicAdd(nlong, 1ull);
     longs[2 * slot] = i;
@@ -79,6 +88,7 @@ __global__ void k_tie_runs(const uint64_t *__restrict__ key, int64_t n, uint32_t
 }
 
 __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order,
+                                                    const uint64_t *__restrict__ rkey,
                                                     const uint64_t *__restrict__ tie,
                                                     const int64_t *__restrict__ longs,
                                                     const unsigned long long *__restrict__ nlong) {
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order
     const int64_t start = longs[2 * r], len = longs[2 * r + 1];
     uint32_t *o = order + start;
     if (len > kBitonic) {
-      if (threadIdx.x == 0) insertion_by_tie(o, len, tie);
+      if (threadIdx.x == 0) insertion_by_tie(o, len, rkey, tie);
       __syncthreads();
       continue;
     }
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order
     while (m < len) m <<= 1;
     for (int t = threadIdx.x; t < m; t += blockDim.x) {
       sv[t] = t < len ? o[t] : 0xffffffffu;
-      sk[t] = t < len ? tie[sv[t]] : ~0ull;
+      sk[t] = t < len ? rkey[sv[t]] : ~0ull;
     }
     __syncthreads();
     for (int size = 2; size <= m; size <<= 1)
@@ -106,7 +116,13 @@ __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order
           const int u = t ^ stride;
           if (u > t) {
             const bool up = (t & size) == 0;
-            const bool gt = sk[t] > sk[u] || (sk[t] == sk[u] && sv[t] > sv[u]);
+            // (full rank key, tie key, particle); padding (sv = ~0) last
+            const bool gt =
+                sk[t] > sk[u] ||
+                (sk[t] == sk[u] &&
+                 (sv[t] == 0xffffffffu ? sv[u] != 0xffffffffu
+                  : sv[u] == 0xffffffffu ? false
+                                         : tie_less(tie, sv[u], sv[t])));
             if (gt == up) {
               const uint64_t tk = sk[t];
               sk[t] = sk[u];
@@ -140,16 +156,17 @@ int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t 
   // one stable sort by rank key from particle (x, comp) order
   size_t b = 0;
   RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, sc.rkey.p, sc.rkey2.p, sc.idx.p, order, n,
-                                           0, 64, s));
+                                           32, 64, s));
   RCB_TRY(sc.tmp.reserve(b, s));
   RCB_CUDA(cub::DeviceRadixSort::SortPairs(sc.tmp.p, b, sc.rkey.p, sc.rkey2.p, sc.idx.p, order, n,
-                                           0, 64, s));
+                                           32, 64, s));
   // equal rank values: (tie key, particle) order, as lexsort's next keys
   unsigned long long *nlong = reinterpret_cast<unsigned long long *>(sc.tie2.p + n);
   RCB_CUDA(cudaMemsetAsync(nlong, 0, sizeof(unsigned long long), s));
   int64_t *longs = reinterpret_cast<int64_t *>(sc.tie2.p);
-  k_tie_runs<<<grid_for(n, 256), 256, 0, s>>>(sc.rkey2.p, n, order, sc.tie.p, longs, nlong);
-  k_long_runs<<<64, 1024, 0, s>>>(order, sc.tie.p, longs, nlong);
+  k_tie_runs<<<grid_for(n, 256), 256, 0, s>>>(sc.rkey2.p, n, order, sc.rkey.p, sc.tie.p, longs,
+                                               nlong);
+  k_long_runs<<<64, 1024, 0, s>>>(order, sc.rkey.p, sc.tie.p, longs, nlong);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
