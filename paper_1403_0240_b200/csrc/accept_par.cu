@@ -3334,24 +3334,26 @@ __global__ void __launch_bounds__(32 * kPsWarps) k_ps_dtot2d(
 // Flip index of the kept moves: sites sorted ascending (row-major), per
 // lattice row [start, end) into the sorted list; used by k_ps_dtot.
 __global__ void k_flip_keys(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
-                            int64_t cap, uint32_t *__restrict__ key, int32_t *__restrict__ val) {
+                            int64_t cap, uint32_t *__restrict__ key, int32_t *__restrict__ val,
+                            uint32_t sentinel) {
   const int64_t n = *moves;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += stride) {
-    key[k] = k < n ? (uint32_t)acc[3 * k] : 0xffffffffu;
+    key[k] = k < n ? (uint32_t)acc[3 * k] : sentinel;
     val[k] = (int32_t)k;
   }
 }
 
 __global__ void k_flip_rows(const uint32_t *__restrict__ key, int64_t cap, int64_t nx,
-                            int32_t *__restrict__ start, int32_t *__restrict__ end) {
+                            int32_t *__restrict__ start, int32_t *__restrict__ end,
+                            uint32_t sentinel) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += stride) {
     const uint32_t sgl = key[i];
-    if (sgl == 0xffffffffu) continue;
+    if (sgl == sentinel) continue;
     const int64_t r = (int64_t)sgl / nx;
     if (i == 0 || (int64_t)key[i - 1] / nx != r) start[r] = (int32_t)i;
-    if (i == cap - 1 || key[i + 1] == 0xffffffffu || (int64_t)key[i + 1] / nx != r)
+    if (i == cap - 1 || key[i + 1] == sentinel || (int64_t)key[i + 1] / nx != r)
       end[r] = (int32_t)(i + 1);
   }
 }
@@ -3862,16 +3864,22 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_TRY(X.labpos->reserve(N, s));
     RCB_TRY(X.labpos2->reserve(N, s));
     RCB_TRY(X.flrows->reserve(2 * rows, s));
-    k_flip_keys<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.evkey->p, X.labpos2->p);
+    // sites need only ceil(log2(V + 1)) bits: the sentinel (no flip) is all
+    // ones within them, so the sort runs fewer digit passes
+    int fb = 1;
+    while (fb < 32 && ((int64_t)1 << fb) <= A.lat.V) ++fb;
+    const uint32_t fsent = fb >= 32 ? 0xffffffffu : (uint32_t)((1ull << fb) - 1);
+    k_flip_keys<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.evkey->p, X.labpos2->p,
+                                                 fsent);
     size_t b4 = 0;
     RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
-                                             X.labpos->p, N, 0, 32, s));
+                                             X.labpos->p, N, 0, fb, s));
     RCB_TRY(X.tmp->reserve(b4, s));
     RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
-                                             X.labpos->p, N, 0, 32, s));
+                                             X.labpos->p, N, 0, fb, s));
     RCB_CUDA(cudaMemsetAsync(X.flrows->p, 0, sizeof(int32_t) * 2 * rows, s));
     k_flip_rows<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, N, A.lat.nx, X.flrows->p,
-                                                 X.flrows->p + rows);
+                                                 X.flrows->p + rows, fsent);
     const int ipl = (X.nball + 1 + 31) / 32;
     if (A.lat.ndim == 2 && ipl <= 4) {
       const int nbk = (int)((A.lat.nx + kColB - 1) / kColB) + 1;
