@@ -293,6 +293,75 @@ __device__ __forceinline__ int window_pieces_3d(const View &v, const Lat &lat, i
   return 0;
 }
 
+// Warp-parallel window_verdict_bits<4> for 3-D (9^3 window): lane k < 9
+// holds plane k as a u128 (81 cells) and one flood step is a 2-D 8-neighbour
+// dilation per plane plus the neighbouring planes' dilations by shuffles, so
+// the floods run 9 planes at a time instead of on one thread.  Same pieces,
+// same order of seed components, same verdicts (1 / 2 / 0) as the serial
+// window_verdict_bits<4>(bits, 9).
+__device__ __noinline__ int warp_window_verdict3(const uint32_t *bits) {
+  typedef unsigned __int128 u128;
+  constexpr int R = 4, W = 9, PL = 81, NZ = 9;
+  const int lane = threadIdx.x & 31;
+  const u128 one = 1;
+  const u128 full = (one << PL) - 1;
+  u128 col0 = 0, colW = 0;
+  for (int r = 0; r < W; ++r) {
+    col0 |= one << (r * W);
+    colW |= one << (r * W + W - 1);
+  }
+  const u128 rim = col0 | colW | ((one << W) - 1) | (((one << W) - 1) << (PL - W));
+  u128 cells = 0, seeds = 0;
+  if (lane < NZ) {
+    for (int q = 0; q < PL; ++q) {
+      const int c = lane * PL + q;
+      if ((bits[c >> 5] >> (c & 31)) & 1u) cells |= one << q;
+    }
+    if (lane >= R - 1 && lane <= R + 1)
+      for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj) seeds |= one << ((R + di) * W + R + dj);
+    seeds &= cells;
+  }
+  auto d2 = [&](u128 p) -> u128 {
+    const u128 l = p & ~col0, h = p & ~colW;
+    return (p | (h << 1) | (l >> 1) | (p << W) | (p >> W) | (h << (W + 1)) | (l << (W - 1)) |
+            (h >> (W - 1)) | (l >> (W + 1))) &
+           full;
+  };
+  auto shfl128 = [&](u128 v, int src) -> u128 {
+    const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+    const unsigned long long a = __shfl_sync(0xffffffffu, lo, src & 31);
+    const unsigned long long b = __shfl_sync(0xffffffffu, hi, src & 31);
+    return ((u128)b << 64) | a;
+  };
+  u128 rest = seeds;
+  bool first = true;
+  for (;;) {
+    const unsigned live = __ballot_sync(0xffffffffu, lane < NZ && rest != 0);
+    if (!live) return 0;
+    const int k0 = __ffs(live) - 1;
+    u128 comp = lane == k0 ? (rest & (~rest + 1)) : (u128)0;
+    for (;;) {  // flood comp through cells (26-connectivity)
+      const u128 dn = lane < NZ ? d2(comp) : (u128)0;
+      const u128 up = shfl128(dn, lane - 1), dw = shfl128(dn, lane + 1);
+      u128 n = dn;
+      if (lane > 0) n |= up;
+      if (lane + 1 < NZ) n |= dw;
+      n = lane < NZ ? (n & cells) : (u128)0;
+      const bool grew = __any_sync(0xffffffffu, n != comp);
+      comp = n;
+      if (!grew) break;
+    }
+    const bool all = !__any_sync(0xffffffffu, lane < NZ && (rest & ~comp) != 0);
+    rest &= ~comp;
+    if (first && all) return 1;
+    first = false;
+    const bool touch = __any_sync(
+        0xffffffffu, lane < NZ && comp != 0 && (lane == 0 || lane == NZ - 1 || (comp & rim) != 0));
+    if (!touch) return 2;
+  }
+}
+
 // Third-tier exact window test, radius R (3-D: 9^3 cells for R = 4; 2-D:
 // 11^2 for R = 5).  Each z-plane of the window is one 128-bit mask
 // (W^2 <= 121 bits); 26-connectivity dilation is the in-plane 8-neighbour
@@ -2643,10 +2712,21 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         }
       }
       __syncwarp();
-      if (lane == 0) {
+      if (is3) {  // warp-parallel floods (the serial one is ~100 us on one lane)
+        uint32_t any_u = 0;
+        for (int q = lane; q < (nb + 31) / 32; q += 32) any_u |= unk[q];
+        any_u = __any_sync(0xffffffffu, any_u != 0);
+        int r = warp_window_verdict3(bits);
+        if (r != 1 && any_u) {
+          __syncwarp();
+          for (int q = lane; q < (nb + 31) / 32; q += 32) bits[q] |= unk[q];
+          __syncwarp();
+          r = warp_window_verdict3(bits) == 2 ? 2 : 0;
+        }
+        if (lane == 0) S.result = r;
+      } else if (lane == 0) {
         auto verdict = [&](const uint32_t *bb) {
-          return is3 ? window_verdict_bits<4>(bb, WB)
-                 : RB == 3 ? window_verdict_bits<3>(bb, 1)
+          return RB == 3 ? window_verdict_bits<3>(bb, 1)
                  : RB == 1 ? 0
                            : window_verdict_bits<5>(bb, 1);
         };
