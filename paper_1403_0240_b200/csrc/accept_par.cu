@@ -1574,8 +1574,13 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
       }
       __syncwarp();
       int ok = 0;
-      if (lane == 0) ok = (is3 ? window_verdict_bits<4>(qbits, WB) : window_verdict_bits<5>(qbits, 1)) == 1;
-      need_uf = !__shfl_sync(0xffffffffu, ok, 0);
+      if (is3) {
+        ok = warp_window_verdict3(qbits) == 1;
+      } else {
+        if (lane == 0) ok = window_verdict_bits<5>(qbits, 1) == 1;
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+      }
+      need_uf = !ok;
       __syncwarp();
     }
     if (lane == 0 && need_uf) atomicAdd(A.ctl + C_MAXLEV, 1);  // diagnostics: scan invalidations
