@@ -1336,10 +1336,16 @@ __device__ bool warp_help(const ParArgs &A) {
       const int64_t y = (zz * lat.ny + yy) * lat.nx + x;
       if (y == f || v.lab(y) != a || (S && is_q(A, y, a, S))) continue;
       // backward half of the full neighbourhood: every edge once (the job box
-      // contains every a-site, so edges to sites outside it never join a-sites)
+      // contains every a-site, so edges to sites outside it never join a-sites).
+      // If the x-predecessor is a member, its own edges already join every
+      // backward neighbour with dx <= 0 (each is a backward neighbour of it,
+      // or of the run's first member), so only the dx = +1 ones and the
+      // predecessor itself remain (5 unions instead of 13 inside runs).
+      const bool pred = x > 0 && y - 1 != f && v.lab(y - 1) == a && !(S && is_q(A, y - 1, a, S));
       for (int k = 0; k < 13; ++k) {
         const int dz = k / 9 - 1, dy = (k / 3) % 3 - 1, dx = k % 3 - 1;  // lexicographically < 0
         if (lat.ndim == 2 && dz != 0) continue;
+        if (pred && dx != 1 && k != 12) continue;
         const int64_t z2 = zz + dz, y2 = yy + dy, x2 = x + dx;
         if (!lat.inb(z2, y2, x2)) continue;
         const int64_t g = (z2 * lat.ny + y2) * lat.nx + x2;
