@@ -240,7 +240,7 @@ struct rcb_engine {
 
   int32_t flush_stats() {  // make tot / tsq current (replay deferred chains)
     if (pending.empty()) return RCB_OK;
-    return replay_chains(pending, nullptr, tot.p, tsq.p, s);
+    return replay_chains(pending, I.p, tot.p, tsq.p, s);
   }
 
   int32_t refresh() {  // energy.py:285-291

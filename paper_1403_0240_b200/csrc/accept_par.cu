@@ -3797,25 +3797,90 @@ struct StageTimer {
   }
 };
 
-int32_t replay_chains(std::vector<PendingChain> &pending, const int64_t *, double *tot,
+int32_t replay_chains(std::vector<PendingChain> &pending, const double *I, double *tot,
                       double *tsq, cudaStream_t s) {
   ParArgs A{};  // the sum chains read only their event lists
-  for (PendingChain &pc : pending) {
-    const int64_t *st = pc.bounds.p, *en = pc.bounds.p + pc.nl;
-    A.nl = pc.nl;
-    k_label_chain<<<2 * pc.nl, 512, 0, s>>>(A, pc.evval.p, pc.evv.p, st, en, tot, tsq, nullptr,
-                                            nullptr, 2);
-    RCB_CUDA(cudaGetLastError());
-  }
+  DBuf<uint32_t> evkey, evkey2, evval, evval2;
+  DBuf<int64_t> bounds;
+  DBuf<double> evv;
+  DBuf<uint8_t> tmp;
+  int32_t rc = RCB_OK;
+  auto run = [&]() -> int32_t {
+    for (PendingChain &pc : pending) {
+      const int64_t cap = pc.cap;
+      A.nl = pc.nl;
+      RCB_TRY(evkey.reserve(2 * cap, s));
+      RCB_TRY(evkey2.reserve(2 * cap, s));
+      RCB_TRY(evval.reserve(2 * cap, s));
+      RCB_TRY(evval2.reserve(2 * cap, s));
+      RCB_TRY(evv.reserve(2 * cap, s));
+      RCB_TRY(bounds.reserve(2 * (size_t)pc.nl, s));
+      k_events<<<grid_for(cap, 256), 256, 0, s>>>(pc.acc.p, pc.moves.p, cap, pc.nl, evkey.p, evval.p);
+      int end_bit = 1;
+      while (end_bit < 32 && ((int64_t)1 << end_bit) <= pc.nl) ++end_bit;
+      size_t b2 = 0;
+      RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, evkey.p, evkey2.p, evval.p, evval2.p,
+                                               2 * cap, 0, end_bit, s));
+      RCB_TRY(tmp.reserve(b2, s));
+      RCB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, b2, evkey.p, evkey2.p, evval.p, evval2.p,
+                                               2 * cap, 0, end_bit, s));
+      int64_t *st = bounds.p, *en = bounds.p + pc.nl;
+      RCB_CUDA(cudaMemsetAsync(st, 0, sizeof(int64_t) * pc.nl, s));
+      RCB_CUDA(cudaMemsetAsync(en, 0, sizeof(int64_t) * pc.nl, s));
+      k_label_bounds<<<grid_for(2 * cap, 256), 256, 0, s>>>(evkey2.p, 2 * cap, pc.nl, st, en);
+      k_event_vals<<<grid_for(2 * cap, 256), 256, 0, s>>>(pc.acc.p, evval2.p, evkey2.p, 2 * cap,
+                                                          pc.nl, I, evv.p);
+      k_label_chain<<<2 * pc.nl, 512, 0, s>>>(A, evval2.p, evv.p, st, en, tot, tsq, nullptr,
+                                              nullptr, 2);
+      RCB_CUDA(cudaGetLastError());
+    }
+    return RCB_OK;
+  };
+  rc = run();
+  evkey.release(s); evkey2.release(s); evval.release(s); evval2.release(s);
+  bounds.release(s); evv.release(s); tmp.release(s);
   drop_chains(pending, s);
-  return RCB_OK;
+  return rc;
+}
+
+// PS: per-label counts after the accepted moves (integer: any order), block
+// histograms in shared memory for nl <= 4096
+__global__ void k_count_moves(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                              int64_t *__restrict__ cnt, int32_t nl) {
+  __shared__ long long h[4096];
+  const int64_t n = *moves;
+  const bool sm = nl <= 4096;
+  if (sm) {
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) h[l] = 0;
+    __syncthreads();
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const int32_t a = (int32_t)acc[3 * k + 1], b = (int32_t)acc[3 * k + 2];
+    if (sm) {
+      atomicAdd((unsigned long long *)&h[a], (unsigned long long)(-1ll));
+      atomicAdd((unsigned long long *)&h[b], 1ull);
+    } else {
+      atomicAdd((unsigned long long *)&cnt[a], (unsigned long long)(-1ll));
+      atomicAdd((unsigned long long *)&cnt[b], 1ull);
+    }
+  }
+  if (sm) {
+    __syncthreads();
+    for (int l = threadIdx.x; l < nl; l += blockDim.x)
+      if (h[l]) atomicAdd((unsigned long long *)&cnt[l], (unsigned long long)h[l]);
+  }
+}
+
+__global__ void k_vanished(const int64_t *__restrict__ cnt, int32_t nl, int32_t *__restrict__ ncomp) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nl; l += gridDim.x * blockDim.x)
+    if (l > 0 && cnt[l] == 0) ncomp[l] = 0;
 }
 
 void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s) {
   for (PendingChain &pc : pending) {
-    pc.evval.release(s);
-    pc.evv.release(s);
-    pc.bounds.release(s);
+    pc.acc.release(s);
+    pc.moves.release(s);
   }
   pending.clear();
 }
@@ -4005,7 +4070,28 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   }
   T.mark("ps-dtot");
   // per-label chains (stats + pre-move snapshots), PC increments, ordered ledger
-  {
+  if (X.region_ps && X.pending) {
+    // counts now (vanish tests, small labels): cnt0 + sum of +-1 over the
+    // moves, integers in any order; the total / total_sq chains are replayed
+    // from the saved move list when the statistics are read
+    const int64_t cap = N;
+    RCB_CUDA(cudaMemcpyAsync(A.cnt, A.cnt0, sizeof(int64_t) * A.nl, cudaMemcpyDeviceToDevice, s));
+    k_count_moves<<<148 * 2, 256, 0, s>>>(X.acc, X.moves, A.cnt, A.nl);
+    k_vanished<<<grid_for(A.nl, 256), 256, 0, s>>>(A.cnt, A.nl, X.ncomp);
+    X.pending->emplace_back();
+    PendingChain &pc = X.pending->back();
+    RCB_TRY(pc.acc.reserve(3 * cap, s));
+    RCB_TRY(pc.moves.reserve(1, s));
+    RCB_CUDA(cudaMemcpyAsync(pc.acc.p, X.acc, sizeof(int64_t) * 3 * cap, cudaMemcpyDeviceToDevice, s));
+    RCB_CUDA(cudaMemcpyAsync(pc.moves.p, X.moves, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    pc.cap = cap;
+    pc.nl = A.nl;
+    if (X.pending->size() > 16) RCB_TRY(replay_chains(*X.pending, X.I, X.tot, X.tsq, s));
+    T.mark("chains");
+    if (!band_ledger) k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
+    T.mark("ledger");
+    nl += 4;
+  } else {
     const int64_t cap = N;
     RCB_TRY(X.evkey->reserve(2 * cap, s));
     RCB_TRY(X.evkey2->reserve(2 * cap, s));
@@ -4029,21 +4115,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_TRY(X.evv->reserve(2 * cap, s));
     k_event_vals<<<grid_for(2 * cap, 256), 256, 0, s>>>(X.acc, X.evval2->p, X.evkey2->p, 2 * cap,
                                                         A.nl, X.I, X.evv->p);
-    if (X.region_ps && X.pending) {
-      // counts now (vanish tests, small labels); the sums when read
-      k_label_chain<<<A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq, nullptr,
-                                         X.ncomp, 1);
-      X.pending->emplace_back();
-      PendingChain &pc = X.pending->back();
-      std::swap(pc.evval, *X.evval2);
-      std::swap(pc.evv, *X.evv);
-      std::swap(pc.bounds, *X.bounds);
-      pc.nl = A.nl;
-      if (X.pending->size() > 16) RCB_TRY(replay_chains(*X.pending, nullptr, X.tot, X.tsq, s));
-    } else {
-      k_label_chain<<<3 * A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq,
-                                             X.snap->p, X.ncomp);
-    }
+    k_label_chain<<<3 * A.nl, 512, 0, s>>>(A, X.evval2->p, X.evv->p, st, en, X.tot, X.tsq,
+                                           X.snap->p, X.ncomp);
     if (!X.region_ps)
       k_pc_dtot<<<grid_for(cap, 256), 256, 0, s>>>(A, X.acc, X.moves, X.I, X.snap->p, X.poisson,
                                                    X.lam, X.dtot);

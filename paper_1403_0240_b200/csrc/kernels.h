@@ -127,9 +127,9 @@ struct ParArgs {
 // sequential kernel read them; the next resync rebuilds them from the raster)
 // are replayed lazily from the saved event lists, in iteration order.
 struct PendingChain {
-  DBuf<uint32_t> evval;
-  DBuf<double> evv;
-  DBuf<int64_t> bounds;
+  DBuf<int64_t> acc;    // the iteration's accepted moves (x, a, b), acceptance order
+  DBuf<int64_t> moves;  // their count (device scalar)
+  int64_t cap = 0;
   int32_t nl = 0;
 };
 
@@ -246,7 +246,7 @@ int32_t label_components(const int32_t *L, const Lat &lat, int full_fg, int32_t 
 // accept_par.cu
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches);
 // replay (then release) deferred total / total_sq chains in order
-int32_t replay_chains(std::vector<PendingChain> &pending, const int64_t *cnt0_unused, double *tot,
+int32_t replay_chains(std::vector<PendingChain> &pending, const double *I, double *tot,
                       double *tsq, cudaStream_t s);
 void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s);
 size_t accept_par_smem();
