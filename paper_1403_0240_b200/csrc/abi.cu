@@ -178,7 +178,7 @@ struct rcb_engine {
   Scalars *hsc = nullptr;  // pinned
   cudaEvent_t ev[6] = {};
   cudaEvent_t ev_acc[2] = {};
-  int32_t hctl[16] = {};
+  int32_t *hctl = nullptr;  // pinned (in the pinned block): acceptance counters read back
   int64_t counters[12] = {};
   bool last_par = false;
   float times[6] = {};
@@ -415,6 +415,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   e->hsc = reinterpret_cast<Scalars *>(e->pinned);
   e->hoff = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(e->pinned) + 2048);
   e->hwatch = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(e->pinned) + 3072);
+  e->hctl = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(e->pinned) + 3584);
+  memset(e->hctl, 0, 16 * sizeof(int32_t));
   memset(e->hsc, 0, sizeof(Scalars));
 
   memset(e->hwatch, 0, 8 * sizeof(unsigned long long));
@@ -511,7 +513,9 @@ static int32_t plane_ranges(rcb_engine *e, const int64_t *planes, int k, int64_t
 // filter (K6).  With a slab [slab_lo, slab_hi) set, ΔE is computed for the
 // slab's particles plus a halo of the stencil's reach (the particles K6 reads)
 // and K6 for the slab's particles only; every other array stays replicated.
+static std::chrono::steady_clock::time_point g_host_t0;
 static int32_t engine_score(rcb_engine *e) {
+  g_host_t0 = std::chrono::steady_clock::now();
   RCB_CUDA(cudaSetDevice(e->device));
   cudaStream_t s = e->s;
   e->iteration += 1;
@@ -876,6 +880,11 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
                            cudaMemcpyDeviceToDevice, s));
   cudaEventRecord(e->ev[5], s);
   RCB_CUDA(cudaMemcpyAsync(e->hsc, d, offsetof(Scalars, limbs), cudaMemcpyDeviceToHost, s));
+  if (getenv("RCB_HOST_LOG")) {  // host time to enqueue the iteration (vs its device time)
+    const double hu = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() -
+                                                                 g_host_t0).count();
+    fprintf(stderr, "[rcb-host] enqueue %.1f us\n", hu);
+  }
   RCB_CUDA(cudaStreamSynchronize(s));
   if (e->hwatch[0]) {  // the dataflow acceptance's watchdog fired (accept_par.cu)
     const unsigned long long w0 = e->hwatch[0];

@@ -3941,8 +3941,24 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       A.bigmap = nullptr;
     }
     {
-      const uint32_t bits = (uint32_t)A.wp_bits;
-      RCB_CUDA(cudaMemcpyToSymbolAsync(c_wp_bits, &bits, sizeof(bits), 0, cudaMemcpyHostToDevice, s));
+      // from pinned memory, and only when the layout changes: a copy from a
+      // pageable stack variable is staged synchronously, which held the host
+      // until the stream had drained -- the iteration's remaining launches
+      // then trickled in behind the GPU (host enqueue time == device time)
+      static uint32_t *hbits = nullptr;
+      static int last_bits = -1, last_dev = -1;
+      int dev = 0;
+      RCB_CUDA(cudaGetDevice(&dev));
+      if (!hbits) RCB_CUDA(cudaMallocHost((void **)&hbits, sizeof(uint32_t)));
+      if (A.wp_bits != last_bits || dev != last_dev) {
+        RCB_CUDA(cudaStreamSynchronize(s));  // no earlier run still reads the old layout
+        *hbits = (uint32_t)A.wp_bits;
+        RCB_CUDA(cudaMemcpyToSymbolAsync(c_wp_bits, hbits, sizeof(uint32_t), 0,
+                                         cudaMemcpyHostToDevice, s));
+        RCB_CUDA(cudaStreamSynchronize(s));
+        last_bits = A.wp_bits;
+        last_dev = dev;
+      }
     }
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
