@@ -3855,12 +3855,23 @@ __global__ void k_count_moves(const int64_t *__restrict__ acc, const int64_t *__
     __syncthreads();
   }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
-    const int32_t a = (int32_t)acc[3 * k + 1], b = (int32_t)acc[3 * k + 2];
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    // warp-uniform: lanes with the same label add once (labels repeat a lot:
+    // the background takes part in most moves)
+    const int64_t k = base + threadIdx.x;
+    const bool in = k < n;
+    const int32_t a = in ? (int32_t)acc[3 * k + 1] : -1, b = in ? (int32_t)acc[3 * k + 2] : -1;
     if (sm) {
-      atomicAdd((unsigned long long *)&h[a], (unsigned long long)(-1ll));
-      atomicAdd((unsigned long long *)&h[b], 1ull);
-    } else {
+      const unsigned ga = __match_any_sync(0xffffffffu, a), gb = __match_any_sync(0xffffffffu, b);
+      if (in && lane == __ffs(ga) - 1)
+        atomicAdd((unsigned long long *)&h[a], (unsigned long long)(-(long long)__popc(ga)));
+      if (in && lane == __ffs(gb) - 1)
+        atomicAdd((unsigned long long *)&h[b], (unsigned long long)(long long)__popc(gb));
+      continue;
+    }
+    if (!in) continue;
+    {
       atomicAdd((unsigned long long *)&cnt[a], (unsigned long long)(-1ll));
       atomicAdd((unsigned long long *)&cnt[b], 1ull);
     }
