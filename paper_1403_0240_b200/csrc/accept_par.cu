@@ -1682,17 +1682,22 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
                                                                 int32_t pos) {
   int ns = 32;
   unsigned long long v = 0;
-  const unsigned long long t0 = gtimer();
+  unsigned long long t0 = 0;
+  int polls = 0;
   for (;;) {
     if (g >= 0) v = ld_rlx64(A.wp + g);
     const bool p = g >= 0 && wp_pend(v) < pos;
     if (!__any_sync(0xffffffffu, p)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
-      if (ns < 512) ns <<= 1;
-      const unsigned bal = __ballot_sync(0xffffffffu, p);
-      const long long gs = __shfl_sync(0xffffffffu, g, bal ? __ffs(bal) - 1 : 0);
-      if (df_watch(A, t0, pos, 1, gs)) break;
+      if (ns < 256) ns <<= 1;
+      // the watchdog looks only every 64 idle polls (the common wait is short)
+      if ((++polls & 63) == 0) {
+        if (polls == 64) t0 = gtimer();
+        const unsigned bal = __ballot_sync(0xffffffffu, p);
+        const long long gs = __shfl_sync(0xffffffffu, g, bal ? __ffs(bal) - 1 : 0);
+        if (df_watch(A, t0, pos, 1, gs)) break;
+      }
     }
   }
   return v;
@@ -4157,7 +4162,10 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
-    if (A.lat.V < ((int64_t)1 << 31) && X.nball_full <= kRfMaxBall && (X.rho0 || !band_ledger))
+    if (!band_ledger && fields_tile2d_ok(A.lat, X.radius, X.nball_full))
+      RCB_TRY(fields_tile2d(X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius, X.dirty,
+                            X.Cown, X.Sown, X.rho0, X.poisson, s));
+    else if (A.lat.V < ((int64_t)1 << 31) && X.nball_full <= kRfMaxBall && (X.rho0 || !band_ledger))
       k_refield_band32<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
           X.Lmut, X.I, (int)A.lat.nx, (int)A.lat.ny, (int)A.lat.nz, X.ball_full, X.nball_full,
           X.dirty, X.Cown, X.Sown, X.rho0, X.poisson, band_ledger ? X.band : nullptr);

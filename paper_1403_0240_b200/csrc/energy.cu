@@ -1,3 +1,4 @@
+#include <vector>
 #include <climits>
 #include <cstring>
 // Energy kernels: K2 region statistics, K3 PC increment + perimeter change,
@@ -111,6 +112,72 @@ __global__ void __launch_bounds__(256) k_ps_fields32(
     Sown[f] = sv;
     if (rho0) rho0[f] = rho(__ldg(&I[f]), sv / (double)c, poisson);
   }
+}
+
+// 2-D own-label fields on 32 x 8 site tiles staged in shared memory with a
+// halo of R: every ball walk reads labels and intensities from the tile, in
+// the same ball order as the global-memory kernels (bit-identical fields).
+// dirty == nullptr: every site (the rebuild); else only the dirty sites,
+// which are cleared (the band refresh, 2-D).
+static constexpr int kTW = 32, kTH = 8, kTRmax = 15;
+__global__ void __launch_bounds__(256) k_fields_tile2d(
+    const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny,
+    const Off *__restrict__ ball, int nball, int R, uint8_t *__restrict__ dirty,
+    int32_t *__restrict__ Cown, double *__restrict__ Sown, double *__restrict__ rho0, int poisson) {
+  constexpr int SH = kTH + 2 * kTRmax, SW = kTW + 2 * kTRmax;
+  __shared__ int32_t sL[SH * SW];
+  __shared__ double sI[SH * SW];
+  __shared__ int sofs[1024];
+  const int tx = threadIdx.x & (kTW - 1), ty = threadIdx.x / kTW;
+  const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool inside = x < nx && y < ny;
+  const int64_t f = (int64_t)y * nx + x;
+  const bool todo = inside && (!dirty || dirty[f]);
+  if (!__syncthreads_or(todo)) return;
+  const int hw = kTW + 2 * R, hh = kTH + 2 * R;
+  for (int i = threadIdx.x; i < hw * hh; i += blockDim.x) {
+    const int hy = i / hw, hx = i - hy * hw;
+    const int gy = y0 - R + hy, gx = x0 - R + hx;
+    const bool ok = (unsigned)gy < (unsigned)ny && (unsigned)gx < (unsigned)nx;
+    const int64_t g = (int64_t)gy * nx + gx;
+    sL[hy * SW + hx] = ok ? __ldg(L + g) : -1;
+    sI[hy * SW + hx] = ok ? __ldg(I + g) : 0.0;
+  }
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = (int)ball[k].dy * SW + (int)ball[k].dx;
+  __syncthreads();
+  if (!todo) return;
+  const int cidx = (ty + R) * SW + (tx + R);
+  const int32_t own = sL[cidx];
+  int32_t c = 0;
+  double sv = 0.0;
+  for (int k = 0; k < nball; ++k) {
+    const int j = cidx + sofs[k];
+    if (sL[j] == own) {
+      c += 1;
+      sv += sI[j];
+    }
+  }
+  Cown[f] = c;
+  Sown[f] = sv;
+  if (rho0) rho0[f] = rho(sI[cidx], sv / (double)c, poisson);
+  if (dirty) dirty[f] = 0;
+}
+
+int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                      int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
+                      double *rho0, int poisson, cudaStream_t s) {
+  dim3 grid((unsigned)((lat.nx + kTW - 1) / kTW), (unsigned)((lat.ny + kTH - 1) / kTH));
+  k_fields_tile2d<<<grid, kTW * kTH, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, ball_full, nball_full,
+                                             R, dirty, Cown, Sown, rho0, poisson);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+bool fields_tile2d_ok(const Lat &lat, int R, int nball_full) {
+  return lat.ndim == 2 && R <= kTRmax && nball_full <= 1024 && lat.ny < 65536 * kTH &&
+         lat.nx < 65536 * kTW;
 }
 
 __global__ void k_rho0(const int32_t *__restrict__ Cown, const double *__restrict__ Sown,
@@ -391,6 +458,20 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s, double *rho0,
                   int poisson) {
+  int R = 0;  // the ball radius (ball_full is on the device: from its site count)
+  if (lat.ndim == 2) {
+    for (int r = 1; r <= kTRmax; ++r) {
+      int cnt = 0;
+      for (int dy = -r; dy <= r; ++dy)
+        for (int dx = -r; dx <= r; ++dx) cnt += dy * dy + dx * dx <= r * r;
+      if (cnt == nball_full) {
+        R = r;
+        break;
+      }
+    }
+  }
+  if (R > 0 && fields_tile2d_ok(lat, R, nball_full))
+    return fields_tile2d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson, s);
   if (lat.V < ((int64_t)1 << 31) && nball_full <= 1024) {
     int64_t g = (lat.V + 255) / 256;
     if (g > 148 * 64) g = 148 * 64;

@@ -188,6 +188,10 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s,
                   double *rho0 = nullptr, int poisson = 0);
+int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                      int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
+                      double *rho0, int poisson, cudaStream_t s);
+bool fields_tile2d_ok(const Lat &lat, int R, int nball_full);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
