@@ -4165,6 +4165,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (!band_ledger && fields_tile2d_ok(A.lat, X.radius, X.nball_full))
       RCB_TRY(fields_tile2d(X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius, X.dirty,
                             X.Cown, X.Sown, X.rho0, X.poisson, s));
+    else if (fields_tile3d_ok(A.lat, X.radius, X.nball_full) && (X.rho0 || !band_ledger))
+      RCB_TRY(fields_tile3d(X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius, X.dirty,
+                            X.Cown, X.Sown, X.rho0, X.poisson, band_ledger ? X.band : nullptr, s));
     else if (A.lat.V < ((int64_t)1 << 31) && X.nball_full <= kRfMaxBall && (X.rho0 || !band_ledger))
       k_refield_band32<<<grid_for(A.lat.V, 256), 256, 0, s>>>(
           X.Lmut, X.I, (int)A.lat.nx, (int)A.lat.ny, (int)A.lat.nz, X.ball_full, X.nball_full,

@@ -165,6 +165,88 @@ __global__ void __launch_bounds__(256) k_fields_tile2d(
   if (dirty) dirty[f] = 0;
 }
 
+// 3-D variant: 16 x 4 x 4 site tiles with a halo of R <= 4 (24 x 12 x 12
+// cells in shared memory), optional band ledger (the exact sum of rho_new -
+// rho_old over the refreshed sites into the superaccumulator band[]).
+static constexpr int kT3X = 16, kT3Y = 4, kT3Z = 4, kT3R = 4;
+__global__ void __launch_bounds__(256) k_fields_tile3d(
+    const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny, int nz,
+    const Off *__restrict__ ball, int nball, int R, uint8_t *__restrict__ dirty,
+    int32_t *__restrict__ Cown, double *__restrict__ Sown, double *__restrict__ rho0, int poisson,
+    long long *__restrict__ band) {
+  constexpr int SX = kT3X + 2 * kT3R, SY = kT3Y + 2 * kT3R, SZ = kT3Z + 2 * kT3R;
+  __shared__ int32_t sL[SX * SY * SZ];
+  __shared__ double sI[SX * SY * SZ];
+  __shared__ int sofs[1024];
+  __shared__ long long sm[kLimbs];
+  const int tx = threadIdx.x % kT3X, ty = (threadIdx.x / kT3X) % kT3Y, tz = threadIdx.x / (kT3X * kT3Y);
+  const int x0 = blockIdx.x * kT3X, y0 = blockIdx.y * kT3Y, z0 = blockIdx.z * kT3Z;
+  const int x = x0 + tx, y = y0 + ty, z = z0 + tz;
+  const bool inside = x < nx && y < ny && z < nz;
+  const int64_t f = ((int64_t)z * ny + y) * nx + x;
+  const bool todo = inside && (!dirty || dirty[f]);
+  if (!__syncthreads_or(todo)) return;
+  const int hx = kT3X + 2 * R, hy = kT3Y + 2 * R, hz = kT3Z + 2 * R;
+  for (int i = threadIdx.x; i < hx * hy * hz; i += blockDim.x) {
+    const int cz = i / (hx * hy), rem = i - cz * hx * hy;
+    const int cy = rem / hx, cx = rem - cy * hx;
+    const int gz = z0 - R + cz, gy = y0 - R + cy, gx = x0 - R + cx;
+    const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
+                    (unsigned)gx < (unsigned)nx;
+    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    const int si = (cz * SY + cy) * SX + cx;
+    sL[si] = ok ? __ldg(L + g) : -1;
+    sI[si] = ok ? __ldg(I + g) : 0.0;
+  }
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = ((int)ball[k].dz * SY + (int)ball[k].dy) * SX + (int)ball[k].dx;
+  if (band)
+    for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  __syncthreads();
+  double oldr = 0.0, newr = 0.0;
+  if (todo) {
+    const int cidx = ((tz + R) * SY + (ty + R)) * SX + (tx + R);
+    const int32_t own = sL[cidx];
+    int32_t c = 0;
+    double sv = 0.0;
+    for (int k = 0; k < nball; ++k) {
+      const int j = cidx + sofs[k];
+      if (sL[j] == own) {
+        c += 1;
+        sv += sI[j];
+      }
+    }
+    if (band) oldr = rho0[f];
+    Cown[f] = c;
+    Sown[f] = sv;
+    newr = rho(sI[cidx], sv / (double)c, poisson);
+    if (rho0) rho0[f] = newr;
+    if (dirty) dirty[f] = 0;
+  }
+  if (band) {  // every thread of the block reaches here (warp-uniform)
+    acc_add_warp(sm, -oldr, todo);
+    acc_add_warp(sm, newr, todo);
+    acc_flush(sm, band);
+  }
+}
+
+int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                      int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
+                      double *rho0, int poisson, long long *band, cudaStream_t s) {
+  dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
+            (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
+  k_fields_tile3d<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, (int)lat.nz,
+                                                       ball_full, nball_full, R, dirty, Cown, Sown,
+                                                       rho0, poisson, band);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+bool fields_tile3d_ok(const Lat &lat, int R, int nball_full) {
+  return lat.ndim == 3 && R <= kT3R && nball_full <= 1024 && (lat.nz + kT3Z - 1) / kT3Z < 65536 &&
+         (lat.ny + kT3Y - 1) / kT3Y < 65536;
+}
+
 int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, cudaStream_t s) {
@@ -469,6 +551,21 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
         break;
       }
     }
+  }
+  if (lat.ndim == 3) {
+    for (int r = 1; r <= kT3R; ++r) {
+      int cnt = 0;
+      for (int dz = -r; dz <= r; ++dz)
+        for (int dy = -r; dy <= r; ++dy)
+          for (int dx = -r; dx <= r; ++dx) cnt += dz * dz + dy * dy + dx * dx <= r * r;
+      if (cnt == nball_full) {
+        R = r;
+        break;
+      }
+    }
+    if (R > 0 && fields_tile3d_ok(lat, R, nball_full))
+      return fields_tile3d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson,
+                           nullptr, s);
   }
   if (R > 0 && fields_tile2d_ok(lat, R, nball_full))
     return fields_tile2d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson, s);

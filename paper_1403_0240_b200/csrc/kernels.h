@@ -192,6 +192,10 @@ int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const O
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, cudaStream_t s);
 bool fields_tile2d_ok(const Lat &lat, int R, int nball_full);
+int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
+                      int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
+                      double *rho0, int poisson, long long *band, cudaStream_t s);
+bool fields_tile3d_ok(const Lat &lat, int R, int nball_full);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
