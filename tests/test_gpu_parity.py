@@ -84,6 +84,21 @@ def test_scan_contour_vs_reference(P):
         assert np.array_equal(ow, lab.ravel()[xs])
 
 
+@pytest.mark.parametrize("shape,nlab", [((131, 257), 7), ((1, 300), 3), ((300, 1), 3),
+                                         ((23, 37, 41), 9), ((1, 1, 50), 2), ((17, 1, 19), 5)])
+def test_scan_contour_face_path_vs_oracle(P, shape, nlab):
+    """The face-adjacency contour kernels (full_fg, 32-bit coordinates,
+    register sort) against the oracle on dense multi-label lattices, where
+    most sites have several distinct competitors, and on degenerate extents."""
+    from paper_1403_0240_b200.contour import scan_particles
+    rng = np.random.default_rng(sum(shape) * 31 + nlab)
+    lab = rng.integers(0, nlab, size=shape).astype(np.int32)
+    lab[tuple(slice(0, max(1, d // 3)) for d in shape)] = nlab + 4  # a flat block
+    xs, ow, cm = scan_particles(lab, P.Connectivity(lab.ndim, 8 if lab.ndim == 2 else 26))
+    oxs, oow, ocm = O.scan_particles(lab, O.Conn(lab.ndim, True))
+    assert np.array_equal(xs, oxs) and np.array_equal(ow, oow) and np.array_equal(cm, ocm)
+
+
 def test_energy_increments_vs_reference(P):
     g = golden("energy.npz")
     for k in range(int(g["n"][0])):
