@@ -388,7 +388,7 @@ def run_ours(args):
             ach = alg_bytes / (energy_sob_ms / 1e3) / 1e9
             traffic = None
             try:
-                with open(os.path.join(ROOT, "profiles", "r01f_traffic.json")) as f:
+                with open(os.path.join(ROOT, "profiles", "r01g_traffic.json")) as f:
                     traffic = json.load(f)["energy_plus_sobolev_dram_bytes"]
             except Exception:
                 pass
