@@ -157,6 +157,7 @@ struct rcb_engine {
   DBuf<int64_t> evbounds;
   DBuf<uint64_t> labkey, labkey2;
   DBuf<int32_t> labpos, labpos2, pos_of, lab_ptr, lbox, flrows, colb;
+  DBuf<uint32_t> fmap;
   DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark, qstate;
   DBuf<uint32_t> qlist, qscr, bigmap, bigfr2;
   DBuf<uint8_t> bigfg2;
@@ -207,7 +208,7 @@ struct rcb_engine {
       small.release(s); dirty.release(s); cnt0.release(s); gq1.release(s); slot.release(s);
       dtot.release(s); snap.release(s); evv.release(s); evkey.release(s); evkey2.release(s); evval.release(s);
       evval2.release(s); evbounds.release(s); labkey.release(s); labkey2.release(s);
-      labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); bigkey.release(s);
+      labpos.release(s); labpos2.release(s); pos_of.release(s); flrows.release(s); fmap.release(s); bigkey.release(s);
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
@@ -803,6 +804,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.labpos = &e->labpos;
       X.labpos2 = &e->labpos2;
       X.flrows = &e->flrows;
+      X.fmap = &e->fmap;
       X.rec = &e->rec;
       RCB_TRY(e->band.reserve(kLimbs + 2, s));
       X.band = e->band.p;

@@ -29,6 +29,8 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "dev.cuh"
 #include "kernels.h"
@@ -3440,6 +3442,44 @@ __global__ void k_flip_keys(const int64_t *__restrict__ acc, const int64_t *__re
   }
 }
 
+// Flip index without a sort (2-D/3-D PS ledger, V <= 2^24): a site flips at
+// most once per iteration (every candidate at x carries owner L[x] of the
+// iteration start, so after one flip the others are stale), so the moves'
+// sites are distinct and their site order is a compaction of the site map
+// fmap (move index + 1 per flipped site, zero elsewhere) — the same keys and
+// values the stable radix sort produces.  fmap is all zero between
+// iterations: k_flip_vals clears the entries it reads.
+__global__ void k_flip_mark(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                            int64_t cap, uint32_t *__restrict__ fmap, uint32_t *__restrict__ key,
+                            uint32_t sentinel) {
+  const int64_t n = *moves;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += stride) {
+    if (k < n)
+      fmap[(uint32_t)acc[3 * k]] = (uint32_t)k + 1;
+    else
+      key[k] = sentinel;
+  }
+}
+
+struct FlipSel {
+  const uint32_t *m;
+  __device__ __forceinline__ bool operator()(const uint32_t &x) const { return m[x] != 0; }
+};
+
+__global__ void k_flip_vals(const int64_t *__restrict__ moves, const uint32_t *__restrict__ key,
+                            uint32_t *__restrict__ fmap, int32_t *__restrict__ val,
+                            const uint32_t *__restrict__ nsel) {
+  const int64_t n = *moves;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (int64_t)*nsel != n) __trap();  // distinct sites
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    const uint32_t g = key[e];
+    val[e] = (int32_t)fmap[g] - 1;
+    fmap[g] = 0;
+  }
+}
+
 __global__ void k_flip_rows(const uint32_t *__restrict__ key, int64_t cap, int64_t nx,
                             int32_t *__restrict__ start, int32_t *__restrict__ end,
                             uint32_t sentinel) {
@@ -4057,14 +4097,33 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     int fb = 1;
     while (fb < 32 && ((int64_t)1 << fb) <= A.lat.V) ++fb;
     const uint32_t fsent = fb >= 32 ? 0xffffffffu : (uint32_t)((1ull << fb) - 1);
-    k_flip_keys<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.evkey->p, X.labpos2->p,
-                                                 fsent);
-    size_t b4 = 0;
-    RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
-                                             X.labpos->p, N, 0, fb, s));
-    RCB_TRY(X.tmp->reserve(b4, s));
-    RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b4, X.evkey->p, X.evkey2->p, X.labpos2->p,
-                                             X.labpos->p, N, 0, fb, s));
+    static const bool flip_sort = getenv("RCB_FLIP_SORT") != nullptr;  // comparison runs
+    if (X.fmap && !flip_sort && A.lat.V <= ((int64_t)1 << 24)) {
+      const size_t cap0 = X.fmap->cap;
+      RCB_TRY(X.fmap->reserve(A.lat.V + 1, s));
+      if (X.fmap->cap != cap0)
+        RCB_CUDA(cudaMemsetAsync(X.fmap->p, 0, sizeof(uint32_t) * X.fmap->cap, s));
+      k_flip_mark<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.fmap->p, X.evkey2->p,
+                                                   fsent);
+      cub::CountingInputIterator<uint32_t> sites(0);
+      size_t b4 = 0;
+      RCB_CUDA(cub::DeviceSelect::If(nullptr, b4, sites, X.evkey2->p, X.fmap->p + A.lat.V,
+                                     (int)A.lat.V, FlipSel{X.fmap->p}, s));
+      RCB_TRY(X.tmp->reserve(b4, s));
+      RCB_CUDA(cub::DeviceSelect::If(X.tmp->p, b4, sites, X.evkey2->p, X.fmap->p + A.lat.V,
+                                     (int)A.lat.V, FlipSel{X.fmap->p}, s));
+      k_flip_vals<<<grid_for(N, 256), 256, 0, s>>>(X.moves, X.evkey2->p, X.fmap->p, X.labpos->p,
+                                                   X.fmap->p + A.lat.V);
+    } else {
+      k_flip_keys<<<grid_for(N, 256), 256, 0, s>>>(X.acc, X.moves, N, X.evkey->p, X.labpos2->p,
+                                                   fsent);
+      size_t b4 = 0;
+      RCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b4, X.evkey->p, X.evkey2->p,
+                                               X.labpos2->p, X.labpos->p, N, 0, fb, s));
+      RCB_TRY(X.tmp->reserve(b4, s));
+      RCB_CUDA(cub::DeviceRadixSort::SortPairs(X.tmp->p, b4, X.evkey->p, X.evkey2->p,
+                                               X.labpos2->p, X.labpos->p, N, 0, fb, s));
+    }
     RCB_CUDA(cudaMemsetAsync(X.flrows->p, 0, sizeof(int32_t) * 2 * rows, s));
     k_flip_rows<<<grid_for(N, 256), 256, 0, s>>>(X.evkey2->p, N, A.lat.nx, X.flrows->p,
                                                  X.flrows->p + rows, fsent);

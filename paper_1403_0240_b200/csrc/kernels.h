@@ -157,6 +157,7 @@ struct ParExtra {
   int accept_mode;  // 0 dataflow (default), 1 rounds
   DBuf<uint64_t> *labkey, *labkey2;
   DBuf<int32_t> *labpos, *labpos2, *flrows;
+  DBuf<uint32_t> *fmap = nullptr;  // per-site flip map of the PS flip index (zero between uses)
   DBuf<int4> *rec;
   long long *band;  // band ledger: kLimbs superaccumulator limbs + dE_int sum
   DBuf<int32_t> *colb;
