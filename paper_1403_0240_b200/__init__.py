@@ -15,12 +15,12 @@ from .contour import ContourState, StaleParticleError, scan_contour  # noqa: E40
 from .optimizer import (IterationRecord, OptimizerConfig, RegionCompetition,  # noqa: E402
                         RunResult, run)
 from .sobolev import SobolevParams, detect_oscillation, kernel_eval, sobolev_filter  # noqa: E402
-from . import report  # noqa: E402
+from . import imageio, report  # noqa: E402
 
 __all__ = [
     "Connectivity", "EnergyConfig", "EnergyValue", "evaluate_total", "EnergyModel",
     "delta_internal", "delta_internal_batch", "DegenerateStatsError", "StatsTable",
     "OptimizerConfig", "RegionCompetition", "RunResult", "IterationRecord", "run",
     "SobolevParams", "kernel_eval", "sobolev_filter", "detect_oscillation",
-    "ContourState", "StaleParticleError", "scan_contour", "report", "__version__",
+    "ContourState", "StaleParticleError", "scan_contour", "imageio", "report", "__version__",
 ]
