@@ -15,7 +15,8 @@ from tests.test_gpu_parity import P, close  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "cli")
-TIMES = {"wall_seconds", "seconds_per_iteration", "rc_threads", "seconds"}
+TIMES = {"wall_seconds", "seconds_per_iteration", "seconds_per_iteration_ratio", "rc_threads",
+         "seconds"}
 
 
 def _strip(d):
