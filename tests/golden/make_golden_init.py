@@ -64,6 +64,9 @@ def main() -> None:
     rc2 = cli.main(["segment", *common, "--model", "ps", "--noise", "poisson", "--smooth-radius", "3",
                     "--init", "otsu", "--output", "seg.pgm", "--overlay", "seg_overlay.pgm",
                     "--trace", "seg.jsonl", "--report", "seg.json"])
+    cli.main(["segment", "--input", "in.pgm", "--max-iter", "3", "--lambda", "0.5", "--init",
+              "bubbles:3", "--output", "p.pgm", "--particles-csv", "particles.csv"])
+    os.unlink("p.pgm")
     with open("exit_codes.txt", "w") as fh:
         fh.write(f"{rc} {rc2}\n")
     for f in os.listdir("."):

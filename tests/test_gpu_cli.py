@@ -64,3 +64,18 @@ def test_cli_compare_and_segment_match_reference(P, tmp_path, monkeypatch):
         a, b = json.loads(a), json.loads(b)
         assert close(a.pop("energy"), b.pop("energy"))
         assert _strip(a) == _strip(b)
+
+
+def test_cli_particles_csv_matches_reference(P, tmp_path, monkeypatch):
+    """--particles-csv (cli.py:117-127): every iteration's candidates with
+    their filtered rank values, same rows as the reference's (pc/gauss:
+    bit-exact values); compared per iteration as row sets."""
+    from paper_1403_0240_b200 import cli
+    shutil.copy(os.path.join(GOLD, "in.pgm"), tmp_path / "in.pgm")
+    monkeypatch.chdir(tmp_path)
+    assert cli.main(["segment", "--input", "in.pgm", "--max-iter", "3", "--lambda", "0.5", "--init",
+                     "bubbles:3", "--output", "p.pgm", "--particles-csv", "particles.csv"]) == 2
+    got = (tmp_path / "particles.csv").read_text().splitlines()
+    want = _gold("particles.csv").decode().splitlines()
+    assert got[0] == want[0] and len(got) == len(want)
+    assert sorted(got[1:]) == sorted(want[1:])
