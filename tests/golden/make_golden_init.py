@@ -67,6 +67,8 @@ def main() -> None:
     cli.main(["segment", "--input", "in.pgm", "--max-iter", "3", "--lambda", "0.5", "--init",
               "bubbles:3", "--output", "p.pgm", "--particles-csv", "particles.csv"])
     os.unlink("p.pgm")
+    cli.render_kernel_figure = lambda *a, **k: None
+    cli.main(["kernel-table", "--E", "9", "--epsilon", "1/30", "--samples", "101", "--out", "kernel.csv"])
     with open("exit_codes.txt", "w") as fh:
         fh.write(f"{rc} {rc2}\n")
     for f in os.listdir("."):

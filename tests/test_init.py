@@ -45,3 +45,14 @@ def test_cli_usage_errors_exit_1(capsys):
         assert e.value.code == 1, argv
     assert cli.main(["segment", "--input", "/nonexistent.pgm", "--output", "o.pgm"]) == 1
     assert "rcseg: error:" in capsys.readouterr().err
+
+
+def test_cli_kernel_table_matches_reference(tmp_path):
+    """`kernel-table` (cli.py:207-215) writes the reference's CSV byte for byte."""
+    import os
+    from paper_1403_0240_b200 import cli
+    out = tmp_path / "k.csv"
+    assert cli.main(["kernel-table", "--E", "9", "--epsilon", "1/30", "--samples", "101",
+                     "--out", str(out)]) == 0
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cli", "kernel.csv"), "rb") as fh:
+        assert out.read_bytes() == fh.read()
