@@ -122,6 +122,46 @@ int32_t rcb_evaluate_total(const double *image, const int32_t *labels, int32_t n
                            const int64_t *dims, const rcb_energy_cfg *cfg, double *external,
                            int64_t *internal);
 
+/* grid.py:99-113 flood_fill_components / count_components: components of
+ * (labels == target) minus site `exclude` (-1: none) under the foreground
+ * adjacency, numbered 1..n in first-encountered raster order like
+ * ndimage.label; comp (nullable) receives the numbering (0 elsewhere). */
+int32_t rcb_label_components(const int32_t *labels, int32_t ndim, const int64_t *dims,
+                             int32_t full_fg, int32_t target, int64_t exclude, int32_t *comp,
+                             int64_t *n_components);
+
+/* contour.py:171-207 is_move_admissible for n (pixel, competitor) queries
+ * against one raster; region_counts (nullable; entries < 0 = count it) is
+ * the reference's region_count argument.  out[i] = 1 admissible, 0 not. */
+int32_t rcb_moves_admissible(const int32_t *labels, int32_t ndim, const int64_t *dims,
+                             int32_t full_fg, const int64_t *pixels, const int64_t *competitors,
+                             const int64_t *region_counts, int64_t n, int32_t allow_fusion,
+                             int32_t allow_vanish, int32_t *out);
+
+/* sobolev.py:99-122 CellList(coords, edge).pairs(cutoff): every ordered
+ * pair (p, q), p == q included, whose buckets (floor_divide(coords, edge))
+ * are box neighbours and whose squared distance is < cutoff^2; sorted by
+ * (p, q).  RCB_ERR_CAPACITY with *n_pairs set when cap is too small. */
+int32_t rcb_cell_pairs(const int64_t *coords, int64_t n, int32_t ndim, double edge,
+                       double cutoff, int64_t *pi, int64_t *qi, double *dist, int64_t cap,
+                       int64_t *n_pairs);
+/* sobolev.py:80-93 CellList.query(point, cutoff, exclude): ascending
+ * indices (out has room for n); exclude < 0 = none. */
+int32_t rcb_cell_query(const int64_t *coords, int64_t n, int32_t ndim, double edge,
+                       const double *point, double cutoff, int64_t exclude, int64_t *out,
+                       int64_t *n_out);
+
+/* energy.py:161-193 _ball_sum(field, radius): ball convolution with zero
+ * borders, by the reference's cumulative-sum spans (same rounding). */
+int32_t rcb_ball_sum(const double *field, int32_t ndim, const int64_t *dims, int32_t radius,
+                     double *out);
+/* energy.py:196-223 smooth_fields(labels, image, radius, n_labels): dense
+ * C, S of n_labels x V doubles each (per-label window = bounding box grown
+ * by the radius, as the reference computes it). */
+int32_t rcb_smooth_fields(const int32_t *labels, const double *image, int32_t ndim,
+                          const int64_t *dims, int32_t radius, int32_t n_labels, double *C,
+                          double *S);
+
 /* ---- the engine: RegionCompetition (optimizer.py:90-230) --------------- */
 
 /* image: float64 C-order (optimizer.py:102); labels: int32 (copied).
@@ -135,6 +175,10 @@ void rcb_engine_destroy(rcb_engine *eng);
 int32_t rcb_engine_iterate(rcb_engine *eng, rcb_iter_record *rec);
 int32_t rcb_engine_get_labels(rcb_engine *eng, int32_t *out);
 int32_t rcb_engine_set_labels(rcb_engine *eng, const int32_t *labels);
+/* Undo the last iteration's accepted moves on the device (the restore of
+ * optimizer.py:259-265's oscillation halt without a per-iteration host copy
+ * of the raster); refresh the statistics afterwards (rcb_engine_refresh). */
+int32_t rcb_engine_undo_last(rcb_engine *eng);
 /* last_candidates (optimizer.py:140-142): (x, owner, competitor, rank). */
 int32_t rcb_engine_get_candidates(rcb_engine *eng, int64_t *xs, int64_t *owners,
                                   int64_t *competitors, double *rank, int64_t cap, int64_t *n);

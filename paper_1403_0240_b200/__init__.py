@@ -10,10 +10,13 @@ __version__ = "0.1.0"
 
 from .energy import (DegenerateStatsError, EnergyConfig, EnergyModel, EnergyValue,  # noqa: E402
                      delta_internal, delta_internal_batch, evaluate_total)
-from .grid import Connectivity, StatsTable  # noqa: E402
+from .grid import (Connectivity, RegionStats, StatsTable, count_components,  # noqa: E402
+                   flood_fill_components)
 from .contour import ContourState, StaleParticleError, scan_contour  # noqa: E402
 from .optimizer import (IterationRecord, OptimizerConfig, RegionCompetition,  # noqa: E402
-                        RunResult, run)
+                        RunResult, initialize, run)
+from .synth import (NoiseSpec, SceneSpec, desk_scene, generate, two_blob_scene,  # noqa: E402
+                    two_sphere_scene)
 from .sobolev import SobolevParams, detect_oscillation, kernel_eval, sobolev_filter  # noqa: E402
 from . import imageio, report  # noqa: E402
 
@@ -23,4 +26,6 @@ __all__ = [
     "OptimizerConfig", "RegionCompetition", "RunResult", "IterationRecord", "run",
     "SobolevParams", "kernel_eval", "sobolev_filter", "detect_oscillation",
     "ContourState", "StaleParticleError", "scan_contour", "imageio", "report", "__version__",
+    "initialize", "SceneSpec", "NoiseSpec", "desk_scene", "generate", "two_blob_scene",
+    "two_sphere_scene", "RegionStats", "flood_fill_components", "count_components",
 ]

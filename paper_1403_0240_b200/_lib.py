@@ -63,11 +63,18 @@ SIGNATURES = {
     "rcb_delta_external_batch": [_P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _I64, _P],
     "rcb_stats_from_labels": [_P, _P, _I64, _I32, _P, _P, _P],
     "rcb_evaluate_total": [_P, _P, _I32, _P, _P, _P, _P],
+    "rcb_label_components": [_P, _I32, _P, _I32, _I32, _I64, _P, _P],
+    "rcb_moves_admissible": [_P, _I32, _P, _I32, _P, _P, _P, _I64, _I32, _I32, _P],
+    "rcb_cell_pairs": [_P, _I64, _I32, _D, _D, _P, _P, _P, _I64, _P],
+    "rcb_cell_query": [_P, _I64, _I32, _D, _P, _D, _I64, _P, _P],
+    "rcb_ball_sum": [_P, _I32, _P, _I32, _P],
+    "rcb_smooth_fields": [_P, _P, _I32, _P, _I32, _I32, _P, _P],
     "rcb_engine_create": [_P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P],
     "rcb_engine_destroy": [_P],
     "rcb_engine_iterate": [_P, _P],
     "rcb_engine_get_labels": [_P, _P],
     "rcb_engine_set_labels": [_P, _P],
+    "rcb_engine_undo_last": [_P],
     "rcb_engine_get_candidates": [_P, _P, _P, _P, _P, _I64, _P],
     "rcb_engine_get_accepted": [_P, _P, _I64, _P],
     "rcb_engine_get_stats": [_P, _P, _P, _P, _I32],

@@ -192,6 +192,11 @@ struct rcb_engine {
   uint32_t *hoff = nullptr;  // pinned: site_off reads
   unsigned long long *hwatch = nullptr;  // pinned: dataflow watchdog words (job[56..61])
   void *pinned = nullptr;                // the pinned block hsc / hoff / hwatch live in
+  // set when the dataflow watchdog fired: the kernels after the decisions ran on
+  // a partly filled decision array, so labels / statistics / ledger are
+  // undefined and every later call fails (destroy the engine)
+  bool poisoned = false;
+  std::string poison_msg;
 
   ~rcb_engine() {
     if (s) {
@@ -893,11 +898,14 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
     char msg[256];
     snprintf(msg, sizeof msg,
              "dataflow acceptance watchdog: wait kind %llu at position %llu (aux %lld), "
-             "low-water %llu, fetched %llu; iteration %lld results discarded",
+             "low-water %llu, fetched %llu, iteration %lld",
              w0, e->hwatch[2], (long long)e->hwatch[3], e->hwatch[4], e->hwatch[5],
              (long long)e->iteration);
     memset(e->hwatch, 0, 8 * sizeof(unsigned long long));
-    return fail(RCB_ERR_CUDA, msg);
+    e->poisoned = true;
+    e->poison_msg = std::string(msg) +
+                    "; the engine state (labels, statistics, ledger) is undefined — destroy it";
+    return fail(RCB_ERR_CUDA, e->poison_msg);
   }
   e->n_scored = n;
   e->last_par = n > 0 && e->cur_par;
@@ -947,6 +955,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
 }
 
 int32_t rcb_engine_iterate(rcb_engine *e, rcb_iter_record *rec) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   if (e->scored) return fail(RCB_ERR_VALUE, "rcb_engine_iterate between score and finish");
   RCB_TRY(engine_score(e));
   return engine_finish(e, rec);
@@ -962,6 +971,7 @@ int32_t rcb_engine_set_slab(rcb_engine *e, int64_t lo, int64_t hi) {
 }
 
 int32_t rcb_engine_score(rcb_engine *e, rcb_slab_info *info) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   if (e->scored) return fail(RCB_ERR_VALUE, "rcb_engine_score called twice");
   RCB_TRY(engine_score(e));
   info->n_particles = e->N;
@@ -975,7 +985,10 @@ int32_t rcb_engine_score(rcb_engine *e, rcb_slab_info *info) {
   return RCB_OK;
 }
 
-int32_t rcb_engine_finish(rcb_engine *e, rcb_iter_record *rec) { return engine_finish(e, rec); }
+int32_t rcb_engine_finish(rcb_engine *e, rcb_iter_record *rec) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
+  return engine_finish(e, rec);
+}
 
 int32_t rcb_engine_particle_ranges(rcb_engine *e, const int64_t *planes, int32_t k, int64_t *out) {
   RCB_CUDA(cudaSetDevice(e->device));
@@ -984,6 +997,7 @@ int32_t rcb_engine_particle_ranges(rcb_engine *e, const int64_t *planes, int32_t
 }
 
 int32_t rcb_engine_get_labels(rcb_engine *e, int32_t *out) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   RCB_CUDA(cudaSetDevice(e->device));
   RCB_CUDA(cudaMemcpyAsync(out, e->L.p, sizeof(int32_t) * e->lat.V, cudaMemcpyDeviceToHost, e->s));
   RCB_CUDA(cudaStreamSynchronize(e->s));
@@ -991,6 +1005,7 @@ int32_t rcb_engine_get_labels(rcb_engine *e, int32_t *out) {
 }
 
 int32_t rcb_engine_set_labels(rcb_engine *e, const int32_t *labels) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   RCB_CUDA(cudaSetDevice(e->device));
   for (int64_t i = 0; i < e->lat.V; ++i)
     if (labels[i] < 0 || labels[i] >= e->nl)
@@ -1002,8 +1017,35 @@ int32_t rcb_engine_set_labels(rcb_engine *e, const int32_t *labels) {
   return RCB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+__global__ void k_undo_moves(const int64_t *__restrict__ acc, int64_t m, int32_t *__restrict__ L) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) L[acc[3 * i]] = (int32_t)acc[3 * i + 1];  // every site flips at most once
+}
+}  // namespace
+
+extern "C" {
+
+int32_t rcb_engine_undo_last(rcb_engine *e) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
+  RCB_CUDA(cudaSetDevice(e->device));
+  const int64_t m = e->last_moves;
+  if (m > 0) {
+    k_undo_moves<<<grid_for(m, 256), 256, 0, e->s>>>(e->acc.p, m, e->L.p);
+    RCB_CUDA(cudaGetLastError());
+  }
+  e->last_moves = 0;
+  e->fields_fresh = false;
+  RCB_TRY(e->components());
+  RCB_TRY(e->prepare());
+  return RCB_OK;
+}
+
 int32_t rcb_engine_get_candidates(rcb_engine *e, int64_t *xs, int64_t *owners, int64_t *comps,
                                   double *rank, int64_t cap, int64_t *n) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   *n = e->n_scored;
   if (cap < e->n_scored) return fail(RCB_ERR_CAPACITY, "candidate buffer too small");
   const int64_t m = e->n_scored;
@@ -1025,6 +1067,7 @@ int32_t rcb_engine_get_candidates(rcb_engine *e, int64_t *xs, int64_t *owners, i
 }
 
 int32_t rcb_engine_get_accepted(rcb_engine *e, int64_t *xab, int64_t cap, int64_t *n) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   *n = e->last_moves;
   if (cap < e->last_moves) return fail(RCB_ERR_CAPACITY, "accepted-move buffer too small");
   if (e->last_moves == 0) return RCB_OK;
@@ -1037,6 +1080,7 @@ int32_t rcb_engine_get_accepted(rcb_engine *e, int64_t *xab, int64_t cap, int64_
 
 int32_t rcb_engine_get_stats(rcb_engine *e, int64_t *count, double *total, double *total_sq,
                              int32_t n_labels) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   if (n_labels < e->nl) return fail(RCB_ERR_CAPACITY, "stats buffers too small");
   RCB_CUDA(cudaSetDevice(e->device));
   RCB_TRY(e->flush_stats());
@@ -1068,6 +1112,7 @@ int32_t rcb_engine_set_energy(rcb_engine *e, double energy) {
 }
 
 int32_t rcb_engine_refresh(rcb_engine *e) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   RCB_CUDA(cudaSetDevice(e->device));
   RCB_TRY(e->refresh());
   RCB_CUDA(cudaStreamSynchronize(e->s));
@@ -1128,6 +1173,7 @@ static int32_t evaluate_on(const int32_t *L, const double *I, const Lat &lat,
 }
 
 int32_t rcb_engine_evaluate(rcb_engine *e, double *external, int64_t *internal) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
   RCB_CUDA(cudaSetDevice(e->device));
   if (!e->fields_fresh)
     return evaluate_on(e->L.p, e->I.p, e->lat, &e->ecfg, e->nl, external, internal, e->s);

@@ -58,6 +58,57 @@ def ball_offsets(ndim: int, radius: int) -> np.ndarray:
     return out
 
 
+@functools.lru_cache(maxsize=None)
+def _ball_mask(ndim: int, radius: int) -> np.ndarray:
+    """energy.py:73-79: boolean (2r+1)^d mask of |o|^2 <= r^2."""
+    g = np.meshgrid(*([np.arange(-radius, radius + 1)] * ndim), indexing="ij")
+    mask = sum(x * x for x in g) <= radius * radius
+    mask.setflags(write=False)
+    return mask
+
+
+def _ball_sum(field: np.ndarray, radius: int) -> np.ndarray:
+    """energy.py:161-193: sum of ``field`` over the radius ball around every
+    cell, zero outside — on the device (rcb_ball_sum) with the reference's
+    cumulative-sum spans, so float fields round identically."""
+    f = np.ascontiguousarray(field, np.float64)
+    if f.ndim not in (2, 3):
+        raise ValueError("field must be 2-D or 3-D")
+    out = np.empty_like(f)
+    _lib.require_device()
+    _lib.check(_lib.lib.rcb_ball_sum(_lib.ptr(f), f.ndim, _lib.ptr(_lib.dims_arr(f.shape)),
+                                     int(radius), _lib.ptr(out)))
+    return out
+
+
+def smooth_fields(labels: np.ndarray, image: np.ndarray, radius: int, n_labels: int):
+    """energy.py:196-223: dense per-label ball counts C and sums S, shape
+    (n_labels, *dims), each label windowed to its bounding box grown by the
+    radius as the reference does (rcb_smooth_fields).  The engine never
+    builds these (it keeps own-label fields only); this is the function-level
+    drop-in."""
+    validate_labels(labels)
+    lab = np.ascontiguousarray(labels, np.int32)
+    img = np.ascontiguousarray(image, np.float64)
+    if lab.shape != img.shape:
+        raise ValueError("label and intensity rasters differ in shape")
+    Cf = np.empty((int(n_labels),) + lab.shape, np.float64)
+    Sf = np.empty_like(Cf)
+    _lib.require_device()
+    _lib.check(_lib.lib.rcb_smooth_fields(_lib.ptr(lab), _lib.ptr(img), lab.ndim,
+                                          _lib.ptr(_lib.dims_arr(lab.shape)), int(radius),
+                                          int(n_labels), _lib.ptr(Cf), _lib.ptr(Sf)))
+    return Cf, Sf
+
+
+def perimeter(labels: np.ndarray) -> int:
+    """energy.py:82-88: face-adjacent pairs with different labels (the
+    device total's internal term)."""
+    validate_labels(labels)
+    lab = np.ascontiguousarray(labels, np.int32)
+    return evaluate_total(lab, np.zeros(lab.shape), EnergyConfig("pc", "gauss")).internal
+
+
 def _particles(labels, pixels, owners, competitors):
     return (_lib.c64(pixels), _lib.c64(owners), _lib.c64(competitors))
 
@@ -105,7 +156,10 @@ class EnergyModel:
     """Incremental energy bookkeeping bound to (labels, image)
     (energy.py:260-408).  PC increments read ``self.stats``; PS increments
     rebuild the own-label ball fields from the current raster on the GPU, so
-    ``apply_flip`` has nothing to shift."""
+    ``apply_flip`` has nothing to shift, and the dense ``_C`` / ``_S`` views
+    are derived from the current raster when read (equal to the reference's
+    incrementally shifted fields for integer data, where every ball sum is
+    exact; within rounding otherwise)."""
 
     def __init__(self, image, labels, config: EnergyConfig):
         validate_image(image)
@@ -157,3 +211,16 @@ class EnergyModel:
         """energy.py:381-408 — a no-op here: PS fields are derived from the
         raster on the device at every evaluation."""
         return None
+
+    @property
+    def _C(self):
+        return self._fields()[0]
+
+    @property
+    def _S(self):
+        return self._fields()[1]
+
+    def _fields(self):
+        if self.config.region_model != "ps":
+            return None, None
+        return smooth_fields(self.labels, self.image, self.config.smooth_radius, self.n_labels)

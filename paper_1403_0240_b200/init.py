@@ -39,13 +39,15 @@ def otsu_threshold(hist: np.ndarray) -> int | None:
 
 
 def split_disjoint_labels(labels: np.ndarray, conn: Connectivity) -> np.ndarray:
-    """optimizer.py:311-322"""
+    """optimizer.py:311-322 (components by the device union-find,
+    grid.flood_fill_components' numbering = ndimage.label's)"""
+    from .grid import _components
     out = np.zeros(labels.shape, dtype=LABEL_DTYPE)
     nxt = 1
     for lab in np.unique(labels):
         if lab <= 0:
             continue
-        comp, n = ndimage.label(labels == lab, structure=conn.fg_structure)
+        comp, n = _components(labels, int(lab), conn)
         for k in range(1, n + 1):
             out[comp == k] = nxt
             nxt += 1

@@ -21,6 +21,7 @@ from . import _lib
 from .contour import ContourState, scan_particles
 from .energy import EnergyConfig, EnergyValue, evaluate_total
 from .grid import LABEL_DTYPE, Connectivity, StatsTable, validate_image, validate_labels
+from .init import initialize, otsu_threshold, split_disjoint_labels  # noqa: F401  (optimizer.py:284-405)
 from .sobolev import SobolevParams, detect_oscillation, sobolev_cfg
 
 
@@ -319,8 +320,9 @@ class RegionCompetition:
         t0 = time.perf_counter()
         status = "max-iter"
         for _ in range(cfg.max_iterations):
-            # only an l2-mode oscillation halt restores the previous labeling
-            prev_labels = self.labels if self.mode == "l2" else None
+            # only an l2-mode oscillation halt restores the previous labeling;
+            # the engine undoes the last iteration's moves on the device
+            # instead of copying the raster to the host every iteration
             prev_energy = self._energy
             rec = self.iterate()
             if on_iteration is not None:
@@ -339,7 +341,7 @@ class RegionCompetition:
                 else:
                     status = "oscillation-halt"
                     if prev_energy < self._energy:
-                        self.labels = prev_labels
+                        _lib.check(_lib.lib.rcb_engine_undo_last(self._h))
                         self.model.refresh()
                         self._energy = prev_energy
                         _lib.check(_lib.lib.rcb_engine_set_energy(self._h, self._energy))

@@ -68,23 +68,68 @@ def sobolev_cfg(params: SobolevParams):
 
 
 class CellList:
-    """Kept for signature compatibility with sobolev_filter(..., cells):
-    the GPU path replaces the bucket grid by the lattice CSR index, so a
-    CellList only records the coordinates it was built on."""
+    """sobolev.py:50-122: the bucket grid's query interface.  Buckets are
+    floor_divide(coords, edge); a pair or point hit needs its buckets to be box
+    neighbours and the squared distance below cutoff^2 (strict) — the
+    reference's semantics, cutoffs beyond the edge included.  Both queries run
+    on the device (rcb_cell_pairs / rcb_cell_query); the engine's Sobolev
+    filter does not use them (it walks the lattice CSR index instead)."""
 
     def __init__(self, coords: np.ndarray, edge: float):
+        coords = np.asarray(coords)
         if coords.ndim != 2 or coords.shape[1] not in (2, 3):
             raise ValueError("coords must be (n, 2) or (n, 3)")
         if edge <= 0:
             raise ValueError("bucket edge must be positive")
-        self.coords = np.asarray(coords, dtype=np.int64)
+        self.coords = np.ascontiguousarray(coords, dtype=np.int64)
         self.edge = float(edge)
 
     def __len__(self) -> int:
         return len(self.coords)
 
+    def query(self, point, cutoff: float, exclude: int | None = None) -> np.ndarray:
+        """Indices of particles strictly within ``cutoff`` of ``point``, ascending."""
+        n = len(self.coords)
+        if n == 0:
+            return np.empty(0, dtype=np.int64)
+        pt = np.ascontiguousarray(np.asarray(point, dtype=np.float64).ravel())
+        if pt.size != self.coords.shape[1]:
+            raise ValueError("point dimension differs from the coordinates")
+        out = np.empty(n, np.int64)
+        k = C.c_int64(0)
+        _lib.require_device()
+        _lib.check(_lib.lib.rcb_cell_query(
+            _lib.ptr(self.coords), n, self.coords.shape[1], self.edge, _lib.ptr(pt), float(cutoff),
+            -1 if exclude is None else int(exclude), _lib.ptr(out), C.byref(k)))
+        return out[:k.value]
+
+    def pairs(self, cutoff: float):
+        """All ordered pairs (p, q) with d(p, q) < cutoff, p == q included:
+        (p_idx, q_idx, distance), sorted by (p, q)."""
+        n = len(self.coords)
+        e = np.empty(0, dtype=np.int64)
+        if n == 0:
+            return e, e, np.empty(0, dtype=np.float64)
+        _lib.require_device()
+        cap = 0
+        bufs = (e, e, np.empty(0, np.float64))
+        tot = C.c_int64(0)
+        for _ in range(2):
+            st = _lib.lib.rcb_cell_pairs(_lib.ptr(self.coords), n, self.coords.shape[1], self.edge,
+                                         float(cutoff), _lib.ptr(bufs[0]), _lib.ptr(bufs[1]),
+                                         _lib.ptr(bufs[2]), cap, C.byref(tot))
+            if st == _lib.RCB_ERR_CAPACITY:
+                cap = tot.value
+                bufs = (np.empty(cap, np.int64), np.empty(cap, np.int64), np.empty(cap, np.float64))
+                continue
+            _lib.check(st)
+            break
+        k = tot.value
+        return bufs[0][:k], bufs[1][:k], bufs[2][:k]
+
 
 def build_cell_list(coords: np.ndarray, params: SobolevParams) -> CellList:
+    """sobolev.py:133-134"""
     return CellList(coords, params.cutoff)
 
 

@@ -204,3 +204,30 @@ def save_scene(spec: SceneSpec, path) -> None:
 def load_scene(path) -> SceneSpec:
     with open(path) as fh:
         return scene_from_dict(json.load(fh))
+
+
+# -- stock benchmark scenes (synth.py:252-296) --------------------------------
+
+def desk_scene(noise_seed: int = 7) -> SceneSpec:
+    """64x64: two blurred disks and a rectangle in Poisson noise."""
+    return SceneSpec(dims=(64, 64), background=0.5,
+                     shapes=[Shape("disk", 10.0, center=(18, 18), radius=8.0),
+                             Shape("disk", 8.0, center=(44, 16), radius=6.0),
+                             Shape("rect", 10.0, origin=(36, 36), size=(16, 13))],
+                     blur_sigma=2.0, noise=NoiseSpec(psnr=6.0, seed=noise_seed))
+
+
+def two_blob_scene(noise_seed: int = 7) -> SceneSpec:
+    """64x64: two blurred disks of different brightness on a dark field."""
+    return SceneSpec(dims=(64, 64), background=0.0,
+                     shapes=[Shape("disk", 10.0, center=(19, 19), radius=7.0),
+                             Shape("disk", 6.0, center=(45, 45), radius=5.0)],
+                     blur_sigma=2.0, noise=NoiseSpec(psnr=6.0, seed=noise_seed))
+
+
+def two_sphere_scene(noise_seed: int = 7) -> SceneSpec:
+    """32^3: two bright spheres, for 3-D sanity runs."""
+    return SceneSpec(dims=(32, 32, 32), background=0.0,
+                     shapes=[Shape("disk", 10.0, center=(10, 10, 10), radius=6.0),
+                             Shape("disk", 8.0, center=(22, 22, 22), radius=5.0)],
+                     blur_sigma=1.5, noise=NoiseSpec(psnr=6.0, seed=noise_seed))

@@ -66,13 +66,69 @@ def bubbles(shape, per_axis: int, radius: float) -> np.ndarray:
     return labels
 
 
+# -- blur / Poisson noise: the reference pipeline (rcseg/synth.py:87-182) ------
+#
+# Every generator below blurs and noises exactly as the reference's
+# ``blur`` / ``poissonize`` do.  By default the device
+# pipeline of this package computes them (bit-identical to the reference,
+# tests/golden/synth.npz); the fixture script (tests/golden/make_golden.py)
+# swaps in the reference's own functions with ``use_backend``, and a GPU
+# test checks the device-made images equal the fixture images bit for bit.
+
+_BACKEND: dict = {"blur": None, "poissonize": None}
+
+
+def use_backend(blur=None, poissonize=None) -> None:
+    """Route blur(image, sigma) / poissonize(image, psnr, seed) through the
+    given callables (None restores the device pipeline)."""
+    _BACKEND["blur"] = blur
+    _BACKEND["poissonize"] = poissonize
+
+
+def _ref_kernel(sigma: float) -> np.ndarray:
+    """synth.py:96-99: exp(-t^2 / (2 sigma^2)) over |t| <= ceil(4 sigma), / sum."""
+    radius = int(np.ceil(4.0 * sigma))
+    t = np.arange(-radius, radius + 1, dtype=np.float64)
+    k = np.exp(-(t * t) / (2.0 * sigma * sigma))
+    k /= k.sum()
+    return k
+
+
+def _device_ok() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
 def _blur(img, sigma):
-    return ndimage.gaussian_filter(img, sigma, mode="mirror", truncate=4.0)
+    """Reference blur; ``sigma`` may be a per-axis tuple (cfg3's anisotropic
+    PSF: the reference's correlate1d pass per axis with that axis' kernel)."""
+    img = np.asarray(img, np.float64)
+    sig = tuple(sigma) if np.ndim(sigma) else (float(sigma),) * img.ndim
+    if _BACKEND["blur"] is not None and len(set(sig)) == 1:
+        return _BACKEND["blur"](img, sig[0])
+    if len(set(sig)) == 1 and _device_ok():
+        from paper_1403_0240_b200 import synth as dsynth
+        return dsynth.blur(img, sig[0])
+    out = img.copy()
+    for axis, s in enumerate(sig):
+        if s > 0:
+            out = ndimage.correlate1d(out, _ref_kernel(s), axis=axis, mode="mirror")
+    return out
 
 
-def _poisson(img, peak, rng):
-    lam = np.clip(img, 0, None) * (peak / float(img.max()))
-    return rng.poisson(lam).astype(np.float32)
+def _poisson(img, peak, seed):
+    """Reference poissonize(img, NoiseSpec(psnr=sqrt(peak), seed)): the blurred
+    image rescaled to peak mean psnr**2, per-pixel counter-based draws."""
+    psnr = float(np.sqrt(peak))
+    if _BACKEND["poissonize"] is not None:
+        out = _BACKEND["poissonize"](img, psnr, seed)
+    else:
+        from paper_1403_0240_b200 import synth as dsynth
+        out = dsynth.poissonize(img, dsynth.NoiseSpec(psnr, seed))
+    return np.asarray(out).astype(np.float32)
 
 
 def cfg1(seed: int = 0) -> Scene:
@@ -96,7 +152,7 @@ def _cfg2_image(n: int, seed: int) -> np.ndarray:
         val = rng.uniform(0.6, 1.0)
         _paint(img, c, a, val)
     img = _blur(img, 1.5)
-    return _poisson(img, 50.0, rng)
+    return _poisson(img, 50.0, seed)
 
 
 def cfg2(seed: int = 2) -> Scene:
@@ -130,7 +186,8 @@ def cfg3(seed: int = 3, n: int = 128) -> Scene:
     return Scene("cfg3", img.astype(np.float32), lab, "pc", "gauss", 4.0, iterations=100)
 
 
-def cfg4(seed: int = 4, n: int = 512, n_obj: int = 64, per_axis: int = 8) -> Scene:
+def cfg4(seed: int = 4, n: int = 512, n_obj: int = 64, per_axis: int = 8,
+         radius: float | None = None) -> Scene:
     rng = np.random.default_rng(seed)
     shape = (n, n, n)
     z = np.arange(n, dtype=np.float64)[:, None, None]
@@ -141,14 +198,17 @@ def cfg4(seed: int = 4, n: int = 512, n_obj: int = 64, per_axis: int = 8) -> Sce
         val = rng.uniform(0.5, 1.0)
         _paint(img, c, a, val)
     img = _blur(img, 1.5)
-    img = _poisson(img, 30.0, rng)
-    lab = bubbles(shape, per_axis, 15.0 * n / 512 if n < 512 else 15.0)
+    img = _poisson(img, 30.0, seed)
+    if radius is None:
+        radius = 15.0 * n / 512 if n < 512 else 15.0
+    lab = bubbles(shape, per_axis, radius)
     return Scene("cfg4", img, lab, "ps", "poisson", 6.0, smooth_radius=4,
                  iterations=200, vanish_grace=5)
 
 
 def cfg4_small(seed: int = 4) -> Scene:
-    s = cfg4(seed, n=128, n_obj=8, per_axis=2)
+    """cfg4': 128^3, 8 ellipsoids, bubbles:2:15, PS/Poisson R=4, E=6."""
+    s = cfg4(seed, n=128, n_obj=8, per_axis=2, radius=15.0)
     s.name = "cfg4_small"
     return s
 

@@ -394,29 +394,6 @@ def test_ordered_sum_exact_vs_sequential(P):
         assert np.array_equal(t.total_sq, o.total_sq, equal_nan=True), (k, t.total_sq, o.total_sq)
 
 
-def test_bench_workload_cfg2_vs_reference(P):
-    """The bench configuration itself (1024^2 PS/Poisson, E = 6): the first
-    three iterations against the reference run — accepted moves in order and
-    label hashes bit-exact, ledger energy within rtol 1e-12."""
-    import scenes
-    g = golden("run_cfg2_full.npz")
-    sc = scenes.cfg2()
-    assert hashlib.sha256(np.ascontiguousarray(sc.image).tobytes()).hexdigest()[:16] == \
-        str(g["image_sha"][0]), "scene generator drifted from the fixture"
-    eng = P.RegionCompetition(sc.image, sc.labels, P.EnergyConfig("ps", "poisson", smooth_radius=4),
-                              P.SobolevParams(6.0), P.OptimizerConfig("sobolev", vanish_grace=5))
-    off = 0
-    for it in range(3):
-        rec = eng.iterate()
-        n = int(g["acc_len"][it])
-        assert np.array_equal(eng.last_accepted, g["acc"][off:off + n]), it
-        off += n
-        h = hashlib.sha256(np.ascontiguousarray(eng.labels, np.int32).tobytes()).hexdigest()[:16]
-        assert h == str(g["hashes"][it]), it
-        assert rec.particles == int(g["particles"][it])
-        assert close(rec.energy, g["energy"][it], 1e-12), (it, rec.energy, g["energy"][it])
-
-
 @pytest.mark.parametrize("cap,box,iters", [("0", "-1", 30), ("8", "0", 12)])
 def test_deferred_registry_equals_full_union_find(P, monkeypatch, cap, box, iters):
     """Dataflow assist jobs through the deferred-candidate registry (one

@@ -51,9 +51,9 @@ def test_slab_sobolev_needs_only_the_halo(which, E, world):
     stencil_reach planes: poison everything else with NaN and the slab's
     oracle Sobolev sums stay bit-identical to the unsharded ones."""
     if which == "2d":
-        labels = scenes.cfg2_small(n=96).labels
+        labels = scenes.bubbles((96, 96), 96 // 64, 10.0)
     else:
-        labels = scenes.cfg4(n=40, n_obj=4, per_axis=2).labels
+        labels = scenes.bubbles((40, 40, 40), 2, 15.0 * 40 / 512)
     xs, ow, cm, coords = _particles(labels)
     rng = np.random.default_rng(5)
     raw = rng.normal(size=len(xs))
@@ -78,7 +78,7 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        labels = scenes.cfg4(n=32, n_obj=3, per_axis=2).labels
+        labels = scenes.bubbles((32, 32, 32), 2, 15.0 * 32 / 512)
         xs, ow, cm, coords = _particles(labels)
         rng = np.random.default_rng(9)
         raw = rng.normal(size=len(xs))
