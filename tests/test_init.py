@@ -10,6 +10,7 @@ from tests.conftest import golden
 HOST_SCHEMES = [0, 1, 2, 3]  # rect, bubbles x2, otsu; maxima blurs on the device (test_gpu_cli)
 
 
+@pytest.mark.gpu  # split_disjoint_labels labels components on the device
 @pytest.mark.parametrize("nd", [2, 3])
 @pytest.mark.parametrize("i", HOST_SCHEMES)
 def test_initialize_matches_reference(nd, i):
@@ -19,6 +20,7 @@ def test_initialize_matches_reference(nd, i):
     assert np.array_equal(got, g[f"init{nd}_{i}"])
 
 
+@pytest.mark.gpu
 def test_otsu_and_split_edges():
     assert otsu_threshold(np.zeros(256)) is None
     h = np.zeros(256)

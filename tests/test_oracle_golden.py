@@ -147,3 +147,29 @@ def test_engine_config_runs(name, iters):
         h = hashlib.sha256(np.ascontiguousarray(eng.labels, np.int32).tobytes()).hexdigest()[:16]
         assert h == str(g["hashes"][it])
         assert rec.energy == g["energy"][it]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,iters", [("cfg5_0", 3), ("cfg3", 1)])
+def test_oracle_on_baseline_configs(name, iters):
+    """The oracle port against the reference's own cfg5 / cfg3 runs (the
+    scenes regenerate on the host: no Poisson noise, numpy + scipy only)."""
+    import hashlib
+
+    import scenes
+    g = dict(golden(f"run_{name}.npz"))
+    sc = scenes.cfg5_image(0) if name == "cfg5_0" else scenes.cfg3()
+    assert hashlib.sha256(np.ascontiguousarray(sc.image).tobytes()).hexdigest()[:16] == \
+        str(g["image_sha"][0])
+    g["image"], g["init"] = sc.image, sc.labels
+    eng = _engine_from_run(g)
+    off = 0
+    for it in range(iters):
+        rec = eng.iterate()
+        n = int(g["acc_len"][it])
+        want = [tuple(int(v) for v in row) for row in g["acc"][off:off + n]]
+        off += n
+        assert rec.accepted == want, (name, it)
+        h = hashlib.sha256(np.ascontiguousarray(eng.labels, np.int32).tobytes()).hexdigest()[:16]
+        assert h == str(g["hashes"][it])
+        assert rec.energy == g["energy"][it]
