@@ -1,24 +1,37 @@
 #!/usr/bin/env python
 """Benchmark of the Region Competition iteration on B200 (driver contract).
 
-Workload (BASELINE.json configs[1]): 2-D 1024x1024
-PS/Poisson, local-mean radius 4, Sobolev width 3 (E = 6), bubbles 16x16 r=10
-init, vanish_grace 5.  A step is one ``RegionCompetition.iterate()`` — particle
-extraction, ΔE, Sobolev filter, ranking and acceptance, plus the resync on
-every 10th iteration — on the device.  Inputs are seeded synthetic images
-(scenes.py); the reference's CPU path is timed beside it.
+Headline workload (N = 1): BASELINE.json configs[3] -- cfg4, the largest
+config that fits one GPU: a 512^3 PS/Poisson volume (64 seeded ellipsoids,
+blur 1.5, Poisson peak 30), local-mean radius 4, Sobolev
+width 3 (E = 6), bubbles 8x8x8 r=15, vanish_grace 5.  A step is one
+``RegionCompetition.iterate()`` -- particle extraction, PS energy, Sobolev
+filter, ranking, exact acceptance, the band refresh of the own-label fields
+and the every-10th-iteration resync -- on the device.  The timed window is
+iterations W+1 .. W+K (default 6-25).
+
+Metric (BASELINE.json): Sobolev particle-interactions/s over the whole
+iteration (interactions = sum over particles of the partners within the
+cutoff, ``len(CellList.pairs)``), plus iterations/s and the HBM roofline of
+the energy + Sobolev kernels.  Interactions/s is size-independent, which is
+what lets the reference arm -- the CPU restatement of the reference, which
+cannot hold cfg4 (its dense PS fields need 1 TiB) and takes
+seconds per iteration on a 64^3 sample -- be compared with the GPU run.
+
+Extra keys: the cfg2 line (configs[1], 1024^2 PS/Poisson, iterations 6-25
+and the full 100-iteration run), fp32 mode, the Sobolev-kernel sweep
+(configs[4], 10^4 - 10^8 particles x w = 1, 2, 4, 8), end-to-end timing
+through the public API from host buffers, clocks.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-Under torchrun each rank runs an independent image (seed 2 + rank): weak
-scaling, no data-path collective (the batched configs shard by image).
+Under torchrun each rank runs an independent volume (seed 4 + rank): weak
+scaling, no data-path collective.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -29,11 +42,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Sobolev particle-interactions/s and iterations/s; % of HBM roofline"
+UNIT = "particle-interactions/s"
 # The reference's drift check is absolute (1e-6, optimizer.py:45).  On cfg2
 # |E| ~ 4.8e7 (ulp 7.5e-9) and ~3e5 ledger additions happen per 10 iterations,
 # so the reference's own ledger drifts past 1e-6 by iteration 20 (measured:
 # 1.07e-6, identical on the oracle and on the GPU).  Both arms use 1e-3.
 DRIFT_TOL = 1e-3
+WORKLOAD = ("cfg4: 3-D 512^3 PS/Poisson R=4, Sobolev w=3 (E=6), 64 ellipsoids, blur 1.5, "
+            "Poisson peak 30, bubbles 8x8x8 r=15; timed iterations W+1..W+K")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_traffic_cfg4.json")
 
 
 def _dist():
@@ -91,27 +108,18 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows), "source": "NVML in-process"}
 
 
-def scene_for(rank: int, small: bool = False):
-    import scenes
-    if small:
-        return scenes.cfg2_small(seed=2 + rank)
-    return scenes.cfg2(seed=2 + rank)
-
-
-def ball_band_sites(labels, xs, radius):
-    """B_R: lattice sites within distance R of a particle."""
-    from scipy import ndimage
-    mask = np.zeros(labels.size, bool)
-    mask[xs] = True
-    mask = mask.reshape(labels.shape)
-    g = np.meshgrid(*([np.arange(-radius, radius + 1)] * labels.ndim), indexing="ij")
-    fp = sum(a * a for a in g) <= radius * radius
-    return int(ndimage.binary_dilation(mask, structure=fp).sum())
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def band_sites_device(labels_shape, xs, radius, device):
-    """B_R on the device (bookkeeping for the large-config roofline): sites
-    within Euclidean distance R of a particle, by a ball convolution."""
+    """B_R of SURVEY §8(d): lattice sites within Euclidean distance R of a
+    particle site (bookkeeping for the roofline, outside the timed region)."""
     import torch
     n = int(np.prod(labels_shape))
     m = torch.zeros(n, dtype=torch.float16, device=device)
@@ -130,64 +138,100 @@ def band_sites_device(labels_shape, xs, radius, device):
     return int((out > 0.5).sum().item())
 
 
-def large_config(P, local, peak):
-    """BASELINE configs[3] (cfg4: 512^3 PS/Poisson, R = 4, Sobolev w = 3) on
-    this GPU: the energy (K5) + Sobolev (K6) kernels at N ~ 10^7 particles,
-    where their HBM roofline is the meaningful bound.  Iterations 4-5 from the
-    bubbles init, CUDA-event phase times on the engine stream; bytes per
-    SURVEY §8(d) (29N + 24B_R for K5, 28N for K6)."""
-    import torch
-    import scenes
-    sc = scenes.cfg4()
+def _configs(P, sc, precision="fp64"):
     ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
-    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
-    eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg,
-                              device=local)
-    for _ in range(3):
+    scfg = P.SobolevParams(sc.length_scale)
+    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL,
+                             precision=precision)
+    return ecfg, scfg, ocfg
+
+
+def timed_window(P, sc, local, warmup, steps, flush, precision="fp64", detail=True):
+    """W untimed iterations, then K iterations each bracketed by CUDA events
+    on the engine's stream (L2 flushed before each)."""
+    import torch
+    ecfg, scfg, ocfg = _configs(P, sc, precision)
+    eng = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    for _ in range(warmup):
         eng.iterate()
-    k5 = k6 = it_ms = 0.0
-    b5 = b6 = 0.0
-    n_tot = pairs = 0
-    steps = 2
+    torch.cuda.synchronize()
+    out = {"ms": [], "pairs": 0, "phase": np.zeros(6), "launches": 0, "iterations": [],
+           "ctr": {}}
     for _ in range(steps):
-        eng.iterate()
-        t, _ = eng.timings()
-        k5 += t[1]
-        k6 += t[2]
-        it_ms += t[5]
-        xs = eng.last_candidates[0]
-        n = len(xs)
-        n_tot += n
-        pairs += eng.last_pairs
-        # the band of this iteration's particles on its start raster: the
-        # particle sites are that raster's contour, so the ball band is the
-        # same set whichever raster the labels come from
-        B = band_sites_device(sc.image.shape, xs, sc.smooth_radius, f"cuda:{local}")
-        b5 += 29 * n + 24 * B
-        b6 += 28 * n
+        flush.zero_()  # L2 flush between timed iterations (126 MB L2 < 512 MB)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rec = eng.iterate()
+        e1.record(stream)
+        e1.synchronize()
+        out["ms"].append(e0.elapsed_time(e1))
+        out["pairs"] += eng.last_pairs
+        out["iterations"].append(rec.iteration)
+        if detail:
+            t, nl = eng.timings()
+            out["phase"] += np.array(t)
+            out["launches"] += nl
+            for k, v in eng.counters().items():
+                out["ctr"][k] = out["ctr"].get(k, 0) + v
     del eng
-    torch.cuda.empty_cache()
-    a5 = b5 / (k5 / 1e3) / 1e9
-    a6 = b6 / (k6 / 1e3) / 1e9
-    a56 = (b5 + b6) / ((k5 + k6) / 1e3) / 1e9
-    return {"workload": "cfg4: 3-D 512^3 PS/Poisson R=4, Sobolev w=3 (E=6), bubbles 8x8x8 "
-                        "r=15, iterations 4-5", "particles_per_iteration": n_tot / steps,
-            "iteration_ms": it_ms / steps, "k5_ms": k5 / steps, "k6_ms": k6 / steps,
-            "particle_interactions_per_s": pairs / (k6 / 1e3),
-            "roofline_k5_k6": {"bound": "hbm", "achieved": a56, "peak": peak, "unit": "GB/s",
-                               "frac": a56 / peak, "k5_GBs": a5, "k6_GBs": a6,
-                               "algorithmic_bytes_per_iteration": (b5 + b6) / steps,
-                               "note": "K5 is fp64-log/issue bound (ncu: FP64 pipe ~50 %, "
-                                       "issue ~78 %), K6 issue bound at w=3"}}
+    return out
 
 
-def peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
-    except Exception:
-        return 6650.0, "fallback"
+def roofline_bytes(P, sc, local, warmup, steps):
+    """SURVEY §8(d) algorithmic bytes of K5 (29 N + 24 B_R) and K6 (28 N) per
+    timed iteration: a second engine replays the same (deterministic)
+    iterations after the timed loop and counts N and B_R."""
+    ecfg, scfg, ocfg = _configs(P, sc)
+    er = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
+    for _ in range(warmup):
+        er.iterate()
+    b5 = b6 = 0.0
+    particles = 0
+    for _ in range(steps):
+        er.iterate()
+        xs = er.last_candidates[0]
+        n = len(xs)
+        particles += n
+        if n:
+            B = band_sites_device(sc.image.shape, xs, sc.smooth_radius, f"cuda:{local}")
+            b5 += 29 * n + 24 * B
+            b6 += 28 * n
+    del er
+    return b5, b6, particles
+
+
+def sweep_points(points, widths, reps, flush, peak):
+    """BASELINE configs[4], second part: K6 alone over sphere-union contours."""
+    import torch
+    from paper_1403_0240_b200.sweep import SobolevSweep
+    lattices = {"1e4": ((64, 64, 64), 3), "1e5": ((128, 128, 128), 24),
+                "1e6": ((256, 256, 256), 240), "1e7": ((512, 512, 512), 2400),
+                "1e8": ((512, 2048, 2048), 24000)}
+    rows = []
+    for pt in points:
+        shape, nsph = lattices[pt]
+        for w in widths:
+            sw = SobolevSweep(shape, nsph, w, seed=11)
+            for _ in range(2):
+                sw.run()
+            tot_ms, pairs = 0.0, 0
+            for _ in range(reps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                pairs, ms = sw.run()
+                tot_ms += ms
+            ms = tot_ms / reps
+            n = sw.n_particles
+            gbs = 28.0 * n / (ms / 1e3) / 1e9
+            rows.append({"point": pt, "width": w, "particles": n, "pairs": pairs,
+                         "k6_ms": round(ms, 4), "interactions_per_s": pairs / (ms / 1e3),
+                         "alg_GBs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4)})
+            del sw
+            torch.cuda.empty_cache()
+    return rows
 
 
 def run_ours(args):
@@ -198,15 +242,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1403_0240_b200 as P
-
-    sc = scene_for(rank, args.small)
-    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
-    scfg = P.SobolevParams(sc.length_scale)
-    ocfg = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace,
-                             drift_tolerance=DRIFT_TOL)
-    eng = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
-    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    import scenes
 
     def barrier():
         torch.cuda.synchronize()
@@ -214,142 +250,146 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        eng.iterate()
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        return float(t.item())
+
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    peak, peak_kind = peaks()
+    sc = scenes.cfg2(seed=2 + rank) if args.workload == "cfg2" else scenes.cfg4(seed=4 + rank)
+
+    # ---- the headline: timed window on the device --------------------------
     barrier()
-    ms_total = 0.0
-    phase = np.zeros(6)
-    launches = 0
-    pairs = 0
-    particles = 0
-    alg_bytes = 0.0
-    energy_sob_ms = 0.0
-    records = []
-    ctr_sum = {}
     with Clocks(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()  # L2 flush between timed iterations (126 MB L2 < 512 MB)
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            rec = eng.iterate()
-            e1.record(stream)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1)
-            ms_total += ms
-            t, nl = eng.timings()
-            phase += np.array(t)
-            launches += nl
-            pairs += eng.last_pairs
-            energy_sob_ms += t[1] + t[2]
-            records.append((rec.iteration, rec.moves, rec.particles, ms))
-            for k, v in eng.counters().items():
-                ctr_sum[k] = ctr_sum.get(k, 0) + v
-    # roofline bookkeeping (host-side, so kept out of the timed loop): replay
-    # the same iterations on a second engine -- the iteration is
-    # deterministic -- and count the algorithmic bytes of each timed one
-    if args.roofline:
-        er = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
-        for _ in range(args.warmup):
-            er.iterate()
-        for _ in range(args.steps):
-            lab_before = er.labels
-            er.iterate()
-            xs = er.last_candidates[0]
-            particles += len(xs)
-            if len(xs):
-                B = ball_band_sites(lab_before, xs, sc.smooth_radius)
-                alg_bytes += 29 * len(xs) + 24 * B + 28 * len(xs)
-        del er
+        win = timed_window(P, sc, local, args.warmup, args.steps, flush)
     barrier()
-    tmax = ms_total
-    if ws > 1:
-        tt = torch.tensor([ms_total], device=f"cuda:{local}", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        tmax = float(tt.item())
-    value = args.steps * ws / (tmax / 1e3)
+    ms_total = sum(win["ms"])
+    tmax = max_over_ranks(ms_total)
+    pairs_all = sum_over_ranks(float(win["pairs"]))
+    value = pairs_all / (tmax / 1e3)
+    its = args.steps * ws / (tmax / 1e3)
+    phase = win["phase"] / args.steps
 
-    # fp32 mode (same workload, gradient path in fp32): device-timed steps
-    fp32_value = None
+    # ---- roofline of the energy (K5) + Sobolev (K6) kernels -----------------
+    roof = None
+    if args.roofline:
+        b5, b6, particles = roofline_bytes(P, sc, local, args.warmup, args.steps)
+        k5_ms, k6_ms = float(win["phase"][1]), float(win["phase"][2])
+        ach = (b5 + b6) / ((k5_ms + k6_ms) / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(TRAFFIC_FILE) as f:
+                tdoc = json.load(f)
+            traffic = tdoc["energy_plus_sobolev_dram_bytes_per_iteration"]
+        except Exception:
+            pass
+        shares = phase / max(phase[5], 1e-9)
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_iteration": (b5 + b6) / args.steps,
+                "k5_GBs": b5 / (k5_ms / 1e3) / 1e9, "k6_GBs": b6 / (k6_ms / 1e3) / 1e9,
+                "k5_ms_per_iteration": k5_ms / args.steps,
+                "k6_ms_per_iteration": k6_ms / args.steps,
+                "particles_per_iteration": particles / args.steps,
+                "kernels": "K5 PS energy (k_delta_ps3d) + K6 Sobolev (k_sob_pack + "
+                           "k_sobolev_pk): SURVEY §8(d) bytes 29N + 24B_R + 28N per iteration "
+                           "over the same window, timed by CUDA events on the engine stream; "
+                           "traffic = ncu dram bytes of K5+K6 per iteration "
+                           f"({os.path.relpath(TRAFFIC_FILE, ROOT)})",
+                "other_bounds": "K5 evaluates one fp64 log and one division per ball hit "
+                                "(FP64 issue bound, ncu); K6 at w=3 in 3-D visits 93 stencil "
+                                "sites per particle (issue bound)",
+                "dominant": {"phase": "accept (K8 v3 dataflow + band refresh + ledger)",
+                             "share": float(shares[4]),
+                             "bound": "latency (dependency waits, BFS), not bandwidth"}}
+
+    # ---- fp32 gradient path, same window --------------------------------------
+    fp32 = None
     if args.fp32:
-        o32 = P.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL,
-                                precision="fp32")
-        e32 = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, o32, device=local)
-        st32 = torch.cuda.ExternalStream(e32.stream, device=torch.device("cuda", local))
-        for _ in range(args.warmup):
-            e32.iterate()
-        t32 = 0.0
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            a0 = torch.cuda.Event(enable_timing=True)
-            a1 = torch.cuda.Event(enable_timing=True)
-            a0.record(st32)
-            e32.iterate()
-            a1.record(st32)
-            a1.synchronize()
-            t32 += a0.elapsed_time(a1)
-        fp32_value = args.steps * ws / (t32 / 1e3)
-        del e32
+        w32 = timed_window(P, sc, local, args.warmup, args.steps, flush, "fp32", detail=False)
+        t32 = max_over_ranks(sum(w32["ms"]))
+        fp32 = {"value": sum_over_ranks(float(w32["pairs"])) / (t32 / 1e3), "unit": UNIT,
+                "iterations_per_s": args.steps * ws / (t32 / 1e3),
+                "what": "same window, raw increments + Sobolev filter in fp32 (gradients rtol "
+                        "1e-4, Dice >= 0.999: tests/test_gpu_fp32.py)"}
 
-    # the whole configured run (BASELINE configs[1]: 100 iterations from the
-    # bubbles init), device-timed on the engine's stream: later iterations
-    # carry more particles and harder topology tests than the timed window
-    full = None
-    if args.full_run:
-        ef = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg, device=local)
-        stf = torch.cuda.ExternalStream(ef.stream, device=torch.device("cuda", local))
-        torch.cuda.synchronize()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stf)
-        for _ in range(sc.iterations):
-            ef.iterate()
-        f1.record(stf)
-        f1.synchronize()
-        full_ms = f0.elapsed_time(f1)
-        if ws > 1:
-            tt = torch.tensor([full_ms], device=f"cuda:{local}", dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            full_ms = float(tt.item())
-        full = {"iterations": sc.iterations, "device_ms": full_ms,
-                "iterations_per_s": sc.iterations * ws / (full_ms / 1e3),
-                "what": f"complete {sc.iterations}-iteration cfg2 run from the initial labels "
-                        "(device time incl. resyncs and host round trips)"}
-        del ef
-
-    # end-to-end through the public API from host buffers: construct from
-    # pinned host arrays (H2D), iterate K times (each reads back its record),
-    # read the labels back (D2H); wall clock, max over ranks.
-    img_h = torch.from_numpy(np.ascontiguousarray(sc.image, np.float64)).pin_memory().numpy()
+    # ---- end to end through the public API from host buffers ----------------
+    # RegionCompetition(float32 host image, int32 host labels) -- the image
+    # crosses PCIe as float32 and is promoted on the device, inside the timed
+    # region -- then W + K iterate() (each reads its record back) and the
+    # labels back to the host; wall clock, max over ranks.
+    img_h = torch.from_numpy(np.ascontiguousarray(sc.image, np.float32)).pin_memory().numpy()
     lab_h = torch.from_numpy(np.ascontiguousarray(sc.labels, np.int32)).pin_memory().numpy()
+    ecfg, scfg, ocfg = _configs(P, sc)
     barrier()
     t0 = time.perf_counter()
     e2 = P.RegionCompetition(img_h, lab_h, ecfg, scfg, ocfg, device=local)
     t_ctor = time.perf_counter()
+    e2e_pairs = 0
     for _ in range(args.warmup + args.steps):
         e2.iterate()
+        e2e_pairs += e2.last_pairs
     t_it = time.perf_counter()
     out_labels = e2.labels
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_parts = {"construct_ms": round(1e3 * (t_ctor - t0), 3),
                  "iterate_ms": round(1e3 * (t_it - t_ctor), 3),
                  "labels_ms": round(1e3 * (time.perf_counter() - t_it), 3)}
-    if ws > 1:
-        tt = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(tt.item())
     n_e2e = args.warmup + args.steps
     del e2
 
+    # ---- the cfg2 line (configs[1]) -------------------------------------------
+    cfg2 = None
+    if args.cfg2 and args.workload != "cfg2":
+        s2 = scenes.cfg2(seed=2 + rank)
+        w2 = timed_window(P, s2, local, args.warmup, args.steps, flush)
+        t2 = max_over_ranks(sum(w2["ms"]))
+        cfg2 = {"workload": "cfg2: 2-D 1024^2 PS/Poisson R=4, Sobolev w=3 (E=6), bubbles "
+                            "16x16 r=10", "iterations": [w2["iterations"][0], w2["iterations"][-1]],
+                "iterations_per_s": args.steps * ws / (t2 / 1e3),
+                "interactions_per_s": sum_over_ranks(float(w2["pairs"])) / (t2 / 1e3),
+                "ms_per_step": t2 / args.steps,
+                "phase_ms_per_iteration": dict(zip(
+                    ["extract", "energy", "sobolev", "rank", "accept+rescan", "iterate"],
+                    (w2["phase"] / args.steps).round(4).tolist())),
+                "reference_window": _recorded("r02_oracle_cfg2_window.json")}
+        if args.full_run:
+            ecfg2, scfg2, ocfg2 = _configs(P, s2)
+            ef = P.RegionCompetition(s2.image, s2.labels, ecfg2, scfg2, ocfg2, device=local)
+            stf = torch.cuda.ExternalStream(ef.stream, device=torch.device("cuda", local))
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stf)
+            for _ in range(s2.iterations):
+                ef.iterate()
+            f1.record(stf)
+            f1.synchronize()
+            full_ms = max_over_ranks(f0.elapsed_time(f1))
+            cfg2["full_run"] = {"iterations": s2.iterations, "device_ms": full_ms,
+                                "iterations_per_s": s2.iterations * ws / (full_ms / 1e3)}
+            del ef
+
+    sweep = None
+    if args.sweep and rank == 0:
+        sweep = sweep_points(args.sweep_points.split(","), [1, 2, 4, 8], 3, flush, peak)
+
     if rank == 0:
-        peak, peak_kind = peaks()
         line = {
             "metric": METRIC,
             "value": value,
-            "unit": "iterations/s",
+            "unit": UNIT,
             "n_gpus": ws,
             "steps": args.steps,
             "warmup": args.warmup,
@@ -358,83 +398,98 @@ def run_ours(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (scenes.cfg2: seeded ellipses, blur 1.5, Poisson peak 50)",
-            "config": {"workload": "cfg2: 2-D 1024x1024 PS/Poisson R=4, Sobolev w=3 (E=6), "
-                                   "bubbles 16x16 r=10, iterations continue from warm-up",
+            "data": "synthetic (scenes.cfg4: seeded ellipsoids, reference blur 1.5 + "
+                    "poissonize peak 30 on the device, bit-identical to rcseg.synth)",
+            "config": {"workload": WORKLOAD if args.workload == "cfg4" else args.workload,
                        "drift_tolerance": DRIFT_TOL,
-                       "l2": "flushed between timed iterations (512 MB write)",
-                       "parallelism": f"{ws} independent images (one per GPU)"},
-            "particle_interactions_per_s": pairs / max(1e-9, phase[2] / 1e3),
-            "interactions_per_iteration": pairs / args.steps,
-            "particles_per_iteration": particles / args.steps if particles else None,
+                       "l2": "inputs (0.5 GB labels, 1 GB image) larger than L2; also "
+                             "flushed between timed iterations (512 MB write)",
+                       "parallelism": f"{ws} independent volumes (one per GPU)"},
+            "iterations_per_s": its,
+            "timed_iterations": [win["iterations"][0], win["iterations"][-1]],
+            "interactions_per_iteration": win["pairs"] / args.steps,
             "phase_ms_per_iteration": dict(zip(["extract", "energy", "sobolev", "rank",
                                                 "accept+rescan", "iterate"],
-                                               (phase / args.steps).round(4).tolist())),
-            "step_ms": [round(r[3], 3) for r in records],
-            "fp32_mode": {"value": fp32_value, "unit": "iterations/s",
-                          "what": "same workload, raw increments + Sobolev filter in fp32 "
-                                  "(gradients rtol 1e-4, Dice >= 0.999: tests/test_gpu_fp32.py)"},
-            "full_run": full,
-            "gpu_launches": int(launches),
-            "acceptance_per_iteration": {k: v / args.steps for k, v in ctr_sum.items()},
+                                               phase.round(4).tolist())),
+            "step_ms": [round(x, 3) for x in win["ms"]],
+            "gpu_launches": int(win["launches"]),
+            "acceptance_per_iteration": {k: v / args.steps for k, v in win["ctr"].items()},
             "clocks": clk.summary(),
-            "e2e": {"value": n_e2e * ws / e2e_s, "unit": "iterations/s",
+            "e2e": {"value": sum_over_ranks(float(e2e_pairs)) / e2e_s, "unit": UNIT,
+                    "iterations_per_s": n_e2e * ws / e2e_s,
                     "h2d_bytes_per_step": (img_h.nbytes + lab_h.nbytes) / n_e2e,
                     "d2h_bytes_per_step": (out_labels.nbytes + 64 * n_e2e) / n_e2e,
-                    "what": "RegionCompetition(host image, host labels) + K iterate() + labels, "
-                            "wall clock", "parts": e2e_parts},
+                    "what": "RegionCompetition(float32 host image, host labels) + W+K "
+                            "iterate() + labels back, wall clock", "parts": e2e_parts},
+            "fp32_mode": fp32,
+            "cfg2": cfg2,
+            "k6_sweep": sweep,
         }
-        if args.roofline and energy_sob_ms > 0:
-            ach = alg_bytes / (energy_sob_ms / 1e3) / 1e9
-            traffic = None
-            try:
-                with open(os.path.join(ROOT, "profiles", "r01g_traffic.json")) as f:
-                    traffic = json.load(f)["energy_plus_sobolev_dram_bytes"]
-            except Exception:
-                pass
-            shares = phase / max(phase[5], 1e-9)
-            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak,
-                                "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
-                                "peak_kind": peak_kind,
-                                "algorithmic_bytes_per_iteration": alg_bytes / args.steps,
-                                "kernels": "K5 PS energy + K6 Sobolev (SURVEY §8d bytes: "
-                                           "29N + 24B_R + 28N per iteration); traffic = ncu "
-                                           "dram bytes of one iteration (profiles/)",
-                                "dominant": {"phase": "accept (K8 v3 + exact ledger/stats)",
-                                             "share": float(shares[4]),
-                                             "bound": "latency / FP64 issue, DRAM < 1 % (ncu)"}}
-        if args.large:
-            line["large_config"] = large_config(P, local, peak)
-        if args.cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args)
+        if roof is not None:
+            line["roofline"] = roof
+        if args.cpu_baseline and ws == 1:
+            line["cpu_baseline"] = cpu_baseline(budget_s=20.0)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(args, steps=None, budget_s=25.0):
-    """The oracle port (oracle/rc_oracle.py, a numpy restatement of the
-    reference; single-threaded like the reference) on the host cores, on a
-    bounded sample of the same workload: the first iterations of cfg2."""
+def _recorded(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---- the reference's CPU path (oracle port) ----------------------------------
+
+def _sample_scene():
+    """cfg4's bounded CPU sample (scenes.cfg4_sample, 64^3), generated by the
+    CPU restatement of the reference's synth pipeline (no device code)."""
+    import scenes
+    from oracle import synth_oracle as SO
+    scenes.use_backend(blur=SO.blur,
+                       poissonize=lambda img, psnr, seed: SO.poissonize(img, psnr, seed))
+    try:
+        return scenes.cfg4_sample()
+    finally:
+        scenes.use_backend()
+
+
+def _oracle_steps(sc, warmup, steps, cap_s):
+    """Time oracle iterations (perf_counter around iterate() only, as the
+    reference's IterationRecord.seconds does); the interaction count of each
+    timed iteration is counted afterwards, outside the timer."""
     from oracle import rc_oracle as O
-    sc = scene_for(0, args.small)
     cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
-    t0 = time.perf_counter()
     eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
                          sc.length_scale, config=cfg)
-    t_init = time.perf_counter() - t0
-    done = 0
-    t1 = time.perf_counter()
-    while True:
+    t_all = time.perf_counter()
+    for _ in range(warmup):
         eng.iterate()
-        done += 1
-        el = time.perf_counter() - t1
-        if (steps is not None and done >= steps) or (steps is None and el > budget_s):
+    secs, pairs, idx = 0.0, 0, []
+    while len(idx) < steps:
+        t0 = time.perf_counter()
+        rec = eng.iterate()
+        secs += time.perf_counter() - t0
+        xs = eng.last_candidates[0]
+        coords = np.stack(np.unravel_index(xs, sc.image.shape), axis=1)
+        pairs += O.pair_count(coords, sc.length_scale) if len(xs) else 0
+        idx.append(rec.iteration)
+        if time.perf_counter() - t_all > cap_s:
             break
-    el = time.perf_counter() - t1
-    return {"value": done / el, "unit": "iterations/s", "cores": 1, "kind": "port",
-            "sample": f"first {done} iterations of cfg2 (after a {t_init:.1f} s constructor), "
-                      f"oracle port of the reference, 1 thread"}
+    return secs, pairs, idx
+
+
+def cpu_baseline(budget_s=20.0):
+    sc = _sample_scene()
+    secs, pairs, idx = _oracle_steps(sc, 0, 10 ** 6, budget_s)
+    return {"value": pairs / secs, "unit": UNIT, "cores": 1, "kind": "port",
+            "iterations_per_s": len(idx) / secs,
+            "sample": f"iterations {idx[0]}-{idx[-1]} of cfg4's 64^3 sample (scenes.cfg4_sample: "
+                      "4 ellipsoids, bubbles:1:15, PS/Poisson R=4, E=6), oracle port of the "
+                      "reference (oracle/rc_oracle.py), 1 thread like the reference"}
 
 
 def run_reference(args):
@@ -443,35 +498,27 @@ def run_reference(args):
         return
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     cap_s = 150.0
-    from oracle import rc_oracle as O
-    sc = scene_for(0, args.small)
-    cfg = O.OptimizerConfig("sobolev", vanish_grace=sc.vanish_grace, drift_tolerance=DRIFT_TOL)
-    eng = O.OracleEngine(sc.image, sc.labels, sc.region, sc.noise, sc.lam, sc.smooth_radius,
-                         sc.length_scale, config=cfg)
-    t_all = time.perf_counter()
-    for _ in range(min(args.warmup, 1)):
-        eng.iterate()
-    done = 0
-    t0 = time.perf_counter()
-    while done < args.steps:
-        eng.iterate()
-        done += 1
-        if time.perf_counter() - t_all > cap_s:
-            break
-    el = time.perf_counter() - t0
-    v = done / el
-    line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": ws, "steps": done,
-            "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * el / done,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (scenes.cfg2)", "impl": "reference",
-            "config": {"workload": "cfg2: 2-D 1024x1024 PS/Poisson R=4, Sobolev w=3 (E=6), "
-                                   "bubbles 16x16 r=10"},
-            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
-                             "sample": f"{done} iterations of cfg2 after {min(args.warmup, 1)} "
-                                       f"warm-up (capped at {cap_s:.0f} s), oracle port of "
-                                       "the reference, single-threaded like the reference"},
-            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    sc = _sample_scene()
+    warm = min(args.warmup, 1)
+    secs, pairs, idx = _oracle_steps(sc, warm, args.steps, cap_s)
+    v = pairs / secs
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": len(idx),
+            "warmup": warm, "ms_per_step": 1e3 * secs / len(idx), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (scenes.cfg4_sample via oracle/synth_oracle.py)",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "drift_tolerance": DRIFT_TOL,
+                       "l2": "inputs (0.5 GB labels, 1 GB image) larger than L2; also "
+                             "flushed between timed iterations (512 MB write)",
+                       "parallelism": f"{ws} independent volumes (one per GPU)"},
+            "iterations_per_s": len(idx) / secs,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"iterations {idx[0]}-{idx[-1]} of cfg4's 64^3 sample "
+                                       f"(scenes.cfg4_sample; capped at {cap_s:.0f} s): the "
+                                       "oracle port holds dense (labels x sites) PS fields like "
+                                       "the reference, so cfg4 itself (1 TiB) cannot run; "
+                                       "single-threaded like the reference"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -481,13 +528,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--small", action="store_true", help="256^2 crop (debug)")
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg2"])
     ap.add_argument("--no-roofline", dest="roofline", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-fp32", dest="fp32", action="store_false")
+    ap.add_argument("--no-cfg2", dest="cfg2", action="store_false")
     ap.add_argument("--no-full-run", dest="full_run", action="store_false")
-    ap.add_argument("--no-large", dest="large", action="store_false",
-                    help="skip the cfg4 (512^3) energy + Sobolev roofline block")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--sweep-points", default="1e4,1e5,1e6,1e7,1e8")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

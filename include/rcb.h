@@ -170,6 +170,14 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
                           const int64_t *dims, const rcb_energy_cfg *ecfg,
                           const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg,
                           int32_t device, void *stream, rcb_engine **out);
+/* As rcb_engine_create, with the image given as float64 (image_dtype 0) or
+ * float32 (1): a float32 raster crosses PCIe at 4 B/site and is promoted on
+ * the device, exactly as the reference's np.ascontiguousarray(image,
+ * float64) promotes it on the host (optimizer.py:102). */
+int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32_t *labels,
+                             int32_t ndim, const int64_t *dims, const rcb_energy_cfg *ecfg,
+                             const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg,
+                             int32_t device, void *stream, rcb_engine **out);
 void rcb_engine_destroy(rcb_engine *eng);
 /* optimizer.py:122-160 iterate(): extraction, ΔE, Sobolev, rank, acceptance. */
 int32_t rcb_engine_iterate(rcb_engine *eng, rcb_iter_record *rec);

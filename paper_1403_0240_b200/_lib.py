@@ -70,6 +70,7 @@ SIGNATURES = {
     "rcb_ball_sum": [_P, _I32, _P, _I32, _P],
     "rcb_smooth_fields": [_P, _P, _I32, _P, _I32, _I32, _P, _P],
     "rcb_engine_create": [_P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P],
+    "rcb_engine_create_ex": [_P, _I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P],
     "rcb_engine_destroy": [_P],
     "rcb_engine_iterate": [_P, _P],
     "rcb_engine_get_labels": [_P, _P],

@@ -145,6 +145,8 @@ struct rcb_engine {
   bool cur_par = false;
   DBuf<int4> pk;  // K6 packed partner records
   bool sob_packed = false;
+  bool sob_site = false;  // w = 1: the stencil is the particle's own site (k_sobolev_site)
+  double w0 = 0.0;
   int nwt = 0;
   DBuf<int64_t> acc;
   // parallel acceptance state (accept_par.cu)
@@ -161,6 +163,8 @@ struct rcb_engine {
   DBuf<unsigned long long> ufp, job, wpk, eval_per, ufq, qmark, qstate;
   DBuf<uint32_t> qlist, qscr, bigmap, bigfr2;
   DBuf<uint8_t> bigfg2;
+  DBuf<uint32_t> bigtouch;
+  DBuf<int2> bigtouch_n;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
   DBuf<unsigned long long> bigkey;
@@ -217,7 +221,8 @@ struct rcb_engine {
       bigfr.release(s); bigtag.release(s); bigfg.release(s); tdbg.release(s); lab_ptr.release(s); lbox.release(s); colb.release(s);
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
-      bigmap.release(s); bigfr2.release(s); bigfg2.release(s);
+      bigmap.release(s); bigfr2.release(s); bigfg2.release(s); bigtouch.release(s);
+      bigtouch_n.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -298,11 +303,33 @@ struct CtorLog {
 };
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+__global__ void k_promote_f32(const float *__restrict__ src, int64_t n, double *__restrict__ dst) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = (double)src[i];  // exact, = numpy's astype(float64) (optimizer.py:102)
+}
+}  // namespace
+
+extern "C" {
+
 int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t ndim,
                           const int64_t *dims, const rcb_energy_cfg *ecfg,
                           const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg, int32_t device,
                           void *stream, rcb_engine **out) {
+  return rcb_engine_create_ex(image, 0, labels, ndim, dims, ecfg, scfg, ocfg, device, stream,
+                              out);
+}
+
+int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32_t *labels,
+                             int32_t ndim, const int64_t *dims, const rcb_energy_cfg *ecfg,
+                             const rcb_sobolev_cfg *scfg, const rcb_opt_cfg *ocfg, int32_t device,
+                             void *stream, rcb_engine **out) {
   *out = nullptr;
+  if (image_dtype != 0 && image_dtype != 1)
+    return fail(RCB_ERR_VALUE, "image_dtype must be 0 (float64) or 1 (float32)");
   CtorLog clog;
   RCB_TRY(check_device());
   RCB_TRY(check_lattice(ndim, dims));
@@ -392,7 +419,16 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   }
   clog.mark("prime");
   TRYB(upload(e->L, labels, V, s));
-  TRYB(upload(e->I, image, V, s));
+  if (image_dtype == 1) {  // float32 input: 4 B/site over PCIe, promoted on the device
+    TRYB(upload(e->I32, static_cast<const float *>(image), V, s));
+    TRYB(e->I.reserve(V, s));
+    k_promote_f32<<<std::min<unsigned>(grid_for(V, 256), 148u * 16u), 256, 0, s>>>(e->I32.p, V,
+                                                                                   e->I.p);
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(RCB_ERR_CUDA, "k_promote_f32"));
+    if (!ocfg->fp32) e->I32.release(s);
+  } else {
+    TRYB(upload(e->I, static_cast<const double *>(image), V, s));
+  }
   {
     // input validation on the device (grid.py:24-39; optimizer.py:100-101):
     // label min / max (-> the label count), non-finite and negative
@@ -456,6 +492,8 @@ int32_t rcb_engine_create(const double *image, const int32_t *labels, int32_t nd
   {
     const char *ks = getenv("RCB_K6");  // "scalar": the unpacked K6 (comparison runs)
     e->sob_packed = sobolev_packable(e->nl, e->nst, maxd2) && !(ks && strcmp(ks, "scalar") == 0);
+    e->sob_site = sobolev_site_only(st.data(), e->nst) && !(ks && strcmp(ks, "scalar") == 0);
+    e->w0 = scfg->weights[0];
   }
   if (ocfg->fp32) {
     TRYB(e->I32.reserve(V, s));
@@ -590,6 +628,9 @@ static int32_t engine_score(rcb_engine *e) {
       if (fp32) {
         RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
                                   e->st.p, e->nst, e->wt32.p, p1, e->smooth.p, &d->pairs, s, p0));
+      } else if (e->sob_site) {
+        RCB_TRY(sobolev_site(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, e->w0, p0, p1, h0, h1,
+                             e->smooth.p, &d->pairs, s));
       } else if (e->sob_packed && e->nst > 1) {
         // packed records of the partners K6 reads ([h0, h1) covers the halo);
         // with one stencil row (w = 1) the unpacked kernel reads less
@@ -768,6 +809,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       }
       ParExtra X{};
       X.n_particles = n;
+      X.hcount = e->hwatch + 7;  // spare word of the engine's pinned block
       X.budget = budget;
       X.slot = e->slot.p;
       X.tmp = &e->tmp;
@@ -825,6 +867,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
           X.bigmap = &e->bigmap;
           X.bigfr2 = &e->bigfr2;
           X.bigfg2 = &e->bigfg2;
+          X.bigtouch = &e->bigtouch;
+          X.bigtouch_n = &e->bigtouch_n;
         }
       }
       int nla = 0;

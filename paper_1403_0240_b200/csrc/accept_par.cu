@@ -1,3 +1,4 @@
+#include <mutex>
 #include <climits>
 #include <algorithm>
 // K8 v2 — parallel, exact rank-ordered acceptance (sobolev mode).
@@ -1101,22 +1102,28 @@ __device__ __forceinline__ unsigned long long ld_rlx64(const unsigned long long 
 // Two layouts, chosen per run by the host (ParArgs.wp_bits): 24-bit positions
 // with 16-bit labels, or 27-bit positions with 10-bit labels (more than 2^24
 // candidates, at most 1024 labels: cfg4's late iterations).
-__constant__ uint32_t c_wp_bits;
-__device__ __forceinline__ uint32_t wp_inf() { return (1u << c_wp_bits) - 1u; }
-__device__ __forceinline__ int32_t wp_pend(unsigned long long v) { return (int32_t)(v & wp_inf()); }
-__device__ __forceinline__ int32_t wp_w(unsigned long long v) {
-  return (int32_t)((v >> c_wp_bits) & wp_inf());
+// The layout travels in ParArgs.wp_bits (a kernel argument), so engines with
+// different layouts can run concurrently on one device.
+__device__ __forceinline__ uint32_t wp_inf(uint32_t bits) { return (1u << bits) - 1u; }
+__device__ __forceinline__ int32_t wp_pend(uint32_t bits, unsigned long long v) {
+  return (int32_t)(v & wp_inf(bits));
 }
-__device__ __forceinline__ int32_t wp_lab(unsigned long long v) { return (int32_t)(v >> (2 * c_wp_bits)); }
-__device__ __forceinline__ unsigned long long wp_pack(int32_t pend, int32_t w, int32_t lab) {
-  const uint32_t inf = wp_inf();
+__device__ __forceinline__ int32_t wp_w(uint32_t bits, unsigned long long v) {
+  return (int32_t)((v >> bits) & wp_inf(bits));
+}
+__device__ __forceinline__ int32_t wp_lab(uint32_t bits, unsigned long long v) {
+  return (int32_t)(v >> (2 * bits));
+}
+__device__ __forceinline__ unsigned long long wp_pack(uint32_t bits, int32_t pend, int32_t w,
+                                                      int32_t lab) {
+  const uint32_t inf = wp_inf(bits);
   const uint32_t p = pend < (int32_t)inf ? (uint32_t)pend : inf;
   const uint32_t q = w < (int32_t)inf ? (uint32_t)w : inf;
-  return ((unsigned long long)(uint32_t)lab << (2 * c_wp_bits)) |
-         ((unsigned long long)q << c_wp_bits) | p;
+  return ((unsigned long long)(uint32_t)lab << (2 * bits)) | ((unsigned long long)q << bits) | p;
 }
-__device__ __forceinline__ int32_t df_lab(unsigned long long v, int32_t l0, int32_t pos) {
-  return wp_w(v) < pos ? wp_lab(v) : l0;
+__device__ __forceinline__ int32_t df_lab(uint32_t bits, unsigned long long v, int32_t l0,
+                                          int32_t pos) {
+  return wp_w(bits, v) < pos ? wp_lab(bits, v) : l0;
 }
 __device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
   int32_t v;
@@ -1688,7 +1695,7 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
   int polls = 0;
   for (;;) {
     if (g >= 0) v = ld_rlx64(A.wp + g);
-    const bool p = g >= 0 && wp_pend(v) < pos;
+    const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos;
     if (!__any_sync(0xffffffffu, p)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
@@ -1783,9 +1790,22 @@ __device__ int warp_verdict8(WarpBfs &S, uint32_t alive) {
 
 // Visit site t (settled, label lab) from group g: insert it or record the
 // union with the group that owns it.  Returns true if newly inserted.
+// Large box tier maps are not cleared in full before each flood (a label's
+// grown box can be 10^6 sites, 512 KB, while a flood that resolves in a few
+// levels touches a few hundred words: clearing the box was ~40 GB of DRAM
+// writes per cfg4 iteration).  Each warp lists the words it sets (first
+// touch = CAS from 0) and clears exactly those at the next flood; on list
+// overflow it clears the range the overflowing flood used.
+static constexpr int kBigTouch = 16384;
+
+__device__ __forceinline__ void big_touch(const ParArgs &A, int64_t wid, uint32_t word) {
+  const int k = atomicAdd(&A.bigtouch_n[wid].x, 1);
+  if (k < kBigTouch) A.bigtouch[wid * kBigTouch + k] = word;
+}
+
 template <bool kBox>
 __device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t *nib, int li,
-                                          int t, int g) {
+                                          int t, int g, int64_t big_wid = -1) {
   bool ins = false;
   if (kBox) {
     uint32_t *wp = nib + (li >> 3);
@@ -1800,6 +1820,7 @@ __device__ __forceinline__ bool bfs_visit(const ParArgs &A, WarpBfs &S, uint32_t
       const uint32_t old = atomicCAS(wp, w, w | ((uint32_t)(g + 1) << sh));
       if (old == w) {
         ins = true;
+        if (w == 0 && big_wid >= 0) big_touch(A, big_wid, (uint32_t)(li >> 3));
         break;
       }
       w = old;
@@ -1919,11 +1940,21 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
          (unsigned)rx < (unsigned)bb.bw;
     return (rz * bb.bh + ry) * bb.bw + rx;
   };
+  const int64_t big_wid = kBig ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : -1;
   if (kBox) {
     const int nw = (bb.bd * bb.bh * bb.bw + 7) >> 3;
     if (kBig) {
-      uint4 *n4 = reinterpret_cast<uint4 *>(nib);
-      for (int k = lane; k < (nw + 3) / 4; k += 32) n4[k] = make_uint4(0, 0, 0, 0);
+      const int2 st = make_int2(*(volatile int *)&A.bigtouch_n[big_wid].x,
+                                *(volatile int *)&A.bigtouch_n[big_wid].y);
+      if (st.x >= 0 && st.x <= kBigTouch) {
+        const uint32_t *tl = A.bigtouch + big_wid * kBigTouch;
+        for (int k = lane; k < st.x; k += 32) nib[tl[k]] = 0u;
+      } else {  // unknown or overflowed list: the whole range last used
+        uint4 *n4 = reinterpret_cast<uint4 *>(nib);
+        for (int k = lane; k < (st.y + 3) / 4; k += 32) n4[k] = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      if (lane == 0) A.bigtouch_n[big_wid] = make_int2(0, nw);
       __threadfence_block();
     } else {
       for (int k = lane; k < nw; k += 32) nib[k] = 0;
@@ -1943,6 +1974,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
     if (kBox) {
       bool ok = true;
       const int li = box_index(fz, fy, fx, ok);
+      if (kBig && nib[li >> 3] == 0u) big_touch(A, big_wid, (uint32_t)(li >> 3));
       nib[li >> 3] |= 15u << (4 * (li & 7));  // x itself: never entered
     } else {
       uint32_t h = hash32((uint32_t)f) & (kHW - 1);
@@ -1961,6 +1993,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
       if (kBox) {
         bool ok = true;
         const int li = box_index(zz, yy, xx, ok);
+        if (kBig && nib[li >> 3] == 0u) big_touch(A, big_wid, (uint32_t)(li >> 3));
         nib[li >> 3] |= (uint32_t)(g + 1) << (4 * (li & 7));
       } else {
         const uint32_t site = (uint32_t)((zz * ny + yy) * nx + xx);
@@ -2043,7 +2076,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
         if (!ok[u]) continue;
-        if (wp_pend(pk[u]) < pos) {
+        if (wp_pend((uint32_t)A.wp_bits, pk[u]) < pos) {
           // skipped as not-a for now; remembered for resuming
           atomicOr(&S.gblk, 1u << g[u]);
           S.bsite = t[u];
@@ -2054,8 +2087,8 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
           }
           continue;
         }
-        if (df_lab(pk[u], l0[u], pos) != a) continue;
-        if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u]))
+        if (df_lab((uint32_t)A.wp_bits, pk[u], l0[u], pos) != a) continue;
+        if (bfs_visit<kBox>(A, S, nib, li[u], t[u], g[u], big_wid))
           bfs_push(S, F, nxt, pack_c<k3D>(zq[u], yq[u], xq[u]), g[u]);
       }
     }
@@ -2085,8 +2118,8 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
           const int yq = rq / nx, xq = rq - yq * nx;
           bool okq = true;
           const int lq = box_index(zq, yq, xq, okq);
-          if (okq && df_lab(v, __ldg(A.L + tq), pos) == a &&
-              bfs_visit<kBox>(A, S, nib, lq, (int)tq, gq))
+          if (okq && df_lab((uint32_t)A.wp_bits, v, __ldg(A.L + tq), pos) == a &&
+              bfs_visit<kBox>(A, S, nib, lq, (int)tq, gq, big_wid))
             bfs_push(S, F, nxt, pack_c<k3D>(zq, yq, xq), gq);
         }
       }
@@ -2180,8 +2213,8 @@ __device__ int window31(const ParArgs &A, int32_t pos, int64_t f, int32_t a) {
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const bool st = in[i] && wp_pend(pk[i]) >= pos;
-      const int32_t lab = st ? df_lab(pk[i], l0[i], pos) : -1;
+      const bool st = in[i] && wp_pend((uint32_t)A.wp_bits, pk[i]) >= pos;
+      const int32_t lab = st ? df_lab((uint32_t)A.wp_bits, pk[i], l0[i], pos) : -1;
       const unsigned mp = __ballot_sync(0xffffffffu, st && lab == a);
       const unsigned mu = __ballot_sync(0xffffffffu, in[i] && !st);
       if (lane == rb + i) {
@@ -2285,8 +2318,8 @@ __device__ __noinline__ int window63(const ParArgs &A, int32_t pos, int64_t f, i
       uint64_t mp = 0, mu = 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const bool st = in[i + h] && wp_pend(pk[i + h]) >= pos;
-        const int32_t lab = st ? df_lab(pk[i + h], l0[i + h], pos) : -1;
+        const bool st = in[i + h] && wp_pend((uint32_t)A.wp_bits, pk[i + h]) >= pos;
+        const int32_t lab = st ? df_lab((uint32_t)A.wp_bits, pk[i + h], l0[i + h], pos) : -1;
         mp |= (uint64_t)__ballot_sync(0xffffffffu, st && lab == a) << (32 * h);
         mu |= (uint64_t)__ballot_sync(0xffffffffu, in[i + h] && !st) << (32 * h);
       }
@@ -2392,7 +2425,7 @@ __global__ void k_df_init2(ParArgs A) {
     const uint32_t p = A.order[pos];
     A.pos_of[p] = (int32_t)pos;
     A.dec[pos] = UNDEC;
-    atomicMin(A.wp + A.px[p], ~(unsigned long long)wp_inf() | (unsigned)pos);  // pend field
+    atomicMin(A.wp + A.px[p], ~(unsigned long long)wp_inf((uint32_t)A.wp_bits) | (unsigned)pos);  // pend field
     const int32_t a = A.pown[p];
     if (a > 0) atomicAdd(A.nown + a, 1);
   }
@@ -2664,9 +2697,9 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     }
     const int32_t l0 = gb >= 0 ? __ldg(A.L + gb) : -1;
     const unsigned long long pk = warp_wait_settled(A, gb, pos);
-    const int32_t mine = gb >= 0 ? df_lab(pk, l0, pos) : -1;
+    const int32_t mine = gb >= 0 ? df_lab((uint32_t)A.wp_bits, pk, l0, pos) : -1;
     const unsigned long long pkc = __shfl_sync(0xffffffffu, pk, 13);  // x's own word
-    const int32_t wold = wp_w(pkc), lold = wp_lab(pkc);
+    const int32_t wold = wp_w((uint32_t)A.wp_bits, pkc), lold = wp_lab((uint32_t)A.wp_bits, pkc);
     int32_t lab[27];
 #pragma unroll
     for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
@@ -2719,8 +2752,8 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
             const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
             const unsigned long long wv = ld_rlx64(A.wp + gw);
             const int32_t lw = __ldg(A.L + gw);
-            u = wp_pend(wv) < pos;
-            bit = !u && df_lab(wv, lw, pos) == a;
+            u = wp_pend((uint32_t)A.wp_bits, wv) < pos;
+            bit = !u && df_lab((uint32_t)A.wp_bits, wv, lw, pos) == a;
           }
         }
         const unsigned m = __ballot_sync(0xffffffffu, bit), mu = __ballot_sync(0xffffffffu, u);
@@ -2888,7 +2921,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       // release: the flip (newlab, w) and counts are visible before the
       // decision, the decision before the site word with its next position
       st_rel_u8(A.dec + pos, d);
-      st_rel64(A.wp + f, d == ACC ? wp_pack(next, pos, b) : wp_pack(next, wold, lold));
+      st_rel64(A.wp + f, d == ACC ? wp_pack((uint32_t)A.wp_bits, next, pos, b) : wp_pack((uint32_t)A.wp_bits, next, wold, lold));
       if (sa) st_rel(A.lab_ptr + a, A.lab_ptr[a] + 1);
       if (sb) st_rel(A.lab_ptr + b, A.lab_ptr[b] + 1);
     }
@@ -3941,10 +3974,23 @@ void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s) {
   pending.clear();
 }
 
+__global__ void k_big_state_init(int2 *st, int64_t n, int words) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) st[i] = make_int2(-1, words);
+}
+
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) {
   StageTimer T(s);
   T.mark("start");
-  static int grid_blocks = 0;
+  // one-time kernel attributes and occupancy, per device, under a lock
+  // (engines on several host threads / devices may get here at once)
+  static std::mutex setup_mu;
+  static int grid_blocks_dev[64] = {}, df_blocks_dev[64] = {};
+  int cur_dev = 0;
+  RCB_CUDA(cudaGetDevice(&cur_dev));
+  if (cur_dev < 0 || cur_dev >= 64) return fail(RCB_ERR_CUDA, "device ordinal beyond 63");
+  std::unique_lock<std::mutex> setup_lock(setup_mu);
+  int &grid_blocks = grid_blocks_dev[cur_dev];
   const size_t smem = sizeof(BfsShared);
   if (grid_blocks == 0) {
     RCB_CUDA(cudaFuncSetAttribute(k_accept_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3962,10 +4008,11 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   if (A.box_cap < 0 || A.box_cap > 16 * kHW) A.box_cap = 16 * kHW;
   void *args[] = {&A};
   if (X.accept_mode == 1) {
+    setup_lock.unlock();
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_par, dim3(grid_blocks), dim3(512), args,
                                          smem, s));
   } else {
-    static int df_blocks = 0;
+    int &df_blocks = df_blocks_dev[cur_dev];
     const size_t dsm = sizeof(WarpBfs) * kDfWarps;
     if (df_blocks == 0) {
       RCB_CUDA(cudaFuncSetAttribute(k_accept_df, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3978,6 +4025,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_df does not fit on an SM");
       df_blocks = per_sm * sms;
     }
+    setup_lock.unlock();
     if (A.lat.ndim == 3 && X.bigmap) {
       // large box tier (3-D; in 2-D the 31x31 / 63x63 window tiers catch wide
       // footprints and the tier measured slower): per warp a 4-bit map of up
@@ -3987,7 +4035,18 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       const int64_t vw = (A.lat.V + 7) / 8 + 4;
       A.big_words = (int)(vw < (1 << 18) ? ((vw + 3) & ~3) : (1 << 18));
       A.big_fcap = 1 << 14;
+      uint32_t *const old_map = X.bigmap->p;
       RCB_TRY(X.bigmap->reserve(warps * (size_t)A.big_words, s));
+      RCB_TRY(X.bigtouch->reserve(warps * (size_t)kBigTouch, s));
+      const uint32_t *const old_n = reinterpret_cast<uint32_t *>(X.bigtouch_n->p);
+      RCB_TRY(X.bigtouch_n->reserve(warps, s));
+      if (X.bigmap->p != old_map || reinterpret_cast<uint32_t *>(X.bigtouch_n->p) != old_n) {
+        // fresh memory: every warp's first flood clears its whole slot
+        k_big_state_init<<<grid_for((int64_t)X.bigtouch_n->cap, 256), 256, 0, s>>>(
+            X.bigtouch_n->p, (int64_t)X.bigtouch_n->cap, A.big_words);
+      }
+      A.bigtouch = X.bigtouch->p;
+      A.bigtouch_n = X.bigtouch_n->p;
       RCB_TRY(X.bigfr2->reserve(warps * 2 * (size_t)A.big_fcap, s));
       RCB_TRY(X.bigfg2->reserve(warps * 2 * (size_t)A.big_fcap, s));
       A.bigmap = X.bigmap->p;
@@ -3995,26 +4054,6 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       A.bigfg2 = X.bigfg2->p;
     } else {
       A.bigmap = nullptr;
-    }
-    {
-      // from pinned memory, and only when the layout changes: a copy from a
-      // pageable stack variable is staged synchronously, which held the host
-      // until the stream had drained -- the iteration's remaining launches
-      // then trickled in behind the GPU (host enqueue time == device time)
-      static uint32_t *hbits = nullptr;
-      static int last_bits = -1, last_dev = -1;
-      int dev = 0;
-      RCB_CUDA(cudaGetDevice(&dev));
-      if (!hbits) RCB_CUDA(cudaMallocHost((void **)&hbits, sizeof(uint32_t)));
-      if (A.wp_bits != last_bits || dev != last_dev) {
-        RCB_CUDA(cudaStreamSynchronize(s));  // no earlier run still reads the old layout
-        *hbits = (uint32_t)A.wp_bits;
-        RCB_CUDA(cudaMemcpyToSymbolAsync(c_wp_bits, hbits, sizeof(uint32_t), 0,
-                                         cudaMemcpyHostToDevice, s));
-        RCB_CUDA(cudaStreamSynchronize(s));
-        last_bits = A.wp_bits;
-        last_dev = dev;
-      }
     }
     k_df_init<<<grid_for(N > A.nl ? N : A.nl, 256), 256, 0, s>>>(A, N);
     k_df_init2<<<grid_for(N, 256), 256, 0, s>>>(A);
@@ -4037,8 +4076,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     // small (cfg4: sorting 2N events cost ~20 ms per iteration)
     bool need_lists = true;
     if (N > ((int64_t)1 << 20)) {
-      static unsigned long long *hcount = nullptr;
-      if (!hcount) RCB_CUDA(cudaMallocHost((void **)&hcount, sizeof(unsigned long long)));
+      // the engine's own pinned word: engines in flight on other host
+      // threads must not share it
+      unsigned long long *hcount = X.hcount;
       RCB_CUDA(cudaMemcpyAsync(hcount, A.job + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       RCB_CUDA(cudaStreamSynchronize(s));
       need_lists = *hcount != 0;

@@ -120,6 +120,10 @@ struct ParArgs {
   uint32_t *bigfr2;               // ... and frontiers (2 x big_fcap per warp)
   uint8_t *bigfg2;
   int big_words, big_fcap;
+  // per warp: words of its map set since the last clear (kBigTouch entries)
+  // and {count, dirty range}: count < 0 or > kBigTouch = clear [0, range)
+  uint32_t *bigtouch;
+  int2 *bigtouch_n;
   const int4 *rec;                // dataflow per-position records
 };
 
@@ -135,6 +139,7 @@ struct PendingChain {
 
 struct ParExtra {
   int64_t n_particles, budget;
+  unsigned long long *hcount = nullptr;  // the engine's pinned word (candidate-list count)
   uint32_t *slot;
   DBuf<uint8_t> *tmp;
   int64_t *acc, *moves;
@@ -165,6 +170,8 @@ struct ParExtra {
   std::vector<PendingChain> *pending = nullptr;  // PS: defer the total / total_sq chains here
   DBuf<uint32_t> *bigmap = nullptr, *bigfr2 = nullptr;  // dataflow large box tier (3-D)
   DBuf<uint8_t> *bigfg2 = nullptr;
+  DBuf<uint32_t> *bigtouch = nullptr;
+  DBuf<int2> *bigtouch_n = nullptr;
 };
 
 // input validation (energy.cu): one pass, one small read-back (synchronises s)
@@ -220,6 +227,10 @@ int32_t sobolev_lattice(const uint32_t *site_off, const int32_t *pown, const uin
 bool sobolev_packable(int32_t n_labels, int nrows, int max_d2);
 int32_t sobolev_pack(const uint32_t *px, const int32_t *pown, const int32_t *pcomp,
                      const double *raw, int64_t lo, int64_t hi, int4 *pk, cudaStream_t s);
+bool sobolev_site_only(const Off *rows_host, int nrows);
+int32_t sobolev_site(const uint32_t *px, const int32_t *pown, const int32_t *pcomp,
+                     const double *raw, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
+                     double *out, unsigned long long *pairs, cudaStream_t s);
 int32_t sobolev_packed(const uint32_t *site_off, const int4 *pk, const Lat &lat, const Off *rows,
                        int nrows, const double *wt, int nwt, int64_t p0, int64_t p1, double *out,
                        unsigned long long *pairs, cudaStream_t s);

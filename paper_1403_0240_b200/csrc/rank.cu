@@ -39,8 +39,9 @@ __global__ void k_rank(const double *__restrict__ base, const int32_t *__restric
 // halves, left in particle order by the stable sort, is then put in (full
 // rank key, tie key, particle index) order -- the complete lexsort order.
 // Short runs: insertion sort by the thread that finds the run; long runs
-// (degenerate inputs, e.g. exact ties): a block bitonic sort in shared
-// memory, or for runs beyond its capacity a serial sort.
+// (degenerate inputs, e.g. exact ties on noise-free or integer images): a
+// block bitonic sort in shared memory, or for runs beyond its capacity a
+// block merge sort through global scratch (O(len log^2 len / threads)).
 static constexpr int kShortRun = 32, kBitonic = 4096;
 
 __device__ __forceinline__ bool tie_less(const uint64_t *tie, uint32_t p, uint32_t q) {
@@ -87,7 +88,48 @@ __global__ void k_tie_runs(const uint64_t *__restrict__ key, int64_t n, uint32_t
   }
 }
 
+// Bottom-up merge sort of one run by the whole block: each pass places every
+// element at (its rank in its own half) + (number of elements of the other
+// half before it), found by binary search -- the order is strict (particle
+// index breaks every tie), so the placement is a permutation.
+__device__ void block_merge_sort(uint32_t *o, uint32_t *scratch, int64_t len,
+                                 const uint64_t *rkey, const uint64_t *tie) {
+  uint32_t *src = o, *dst = scratch;
+  for (int64_t w = 1; w < len; w <<= 1) {
+    for (int64_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const int64_t lo = (t / (2 * w)) * (2 * w);
+      const int64_t mid = min(lo + w, len), hi = min(lo + 2 * w, len);
+      const uint32_t v = src[t];
+      int64_t a, b;
+      if (t < mid) {
+        a = mid;
+        b = hi;
+      } else {
+        a = lo;
+        b = mid;
+      }
+      const int64_t base = a;
+      while (a < b) {
+        const int64_t m = (a + b) >> 1;
+        if (rank_less(rkey, tie, src[m], v)) a = m + 1;
+        else b = m;
+      }
+      const int64_t pos = t < mid ? t + (a - base) : lo + (t - mid) + (a - base);
+      dst[pos] = v;
+    }
+    __syncthreads();
+    uint32_t *x = src;
+    src = dst;
+    dst = x;
+  }
+  if (src != o) {
+    for (int64_t t = threadIdx.x; t < len; t += blockDim.x) o[t] = src[t];
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order,
+                                                    uint32_t *__restrict__ scratch,
                                                     const uint64_t *__restrict__ rkey,
                                                     const uint64_t *__restrict__ tie,
                                                     const int64_t *__restrict__ longs,
@@ -99,8 +141,7 @@ __global__ void __launch_bounds__(1024) k_long_runs(uint32_t *__restrict__ order
     const int64_t start = longs[2 * r], len = longs[2 * r + 1];
     uint32_t *o = order + start;
     if (len > kBitonic) {
-      if (threadIdx.x == 0) insertion_by_tie(o, len, rkey, tie);
-      __syncthreads();
+      block_merge_sort(o, scratch + start, len, rkey, tie);
       continue;
     }
     int m = 1;
@@ -166,7 +207,8 @@ int32_t rank_order(const double *base, const int32_t *dint, double lam, int64_t 
   int64_t *longs = reinterpret_cast<int64_t *>(sc.tie2.p);
   k_tie_runs<<<grid_for(n, 256), 256, 0, s>>>(sc.rkey2.p, n, order, sc.rkey.p, sc.tie.p, longs,
                                                nlong);
-  k_long_runs<<<64, 1024, 0, s>>>(order, sc.rkey.p, sc.tie.p, longs, nlong);
+  // sc.idx (the sort's input values) is free now: scratch for the merge sort
+  k_long_runs<<<64, 1024, 0, s>>>(order, sc.idx.p, sc.rkey.p, sc.tie.p, longs, nlong);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

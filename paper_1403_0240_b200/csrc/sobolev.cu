@@ -223,6 +223,64 @@ __global__ void __launch_bounds__(128) k_sobolev_pk(
   }
 }
 
+// ---- K6 at w = 1 (E <= 2): the stencil is the particle's own site ----------
+// The partners of p are the particles of its own site: the run of equal px
+// around p in the (site, competitor)-sorted list, at most 26 long.  A pure
+// streaming pass -- px, owner, competitor, raw in and out, 28 B per particle
+// -- with the run's few neighbours read from L1.  The sums
+// follow the same canonical order (index order within the site) and the same
+// expressions as k_sobolev, so the results are bit-identical.
+__global__ void __launch_bounds__(256) k_sobolev_site(
+    const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+    const int32_t *__restrict__ pcomp, const double *__restrict__ raw, double w0, int64_t p0,
+    int64_t p1, int64_t lo, int64_t hi, double *__restrict__ out,
+    unsigned long long *__restrict__ pairs) {
+  const int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long np = 0;
+  if (p < p1) {
+    const uint32_t f = __ldg(&px[p]);
+    const int32_t own = __ldg(&pown[p]);
+    int64_t s = p, e = p + 1;
+    while (s > lo && __ldg(&px[s - 1]) == f) --s;
+    while (e < hi && __ldg(&px[e]) == f) ++e;
+    double same = 0.0, opp = 0.0;
+    int cs = 0, co = 0;
+    for (int64_t q = s; q < e; ++q) {
+      const double c = w0 * __ldg(&raw[q]);
+      if (__ldg(&pown[q]) == own) {
+        same += c;
+        ++cs;
+      }
+      if (__ldg(&pcomp[q]) == own) {
+        opp += c;
+        ++co;
+      }
+    }
+    np = (unsigned long long)(e - s);
+    const double a = cs > 0 ? same / (double)cs : 0.0;
+    const double b = co > 0 ? opp / (double)co : 0.0;
+    out[p] = a - b;
+  }
+  if (pairs) {
+    for (int sh = 16; sh; sh >>= 1) np += __shfl_down_sync(0xffffffffu, np, sh);
+    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
+  }
+}
+
+bool sobolev_site_only(const Off *rows_host, int nrows) {
+  return nrows == 1 && rows_host[0].dz == 0 && rows_host[0].dy == 0 && rows_host[0].dx == 0;
+}
+
+int32_t sobolev_site(const uint32_t *px, const int32_t *pown, const int32_t *pcomp,
+                     const double *raw, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
+                     double *out, unsigned long long *pairs, cudaStream_t s) {
+  if (p1 <= p0) return RCB_OK;
+  k_sobolev_site<<<grid_for(p1 - p0, 256), 256, 0, s>>>(px, pown, pcomp, raw, w0, p0, p1, lo, hi,
+                                                        out, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 bool sobolev_packable(int32_t n_labels, int nrows, int max_d2) {
   return n_labels <= 65536 && nrows <= kSobRows && max_d2 < kSobW;
 }

@@ -71,6 +71,8 @@ struct rcb_sweep {
   DBuf<Off> st;
   int nst = 0, nwt = 0;
   bool packed = false;
+  bool site = false;  // w = 1: k_sobolev_site
+  double w0 = 0.0;
   DBuf<int4> pk;  // K6 packed partner records
   DBuf<unsigned long long> pairs;
   DBuf<uint8_t> tmp;
@@ -153,6 +155,8 @@ int32_t rcb_sweep_create(int32_t ndim, const int64_t *dims, const float *spheres
     // one stencil row (w = 1): the unpacked kernel reads less (no packing pass)
     w->packed = sobolev_packable(2, w->nst, maxd2) && w->nst > 1 &&
                 !(ks && strcmp(ks, "scalar") == 0);
+    w->site = sobolev_site_only(stv.data(), w->nst) && !(ks && strcmp(ks, "scalar") == 0);
+    w->w0 = scfg->weights[0];
   }
   if (w->packed) TRYB(w->pk.reserve(n, s));
   TRYB(w->st.reserve(stv.size(), s));
@@ -181,7 +185,10 @@ int32_t rcb_sweep_run(rcb_sweep *w, int64_t *pairs, float *ms) {
   cudaStream_t s = w->s;
   RCB_CUDA(cudaMemsetAsync(w->pairs.p, 0, sizeof(unsigned long long), s));
   RCB_CUDA(cudaEventRecord(w->e0, s));
-  if (w->packed) {  // the record packing is part of K6's cost: timed with it
+  if (w->site) {  // w = 1: one streaming pass over the particle list
+    RCB_TRY(sobolev_site(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, w->w0, 0, w->n, 0, w->n,
+                         w->out.p, w->pairs.p, s));
+  } else if (w->packed) {  // the record packing is part of K6's cost: timed with it
     RCB_TRY(sobolev_pack(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, 0, w->n, w->pk.p, s));
     RCB_TRY(sobolev_packed(w->site_off.p, w->pk.p, w->lat, w->st.p, w->nst, w->wt.p, w->nwt, 0,
                            w->n, w->out.p, w->pairs.p, s));

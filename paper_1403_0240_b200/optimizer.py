@@ -119,9 +119,17 @@ class RegionCompetition:
         self.device = int(device)
         self._slab = None
         self._exchange = None
-        self.image = np.ascontiguousarray(image, dtype=np.float64)
-        self.shape = self.image.shape
-        self.conn = conn if conn is not None else Connectivity.default(self.image.ndim)
+        # float32 rasters go to the device as float32 and are promoted there
+        # (exactly numpy's astype, optimizer.py:102); anything else is promoted
+        # to float64 on the host as the reference does
+        if isinstance(image, np.ndarray) and image.dtype == np.float32:
+            src, dtype_code = np.ascontiguousarray(image), 1
+        else:
+            src, dtype_code = np.ascontiguousarray(image, dtype=np.float64), 0
+        self._image_src = src
+        self._image64 = src if dtype_code == 0 else None
+        self.shape = src.shape
+        self.conn = conn if conn is not None else Connectivity.default(src.ndim)
         self.energy_config = energy_config
         self.sobolev_params = sobolev_params if sobolev_params is not None else SobolevParams()
         self.config = config if config is not None else OptimizerConfig()
@@ -136,8 +144,8 @@ class RegionCompetition:
                                  int(self.conn.full_fg), int(cfg.precision == "fp32"))
         dims = _lib.dims_arr(self.shape)
         h = C.c_void_p()
-        _lib.check(_lib.lib.rcb_engine_create(
-            _lib.ptr(self.image), _lib.ptr(lab), lab.ndim, _lib.ptr(dims), C.byref(self._ecfg),
+        _lib.check(_lib.lib.rcb_engine_create_ex(
+            _lib.ptr(src), dtype_code, _lib.ptr(lab), lab.ndim, _lib.ptr(dims), C.byref(self._ecfg),
             C.byref(self._scfg), C.byref(self._ocfg), int(device),
             C.c_void_p(int(stream) if stream else 0), C.byref(h)))
         self._h = h
@@ -162,6 +170,13 @@ class RegionCompetition:
         if h:
             _lib.lib.rcb_engine_destroy(h)
             self._h = None
+
+    @property
+    def image(self) -> np.ndarray:
+        """The float64 intensity raster (optimizer.py:102), promoted on first use."""
+        if self._image64 is None:
+            self._image64 = np.ascontiguousarray(self._image_src, dtype=np.float64)
+        return self._image64
 
     # -- device state views ----------------------------------------------------
     @property

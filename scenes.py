@@ -213,6 +213,17 @@ def cfg4_small(seed: int = 4) -> Scene:
     return s
 
 
+def cfg4_sample(seed: int = 4, n: int = 64) -> Scene:
+    """The bounded CPU sample of cfg4 that the reference arm and the CPU
+    baseline time (bench.py): the cfg4 generator at 64^3 -- smooth
+    background, 4 ellipsoids (semi-axes scaled by n/512), blur 1.5, Poisson
+    peak 30 -- with one seed sphere of cfg4's radius 15 (bubbles:1:15);
+    PS/Poisson R = 4, E = 6 like cfg4."""
+    s = cfg4(seed, n=n, n_obj=4, per_axis=1, radius=15.0)
+    s.name = "cfg4_sample"
+    return s
+
+
 def cfg5_image(i: int, n: int = 512) -> Scene:
     rng = np.random.default_rng(1000 + i)
     shape = (n, n)

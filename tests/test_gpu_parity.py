@@ -263,6 +263,34 @@ def test_rank_ties_noiseless_vs_oracle(P, mode, monkeypatch):
     assert longest > 32  # exercises the long-run (block bitonic) fix-up too
 
 
+@pytest.mark.parametrize("gradient", ["l2", "sobolev"])
+def test_rank_tie_run_beyond_block_sort(P, gradient):
+    """One run of > 4096 exactly equal rank values (a straight 6000-pixel
+    edge of a noiseless two-level image): the block merge sort of K7 must
+    give lexsort's (rank, tie, x, comp) order -- accepted moves in order and
+    labels equal to the oracle's."""
+    img = np.zeros((12, 6000))
+    img[:8] = 1.0
+    lab = np.zeros((12, 6000), np.int32)
+    lab[:4] = 1
+    cfg = P.OptimizerConfig(gradient)
+    eng = P.RegionCompetition(img, lab, P.EnergyConfig("pc", "gauss"), P.SobolevParams(4.0), cfg)
+    o = O.OracleEngine(img, lab, "pc", "gauss", 0.0, 8, 4.0,
+                       config=O.OptimizerConfig(gradient))
+    longest = 0
+    for it in range(3):
+        rec = eng.iterate()
+        orec = o.iterate()
+        rk = eng.last_candidates[3]
+        _, cnt = np.unique(rk[rk < 0], return_counts=True)
+        longest = max(longest, int(cnt.max()) if cnt.size else 0)
+        want = np.asarray(orec.accepted, np.int64).reshape(-1, 3)
+        assert np.array_equal(eng.last_accepted, want), (gradient, it)
+        assert np.array_equal(eng.labels, o.labels), (gradient, it)
+        assert rec.energy == orec.energy, (gradient, it)
+    assert longest > 4096
+
+
 def test_engine_invariants_at_full_cfg2_size(P):
     """Size-independent properties on the 1024^2 PS-Poisson config: the
     device contour equals a fresh scan, the ledger agrees with the from-scratch

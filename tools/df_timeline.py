@@ -21,7 +21,7 @@ for _ in range(it_target - 1):
 cnt0 = eng.model.stats.count.copy()
 eng.iterate()
 n = C.c_int64()
-cap = 400000
+cap = int(os.environ.get("DF_CAP", "400000"))
 t = np.zeros(4 * cap, np.int64)
 part = np.zeros(cap, np.int32)
 code = np.zeros(cap, np.int32)
@@ -37,6 +37,10 @@ print("decide-latency us: p50 %.1f p90 %.1f p99 %.1f max %.1f" % tuple(np.percen
 print("fetch time us: p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(f, [50, 90, 100])))
 for q in (0.5, 0.9, 0.99, 0.999, 1.0):
     print(f"decided by {q:6.3f} of candidates: {np.quantile(d, q):9.1f} us")
+hist, edges = np.histogram(d, bins=20)
+print("decisions per 5% of the span:", hist.tolist(), "span us", round(float(d.max()), 1))
+lat_hist = np.histogram(lat, bins=[0, 1, 2, 5, 10, 20, 50, 100, 200, 500, 1e9])[0]
+print("latency histogram us [0,1,2,5,10,20,50,100,200,500,inf):", lat_hist.tolist())
 slow = np.argsort(-lat)[:15]
 print("slowest (pos, code, fetch, latency):")
 for p in slow:
