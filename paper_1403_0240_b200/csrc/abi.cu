@@ -164,6 +164,7 @@ struct rcb_engine {
   DBuf<uint32_t> qlist, qscr, bigmap, bigfr2;
   DBuf<uint8_t> bigfg2;
   DBuf<uint32_t> bigtouch;
+  DBuf<uint8_t> tflag;
   DBuf<int2> bigtouch_n;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
@@ -222,7 +223,7 @@ struct rcb_engine {
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
       bigmap.release(s); bigfr2.release(s); bigfg2.release(s); bigtouch.release(s);
-      bigtouch_n.release(s);
+      bigtouch_n.release(s); tflag.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -857,6 +858,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.band = e->band.p;
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
+      X.tflag = &e->tflag;
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
         X.pending = (ds && ds[0] == '0') ? nullptr : &e->pending;

@@ -2140,7 +2140,7 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
     if (r >= 0) return r;
     // the large tier is for footprints that resolve within a few dozen
     // levels; a long flood (a big piece to exhaust) goes to the assist job
-    if (kBig && S.levels >= kBigLevels) return 3;
+    if (kBig && S.levels >= (k3D ? kBigLevels : A.big_levels2d)) return 3;
     cur = nxt;
   }
 }
@@ -3651,7 +3651,10 @@ __global__ void k_pc_dtot(const ParArgs A, const int64_t *__restrict__ acc,
       double after = g_poisson(s[0] - 1.0, s[1] - v) + g_poisson(s[3] + 1.0, s[4] + v);
       dext = after - before;
     }
-    dtot[k] = dext + lam * (double)A.dint_acc[k];
+    // lam == 0 (every BASELINE config): dE_int is not needed and not
+    // computed (k_dint_acc skipped); d_ext + 0 * dE_int == d_ext up to the
+    // sign of a zero, which the ledger sum never sees
+    dtot[k] = lam != 0.0 ? dext + lam * (double)A.dint_acc[k] : dext;
   }
 }
 
@@ -4026,7 +4029,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       df_blocks = per_sm * sms;
     }
     setup_lock.unlock();
-    if (A.lat.ndim == 3 && X.bigmap) {
+    const char *b2d = getenv("RCB_DF_BIGBOX2D");  // 2-D large box tier (experiment)
+    if (X.bigmap && (A.lat.ndim == 3 || (b2d && b2d[0] == '1'))) {
       // large box tier (3-D; in 2-D the 31x31 / 63x63 window tiers catch wide
       // footprints and the tier measured slower): per warp a 4-bit map of up
       // to 2M sites (at most the lattice) and two frontiers of 16K sites
@@ -4035,6 +4039,10 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
       const int64_t vw = (A.lat.V + 7) / 8 + 4;
       A.big_words = (int)(vw < (1 << 18) ? ((vw + 3) & ~3) : (1 << 18));
       A.big_fcap = 1 << 14;
+      {
+        const char *bl = getenv("RCB_DF_BIGLEVELS2D");
+        A.big_levels2d = bl ? atoi(bl) : 256;
+      }
       uint32_t *const old_map = X.bigmap->p;
       RCB_TRY(X.bigmap->reserve(warps * (size_t)A.big_words, s));
       RCB_TRY(X.bigtouch->reserve(warps * (size_t)kBigTouch, s));
@@ -4118,7 +4126,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   RCB_TRY(X.tmp->reserve(bytes, s));
   RCB_CUDA(cub::DeviceScan::ExclusiveSum(X.tmp->p, bytes, X.slot, X.slot, N + 1, s));
   k_acc_write<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.acc, X.moves);
-  k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
+  if (X.lam != 0.0) k_dint_acc<<<grid_for(N, 256), 256, 0, s>>>(A, X.acc, X.moves);
   T.mark("compact");
   int nl = 6;
   // 3-D PS: the per-move exact ledger terms cost moves x ball x nearby flips,
@@ -4258,7 +4266,24 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   }
   k_final_labels<<<grid_for(N, 256), 256, 0, s>>>(A, X.slot, X.budget, X.Lmut);
   T.mark("labels");
-  if (X.region_ps) {
+  const bool flipmap3d = X.region_ps && X.tflag && fields_tile3d_ok(A.lat, X.radius, X.nball_full) &&
+                        (X.rho0 || !band_ledger) && !getenv("RCB_BAND_SCATTER");
+  if (flipmap3d) {
+    if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
+    const int64_t nt = band3d_tiles(A.lat);
+    const bool fresh = X.tflag->cap < (size_t)nt;
+    RCB_TRY(X.tflag->reserve(nt, s));
+    if (fresh) RCB_CUDA(cudaMemsetAsync(X.tflag->p, 0, X.tflag->cap, s));
+    RCB_TRY(fields_band3d(X.acc, X.moves, X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius,
+                          X.dirty, X.tflag->p, X.Cown, X.Sown, X.rho0, X.poisson,
+                          band_ledger ? X.band : nullptr, s));
+    nl += 3;
+    if (band_ledger) {
+      if (X.lam != 0.0) k_dint_sum<<<grid_for(N, 256), 256, 0, s>>>(A, X.moves, X.band);
+      k_band_ledger<<<1, 32, 0, s>>>(X.band, X.lam, X.energy);
+      nl += 2;
+    }
+  } else if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
     if (!band_ledger && fields_tile2d_ok(A.lat, X.radius, X.nball_full))

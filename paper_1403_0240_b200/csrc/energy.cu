@@ -230,6 +230,150 @@ __global__ void __launch_bounds__(256) k_fields_tile3d(
   }
 }
 
+// 3-D band refresh from the flip map: flips[x] = 1 at this iteration's
+// flipped sites and tflag[t] = 1 for the tiles holding them (k_mark_flips).
+// A tile is processed iff one of the 27 tiles around it (R <= the tile
+// extents) holds a flip; its sites whose ball holds a flip (checked on the
+// staged flip flags, nearest offsets first) are recomputed as in
+// k_fields_tile3d -- the sites the per-flip ball scatter used to mark, without
+// the ~3e9 scattered byte writes per cfg4 iteration.
+__global__ void __launch_bounds__(256) k_fields_band3d(
+    const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny, int nz,
+    const Off *__restrict__ ball, int nball, int R, const uint8_t *__restrict__ flips,
+    const uint8_t *__restrict__ tflag, int32_t *__restrict__ Cown, double *__restrict__ Sown,
+    double *__restrict__ rho0, int poisson, long long *__restrict__ band) {
+  constexpr int SX = kT3X + 2 * kT3R, SY = kT3Y + 2 * kT3R, SZ = kT3Z + 2 * kT3R;
+  static_assert(SX <= 32, "a halo row's flips must fit one 32-bit mask");
+  __shared__ int32_t sL[SX * SY * SZ];
+  __shared__ double sI[SX * SY * SZ];
+  __shared__ uint32_t rowbits[SY * SZ];  // flips of each halo row, bit = x cell
+  __shared__ int srow[(2 * kT3R + 1) * (2 * kT3R + 1)];  // ball rows: dz:8 | dy:8 | h:8
+  __shared__ int nrow;
+  __shared__ int sofs[512];  // R <= kT3R = 4: <= 257 ball offsets
+  __shared__ long long sm[kLimbs];
+  const int ntx = gridDim.x, nty = gridDim.y, ntz = gridDim.z;
+  bool any = false;
+  if (threadIdx.x < 27) {
+    const int tz = (int)blockIdx.z + (int)threadIdx.x / 9 - 1;
+    const int ty = (int)blockIdx.y + ((int)threadIdx.x / 3) % 3 - 1;
+    const int tx = (int)blockIdx.x + (int)threadIdx.x % 3 - 1;
+    if ((unsigned)tz < (unsigned)ntz && (unsigned)ty < (unsigned)nty && (unsigned)tx < (unsigned)ntx)
+      any = tflag[((int64_t)tz * nty + ty) * ntx + tx] != 0;
+  }
+  if (!__syncthreads_or(any)) return;
+  const int tx = threadIdx.x % kT3X, ty = (threadIdx.x / kT3X) % kT3Y, tz = threadIdx.x / (kT3X * kT3Y);
+  const int x0 = blockIdx.x * kT3X, y0 = blockIdx.y * kT3Y, z0 = blockIdx.z * kT3Z;
+  const int x = x0 + tx, y = y0 + ty, z = z0 + tz;
+  const bool inside = x < nx && y < ny && z < nz;
+  const int64_t f = ((int64_t)z * ny + y) * nx + x;
+  const int hx = kT3X + 2 * R, hy = kT3Y + 2 * R, hz = kT3Z + 2 * R;
+  for (int i = threadIdx.x; i < hy * hz; i += blockDim.x) rowbits[i] = 0u;
+  if (threadIdx.x == 0) {  // the ball as x-runs per (dz, dy): |o|^2 <= R^2
+    int k = 0;
+    for (int dz = -R; dz <= R; ++dz)
+      for (int dy = -R; dy <= R; ++dy) {
+        const int t = R * R - dz * dz - dy * dy;
+        if (t < 0) continue;
+        int h = 0;
+        while ((h + 1) * (h + 1) <= t) ++h;
+        srow[k++] = ((dz & 0xff) << 16) | ((dy & 0xff) << 8) | h;
+      }
+    nrow = k;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hx * hy * hz; i += blockDim.x) {
+    const int cz = i / (hx * hy), rem = i - cz * hx * hy;
+    const int cy = rem / hx, cx = rem - cy * hx;
+    const int gz = z0 - R + cz, gy = y0 - R + cy, gx = x0 - R + cx;
+    const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
+                    (unsigned)gx < (unsigned)nx;
+    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    const int si = (cz * SY + cy) * SX + cx;
+    if (ok && __ldg(flips + g)) atomicOr(&rowbits[cz * hy + cy], 1u << cx);
+    sL[si] = ok ? __ldg(L + g) : -1;
+    sI[si] = ok ? __ldg(I + g) : 0.0;
+  }
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = ((int)ball[k].dz * SY + (int)ball[k].dy) * SX + (int)ball[k].dx;
+  if (band)
+    for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  __syncthreads();
+  // a flip within the ball: one mask test per ball row
+  bool todo = false;
+  if (inside) {
+    const int nr = nrow;
+    for (int k = 0; k < nr; ++k) {
+      const int r = srow[k];
+      const int dz = (int)(int8_t)(r >> 16), dy = (int)(int8_t)(r >> 8), h = r & 0xff;
+      const uint32_t m = ((2u << (2 * h)) - 1u) << (tx + R - h);
+      if (rowbits[(tz + R + dz) * hy + (ty + R + dy)] & m) {
+        todo = true;
+        break;
+      }
+    }
+  }
+  const int cidx = ((tz + R) * SY + (ty + R)) * SX + (tx + R);
+  double oldr = 0.0, newr = 0.0;
+  if (todo) {
+    const int32_t own = sL[cidx];
+    int32_t c = 0;
+    double sv = 0.0;
+    for (int k = 0; k < nball; ++k) {
+      const int j = cidx + sofs[k];
+      if (sL[j] == own) {
+        c += 1;
+        sv += sI[j];
+      }
+    }
+    if (band) oldr = rho0[f];
+    Cown[f] = c;
+    Sown[f] = sv;
+    newr = rho(sI[cidx], sv / (double)c, poisson);
+    if (rho0) rho0[f] = newr;
+  }
+  if (band) {  // every thread of the block reaches here (warp-uniform)
+    acc_add_warp(sm, -oldr, todo);
+    acc_add_warp(sm, newr, todo);
+    acc_flush(sm, band);
+  }
+}
+
+// per accepted move: flips[x] = v, tflag[tile(x)] = v (v = 1 mark, 0 clear)
+__global__ void k_mark_flips(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
+                             Lat lat, uint8_t v, uint8_t *__restrict__ flips,
+                             uint8_t *__restrict__ tflag) {
+  const int64_t n = *moves;
+  const int ntx = (int)((lat.nx + kT3X - 1) / kT3X), nty = (int)((lat.ny + kT3Y - 1) / kT3Y);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = acc[3 * k];
+    int64_t z, y, x;
+    lat.coord(f, z, y, x);
+    flips[f] = v;
+    tflag[((z / kT3Z) * nty + y / kT3Y) * ntx + x / kT3X] = v;
+  }
+}
+
+int64_t band3d_tiles(const Lat &lat) {
+  return ((lat.nx + kT3X - 1) / kT3X) * ((lat.ny + kT3Y - 1) / kT3Y) *
+         ((lat.nz + kT3Z - 1) / kT3Z);
+}
+
+int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
+                      const Lat &lat, const Off *ball_full, int nball_full, int R, uint8_t *flips,
+                      uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0, int poisson,
+                      long long *band, cudaStream_t s) {
+  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, flips, tflag);
+  dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
+            (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
+  k_fields_band3d<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, (int)lat.nz,
+                                                       ball_full, nball_full, R, flips, tflag,
+                                                       Cown, Sown, rho0, poisson, band);
+  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, flips, tflag);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, long long *band, cudaStream_t s) {

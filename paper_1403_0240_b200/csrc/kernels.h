@@ -119,7 +119,7 @@ struct ParArgs {
   uint32_t *bigmap;               // dataflow large box tier: per-warp 4-bit maps (big_words each)
   uint32_t *bigfr2;               // ... and frontiers (2 x big_fcap per warp)
   uint8_t *bigfg2;
-  int big_words, big_fcap;
+  int big_words, big_fcap, big_levels2d;
   // per warp: words of its map set since the last clear (kBigTouch entries)
   // and {count, dirty range}: count < 0 or > kBigTouch = clear [0, range)
   uint32_t *bigtouch;
@@ -151,6 +151,7 @@ struct ParExtra {
   const Off *ball, *ball_full;
   int nball, nball_full, radius;
   uint8_t *dirty;
+  DBuf<uint8_t> *tflag = nullptr;  // 3-D band refresh: per-tile flip flags (zero between uses)
   int32_t *Cown;
   double *Sown;
   double *rho0;
@@ -204,6 +205,11 @@ int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const O
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, long long *band, cudaStream_t s);
 bool fields_tile3d_ok(const Lat &lat, int R, int nball_full);
+int64_t band3d_tiles(const Lat &lat);
+int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
+                      const Lat &lat, const Off *ball_full, int nball_full, int R, uint8_t *flips,
+                      uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0, int poisson,
+                      long long *band, cudaStream_t s);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,

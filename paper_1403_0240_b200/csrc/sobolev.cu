@@ -19,6 +19,23 @@
 
 namespace rcb {
 
+// Interaction count: one atomic per block (a same-address atomic per warp
+// cost more than the w = 1 kernel's whole memory pass at 10^7 particles).
+__device__ __forceinline__ void block_add_pairs(unsigned long long np,
+                                                unsigned long long *pairs) {
+  __shared__ unsigned long long red[32];
+  for (int sh = 16; sh; sh >>= 1) np += __shfl_down_sync(0xffffffffu, np, sh);
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = np;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < nw; ++k) t += red[k];
+    if (t) atomicAdd(pairs, t);
+  }
+}
+
+
 // One thread per particle p.  The stencil {o : |o|^2 < (E/2)^2} is walked row
 // by row: for each (dz, dy) in lexicographic order the partners are the
 // particles of the contiguous site range [x - h, x + h] of that lattice row,
@@ -69,10 +86,7 @@ __global__ void __launch_bounds__(128) k_sobolev(
     const double b = co > 0 ? opp / (double)co : 0.0;
     out[oidx ? oidx[p] : p] = a - b;
   }
-  if (pairs) {
-    for (int s = 16; s; s >>= 1) np += __shfl_down_sync(0xffffffffu, np, s);
-    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
-  }
+  if (pairs) block_add_pairs(np, pairs);
 }
 
 // fp32 variant of K6 (fp32 mode): float increments, weights and sums.
@@ -118,10 +132,7 @@ __global__ void __launch_bounds__(128) k_sobolev32(
     const float b = co > 0 ? opp / (float)co : 0.f;
     out[p] = (double)(a - b);
   }
-  if (pairs) {
-    for (int s = 16; s; s >>= 1) np += __shfl_down_sync(0xffffffffu, np, s);
-    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
-  }
+  if (pairs) block_add_pairs(np, pairs);
 }
 
 int32_t sobolev_lattice32(const uint32_t *site_off, const int32_t *pown, const uint32_t *px,
@@ -217,10 +228,7 @@ __global__ void __launch_bounds__(128) k_sobolev_pk(
     const double b = co > 0 ? opp / (double)co : 0.0;
     out[p] = a - b;
   }
-  if (pairs) {
-    for (int sh = 16; sh; sh >>= 1) np += __shfl_down_sync(0xffffffffu, np, sh);
-    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
-  }
+  if (pairs) block_add_pairs(np, pairs);
 }
 
 // ---- K6 at w = 1 (E <= 2): the stencil is the particle's own site ----------
@@ -230,41 +238,115 @@ __global__ void __launch_bounds__(128) k_sobolev_pk(
 // -- with the run's few neighbours read from L1.  The sums
 // follow the same canonical order (index order within the site) and the same
 // expressions as k_sobolev, so the results are bit-identical.
+// General run sum (any owners/competitors): the partners of p are the
+// particles of its own site, the run of equal px around p.
+__device__ __forceinline__ double site_run_value(const uint32_t *__restrict__ px,
+                                                 const int32_t *__restrict__ pown,
+                                                 const int32_t *__restrict__ pcomp,
+                                                 const double *__restrict__ raw, double w0,
+                                                 int64_t p, int64_t lo, int64_t hi, int64_t &len) {
+  const uint32_t f = __ldg(&px[p]);
+  const int32_t own = __ldg(&pown[p]);
+  int64_t s = p, e = p + 1;
+  while (s > lo && __ldg(&px[s - 1]) == f) --s;
+  while (e < hi && __ldg(&px[e]) == f) ++e;
+  double same = 0.0, opp = 0.0;
+  int cs = 0, co = 0;
+  for (int64_t q = s; q < e; ++q) {
+    const double c = w0 * __ldg(&raw[q]);
+    if (__ldg(&pown[q]) == own) {
+      same += c;
+      ++cs;
+    }
+    if (__ldg(&pcomp[q]) == own) {
+      opp += c;
+      ++co;
+    }
+  }
+  len = e - s;
+  const double a = cs > 0 ? same / (double)cs : 0.0;
+  const double b = co > 0 ? opp / (double)co : 0.0;
+  return a - b;
+}
+
+// Warp-cooperative pass: each warp streams 32 consecutive particles with
+// coalesced loads; runs of equal px that lie inside the warp, share one owner
+// and hold no competitor equal to it (every run of an engine or sweep
+// particle list: competitors differ from the site's own label) are summed by
+// a ripple of shuffles -- acc(lane) = acc(lane - 1) + c(lane), from 0.0 at
+// the run head, i.e. the canonical sequential order -- and every lane of the
+// run takes the run total; other runs (crossing a warp edge, mixed owners)
+// take site_run_value.  Bit-identical to k_sobolev.
+static constexpr int kRipple = 8, kSiteChunks = 8;
 __global__ void __launch_bounds__(256) k_sobolev_site(
     const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
     const int32_t *__restrict__ pcomp, const double *__restrict__ raw, double w0, int64_t p0,
     int64_t p1, int64_t lo, int64_t hi, double *__restrict__ out,
     unsigned long long *__restrict__ pairs) {
-  const int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // each warp streams kSiteChunks consecutive chunks of 32 particles, all
+  // their loads in flight before the first is used (bytes in flight per SM
+  // are what an HBM-bound pass needs)
+  const int64_t wbase = p0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 * kSiteChunks);
+  uint32_t fv[kSiteChunks];
+  int32_t ov[kSiteChunks], cv[kSiteChunks];
+  double rv[kSiteChunks];
+#pragma unroll
+  for (int j = 0; j < kSiteChunks; ++j) {
+    const int64_t p = wbase + 32 * j + lane;
+    const bool in = p < p1;
+    fv[j] = in ? __ldg(&px[p]) : 0xffffffffu - (uint32_t)lane;  // distinct sentinels
+    ov[j] = in ? __ldg(&pown[p]) : -1;
+    cv[j] = in ? __ldg(&pcomp[p]) : -2;
+    rv[j] = in ? __ldg(&raw[p]) : 0.0;
+  }
   unsigned long long np = 0;
-  if (p < p1) {
-    const uint32_t f = __ldg(&px[p]);
-    const int32_t own = __ldg(&pown[p]);
-    int64_t s = p, e = p + 1;
-    while (s > lo && __ldg(&px[s - 1]) == f) --s;
-    while (e < hi && __ldg(&px[e]) == f) ++e;
-    double same = 0.0, opp = 0.0;
-    int cs = 0, co = 0;
-    for (int64_t q = s; q < e; ++q) {
-      const double c = w0 * __ldg(&raw[q]);
-      if (__ldg(&pown[q]) == own) {
-        same += c;
-        ++cs;
-      }
-      if (__ldg(&pcomp[q]) == own) {
-        opp += c;
-        ++co;
+#pragma unroll
+  for (int j = 0; j < kSiteChunks; ++j) {
+    const int64_t p = wbase + 32 * j + lane;
+    const bool in = p < p1;
+    const uint32_t f = fv[j];
+    const int32_t own = ov[j], cmp = cv[j];
+    const double c = w0 * rv[j];
+    const uint32_t fu = __shfl_up_sync(0xffffffffu, f, 1), fd = __shfl_down_sync(0xffffffffu, f, 1);
+    const int32_t ou = __shfl_up_sync(0xffffffffu, own, 1);
+    const bool head = lane == 0 || fu != f;
+    const bool tail = lane == 31 || fd != f;
+    // a run is summed here if it lies inside the chunk, has one owner and
+    // no competitor equal to it; otherwise site_run_value
+    const bool edge = (lane == 0 && in && p > lo && __ldg(&px[p - 1]) == f) ||
+                      (lane == 31 && in && p + 1 < hi && __ldg(&px[p + 1]) == f);
+    const bool bad = edge || (!head && ou != own) || (cmp == own);
+    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    const int hl = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));  // highest head lane <= lane
+    const unsigned tm = __ballot_sync(0xffffffffu, tail);
+    const int tl = __ffs(tm & (0xffffffffu << lane)) - 1;           // lowest tail lane >= lane
+    const unsigned bm = __ballot_sync(0xffffffffu, bad);
+    const unsigned runmask =
+        (tl == 31 ? 0xffffffffu : ((1u << (tl + 1)) - 1u)) & (0xffffffffu << hl);
+    const int len = tl - hl + 1;
+    const bool simple = in && !(bm & runmask) && len <= kRipple;
+    // ripple: at step k the lane k places after its run head adds its term to
+    // its left neighbour's (already final) partial sum -- sequential order
+    double acc = 0.0 + c;
+#pragma unroll
+    for (int k = 1; k < kRipple; ++k) {
+      const double up = __shfl_up_sync(0xffffffffu, acc, 1);
+      if (lane - hl == k) acc = up + c;
+    }
+    const double total = __shfl_sync(0xffffffffu, acc, tl);
+    if (in) {
+      if (simple) {
+        out[p] = total / (double)len - 0.0;
+        np += (unsigned long long)len;
+      } else {
+        int64_t L = 0;
+        out[p] = site_run_value(px, pown, pcomp, raw, w0, p, lo, hi, L);
+        np += (unsigned long long)L;
       }
     }
-    np = (unsigned long long)(e - s);
-    const double a = cs > 0 ? same / (double)cs : 0.0;
-    const double b = co > 0 ? opp / (double)co : 0.0;
-    out[p] = a - b;
   }
-  if (pairs) {
-    for (int sh = 16; sh; sh >>= 1) np += __shfl_down_sync(0xffffffffu, np, sh);
-    if ((threadIdx.x & 31) == 0 && np) atomicAdd(pairs, np);
-  }
+  if (pairs) block_add_pairs(np, pairs);
 }
 
 bool sobolev_site_only(const Off *rows_host, int nrows) {
@@ -275,8 +357,8 @@ int32_t sobolev_site(const uint32_t *px, const int32_t *pown, const int32_t *pco
                      const double *raw, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
                      double *out, unsigned long long *pairs, cudaStream_t s) {
   if (p1 <= p0) return RCB_OK;
-  k_sobolev_site<<<grid_for(p1 - p0, 256), 256, 0, s>>>(px, pown, pcomp, raw, w0, p0, p1, lo, hi,
-                                                        out, pairs);
+  k_sobolev_site<<<grid_for(p1 - p0, 256 * kSiteChunks), 256, 0, s>>>(px, pown, pcomp, raw, w0,
+                                                                      p0, p1, lo, hi, out, pairs);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

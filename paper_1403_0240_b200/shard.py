@@ -86,10 +86,11 @@ def device_view(ptr: int, n: int, dtype, device: int):
 
 
 class TorchExchange:
-    """All-gather of the slabs' score slices, in place, with one broadcast
-    per (owner rank, buffer) through torch.distributed: NCCL over NVLink on
-    GPUs, gloo on CPU tensors (tests).  Each rank's slice lands at the same
-    offsets everywhere, so no unpacking pass follows."""
+    """All-gather of the slabs' score slices: every rank packs its slice of
+    each buffer (as bytes) into one send tensor padded to the longest slice,
+    ONE all_gather moves them (NCCL over NVLink on GPUs, gloo on CPU tensors
+    in the tests), and each foreign slice is copied into place at the same
+    offsets as on its owner, so every rank ends with the full buffers."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -101,12 +102,33 @@ class TorchExchange:
         ranges[r] = (p0, p1) of rank r."""
         import torch
         ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream)) if stream else _null()
+        world = len(ranges)
+        me = self.dist.get_rank(self.group)
         with ctx:
+            views = [b.view(torch.uint8).view(b.numel(), b.element_size()) for b in bufs]
+            width = sum(v.shape[1] for v in views)          # bytes per particle, all buffers
+            m = max(b - a for a, b in ranges)
+            if m <= 0:
+                return
+            dev = bufs[0].device
+            send = torch.zeros((m, width), dtype=torch.uint8, device=dev)
+            a, b = ranges[me]
+            col = 0
+            for v in views:
+                w = v.shape[1]
+                if b > a:
+                    send[:b - a, col:col + w] = v[a:b]
+                col += w
+            recv = [torch.empty_like(send) for _ in range(world)]
+            self.dist.all_gather(recv, send, group=self.group)
             for r, (a, b) in enumerate(ranges):
-                if b <= a:
+                if r == me or b <= a:
                     continue
-                for buf in bufs:
-                    self.dist.broadcast(buf[a:b], src=self._global(r), group=self.group)
+                col = 0
+                for v in views:
+                    w = v.shape[1]
+                    v[a:b] = recv[r][:b - a, col:col + w]
+                    col += w
 
     def _global(self, r: int) -> int:
         if self.group is None:

@@ -255,4 +255,5 @@ def two_region_small(shape=(48, 48), seed: int = 0) -> Scene:
 
 
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg2_small": cfg2_small, "cfg3": cfg3,
-           "cfg4": cfg4, "cfg4_small": cfg4_small}
+           "cfg4": cfg4, "cfg4_small": cfg4_small, "cfg4_sample": cfg4_sample,
+           "cfg5_0": lambda: cfg5_image(0), "cfg5_1": lambda: cfg5_image(1)}

@@ -555,3 +555,28 @@ def test_ps_deferred_stats_chains(P, monkeypatch):
     assert np.array_equal(out[0][1][0], ref.stats.count)
     assert np.array_equal(out[0][1][1], ref.stats.total)
     assert np.array_equal(out[0][1][2], ref.stats.total_sq)
+
+
+@pytest.mark.parametrize("shape", [(72, 80), (20, 22, 24)])
+def test_sobolev_site_kernel_multilabel_vs_oracle(P, shape):
+    """w = 1 (E = 2): K6 is the warp-cooperative site-run kernel.  Touching
+    bubbles make sites with 2-4 competitors (runs of equal px that cross warp
+    edges, too): accepted moves, labels and ledger equal the oracle's."""
+    import scenes
+    rng = np.random.default_rng(31)
+    per = 4 if len(shape) == 2 else 2
+    lab = scenes.bubbles(shape, per, (shape[0] / per) * 0.62)
+    img = rng.normal(0.0, 1.0, size=shape) + (lab % 3).astype(np.float64)
+    eng = P.RegionCompetition(img, lab, P.EnergyConfig("pc", "gauss"), P.SobolevParams(2.0),
+                              P.OptimizerConfig("sobolev"))
+    o = O.OracleEngine(img, lab, "pc", "gauss", 0.0, 8, 2.0)
+    for it in range(4):
+        rec = eng.iterate()
+        orec = o.iterate()
+        want = np.asarray(orec.accepted, np.int64).reshape(-1, 3)
+        assert np.array_equal(eng.last_accepted, want), it
+        assert np.array_equal(eng.labels, o.labels), it
+        assert rec.energy == orec.energy, it
+        xs, ow, cm, rk = eng.last_candidates
+        _, cnt = np.unique(xs, return_counts=True)
+        assert cnt.max() >= 2

@@ -13,7 +13,7 @@ import csv
 import json
 import sys
 
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
          "msecond": 1e3, "second": 1e6}
 
 rows = list(csv.reader(l for l in open(sys.argv[1]) if not l.startswith("==")))
