@@ -228,6 +228,7 @@ struct rcb_engine {
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
       drop_chains(pending, s);
+      drop_chains(chain_pool, s);
       cudaStreamSynchronize(s);
       for (auto &e : ev)
         if (e) cudaEventDestroy(e);
@@ -248,15 +249,16 @@ struct rcb_engine {
     return RCB_OK;
   }
 
-  std::vector<PendingChain> pending;  // PS: deferred total / total_sq chains
+  std::vector<PendingChain> pending;     // PS: deferred total / total_sq chains
+  std::vector<PendingChain> chain_pool;  // their buffers, recycled
 
   int32_t flush_stats() {  // make tot / tsq current (replay deferred chains)
     if (pending.empty()) return RCB_OK;
-    return replay_chains(pending, I.p, tot.p, tsq.p, s);
+    return replay_chains(pending, I.p, tot.p, tsq.p, s, &chain_pool);
   }
 
   int32_t refresh() {  // energy.py:285-291
-    drop_chains(pending, s);  // superseded by the rebuild
+    drop_chains(pending, s, &chain_pool);  // superseded by the rebuild
     RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
     if (ecfg.region_model == 1)
       RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s, rho0.p,
@@ -682,9 +684,15 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
     const bool df24 = n < 0xffffff && e->nl <= 65536;
     const bool df27 = n < 0x7ffffff && e->nl <= 1024;
     const bool use_df = fits && e->accept_mode != 1 && (df24 || df27);
-    // l2 mode runs in parallel for PC through the dataflow kernel (every label
-    // sequenced, the d_tot < 0 gate on running statistics); PS keeps K8 v1
-    const bool l2par = e->mode == 0 && e->ecfg.region_model == 0 && use_df;
+    // l2 mode runs in parallel through the dataflow kernel: every label
+    // sequenced, the d_tot < 0 gate on running statistics (PC) or on the
+    // own-label fields corrected by the earlier flips within 2R (PS, fp64
+    // Poisson or Gauss with the rho0 table and the K5 competitor terms)
+    const char *psl2 = getenv("RCB_PS_L2");  // "seq": PS l2 on K8 v1 (comparison runs)
+    const bool ps_l2_ok = e->ecfg.region_model == 1 && e->rho0.p && e->cb0.p && !e->ocfg.fp32 &&
+                          !(psl2 && strcmp(psl2, "seq") == 0) &&
+                          e->ecfg.smooth_radius <= 7;
+    const bool l2par = e->mode == 0 && (e->ecfg.region_model == 0 || ps_l2_ok) && use_df;
     const bool par = (e->mode == 1 || l2par) && e->ocfg.full_fg && e->simple_topology &&
                      !e->force_sequential;
     e->cur_par = par;
@@ -755,7 +763,18 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       P.poisson = poisson;
       P.lam = e->ecfg.lam;
       P.I = e->I.p;
-      if (P.l2) {
+      P.region_ps = e->ecfg.region_model == 1;
+      if (P.region_ps) {
+        P.Cown = e->Cown.p;
+        P.Sown = e->Sown.p;
+        P.rho0 = e->rho0.p;
+        P.cb0 = e->cb0.p;
+        P.sb0 = e->sb0.p;
+        P.ball = e->ball.p;
+        P.nball = e->nball;
+        P.radius = e->ecfg.smooth_radius;
+      }
+      if (P.l2 && !P.region_ps) {
         RCB_TRY(e->tot_run.reserve(e->nl, s));
         RCB_TRY(e->tsq_run.reserve(e->nl, s));
         RCB_CUDA(cudaMemcpyAsync(e->tot_run.p, e->tot.p, sizeof(double) * e->nl,
@@ -859,6 +878,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
       X.tflag = &e->tflag;
+      X.chain_pool = &e->chain_pool;
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
         X.pending = (ds && ds[0] == '0') ? nullptr : &e->pending;

@@ -2654,6 +2654,9 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
 }
 
 
+__device__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t pos, int32_t f, int32_t a,
+                             int32_t b, int di);
+
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
@@ -2889,7 +2892,13 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       if (sb) warp_wait_label(A, b, pos);
       if (a > 0 && __ldcg((const long long *)A.cnt + a) == 1)
         d = (d_base == ACC && A.vanish_ok && !fus_bad) ? ACC : REJ;
-      if (d == ACC) {
+      if (d == ACC && A.region_ps) {
+        int di = 0;
+        for (int k = 0; k < 27; ++k)
+          if (is_face(k) && lab[k] >= 0) di += (int)(lab[k] != b) - (int)(lab[k] != a);
+        const double dt = df_ps_dtot(A, S, pos, f, a, b, di);
+        if (!(dt < 0.0)) d = REJ;
+      } else if (d == ACC) {
         const double v = __ldg(A.I + f);
         const long long ca = __ldcg((const long long *)A.cnt + a);
         const long long cb = __ldcg((const long long *)A.cnt + b);
@@ -2991,6 +3000,183 @@ struct FlipList {
   double ta[32], tb[32], ib[32];
   int n;
 };
+
+// l2 mode, PS (optimizer.py:186-193, energy.py:326-372): the true increment
+// of candidate pos in its view V_pos, computed inside the dataflow kernel as
+// k_ps_dtot computes it after the fact: every site within 2R of x is waited
+// for (settled for pos), the sites flipped earlier in this iteration are
+// gathered from their site words into a shared flip list (aliasing the warp's
+// BFS memory, idle here), and each ball site's own-label field is the
+// iteration-start Cown/Sown (or, for a site flipped earlier, the K5 competitor
+// count/sum of its accepted particle) plus the listed corrections within R;
+// with too many flips the field is recounted in the view.  Same expressions
+// and summation order as delta_ps / K8 v1, so the gate is bit-identical on
+// integer (Poisson) data.
+__device__ __noinline__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t pos, int32_t f,
+                                          int32_t a, int32_t b, int di) {
+  static_assert(sizeof(FlipList) <= sizeof(WarpBfs), "flip list aliases the warp BFS memory");
+  FlipList &F = *reinterpret_cast<FlipList *>(&S);
+  const Lat &lat = A.lat;
+  const int lane = threadIdx.x & 31;
+  const uint32_t bits = (uint32_t)A.wp_bits;
+  const int R = A.radius, R2 = R * R, R2w = 4 * R2, side = 4 * R + 1;
+  const bool is3 = lat.ndim == 3;
+  const int nx = (int)lat.nx, ny = (int)lat.ny, nz = (int)lat.nz;
+  const int nxy = nx * ny;
+  const int z = is3 ? f / nxy : 0, frem = f - z * nxy;
+  const int y = frem / nx, x = frem - y * nx;
+  const double vx = __ldg(A.I + f);
+  __syncwarp();
+  if (lane == 0) F.n = 0;
+  __syncwarp();
+  // 1. settle the 2R neighbourhood and list its earlier flips
+  const int ncell = (is3 ? side : 1) * side * side;
+  for (int base = 0; base < ncell; base += 32) {
+    const int c = base + lane;
+    int64_t g = -1;
+    int ddz = 0, ddy = 0, ddx = 0;
+    if (c < ncell) {
+      ddz = is3 ? c / (side * side) - 2 * R : 0;
+      ddy = (c / side) % side - 2 * R;
+      ddx = c % side - 2 * R;
+      const int zz = z + ddz, yy = y + ddy, xx = x + ddx;
+      if (ddz * ddz + ddy * ddy + ddx * ddx <= R2w && (unsigned)zz < (unsigned)nz &&
+          (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx)
+        g = ((int64_t)zz * ny + yy) * nx + xx;
+    }
+    const unsigned long long v = warp_wait_settled(A, g, pos);
+    if (g >= 0 && wp_w(bits, v) < pos) {
+      const int slot = atomicAdd(&F.n, 1);
+      if (slot < kFlipCap) {
+        F.dz[slot] = (int8_t)ddz;
+        F.dy[slot] = (int8_t)ddy;
+        F.dx[slot] = (int8_t)ddx;
+        F.oldl[slot] = __ldg(A.L + g);
+        F.newl[slot] = wp_lab(bits, v);
+        F.val[slot] = __ldg(A.I + g);
+      }
+    }
+  }
+  __syncwarp();
+  const int nf = F.n;
+  const bool list_ok = nf <= kFlipCap;
+  auto view_lab = [&](int64_t h) -> int32_t {
+    return df_lab(bits, ld_rlx64(A.wp + h), __ldg(A.L + h), pos);
+  };
+  // own-label count/sum at pos of the label lg at offset (oz, oy, ox) = site g
+  auto own_field = [&](int oz, int oy, int ox, int64_t g, int32_t lg, int32_t &c,
+                       double &sv) -> bool {
+    const unsigned long long wv = ld_rlx64(A.wp + g);
+    const bool flipped = wp_w(bits, wv) < pos;
+    if (list_ok) {
+      bool touched = false;
+      if (!flipped) {
+        c = A.Cown[g];
+        sv = A.Sown[g];
+      } else {  // flipped earlier to lg: K5's competitor count/sum of its particle
+        const uint32_t pg = A.order[wp_w(bits, wv)];
+        c = A.cb0[pg];
+        sv = A.sb0[pg];
+        touched = true;
+      }
+      for (int e = 0; e < nf; ++e) {
+        const int ez = F.dz[e] - oz, ey = F.dy[e] - oy, ex = F.dx[e] - ox;
+        if (ez * ez + ey * ey + ex * ex > R2) continue;
+        if (F.newl[e] == lg) {
+          c += 1;
+          sv += F.val[e];
+          touched = true;
+        }
+        if (F.oldl[e] == lg) {
+          c -= 1;
+          sv -= F.val[e];
+          touched = true;
+        }
+      }
+      return !touched;  // true: the iteration-start field (and rho0) still hold
+    }
+    const int gz = is3 ? (int)(g / nxy) : 0, grem = (int)(g - (int64_t)gz * nxy);
+    const int gy = grem / nx, gx = grem - gy * nx;
+    c = 0;
+    sv = 0.0;
+    for (int q = 0; q <= A.nball; ++q) {
+      const Off o2 = q == 0 ? Off{0, 0, 0, 0} : A.ball[q - 1];
+      const int z2 = gz + o2.dz, y2 = gy + o2.dy, x2 = gx + o2.dx;
+      if ((unsigned)z2 >= (unsigned)nz || (unsigned)y2 >= (unsigned)ny || (unsigned)x2 >= (unsigned)nx)
+        continue;
+      const int64_t h = ((int64_t)z2 * ny + y2) * nx + x2;
+      if (view_lab(h) != lg) continue;
+      c += 1;
+      sv += __ldg(A.I + h);
+    }
+    return false;
+  };
+  // 2. ball terms, lanes over offsets; lane 0 replays the ordered sums
+  double ta = 0.0, tb = 0.0, sb = 0.0;
+  int cb = 0;
+  for (int base = 0; base < A.nball; base += 32) {
+    const int kk = base + lane;
+    double term_a = 0.0, term_b = 0.0, ib = 0.0;
+    bool hit_a = false, hit_b = false;
+    if (kk < A.nball) {
+      const Off o = A.ball[kk];
+      const int zz = z + o.dz, yy = y + o.dy, xx = x + o.dx;
+      if ((unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx) {
+        const int64_t g = ((int64_t)zz * ny + yy) * nx + xx;
+        const int32_t lg = view_lab(g);
+        if (lg == a || lg == b) {
+          int32_t c;
+          double sv;
+          const bool clean = own_field(o.dz, o.dy, o.dx, g, lg, c, sv);
+          const double cy = (double)c, iy = __ldg(A.I + g);
+          const double r_old = clean ? A.rho0[g] : rho(iy, sv / cy, A.poisson);
+          const bool isa = lg == a;
+          const double t =
+              rho(iy, (sv + (isa ? -vx : vx)) / (cy + (isa ? -1.0 : 1.0)), A.poisson) - r_old;
+          if (isa) {
+            term_a = t;
+            hit_a = true;
+          } else {
+            term_b = t;
+            hit_b = true;
+            ib = iy;
+          }
+        }
+      }
+    }
+    const unsigned ma = __ballot_sync(0xffffffffu, hit_a);
+    const unsigned mb = __ballot_sync(0xffffffffu, hit_b);
+    F.ta[lane] = term_a;
+    F.tb[lane] = term_b;
+    F.ib[lane] = ib;
+    __syncwarp();
+    if (lane == 0) {
+      for (unsigned m = ma; m; m &= m - 1) ta += F.ta[__ffs(m) - 1];
+      for (unsigned m = mb; m; m &= m - 1) {
+        const int j2 = __ffs(m) - 1;
+        tb += F.tb[j2];
+        cb += 1;
+        sb += F.ib[j2];
+      }
+    }
+    __syncwarp();
+  }
+  // 3. centre terms (lane 0): own field of a at x, competitor count/sum at x
+  double d = 0.0;
+  if (lane == 0) {
+    int32_t ca;
+    double sa;
+    const bool clean = own_field(0, 0, 0, f, a, ca, sa);
+    d = 0.0 + ta;
+    d = d + tb;
+    d += rho(vx, (sb + vx) / ((double)cb + 1.0), A.poisson);
+    d -= clean ? A.rho0[f] : rho(vx, sa / (double)ca, A.poisson);
+    d = d + A.lam * (double)di;
+  }
+  d = __shfl_sync(0xffffffffu, d, 0);
+  __syncwarp();
+  return d;
+}
 
 __global__ void __launch_bounds__(256) k_ps_dtot(const ParArgs A, const int64_t *__restrict__ acc,
                                                  const int64_t *__restrict__ moves,
@@ -3879,7 +4065,8 @@ struct StageTimer {
 };
 
 int32_t replay_chains(std::vector<PendingChain> &pending, const double *I, double *tot,
-                      double *tsq, cudaStream_t s) {
+                      double *tsq, cudaStream_t s,
+                      std::vector<PendingChain> *pool) {
   ParArgs A{};  // the sum chains read only their event lists
   DBuf<uint32_t> evkey, evkey2, evval, evval2;
   DBuf<int64_t> bounds;
@@ -3920,7 +4107,7 @@ int32_t replay_chains(std::vector<PendingChain> &pending, const double *I, doubl
   rc = run();
   evkey.release(s); evkey2.release(s); evval.release(s); evval2.release(s);
   bounds.release(s); evv.release(s); tmp.release(s);
-  drop_chains(pending, s);
+  drop_chains(pending, s, pool);
   return rc;
 }
 
@@ -3969,10 +4156,15 @@ __global__ void k_vanished(const int64_t *__restrict__ cnt, int32_t nl, int32_t 
     if (l > 0 && cnt[l] == 0) ncomp[l] = 0;
 }
 
-void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s) {
+void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s,
+                 std::vector<PendingChain> *pool) {
   for (PendingChain &pc : pending) {
-    pc.acc.release(s);
-    pc.moves.release(s);
+    if (pool) {
+      pool->push_back(pc);
+    } else {
+      pc.acc.release(s);
+      pc.moves.release(s);
+    }
   }
   pending.clear();
 }
@@ -4217,7 +4409,12 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaMemcpyAsync(A.cnt, A.cnt0, sizeof(int64_t) * A.nl, cudaMemcpyDeviceToDevice, s));
     k_count_moves<<<148 * 2, 256, 0, s>>>(X.acc, X.moves, A.cnt, A.nl);
     k_vanished<<<grid_for(A.nl, 256), 256, 0, s>>>(A.cnt, A.nl, X.ncomp);
-    X.pending->emplace_back();
+    if (X.chain_pool && !X.chain_pool->empty()) {
+      X.pending->push_back(X.chain_pool->back());
+      X.chain_pool->pop_back();
+    } else {
+      X.pending->emplace_back();
+    }
     PendingChain &pc = X.pending->back();
     RCB_TRY(pc.acc.reserve(3 * cap, s));
     RCB_TRY(pc.moves.reserve(1, s));
@@ -4225,7 +4422,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaMemcpyAsync(pc.moves.p, X.moves, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
     pc.cap = cap;
     pc.nl = A.nl;
-    if (X.pending->size() > 16) RCB_TRY(replay_chains(*X.pending, X.I, X.tot, X.tsq, s));
+    if (X.pending->size() > 16)
+      RCB_TRY(replay_chains(*X.pending, X.I, X.tot, X.tsq, s, X.chain_pool));
     T.mark("chains");
     if (!band_ledger) k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
     T.mark("ledger");

@@ -125,6 +125,13 @@ struct ParArgs {
   uint32_t *bigtouch;
   int2 *bigtouch_n;
   const int4 *rec;                // dataflow per-position records
+  // l2 mode, PS: the exact d_tot < 0 gate in the candidate's view
+  // (iteration-start own-label fields + corrections of earlier flips within 2R)
+  int region_ps;
+  const int32_t *Cown, *cb0;
+  const double *Sown, *rho0, *sb0;
+  const Off *ball;  // non-centre ball offsets, ball_offsets order
+  int nball, radius;
 };
 
 // PS runs: the per-label total / total_sq chains (only the stats API and the
@@ -168,7 +175,8 @@ struct ParExtra {
   long long *band;  // band ledger: kLimbs superaccumulator limbs + dE_int sum
   DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
-  std::vector<PendingChain> *pending = nullptr;  // PS: defer the total / total_sq chains here
+  std::vector<PendingChain> *pending = nullptr;
+  std::vector<PendingChain> *chain_pool = nullptr;  // recycled chain buffers  // PS: defer the total / total_sq chains here
   DBuf<uint32_t> *bigmap = nullptr, *bigfr2 = nullptr;  // dataflow large box tier (3-D)
   DBuf<uint8_t> *bigfg2 = nullptr;
   DBuf<uint32_t> *bigtouch = nullptr;
@@ -273,8 +281,12 @@ int32_t label_components(const int32_t *L, const Lat &lat, int full_fg, int32_t 
 int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches);
 // replay (then release) deferred total / total_sq chains in order
 int32_t replay_chains(std::vector<PendingChain> &pending, const double *I, double *tot,
-                      double *tsq, cudaStream_t s);
-void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s);
+                      double *tsq, cudaStream_t s,
+                      std::vector<PendingChain> *pool = nullptr);
+// pool != nullptr: keep the buffers there for reuse (no per-iteration
+// cudaMallocAsync of 10^8-byte lists, which mapped memory for ms at cfg4)
+void drop_chains(std::vector<PendingChain> &pending, cudaStream_t s,
+                 std::vector<PendingChain> *pool = nullptr);
 size_t accept_par_smem();
 
 // tables (abi.cu)

@@ -337,7 +337,19 @@ def big_runs():
         record_run(f"cfg5_{i}", s.image, s.labels, E("pc", "gauss"), S(4.0), O("sobolev"), 50,
                    keep_labels=False)
 
-    jobs = {"cfg2_full": cfg2_full, "cfg3": cfg3, "cfg4s": cfg4s}
+    def cfg4s_l2():
+        # PS/Poisson in l2 mode (the d_tot < 0 gate with PS fields), 3-D
+        s = scenes.cfg4_small()
+        record_run("cfg4s_l2", s.image, s.labels, E("ps", "poisson", **ps4), S(6.0),
+                   O("l2", vanish_grace=5, drift_tolerance=1e-3), 3, keep_labels=False)
+
+    def cfg2s_l2():
+        s = scenes.cfg2_small()
+        record_run("cfg2s_l2", s.image, s.labels, E("ps", "poisson", **ps4), S(6.0),
+                   O("l2", vanish_grace=5, drift_tolerance=1e-3), 4, keep_labels=False)
+
+    jobs = {"cfg2_full": cfg2_full, "cfg3": cfg3, "cfg4s": cfg4s, "cfg4s_l2": cfg4s_l2,
+            "cfg2s_l2": cfg2s_l2}
     for i in range(4):
         jobs[f"cfg5_{i}"] = (lambda i=i: cfg5(i))
     return jobs

@@ -9,7 +9,9 @@ acceptance order):
 * ``run_cfg3``       cfg3 128^3 PC/Gauss, E=4, iterations 1-3;
 * ``run_cfg4s``      cfg4' 128^3, 8 ellipsoids, bubbles:2:15, PS/Poisson R=4,
   E=6, iterations 1-6 (cfg4 itself needs a 1 TiB oracle, SURVEY §8c);
-* ``run_cfg5_{0..3}`` cfg5 images 0-3, 512^2 PC/Gauss, E=4, 50 iterations.
+* ``run_cfg5_{0..3}`` cfg5 images 0-3, 512^2 PC/Gauss, E=4, 50 iterations;
+* ``run_cfg2s_l2`` / ``run_cfg4s_l2``  the scaled cfg2 (256^2) and cfg4' in l2
+  mode: the PS d_tot < 0 gate of the dataflow acceptance (4 / 3 iterations).
 
 The scenes are regenerated here by ``scenes.py`` through the DEVICE synth
 pipeline (render, blur, poissonize); their sha-256 must equal the images the
@@ -45,6 +47,10 @@ def _cfgs(P, g, drift):
 
 def _scene(name):
     import scenes
+    if name == "cfg2s_l2":
+        return scenes.cfg2_small()
+    if name == "cfg4s_l2":
+        return scenes.cfg4_small()
     if name == "cfg2_full":
         return scenes.cfg2()
     if name == "cfg3":
@@ -85,13 +91,13 @@ def P():
 
 
 @pytest.mark.parametrize("name", ["cfg2_full", "cfg3", "cfg4s", "cfg5_0", "cfg5_1", "cfg5_2",
-                                  "cfg5_3"])
+                                  "cfg5_3", "cfg2s_l2", "cfg4s_l2"])
 def test_config_vs_reference_run(P, name):
     g = golden(f"run_{name}.npz")
     sc = _scene(name)
     assert sha(sc.image) == str(g["image_sha"][0]), f"{name}: device scene != reference scene"
     assert sha(sc.labels, np.int32) == str(g["init_sha"][0]), name
-    drift = 1e-3 if name in ("cfg2_full", "cfg4s") else 1e-6
+    drift = 1e-3 if name in ("cfg2_full", "cfg4s", "cfg2s_l2", "cfg4s_l2") else 1e-6
     ecfg, scfg, ocfg, approx = _cfgs(P, g, drift)
     eng = P.RegionCompetition(sc.image, sc.labels, ecfg, scfg, ocfg)
     _replay(eng, g, approx, name)

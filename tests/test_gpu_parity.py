@@ -580,3 +580,35 @@ def test_sobolev_site_kernel_multilabel_vs_oracle(P, shape):
         xs, ow, cm, rk = eng.last_candidates
         _, cnt = np.unique(xs, return_counts=True)
         assert cnt.max() >= 2
+
+
+@pytest.mark.parametrize("which,iters", [("ps2d", 4), ("ps3d", 3)])
+def test_ps_l2_dataflow_equals_sequential(P, monkeypatch, which, iters):
+    """l2 mode (PS/Poisson): the dataflow kernel's d_tot < 0 gate on own-label
+    fields corrected by the earlier flips within 2R, against K8 v1 (one
+    thread, incremental fields): moves in order, labels and ledger identical."""
+    import scenes
+    if which == "ps2d":
+        sc = scenes.cfg2_small(n=128)
+    else:
+        sc = scenes.cfg4(n=40, n_obj=5, per_axis=2, radius=9.0)
+    ecfg = P.EnergyConfig(sc.region, sc.noise, sc.lam, sc.smooth_radius)
+    ocfg = P.OptimizerConfig("l2", vanish_grace=sc.vanish_grace, drift_tolerance=1e-3)
+    runs = []
+    for mode in ("df", "seq"):
+        monkeypatch.setenv("RCB_PS_L2", mode)
+        eng = P.RegionCompetition(sc.image, sc.labels, ecfg, P.SobolevParams(sc.length_scale), ocfg)
+        out = []
+        for _ in range(iters):
+            rec = eng.iterate()
+            out.append((rec.moves, rec.energy, eng.last_accepted.copy(), eng.counters()["parallel"]))
+        out.append(eng.labels)
+        runs.append(out)
+    assert all(r[3] == 1 for r in runs[0][:-1]) and all(r[3] == 0 for r in runs[1][:-1])
+    for it, (a, b) in enumerate(zip(runs[0][:-1], runs[1][:-1])):
+        assert a[0] == b[0], (which, it, a[0], b[0])
+        assert np.array_equal(a[2], b[2]), (which, it)
+        # 3-D PS keeps the exact band ledger (K8 v1 sums d_tot in order): the
+        # two ledgers agree to rounding, the moves and labels bit for bit
+        assert abs(a[1] - b[1]) <= 1e-12 * abs(b[1]), (which, it, a[1], b[1])
+    assert np.array_equal(runs[0][-1], runs[1][-1])
