@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librcseg_b200.so")
+LIB_PATH = os.environ.get("RCB_LIB_PATH") or os.path.join(_HERE, "librcseg_b200.so")
 
 RCB_OK = 0
 RCB_ERR_VALUE = -1

@@ -101,3 +101,34 @@ def gather_summaries(local, group=None):
     except ImportError:
         pass
     return sorted(mine, key=lambda s: s.index)
+
+
+def compare_batch(images, inits, energy_config, sobolev_params=None, config=None, *,
+                  rank=None, world=None, device=None, in_flight: int = 8):
+    """Batched L2-vs-Sobolev comparison (cli.py:152-194 ``compare`` over many
+    images): every (image, gradient) pair is one device
+    engine, up to ``in_flight`` of them running concurrently on their own
+    streams; this rank takes its contiguous shard of the images.  Returns
+    [(index, {"l2": RunResult, "sobolev": RunResult})] in image order; each
+    result equals the one-at-a-time run (tests/test_gpu_batch.py)."""
+    from dataclasses import replace
+
+    from .optimizer import OptimizerConfig
+    if len(images) != len(inits):
+        raise ValueError("images and inits differ in length")
+    r, w = dist_info()
+    rank = r if rank is None else rank
+    world = w if world is None else world
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    base = config if config is not None else OptimizerConfig()
+    run_one = _device_runner(device)
+    mine = list(shard(len(images), world, rank))
+    with ThreadPoolExecutor(max_workers=max(1, in_flight)) as pool:
+        futs = [(i, g, pool.submit(run_one, images[i], inits[i], energy_config, sobolev_params,
+                                   replace(base, gradient=g)))
+                for i in mine for g in ("l2", "sobolev")]
+        out = {}
+        for i, g, f in futs:
+            out.setdefault(i, {})[g] = f.result()
+    return [(i, out[i]) for i in mine]

@@ -165,6 +165,8 @@ struct rcb_engine {
   DBuf<uint8_t> bigfg2;
   DBuf<uint32_t> bigtouch;
   DBuf<uint8_t> tflag;
+  DBuf<int32_t> ps_cells;  // l2 PS gate: the 2R ball as cube indices
+  int ps_ncells = 0;
   DBuf<int2> bigtouch_n;
   DBuf<long long> eval_limbs, band;
   DBuf<int4> rec;
@@ -223,7 +225,7 @@ struct rcb_engine {
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
       bigmap.release(s); bigfr2.release(s); bigfg2.release(s); bigtouch.release(s);
-      bigtouch_n.release(s); tflag.release(s);
+      bigtouch_n.release(s); tflag.release(s); ps_cells.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -398,8 +400,18 @@ int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b / 2 > cap) cap = free_b / 2;
       }
       if (want > cap) want = cap;
-      void *prime = nullptr;
-      if (cudaMallocAsync(&prime, want, s) == cudaSuccess) cudaFreeAsync(prime, s);
+      // prime in 1 GB blocks: the pool reuses freed blocks of the requested
+      // size class, and one huge priming block left later 10^8-byte requests
+      // mapping fresh memory (up to ~0.8 s per allocation on the first cfg4
+      // engine of a process, tools/alloc_probe.py)
+      std::vector<void *> blocks;
+      const size_t blk = (size_t)1 << 30;
+      for (size_t got = 0; got < want; got += blk) {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, std::min(blk, want - got), s) != cudaSuccess) break;
+        blocks.push_back(p);
+      }
+      for (void *p : blocks) cudaFreeAsync(p, s);
     }
     cudaGetLastError();
   }
@@ -773,6 +785,22 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.ball = e->ball.p;
         P.nball = e->nball;
         P.radius = e->ecfg.smooth_radius;
+        const char *fc = getenv("RCB_PS_L2_FLIPCAP");  // tests: 0 = always recount
+        P.ps_flipcap = fc ? atoi(fc) : 1 << 30;
+        if (P.l2 && !e->ps_cells.p) {  // the 2R ball as cube indices (side 4R + 1)
+          const int R = e->ecfg.smooth_radius, side = 4 * R + 1;
+          std::vector<int32_t> cells;
+          for (int dz = (lat.ndim == 3 ? -2 * R : 0); dz <= (lat.ndim == 3 ? 2 * R : 0); ++dz)
+            for (int dy = -2 * R; dy <= 2 * R; ++dy)
+              for (int dx = -2 * R; dx <= 2 * R; ++dx)
+                if (dz * dz + dy * dy + dx * dx <= 4 * R * R)
+                  cells.push_back(((lat.ndim == 3 ? dz + 2 * R : 0) * side + dy + 2 * R) * side +
+                                  dx + 2 * R);
+          RCB_TRY(upload(e->ps_cells, cells.data(), cells.size(), s));
+          e->ps_ncells = (int)cells.size();
+        }
+        P.ps_cells = e->ps_cells.p;
+        P.ps_ncells = e->ps_ncells;
       }
       if (P.l2 && !P.region_ps) {
         RCB_TRY(e->tot_run.reserve(e->nl, s));

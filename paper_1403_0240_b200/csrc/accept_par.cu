@@ -1075,7 +1075,10 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
 static constexpr int kHW = 1024;  // warp BFS hash entries
 static constexpr int kFW = 256;   // warp BFS frontier capacity
 static constexpr int kMaxInsertW = kHW * 5 / 8;
-static constexpr int kDfWarps = 16;
+#ifndef RCB_DF_WARPS
+#define RCB_DF_WARPS 16
+#endif
+static constexpr int kDfWarps = RCB_DF_WARPS;  // warps per dataflow block (one block per SM)
 
 // Polls use relaxed L2 loads; the waiter orders its later reads with one
 // acquire fence once the condition holds (fence-based synchronisation with the
@@ -2577,7 +2580,11 @@ __global__ void k_df_records(ParArgs A, int4 *__restrict__ rec) {
 __global__ void k_df_small(ParArgs A) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < A.nl; l += stride) {
-    const uint8_t sm = A.l2 || (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1) ? 1 : 0;
+    // PC l2 sequences every label (its d_tot reads the running statistics);
+    // PS d_tot reads only local fields, so as in Sobolev mode only labels that
+    // could run out of pixels (the vanish rule reads their count) are sequenced
+    const uint8_t sm = (A.l2 && !A.region_ps) || (l > 0 && A.cnt0[l] - (int64_t)A.nown[l] <= 1)
+                           ? 1 : 0;
     A.small[l] = sm;
     if (sm) atomicAdd(A.job + 4, 1ull);  // small-label count (host: skip empty event lists)
   }
@@ -3026,25 +3033,40 @@ __device__ __noinline__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t 
   const int z = is3 ? f / nxy : 0, frem = f - z * nxy;
   const int y = frem / nx, x = frem - y * nx;
   const double vx = __ldg(A.I + f);
+  // view-label bitmaps of the 2R cube (bit c: cell c has label a / b at
+  // pos), for R <= kMaskR: the exact recount when the flip list overflows
+  // (dense flips: cfg4's l2 iterations move a third of the sites)
+  constexpr int kMaskR = 4, kMaskWords = ((4 * kMaskR + 1) * (4 * kMaskR + 1) * (4 * kMaskR + 1) + 31) / 32;
+  static_assert(2 * kMaskWords * 4 <= sizeof(S.fr), "label bitmaps alias the frontier arrays");
+  uint32_t *mask_a = reinterpret_cast<uint32_t *>(S.fr), *mask_b = mask_a + kMaskWords;
+  const bool use_mask = R <= kMaskR;
+  const int ncell = (is3 ? side : 1) * side * side;
   __syncwarp();
   if (lane == 0) F.n = 0;
+  if (use_mask)
+    for (int k = lane; k < (ncell + 31) / 32; k += 32) mask_a[k] = mask_b[k] = 0u;
   __syncwarp();
-  // 1. settle the 2R neighbourhood and list its earlier flips
-  const int ncell = (is3 ? side : 1) * side * side;
-  for (int base = 0; base < ncell; base += 32) {
-    const int c = base + lane;
+  // 1. settle the 2R neighbourhood and list its earlier flips (lanes over
+  // the cells of the 2R ball, listed by the host as cube indices)
+  for (int base = 0; base < A.ps_ncells; base += 32) {
+    const int c = base + lane < A.ps_ncells ? __ldg(A.ps_cells + base + lane) : -1;
     int64_t g = -1;
     int ddz = 0, ddy = 0, ddx = 0;
-    if (c < ncell) {
+    if (c >= 0) {
       ddz = is3 ? c / (side * side) - 2 * R : 0;
       ddy = (c / side) % side - 2 * R;
       ddx = c % side - 2 * R;
       const int zz = z + ddz, yy = y + ddy, xx = x + ddx;
-      if (ddz * ddz + ddy * ddy + ddx * ddx <= R2w && (unsigned)zz < (unsigned)nz &&
-          (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx)
+      if ((unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx)
         g = ((int64_t)zz * ny + yy) * nx + xx;
     }
     const unsigned long long v = warp_wait_settled(A, g, pos);
+    (void)R2w;
+    if (use_mask && g >= 0) {
+      const int32_t lv = df_lab(bits, v, __ldg(A.L + g), pos);
+      if (lv == a) atomicOr(&mask_a[c >> 5], 1u << (c & 31));
+      if (lv == b) atomicOr(&mask_b[c >> 5], 1u << (c & 31));
+    }
     if (g >= 0 && wp_w(bits, v) < pos) {
       const int slot = atomicAdd(&F.n, 1);
       if (slot < kFlipCap) {
@@ -3059,7 +3081,7 @@ __device__ __noinline__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t 
   }
   __syncwarp();
   const int nf = F.n;
-  const bool list_ok = nf <= kFlipCap;
+  const bool list_ok = nf <= (A.ps_flipcap < kFlipCap ? A.ps_flipcap : kFlipCap);
   auto view_lab = [&](int64_t h) -> int32_t {
     return df_lab(bits, ld_rlx64(A.wp + h), __ldg(A.L + h), pos);
   };
@@ -3099,6 +3121,24 @@ __device__ __noinline__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t 
     const int gy = grem / nx, gx = grem - gy * nx;
     c = 0;
     sv = 0.0;
+    if (use_mask && (lg == a || lg == b)) {
+      // the ball of g from the view-label bitmap of the 2R cube: cell index
+      // of offset (oz + qz, oy + qy, ox + qx) around x; I from global memory
+      const uint32_t *m = lg == a ? mask_a : mask_b;
+      for (int q = 0; q <= A.nball; ++q) {
+        const Off o2 = q == 0 ? Off{0, 0, 0, 0} : A.ball[q - 1];
+        const int z2 = gz + o2.dz, y2 = gy + o2.dy, x2 = gx + o2.dx;
+        if ((unsigned)z2 >= (unsigned)nz || (unsigned)y2 >= (unsigned)ny ||
+            (unsigned)x2 >= (unsigned)nx)
+          continue;
+        const int cz = is3 ? oz + o2.dz + 2 * R : 0;
+        const int ci = (cz * side + (oy + o2.dy + 2 * R)) * side + (ox + o2.dx + 2 * R);
+        if (!((m[ci >> 5] >> (ci & 31)) & 1u)) continue;
+        c += 1;
+        sv += __ldg(A.I + ((int64_t)z2 * ny + y2) * nx + x2);
+      }
+      return false;
+    }
     for (int q = 0; q <= A.nball; ++q) {
       const Off o2 = q == 0 ? Off{0, 0, 0, 0} : A.ball[q - 1];
       const int z2 = gz + o2.dz, y2 = gy + o2.dy, x2 = gx + o2.dx;

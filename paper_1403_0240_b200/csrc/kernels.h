@@ -132,6 +132,9 @@ struct ParArgs {
   const double *Sown, *rho0, *sb0;
   const Off *ball;  // non-centre ball offsets, ball_offsets order
   int nball, radius;
+  int ps_flipcap;   // flip-list capacity used (tests: 0 forces the bitmap recount)
+  const int32_t *ps_cells;  // cube indices (side 4R+1) of the 2R-ball offsets
+  int ps_ncells;
 };
 
 // PS runs: the per-label total / total_sq chains (only the stats API and the

@@ -295,10 +295,11 @@ __global__ void __launch_bounds__(256) k_sobolev_site(
   for (int j = 0; j < kSiteChunks; ++j) {
     const int64_t p = wbase + 32 * j + lane;
     const bool in = p < p1;
-    fv[j] = in ? __ldg(&px[p]) : 0xffffffffu - (uint32_t)lane;  // distinct sentinels
-    ov[j] = in ? __ldg(&pown[p]) : -1;
-    cv[j] = in ? __ldg(&pcomp[p]) : -2;
-    rv[j] = in ? __ldg(&raw[p]) : 0.0;
+    // streaming loads: every byte is read once (neighbour probes hit L1/L2)
+    fv[j] = in ? __ldcs(&px[p]) : 0xffffffffu - (uint32_t)lane;  // distinct sentinels
+    ov[j] = in ? __ldcs(&pown[p]) : -1;
+    cv[j] = in ? __ldcs(&pcomp[p]) : -2;
+    rv[j] = in ? __ldcs(&raw[p]) : 0.0;
   }
   unsigned long long np = 0;
 #pragma unroll
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(256) k_sobolev_site(
     const double total = __shfl_sync(0xffffffffu, acc, tl);
     if (in) {
       if (simple) {
-        out[p] = total / (double)len - 0.0;
+        __stcs(&out[p], total / (double)len - 0.0);
         np += (unsigned long long)len;
       } else {
         int64_t L = 0;
