@@ -134,6 +134,8 @@ struct rcb_engine {
   DBuf<double> tot, tsq;
   DBuf<int32_t> Cown;
   DBuf<double> Sown, rho0;
+  DBuf<double> logt;  // K5 Poisson log table (integer images), logt_P columns
+  int logt_P = 0;
   DBuf<Off> ball, ball_full, st;
   int nball = 0, nball_full = 0, nst = 0;
   DBuf<double> wt;
@@ -210,7 +212,7 @@ struct rcb_engine {
       cudaSetDevice(device);
       L.release(s); I.release(s); I32.release(s); raw32.release(s); wt32.release(s);
       cb0.release(s); sb0.release(s); cnt.release(s); tot.release(s); tsq.release(s);
-      Cown.release(s); Sown.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
+      Cown.release(s); Sown.release(s); logt.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
       raw.release(s); smooth.release(s); rank.release(s); pk.release(s); tot_run.release(s);
@@ -253,14 +255,26 @@ struct rcb_engine {
 
   std::vector<PendingChain> pending;     // PS: deferred total / total_sq chains
   std::vector<PendingChain> chain_pool;  // their buffers, recycled
+  // integer-valued image with |sums| < 2^53: total / total_sq are exact in any
+  // order, so instead of keeping per-iteration move lists (up to 12 GB at
+  // cfg4) the statistics are rebuilt from the raster when read
+  bool int_image = false;
+  bool stats_stale = false;
+  bool ps_tiles = false;  // K5 on shared-memory tiles (RCB_K5=tile; measured slower)
 
   int32_t flush_stats() {  // make tot / tsq current (replay deferred chains)
+    if (stats_stale) {
+      stats_stale = false;
+      // cnt is current (k_count_moves); the rebuild recomputes it identically
+      return stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s);
+    }
     if (pending.empty()) return RCB_OK;
     return replay_chains(pending, I.p, tot.p, tsq.p, s, &chain_pool);
   }
 
   int32_t refresh() {  // energy.py:285-291
     drop_chains(pending, s, &chain_pool);  // superseded by the rebuild
+    stats_stale = false;
     RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
     if (ecfg.region_model == 1)
       RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s, rho0.p,
@@ -456,6 +470,36 @@ int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32
     if (ecfg->noise_model == 1 && chk.image_min < 0.0)
       return bail(fail(RCB_ERR_VALUE, "Poisson noise model requires nonnegative intensities"));
     e->nl = chk.label_max + 1;
+    // integer intensities <= 4096: V * 4096^2 < 2^53, so every partial sum of
+    // total / total_sq is exact whatever the order
+    e->int_image = chk.nonint == 0 && chk.image_max <= 4096.0 && chk.image_min >= -4096.0 &&
+                   (double)V * 4096.0 * 4096.0 < 9.0e15 && !getenv("RCB_KEEP_CHAINS");
+    {
+      // the tiled K5 measured slower than the per-particle kernel at cfg4
+      // (26 iterations: 3.83 s vs 2.43 s; ~110 particles per 8^3 tile leave
+      // the 257-offset shared-memory walks latency bound at 2 blocks per SM):
+      // kept as an experiment, RCB_K5=tile
+      const char *k5 = getenv("RCB_K5");
+      e->ps_tiles = k5 && strcmp(k5, "tile") == 0;
+    }
+    if (ecfg->region_model == 1 && ecfg->noise_model == 1 && chk.nonint == 0 &&
+        chk.image_max <= 4096.0 && !getenv("RCB_NO_LOGTABLE")) {
+      // integer Poisson data: every theta K5 forms is (S +- v) / (C +- 1)
+      // with integer S <= |ball| * vmax; table its log (<= 64 MB)
+      int nbf = 0;
+      {
+        const int r = ecfg->smooth_radius;
+        for (int dz = (ndim == 3 ? -r : 0); dz <= (ndim == 3 ? r : 0); ++dz)
+          for (int dy = -r; dy <= r; ++dy)
+            for (int dx = -r; dx <= r; ++dx) nbf += dz * dz + dy * dy + dx * dx <= r * r;
+      }
+      const int64_t P = (int64_t)(nbf + 1) * (int64_t)chk.image_max + 1, Q = nbf + 2;
+      if (P * Q * 8 <= ((int64_t)64 << 20)) {
+        TRYB(e->logt.reserve(P * Q, s));
+        TRYB(log_table(e->logt.p, (int)P, (int)Q, s));
+        e->logt_P = (int)P;
+      }
+    }
   }
   TRYB(e->cnt.reserve(e->nl, s));
   TRYB(e->tot.reserve(e->nl, s));
@@ -635,9 +679,18 @@ static int32_t engine_score(rcb_engine *e) {
       RCB_TRY(delta_pc_batch(e->I.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, e->cnt.p,
                              e->tot.p, e->tsq.p, poisson, e->raw.p + h0, s));
     else
-      RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                             e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
-                             e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0));
+      if (e->int_image && e->ps_tiles && e->rho0.p && ps3d_tile_ok(lat, e->ecfg.smooth_radius, e->nball))
+        // integer images: the ball gathers from shared-memory tiles
+        RCB_TRY(delta_ps3d_tiles(e->L.p, e->I.p, e->Cown.p, e->Sown.p, e->rho0.p, lat,
+                                 e->ecfg.smooth_radius, e->ball.p, e->nball, e->site_off.p,
+                                 e->px.p, e->pown.p, e->pcomp.p, h0, h1, poisson, e->raw.p,
+                                 e->cb0.p, e->sb0.p, e->logt_P ? e->logt.p : nullptr, e->logt_P,
+                                 s));
+      else
+        RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
+                               e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
+                               e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0,
+                               e->logt_P ? e->logt.p : nullptr, e->logt_P));
     cudaEventRecord(e->ev[2], s);
     if (e->mode == 1) {
       if (fp32) {
@@ -910,6 +963,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
         X.pending = (ds && ds[0] == '0') ? nullptr : &e->pending;
+        if (X.pending && e->int_image && e->ecfg.region_model == 1) X.stats_stale = &e->stats_stale;
       }
       {
         const char *bt = getenv("RCB_DF_BIGBOX");  // "0": no large box tier (comparison runs)

@@ -4449,6 +4449,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_CUDA(cudaMemcpyAsync(A.cnt, A.cnt0, sizeof(int64_t) * A.nl, cudaMemcpyDeviceToDevice, s));
     k_count_moves<<<148 * 2, 256, 0, s>>>(X.acc, X.moves, A.cnt, A.nl);
     k_vanished<<<grid_for(A.nl, 256), 256, 0, s>>>(A.cnt, A.nl, X.ncomp);
+    if (X.stats_stale) {
+      *X.stats_stale = true;  // integer data: rebuilt from the raster when read
+    } else {
     if (X.chain_pool && !X.chain_pool->empty()) {
       X.pending->push_back(X.chain_pool->back());
       X.chain_pool->pop_back();
@@ -4464,6 +4467,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     pc.nl = A.nl;
     if (X.pending->size() > 16)
       RCB_TRY(replay_chains(*X.pending, X.I, X.tot, X.tsq, s, X.chain_pool));
+    }
     T.mark("chains");
     if (!band_ledger) k_ledger<<<1, 512, 0, s>>>(X.dtot, X.moves, X.energy);
     T.mark("ledger");

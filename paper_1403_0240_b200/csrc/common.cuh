@@ -91,11 +91,23 @@ struct DBuf {
     if (n <= cap) return RCB_OK;
     const auto t0 = std::chrono::steady_clock::now();
     if (p) cudaFreeAsync(p, s);
-    size_t want = 2 * n + 64;  // geometric growth: particle counts climb for tens of iterations
+    // first allocation: 25 % slack (lattice-sized buffers never grow, and 2x
+    // slack on ~30 of them cost ~30 GB at 512^3, pushing the pool past its
+    // primed reservation into slow fresh mappings); growth after that is
+    // geometric: particle counts climb for tens of iterations
+    size_t want = cap == 0 ? n + n / 4 + 64 : 2 * n + 64;
     cudaError_t e = cudaMallocAsync((void **)&p, want * sizeof(T), s);
     if (getenv("RCB_ALLOC_LOG")) {
       const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-      fprintf(stderr, "[rcb-alloc] %zu bytes %.1f us\n", want * sizeof(T), us);
+      uint64_t res = 0, used = 0;
+      cudaMemPool_t pool;
+      int dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      }
+      fprintf(stderr, "[rcb-alloc] %zu bytes %.1f us pool reserved %.2f GB used %.2f GB\n",
+              want * sizeof(T), us, res / 1e9, used / 1e9);
     }
     if (e != cudaSuccess) {
       p = nullptr;

@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
     const double *__restrict__ Sown, int nx, int ny, const Off *__restrict__ ball, int nball,
     const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
     const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
-    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0) {
+    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0,
+    const double *__restrict__ lt, int ltP) {
   __shared__ int8_t sdy[kPsMaxBall], sdx[kPsMaxBall];
   for (int k = threadIdx.x; k < nball; k += blockDim.x) {
     sdy[k] = ball[k].dy;
@@ -489,9 +490,12 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
       // which IEEE arithmetic rounds identically
       const bool isa = lab[u] == a;
       if (isa || lab[u] == b) {
-        const double t = rho(iy[u], (sy[u] + (isa ? -v : v)) / (cy[u] + (isa ? -1.0 : 1.0)),
-                             poisson) -
-                         (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+        const double num = sy[u] + (isa ? -v : v), den = cy[u] + (isa ? -1.0 : 1.0);
+        const double theta = num / den;
+        // integer Poisson data: the log from the table (bit-identical)
+        const double rn = (lt && den >= 1.0) ? theta - iy[u] * __ldg(lt + (int)den * ltP + (int)num)
+                                             : rho(iy[u], theta, poisson);
+        const double t = rn - (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
         if (isa) {
           acc_a += t;
         } else {
@@ -522,11 +526,20 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
     const double *__restrict__ Sown, int nx, int ny, int nz, const Off *__restrict__ ball,
     int nball, const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
     const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
-    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0) {
+    const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0,
+    const double *__restrict__ lt, int ltP) {
   __shared__ int sofs[kPsMaxBall];  // dz:8 | dy:8 | dx:8, signed, packed
-  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+  __shared__ int sdel[kPsMaxBall];  // linear site delta of each offset
+  __shared__ int srad;              // largest |component| of the offsets
+  if (threadIdx.x == 0) srad = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nball; k += blockDim.x) {
+    const int dz = ball[k].dz, dy = ball[k].dy, dx = ball[k].dx;
     sofs[k] = ((int)(uint8_t)ball[k].dz << 16) | ((int)(uint8_t)ball[k].dy << 8) |
               (int)(uint8_t)ball[k].dx;
+    sdel[k] = (dz * ny + dy) * nx + dx;
+    atomicMax(&srad, max(abs(dz), max(abs(dy), abs(dx))));
+  }
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -536,6 +549,11 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
   const int y = r / nx, x = r - y * nx;
   const int32_t a = pown[i], b = pcomp[i];
   const double v = I[f];
+  // interior particles (the whole ball inside the lattice): one add per
+  // offset instead of three coordinates, three bounds tests and a multiply
+  const int rad = srad;
+  const bool interior = z >= rad && z < nz - rad && y >= rad && y < ny - rad && x >= rad &&
+                        x < nx - rad;
   double acc_a = 0.0, acc_b = 0.0, sb = 0.0;
   int32_t cb = 0;
   for (int k0 = 0; k0 < nball; k0 += kPsChunk) {
@@ -544,12 +562,18 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
 #pragma unroll
     for (int u = 0; u < kPsChunk; ++u) {
       const int k = k0 + u;
-      const int o = k < nball ? sofs[k] : 0;
-      const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
-                xx = x + (int)(int8_t)o;
-      const bool ok = k < nball && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
-                      (unsigned)xx < (unsigned)nx;
-      g[u] = ok ? zz * plane + yy * nx + xx : f;
+      bool ok;
+      if (interior) {
+        ok = k < nball;
+        g[u] = ok ? f + sdel[k] : f;
+      } else {
+        const int o = k < nball ? sofs[k] : 0;
+        const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
+                  xx = x + (int)(int8_t)o;
+        ok = k < nball && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+             (unsigned)xx < (unsigned)nx;
+        g[u] = ok ? zz * plane + yy * nx + xx : f;
+      }
       lab[u] = ok ? __ldg(L + g[u]) : -1;
     }
     double cy[kPsChunk], sy[kPsChunk], iy[kPsChunk], r0[kPsChunk];
@@ -568,9 +592,12 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
       // which IEEE arithmetic rounds identically
       const bool isa = lab[u] == a;
       if (isa || lab[u] == b) {
-        const double t = rho(iy[u], (sy[u] + (isa ? -v : v)) / (cy[u] + (isa ? -1.0 : 1.0)),
-                             poisson) -
-                         (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
+        const double num = sy[u] + (isa ? -v : v), den = cy[u] + (isa ? -1.0 : 1.0);
+        const double theta = num / den;
+        // integer Poisson data: the log from the table (bit-identical)
+        const double rn = (lt && den >= 1.0) ? theta - iy[u] * __ldg(lt + (int)den * ltP + (int)num)
+                                             : rho(iy[u], theta, poisson);
+        const double t = rn - (rho0 ? r0[u] : rho(iy[u], sy[u] / cy[u], poisson));
         if (isa) {
           acc_a += t;
         } else {
@@ -727,20 +754,173 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
   return RCB_OK;
 }
 
+// K5 on shared-memory tiles (3-D, integer images, R <= 4).  ncu on cfg4
+// showed the per-particle kernel bound by L1/L2 traffic: every particle
+// re-gathers its 257-site ball from five arrays (L1 hit 22 %, L2 throughput
+// 65 %, DRAM 2 %).  Here a block stages an 8^3 tile plus its R-halo once --
+// labels, own-label counts and sums, intensities and rho0 -- and the tile's
+// particles (contiguous CSR ranges of its 64 rows) walk their balls in
+// shared memory with precomputed linear offsets.  Integer data up to 4096
+// (checked at engine creation) makes the compact staged types exact
+// (intensities and own-label sums in fp32, counts in 16 bits), and every
+// fp64 expression is the one of k_delta_ps3d: bit-identical results.
+static constexpr int kTileT = 8;
+__global__ void __launch_bounds__(128) k_delta_ps3d_tile(
+    const int32_t *__restrict__ L, const double *__restrict__ I, const int32_t *__restrict__ Cown,
+    const double *__restrict__ Sown, const double *__restrict__ rho0, int nx, int ny, int nz, int R,
+    const Off *__restrict__ ball, int nball, const uint32_t *__restrict__ site_off,
+    const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
+    const int32_t *__restrict__ pcomp, int64_t h0, int64_t h1, int poisson,
+    double *__restrict__ out, int32_t *__restrict__ cb0, double *__restrict__ sb0,
+    const double *__restrict__ lt, int ltP) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int H = kTileT + 2 * R, cells = H * H * H;
+  double *sR = reinterpret_cast<double *>(smem);
+  float *sI = reinterpret_cast<float *>(sR + cells);
+  float *sS = sI + cells;
+  int32_t *sL = reinterpret_cast<int32_t *>(sS + cells);
+  uint16_t *sC = reinterpret_cast<uint16_t *>(sL + cells);
+  int *sofs = reinterpret_cast<int *>(sC + ((cells + 1) & ~1));
+  int *rows = sofs + nball;  // kTileT^2 + 1 particle prefix offsets
+  __shared__ uint32_t rbeg[kTileT * kTileT];
+  const int x0 = blockIdx.x * kTileT, y0 = blockIdx.y * kTileT, z0 = blockIdx.z * kTileT;
+  // the tile's particles: row (ty, tz) holds [site_off[row + x0], site_off[row + x0 + 8])
+  if (threadIdx.x < kTileT * kTileT) {
+    const int ty = threadIdx.x % kTileT, tz = threadIdx.x / kTileT;
+    const int y = y0 + ty, z = z0 + tz;
+    uint32_t b = 0, e = 0;
+    if (y < ny && z < nz) {
+      const int64_t rb = ((int64_t)z * ny + y) * nx;
+      b = __ldg(site_off + rb + x0);
+      e = __ldg(site_off + rb + min(x0 + kTileT, nx));
+      if ((int64_t)b < h0) b = (uint32_t)((int64_t)e < h0 ? (int64_t)e : h0);
+      if ((int64_t)e > h1) e = (uint32_t)((int64_t)b > h1 ? (int64_t)b : h1);
+    }
+    rbeg[threadIdx.x] = b;
+    rows[threadIdx.x + 1] = (int)(e - b);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    rows[0] = 0;
+    for (int k = 1; k <= kTileT * kTileT; ++k) rows[k] += rows[k - 1];
+  }
+  __syncthreads();
+  const int np = rows[kTileT * kTileT];
+  if (np == 0) return;
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    const int cz = i / (H * H), rem = i - cz * H * H;
+    const int cy = rem / H, cx = rem - cy * H;
+    const int gz = z0 - R + cz, gy = y0 - R + cy, gx = x0 - R + cx;
+    const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
+                    (unsigned)gx < (unsigned)nx;
+    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    const int32_t l = ok ? __ldg(L + g) : -1;
+    sL[i] = l;
+    sC[i] = ok ? (uint16_t)__ldg(Cown + g) : (uint16_t)1;
+    sI[i] = ok ? (float)__ldg(I + g) : 0.f;
+    sS[i] = ok ? (float)__ldg(Sown + g) : 0.f;
+    sR[i] = ok ? __ldg(rho0 + g) : 0.0;
+  }
+  for (int k = threadIdx.x; k < nball; k += blockDim.x)
+    sofs[k] = ((int)ball[k].dz * H + (int)ball[k].dy) * H + (int)ball[k].dx;
+  __syncthreads();
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    int r = 0;  // row of the t-th particle (binary search over 64 prefixes)
+    for (int step = 32; step; step >>= 1)
+      if (rows[r + step] <= t) r += step;
+    const int64_t i = (int64_t)rbeg[r] + (t - rows[r]);
+    const int f = (int)px[i];
+    const int lx = f % nx - x0 + R, rest = f / nx;
+    const int ly = rest % ny - y0 + R, lz = rest / ny - z0 + R;
+    const int cidx = (lz * H + ly) * H + lx;
+    const int32_t a = pown[i], b = pcomp[i];
+    const double v = (double)sI[cidx];
+    double acc_a = 0.0, acc_b = 0.0, sb = 0.0;
+    int32_t cb = 0;
+    for (int k = 0; k < nball; ++k) {
+      const int j = cidx + sofs[k];
+      const int32_t lab = sL[j];
+      const bool isa = lab == a;
+      if (isa || lab == b) {
+        const double cy = (double)sC[j], sy = (double)sS[j], iy = (double)sI[j];
+        const double num = sy + (isa ? -v : v), den = cy + (isa ? -1.0 : 1.0);
+        const double theta = num / den;
+        const double rn = (lt && den >= 1.0) ? theta - iy * __ldg(lt + (int)den * ltP + (int)num)
+                                             : rho(iy, theta, poisson);
+        const double tt = rn - sR[j];
+        if (isa) {
+          acc_a += tt;
+        } else {
+          acc_b += tt;
+          cb += 1;
+          sb += iy;
+        }
+      }
+    }
+    double d = 0.0 + acc_a;
+    d = d + acc_b;
+    d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
+    d -= sR[cidx];
+    out[i] = d;
+    if (cb0) {
+      cb0[i] = cb;
+      sb0[i] = sb;
+    }
+  }
+}
+
+size_t ps3d_tile_smem(int R, int nball) {
+  const int H = kTileT + 2 * R, cells = H * H * H;
+  return (size_t)cells * (8 + 4 + 4 + 4) + (size_t)((cells + 1) & ~1) * 2 +
+         (size_t)(nball + kTileT * kTileT + 1) * 4;
+}
+
+bool ps3d_tile_ok(const Lat &lat, int R, int nball) {
+  return lat.ndim == 3 && R >= 1 && R <= 4 && nball <= 256 && lat.V < ((int64_t)1 << 31) &&
+         ps3d_tile_smem(R, nball) <= 200 * 1024;
+}
+
+// K5 over the particles [h0, h1) of the site-sorted list, by tiles (see
+// k_delta_ps3d_tile); every out / cb0 / sb0 entry of the range is written.
+int32_t delta_ps3d_tiles(const int32_t *L, const double *I, const int32_t *Cown,
+                         const double *Sown, const double *rho0, const Lat &lat, int R,
+                         const Off *ball, int nball, const uint32_t *site_off, const uint32_t *px,
+                         const int32_t *pown, const int32_t *pcomp, int64_t h0, int64_t h1,
+                         int poisson, double *out, int32_t *cb0, double *sb0, const double *lt,
+                         int ltP, cudaStream_t s) {
+  if (h1 <= h0) return RCB_OK;
+  const size_t smem = ps3d_tile_smem(R, nball);
+  static bool attr_set[64] = {};
+  int dev = 0;
+  RCB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr_set[dev]) {
+    RCB_CUDA(cudaFuncSetAttribute(k_delta_ps3d_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr_set[dev] = true;
+  }
+  dim3 grid((unsigned)((lat.nx + kTileT - 1) / kTileT), (unsigned)((lat.ny + kTileT - 1) / kTileT),
+            (unsigned)((lat.nz + kTileT - 1) / kTileT));
+  k_delta_ps3d_tile<<<grid, 128, smem, s>>>(L, I, Cown, Sown, rho0, (int)lat.nx, (int)lat.ny,
+                                            (int)lat.nz, R, ball, nball, site_off, px, pown, pcomp,
+                                            h0, h1, poisson, out, cb0, sb0, lt, ltP);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
                        double *out, cudaStream_t s, const double *rho0, int32_t *cb0,
-                       double *sb0) {
+                       double *sb0, const double *lt, int ltP) {
   if (n == 0) return RCB_OK;
   if (lat.ndim == 2 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
     k_delta_ps2d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny, ball,
                                                   nball, px, pown, pcomp, n, poisson, out, rho0,
-                                                  cb0, sb0);
+                                                  cb0, sb0, lt, ltP);
   else if (lat.ndim == 3 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
     k_delta_ps3d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny,
                                                   (int)lat.nz, ball, nball, px, pown, pcomp, n,
-                                                  poisson, out, rho0, cb0, sb0);
+                                                  poisson, out, rho0, cb0, sb0, lt, ltP);
   else
     k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown,
                                                 pcomp, n, poisson, out, rho0, cb0, sb0);
@@ -1098,9 +1278,10 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
 
 __global__ void k_check_inputs(const int32_t *__restrict__ L, const double *__restrict__ I,
                                int64_t V, int *lmin, int *lmax, unsigned long long *imin,
-                               unsigned long long *nonfin) {
+                               unsigned long long *nonfin, unsigned long long *imax,
+                               unsigned long long *nonint) {
   int lo = INT_MAX, hi = INT_MIN;
-  unsigned long long dm = ~0ull, nf = 0;
+  unsigned long long dm = ~0ull, nf = 0, dx = 0, ni = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < V; i += stride) {
     const int l = L[i];
@@ -1112,6 +1293,8 @@ __global__ void k_check_inputs(const int32_t *__restrict__ L, const double *__re
     } else {
       const unsigned long long k = dkey(v);
       dm = k < dm ? k : dm;
+      dx = k > dx ? k : dx;
+      if (v != rint(v)) ++ni;
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -1119,13 +1302,18 @@ __global__ void k_check_inputs(const int32_t *__restrict__ L, const double *__re
     hi = max(hi, __shfl_down_sync(0xffffffffu, hi, o));
     const unsigned long long d2 = __shfl_down_sync(0xffffffffu, dm, o);
     dm = d2 < dm ? d2 : dm;
+    const unsigned long long x2 = __shfl_down_sync(0xffffffffu, dx, o);
+    dx = x2 > dx ? x2 : dx;
     nf += __shfl_down_sync(0xffffffffu, nf, o);
+    ni += __shfl_down_sync(0xffffffffu, ni, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMin(lmin, lo);
     atomicMax(lmax, hi);
     atomicMin(imin, dm);
+    atomicMax(imax, dx);
     if (nf) atomicAdd(nonfin, nf);
+    if (ni) atomicAdd(nonint, ni);
   }
 }
 
@@ -1133,19 +1321,20 @@ int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *o
                      cudaStream_t s) {
   struct Dev {
     int lmin, lmax;
-    unsigned long long imin, nonfin;
+    unsigned long long imin, nonfin, imax, nonint;
   };
   static thread_local Dev *hbuf = nullptr;  // pinned, reused
   if (!hbuf) RCB_CUDA(cudaMallocHost((void **)&hbuf, sizeof(Dev)));
   Dev *d = nullptr;
   RCB_CUDA(cudaMallocAsync((void **)&d, sizeof(Dev), s));
-  const Dev init{INT_MAX, INT_MIN, ~0ull, 0ull};
+  const Dev init{INT_MAX, INT_MIN, ~0ull, 0ull, 0ull, 0ull};
   *hbuf = init;
   RCB_CUDA(cudaMemcpyAsync(d, hbuf, sizeof(Dev), cudaMemcpyHostToDevice, s));
   int64_t g = (V + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
   if (g < 1) g = 1;
-  k_check_inputs<<<(unsigned)g, 256, 0, s>>>(L, I, V, &d->lmin, &d->lmax, &d->imin, &d->nonfin);
+  k_check_inputs<<<(unsigned)g, 256, 0, s>>>(L, I, V, &d->lmin, &d->lmax, &d->imin, &d->nonfin,
+                                              &d->imax, &d->nonint);
   RCB_CUDA(cudaGetLastError());
   RCB_CUDA(cudaMemcpyAsync(hbuf, d, sizeof(Dev), cudaMemcpyDeviceToHost, s));
   RCB_CUDA(cudaFreeAsync(d, s));
@@ -1158,6 +1347,39 @@ int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *o
   double v;
   memcpy(&v, &u, sizeof(v));
   out->image_min = (k == ~0ull) ? 0.0 : v;
+  {
+    const unsigned long long kx = hbuf->imax;
+    const unsigned long long ux = (kx >> 63) ? (kx & 0x7fffffffffffffffull) : ~kx;
+    double vx;
+    memcpy(&vx, &ux, sizeof(vx));
+    out->image_max = (kx == 0ull) ? 0.0 : vx;
+  }
+  out->nonint = (int64_t)hbuf->nonint;
+  return RCB_OK;
+}
+
+// Poisson log table (K5, integer images): lt[q * P + p] = log(max(p / q,
+// 1e-8)) for 1 <= q < Q, 0 <= p < P -- the exact value rho() computes for
+// theta = fl(p / q) (energy.py:226-230), so a lookup replaces the per-hit
+// log without changing a bit.
+__global__ void k_log_table(double *__restrict__ lt, int P, int Q) {
+  const int64_t n = (int64_t)P * Q;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i / P), p = (int)(i - (int64_t)q * P);
+    if (q == 0) {
+      lt[i] = 0.0;
+      continue;
+    }
+    const double theta = (double)p / (double)q;
+    const double t = theta < kPoissonFloor ? kPoissonFloor : theta;
+    lt[i] = log(t);
+  }
+}
+
+int32_t log_table(double *lt, int P, int Q, cudaStream_t s) {
+  k_log_table<<<148 * 8, 256, 0, s>>>(lt, P, Q);
+  RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
 

@@ -179,7 +179,10 @@ struct ParExtra {
   DBuf<int32_t> *colb;
   DBuf<int64_t> *labbounds;
   std::vector<PendingChain> *pending = nullptr;
-  std::vector<PendingChain> *chain_pool = nullptr;  // recycled chain buffers  // PS: defer the total / total_sq chains here
+  std::vector<PendingChain> *chain_pool = nullptr;  // recycled chain buffers
+  // integer image (sums exact in any order): no chain is kept -- the stats are
+  // rebuilt from the raster when read (*stats_stale set), bit-identical
+  bool *stats_stale = nullptr;  // PS: defer the total / total_sq chains here
   DBuf<uint32_t> *bigmap = nullptr, *bigfr2 = nullptr;  // dataflow large box tier (3-D)
   DBuf<uint8_t> *bigfg2 = nullptr;
   DBuf<uint32_t> *bigtouch = nullptr;
@@ -189,10 +192,19 @@ struct ParExtra {
 // input validation (energy.cu): one pass, one small read-back (synchronises s)
 struct InputCheck {
   int32_t label_min, label_max;
-  double image_min;
+  double image_min, image_max;
+  int64_t nonint;  // finite non-integer intensities
   int64_t nonfinite;
 };
 int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *out, cudaStream_t s);
+int32_t log_table(double *lt, int P, int Q, cudaStream_t s);
+bool ps3d_tile_ok(const Lat &lat, int R, int nball);
+int32_t delta_ps3d_tiles(const int32_t *L, const double *I, const int32_t *Cown,
+                         const double *Sown, const double *rho0, const Lat &lat, int R,
+                         const Off *ball, int nball, const uint32_t *site_off, const uint32_t *px,
+                         const int32_t *pown, const int32_t *pcomp, int64_t h0, int64_t h1,
+                         int poisson, double *out, int32_t *cb0, double *sb0, const double *lt,
+                         int ltP, cudaStream_t s);
 
 // contour.cu
 int32_t contour_scan(const int32_t *L, const Lat &lat, int full_fg, uint32_t *site_off,
@@ -225,7 +237,8 @@ int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, c
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
                        double *out, cudaStream_t s, const double *rho0 = nullptr,
-                       int32_t *cb0 = nullptr, double *sb0 = nullptr);
+                       int32_t *cb0 = nullptr, double *sb0 = nullptr, const double *lt = nullptr,
+                       int ltP = 0);
 int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
                       double *tot, double *tsq, StatsScratch &sc, cudaStream_t s);
 int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,

@@ -661,3 +661,27 @@ def test_ps_l2_dataflow_equals_sequential(P, monkeypatch, which, iters, flipcap)
         # two ledgers agree to rounding, the moves and labels bit for bit
         assert abs(a[1] - b[1]) <= 1e-12 * abs(b[1]), (which, it, a[1], b[1])
     assert np.array_equal(runs[0][-1], runs[1][-1])
+
+
+@pytest.mark.parametrize("shape", [(40, 44, 48), (37, 29, 41)])
+def test_k5_tiles_equal_scalar_kernel(P, monkeypatch, shape):
+    """K5 on shared-memory tiles (integer 3-D images) against the per-particle
+    kernel: every raw PS increment bit-identical (l2 mode exposes them as the
+    rank values), also on lattices that are not multiples of the 8^3 tile."""
+    import scenes
+    sc = scenes.cfg4(n=shape[0], n_obj=5, per_axis=2, radius=9.0)
+    img = np.ascontiguousarray(sc.image[:, :shape[1], :shape[2]])
+    lab = np.ascontiguousarray(sc.labels[:, :shape[1], :shape[2]])
+    ecfg = P.EnergyConfig("ps", "poisson", 0.0, 4)
+    runs = []
+    for k5 in ("tile", "scalar"):
+        monkeypatch.setenv("RCB_K5", k5)
+        eng = P.RegionCompetition(img, lab, ecfg, P.SobolevParams(6.0),
+                                  P.OptimizerConfig("l2", vanish_grace=5, drift_tolerance=1e-3))
+        out = []
+        for _ in range(3):
+            eng.iterate()
+            out.append(eng.last_candidates[3].copy())
+        runs.append(out)
+    for it, (a, b) in enumerate(zip(*runs)):
+        assert a.shape == b.shape and np.array_equal(a, b), it
