@@ -668,6 +668,15 @@ static int32_t engine_score(rcb_engine *e) {
       RCB_TRY(e->sb0.reserve(n, s));
     }
     const int64_t m = h1 - h0;
+    // K6's packed partner records come straight from the energy kernel (no
+    // packing pass) when K6 reads them: Sobolev mode, labels < 2^16
+    const bool ps_tiles_now = e->ecfg.region_model == 1 && e->int_image && e->ps_tiles &&
+                              e->rho0.p && ps3d_tile_ok(lat, e->ecfg.smooth_radius, e->nball);
+    const bool pk_direct = e->mode == 1 && !fp32 && e->sob_packed && (e->sob_site || e->nst > 1) &&
+                           (e->ecfg.region_model == 0 ||
+                            (!ps_tiles_now && delta_ps_writes_pk(lat, e->nball)));
+    if (pk_direct) RCB_TRY(e->pk.reserve(n, s));
+    int4 *pkh = pk_direct ? e->pk.p + h0 : nullptr;
     if (fp32 && e->ecfg.region_model == 0)
       RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m,
                                e->cnt.p, e->tot.p, poisson, e->raw32.p + h0, e->raw.p + h0, s));
@@ -677,36 +686,40 @@ static int32_t engine_score(rcb_engine *e) {
                                e->raw32.p + h0, e->raw.p + h0, s, e->cb0.p + h0, e->sb0.p + h0));
     else if (e->ecfg.region_model == 0)
       RCB_TRY(delta_pc_batch(e->I.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, e->cnt.p,
-                             e->tot.p, e->tsq.p, poisson, e->raw.p + h0, s));
+                             e->tot.p, e->tsq.p, poisson, e->raw.p + h0, s, pkh));
+    else if (ps_tiles_now)
+      // integer images: the ball gathers from shared-memory tiles (RCB_K5=tile)
+      RCB_TRY(delta_ps3d_tiles(e->L.p, e->I.p, e->Cown.p, e->Sown.p, e->rho0.p, lat,
+                               e->ecfg.smooth_radius, e->ball.p, e->nball, e->site_off.p, e->px.p,
+                               e->pown.p, e->pcomp.p, h0, h1, poisson, e->raw.p, e->cb0.p,
+                               e->sb0.p, e->logt_P ? e->logt.p : nullptr, e->logt_P, s));
     else
-      if (e->int_image && e->ps_tiles && e->rho0.p && ps3d_tile_ok(lat, e->ecfg.smooth_radius, e->nball))
-        // integer images: the ball gathers from shared-memory tiles
-        RCB_TRY(delta_ps3d_tiles(e->L.p, e->I.p, e->Cown.p, e->Sown.p, e->rho0.p, lat,
-                                 e->ecfg.smooth_radius, e->ball.p, e->nball, e->site_off.p,
-                                 e->px.p, e->pown.p, e->pcomp.p, h0, h1, poisson, e->raw.p,
-                                 e->cb0.p, e->sb0.p, e->logt_P ? e->logt.p : nullptr, e->logt_P,
-                                 s));
-      else
-        RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
-                               e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
-                               e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0,
-                               e->logt_P ? e->logt.p : nullptr, e->logt_P));
+      RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
+                             e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
+                             e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0,
+                             e->logt_P ? e->logt.p : nullptr, e->logt_P, pkh));
     cudaEventRecord(e->ev[2], s);
     if (e->mode == 1) {
       if (fp32) {
         RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
                                   e->st.p, e->nst, e->wt32.p, p1, e->smooth.p, &d->pairs, s, p0));
+      } else if (e->sob_site && pk_direct) {
+        if (p0 == 0 && p1 == n && h0 == 0 && h1 == n)  // the whole list: TMA-staged pass
+          RCB_TRY(sobolev_site_bulk(e->pk.p, e->w0, n, e->smooth.p, &d->pairs, s));
+        else
+          RCB_TRY(sobolev_site_pk(e->pk.p, e->w0, p0, p1, h0, h1, e->smooth.p, &d->pairs, s));
       } else if (e->sob_site) {
         RCB_TRY(sobolev_site(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, e->w0, p0, p1, h0, h1,
                              e->smooth.p, &d->pairs, s));
       } else if (e->sob_packed && e->nst > 1) {
-        // packed records of the partners K6 reads ([h0, h1) covers the halo);
-        // with one stencil row (w = 1) the unpacked kernel reads less
-        RCB_TRY(e->pk.reserve(n, s));
-        RCB_TRY(sobolev_pack(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, h0, h1, e->pk.p, s));
+        // packed records of the partners K6 reads ([h0, h1) covers the halo)
+        if (!pk_direct) {
+          RCB_TRY(e->pk.reserve(n, s));
+          RCB_TRY(sobolev_pack(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, h0, h1, e->pk.p, s));
+          launches += 1;
+        }
         RCB_TRY(sobolev_packed(e->site_off.p, e->pk.p, lat, e->st.p, e->nst, e->wt.p, e->nwt, p0,
                                p1, e->smooth.p, &d->pairs, s));
-        launches += 1;
       } else {
         RCB_TRY(sobolev_lattice(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw.p, lat,
                                 e->st.p, e->nst, e->wt.p, p1, e->smooth.p, &d->pairs, s, p0));
@@ -829,6 +842,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       P.lam = e->ecfg.lam;
       P.I = e->I.p;
       P.region_ps = e->ecfg.region_model == 1;
+
       if (P.region_ps) {
         P.Cown = e->Cown.p;
         P.Sown = e->Sown.p;

@@ -24,15 +24,27 @@ __global__ void k_delta_int(const int32_t *__restrict__ L, Lat lat, const uint32
   out[i] = delta_internal(L, lat, z, y, x, pown[i], pcomp[i]);
 }
 
+// K6's 16-byte partner record {raw, site, owner | competitor << 16}
+// (sobolev.cu:k_sobolev_pk), written by the energy kernels so that K6 needs
+// no separate packing pass (labels < 2^16).
+__device__ __forceinline__ int4 pack_record(double raw, uint32_t site, int32_t own, int32_t comp) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(raw);
+  return make_int4((int)(uint32_t)u, (int)(uint32_t)(u >> 32), (int)site,
+                   (int)((uint32_t)own | ((uint32_t)comp << 16)));
+}
+
 __global__ void k_delta_pc(const double *__restrict__ I, const uint32_t *__restrict__ px,
                            const int32_t *__restrict__ pown, const int32_t *__restrict__ pcomp,
                            int64_t n, const int64_t *__restrict__ cnt,
                            const double *__restrict__ tot, const double *__restrict__ tsq,
-                           int poisson, double *__restrict__ out) {
+                           int poisson, double *__restrict__ out, int4 *__restrict__ pk) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int32_t a = pown[i], b = pcomp[i];
-  out[i] = delta_pc(__ldg(&I[px[i]]), cnt[a], tot[a], tsq[a], cnt[b], tot[b], tsq[b], poisson);
+  const uint32_t f = px[i];
+  const double d = delta_pc(__ldg(&I[f]), cnt[a], tot[a], tsq[a], cnt[b], tot[b], tsq[b], poisson);
+  out[i] = d;
+  if (pk) pk[i] = pack_record(d, f, a, b);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
     const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
     const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
     const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0,
-    const double *__restrict__ lt, int ltP) {
+    const double *__restrict__ lt, int ltP, int4 *__restrict__ pk) {
   __shared__ int8_t sdy[kPsMaxBall], sdx[kPsMaxBall];
   for (int k = threadIdx.x; k < nball; k += blockDim.x) {
     sdy[k] = ball[k].dy;
@@ -511,6 +523,7 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps2d(
   d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
   d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
   out[i] = d;
+  if (pk) pk[i] = pack_record(d, (uint32_t)f, a, b);
   if (cb0) {  // the competitor's iteration-start ball count/sum at x (PS ledger terms)
     cb0[i] = cb;
     sb0[i] = sb;
@@ -527,7 +540,7 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
     int nball, const uint32_t *__restrict__ px, const int32_t *__restrict__ pown,
     const int32_t *__restrict__ pcomp, int64_t n, int poisson, double *__restrict__ out,
     const double *__restrict__ rho0, int32_t *__restrict__ cb0, double *__restrict__ sb0,
-    const double *__restrict__ lt, int ltP) {
+    const double *__restrict__ lt, int ltP, int4 *__restrict__ pk) {
   __shared__ int sofs[kPsMaxBall];  // dz:8 | dy:8 | dx:8, signed, packed
   __shared__ int sdel[kPsMaxBall];  // linear site delta of each offset
   __shared__ int srad;              // largest |component| of the offsets
@@ -613,6 +626,7 @@ __global__ void __launch_bounds__(128, 6) k_delta_ps3d(
   d += rho(v, (sb + v) / ((double)cb + 1.0), poisson);
   d -= rho0 ? rho0[f] : rho(v, Sown[f] / (double)Cown[f], poisson);
   out[i] = d;
+  if (pk) pk[i] = pack_record(d, (uint32_t)f, a, b);
   if (cb0) {
     cb0[i] = cb;
     sb0[i] = sb;
@@ -701,9 +715,10 @@ int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, co
 
 int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
                        const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
-                       const double *tsq, int poisson, double *out, cudaStream_t s) {
+                       const double *tsq, int poisson, double *out, cudaStream_t s, int4 *pk) {
   if (n == 0) return RCB_OK;
-  k_delta_pc<<<grid_for(n, 256), 256, 0, s>>>(I, px, pown, pcomp, n, cnt, tot, tsq, poisson, out);
+  k_delta_pc<<<grid_for(n, 256), 256, 0, s>>>(I, px, pown, pcomp, n, cnt, tot, tsq, poisson, out,
+                                              pk);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -907,20 +922,25 @@ int32_t delta_ps3d_tiles(const int32_t *L, const double *I, const int32_t *Cown,
   return RCB_OK;
 }
 
+// whether delta_ps_batch's kernel for this lattice writes K6's packed records
+bool delta_ps_writes_pk(const Lat &lat, int nball) {
+  return nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31);
+}
+
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
                        const Lat &lat, const Off *ball, int nball, const uint32_t *px,
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
                        double *out, cudaStream_t s, const double *rho0, int32_t *cb0,
-                       double *sb0, const double *lt, int ltP) {
+                       double *sb0, const double *lt, int ltP, int4 *pk) {
   if (n == 0) return RCB_OK;
   if (lat.ndim == 2 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
     k_delta_ps2d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny, ball,
                                                   nball, px, pown, pcomp, n, poisson, out, rho0,
-                                                  cb0, sb0, lt, ltP);
+                                                  cb0, sb0, lt, ltP, pk);
   else if (lat.ndim == 3 && nball <= kPsMaxBall && lat.V < ((int64_t)1 << 31))
     k_delta_ps3d<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, (int)lat.nx, (int)lat.ny,
                                                   (int)lat.nz, ball, nball, px, pown, pcomp, n,
-                                                  poisson, out, rho0, cb0, sb0, lt, ltP);
+                                                  poisson, out, rho0, cb0, sb0, lt, ltP, pk);
   else
     k_delta_ps<<<grid_for(n, 128), 128, 0, s>>>(L, I, Cown, Sown, lat, ball, nball, px, pown,
                                                 pcomp, n, poisson, out, rho0, cb0, sb0);

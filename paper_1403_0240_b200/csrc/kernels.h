@@ -198,6 +198,11 @@ struct InputCheck {
 };
 int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *out, cudaStream_t s);
 int32_t log_table(double *lt, int P, int Q, cudaStream_t s);
+bool delta_ps_writes_pk(const Lat &lat, int nball);
+int32_t sobolev_site_pk(const int4 *pk, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
+                        double *out, unsigned long long *pairs, cudaStream_t s);
+int32_t sobolev_site_bulk(const int4 *pk, double w0, int64_t n, double *out,
+                          unsigned long long *pairs, cudaStream_t s);
 bool ps3d_tile_ok(const Lat &lat, int R, int nball);
 int32_t delta_ps3d_tiles(const int32_t *L, const double *I, const int32_t *Cown,
                          const double *Sown, const double *rho0, const Lat &lat, int R,
@@ -216,7 +221,8 @@ int32_t delta_int_batch(const int32_t *L, const Lat &lat, const uint32_t *px, co
                         const int32_t *pcomp, int64_t n, int32_t *out, cudaStream_t s);
 int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
                        const int32_t *pcomp, int64_t n, const int64_t *cnt, const double *tot,
-                       const double *tsq, int poisson, double *out, cudaStream_t s);
+                       const double *tsq, int poisson, double *out, cudaStream_t s,
+                       int4 *pk = nullptr);
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s,
                   double *rho0 = nullptr, int poisson = 0);
@@ -238,7 +244,7 @@ int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, c
                        const int32_t *pown, const int32_t *pcomp, int64_t n, int poisson,
                        double *out, cudaStream_t s, const double *rho0 = nullptr,
                        int32_t *cb0 = nullptr, double *sb0 = nullptr, const double *lt = nullptr,
-                       int ltP = 0);
+                       int ltP = 0, int4 *pk = nullptr);
 int32_t stats_rebuild(const int32_t *L, const double *I, int64_t V, int32_t nl, int64_t *cnt,
                       double *tot, double *tsq, StatsScratch &sc, cudaStream_t s);
 int32_t pc_terms_exact(const int64_t *cnt, const double *tot, const double *tsq, int32_t nl,

@@ -295,11 +295,10 @@ __global__ void __launch_bounds__(256) k_sobolev_site(
   for (int j = 0; j < kSiteChunks; ++j) {
     const int64_t p = wbase + 32 * j + lane;
     const bool in = p < p1;
-    // streaming loads: every byte is read once (neighbour probes hit L1/L2)
-    fv[j] = in ? __ldcs(&px[p]) : 0xffffffffu - (uint32_t)lane;  // distinct sentinels
-    ov[j] = in ? __ldcs(&pown[p]) : -1;
-    cv[j] = in ? __ldcs(&pcomp[p]) : -2;
-    rv[j] = in ? __ldcs(&raw[p]) : 0.0;
+    fv[j] = in ? __ldg(&px[p]) : 0xffffffffu - (uint32_t)lane;  // distinct sentinels
+    ov[j] = in ? __ldg(&pown[p]) : -1;
+    cv[j] = in ? __ldg(&pcomp[p]) : -2;
+    rv[j] = in ? __ldg(&raw[p]) : 0.0;
   }
   unsigned long long np = 0;
 #pragma unroll
@@ -330,15 +329,17 @@ __global__ void __launch_bounds__(256) k_sobolev_site(
     // ripple: at step k the lane k places after its run head adds its term to
     // its left neighbour's (already final) partial sum -- sequential order
     double acc = 0.0 + c;
-#pragma unroll
-    for (int k = 1; k < kRipple; ++k) {
+    // as many ripple steps as the chunk's longest simple run needs (none when
+    // every site holds one particle)
+    const int steps = (int)__reduce_max_sync(0xffffffffu, simple ? (unsigned)len : 1u);
+    for (int k = 1; k < steps; ++k) {
       const double up = __shfl_up_sync(0xffffffffu, acc, 1);
       if (lane - hl == k) acc = up + c;
     }
     const double total = __shfl_sync(0xffffffffu, acc, tl);
     if (in) {
       if (simple) {
-        __stcs(&out[p], total / (double)len - 0.0);
+        out[p] = total / (double)len - 0.0;
         np += (unsigned long long)len;
       } else {
         int64_t L = 0;
@@ -348,6 +349,256 @@ __global__ void __launch_bounds__(256) k_sobolev_site(
     }
   }
   if (pairs) block_add_pairs(np, pairs);
+}
+
+// The w = 1 site kernel over K6's packed records (written by the energy
+// kernels, or once by the sweep's generator): one 16-byte record per
+// particle in, one 8-byte result out.
+__device__ __forceinline__ double pk_raw(const int4 v) {
+  return __longlong_as_double(((long long)(uint32_t)v.y << 32) | (long long)(uint32_t)v.x);
+}
+
+__device__ __forceinline__ double site_run_value_pk(const int4 *__restrict__ pk, double w0,
+                                                    int64_t p, int64_t lo, int64_t hi,
+                                                    int64_t &len) {
+  const int4 me = __ldg(&pk[p]);
+  const uint32_t f = (uint32_t)me.z;
+  const uint32_t own = (uint32_t)me.w & 0xffffu;
+  int64_t s = p, e = p + 1;
+  while (s > lo && (uint32_t)__ldg(&pk[s - 1]).z == f) --s;
+  while (e < hi && (uint32_t)__ldg(&pk[e]).z == f) ++e;
+  double same = 0.0, opp = 0.0;
+  int cs = 0, co = 0;
+  for (int64_t q = s; q < e; ++q) {
+    const int4 r = __ldg(&pk[q]);
+    const double c = w0 * pk_raw(r);
+    if (((uint32_t)r.w & 0xffffu) == own) {
+      same += c;
+      ++cs;
+    }
+    if (((uint32_t)r.w >> 16) == own) {
+      opp += c;
+      ++co;
+    }
+  }
+  len = e - s;
+  const double a = cs > 0 ? same / (double)cs : 0.0;
+  const double b = co > 0 ? opp / (double)co : 0.0;
+  return a - b;
+}
+
+__global__ void __launch_bounds__(256) k_sobolev_site_pk(const int4 *__restrict__ pk, double w0,
+                                                         int64_t p0, int64_t p1, int64_t lo,
+                                                         int64_t hi, double *__restrict__ out,
+                                                         unsigned long long *__restrict__ pairs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wbase = p0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 * kSiteChunks);
+  int4 rv[kSiteChunks];
+#pragma unroll
+  for (int j = 0; j < kSiteChunks; ++j) {
+    const int64_t p = wbase + 32 * j + lane;
+    rv[j] = p < p1 ? __ldg(&pk[p]) : make_int4(0, 0, (int)(0xffffffffu - (uint32_t)lane), -1);
+  }
+  unsigned long long np = 0;
+#pragma unroll
+  for (int j = 0; j < kSiteChunks; ++j) {
+    const int64_t p = wbase + 32 * j + lane;
+    const bool in = p < p1;
+    const uint32_t f = (uint32_t)rv[j].z;
+    const int32_t own = in ? (int32_t)((uint32_t)rv[j].w & 0xffffu) : -1;
+    const int32_t cmp = in ? (int32_t)((uint32_t)rv[j].w >> 16) : -2;
+    const double c = in ? w0 * pk_raw(rv[j]) : 0.0;
+    const uint32_t fu = __shfl_up_sync(0xffffffffu, f, 1), fd = __shfl_down_sync(0xffffffffu, f, 1);
+    const int32_t ou = __shfl_up_sync(0xffffffffu, own, 1);
+    const bool head = lane == 0 || fu != f;
+    const bool tail = lane == 31 || fd != f;
+    const bool edge = (lane == 0 && in && p > lo && (uint32_t)__ldg(&pk[p - 1]).z == f) ||
+                      (lane == 31 && in && p + 1 < hi && (uint32_t)__ldg(&pk[p + 1]).z == f);
+    const bool bad = edge || (!head && ou != own) || (cmp == own);
+    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    const int hl = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+    const unsigned tm = __ballot_sync(0xffffffffu, tail);
+    const int tl = __ffs(tm & (0xffffffffu << lane)) - 1;
+    const unsigned bm = __ballot_sync(0xffffffffu, bad);
+    const unsigned runmask =
+        (tl == 31 ? 0xffffffffu : ((1u << (tl + 1)) - 1u)) & (0xffffffffu << hl);
+    const int len = tl - hl + 1;
+    const bool simple = in && !(bm & runmask) && len <= kRipple;
+    double acc = 0.0 + c;
+    // as many ripple steps as the chunk's longest simple run needs (none when
+    // every site holds one particle)
+    const int steps = (int)__reduce_max_sync(0xffffffffu, simple ? (unsigned)len : 1u);
+    for (int k = 1; k < steps; ++k) {
+      const double up = __shfl_up_sync(0xffffffffu, acc, 1);
+      if (lane - hl == k) acc = up + c;
+    }
+    const double total = __shfl_sync(0xffffffffu, acc, tl);
+    if (in) {
+      if (simple) {
+        out[p] = total / (double)len - 0.0;
+        np += (unsigned long long)len;
+      } else {
+        int64_t L = 0;
+        out[p] = site_run_value_pk(pk, w0, p, lo, hi, L);
+        np += (unsigned long long)L;
+      }
+    }
+  }
+  if (pairs) block_add_pairs(np, pairs);
+}
+
+// The same pass with the records staged by the Tensor Memory Accelerator: a
+// persistent grid (2 blocks per SM) streams 1024-record tiles (16 KB) through
+// a 4-stage shared-memory ring with 1-D bulk copies (cp.async.bulk, mbarrier
+// completion), so each SM keeps ~64 KB of loads in flight without holding
+// them in registers; warps then run the site-run logic on shared memory.
+static constexpr int kBulkTile = 1024, kBulkStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_sobolev_site_bulk(const int4 *__restrict__ pk, double w0,
+                                                           int64_t n, double *__restrict__ out,
+                                                           unsigned long long *__restrict__ pairs) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  int4 *buf = reinterpret_cast<int4 *>(smem_raw);
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ntiles = (n + kBulkTile - 1) / kBulkTile;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kBulkStages; ++st) mbar_init(&bar[st]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t b = tile * kBulkTile;
+    const int64_t cnt = n - b < kBulkTile ? n - b : kBulkTile;
+    bulk_load(buf + st * kBulkTile, pk + b, (uint32_t)(cnt * sizeof(int4)), &bar[st]);
+  };
+  // prologue: the first tiles of this block
+  if (threadIdx.x == 0)
+    for (int st = 0; st < kBulkStages; ++st) {
+      const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+      if (t < ntiles) issue(t, st);
+    }
+  unsigned long long np = 0;
+  int64_t k = 0;  // local tile counter
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int st = (int)(k % kBulkStages);
+    const uint32_t phase = (uint32_t)((k / kBulkStages) & 1);
+    mbar_wait(&bar[st], phase);
+    const int4 *tb = buf + st * kBulkTile;
+    const int64_t base = t * kBulkTile;
+    const int64_t cnt = n - base < kBulkTile ? n - base : kBulkTile;
+#pragma unroll
+    for (int j = 0; j < kBulkTile / 256; ++j) {
+      const int li = warp * (kBulkTile / 8) + j * 32 + lane;  // record in the tile
+      const int64_t p = base + li;
+      const bool in = li < cnt;
+      const int4 r = in ? tb[li] : make_int4(0, 0, (int)(0xffffffffu - (uint32_t)lane), -1);
+      const uint32_t f = (uint32_t)r.z;
+      const int32_t own = in ? (int32_t)((uint32_t)r.w & 0xffffu) : -1;
+      const int32_t cmp = in ? (int32_t)((uint32_t)r.w >> 16) : -2;
+      const double c = in ? w0 * pk_raw(r) : 0.0;
+      const uint32_t fu = __shfl_up_sync(0xffffffffu, f, 1), fd = __shfl_down_sync(0xffffffffu, f, 1);
+      const int32_t ou = __shfl_up_sync(0xffffffffu, own, 1);
+      const bool head = lane == 0 || fu != f;
+      const bool tail = lane == 31 || fd != f;
+      bool edge = false;
+      if (in && lane == 0 && p > 0)
+        edge = (uint32_t)(li > 0 ? tb[li - 1].z : __ldg(&pk[p - 1]).z) == f;
+      if (in && lane == 31 && p + 1 < n)
+        edge = edge || (uint32_t)(li + 1 < cnt ? tb[li + 1].z : __ldg(&pk[p + 1]).z) == f;
+      const bool bad = edge || (!head && ou != own) || (cmp == own);
+      const unsigned hm = __ballot_sync(0xffffffffu, head);
+      const int hl = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+      const unsigned tm = __ballot_sync(0xffffffffu, tail);
+      const int tl = __ffs(tm & (0xffffffffu << lane)) - 1;
+      const unsigned bm = __ballot_sync(0xffffffffu, bad);
+      const unsigned runmask =
+          (tl == 31 ? 0xffffffffu : ((1u << (tl + 1)) - 1u)) & (0xffffffffu << hl);
+      const int len = tl - hl + 1;
+      const bool simple = in && !(bm & runmask) && len <= kRipple;
+      double acc = 0.0 + c;
+      const int steps = (int)__reduce_max_sync(0xffffffffu, simple ? (unsigned)len : 1u);
+      for (int q = 1; q < steps; ++q) {
+        const double up = __shfl_up_sync(0xffffffffu, acc, 1);
+        if (lane - hl == q) acc = up + c;
+      }
+      const double total = __shfl_sync(0xffffffffu, acc, tl);
+      if (in) {
+        if (simple) {
+          out[p] = total / (double)len - 0.0;
+          np += (unsigned long long)len;
+        } else {
+          int64_t L = 0;
+          out[p] = site_run_value_pk(pk, w0, p, 0, n, L);
+          np += (unsigned long long)L;
+        }
+      }
+    }
+    __syncthreads();  // the stage is consumed: refill it with this block's next-but-3 tile
+    if (threadIdx.x == 0) {
+      const int64_t nt = t + (int64_t)kBulkStages * gridDim.x;
+      if (nt < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nt, st);
+      }
+    }
+  }
+  if (pairs) block_add_pairs(np, pairs);
+}
+
+int32_t sobolev_site_bulk(const int4 *pk, double w0, int64_t n, double *out,
+                          unsigned long long *pairs, cudaStream_t s) {
+  if (n <= 0) return RCB_OK;
+  const size_t smem = (size_t)kBulkStages * kBulkTile * sizeof(int4);
+  static bool attr[64] = {};
+  int dev = 0;
+  RCB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    RCB_CUDA(cudaFuncSetAttribute(k_sobolev_site_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr[dev] = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (n + kBulkTile - 1) / kBulkTile;
+  const int64_t grid = ntiles < 2 * sms ? ntiles : 2 * sms;
+  k_sobolev_site_bulk<<<(unsigned)grid, 256, smem, s>>>(pk, w0, n, out, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t sobolev_site_pk(const int4 *pk, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
+                        double *out, unsigned long long *pairs, cudaStream_t s) {
+  if (p1 <= p0) return RCB_OK;
+  k_sobolev_site_pk<<<grid_for(p1 - p0, 256 * kSiteChunks), 256, 0, s>>>(pk, w0, p0, p1, lo, hi,
+                                                                         out, pairs);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
 }
 
 bool sobolev_site_only(const Off *rows_host, int nrows) {

@@ -158,7 +158,11 @@ int32_t rcb_sweep_create(int32_t ndim, const int64_t *dims, const float *spheres
     w->site = sobolev_site_only(stv.data(), w->nst) && !(ks && strcmp(ks, "scalar") == 0);
     w->w0 = scfg->weights[0];
   }
-  if (w->packed) TRYB(w->pk.reserve(n, s));
+  if (w->packed || w->site) {
+    // K6's input records, as the engine's energy kernels write them
+    TRYB(w->pk.reserve(n, s));
+    if (w->n > 0) TRYB(sobolev_pack(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, 0, w->n, w->pk.p, s));
+  }
   TRYB(w->st.reserve(stv.size(), s));
   TRYB(w->wt.reserve(scfg->n_weights, s));
   cudaMemcpyAsync(w->st.p, stv.data(), sizeof(Off) * stv.size(), cudaMemcpyHostToDevice, s);
@@ -185,11 +189,13 @@ int32_t rcb_sweep_run(rcb_sweep *w, int64_t *pairs, float *ms) {
   cudaStream_t s = w->s;
   RCB_CUDA(cudaMemsetAsync(w->pairs.p, 0, sizeof(unsigned long long), s));
   RCB_CUDA(cudaEventRecord(w->e0, s));
-  if (w->site) {  // w = 1: one streaming pass over the particle list
-    RCB_TRY(sobolev_site(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, w->w0, 0, w->n, 0, w->n,
-                         w->out.p, w->pairs.p, s));
-  } else if (w->packed) {  // the record packing is part of K6's cost: timed with it
-    RCB_TRY(sobolev_pack(w->px.p, w->pown.p, w->pcomp.p, w->raw.p, 0, w->n, w->pk.p, s));
+  if (w->site) {  // w = 1: one streaming pass over the packed records
+    const char *sb = getenv("RCB_K6_SITE");  // "lsu": register-staged loads instead of TMA
+    if (sb && strcmp(sb, "lsu") == 0)
+      RCB_TRY(sobolev_site_pk(w->pk.p, w->w0, 0, w->n, 0, w->n, w->out.p, w->pairs.p, s));
+    else
+      RCB_TRY(sobolev_site_bulk(w->pk.p, w->w0, w->n, w->out.p, w->pairs.p, s));
+  } else if (w->packed) {  // the records come from the energy kernel (built at create)
     RCB_TRY(sobolev_packed(w->site_off.p, w->pk.p, w->lat, w->st.p, w->nst, w->wt.p, w->nwt, 0,
                            w->n, w->out.p, w->pairs.p, s));
   } else {
