@@ -136,6 +136,9 @@ struct rcb_engine {
   DBuf<double> Sown, rho0;
   DBuf<double> logt;  // K5 Poisson log table (integer images), logt_P columns
   int logt_P = 0;
+  DBuf<int4> srec;        // K5 packed site records (ps_rec_ok)
+  DBuf<double2> thetat;   // K5 {theta, log theta} table, thetat_P columns
+  int thetat_P = 0;
   DBuf<Off> ball, ball_full, st;
   int nball = 0, nball_full = 0, nst = 0;
   DBuf<double> wt;
@@ -212,7 +215,7 @@ struct rcb_engine {
       cudaSetDevice(device);
       L.release(s); I.release(s); I32.release(s); raw32.release(s); wt32.release(s);
       cb0.release(s); sb0.release(s); cnt.release(s); tot.release(s); tsq.release(s);
-      Cown.release(s); Sown.release(s); logt.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
+      Cown.release(s); Sown.release(s); logt.release(s); srec.release(s); thetat.release(s); rho0.release(s); ball.release(s); ball_full.release(s); st.release(s);
       wt.release(s); ncomp.release(s); vis.release(s); queue.release(s); site_off.release(s);
       px.release(s); order.release(s); pown.release(s); pcomp.release(s); dint.release(s);
       raw.release(s); smooth.release(s); rank.release(s); pk.release(s); tot_run.release(s);
@@ -499,6 +502,12 @@ int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32
         TRYB(log_table(e->logt.p, (int)P, (int)Q, s));
         e->logt_P = (int)P;
       }
+      if (P * Q * 16 <= ((int64_t)128 << 20) &&
+          ps_rec_ok(e->lat, nbf, chk.label_max + 1, chk.image_max) && !getenv("RCB_NO_K5REC")) {
+        TRYB(e->thetat.reserve(P * Q, s));
+        TRYB(theta_table(e->thetat.p, (int)P, (int)Q, s));
+        e->thetat_P = (int)P;
+      }
     }
   }
   TRYB(e->cnt.reserve(e->nl, s));
@@ -693,7 +702,15 @@ static int32_t engine_score(rcb_engine *e) {
                                e->ecfg.smooth_radius, e->ball.p, e->nball, e->site_off.p, e->px.p,
                                e->pown.p, e->pcomp.p, h0, h1, poisson, e->raw.p, e->cb0.p,
                                e->sb0.p, e->logt_P ? e->logt.p : nullptr, e->logt_P, s));
-    else
+    else if (e->thetat_P && e->rho0.p && e->ecfg.noise_model == 1) {
+      // integer Poisson data: one 16-byte record per ball site (k_delta_ps_rec)
+      RCB_TRY(e->srec.reserve(lat.V, s));
+      RCB_TRY(pack_sites(e->L.p, e->Cown.p, e->Sown.p, e->I.p, e->rho0.p, lat.V, e->srec.p, s));
+      RCB_TRY(delta_ps_rec(e->srec.p, e->I.p, lat, e->ball.p, e->nball, e->px.p + h0,
+                           e->pown.p + h0, e->pcomp.p + h0, m, e->raw.p + h0, e->rho0.p,
+                           e->cb0.p + h0, e->sb0.p + h0, e->thetat.p, e->thetat_P, pkh, s));
+      launches += 1;
+    } else
       RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
                              e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
                              e->raw.p + h0, s, e->rho0.p, e->cb0.p + h0, e->sb0.p + h0,

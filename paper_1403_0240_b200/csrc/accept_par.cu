@@ -133,20 +133,42 @@ __device__ __forceinline__ bool is_face(int k) {
   return abs(dz) + abs(dy) + abs(dx) == 1;
 }
 
+// Box-local component count of the cell mask (a-cells of the punctured box,
+// x excluded), full-box adjacency: 0 none, 1 one piece, 2 inconclusive.
+__device__ __forceinline__ int box_count_bits(uint32_t cells) {
+  if (!cells) return 0;
+  uint32_t reach = cells & (~cells + 1);
+  for (;;) {
+    const uint32_t grow = box_dilate(reach, 1) & cells;
+    if (grow == reach) break;
+    reach = grow;
+  }
+  return (cells & ~reach) ? 2 : 1;
+}
+
+// Seed groups of a cell mask: one group per box-local component (<= 8).
+__device__ __forceinline__ void box_groups_bits(uint32_t cells, uint8_t *grp, int &ngrp) {
+  ngrp = 0;
+  for (uint32_t rest = cells; rest;) {
+    uint32_t reach = rest & (~rest + 1);
+    for (;;) {
+      const uint32_t grow = box_dilate(reach, 1) & cells;
+      if (grow == reach) break;
+      reach = grow;
+    }
+    for (uint32_t r = reach; r; r &= r - 1) grp[__ffs(r) - 1] = (uint8_t)ngrp;
+    ++ngrp;
+    rest &= ~reach;
+  }
+}
+
 // Local component count from box labels (contour.py:128-162), fg = full box.
 __device__ __forceinline__ int box_local_count(const int32_t *lab, int32_t a) {
   uint32_t cells = 0;
   for (int k = 0; k < 27; ++k)
     if (k != 13 && lab[k] == a) cells |= 1u << k;
   if (!cells) return 0;
-  uint32_t reach = cells & (~cells + 1);
-  for (;;) {
-    uint32_t grow = reach;
-    for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, 1) & cells;
-    if (grow == reach) break;
-    reach = grow;
-  }
-  return (cells & ~reach) ? 2 : 1;
+  return box_count_bits(cells);
 }
 
 // Seed groups for the BFS tiers: the a-cells of x's box (x excluded), one
@@ -157,19 +179,7 @@ __device__ __forceinline__ uint32_t box_groups(const int32_t *lab, int32_t a, ui
   uint32_t cells = 0;
   for (int k = 0; k < 27; ++k)
     if (k != 13 && lab[k] == a) cells |= 1u << k;
-  ngrp = 0;
-  for (uint32_t rest = cells; rest;) {
-    uint32_t reach = rest & (~rest + 1);
-    for (;;) {
-      uint32_t grow = reach;
-      for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, 1) & cells;
-      if (grow == reach) break;
-      reach = grow;
-    }
-    for (uint32_t r = reach; r; r &= r - 1) grp[__ffs(r) - 1] = (uint8_t)ngrp;
-    ++ngrp;
-    rest &= ~reach;
-  }
+  box_groups_bits(cells, grp, ngrp);
   return cells;
 }
 
@@ -1537,14 +1547,7 @@ __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t 
         if ((rc.y & 0x7fffffff) != a || is_q(A, rc.x, a, S)) continue;
         const uint32_t cells = __ldcg(A.qscr + q);
         if (!cells) continue;
-        uint32_t reach = cells & (~cells + 1);
-        for (;;) {
-          uint32_t grow = reach;
-          for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, 1) & cells;
-          if (grow == reach) break;
-          reach = grow;
-        }
-        if (cells & ~reach) {
+        if (box_count_bits(cells) == 2) {
           const unsigned long long w = atomicAdd(A.job + 47, 1ull);
           if (w < 8) A.job[48 + w] = (unsigned long long)(uint32_t)p;
           else atomicExch(A.job + 46, 1ull);
@@ -2672,11 +2675,16 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   const int32_t M = (int32_t)*A.nneg;
   const int nx = (int)lat.nx, ny = (int)lat.ny, nz = (int)lat.nz;
   int32_t *ctl = A.ctl;
-  // positions come from an atomic counter one at a time: a position held
-  // ahead by a warp stuck in a long BFS would stall its dependants
+  // positions come from an atomic counter in rank order, one ahead: the warp
+  // claims its next position (and loads that position's record) while it
+  // decides the current one, so the claim and record round trips overlap the
+  // box loads instead of preceding them.  No deadlock: the earliest undecided
+  // position is always the current one of the warp holding it (a warp's
+  // claimed-ahead position is later than its current one).  Only one ahead:
+  // a position held behind a warp stuck in a long BFS stalls its dependants.
+  int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
+  int4 rc = pos < M ? __ldg(A.rec + pos) : make_int4(0, 0, 0, 0);
   for (;;) {
-    if (__shfl_sync(0xffffffffu, lane == 0 ? (int)df_aborted(A) : 0, 0)) break;  // watchdog
-    const int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
     if (pos >= M) {
       // stay as a helper for assist jobs until every position is decided,
       // polling slowly (a tight spin of thousands of finished warps would
@@ -2684,7 +2692,9 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       warp_idle_help(A);
       break;
     }
-    const int4 rc = __ldg(A.rec + pos);
+    // next claim and the watchdog flag: consumed after the box wait
+    const int32_t nclaim = lane == 0 ? atomicAdd(ctl + 12, 1) : 0;
+    const int stop = lane == 0 ? (int)df_aborted(A) : 0;
     df_stamp(A, pos, 0);
     const int32_t f = rc.x, next = rc.w;
     const int32_t a = rc.y & 0x7fffffff, b = rc.z & 0x7fffffff;
@@ -2707,29 +2717,33 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
     }
     const int32_t l0 = gb >= 0 ? __ldg(A.L + gb) : -1;
     const unsigned long long pk = warp_wait_settled(A, gb, pos);
+    // the next position's record is in flight while this one is decided
+    const int32_t npos = __shfl_sync(0xffffffffu, nclaim, 0);
+    const int4 nrc = npos < M ? __ldg(A.rec + npos) : make_int4(0, 0, 0, 0);
     const int32_t mine = gb >= 0 ? df_lab((uint32_t)A.wp_bits, pk, l0, pos) : -1;
     const unsigned long long pkc = __shfl_sync(0xffffffffu, pk, 13);  // x's own word
     const int32_t wold = wp_w((uint32_t)A.wp_bits, pkc), lold = wp_lab((uint32_t)A.wp_bits, pkc);
-    int32_t lab[27];
-#pragma unroll
-    for (int k = 0; k < 27; ++k) lab[k] = __shfl_sync(0xffffffffu, mine, k);
+    // the box as cell masks (bit k = lane k of the 3^3 layout): the box
+    // tests below are bit operations on these instead of loops over 27 labels
+    constexpr uint32_t kFace = (1u << 4) | (1u << 10) | (1u << 12) | (1u << 14) | (1u << 16) |
+                               (1u << 22);
+    const bool in_box = lane < 27;
+    const uint32_t eqa = __ballot_sync(0xffffffffu, in_box && mine == a) & ~(1u << 13);
+    const uint32_t eqb = __ballot_sync(0xffffffffu, in_box && mine == b);
+    const uint32_t valid = __ballot_sync(0xffffffffu, in_box && mine >= 0);
+    const uint32_t other = __ballot_sync(0xffffffffu, in_box && lane != 13 && mine > 0 &&
+                                                          mine != a && mine != b);
+    const int32_t lab13 = __shfl_sync(0xffffffffu, mine, 13);
     uint8_t d = ACC;
     int how = 0;  // 1: needs the window test
     int dbg = 0;  // decision path (tools/df_timeline.py decodes it)
-    if (lab[13] != a) {
-      d = REJ;
-    } else {
-      bool adj = false;
-      for (int k = 0; k < 27; ++k)
-        if (is_face(k) && lab[k] == b) adj = true;
-      if (!adj) d = REJ;
-    }
+    if (lab13 != a || !(eqb & kFace)) d = REJ;
     const uint8_t d_base = d;  // stale / adjacency verdict (l2: vanish override below)
     if (d == ACC && a > 0) {
       if (sa && !A.l2 && __ldcg((const long long *)A.cnt + a) == 1) {
         if (!A.vanish_ok) d = REJ;
       } else {
-        const int k = box_local_count(lab, a);
+        const int k = box_count_bits(eqa);
         if (k == 0)
           d = REJ;
         else if (k != 1)
@@ -2824,7 +2838,8 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         const bool use_box = (int64_t)bb.bd * bb.bh * bb.bw <= (int64_t)A.box_cap;
         uint8_t sgrp[27];
         int ngrp = 0;
-        const uint32_t seeds = box_groups(lab, a, sgrp, ngrp);
+        const uint32_t seeds = eqa;
+        box_groups_bits(eqa, sgrp, ngrp);
         int r;
         for (;;) {
           if (is3)
@@ -2890,7 +2905,9 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         dbg += 10 * (r + 1) + 10000 * (S.levels < 99 ? S.levels : 99);  // +1e6 w63, +1e7 w31, +1e8 box, +1e9 job
       }
     }
-    const bool fus_bad = b > 0 && !A.allow_fusion && box_fusion_bad(lab, a, b);
+    const bool fus_bad = b > 0 && !A.allow_fusion && other != 0;
+    // delta_internal (energy.py:111-126) from the settled box: face cells
+    const int di_box = __popc(kFace & valid & ~eqb) - __popc(kFace & valid & ~eqa);
     if (d == ACC && fus_bad) d = REJ;
     if (A.l2) {
       // l2 mode (optimizer.py:190-191, PC): admissible and d_tot < 0 with the
@@ -2900,9 +2917,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       if (a > 0 && __ldcg((const long long *)A.cnt + a) == 1)
         d = (d_base == ACC && A.vanish_ok && !fus_bad) ? ACC : REJ;
       if (d == ACC && A.region_ps) {
-        int di = 0;
-        for (int k = 0; k < 27; ++k)
-          if (is_face(k) && lab[k] >= 0) di += (int)(lab[k] != b) - (int)(lab[k] != a);
+        const int di = di_box;
         const double dt = df_ps_dtot(A, S, pos, f, a, b, di);
         if (!(dt < 0.0)) d = REJ;
       } else if (d == ACC) {
@@ -2911,9 +2926,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         const long long cb = __ldcg((const long long *)A.cnt + b);
         const double ta = __ldcg(A.tot_run + a), qa = __ldcg(A.tsq_run + a);
         const double tb = __ldcg(A.tot_run + b), qb = __ldcg(A.tsq_run + b);
-        int di = 0;
-        for (int k = 0; k < 27; ++k)
-          if (is_face(k) && lab[k] >= 0) di += (int)(lab[k] != b) - (int)(lab[k] != a);
+        const int di = di_box;
         const double dt = delta_pc(v, ca, ta, qa, cb, tb, qb, A.poisson) + A.lam * (double)di;
         if (!(dt < 0.0)) {
           d = REJ;
@@ -2942,6 +2955,9 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       if (sb) st_rel(A.lab_ptr + b, A.lab_ptr[b] + 1);
     }
     __syncwarp();
+    if (__shfl_sync(0xffffffffu, stop, 0)) break;  // watchdog
+    pos = npos;
+    rc = nrc;
   }
 }
 

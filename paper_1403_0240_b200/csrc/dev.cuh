@@ -55,19 +55,26 @@ __host__ __device__ __forceinline__ int box_bit(int dz, int dy, int dx) {
   return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
 }
 
-// Foreground adjacency among the 27 box cells: bit i of adj[j] set when
-// cells i and j are fg-adjacent (Chebyshev 1 for full_fg, Manhattan 1 else).
-__device__ __forceinline__ uint32_t box_adj(int j, int full_fg) {
-  int jz = j / 9 - 1, jy = (j / 3) % 3 - 1, jx = j % 3 - 1;
-  uint32_t m = 0;
-  for (int i = 0; i < 27; ++i) {
-    int iz = i / 9 - 1, iy = (i / 3) % 3 - 1, ix = i % 3 - 1;
-    int dz = abs(iz - jz), dy = abs(iy - jy), dx = abs(ix - jx);
-    int cheb = max(dz, max(dy, dx)), man = dz + dy + dx;
-    if (cheb == 0) continue;
-    if (full_fg ? cheb == 1 : man == 1) m |= 1u << i;
+// Foreground adjacency among the 27 box cells (bit box_bit(dz, dy, dx)):
+// the cells of m together with their fg-neighbours inside the box
+// (Chebyshev 1 for full_fg, Manhattan 1 else), by shifts and row masks.
+__host__ __device__ __forceinline__ uint32_t box_dilate(uint32_t m, int full_fg) {
+  constexpr uint32_t kFull = 0x7ffffffu;
+  constexpr uint32_t kXlo = 0x1249249u, kXhi = kXlo << 2;      // dx = -1 / +1 cells
+  constexpr uint32_t kYlo = 0x1c0e07u, kYhi = kYlo << 6;       // dy = -1 / +1 cells
+  const uint32_t xs = (((m << 1) & ~kXlo) | ((m >> 1) & ~kXhi)) & kFull;
+  if (full_fg) {
+    const uint32_t m1 = m | xs;
+    const uint32_t m2 = (m1 | ((m1 << 3) & ~kYlo) | ((m1 >> 3) & ~kYhi)) & kFull;
+    return (m2 | (m2 << 9) | (m2 >> 9)) & kFull;
   }
-  return m;
+  const uint32_t ys = (((m << 3) & ~kYlo) | ((m >> 3) & ~kYhi)) & kFull;
+  return (m | xs | ys | (m << 9) | (m >> 9)) & kFull;
+}
+
+// bit i of box_adj(j) set when cells i and j are fg-adjacent
+__device__ __forceinline__ uint32_t box_adj(int j, int full_fg) {
+  return box_dilate(1u << j, full_fg) & ~(1u << j);
 }
 
 // Local component count of label a in the punctured 3^d box around a site
@@ -94,8 +101,7 @@ __device__ __forceinline__ int local_component_count(const int32_t *__restrict__
   if (!seeds) return 2;
   uint32_t reach = seeds & (~seeds + 1);  // lowest seed
   for (;;) {
-    uint32_t grow = reach;
-    for (uint32_t r = reach; r; r &= r - 1) grow |= box_adj(__ffs(r) - 1, full_fg) & cells;
+    const uint32_t grow = box_dilate(reach, full_fg) & cells;
     if (grow == reach) break;
     reach = grow;
   }

@@ -1403,4 +1403,188 @@ int32_t log_table(double *lt, int P, int Q, cudaStream_t s) {
   return RCB_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// K5 over packed site records (integer Poisson images).  Every ball hit of
+// k_delta_ps2d/3d gathers five arrays (L, Cown, Sown, I, rho0: 32 B from five
+// cache lines); here one 16-byte record per site carries all of them:
+//   x = label (16 bits) | Cown << 16,  y = Sown (20 bits) | I << 20,
+//   z:w = rho0 (fp64 bits),
+// exact for labels, counts < 2^16, integer intensities < 2^12 and ball sums
+// < 2^20 (checked on the host, rec_ok).  theta = fl(p / q) and its log come
+// from one 16-byte table entry (no per-hit division or log), so every term
+// is the same fp64 value k_delta_ps3d forms, summed in the same ball-offset
+// order: bit-identical results.
+// ---------------------------------------------------------------------------
+__global__ void k_pack_sites(const int32_t *__restrict__ L, const int32_t *__restrict__ Cown,
+                             const double *__restrict__ Sown, const double *__restrict__ I,
+                             const double *__restrict__ rho0, int64_t V, int4 *__restrict__ rec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < V; f += stride) {
+    const unsigned long long r = (unsigned long long)__double_as_longlong(__ldg(rho0 + f));
+    const uint32_t w0 = (uint32_t)__ldg(L + f) | ((uint32_t)__ldg(Cown + f) << 16);
+    const uint32_t w1 = (uint32_t)__ldg(Sown + f) | ((uint32_t)__ldg(I + f) << 20);
+    __stcs(rec + f, make_int4((int)w0, (int)w1, (int)(uint32_t)r, (int)(uint32_t)(r >> 32)));
+  }
+}
+
+// tl[q * P + p] = {fl(p / q), log(max(fl(p / q), 1e-8))} for 1 <= q < Q
+__global__ void k_theta_table(double2 *__restrict__ tl, int P, int Q) {
+  const int64_t n = (int64_t)P * Q;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i / P), p = (int)(i - (int64_t)q * P);
+    if (q == 0) {
+      tl[i] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double theta = (double)p / (double)q;
+    const double t = theta < kPoissonFloor ? kPoissonFloor : theta;
+    tl[i] = make_double2(theta, log(t));
+  }
+}
+
+template <int ND>
+__global__ void __launch_bounds__(128, 6) k_delta_ps_rec(
+    const int4 *__restrict__ rec, const double *__restrict__ I, int nx, int ny, int nz,
+    const Off *__restrict__ ball, int nball, const uint32_t *__restrict__ px,
+    const int32_t *__restrict__ pown, const int32_t *__restrict__ pcomp, int64_t n,
+    double *__restrict__ out, const double *__restrict__ rho0, int32_t *__restrict__ cb0,
+    double *__restrict__ sb0, const double2 *__restrict__ tl, int tlP, int4 *__restrict__ pk) {
+  __shared__ int sofs[kPsMaxBall];  // dz:8 | dy:8 | dx:8, signed, packed
+  __shared__ int sdel[kPsMaxBall];  // linear site delta of each offset
+  __shared__ int srad;
+  if (threadIdx.x == 0) srad = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nball; k += blockDim.x) {
+    const int dz = ND == 3 ? ball[k].dz : 0, dy = ball[k].dy, dx = ball[k].dx;
+    sofs[k] = ((int)(uint8_t)dz << 16) | ((int)(uint8_t)dy << 8) | (int)(uint8_t)dx;
+    sdel[k] = (dz * ny + dy) * nx + dx;
+    atomicMax(&srad, max(abs(dz), max(abs(dy), abs(dx))));
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int f = (int)px[i];
+  const int plane = nx * ny;
+  const int z = ND == 3 ? f / plane : 0, r = f - z * plane;
+  const int y = r / nx, x = r - y * nx;
+  const int32_t a = pown[i], b = pcomp[i];
+  const double v = I[f];
+  const int iv = (int)v;
+  const int rad = srad;
+  const bool interior = (ND == 2 || (z >= rad && z < nz - rad)) && y >= rad && y < ny - rad &&
+                        x >= rad && x < nx - rad;
+  double acc_a = 0.0, acc_b = 0.0, sb = 0.0;
+  int32_t cb = 0;
+  constexpr int U = 4;
+  for (int k0 = 0; k0 < nball; k0 += U) {
+    int4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u;
+      bool ok;
+      int g;
+      if (interior) {
+        ok = k < nball;
+        g = f + (ok ? sdel[k] : 0);
+      } else {
+        const int o = k < nball ? sofs[k] : 0;
+        const int zz = z + (int)(int8_t)(o >> 16), yy = y + (int)(int8_t)(o >> 8),
+                  xx = x + (int)(int8_t)o;
+        ok = k < nball && (ND == 2 || (unsigned)zz < (unsigned)nz) && (unsigned)yy < (unsigned)ny &&
+             (unsigned)xx < (unsigned)nx;
+        g = ok ? (zz * ny + yy) * nx + xx : f;
+      }
+      q[u] = __ldg(rec + g);
+      if (!ok) q[u].x = -1;
+    }
+    double2 t2[U];
+    int lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      lab[u] = q[u].x < 0 ? -1 : (q[u].x & 0xffff);
+      const bool isa = lab[u] == a, hit = isa || lab[u] == b;
+      const int c = (int)((uint32_t)q[u].x >> 16), sv = q[u].y & 0xfffff;
+      // (S - v) / (C - 1) for the donor side, (S + v) / (C + 1) for the target
+      const int num = isa ? sv - iv : sv + iv, den = isa ? c - 1 : c + 1;
+      t2[u] = (hit && den >= 1) ? __ldg(tl + (int64_t)den * tlP + num) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool isa = lab[u] == a;
+      if (isa || lab[u] == b) {
+        const double iy = (double)((uint32_t)q[u].y >> 20);
+        const double r0 = __longlong_as_double(((long long)(uint32_t)q[u].w << 32) |
+                                               (long long)(uint32_t)q[u].z);
+        double rn;
+        const int c = (int)((uint32_t)q[u].x >> 16);
+        if ((isa ? c - 1 : c + 1) >= 1) {
+          rn = t2[u].x - iy * t2[u].y;
+        } else {  // den == 0: theta = +-inf / nan, as numpy forms it
+          const double sy = (double)(q[u].y & 0xfffff);
+          const double num = sy + (isa ? -v : v), den = (double)c + (isa ? -1.0 : 1.0);
+          rn = rho(iy, num / den, 1);
+        }
+        const double t = rn - r0;
+        if (isa) {
+          acc_a += t;
+        } else {
+          acc_b += t;
+          cb += 1;
+          sb += iy;
+        }
+      }
+    }
+  }
+  double d = 0.0 + acc_a;
+  d = d + acc_b;
+  d += rho(v, (sb + v) / ((double)cb + 1.0), 1);
+  d -= rho0[f];
+  out[i] = d;
+  if (pk) pk[i] = pack_record(d, (uint32_t)f, a, b);
+  if (cb0) {
+    cb0[i] = cb;
+    sb0[i] = sb;
+  }
+}
+
+// whether the packed-record K5 applies: integer Poisson intensities in
+// [0, 2^12), labels and ball counts < 2^16, ball sums < 2^20, 32-bit sites
+bool ps_rec_ok(const Lat &lat, int nball_full, int32_t nl, double image_max) {
+  return nball_full < kPsMaxBall && nl < 65536 && image_max < 4096.0 &&
+         (double)(nball_full + 1) * image_max < (double)(1 << 20) && lat.V < ((int64_t)1 << 31) &&
+         (lat.ndim == 2 || lat.ndim == 3);
+}
+
+int32_t pack_sites(const int32_t *L, const int32_t *Cown, const double *Sown, const double *I,
+                   const double *rho0, int64_t V, int4 *rec, cudaStream_t s) {
+  k_pack_sites<<<148 * 16, 256, 0, s>>>(L, Cown, Sown, I, rho0, V, rec);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t theta_table(double2 *tl, int P, int Q, cudaStream_t s) {
+  k_theta_table<<<148 * 8, 256, 0, s>>>(tl, P, Q);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
+int32_t delta_ps_rec(const int4 *rec, const double *I, const Lat &lat, const Off *ball, int nball,
+                     const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
+                     double *out, const double *rho0, int32_t *cb0, double *sb0,
+                     const double2 *tl, int tlP, int4 *pk, cudaStream_t s) {
+  if (n == 0) return RCB_OK;
+  if (lat.ndim == 3)
+    k_delta_ps_rec<3><<<grid_for(n, 128), 128, 0, s>>>(rec, I, (int)lat.nx, (int)lat.ny,
+                                                       (int)lat.nz, ball, nball, px, pown, pcomp, n,
+                                                       out, rho0, cb0, sb0, tl, tlP, pk);
+  else
+    k_delta_ps_rec<2><<<grid_for(n, 128), 128, 0, s>>>(rec, I, (int)lat.nx, (int)lat.ny, 1, ball,
+                                                       nball, px, pown, pcomp, n, out, rho0, cb0,
+                                                       sb0, tl, tlP, pk);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 }  // namespace rcb

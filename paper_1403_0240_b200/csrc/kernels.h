@@ -198,6 +198,15 @@ struct InputCheck {
 };
 int32_t check_inputs(const int32_t *L, const double *I, int64_t V, InputCheck *out, cudaStream_t s);
 int32_t log_table(double *lt, int P, int Q, cudaStream_t s);
+// K5 over packed site records (integer Poisson images)
+bool ps_rec_ok(const Lat &lat, int nball_full, int32_t nl, double image_max);
+int32_t pack_sites(const int32_t *L, const int32_t *Cown, const double *Sown, const double *I,
+                   const double *rho0, int64_t V, int4 *rec, cudaStream_t s);
+int32_t theta_table(double2 *tl, int P, int Q, cudaStream_t s);
+int32_t delta_ps_rec(const int4 *rec, const double *I, const Lat &lat, const Off *ball, int nball,
+                     const uint32_t *px, const int32_t *pown, const int32_t *pcomp, int64_t n,
+                     double *out, const double *rho0, int32_t *cb0, double *sb0,
+                     const double2 *tl, int tlP, int4 *pk, cudaStream_t s);
 bool delta_ps_writes_pk(const Lat &lat, int nball);
 int32_t sobolev_site_pk(const int4 *pk, double w0, int64_t p0, int64_t p1, int64_t lo, int64_t hi,
                         double *out, unsigned long long *pairs, cudaStream_t s);

@@ -685,3 +685,38 @@ def test_k5_tiles_equal_scalar_kernel(P, monkeypatch, shape):
         runs.append(out)
     for it, (a, b) in enumerate(zip(*runs)):
         assert a.shape == b.shape and np.array_equal(a, b), it
+
+
+@pytest.mark.parametrize("shape", [(40, 44, 48), (37, 29, 41), (2, 300, 257)])
+def test_k5_packed_records_equal_gather_kernel(P, monkeypatch, shape):
+    """K5 over packed 16-byte site records with the {theta, log theta} table
+    (integer Poisson images, the default) against the five-array gather
+    kernel (RCB_NO_K5REC=1): every raw PS increment bit-identical over three
+    l2 iterations (labels move, so the records are re-packed from refreshed
+    fields), in 3-D and 2-D, on lattices that are not tile multiples."""
+    import scenes
+    if shape[0] == 2:
+        sc = scenes.cfg4(n=shape[2], n_obj=5, per_axis=2, radius=9.0)
+        img = np.ascontiguousarray(sc.image[shape[2] // 2, :shape[1], :shape[2]])
+        lab = np.ascontiguousarray(sc.labels[shape[2] // 2, :shape[1], :shape[2]])
+    else:
+        sc = scenes.cfg4(n=shape[0], n_obj=5, per_axis=2, radius=9.0)
+        img = np.ascontiguousarray(sc.image[:, :shape[1], :shape[2]])
+        lab = np.ascontiguousarray(sc.labels[:, :shape[1], :shape[2]])
+    ecfg = P.EnergyConfig("ps", "poisson", 0.0, 4)
+    runs = []
+    for norec in ("0", "1"):
+        if norec == "1":
+            monkeypatch.setenv("RCB_NO_K5REC", "1")
+        else:
+            monkeypatch.delenv("RCB_NO_K5REC", raising=False)
+        eng = P.RegionCompetition(img, lab, ecfg, P.SobolevParams(6.0),
+                                  P.OptimizerConfig("l2", vanish_grace=5, drift_tolerance=1e-3))
+        out = []
+        for _ in range(3):
+            eng.iterate()
+            out.append(eng.last_candidates[3].copy())
+        out.append(eng.labels.copy())
+        runs.append(out)
+    for it, (a, b) in enumerate(zip(*runs)):
+        assert a.shape == b.shape and np.array_equal(a, b), it
