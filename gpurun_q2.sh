@@ -1,0 +1,9 @@
+#!/bin/bash
+# parity subset + cfg4/cfg2 bench lines without extras; BENCH_ENVS: space-separated env settings to compare
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_shard.py -m gpu -x -q ${PT_K:+-k "$PT_K"} > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
+for cfg in "" ${BENCH_ENVS}; do
+  env $cfg python bench.py --no-cpu-baseline --no-fp32 --no-full-run --no-sweep ${BENCH_EXTRA} > gpurun_out/bq.json 2>gpurun_out/bq.err || tail -5 gpurun_out/bq.err
+  python -c "
+import json;d=json.load(open('gpurun_out/bq.json'));print('[$cfg] cfg4',round(d['value']/1e9,3),'G/s',round(d['ms_per_step'],2),'ms',d['phase_ms_per_iteration'])
+c=d.get('cfg2');print('cfg2',c and (round(c['iterations_per_s'],1), c['phase_ms_per_iteration']))"
+done

@@ -837,6 +837,14 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       {
         const char *wr = getenv("RCB_DF_WINDOW");
         P.win_r = wr ? atoi(wr) : 0;
+        const char *w5 = getenv("RCB_DF_WIN5");  // comparison runs
+        P.win5 = !(w5 && w5[0] == '0');
+        const char *wf = getenv("RCB_DF_WPFIRST");  // comparison runs
+        P.wp_first = !(wf && wf[0] == '0');
+        const char *cc = getenv("RCB_DF_CLAIM");
+        P.claim_chunk = cc && cc[0] == 'c';
+        const char *nw = getenv("RCB_DF_NOWAIT");  // timing experiment: wrong results
+        P.nowait = nw && nw[0] == '1';
         const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs
         P.max_insert = mi ? atoi(mi) : 0;
         const char *bc = getenv("RCB_DF_BOXCAP");  // tests: 0 sends overflows to assist jobs

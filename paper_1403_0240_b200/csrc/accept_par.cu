@@ -894,7 +894,7 @@ __device__ __forceinline__ void finish_topology(const ParArgs &A, int32_t pos, i
   A.dround[pos] = round;
 }
 
-__global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
+__global__ void __launch_bounds__(512) k_accept_par(const __grid_constant__ ParArgs A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   BfsShared &S = *reinterpret_cast<BfsShared *>(smem_raw);
@@ -1082,7 +1082,10 @@ __global__ void __launch_bounds__(512) k_accept_par(ParArgs A) {
 // candidate never waits and the scheme cannot deadlock.  Verdicts are the
 // same functions of the same view V_i as in the round-based kernel.
 // ---------------------------------------------------------------------------
-static constexpr int kHW = 1024;  // warp BFS hash entries
+#ifndef RCB_DF_HW
+#define RCB_DF_HW 1024
+#endif
+static constexpr int kHW = RCB_DF_HW;  // warp BFS hash entries
 static constexpr int kFW = 256;   // warp BFS frontier capacity
 static constexpr int kMaxInsertW = kHW * 5 / 8;
 #ifndef RCB_DF_WARPS
@@ -1153,6 +1156,9 @@ __device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long 
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_rlx64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_rel64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1701,7 +1707,7 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
   int polls = 0;
   for (;;) {
     if (g >= 0) v = ld_rlx64(A.wp + g);
-    const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos;
+    const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos && !A.nowait;
     if (!__any_sync(0xffffffffu, p)) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
@@ -2667,7 +2673,175 @@ __device__ __forceinline__ void warp_wait_label(const ParArgs &A, int32_t l, int
 __device__ double df_ps_dtot(const ParArgs &A, WarpBfs &S, int32_t pos, int32_t f, int32_t a,
                              int32_t b, int di);
 
-__global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
+// Window cells of one candidate, gathered with every load in flight: up to
+// eight rounds of 32 cells are issued before the first is used (a round per
+// DRAM round trip cost the 9^3 window ~23 dependent trips).  bits = settled
+// donor-label cells P, unk = pending cells U, as in the window test below.
+__device__ __noinline__ void warp_window_fill(const ParArgs &A, int32_t pos, int z, int y, int x,
+                                              int32_t a, bool is3, int RB, uint32_t *bits,
+                                              uint32_t *unk) {
+  const int lane = threadIdx.x & 31;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny, nz = (int)A.lat.nz;
+  const int WB = 2 * RB + 1, nb = is3 ? WB * WB * WB : WB * WB;
+  constexpr int U = 8;
+  for (int base0 = 0; base0 < nb; base0 += 32 * U) {
+    unsigned long long wv[U];
+    int32_t lw[U];
+    bool ok[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int c = base0 + 32 * j + lane;
+      const int dz = is3 ? c / (WB * WB) - RB : 0;
+      const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
+      const int zz = z + dz, yy = y + dy, xx = x + dx;
+      ok[j] = c < nb && (dz || dy || dx) && (unsigned)zz < (unsigned)nz &&
+              (unsigned)yy < (unsigned)ny && (unsigned)xx < (unsigned)nx;
+      wv[j] = 0ull;
+      lw[j] = -1;
+      if (ok[j]) {
+        const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
+        wv[j] = ld_rlx64(A.wp + gw);
+        lw[j] = __ldg(A.L + gw);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (base0 + 32 * j < nb) {  // warp-uniform
+        const bool u = ok[j] && wp_pend((uint32_t)A.wp_bits, wv[j]) < pos;
+        const bool bit = ok[j] && !u && df_lab((uint32_t)A.wp_bits, wv[j], lw[j], pos) == a;
+        const unsigned m = __ballot_sync(0xffffffffu, bit), mu = __ballot_sync(0xffffffffu, u);
+        if (lane == 0) {
+          bits[(base0 >> 5) + j] = m;
+          unk[(base0 >> 5) + j] = mu;
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// First window tier in 3-D: the 5^3 window (124 cells, four loads per lane,
+// all in flight at once).  Lane k < 5 holds plane k as a 25-bit mask; a
+// flood step is the in-plane 8-neighbour dilation plus the neighbouring
+// planes' dilations by shuffles (26-connectivity), as warp_window_verdict3.
+// The verdict rules are those of the 9^3 window and exact for any window
+// size: 1 if the settled donor cells P join every seed, 2 if P|U leaves a
+// seed piece that cannot reach the rim, 0 otherwise (the 9^3 window and the
+// BFS tiers decide).
+__device__ __noinline__ int warp_window5(const ParArgs &A, int32_t pos, int z, int y, int x,
+                                         int32_t a) {
+  const int lane = threadIdx.x & 31;
+  const int nx = (int)A.lat.nx, ny = (int)A.lat.ny, nz = (int)A.lat.nz;
+  unsigned long long wv[4];
+  int32_t lw[4];
+  bool ok[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = 32 * j + lane;
+    const int dz = c / 25 - 2, dy = (c / 5) % 5 - 2, dx = c % 5 - 2;
+    const int zz = z + dz, yy = y + dy, xx = x + dx;
+    ok[j] = c < 125 && c != 62 && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+            (unsigned)xx < (unsigned)nx;
+    wv[j] = 0ull;
+    lw[j] = -1;
+    if (ok[j]) {
+      const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
+      wv[j] = ld_rlx64(A.wp + gw);
+      lw[j] = __ldg(A.L + gw);
+    }
+  }
+  uint32_t mp[4], mu[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool u = ok[j] && wp_pend((uint32_t)A.wp_bits, wv[j]) < pos;
+    const bool bit = ok[j] && !u && df_lab((uint32_t)A.wp_bits, wv[j], lw[j], pos) == a;
+    mp[j] = __ballot_sync(0xffffffffu, bit);
+    mu[j] = __ballot_sync(0xffffffffu, u);
+  }
+  // plane k = cells [25k, 25k + 25) of the 125-bit vectors
+  auto plane = [&](const uint32_t *m) -> uint32_t {
+    if (lane >= 5) return 0u;
+    const int sh = 25 * lane, w = sh >> 5, o = sh & 31;
+    const uint32_t lo = w == 0 ? m[0] : w == 1 ? m[1] : w == 2 ? m[2] : m[3];
+    const uint32_t hi = w == 0 ? m[1] : w == 1 ? m[2] : w == 2 ? m[3] : 0u;
+    return __funnelshift_r(lo, hi, o) & 0x1ffffffu;
+  };
+  const uint32_t P = plane(mp), Uu = plane(mu);
+  constexpr uint32_t kCol0 = 0x0108421u, kCol4 = 0x1084210u;
+  constexpr uint32_t kRim = kCol0 | kCol4 | 0x1fu | (0x1fu << 20);
+  constexpr uint32_t kSeed = 0x739C0u;  // rows 1..3, columns 1..3
+  auto d2 = [&](uint32_t p) -> uint32_t {
+    const uint32_t l = p & ~kCol0, h = p & ~kCol4;
+    return (p | (h << 1) | (l >> 1) | (p << 5) | (p >> 5) | (h << 6) | (l << 4) | (h >> 4) |
+            (l >> 6)) &
+           0x1ffffffu;
+  };
+  auto verdict = [&](uint32_t cells) -> int {
+    uint32_t rest = (lane >= 1 && lane <= 3) ? (cells & kSeed) : 0u;
+    bool first = true;
+    for (;;) {
+      const unsigned live = __ballot_sync(0xffffffffu, rest != 0);
+      if (!live) return 0;
+      const int k0 = __ffs(live) - 1;
+      uint32_t comp = lane == k0 ? (rest & (~rest + 1u)) : 0u;
+      for (;;) {
+        const uint32_t dn = d2(comp);
+        const uint32_t up = __shfl_up_sync(0xffffffffu, dn, 1);
+        const uint32_t dw = __shfl_down_sync(0xffffffffu, dn, 1);
+        const uint32_t n = (dn | up | dw) & cells;  // lanes >= 5 hold no cells
+        const bool grew = __any_sync(0xffffffffu, n != comp);
+        comp = n;
+        if (!grew) break;
+      }
+      const bool all = !__any_sync(0xffffffffu, (rest & ~comp) != 0);
+      rest &= ~comp;
+      if (first && all) return 1;
+      first = false;
+      const bool touch =
+          __any_sync(0xffffffffu, comp != 0 && (lane == 0 || lane == 4 || (comp & kRim) != 0));
+      if (!touch) return 2;
+    }
+  };
+  int r = verdict(P);
+  if (r != 1 && __any_sync(0xffffffffu, Uu != 0)) r = verdict(P | Uu) == 2 ? 2 : 0;
+  return r;
+}
+
+
+// Rank positions are handed out in order.  One global counter bumped by every
+// warp for every candidate saturates the L2's same-address atomic rate
+// (~430 M/s measured: 2 368 warps queue ~3 us per claim, which was the whole
+// box phase of every candidate).  A block therefore takes kClaimChunk
+// consecutive positions with ONE global atomic and its warps draw them, in
+// order, from a shared-memory word (next | end << 32).  Deadlock freedom is
+// unchanged: the earliest undecided position lies in some block's chunk, every
+// earlier position of that chunk is decided, so it is the current position of
+// a warp of that block or the next one drawn by the first warp to finish.
+static constexpr int kClaimChunk = 2 * kDfWarps;
+__device__ __forceinline__ int32_t df_claim(const ParArgs &A, unsigned long long *sc) {
+  constexpr unsigned long long kLock = ~0ull;
+  if (!A.claim_chunk) return atomicAdd(A.ctl + 12, 1);
+  for (;;) {
+    const unsigned long long v = *(volatile unsigned long long *)sc;
+    if (v == kLock) {
+      __nanosleep(40);
+      continue;
+    }
+    const uint32_t p = (uint32_t)v, e = (uint32_t)(v >> 32);
+    if (p < e) {
+      if (atomicCAS(sc, v, v + 1) == v) return (int32_t)p;
+      continue;
+    }
+    if (atomicCAS(sc, v, kLock) == v) {  // this warp refills
+      const int32_t g = atomicAdd(A.ctl + 12, kClaimChunk);
+      *(volatile unsigned long long *)sc =
+          ((unsigned long long)(uint32_t)(g + kClaimChunk) << 32) | (uint32_t)(g + 1);
+      return g;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_constant__ ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
   const Lat &lat = A.lat;
@@ -2682,7 +2856,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
   // position is always the current one of the warp holding it (a warp's
   // claimed-ahead position is later than its current one).  Only one ahead:
   // a position held behind a warp stuck in a long BFS stalls its dependants.
-  int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
+  __shared__ unsigned long long s_claim;
+  if (threadIdx.x == 0) s_claim = 0ull;  // empty chunk: the first draw refills
+  __syncthreads();
+  int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? df_claim(A, &s_claim) : 0, 0);
   int4 rc = pos < M ? __ldg(A.rec + pos) : make_int4(0, 0, 0, 0);
   for (;;) {
     if (pos >= M) {
@@ -2693,7 +2870,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       break;
     }
     // next claim and the watchdog flag: consumed after the box wait
-    const int32_t nclaim = lane == 0 ? atomicAdd(ctl + 12, 1) : 0;
+    const int32_t nclaim = lane == 0 ? df_claim(A, &s_claim) : 0;
     const int stop = lane == 0 ? (int)df_aborted(A) : 0;
     df_stamp(A, pos, 0);
     const int32_t f = rc.x, next = rc.w;
@@ -2764,28 +2941,12 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       const int RB = is3 ? 4 : (A.win_r ? A.win_r : 5), WB = 2 * RB + 1;
       const int nb = is3 ? WB * WB * WB : WB * WB;
       uint32_t *bits = S.fr[0], *unk = S.fr[1];
-      for (int base = 0; base < nb; base += 32) {
-        const int c = base + lane;
-        bool bit = false, u = false;
-        if (c < nb) {
-          const int dz = is3 ? c / (WB * WB) - RB : 0;
-          const int dy = (c / WB) % WB - RB, dx = c % WB - RB;
-          const int zz = z + dz, yy = y + dy, xx = x + dx;
-          if ((dz || dy || dx) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
-              (unsigned)xx < (unsigned)nx) {
-            const int64_t gw = ((int64_t)zz * ny + yy) * nx + xx;
-            const unsigned long long wv = ld_rlx64(A.wp + gw);
-            const int32_t lw = __ldg(A.L + gw);
-            u = wp_pend((uint32_t)A.wp_bits, wv) < pos;
-            bit = !u && df_lab((uint32_t)A.wp_bits, wv, lw, pos) == a;
-          }
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, bit), mu = __ballot_sync(0xffffffffu, u);
-        if (lane == 0) {
-          bits[base >> 5] = m;
-          unk[base >> 5] = mu;
-        }
-      }
+      // 3-D: the 5^3 window first (one round trip); most inconclusive boxes
+      // resolve there and never read the 9^3 window's 81 rows
+      int w5 = 0;
+      if (is3 && A.win5) w5 = warp_window5(A, pos, z, y, x, a);
+      if (w5 == 0) {
+      warp_window_fill(A, pos, z, y, x, a, is3, RB, bits, unk);
       __syncwarp();
       if (is3) {  // warp-parallel floods (the serial one is ~100 us on one lane)
         uint32_t any_u = 0;
@@ -2815,9 +2976,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         S.result = r;
       }
       __syncwarp();
-      int wb = S.result;
+      }  // w5 == 0
+      int wb = w5 ? w5 : S.result;
       __syncwarp();
-      dbg = 1000 + 100 * (wb + 2);
+      dbg = 1000 + 100 * (wb + 2) + (w5 ? 7 : 0);
       df_stamp(A, pos, 3);
       if (wb == 0 && !is3) {
         wb = window31(A, pos, f, a);
@@ -2939,6 +3101,16 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
       }
     }
     if (lane == 0) {
+      // The site word first: it carries everything a dependant reads (next
+      // pending position, flip position, new label), so the candidates
+      // waiting on x go on one L2 trip after this store instead of after the
+      // two release fences below (~1.4 us per hop of every dependency chain).
+      // Readers that trust dec[] (the low-water mark, the assist jobs) see
+      // the word too: dec is released after it.
+      const unsigned long long word =
+          d == ACC ? wp_pack((uint32_t)A.wp_bits, next, pos, b)
+                   : wp_pack((uint32_t)A.wp_bits, next, wold, lold);
+      if (A.wp_first && !sa && !sb) st_rlx64(A.wp + f, word);
       A.blocker[pos] = dbg;
       if (d == ACC) {
         A.newlab[f] = b;
@@ -2947,10 +3119,10 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(ParArgs A) {
         if (sb) atomicAdd((unsigned long long *)(A.cnt + b), 1ull);
       }
       df_stamp(A, pos, 1);
-      // release: the flip (newlab, w) and counts are visible before the
-      // decision, the decision before the site word with its next position
+      // release: the flip (newlab, w), the counts and the site word are
+      // visible before the decision
       st_rel_u8(A.dec + pos, d);
-      st_rel64(A.wp + f, d == ACC ? wp_pack((uint32_t)A.wp_bits, next, pos, b) : wp_pack((uint32_t)A.wp_bits, next, wold, lold));
+      if (!(A.wp_first && !sa && !sb)) st_rel64(A.wp + f, word);
       if (sa) st_rel(A.lab_ptr + a, A.lab_ptr[a] + 1);
       if (sb) st_rel(A.lab_ptr + b, A.lab_ptr[b] + 1);
     }

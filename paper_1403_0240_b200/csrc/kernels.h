@@ -100,6 +100,10 @@ struct ParArgs {
   uint8_t *bigfg;
   long long *tdbg;  // RCB_PROFILE: per position (fetch, decide, box, window) globaltimer ns
   int win_r;        // dataflow window radius in 2-D (0: default 5; 1: none)
+  int wp_first;     // publish the site word before the decision's release fence (RCB_DF_WPFIRST=0: after)
+  int claim_chunk;  // rank positions drawn per block chunk (RCB_DF_CLAIM=chunk; default: one global atomic each)
+  int nowait;       // timing experiment only (RCB_DF_NOWAIT=1): ignore box dependencies, results are wrong
+  int win5;         // 3-D: 5^3 window tier before the 9^3 window (RCB_DF_WIN5=0 turns it off)
   int max_insert;   // dataflow warp-BFS footprint cap (0: default)
   int box_cap;      // dataflow box-map BFS capacity in sites (-1: default, 0: off)
   unsigned long long *job, *ufp;  // dataflow assist jobs (accept_par.cu)
