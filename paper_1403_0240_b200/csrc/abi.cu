@@ -170,6 +170,7 @@ struct rcb_engine {
   DBuf<uint8_t> bigfg2;
   DBuf<uint32_t> bigtouch;
   DBuf<uint8_t> tflag;
+  DBuf<uint16_t> I16;     // integer image as 16-bit words (integer band refresh), empty otherwise
   DBuf<int32_t> ps_cells;  // l2 PS gate: the 2R ball as cube indices
   int ps_ncells = 0;
   DBuf<int2> bigtouch_n;
@@ -230,7 +231,7 @@ struct rcb_engine {
       ufp.release(s); job.release(s); wpk.release(s); rec.release(s);
       ufq.release(s); qmark.release(s); qlist.release(s); qscr.release(s); qstate.release(s);
       bigmap.release(s); bigfr2.release(s); bigfg2.release(s); bigtouch.release(s);
-      bigtouch_n.release(s); tflag.release(s); ps_cells.release(s);
+      bigtouch_n.release(s); tflag.release(s); I16.release(s); ps_cells.release(s);
       eval_per.release(s); eval_limbs.release(s); band.release(s);
       labbounds.release(s);
       tmp.release(s); ssc.release(s); rsc.release(s);
@@ -501,6 +502,13 @@ int32_t rcb_engine_create_ex(const void *image, int32_t image_dtype, const int32
         TRYB(e->logt.reserve(P * Q, s));
         TRYB(log_table(e->logt.p, (int)P, (int)Q, s));
         e->logt_P = (int)P;
+      }
+      // 3-D band refresh by prefix-sum ball runs (k_fields_band3d_int): exact
+      // for integer intensities in [0, 2^12) with ball sums < 2^20
+      if (ndim == 3 && chk.image_min >= 0.0 && ps_rec_ok(e->lat, nbf, chk.label_max + 2, chk.image_max) &&
+          !getenv("RCB_NO_BANDINT")) {
+        TRYB(e->I16.reserve(V, s));
+        TRYB(image_u16(e->I.p, V, e->I16.p, s));
       }
       if (P * Q * 16 <= ((int64_t)128 << 20) &&
           ps_rec_ok(e->lat, nbf, chk.label_max + 1, chk.image_max) && !getenv("RCB_NO_K5REC")) {
@@ -841,8 +849,6 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.win5 = !(w5 && w5[0] == '0');
         const char *wf = getenv("RCB_DF_WPFIRST");  // comparison runs
         P.wp_first = !(wf && wf[0] == '0');
-        const char *cc = getenv("RCB_DF_CLAIM");
-        P.claim_chunk = cc && cc[0] == 'c';
         const char *nw = getenv("RCB_DF_NOWAIT");  // timing experiment: wrong results
         P.nowait = nw && nw[0] == '1';
         const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs
@@ -998,6 +1004,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.colb = &e->colb;
       X.labbounds = &e->labbounds;
       X.tflag = &e->tflag;
+      X.I16 = e->I16.p;
       X.chain_pool = &e->chain_pool;
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)

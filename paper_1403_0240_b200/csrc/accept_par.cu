@@ -2808,39 +2808,6 @@ __device__ __noinline__ int warp_window5(const ParArgs &A, int32_t pos, int z, i
 }
 
 
-// Rank positions are handed out in order.  One global counter bumped by every
-// warp for every candidate saturates the L2's same-address atomic rate
-// (~430 M/s measured: 2 368 warps queue ~3 us per claim, which was the whole
-// box phase of every candidate).  A block therefore takes kClaimChunk
-// consecutive positions with ONE global atomic and its warps draw them, in
-// order, from a shared-memory word (next | end << 32).  Deadlock freedom is
-// unchanged: the earliest undecided position lies in some block's chunk, every
-// earlier position of that chunk is decided, so it is the current position of
-// a warp of that block or the next one drawn by the first warp to finish.
-static constexpr int kClaimChunk = 2 * kDfWarps;
-__device__ __forceinline__ int32_t df_claim(const ParArgs &A, unsigned long long *sc) {
-  constexpr unsigned long long kLock = ~0ull;
-  if (!A.claim_chunk) return atomicAdd(A.ctl + 12, 1);
-  for (;;) {
-    const unsigned long long v = *(volatile unsigned long long *)sc;
-    if (v == kLock) {
-      __nanosleep(40);
-      continue;
-    }
-    const uint32_t p = (uint32_t)v, e = (uint32_t)(v >> 32);
-    if (p < e) {
-      if (atomicCAS(sc, v, v + 1) == v) return (int32_t)p;
-      continue;
-    }
-    if (atomicCAS(sc, v, kLock) == v) {  // this warp refills
-      const int32_t g = atomicAdd(A.ctl + 12, kClaimChunk);
-      *(volatile unsigned long long *)sc =
-          ((unsigned long long)(uint32_t)(g + kClaimChunk) << 32) | (uint32_t)(g + 1);
-      return g;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_constant__ ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
@@ -2856,10 +2823,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
   // position is always the current one of the warp holding it (a warp's
   // claimed-ahead position is later than its current one).  Only one ahead:
   // a position held behind a warp stuck in a long BFS stalls its dependants.
-  __shared__ unsigned long long s_claim;
-  if (threadIdx.x == 0) s_claim = 0ull;  // empty chunk: the first draw refills
-  __syncthreads();
-  int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? df_claim(A, &s_claim) : 0, 0);
+  int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
   int4 rc = pos < M ? __ldg(A.rec + pos) : make_int4(0, 0, 0, 0);
   for (;;) {
     if (pos >= M) {
@@ -2870,7 +2834,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
       break;
     }
     // next claim and the watchdog flag: consumed after the box wait
-    const int32_t nclaim = lane == 0 ? df_claim(A, &s_claim) : 0;
+    const int32_t nclaim = lane == 0 ? atomicAdd(ctl + 12, 1) : 0;
     const int stop = lane == 0 ? (int)df_aborted(A) : 0;
     df_stamp(A, pos, 0);
     const int32_t f = rc.x, next = rc.w;
@@ -4704,7 +4668,7 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     const bool fresh = X.tflag->cap < (size_t)nt;
     RCB_TRY(X.tflag->reserve(nt, s));
     if (fresh) RCB_CUDA(cudaMemsetAsync(X.tflag->p, 0, X.tflag->cap, s));
-    RCB_TRY(fields_band3d(X.acc, X.moves, X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius,
+    RCB_TRY(fields_band3d(X.acc, X.moves, X.Lmut, X.I, X.I16, A.lat, X.ball_full, X.nball_full, X.radius,
                           X.dirty, X.tflag->p, X.Cown, X.Sown, X.rho0, X.poisson,
                           band_ledger ? X.band : nullptr, s));
     nl += 3;

@@ -350,6 +350,147 @@ __global__ void __launch_bounds__(256) k_fields_band3d(
   }
 }
 
+// 3-D band refresh for integer images (0 <= I < 2^12, labels < 2^16 - 1, ball
+// sums < 2^20: the conditions of the packed K5 records).  Integer sums are
+// exact in any order, so the own-label ball sums need not follow the ball's
+// offset order: the ball is cut into its x-runs (one per (dz, dy), 49 for
+// R = 4) and a run's sum is a difference of two entries of a per-row prefix
+// sum of the packed word (1 << 20 | I) over the cells of one label -- 98
+// shared-memory reads per site instead of 257 compare-and-add steps over two
+// arrays.  One prefix table is built per label present among the tile's own
+// sites (usually one or two).  Every site of an active tile is evaluated and
+// written only where (C, S) changed: a site whose ball holds a flip that left
+// its own-label sums alone kept the same rho0, and its ledger term was an
+// exact zero.  Same Cown / Sown / rho0 / band sums as k_fields_band3d.
+static constexpr int kBiPS = kT3X + 2 * kT3R + 1;  // row stride (odd: conflict-free row walks)
+__global__ void __launch_bounds__(256) k_fields_band3d_int(
+    const int32_t *__restrict__ L, const uint16_t *__restrict__ I16, int nx, int ny, int nz, int R,
+    const uint8_t *__restrict__ tflag, int32_t *__restrict__ Cown, double *__restrict__ Sown,
+    double *__restrict__ rho0, int poisson, long long *__restrict__ band) {
+  constexpr int SY = kT3Y + 2 * kT3R, SZ = kT3Z + 2 * kT3R;
+  __shared__ uint32_t sW[SZ * SY * kBiPS];  // label | I << 16 (0xffff: outside the lattice)
+  __shared__ uint32_t sP[SZ * SY * kBiPS];  // per row: prefix sums of (1 << 20 | I) over one label
+  __shared__ int2 srow[(2 * kT3R + 1) * (2 * kT3R + 1)];  // per ball row: offsets of the two prefix entries
+  __shared__ int nrow, s_pick;
+  __shared__ long long sm[kLimbs];
+  const int ntx = gridDim.x, nty = gridDim.y, ntz = gridDim.z;
+  bool any = false;
+  if (threadIdx.x < 27) {
+    const int tz = (int)blockIdx.z + (int)threadIdx.x / 9 - 1;
+    const int ty = (int)blockIdx.y + ((int)threadIdx.x / 3) % 3 - 1;
+    const int tx = (int)blockIdx.x + (int)threadIdx.x % 3 - 1;
+    if ((unsigned)tz < (unsigned)ntz && (unsigned)ty < (unsigned)nty && (unsigned)tx < (unsigned)ntx)
+      any = tflag[((int64_t)tz * nty + ty) * ntx + tx] != 0;
+  }
+  if (!__syncthreads_or(any)) return;
+  const int tx = threadIdx.x % kT3X, ty = (threadIdx.x / kT3X) % kT3Y, tz = threadIdx.x / (kT3X * kT3Y);
+  const int x0 = blockIdx.x * kT3X, y0 = blockIdx.y * kT3Y, z0 = blockIdx.z * kT3Z;
+  const int x = x0 + tx, y = y0 + ty, z = z0 + tz;
+  const bool inside = x < nx && y < ny && z < nz;
+  const int64_t f = ((int64_t)z * ny + y) * nx + x;
+  const int hx = kT3X + 2 * R, hy = kT3Y + 2 * R, hz = kT3Z + 2 * R;
+  if (threadIdx.x == 0) {  // the ball as x-runs per (dz, dy): |o|^2 <= R^2
+    int k = 0;
+    for (int dz = -R; dz <= R; ++dz)
+      for (int dy = -R; dy <= R; ++dy) {
+        const int t = R * R - dz * dz - dy * dy;
+        if (t < 0) continue;
+        int h = 0;
+        while ((h + 1) * (h + 1) <= t) ++h;
+        const int rb = (dz * SY + dy) * kBiPS;
+        srow[k++] = make_int2(rb + h + 1, rb - h);  // prefix[x + h + 1] - prefix[x - h]
+      }
+    nrow = k;
+  }
+  for (int i = threadIdx.x; i < hx * hy * hz; i += blockDim.x) {
+    const int cz = i / (hx * hy), rem = i - cz * hx * hy;
+    const int cy = rem / hx, cx = rem - cy * hx;
+    const int gz = z0 - R + cz, gy = y0 - R + cy, gx = x0 - R + cx;
+    const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
+                    (unsigned)gx < (unsigned)nx;
+    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+    sW[(cz * SY + cy) * kBiPS + cx] =
+        ok ? ((uint32_t)__ldg(L + g) | ((uint32_t)__ldg(I16 + g) << 16)) : 0xffffu;
+  }
+  if (band)
+    for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
+  __syncthreads();
+  const int cbase = ((tz + R) * SY + (ty + R)) * kBiPS + tx + R;
+  const uint32_t wc = sW[cbase];
+  const int own = inside ? (int)(wc & 0xffffu) : 0x7fffffff;
+  bool todo = inside;
+  uint32_t tot = 0;
+  for (;;) {  // one pass per label among the tile's own sites, smallest first
+    if (threadIdx.x == 0) s_pick = 0x7fffffff;
+    __syncthreads();
+    const int wmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)(todo ? own : 0x7fffffff));
+    if ((threadIdx.x & 31) == 0 && wmin != 0x7fffffff) atomicMin(&s_pick, wmin);
+    __syncthreads();
+    const int l = s_pick;
+    if (l == 0x7fffffff) break;
+    if (threadIdx.x < hy * hz) {  // this row's prefix sums over the cells of label l
+      const int cz = threadIdx.x / hy, cy = threadIdx.x - cz * hy;
+      const int rb = (cz * SY + cy) * kBiPS;
+      uint32_t a = 0;
+      sP[rb] = 0;
+#pragma unroll 8
+      for (int cx = 0; cx < hx; ++cx) {
+        const uint32_t w = sW[rb + cx];
+        if ((int)(w & 0xffffu) == l) a += (1u << 20) + (w >> 16);
+        sP[rb + cx + 1] = a;
+      }
+    }
+    __syncthreads();
+    if (todo && own == l) {
+      const int nr = nrow;
+      uint32_t t0 = 0, t1 = 0;
+      int k = 0;
+      for (; k + 1 < nr; k += 2) {
+        const int2 r0 = srow[k], r1 = srow[k + 1];
+        t0 += sP[cbase + r0.x] - sP[cbase + r0.y];
+        t1 += sP[cbase + r1.x] - sP[cbase + r1.y];
+      }
+      if (k < nr) {
+        const int2 r0 = srow[k];
+        t0 += sP[cbase + r0.x] - sP[cbase + r0.y];
+      }
+      tot = t0 + t1;
+      todo = false;
+    }
+  }
+  double oldr = 0.0, newr = 0.0;
+  bool changed = false;
+  if (inside) {
+    const int32_t c = (int32_t)(tot >> 20);
+    const double sv = (double)(tot & 0xfffffu);
+    changed = Cown[f] != c || Sown[f] != sv;
+    if (changed) {
+      if (band) oldr = rho0[f];
+      Cown[f] = c;
+      Sown[f] = sv;
+      newr = rho((double)(wc >> 16), sv / (double)c, poisson);
+      if (rho0) rho0[f] = newr;
+    }
+  }
+  if (band) {  // every thread of the block reaches here (warp-uniform)
+    acc_add_warp(sm, -oldr, changed);
+    acc_add_warp(sm, newr, changed);
+    acc_flush(sm, band);
+  }
+}
+
+__global__ void k_to_u16(const double *__restrict__ src, int64_t n, uint16_t *__restrict__ dst) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = (uint16_t)src[i];
+}
+
+int32_t image_u16(const double *I, int64_t V, uint16_t *I16, cudaStream_t s) {
+  k_to_u16<<<148 * 16, 256, 0, s>>>(I, V, I16);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 // per accepted move: flips[x] = v, tflag[tile(x)] = v (v = 1 mark, 0 clear)
 __global__ void k_mark_flips(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
                              Lat lat, uint8_t v, uint8_t *__restrict__ flips,
@@ -372,12 +513,17 @@ int64_t band3d_tiles(const Lat &lat) {
 }
 
 int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
-                      const Lat &lat, const Off *ball_full, int nball_full, int R, uint8_t *flips,
-                      uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0, int poisson,
-                      long long *band, cudaStream_t s) {
+                      const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
+                      int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
+                      double *rho0, int poisson, long long *band, cudaStream_t s) {
   k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, flips, tflag);
   dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
             (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
+  if (I16)  // integer image: prefix-sum ball runs (the caller checked the ranges)
+    k_fields_band3d_int<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I16, (int)lat.nx, (int)lat.ny,
+                                                             (int)lat.nz, R, tflag, Cown, Sown,
+                                                             rho0, poisson, band);
+  else
   k_fields_band3d<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, (int)lat.nz,
                                                        ball_full, nball_full, R, flips, tflag,
                                                        Cown, Sown, rho0, poisson, band);
