@@ -282,7 +282,7 @@ struct rcb_engine {
     RCB_TRY(stats_rebuild(L.p, I.p, lat.V, nl, cnt.p, tot.p, tsq.p, ssc, s));
     if (ecfg.region_model == 1)
       RCB_TRY(ps_fields(L.p, I.p, lat, ball_full.p, nball_full, Cown.p, Sown.p, s, rho0.p,
-                        ecfg.noise_model == 1));
+                        ecfg.noise_model == 1, I16.p));
     return RCB_OK;
   }
 
@@ -851,6 +851,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.wp_first = !(wf && wf[0] == '0');
         const char *nw = getenv("RCB_DF_NOWAIT");  // timing experiment: wrong results
         P.nowait = nw && nw[0] == '1';
+        const char *ha = getenv("RCB_DF_HELPAFTER");
+        P.help_after = ha ? atoi(ha) : 0;
         const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs
         P.max_insert = mi ? atoi(mi) : 0;
         const char *bc = getenv("RCB_DF_BOXCAP");  // tests: 0 sends overflows to assist jobs

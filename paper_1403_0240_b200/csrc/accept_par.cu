@@ -1709,7 +1709,10 @@ __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A
     if (g >= 0) v = ld_rlx64(A.wp + g);
     const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos && !A.nowait;
     if (!__any_sync(0xffffffffu, p)) break;
-    if (!warp_help(A)) {
+    // short waits (the common case: a box neighbour a few positions earlier
+    // is being decided) only poll the site words; the assist-job word joins
+    // after kHelpAfter polls (each look at it is one more L2 trip per poll)
+    if (polls < A.help_after || !warp_help(A)) {
       __nanosleep(ns);
       if (ns < 256) ns <<= 1;
       // the watchdog looks only every 64 idle polls (the common wait is short)

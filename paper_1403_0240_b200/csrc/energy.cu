@@ -374,15 +374,17 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
   __shared__ int nrow, s_pick;
   __shared__ long long sm[kLimbs];
   const int ntx = gridDim.x, nty = gridDim.y, ntz = gridDim.z;
-  bool any = false;
-  if (threadIdx.x < 27) {
-    const int tz = (int)blockIdx.z + (int)threadIdx.x / 9 - 1;
-    const int ty = (int)blockIdx.y + ((int)threadIdx.x / 3) % 3 - 1;
-    const int tx = (int)blockIdx.x + (int)threadIdx.x % 3 - 1;
-    if ((unsigned)tz < (unsigned)ntz && (unsigned)ty < (unsigned)nty && (unsigned)tx < (unsigned)ntx)
-      any = tflag[((int64_t)tz * nty + ty) * ntx + tx] != 0;
+  if (tflag) {  // null: every tile (the full rebuild), every site written
+    bool any = false;
+    if (threadIdx.x < 27) {
+      const int tz = (int)blockIdx.z + (int)threadIdx.x / 9 - 1;
+      const int ty = (int)blockIdx.y + ((int)threadIdx.x / 3) % 3 - 1;
+      const int tx = (int)blockIdx.x + (int)threadIdx.x % 3 - 1;
+      if ((unsigned)tz < (unsigned)ntz && (unsigned)ty < (unsigned)nty && (unsigned)tx < (unsigned)ntx)
+        any = tflag[((int64_t)tz * nty + ty) * ntx + tx] != 0;
+    }
+    if (!__syncthreads_or(any)) return;
   }
-  if (!__syncthreads_or(any)) return;
   const int tx = threadIdx.x % kT3X, ty = (threadIdx.x / kT3X) % kT3Y, tz = threadIdx.x / (kT3X * kT3Y);
   const int x0 = blockIdx.x * kT3X, y0 = blockIdx.y * kT3Y, z0 = blockIdx.z * kT3Z;
   const int x = x0 + tx, y = y0 + ty, z = z0 + tz;
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
   if (inside) {
     const int32_t c = (int32_t)(tot >> 20);
     const double sv = (double)(tot & 0xfffffu);
-    changed = Cown[f] != c || Sown[f] != sv;
+    changed = !tflag || Cown[f] != c || Sown[f] != sv;
     if (changed) {
       if (band) oldr = rho0[f];
       Cown[f] = c;
@@ -871,7 +873,7 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
 
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s, double *rho0,
-                  int poisson) {
+                  int poisson, const uint16_t *I16) {
   int R = 0;  // the ball radius (ball_full is on the device: from its site count)
   if (lat.ndim == 2) {
     for (int r = 1; r <= kTRmax; ++r) {
@@ -895,9 +897,19 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
         break;
       }
     }
-    if (R > 0 && fields_tile3d_ok(lat, R, nball_full))
+    if (R > 0 && fields_tile3d_ok(lat, R, nball_full)) {
+      if (I16 && rho0) {  // integer image: prefix-sum ball runs over every tile
+        dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
+                  (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
+        k_fields_band3d_int<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I16, (int)lat.nx, (int)lat.ny,
+                                                                 (int)lat.nz, R, nullptr, Cown,
+                                                                 Sown, rho0, poisson, nullptr);
+        RCB_CUDA(cudaGetLastError());
+        return RCB_OK;
+      }
       return fields_tile3d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson,
                            nullptr, s);
+    }
   }
   if (R > 0 && fields_tile2d_ok(lat, R, nball_full))
     return fields_tile2d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson, s);

@@ -101,6 +101,7 @@ struct ParArgs {
   long long *tdbg;  // RCB_PROFILE: per position (fetch, decide, box, window) globaltimer ns
   int win_r;        // dataflow window radius in 2-D (0: default 5; 1: none)
   int wp_first;     // publish the site word before the decision's release fence (RCB_DF_WPFIRST=0: after)
+  int help_after;   // settled waits look for assist jobs only after this many polls (RCB_DF_HELPAFTER)
   int nowait;       // timing experiment only (RCB_DF_NOWAIT=1): ignore box dependencies, results are wrong
   int win5;         // 3-D: 5^3 window tier before the 9^3 window (RCB_DF_WIN5=0 turns it off)
   int max_insert;   // dataflow warp-BFS footprint cap (0: default)
@@ -238,7 +239,7 @@ int32_t delta_pc_batch(const double *I, const uint32_t *px, const int32_t *pown,
                        int4 *pk = nullptr);
 int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                   int nball_full, int32_t *Cown, double *Sown, cudaStream_t s,
-                  double *rho0 = nullptr, int poisson = 0);
+                  double *rho0 = nullptr, int poisson = 0, const uint16_t *I16 = nullptr);
 int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, cudaStream_t s);
