@@ -296,6 +296,70 @@ __device__ __forceinline__ void acc_add_warp(long long *limbs, double d, bool ha
   }
 }
 
+// Per-thread staging for the superaccumulator: values whose limb window
+// (k0) matches the staged one are merged in registers (integer limb parts:
+// exact in any order); a value on another window goes straight to the shared
+// limbs with per-lane atomics.  flush_warp() is warp-collective and adds the
+// staged parts with one shared atomic per limb and window, like acc_add_warp.
+struct AccStage {
+  int k0 = -1;
+  long long c0 = 0, c1 = 0, c2 = 0;
+  __device__ __forceinline__ void add(long long *limbs, double d) {
+    if (d == 0.0) return;
+    const uint64_t u = (uint64_t)__double_as_longlong(d);
+    const int ex = (int)((u >> 52) & 0x7ff);
+    uint64_t m = u & ((1ull << 52) - 1);
+    int e;
+    if (ex == 0) {
+      e = -1074;
+    } else {
+      m |= 1ull << 52;
+      e = ex - 1075;
+    }
+    const int pos = e + 1074, k = pos >> 5, sh = pos & 31;
+    const uint64_t lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0;
+    long long a0 = (long long)(lo & 0xffffffffull), a1 = (long long)(lo >> 32), a2 = (long long)hi;
+    if (u >> 63) {
+      a0 = -a0;
+      a1 = -a1;
+      a2 = -a2;
+    }
+    if (k0 < 0) k0 = k;
+    if (k == k0) {
+      c0 += a0;
+      c1 += a1;
+      c2 += a2;
+    } else {
+      if (a0) atomicAdd((unsigned long long *)&limbs[k], (unsigned long long)a0);
+      if (a1) atomicAdd((unsigned long long *)&limbs[k + 1], (unsigned long long)a1);
+      if (a2) atomicAdd((unsigned long long *)&limbs[k + 2], (unsigned long long)a2);
+    }
+  }
+  __device__ __forceinline__ void flush_warp(long long *limbs) {  // all lanes call it
+    const int lane = threadIdx.x & 31;
+    bool has = k0 >= 0 && (c0 | c1 | c2) != 0;
+    unsigned act = __ballot_sync(0xffffffffu, has);
+    while (act) {
+      const int leader = __ffs(act) - 1;
+      const int k = __shfl_sync(0xffffffffu, k0, leader);
+      const bool mine = has && k0 == k;
+      long long s0 = mine ? c0 : 0, s1 = mine ? c1 : 0, s2 = mine ? c2 : 0;
+      for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      if (lane == leader) {
+        if (s0) atomicAdd((unsigned long long *)&limbs[k], (unsigned long long)s0);
+        if (s1) atomicAdd((unsigned long long *)&limbs[k + 1], (unsigned long long)s1);
+        if (s2) atomicAdd((unsigned long long *)&limbs[k + 2], (unsigned long long)s2);
+      }
+      if (mine) has = false;
+      act = __ballot_sync(0xffffffffu, has);
+    }
+  }
+};
+
 __device__ __forceinline__ void acc_flush(long long *sm, long long *gl) {
   __syncthreads();
   for (int k = threadIdx.x; k < kLimbs; k += blockDim.x)

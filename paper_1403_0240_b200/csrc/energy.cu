@@ -362,14 +362,19 @@ __global__ void __launch_bounds__(256) k_fields_band3d(
 // written only where (C, S) changed: a site whose ball holds a flip that left
 // its own-label sums alone kept the same rho0, and its ledger term was an
 // exact zero.  Same Cown / Sown / rho0 / band sums as k_fields_band3d.
-static constexpr int kBiPS = kT3X + 2 * kT3R + 1;  // row stride (odd: conflict-free row walks)
+// Tiles of 16 x 8 x 8 sites, four sites (z, z + 2, z + 4, z + 6) per thread:
+// the 24 x 16 x 16 halo costs 6 staged cells per site (13.5 with the 16 x 4 x 4
+// tiles of the fp64 kernels) and a prefix table serves 1 024 sites.
+static constexpr int kBiX = 16, kBiY = 8, kBiZ = 8, kBiZT = 2, kBiS = kBiZ / kBiZT;
+static constexpr int kBiPS = kBiX + 2 * kT3R + 1;  // row stride (odd: conflict-free row walks)
 __global__ void __launch_bounds__(256) k_fields_band3d_int(
     const int32_t *__restrict__ L, const uint16_t *__restrict__ I16, int nx, int ny, int nz, int R,
     const uint8_t *__restrict__ tflag, int32_t *__restrict__ Cown, double *__restrict__ Sown,
     double *__restrict__ rho0, int poisson, long long *__restrict__ band) {
-  constexpr int SY = kT3Y + 2 * kT3R, SZ = kT3Z + 2 * kT3R;
-  __shared__ uint32_t sW[SZ * SY * kBiPS];  // label | I << 16 (0xffff: outside the lattice)
-  __shared__ uint32_t sP[SZ * SY * kBiPS];  // per row: prefix sums of (1 << 20 | I) over one label
+  constexpr int SY = kBiY + 2 * kT3R, SZ = kBiZ + 2 * kT3R;
+  extern __shared__ __align__(16) uint32_t bi_smem[];
+  uint32_t *sW = bi_smem;                   // label | I << 16 (0xffff: outside the lattice)
+  uint32_t *sP = bi_smem + SZ * SY * kBiPS;  // per row: prefix sums of (1 << 20 | I) over one label
   __shared__ int2 srow[(2 * kT3R + 1) * (2 * kT3R + 1)];  // per ball row: offsets of the two prefix entries
   __shared__ int nrow, s_pick;
   __shared__ long long sm[kLimbs];
@@ -385,12 +390,10 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
     }
     if (!__syncthreads_or(any)) return;
   }
-  const int tx = threadIdx.x % kT3X, ty = (threadIdx.x / kT3X) % kT3Y, tz = threadIdx.x / (kT3X * kT3Y);
-  const int x0 = blockIdx.x * kT3X, y0 = blockIdx.y * kT3Y, z0 = blockIdx.z * kT3Z;
-  const int x = x0 + tx, y = y0 + ty, z = z0 + tz;
-  const bool inside = x < nx && y < ny && z < nz;
-  const int64_t f = ((int64_t)z * ny + y) * nx + x;
-  const int hx = kT3X + 2 * R, hy = kT3Y + 2 * R, hz = kT3Z + 2 * R;
+  const int tx = threadIdx.x % kBiX, ty = (threadIdx.x / kBiX) % kBiY, tz = threadIdx.x / (kBiX * kBiY);
+  const int x0 = blockIdx.x * kBiX, y0 = blockIdx.y * kBiY, z0 = blockIdx.z * kBiZ;
+  const int x = x0 + tx, y = y0 + ty;
+  const int hx = kBiX + 2 * R, hy = kBiY + 2 * R, hz = kBiZ + 2 * R;
   if (threadIdx.x == 0) {  // the ball as x-runs per (dz, dy): |o|^2 <= R^2
     int k = 0;
     for (int dz = -R; dz <= R; ++dz)
@@ -404,34 +407,51 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
       }
     nrow = k;
   }
-  for (int i = threadIdx.x; i < hx * hy * hz; i += blockDim.x) {
-    const int cz = i / (hx * hy), rem = i - cz * hx * hy;
-    const int cy = rem / hx, cx = rem - cy * hx;
-    const int gz = z0 - R + cz, gy = y0 - R + cy, gx = x0 - R + cx;
-    const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
-                    (unsigned)gx < (unsigned)nx;
-    const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
-    sW[(cz * SY + cy) * kBiPS + cx] =
-        ok ? ((uint32_t)__ldg(L + g) | ((uint32_t)__ldg(I16 + g) << 16)) : 0xffffu;
+  // halo rows (cz, cy) x hx cells; one row per warp pass keeps the loads coalesced
+  for (int row = threadIdx.x >> 5; row < hy * hz; row += 8) {
+    const int cz = row / hy, cy = row - cz * hy;
+    const int gz = z0 - R + cz, gy = y0 - R + cy;
+    const int cx = threadIdx.x & 31;
+    if (cx < hx) {
+      const int gx = x0 - R + cx;
+      const bool ok = (unsigned)gz < (unsigned)nz && (unsigned)gy < (unsigned)ny &&
+                      (unsigned)gx < (unsigned)nx;
+      const int64_t g = ((int64_t)gz * ny + gy) * nx + gx;
+      sW[(cz * SY + cy) * kBiPS + cx] =
+          ok ? ((uint32_t)__ldg(L + g) | ((uint32_t)__ldg(I16 + g) << 16)) : 0xffffu;
+    }
   }
   if (band)
     for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
   __syncthreads();
-  const int cbase = ((tz + R) * SY + (ty + R)) * kBiPS + tx + R;
-  const uint32_t wc = sW[cbase];
-  const int own = inside ? (int)(wc & 0xffffu) : 0x7fffffff;
-  bool todo = inside;
-  uint32_t tot = 0;
+  int cb[kBiS], own[kBiS];
+  uint32_t tot[kBiS], wc[kBiS];
+  bool todo[kBiS], inside[kBiS];
+#pragma unroll
+  for (int j = 0; j < kBiS; ++j) {
+    const int zl = tz + kBiZT * j;
+    cb[j] = ((zl + R) * SY + (ty + R)) * kBiPS + tx + R;
+    wc[j] = sW[cb[j]];
+    inside[j] = x < nx && y < ny && z0 + zl < nz;
+    own[j] = inside[j] ? (int)(wc[j] & 0xffffu) : 0x7fffffff;
+    todo[j] = inside[j];
+    tot[j] = 0;
+  }
   for (;;) {  // one pass per label among the tile's own sites, smallest first
     if (threadIdx.x == 0) s_pick = 0x7fffffff;
     __syncthreads();
-    const int wmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)(todo ? own : 0x7fffffff));
+    int mine = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < kBiS; ++j)
+      if (todo[j] && own[j] < mine) mine = own[j];
+    const int wmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)mine);
     if ((threadIdx.x & 31) == 0 && wmin != 0x7fffffff) atomicMin(&s_pick, wmin);
     __syncthreads();
     const int l = s_pick;
     if (l == 0x7fffffff) break;
-    if (threadIdx.x < hy * hz) {  // this row's prefix sums over the cells of label l
-      const int cz = threadIdx.x / hy, cy = threadIdx.x - cz * hy;
+    for (int row = threadIdx.x; row < hy * hz; row += blockDim.x) {
+      // this row's prefix sums over the cells of label l
+      const int cz = row / hy, cy = row - cz * hy;
       const int rb = (cz * SY + cy) * kBiPS;
       uint32_t a = 0;
       sP[rb] = 0;
@@ -443,42 +463,78 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
       }
     }
     __syncthreads();
-    if (todo && own == l) {
+    bool any_mine = false;
+#pragma unroll
+    for (int j = 0; j < kBiS; ++j) any_mine |= todo[j] && own[j] == l;
+    if (any_mine) {
       const int nr = nrow;
-      uint32_t t0 = 0, t1 = 0;
-      int k = 0;
-      for (; k + 1 < nr; k += 2) {
-        const int2 r0 = srow[k], r1 = srow[k + 1];
-        t0 += sP[cbase + r0.x] - sP[cbase + r0.y];
-        t1 += sP[cbase + r1.x] - sP[cbase + r1.y];
+      uint32_t t[kBiS];
+#pragma unroll
+      for (int j = 0; j < kBiS; ++j) t[j] = 0;
+      for (int k = 0; k < nr; ++k) {
+        const int2 r = srow[k];
+#pragma unroll
+        for (int j = 0; j < kBiS; ++j) t[j] += sP[cb[j] + r.x] - sP[cb[j] + r.y];
       }
-      if (k < nr) {
-        const int2 r0 = srow[k];
-        t0 += sP[cbase + r0.x] - sP[cbase + r0.y];
-      }
-      tot = t0 + t1;
-      todo = false;
+#pragma unroll
+      for (int j = 0; j < kBiS; ++j)
+        if (todo[j] && own[j] == l) {
+          tot[j] = t[j];
+          todo[j] = false;
+        }
     }
   }
-  double oldr = 0.0, newr = 0.0;
-  bool changed = false;
-  if (inside) {
-    const int32_t c = (int32_t)(tot >> 20);
-    const double sv = (double)(tot & 0xfffffu);
-    changed = !tflag || Cown[f] != c || Sown[f] != sv;
-    if (changed) {
-      if (band) oldr = rho0[f];
-      Cown[f] = c;
-      Sown[f] = sv;
-      newr = rho((double)(wc >> 16), sv / (double)c, poisson);
-      if (rho0) rho0[f] = newr;
+  AccStage stage;
+#pragma unroll
+  for (int j = 0; j < kBiS; ++j) {
+    double oldr = 0.0, newr = 0.0;
+    bool changed = false;
+    if (inside[j]) {
+      const int64_t f = ((int64_t)(z0 + tz + kBiZT * j) * ny + y) * nx + x;
+      const int32_t c = (int32_t)(tot[j] >> 20);
+      const double sv = (double)(tot[j] & 0xfffffu);
+      changed = !tflag || Cown[f] != c || Sown[f] != sv;
+      if (changed) {
+        if (band) oldr = rho0[f];
+        Cown[f] = c;
+        Sown[f] = sv;
+        newr = rho((double)(wc[j] >> 16), sv / (double)c, poisson);
+        if (rho0) rho0[f] = newr;
+      }
+    }
+    if (band && changed) {
+      stage.add(sm, -oldr);
+      stage.add(sm, newr);
     }
   }
   if (band) {  // every thread of the block reaches here (warp-uniform)
-    acc_add_warp(sm, -oldr, changed);
-    acc_add_warp(sm, newr, changed);
+    stage.flush_warp(sm);
     acc_flush(sm, band);
   }
+}
+
+static size_t band3d_int_smem() {
+  return 2 * (size_t)(kBiZ + 2 * kT3R) * (kBiY + 2 * kT3R) * kBiPS * sizeof(uint32_t);
+}
+
+static int32_t launch_band3d_int(const int32_t *L, const uint16_t *I16, const Lat &lat, int R,
+                                 const uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0,
+                                 int poisson, long long *band, cudaStream_t s) {
+  static bool attr[64] = {};
+  int dev = 0;
+  RCB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    RCB_CUDA(cudaFuncSetAttribute(k_fields_band3d_int, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)band3d_int_smem()));
+    attr[dev] = true;
+  }
+  dim3 grid((unsigned)((lat.nx + kBiX - 1) / kBiX), (unsigned)((lat.ny + kBiY - 1) / kBiY),
+            (unsigned)((lat.nz + kBiZ - 1) / kBiZ));
+  k_fields_band3d_int<<<grid, 256, band3d_int_smem(), s>>>(L, I16, (int)lat.nx, (int)lat.ny,
+                                                           (int)lat.nz, R, tflag, Cown, Sown, rho0,
+                                                           poisson, band);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
 }
 
 __global__ void k_to_u16(const double *__restrict__ src, int64_t n, uint16_t *__restrict__ dst) {
@@ -496,7 +552,7 @@ int32_t image_u16(const double *I, int64_t V, uint16_t *I16, cudaStream_t s) {
 // per accepted move: flips[x] = v, tflag[tile(x)] = v (v = 1 mark, 0 clear)
 __global__ void k_mark_flips(const int64_t *__restrict__ acc, const int64_t *__restrict__ moves,
                              Lat lat, uint8_t v, uint8_t *__restrict__ flips,
-                             uint8_t *__restrict__ tflag) {
+                             uint8_t *__restrict__ tflag, int kT3X, int kT3Y, int kT3Z) {
   const int64_t n = *moves;
   const int ntx = (int)((lat.nx + kT3X - 1) / kT3X), nty = (int)((lat.ny + kT3Y - 1) / kT3Y);
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
@@ -504,7 +560,7 @@ __global__ void k_mark_flips(const int64_t *__restrict__ acc, const int64_t *__r
     const int64_t f = acc[3 * k];
     int64_t z, y, x;
     lat.coord(f, z, y, x);
-    flips[f] = v;
+    if (flips) flips[f] = v;
     tflag[((z / kT3Z) * nty + y / kT3Y) * ntx + x / kT3X] = v;
   }
 }
@@ -518,18 +574,22 @@ int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L
                       const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
                       int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, long long *band, cudaStream_t s) {
-  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, flips, tflag);
+  if (I16) {
+    // integer image: prefix-sum ball runs on 16 x 8 x 8 tiles (the caller
+    // checked the ranges); only the tile flags are marked, no per-site map
+    k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, nullptr, tflag, kBiX, kBiY, kBiZ);
+    RCB_TRY(launch_band3d_int(L, I16, lat, R, tflag, Cown, Sown, rho0, poisson, band, s));
+    k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, nullptr, tflag, kBiX, kBiY, kBiZ);
+    RCB_CUDA(cudaGetLastError());
+    return RCB_OK;
+  }
+  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, flips, tflag, kT3X, kT3Y, kT3Z);
   dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
             (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
-  if (I16)  // integer image: prefix-sum ball runs (the caller checked the ranges)
-    k_fields_band3d_int<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I16, (int)lat.nx, (int)lat.ny,
-                                                             (int)lat.nz, R, tflag, Cown, Sown,
-                                                             rho0, poisson, band);
-  else
   k_fields_band3d<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, (int)lat.nz,
                                                        ball_full, nball_full, R, flips, tflag,
                                                        Cown, Sown, rho0, poisson, band);
-  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, flips, tflag);
+  k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, flips, tflag, kT3X, kT3Y, kT3Z);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -898,15 +958,8 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
       }
     }
     if (R > 0 && fields_tile3d_ok(lat, R, nball_full)) {
-      if (I16 && rho0) {  // integer image: prefix-sum ball runs over every tile
-        dim3 grid((unsigned)((lat.nx + kT3X - 1) / kT3X), (unsigned)((lat.ny + kT3Y - 1) / kT3Y),
-                  (unsigned)((lat.nz + kT3Z - 1) / kT3Z));
-        k_fields_band3d_int<<<grid, kT3X * kT3Y * kT3Z, 0, s>>>(L, I16, (int)lat.nx, (int)lat.ny,
-                                                                 (int)lat.nz, R, nullptr, Cown,
-                                                                 Sown, rho0, poisson, nullptr);
-        RCB_CUDA(cudaGetLastError());
-        return RCB_OK;
-      }
+      if (I16 && rho0)  // integer image: prefix-sum ball runs over every tile
+        return launch_band3d_int(L, I16, lat, R, nullptr, Cown, Sown, rho0, poisson, nullptr, s);
       return fields_tile3d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson,
                            nullptr, s);
     }
