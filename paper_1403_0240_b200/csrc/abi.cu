@@ -263,6 +263,7 @@ struct rcb_engine {
   // order, so instead of keeping per-iteration move lists (up to 12 GB at
   // cfg4) the statistics are rebuilt from the raster when read
   bool int_image = false;
+  bool srec_current = false;  // srec matches L / Cown / Sown / rho0 (kept so by the integer band refresh)
   bool stats_stale = false;
   bool ps_tiles = false;  // K5 on shared-memory tiles (RCB_K5=tile; measured slower)
 
@@ -712,8 +713,11 @@ static int32_t engine_score(rcb_engine *e) {
                                e->sb0.p, e->logt_P ? e->logt.p : nullptr, e->logt_P, s));
     else if (e->thetat_P && e->rho0.p && e->ecfg.noise_model == 1) {
       // integer Poisson data: one 16-byte record per ball site (k_delta_ps_rec)
+      const int4 *const srec_old = e->srec.p;
       RCB_TRY(e->srec.reserve(lat.V, s));
-      RCB_TRY(pack_sites(e->L.p, e->Cown.p, e->Sown.p, e->I.p, e->rho0.p, lat.V, e->srec.p, s));
+      if (!e->srec_current || e->srec.p != srec_old || getenv("RCB_PACK_ALWAYS"))
+        RCB_TRY(pack_sites(e->L.p, e->Cown.p, e->Sown.p, e->I.p, e->rho0.p, lat.V, e->srec.p, s));
+      e->srec_current = false;  // until this iteration's band refresh says otherwise
       RCB_TRY(delta_ps_rec(e->srec.p, e->I.p, lat, e->ball.p, e->nball, e->px.p + h0,
                            e->pown.p + h0, e->pcomp.p + h0, m, e->raw.p + h0, e->rho0.p,
                            e->cb0.p + h0, e->sb0.p + h0, e->thetat.p, e->thetat_P, pkh, s));
@@ -729,10 +733,9 @@ static int32_t engine_score(rcb_engine *e) {
         RCB_TRY(sobolev_lattice32(e->site_off.p, e->pown.p, e->px.p, e->pcomp.p, e->raw32.p, lat,
                                   e->st.p, e->nst, e->wt32.p, p1, e->smooth.p, &d->pairs, s, p0));
       } else if (e->sob_site && pk_direct) {
-        if (p0 == 0 && p1 == n && h0 == 0 && h1 == n)  // the whole list: TMA-staged pass
-          RCB_TRY(sobolev_site_bulk(e->pk.p, e->w0, n, e->smooth.p, &d->pairs, s));
-        else
-          RCB_TRY(sobolev_site_pk(e->pk.p, e->w0, p0, p1, h0, h1, e->smooth.p, &d->pairs, s));
+        // register-staged vector loads (measured faster than the TMA ring of
+        // sobolev_site_bulk at every size, profiles/README.md)
+        RCB_TRY(sobolev_site_pk(e->pk.p, e->w0, p0, p1, h0, h1, e->smooth.p, &d->pairs, s));
       } else if (e->sob_site) {
         RCB_TRY(sobolev_site(e->px.p, e->pown.p, e->pcomp.p, e->raw.p, e->w0, p0, p1, h0, h1,
                              e->smooth.p, &d->pairs, s));
@@ -851,6 +854,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.wp_first = !(wf && wf[0] == '0');
         const char *nw = getenv("RCB_DF_NOWAIT");  // timing experiment: wrong results
         P.nowait = nw && nw[0] == '1';
+        const char *in = getenv("RCB_DF_IDLE_NS");
+        P.idle_ns = in ? atoi(in) : 2000;
         const char *ha = getenv("RCB_DF_HELPAFTER");
         P.help_after = ha ? atoi(ha) : 0;
         const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs
@@ -1007,6 +1012,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.labbounds = &e->labbounds;
       X.tflag = &e->tflag;
       X.I16 = e->I16.p;
+      X.srec = e->srec.p;  // null unless K5 reads packed site records
+      X.srec_current = &e->srec_current;
       X.chain_pool = &e->chain_pool;
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
@@ -1207,6 +1214,7 @@ int32_t rcb_engine_set_labels(rcb_engine *e, const int32_t *labels) {
     if (labels[i] < 0 || labels[i] >= e->nl)
       return fail(RCB_ERR_VALUE, "labels outside the engine's label table");
   e->fields_fresh = false;
+  e->srec_current = false;
   RCB_CUDA(cudaMemcpyAsync(e->L.p, labels, sizeof(int32_t) * e->lat.V, cudaMemcpyHostToDevice, e->s));
   RCB_TRY(e->components());
   RCB_TRY(e->prepare());
@@ -1234,6 +1242,7 @@ int32_t rcb_engine_undo_last(rcb_engine *e) {
   }
   e->last_moves = 0;
   e->fields_fresh = false;
+  e->srec_current = false;
   RCB_TRY(e->components());
   RCB_TRY(e->prepare());
   return RCB_OK;
@@ -1313,6 +1322,7 @@ int32_t rcb_engine_refresh(rcb_engine *e) {
   RCB_TRY(e->refresh());
   RCB_CUDA(cudaStreamSynchronize(e->s));
   e->fields_fresh = true;
+  e->srec_current = false;  // the rebuild rewrote Cown / Sown / rho0
   return RCB_OK;
 }
 

@@ -2649,7 +2649,7 @@ __device__ void warp_idle_help(const ParArgs &A) {
     if (warp_help(A)) continue;
     const int idle = __shfl_sync(0xffffffffu, lane == 0 ? ld_rlx(A.ctl + 11) : 0, 0);
     if (idle >= nwarps || df_aborted(A)) return;
-    __nanosleep(2000);
+    __nanosleep(A.idle_ns);
   }
 }
 
@@ -4673,7 +4673,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (fresh) RCB_CUDA(cudaMemsetAsync(X.tflag->p, 0, X.tflag->cap, s));
     RCB_TRY(fields_band3d(X.acc, X.moves, X.Lmut, X.I, X.I16, A.lat, X.ball_full, X.nball_full, X.radius,
                           X.dirty, X.tflag->p, X.Cown, X.Sown, X.rho0, X.poisson,
-                          band_ledger ? X.band : nullptr, s));
+                          band_ledger ? X.band : nullptr, s, X.srec));
+    if (X.I16 && X.srec && X.rho0 && X.srec_current) *X.srec_current = true;
     nl += 3;
     if (band_ledger) {
       if (X.lam != 0.0) k_dint_sum<<<grid_for(N, 256), 256, 0, s>>>(A, X.moves, X.band);

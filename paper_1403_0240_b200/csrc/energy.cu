@@ -370,7 +370,7 @@ static constexpr int kBiPS = kBiX + 2 * kT3R + 1;  // row stride (odd: conflict-
 __global__ void __launch_bounds__(256) k_fields_band3d_int(
     const int32_t *__restrict__ L, const uint16_t *__restrict__ I16, int nx, int ny, int nz, int R,
     const uint8_t *__restrict__ tflag, int32_t *__restrict__ Cown, double *__restrict__ Sown,
-    double *__restrict__ rho0, int poisson, long long *__restrict__ band) {
+    double *__restrict__ rho0, int poisson, long long *__restrict__ band, int4 *__restrict__ rec) {
   constexpr int SY = kBiY + 2 * kT3R, SZ = kBiZ + 2 * kT3R;
   extern __shared__ __align__(16) uint32_t bi_smem[];
   uint32_t *sW = bi_smem;                   // label | I << 16 (0xffff: outside the lattice)
@@ -493,13 +493,27 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
       const int64_t f = ((int64_t)(z0 + tz + kBiZT * j) * ny + y) * nx + x;
       const int32_t c = (int32_t)(tot[j] >> 20);
       const double sv = (double)(tot[j] & 0xfffffu);
-      changed = !tflag || Cown[f] != c || Sown[f] != sv;
+      // K5's packed site record (k_pack_sites' layout) is kept current here,
+      // so the energy kernel needs no packing pass over the lattice: a site
+      // whose label, count or sum changed is exactly one whose record did
+      const uint32_t w0 = (uint32_t)own[j] | ((uint32_t)c << 16);
+      const uint32_t w1 = (tot[j] & 0xfffffu) | ((wc[j] >> 16) << 20);
+      if (rec) {
+        const int2 old = __ldg(reinterpret_cast<const int2 *>(rec + f));
+        changed = !tflag || (uint32_t)old.x != w0 || (uint32_t)old.y != w1;
+      } else {
+        changed = !tflag || Cown[f] != c || Sown[f] != sv;
+      }
       if (changed) {
         if (band) oldr = rho0[f];
         Cown[f] = c;
         Sown[f] = sv;
         newr = rho((double)(wc[j] >> 16), sv / (double)c, poisson);
         if (rho0) rho0[f] = newr;
+        if (rec) {
+          const unsigned long long rb = (unsigned long long)__double_as_longlong(newr);
+          rec[f] = make_int4((int)w0, (int)w1, (int)(uint32_t)rb, (int)(uint32_t)(rb >> 32));
+        }
       }
     }
     if (band && changed) {
@@ -519,7 +533,7 @@ static size_t band3d_int_smem() {
 
 static int32_t launch_band3d_int(const int32_t *L, const uint16_t *I16, const Lat &lat, int R,
                                  const uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0,
-                                 int poisson, long long *band, cudaStream_t s) {
+                                 int poisson, long long *band, int4 *rec, cudaStream_t s) {
   static bool attr[64] = {};
   int dev = 0;
   RCB_CUDA(cudaGetDevice(&dev));
@@ -532,7 +546,7 @@ static int32_t launch_band3d_int(const int32_t *L, const uint16_t *I16, const La
             (unsigned)((lat.nz + kBiZ - 1) / kBiZ));
   k_fields_band3d_int<<<grid, 256, band3d_int_smem(), s>>>(L, I16, (int)lat.nx, (int)lat.ny,
                                                            (int)lat.nz, R, tflag, Cown, Sown, rho0,
-                                                           poisson, band);
+                                                           poisson, band, rho0 ? rec : nullptr);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -573,12 +587,12 @@ int64_t band3d_tiles(const Lat &lat) {
 int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
                       const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
                       int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
-                      double *rho0, int poisson, long long *band, cudaStream_t s) {
+                      double *rho0, int poisson, long long *band, cudaStream_t s, int4 *rec) {
   if (I16) {
     // integer image: prefix-sum ball runs on 16 x 8 x 8 tiles (the caller
     // checked the ranges); only the tile flags are marked, no per-site map
     k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, nullptr, tflag, kBiX, kBiY, kBiZ);
-    RCB_TRY(launch_band3d_int(L, I16, lat, R, tflag, Cown, Sown, rho0, poisson, band, s));
+    RCB_TRY(launch_band3d_int(L, I16, lat, R, tflag, Cown, Sown, rho0, poisson, band, rec, s));
     k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, nullptr, tflag, kBiX, kBiY, kBiZ);
     RCB_CUDA(cudaGetLastError());
     return RCB_OK;
@@ -959,7 +973,8 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
     }
     if (R > 0 && fields_tile3d_ok(lat, R, nball_full)) {
       if (I16 && rho0)  // integer image: prefix-sum ball runs over every tile
-        return launch_band3d_int(L, I16, lat, R, nullptr, Cown, Sown, rho0, poisson, nullptr, s);
+        return launch_band3d_int(L, I16, lat, R, nullptr, Cown, Sown, rho0, poisson, nullptr,
+                                 nullptr, s);
       return fields_tile3d(L, I, lat, ball_full, nball_full, R, nullptr, Cown, Sown, rho0, poisson,
                            nullptr, s);
     }

@@ -102,6 +102,7 @@ struct ParArgs {
   int win_r;        // dataflow window radius in 2-D (0: default 5; 1: none)
   int wp_first;     // publish the site word before the decision's release fence (RCB_DF_WPFIRST=0: after)
   int help_after;   // settled waits look for assist jobs only after this many polls (RCB_DF_HELPAFTER)
+  int idle_ns;      // poll interval of finished warps waiting for assist jobs
   int nowait;       // timing experiment only (RCB_DF_NOWAIT=1): ignore box dependencies, results are wrong
   int win5;         // 3-D: 5^3 window tier before the 9^3 window (RCB_DF_WIN5=0 turns it off)
   int max_insert;   // dataflow warp-BFS footprint cap (0: default)
@@ -167,6 +168,8 @@ struct ParExtra {
   uint8_t *dirty;
   DBuf<uint8_t> *tflag = nullptr;  // 3-D band refresh: per-tile flip flags (zero between uses)
   const uint16_t *I16 = nullptr;   // integer image, 16 bits per site (integer band refresh), or null
+  int4 *srec = nullptr;            // K5's packed site records, kept current by the integer band refresh
+  bool *srec_current = nullptr;    // set when the band refresh left srec current
   int32_t *Cown;
   double *Sown;
   double *rho0;
@@ -252,7 +255,8 @@ int64_t band3d_tiles(const Lat &lat);
 int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
                       const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
                       int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
-                      double *rho0, int poisson, long long *band, cudaStream_t s);
+                      double *rho0, int poisson, long long *band, cudaStream_t s,
+                      int4 *rec = nullptr);
 // integer image as 16-bit words (the integer band refresh reads 2 B per site)
 int32_t image_u16(const double *I, int64_t V, uint16_t *I16, cudaStream_t s);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,
