@@ -50,7 +50,7 @@ UNIT = "particle-interactions/s"
 DRIFT_TOL = 1e-3
 WORKLOAD = ("cfg4: 3-D 512^3 PS/Poisson R=4, Sobolev w=3 (E=6), 64 ellipsoids, blur 1.5, "
             "Poisson peak 30, bubbles 8x8x8 r=15; timed iterations W+1..W+K")
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_traffic_cfg4.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02b_traffic_cfg4.json")
 
 
 def _dist():
@@ -301,14 +301,18 @@ def run_ours(args):
                 "k5_ms_per_iteration": k5_ms / args.steps,
                 "k6_ms_per_iteration": k6_ms / args.steps,
                 "particles_per_iteration": particles / args.steps,
-                "kernels": "K5 PS energy (k_delta_ps3d) + K6 Sobolev (k_sob_pack + "
-                           "k_sobolev_pk): SURVEY §8(d) bytes 29N + 24B_R + 28N per iteration "
-                           "over the same window, timed by CUDA events on the engine stream; "
-                           "traffic = ncu dram bytes of K5+K6 per iteration "
+                "kernels": "K5 PS energy (k_delta_ps_rec over packed site records kept current "
+                           "by the band refresh; k_pack_sites only after a full rebuild; "
+                           "k_delta_int) + K6 Sobolev (k_sobolev_pk over the records K5 writes): "
+                           "SURVEY §8(d) bytes 29N + 24B_R + 28N per iteration over the same "
+                           "window, timed by CUDA events on the engine stream; traffic = ncu dram "
+                           "bytes of these kernels per iteration "
                            f"({os.path.relpath(TRAFFIC_FILE, ROOT)})",
-                "other_bounds": "K5 evaluates one fp64 log and one division per ball hit "
-                                "(FP64 issue bound, ncu); K6 at w=3 in 3-D visits 93 stencil "
-                                "sites per particle (issue bound)",
+                "other_bounds": "K5 is bound by the L1 tag stage (ncu: L1/TEX throughput 81 %, "
+                                "DRAM 1.4 %): every ball hit gathers one 16-byte site record and "
+                                "one 16-byte {theta, log theta} table entry (6.9e9 tag requests "
+                                "per iteration, L2 hit rate 98 %); K6 at w=3 in 3-D visits 93 "
+                                "stencil sites per particle (issue bound)",
                 "dominant": {"phase": "accept (K8 v3 dataflow + band refresh + ledger)",
                              "share": float(shares[4]),
                              "bound": "latency (dependency waits, BFS), not bandwidth"}}

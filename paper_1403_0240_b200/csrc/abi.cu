@@ -853,7 +853,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         const char *wf = getenv("RCB_DF_WPFIRST");  // comparison runs
         P.wp_first = !(wf && wf[0] == '0');
         const char *nw = getenv("RCB_DF_NOWAIT");  // timing experiment: wrong results
-        P.nowait = nw && nw[0] == '1';
+        P.nowait = nw ? atoi(nw) : 0;  // bit 0: no dependency waits; bit 1: an extra raster read per box cell
         const char *in = getenv("RCB_DF_IDLE_NS");
         P.idle_ns = in ? atoi(in) : 2000;
         const char *ha = getenv("RCB_DF_HELPAFTER");

@@ -1699,15 +1699,23 @@ __global__ void k_q_reset(ParArgs A) {
 // Warp-level wait until every lane's site g (or -1) is settled for V_pos (no
 // candidate before pos pending there); helps the current job meanwhile.
 // Returns this lane's packed site word.
+// pre: v0 is the lane's site word loaded earlier (the box prefetch).  A word
+// that shows pend >= pos is final for V_pos whenever it was read (pend only
+// grows, and no candidate before pos can flip the site any more), so only the
+// lanes still pending load again.
 __device__ __forceinline__ unsigned long long warp_wait_settled(const ParArgs &A, int64_t g,
-                                                                int32_t pos) {
+                                                                int32_t pos,
+                                                                unsigned long long v0 = 0,
+                                                                bool pre = false) {
   int ns = 32;
-  unsigned long long v = 0;
+  unsigned long long v = v0;
   unsigned long long t0 = 0;
   int polls = 0;
+  bool load = !pre;
   for (;;) {
-    if (g >= 0) v = ld_rlx64(A.wp + g);
-    const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos && !A.nowait;
+    if (g >= 0 && load) v = ld_rlx64(A.wp + g);
+    const bool p = g >= 0 && wp_pend((uint32_t)A.wp_bits, v) < pos && !(A.nowait & 1);
+    load = p;
     if (!__any_sync(0xffffffffu, p)) break;
     // short waits (the common case: a box neighbour a few positions earlier
     // is being decided) only poll the site words; the assist-job word joins
@@ -2828,6 +2836,41 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
   // a position held behind a warp stuck in a long BFS stalls its dependants.
   int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
   int4 rc = pos < M ? __ldg(A.rec + pos) : make_int4(0, 0, 0, 0);
+  const bool is3 = lat.ndim == 3;
+  // The box of the NEXT position is loaded while the current decision is
+  // published (its labels L are static, and a site word that already shows
+  // pend >= next position is final): the ~1 us box round trip leaves the
+  // critical path of every candidate.  Coordinates by multiply-shift
+  // (f < 2^31; magic numbers from the host) instead of two 32-bit divisions.
+  int cz = 0, cy = 0, cx = 0;
+  int32_t pl0 = -1;
+  unsigned long long ppk = 0;
+  auto box_site = [&](int z, int y, int x) -> int64_t {
+    int64_t g = -1;
+    if (lane < 27) {
+      const int dz = lane / 9 - 1, zz = z + dz, yy = y + (lane / 3) % 3 - 1, xx = x + lane % 3 - 1;
+      if ((is3 || dz == 0) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
+          (unsigned)xx < (unsigned)nx)
+        g = ((int64_t)zz * ny + yy) * nx + xx;
+    }
+    return g;
+  };
+  auto prefetch_box = [&](int32_t f, int32_t p) {
+    if (p >= M) return;
+    const uint32_t uf = (uint32_t)f;
+    cz = is3 ? (int)((__umulhi(A.div_mxy, uf) + uf) >> A.div_lxy) : 0;
+    const uint32_t fr = uf - (uint32_t)cz * (uint32_t)(nx * ny);
+    cy = (int)((__umulhi(A.div_mx, fr) + fr) >> A.div_lx);
+    cx = (int)(fr - (uint32_t)cy * (uint32_t)nx);
+    const int64_t g = box_site(cz, cy, cx);
+    pl0 = g >= 0 ? __ldg(A.L + g) : -1;
+    ppk = g >= 0 ? ld_rlx64(A.wp + g) : 0ull;
+    if (A.nowait & 2) {  // timing experiment: one more scattered raster read per box cell
+      const int32_t dummy = g >= 0 ? __ldcg(A.w + g) : 0;
+      if (dummy == 0x12345678) pl0 = -2;
+    }
+  };
+  prefetch_box(rc.x, pos);
   for (;;) {
     if (pos >= M) {
       // stay as a helper for assist jobs until every position is decided,
@@ -2847,20 +2890,12 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
     // the topology tests (those need settled footprints, not the statistics)
     if (sa && !A.l2) warp_wait_label(A, a, pos);
     if (sb && !A.l2) warp_wait_label(A, b, pos);
-    const bool is3 = lat.ndim == 3;
-    const int nxy = nx * ny;
-    const int z = is3 ? f / nxy : 0, frem = f - z * nxy;
-    const int y = frem / nx, x = frem - y * nx;
-    // the 3^d box, one cell per lane in the 3^3 layout of lab[] (13 = x)
-    int64_t gb = -1;
-    if (lane < 27) {
-      const int dz = lane / 9 - 1, zz = z + dz, yy = y + (lane / 3) % 3 - 1, xx = x + lane % 3 - 1;
-      if ((is3 || dz == 0) && (unsigned)zz < (unsigned)nz && (unsigned)yy < (unsigned)ny &&
-          (unsigned)xx < (unsigned)nx)
-        gb = ((int64_t)zz * ny + yy) * nx + xx;
-    }
-    const int32_t l0 = gb >= 0 ? __ldg(A.L + gb) : -1;
-    const unsigned long long pk = warp_wait_settled(A, gb, pos);
+    const int z = cz, y = cy, x = cx;
+    // the 3^d box, one cell per lane in the 3^3 layout of lab[] (13 = x):
+    // labels and site words were loaded one position ahead
+    const int64_t gb = box_site(z, y, x);
+    const int32_t l0 = pl0;
+    const unsigned long long pk = warp_wait_settled(A, gb, pos, ppk, true);
     // the next position's record is in flight while this one is decided
     const int32_t npos = __shfl_sync(0xffffffffu, nclaim, 0);
     const int4 nrc = npos < M ? __ldg(A.rec + npos) : make_int4(0, 0, 0, 0);
@@ -3067,6 +3102,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
         }
       }
     }
+    prefetch_box(nrc.x, npos);  // in flight during the release fence below
     if (lane == 0) {
       // The site word first: it carries everything a dependant reads (next
       // pending position, flip position, new label), so the candidates
@@ -4396,6 +4432,15 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   const int64_t N = X.n_particles;
   if (A.max_insert <= 0 || A.max_insert > kMaxInsertW) A.max_insert = kMaxInsertW;
   if (A.box_cap < 0 || A.box_cap > 16 * kHW) A.box_cap = 16 * kHW;
+  {  // multiply-shift division of site indices (k_accept_df; sites < 2^31)
+    auto magic = [](uint32_t d, uint32_t &m, uint32_t &l) {
+      l = 0;
+      while ((1ull << l) < d) ++l;
+      m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    };
+    magic((uint32_t)(A.lat.nx * A.lat.ny), A.div_mxy, A.div_lxy);
+    magic((uint32_t)A.lat.nx, A.div_mx, A.div_lx);
+  }
   void *args[] = {&A};
   if (X.accept_mode == 1) {
     setup_lock.unlock();

@@ -102,6 +102,7 @@ struct ParArgs {
   int win_r;        // dataflow window radius in 2-D (0: default 5; 1: none)
   int wp_first;     // publish the site word before the decision's release fence (RCB_DF_WPFIRST=0: after)
   int help_after;   // settled waits look for assist jobs only after this many polls (RCB_DF_HELPAFTER)
+  uint32_t div_mxy, div_lxy, div_mx, div_lx;  // f / (nx * ny) and f / nx by multiply-shift (f < 2^31)
   int idle_ns;      // poll interval of finished warps waiting for assist jobs
   int nowait;       // timing experiment only (RCB_DF_NOWAIT=1): ignore box dependencies, results are wrong
   int win5;         // 3-D: 5^3 window tier before the 9^3 window (RCB_DF_WIN5=0 turns it off)

@@ -22,8 +22,14 @@ ki, mi, ui, vi = (h.index(k) for k in ("Kernel Name", "Metric Name", "Metric Uni
 iters = int(sys.argv[2])
 agg = collections.defaultdict(lambda: collections.defaultdict(float))
 launches = collections.Counter()
+import re  # noqa: E402
+
+# K5 + K6: the energy and Sobolev kernels of the window (argv[4]: another regex)
+KEEP = re.compile(sys.argv[4] if len(sys.argv) > 4 else r"k_delta_|k_pack_sites|k_sob_pack|k_sobolev")
 for r in rows[1:]:
     name = r[ki].split("(")[0].replace("void ", "").replace("rcb::", "")
+    if not KEEP.search(name):
+        continue
     v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
     agg[name][r[mi]] += v
     if r[mi] == "gpu__time_duration.sum":
@@ -37,7 +43,7 @@ doc = {"source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over 
        "kernels": kern,
        "energy_plus_sobolev_dram_bytes_per_iteration":
            sum(v["dram_bytes_per_iteration"] for v in kern.values())}
-out = sys.argv[3] if len(sys.argv) > 3 else "profiles/r02_traffic_cfg4.json"
+out = sys.argv[3] if len(sys.argv) > 3 else "profiles/r02b_traffic_cfg4.json"
 with open(out, "w") as fh:
     json.dump(doc, fh, indent=1)
 print(json.dumps(doc, indent=1))
