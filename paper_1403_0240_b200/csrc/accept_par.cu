@@ -4564,7 +4564,14 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   // 3-D PS: the per-move exact ledger terms cost moves x ball x nearby flips,
   // so the ledger takes the iteration's exact band change instead (see
   // k_refield_band); 2-D keeps the per-move terms of the reference's ledger
-  const bool band_ledger = X.region_ps && A.lat.ndim == 3 && X.rho0 && X.band;
+  // Round 2b: 2-D Poisson runs take the band ledger too (their ledger is
+  // compared at rtol 1e-12, CUDA's log differing from numpy's by an ulp): the
+  // per-move terms (flip index, k_ps_dtot2d, ordered chains) were ~25 % of a
+  // cfg2 iteration.  2-D Gauss keeps the per-move ledger (bit-exact energies).
+  static const bool permove2d = getenv("RCB_LEDGER_PERMOVE") != nullptr;
+  const bool band_ledger = X.region_ps && X.rho0 && X.band &&
+                           (A.lat.ndim == 3 || (A.lat.ndim == 2 && X.poisson && !permove2d &&
+                                                fields_tile2d_ok(A.lat, X.radius, X.nball_full)));
   if (X.region_ps && !band_ledger) {
     const int64_t rows = A.lat.nz * A.lat.ny;
     RCB_TRY(X.evkey->reserve(N, s));
@@ -4729,9 +4736,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
   } else if (X.region_ps) {
     k_mark_band<<<148 * 8, 256, 0, s>>>(X.acc, X.moves, A.lat, X.ball_full, X.nball_full, X.dirty);
     if (band_ledger) RCB_CUDA(cudaMemsetAsync(X.band, 0, sizeof(long long) * (kLimbs + 1), s));
-    if (!band_ledger && fields_tile2d_ok(A.lat, X.radius, X.nball_full))
+    if (fields_tile2d_ok(A.lat, X.radius, X.nball_full))
       RCB_TRY(fields_tile2d(X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius, X.dirty,
-                            X.Cown, X.Sown, X.rho0, X.poisson, s));
+                            X.Cown, X.Sown, X.rho0, X.poisson, s, band_ledger ? X.band : nullptr));
     else if (fields_tile3d_ok(A.lat, X.radius, X.nball_full) && (X.rho0 || !band_ledger))
       RCB_TRY(fields_tile3d(X.Lmut, X.I, A.lat, X.ball_full, X.nball_full, X.radius, X.dirty,
                             X.Cown, X.Sown, X.rho0, X.poisson, band_ledger ? X.band : nullptr, s));

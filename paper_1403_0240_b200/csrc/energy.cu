@@ -135,11 +135,13 @@ static constexpr int kTW = 32, kTH = 8, kTRmax = 15;
 __global__ void __launch_bounds__(256) k_fields_tile2d(
     const int32_t *__restrict__ L, const double *__restrict__ I, int nx, int ny,
     const Off *__restrict__ ball, int nball, int R, uint8_t *__restrict__ dirty,
-    int32_t *__restrict__ Cown, double *__restrict__ Sown, double *__restrict__ rho0, int poisson) {
+    int32_t *__restrict__ Cown, double *__restrict__ Sown, double *__restrict__ rho0, int poisson,
+    long long *__restrict__ band) {
   constexpr int SH = kTH + 2 * kTRmax, SW = kTW + 2 * kTRmax;
   __shared__ int32_t sL[SH * SW];
   __shared__ double sI[SH * SW];
   __shared__ int sofs[1024];
+  __shared__ long long sm[kLimbs];
   const int tx = threadIdx.x & (kTW - 1), ty = threadIdx.x / kTW;
   const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
   const int x = x0 + tx, y = y0 + ty;
@@ -158,23 +160,34 @@ __global__ void __launch_bounds__(256) k_fields_tile2d(
   }
   for (int k = threadIdx.x; k < nball; k += blockDim.x)
     sofs[k] = (int)ball[k].dy * SW + (int)ball[k].dx;
+  if (band)
+    for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) sm[k] = 0;
   __syncthreads();
-  if (!todo) return;
-  const int cidx = (ty + R) * SW + (tx + R);
-  const int32_t own = sL[cidx];
-  int32_t c = 0;
-  double sv = 0.0;
-  for (int k = 0; k < nball; ++k) {
-    const int j = cidx + sofs[k];
-    if (sL[j] == own) {
-      c += 1;
-      sv += sI[j];
+  double oldr = 0.0, newr = 0.0;
+  if (todo) {
+    const int cidx = (ty + R) * SW + (tx + R);
+    const int32_t own = sL[cidx];
+    int32_t c = 0;
+    double sv = 0.0;
+    for (int k = 0; k < nball; ++k) {
+      const int j = cidx + sofs[k];
+      if (sL[j] == own) {
+        c += 1;
+        sv += sI[j];
+      }
     }
+    if (band) oldr = rho0[f];
+    Cown[f] = c;
+    Sown[f] = sv;
+    newr = rho(sI[cidx], sv / (double)c, poisson);
+    if (rho0) rho0[f] = newr;
+    if (dirty) dirty[f] = 0;
   }
-  Cown[f] = c;
-  Sown[f] = sv;
-  if (rho0) rho0[f] = rho(sI[cidx], sv / (double)c, poisson);
-  if (dirty) dirty[f] = 0;
+  if (band) {  // exact band ledger (every thread of the block reaches here)
+    acc_add_warp(sm, -oldr, todo);
+    acc_add_warp(sm, newr, todo);
+    acc_flush(sm, band);
+  }
 }
 
 // 3-D variant: 16 x 4 x 4 site tiles with a halo of R <= 4 (24 x 12 x 12
@@ -627,10 +640,11 @@ bool fields_tile3d_ok(const Lat &lat, int R, int nball_full) {
 
 int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
-                      double *rho0, int poisson, cudaStream_t s) {
+                      double *rho0, int poisson, cudaStream_t s, long long *band) {
   dim3 grid((unsigned)((lat.nx + kTW - 1) / kTW), (unsigned)((lat.ny + kTH - 1) / kTH));
   k_fields_tile2d<<<grid, kTW * kTH, 0, s>>>(L, I, (int)lat.nx, (int)lat.ny, ball_full, nball_full,
-                                             R, dirty, Cown, Sown, rho0, poisson);
+                                             R, dirty, Cown, Sown, rho0, poisson,
+                                             rho0 ? band : nullptr);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }

@@ -246,7 +246,7 @@ int32_t ps_fields(const int32_t *L, const double *I, const Lat &lat, const Off *
                   double *rho0 = nullptr, int poisson = 0, const uint16_t *I16 = nullptr);
 int32_t fields_tile2d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,
-                      double *rho0, int poisson, cudaStream_t s);
+                      double *rho0, int poisson, cudaStream_t s, long long *band = nullptr);
 bool fields_tile2d_ok(const Lat &lat, int R, int nball_full);
 int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const Off *ball_full,
                       int nball_full, int R, uint8_t *dirty, int32_t *Cown, double *Sown,

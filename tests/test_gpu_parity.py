@@ -400,9 +400,10 @@ def test_parallel_acceptance_equals_sequential(P, which, monkeypatch):
             rec = eng.iterate()
             out.append((rec.moves, rec.energy, eng.last_accepted.copy(), eng.labels))
         runs.append(out)
-    # 3-D PS: the dataflow/rounds kernels keep the ledger with the exact band
-    # change per iteration, the sequential kernel with per-move terms
-    band = sc.region == "ps" and sc.image.ndim == 3
+    # 3-D PS and 2-D PS/Poisson: the dataflow/rounds kernels keep the ledger
+    # with the exact band change per iteration, the sequential kernel with
+    # per-move terms
+    band = sc.region == "ps" and (sc.image.ndim == 3 or sc.noise == "poisson")
     for other in runs[1:]:
         for it, (a, b) in enumerate(zip(runs[0], other)):
             assert a[0] == b[0], (which, it)
