@@ -864,6 +864,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.box_cap = bc ? atoi(bc) : -1;
         const char *qj = getenv("RCB_DF_QJOB");  // "0": a full union-find per deferred candidate
         P.qjob = !(qj && qj[0] == '0');
+        const char *qp = getenv("RCB_DF_PREREG");
+        P.qprereg = !(qp && qp[0] == '0');
         const char *ws = getenv("RCB_DF_WATCH_S");  // watchdog seconds (default 60)
         P.watch_ns = (unsigned long long)((ws ? atof(ws) : 60.0) * 1e9);
       }
@@ -920,8 +922,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       if (use_df) {
         if (!e->ufp.p) {
           RCB_TRY(e->ufq.reserve(lat.V, s));
-          RCB_TRY(e->qstate.reserve(2 * (size_t)e->nl, s));
-          RCB_CUDA(cudaMemsetAsync(e->qstate.p, 0, sizeof(unsigned long long) * 2 * e->nl, s));
+          RCB_TRY(e->qstate.reserve(3 * (size_t)e->nl, s));
+          RCB_CUDA(cudaMemsetAsync(e->qstate.p, 0, sizeof(unsigned long long) * 3 * e->nl, s));
           RCB_TRY(e->qmark.reserve(lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->ufq.p, 0xff, sizeof(unsigned long long) * lat.V, s));
           RCB_CUDA(cudaMemsetAsync(e->qmark.p, 0xff, sizeof(unsigned long long) * lat.V, s));
@@ -933,7 +935,7 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
           RCB_CUDA(cudaMemsetAsync(e->job.p, 0, sizeof(unsigned long long) * 64, s));
         }
         // registry of deferred candidates (cleared after each run by k_q_reset)
-        RCB_TRY(e->qlist.reserve(n, s));
+        RCB_TRY(e->qlist.reserve(2 * n, s));  // up-front registrations + the deferring warps' own
         RCB_TRY(e->qscr.reserve(n, s));
         P.ufq = e->ufq.p;
         P.qmark = e->qmark.p;

@@ -1502,6 +1502,10 @@ __device__ __forceinline__ unsigned long long job_chunks(int64_t n) {
 __device__ int warp_job_owner(const ParArgs &A, int32_t pos, int64_t f, int32_t a,
                                uint32_t *qbits) {
   const int lane = threadIdx.x & 31;
+  // labels that need assist jobs keep needing them (tails of thin bridges and
+  // tubes persist over iterations): from the next iteration on every
+  // candidate they own is registered up front (k_df_prereg)
+  if (lane == 0 && A.qprereg) A.qstate[2 * (size_t)A.nl + a] = 1ull;
   // 1. bring the Q-UF of label a up to V_pos, or rebuild it
   int need_uf = 0;
   uint32_t tag = 0, T = 0, S = 0;
@@ -2594,6 +2598,42 @@ __global__ void k_df_records(ParArgs A, int4 *__restrict__ rec) {
     }
     rec[pos] = make_int4((int32_t)f, (int32_t)((uint32_t)a | (A.small[a] ? 0x80000000u : 0u)),
                          (int32_t)((uint32_t)b | (A.small[b] ? 0x80000000u : 0u)), nxt);
+  }
+}
+
+// Registry of deferred candidates, filled up front for the labels whose
+// candidates deferred to assist jobs in an earlier iteration: every candidate
+// such a label owns joins Q before the dataflow starts.  The Q-UF of that
+// label (the union-find of a \ Q) is then built once per iteration -- a
+// registration arriving after a build (seq >= S) forced a rebuild for almost
+// every deferred candidate -- and is never invalidated by a member leaving
+// the label (only candidates flip, and they are all in Q); a deferred
+// candidate costs a scan of the flips since the last job plus the contracted
+// graph over Q instead of a union-find over the label's box.  Q may be any
+// superset of the deferred candidates: its sites are simply the ones the
+// query handles explicitly.
+__global__ void k_df_prereg(ParArgs A, const int4 *__restrict__ rec) {
+  const int32_t M = (int32_t)*A.nneg;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < M; pos += stride) {
+    const int4 rc = rec[pos];
+    const int32_t a = rc.y & 0x7fffffff;
+    if (a <= 0 || A.qstate[2 * (size_t)A.nl + a] == 0ull) continue;
+    // worth it only while the contracted graph over Q (26 items per
+    // registered site, ~0.1 ns each, for every deferred candidate) stays
+    // cheaper than the union-find rebuilds it avoids: cfg5's thin bridges
+    // (6-9e3 candidates in a 512^2 box: 0.43 -> 0.26 s per image) yes, cfg3's
+    // tube network (0.7-2.5e5 candidates in 128^3: measured 1.6x slower) no
+    {
+      const LabBox bx = grown_box(A, a);
+      const long long na = (long long)A.nown[a];
+      if (na > 16384 || 26ll * na > 2ll * (long long)bx.bd * bx.bh * bx.bw) continue;
+    }
+    const unsigned long long m = __ldcg(A.qmark + rc.x);
+    if ((uint32_t)m == (uint32_t)a) continue;  // another candidate of this site registered it
+    const uint32_t seq = (uint32_t)atomicAdd((unsigned long long *)(A.job + 40), 1ull);
+    A.qlist[seq] = (uint32_t)rc.x;
+    atomicMin(A.qmark + rc.x, ((unsigned long long)seq << 32) | (uint32_t)a);
   }
 }
 
@@ -4507,6 +4547,12 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     RCB_TRY(X.rec->reserve(N, s));
     k_df_records<<<grid_for(N, 256), 256, 0, s>>>(A, X.rec->p);
     A.rec = X.rec->p;
+    if (A.qprereg && A.qjob) {
+      k_df_prereg<<<grid_for(N, 256), 256, 0, s>>>(A, X.rec->p);
+      // every registration so far is published (job[41] = job[40])
+      RCB_CUDA(cudaMemcpyAsync(A.job + 41, A.job + 40, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToDevice, s));
+    }
     RCB_TRY(X.evkey->reserve(2 * N, s));
     RCB_TRY(X.evkey2->reserve(2 * N, s));
     RCB_TRY(X.labpos->reserve(2 * N, s));

@@ -114,8 +114,9 @@ struct ParArgs {
   unsigned long long *qmark;      // deferred-candidate registry: (seq << 32 | label) per site
   uint32_t *qlist;                // registered sites by sequence
   uint32_t *qscr;                 // assist-job scans: per-position neighbour masks
-  unsigned long long *qstate;     // per label: Q-UF tag | S << 32, position reached
+  unsigned long long *qstate;     // per label: Q-UF tag | S << 32, position reached; [2 nl + a]: label a ran assist jobs (sticky)
   int qjob;                       // 0: no registry (one full union-find per deferred candidate)
+  int qprereg;                    // register every candidate of job-prone labels up front (RCB_DF_PREREG=0: off)
   unsigned long long watch_ns;    // dataflow watchdog: longest single wait
   int l2, poisson;                // l2 mode (PC): every label sequenced, d_tot < 0 gate
   double lam;
