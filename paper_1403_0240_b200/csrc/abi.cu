@@ -856,6 +856,8 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
         P.nowait = nw ? atoi(nw) : 0;  // bit 0: no dependency waits; bit 1: an extra raster read per box cell
         const char *in = getenv("RCB_DF_IDLE_NS");
         P.idle_ns = in ? atoi(in) : 2000;
+        const char *lm = getenv("RCB_DF_LOWMARK_NS");
+        P.lowmark_ns = lm ? atoi(lm) : 1024;
         const char *ha = getenv("RCB_DF_HELPAFTER");
         P.help_after = ha ? atoi(ha) : 0;
         const char *mi = getenv("RCB_DF_MAXINSERT");  // tests: force assist jobs

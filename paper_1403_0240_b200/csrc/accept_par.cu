@@ -2420,7 +2420,7 @@ __device__ __forceinline__ void warp_wait_lowmark(const ParArgs &A, int32_t pos)
     if (m >= pos) break;
     if (!warp_help(A)) {
       __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
+      if (ns < A.lowmark_ns) ns <<= 1;
       if (df_watch(A, t0, pos, 2, m)) break;
     }
     const int32_t h = __shfl_sync(0xffffffffu, lane == 0 ? ld_acq(A.ctl + 13) : 0, 0);

@@ -103,6 +103,7 @@ struct ParArgs {
   int wp_first;     // publish the site word before the decision's release fence (RCB_DF_WPFIRST=0: after)
   int help_after;   // settled waits look for assist jobs only after this many polls (RCB_DF_HELPAFTER)
   uint32_t div_mxy, div_lxy, div_mx, div_lx;  // f / (nx * ny) and f / nx by multiply-shift (f < 2^31)
+  int lowmark_ns;   // longest poll interval of warps waiting for the low-water mark
   int idle_ns;      // poll interval of finished warps waiting for assist jobs
   int nowait;       // timing experiment only (RCB_DF_NOWAIT=1): ignore box dependencies, results are wrong
   int win5;         // 3-D: 5^3 window tier before the 9^3 window (RCB_DF_WIN5=0 turns it off)
