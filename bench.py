@@ -324,7 +324,9 @@ def run_ours(args):
         t32 = max_over_ranks(sum(w32["ms"]))
         fp32 = {"value": sum_over_ranks(float(w32["pairs"])) / (t32 / 1e3), "unit": UNIT,
                 "iterations_per_s": args.steps * ws / (t32 / 1e3),
-                "what": "same window, raw increments + Sobolev filter in fp32 (gradients rtol "
+                "what": "same window, fp32 gradient path: raw increments rounded to fp32 (on "
+                        "integer Poisson data they come from the table-driven fp64 energy kernel, "
+                        "faster than the fp32 ball gather) + Sobolev filter in fp32 (gradients rtol "
                         "1e-4, Dice >= 0.999: tests/test_gpu_fp32.py)"}
 
     # ---- end to end through the public API from host buffers ----------------

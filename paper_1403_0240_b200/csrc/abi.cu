@@ -698,7 +698,7 @@ static int32_t engine_score(rcb_engine *e) {
     if (fp32 && e->ecfg.region_model == 0)
       RCB_TRY(delta_pc32_batch(e->I32.p, e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m,
                                e->cnt.p, e->tot.p, poisson, e->raw32.p + h0, e->raw.p + h0, s));
-    else if (fp32)
+    else if (fp32 && !(e->thetat_P && e->rho0.p && e->ecfg.noise_model == 1))
       RCB_TRY(delta_ps32_batch(e->L.p, e->I32.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
                                e->px.p + h0, e->pown.p + h0, e->pcomp.p + h0, m, poisson,
                                e->raw32.p + h0, e->raw.p + h0, s, e->cb0.p + h0, e->sb0.p + h0));
@@ -721,6 +721,10 @@ static int32_t engine_score(rcb_engine *e) {
       RCB_TRY(delta_ps_rec(e->srec.p, e->I.p, lat, e->ball.p, e->nball, e->px.p + h0,
                            e->pown.p + h0, e->pcomp.p + h0, m, e->raw.p + h0, e->rho0.p,
                            e->cb0.p + h0, e->sb0.p + h0, e->thetat.p, e->thetat_P, pkh, s));
+      // fp32 mode on integer Poisson data: the table-driven fp64 kernel is
+      // faster than the fp32 five-array gather; its increments are rounded
+      // to fp32 for the fp32 Sobolev filter
+      if (fp32) RCB_TRY(to_float(e->raw.p + h0, m, e->raw32.p + h0, s));
       launches += 1;
     } else
       RCB_TRY(delta_ps_batch(e->L.p, e->I.p, e->Cown.p, e->Sown.p, lat, e->ball.p, e->nball,
