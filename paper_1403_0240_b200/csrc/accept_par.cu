@@ -1929,11 +1929,18 @@ __device__ __forceinline__ void unpack_c(uint32_t e, int &z, int &y, int &x) {
 // seeds: bit k of seedmask (3^3 layout, k != 13) is an a-cell of x's box;
 // sgrp[k] its group (box-local component, < 8)
 static constexpr int kBigLevels = 32;
+#ifndef RCB_BFS_INLINE
+#define RCB_BFS_INLINE
+#endif
+#ifndef RCB_BFS_U
+#define RCB_BFS_U 3
+#endif
+static constexpr int kBfsU = RCB_BFS_U;  // (site, neighbour) pairs in flight per lane
 // kBig: the bounding-box map and the frontiers live in the warp's slot of
 // global memory (labels whose grown box exceeds the shared-memory map; run
 // after the hash tier overflowed, before deferring to an assist job).
 template <bool kBox, bool k3D, bool kBig = false>
-__device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
+__device__ RCB_BFS_INLINE int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, int32_t a,
                         uint32_t seedmask, const uint8_t *sgrp, int ngrp, const LabBox bb) {
   const int lane = threadIdx.x & 31;
   Frontier F;
@@ -2040,14 +2047,16 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
   __syncwarp();
   int cur = 0;
   for (;;) {
-    // (frontier site, neighbour) pairs, three per lane with all their loads
-    // issued before any is used; lanes sharing a site coalesce
+    // (frontier site, neighbour) pairs, kBfsU per lane with all their loads
+    // issued before any is used; lanes sharing a site coalesce.  A level costs
+    // one memory round trip per 32 * kBfsU pairs (two with the global map of
+    // the large tier), so the batch width sets the speed of the long floods.
     const int n = S.nfr[cur], nxt = cur ^ 1;
-    for (int base = 0; base < kNb * n; base += 96) {
-      int t[3], li[3], g[3], zq[3], yq[3], xq[3];
-      bool ok[3];
+    for (int base = 0; base < kNb * n; base += 32 * kBfsU) {
+      int t[kBfsU], li[kBfsU], g[kBfsU], zq[kBfsU], yq[kBfsU], xq[kBfsU];
+      bool ok[kBfsU];
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < kBfsU; ++u) {
         const int p = base + 32 * u + lane;
         ok[u] = p < kNb * n;
         const int j = ok[u] ? p / kNb : 0, k = p - j * kNb;
@@ -2069,15 +2078,28 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
                 (unsigned)xq[u] < (unsigned)nx;
         t[u] = (zq[u] * ny + yq[u]) * nx + xq[u];
         li[u] = box_index(zq[u], yq[u], xq[u], ok[u]);
+      }
+      if (kBox) {  // the visited map: every word loaded before any is used
+        uint32_t nwv[kBfsU];
+#pragma unroll
+        for (int u = 0; u < kBfsU; ++u)
+          nwv[u] = !ok[u] ? 0u
+                   : kBig ? *(volatile uint32_t *)(nib + (li[u] >> 3))
+                          : nib[li[u] >> 3];
+#pragma unroll
+        for (int u = 0; u < kBfsU; ++u) {
+          if (!ok[u]) continue;
+          const int cg = (int)((nwv[u] >> (4 * (li[u] & 7))) & 15u);
+          if (cg) {
+            if (cg != 15 && cg - 1 != g[u]) atomicOr(&S.unions[g[u]], 1u << (cg - 1));
+            ok[u] = false;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBfsU; ++u) {
         if (ok[u]) {
-          if (kBox) {
-            const uint32_t nw = kBig ? *(volatile uint32_t *)(nib + (li[u] >> 3)) : nib[li[u] >> 3];
-            const int cg = (int)((nw >> (4 * (li[u] & 7))) & 15u);
-            if (cg) {
-              if (cg != 15 && cg - 1 != g[u]) atomicOr(&S.unions[g[u]], 1u << (cg - 1));
-              ok[u] = false;
-            }
-          } else {
+          if (!kBox) {
             uint32_t h = hash32((uint32_t)t[u]) & (kHW - 1);
             for (int probe = 0; probe < kHW; ++probe) {
               const unsigned long long cv = S.key[h];
@@ -2093,15 +2115,15 @@ __device__ int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos, int64_t f, in
           }
         }
       }
-      unsigned long long pk[3];
-      int32_t l0[3];
+      unsigned long long pk[kBfsU];
+      int32_t l0[kBfsU];
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < kBfsU; ++u) {
         pk[u] = ok[u] ? ld_rlx64(A.wp + t[u]) : ~0ull;
         l0[u] = ok[u] ? __ldg(A.L + t[u]) : -1;
       }
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < kBfsU; ++u) {
         if (!ok[u]) continue;
         if (wp_pend((uint32_t)A.wp_bits, pk[u]) < pos) {
           // skipped as not-a for now; remembered for resuming

@@ -55,3 +55,13 @@ print("total warp-ms fetch->decided", round(lat.sum() / 1e3, 1), " per-warp (236
 order = np.argsort(f)
 print("box histogram us [0,.5,1,1.5,2,3,5,10,20,50,100,1e9):",
       np.histogram(tb - f, bins=[0, .5, 1, 1.5, 2, 3, 5, 10, 20, 50, 100, 1e9])[0].tolist())
+# stragglers: long topology tests and when the kernel would end without them
+rest = d - tw
+for thr in (500, 1000, 2000, 5000, 10000):
+    sel = rest > thr
+    print(f"candidates with > {thr} us after the window test: {int(sel.sum())}, warp-ms {rest[sel].sum() / 1e3:.1f}")
+nolong = d[rest <= 1000]
+print("last decision among candidates without a long test: %.1f us; kernel span %.1f us" % (nolong.max(), span))
+dd = np.sort(d)
+for q in (0.99, 0.999, 0.9999):
+    print(f"decided by {q}: {dd[int(q * (m - 1))]:.1f} us")
