@@ -1933,9 +1933,9 @@ static constexpr int kBigLevels = 32;
 #define RCB_BFS_INLINE
 #endif
 #ifndef RCB_BFS_U
-#define RCB_BFS_U 3
+#define RCB_BFS_U 2
 #endif
-static constexpr int kBfsU = RCB_BFS_U;  // (site, neighbour) pairs in flight per lane
+static constexpr int kBfsU = RCB_BFS_U;  // (site, neighbour) pairs in flight per lane (cfg4 accept phase: 1: 42.8, 2: 39.1, 3: 39.6, 4: 42.3, 6: 45.4 ms)
 // kBig: the bounding-box map and the frontiers live in the warp's slot of
 // global memory (labels whose grown box exceeds the shared-memory map; run
 // after the hash tier overflowed, before deferring to an assist job).
