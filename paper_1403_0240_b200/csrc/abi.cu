@@ -677,7 +677,10 @@ static int32_t engine_score(rcb_engine *e) {
     RCB_TRY(contour_emit(e->L.p, lat, e->ocfg.full_fg, e->site_off.p, e->px.p, e->pown.p,
                          e->pcomp.p, s));
     cudaEventRecord(e->ev[1], s);
-    RCB_TRY(delta_int_batch(e->L.p, lat, e->px.p, e->pown.p, e->pcomp.p, n, e->dint.p, s));
+    // lam = 0 (every BASELINE config): rank = base + 0 * dint = base whatever
+    // the (finite, integer) dint holds, so the pass is skipped
+    if (e->ecfg.lam != 0.0)
+      RCB_TRY(delta_int_batch(e->L.p, lat, e->px.p, e->pown.p, e->pcomp.p, n, e->dint.p, s));
     const int poisson = e->ecfg.noise_model == 1;
     const bool fp32 = e->ocfg.fp32 != 0;
     if (fp32) RCB_TRY(e->raw32.reserve(n, s));
