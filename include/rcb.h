@@ -248,6 +248,18 @@ int32_t rcb_engine_score(rcb_engine *eng, rcb_slab_info *info);
 /* Second half, after every slab's [p0, p1) of base/cb0/sb0 is in place:
  * rank order, acceptance and bookkeeping (replicated on every rank). */
 int32_t rcb_engine_finish(rcb_engine *eng, rcb_iter_record *rec);
+/* z-slab sharded 3-D PS runs on integer images refresh the own-label fields of
+ * the slab plus its halo only and sum the exact band ledger over the slab:
+ * after finish, *pending = 1 means limbs[0 .. n_limbs) (int64, device memory,
+ * engine stream *stream) hold this rank's share of the iteration's energy
+ * change and rec->energy is still the previous energy.  The host sums the
+ * limbs over the ranks (one all-reduce of n_limbs int64: exact), writes the
+ * sums back and calls rcb_engine_band_apply, which rounds them once into the
+ * ledger (energy.py:233-257 semantics, as on one GPU) and returns the energy.
+ * With *pending = 0 nothing is to be done (band_apply returns the energy). */
+int32_t rcb_engine_band_limbs(rcb_engine *eng, void **limbs, int32_t *n_limbs, int32_t *pending,
+                              void **stream);
+int32_t rcb_engine_band_apply(rcb_engine *eng, double *energy);
 /* Particle index of the first site of each outer plane planes[i] (clamped
  * to [0, planes]); a slab [lo, hi) owns [out(lo), out(hi)). */
 int32_t rcb_engine_particle_ranges(rcb_engine *eng, const int64_t *planes, int32_t k,

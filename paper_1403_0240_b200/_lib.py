@@ -92,6 +92,8 @@ SIGNATURES = {
     "rcb_engine_set_slab": [_P, _I64, _I64],
     "rcb_engine_score": [_P, _P],
     "rcb_engine_finish": [_P, _P],
+    "rcb_engine_band_limbs": [_P, _P, _P, _P, _P],
+    "rcb_engine_band_apply": [_P, _P],
     "rcb_engine_particle_ranges": [_P, _P, _I32, _P],
     "rcb_synth_generate": [_I32, _P, _D, _P, _I32, _P, _I32, _I32, _D, C.c_uint64, _P, _P, _P],
     "rcb_synth_blur": [_P, _I32, _P, _P, _I32, _P],

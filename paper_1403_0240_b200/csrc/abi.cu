@@ -264,6 +264,12 @@ struct rcb_engine {
   // cfg4) the statistics are rebuilt from the raster when read
   bool int_image = false;
   bool srec_current = false;  // srec matches L / Cown / Sown / rho0 (kept so by the integer band refresh)
+  // z-slab sharded 3-D PS runs on integer images: the band refresh covers the
+  // slab plus the halo the energy kernel reads, the ledger is summed over the
+  // slab only and applied after the ranks' all-reduce (rcb_engine_band_apply)
+  BandSlab band_slab{0, 0, 0, 0};
+  bool fields_partial = false;  // own-label fields outside band_slab's planes are stale
+  bool band_pending = false;    // band[] holds this rank's ledger share, not yet applied
   bool stats_stale = false;
   bool ps_tiles = false;  // K5 on shared-memory tiles (RCB_K5=tile; measured slower)
 
@@ -642,6 +648,18 @@ static int32_t engine_score(rcb_engine *e) {
   e->iteration += 1;
   e->launches = 0;
   e->fields_fresh = false;
+  if (e->band_pending) return fail(RCB_ERR_VALUE, "rcb_engine_band_apply not called after finish");
+  if (e->fields_partial) {
+    const int64_t halo = e->stencil_reach + e->ecfg.smooth_radius;
+    const bool same = e->mode == 1 && e->slab_hi > e->slab_lo &&
+                      e->band_slab.own0 == e->slab_lo && e->band_slab.own1 == e->slab_hi &&
+                      e->band_slab.z0 == e->slab_lo - halo;
+    if (!same) {  // l2 mode reads fields anywhere; another slab needs other planes
+      RCB_TRY(e->refresh());
+      e->fields_partial = false;
+      e->srec_current = false;
+    }
+  }
   cudaEventRecord(e->ev[0], s);
   if (!e->prepared) RCB_TRY(e->prepare());
   const int64_t n = e->N;
@@ -1025,6 +1043,14 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       X.I16 = e->I16.p;
       X.srec = e->srec.p;  // null unless K5 reads packed site records
       X.srec_current = &e->srec_current;
+      if (e->slab_hi > e->slab_lo && lat.ndim == 3 && e->ecfg.region_model == 1 && e->mode == 1 &&
+          e->I16.p && e->rho0.p && !getenv("RCB_SLAB_BAND_OFF")) {
+        const int64_t halo = e->stencil_reach + e->ecfg.smooth_radius;
+        e->band_slab = BandSlab{e->slab_lo - halo, e->slab_hi + halo, e->slab_lo, e->slab_hi};
+        X.band_slab = &e->band_slab;
+        e->fields_partial = true;
+        e->band_pending = true;
+      }
       X.chain_pool = &e->chain_pool;
       {
         const char *ds = getenv("RCB_DEFER_STATS");  // "0": eager sum chains (comparison runs)
@@ -1204,6 +1230,29 @@ int32_t rcb_engine_finish(rcb_engine *e, rcb_iter_record *rec) {
   return engine_finish(e, rec);
 }
 
+int32_t rcb_engine_band_limbs(rcb_engine *e, void **limbs, int32_t *n_limbs, int32_t *pending,
+                              void **stream) {
+  *limbs = e->band.p;
+  *n_limbs = kLimbs;
+  *pending = e->band_pending ? 1 : 0;
+  *stream = (void *)e->s;
+  return RCB_OK;
+}
+
+int32_t rcb_engine_band_apply(rcb_engine *e, double *energy) {
+  if (e->poisoned) return fail(RCB_ERR_CUDA, e->poison_msg);
+  RCB_CUDA(cudaSetDevice(e->device));
+  if (e->band_pending) {
+    RCB_TRY(band_ledger_apply(e->band.p, e->ecfg.lam, &e->sc.p->energy, e->s));
+    e->band_pending = false;
+  }
+  RCB_CUDA(cudaMemcpyAsync(&e->hsc->energy, &e->sc.p->energy, sizeof(double),
+                           cudaMemcpyDeviceToHost, e->s));
+  RCB_CUDA(cudaStreamSynchronize(e->s));
+  *energy = e->hsc->energy;
+  return RCB_OK;
+}
+
 int32_t rcb_engine_particle_ranges(rcb_engine *e, const int64_t *planes, int32_t k, int64_t *out) {
   RCB_CUDA(cudaSetDevice(e->device));
   for (int32_t i = 0; i < k; i += 4) RCB_TRY(plane_ranges(e, planes + i, std::min(4, k - i), out + i));
@@ -1333,6 +1382,7 @@ int32_t rcb_engine_refresh(rcb_engine *e) {
   RCB_TRY(e->refresh());
   RCB_CUDA(cudaStreamSynchronize(e->s));
   e->fields_fresh = true;
+  e->fields_partial = false;
   e->srec_current = false;  // the rebuild rewrote Cown / Sown / rho0
   return RCB_OK;
 }

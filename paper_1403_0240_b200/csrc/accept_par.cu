@@ -4325,6 +4325,14 @@ __global__ void k_band_ledger(const long long *__restrict__ band, double lam,
   *energy = *energy + (dext + lam * (double)band[kLimbs]);
 }
 
+// The ledger step alone (z-slab sharded runs apply it after the ranks summed
+// their band limbs).
+int32_t band_ledger_apply(const long long *band, double lam, double *energy, cudaStream_t s) {
+  k_band_ledger<<<1, 32, 0, s>>>(band, lam, energy);
+  RCB_CUDA(cudaGetLastError());
+  return RCB_OK;
+}
+
 size_t accept_par_smem() { return sizeof(BfsShared); }
 
 // RCB_PROFILE=1: warm per-stage device times of the acceptance (stderr).
@@ -4798,12 +4806,15 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     if (fresh) RCB_CUDA(cudaMemsetAsync(X.tflag->p, 0, X.tflag->cap, s));
     RCB_TRY(fields_band3d(X.acc, X.moves, X.Lmut, X.I, X.I16, A.lat, X.ball_full, X.nball_full, X.radius,
                           X.dirty, X.tflag->p, X.Cown, X.Sown, X.rho0, X.poisson,
-                          band_ledger ? X.band : nullptr, s, X.srec));
+                          band_ledger ? X.band : nullptr, s, X.srec,
+                          X.I16 ? X.band_slab : nullptr));
     if (X.I16 && X.srec && X.rho0 && X.srec_current) *X.srec_current = true;
     nl += 3;
     if (band_ledger) {
       if (X.lam != 0.0) k_dint_sum<<<grid_for(N, 256), 256, 0, s>>>(A, X.moves, X.band);
-      k_band_ledger<<<1, 32, 0, s>>>(X.band, X.lam, X.energy);
+      // slab-local refresh: band[] holds this rank's share; the ranks sum the
+      // limbs and apply them once (rcb_engine_band_apply)
+      if (!(X.I16 && X.band_slab)) k_band_ledger<<<1, 32, 0, s>>>(X.band, X.lam, X.energy);
       nl += 2;
     }
   } else if (X.region_ps) {

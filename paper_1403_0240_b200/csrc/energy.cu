@@ -383,7 +383,11 @@ static constexpr int kBiPS = kBiX + 2 * kT3R + 1;  // row stride (odd: conflict-
 __global__ void __launch_bounds__(256) k_fields_band3d_int(
     const int32_t *__restrict__ L, const uint16_t *__restrict__ I16, int nx, int ny, int nz, int R,
     const uint8_t *__restrict__ tflag, int32_t *__restrict__ Cown, double *__restrict__ Sown,
-    double *__restrict__ rho0, int poisson, long long *__restrict__ band, int4 *__restrict__ rec) {
+    double *__restrict__ rho0, int poisson, long long *__restrict__ band, int4 *__restrict__ rec,
+    int ztile0, int ntz_all, int own_z0, int own_z1) {
+  // ztile0 / gridDim.z: the z-tiles to refresh (a rank of a z-slab sharded run
+  // refreshes its slab plus the halo its energy kernel reads); [own_z0, own_z1):
+  // the planes whose ledger terms this call sums (the rank's own slab).
   constexpr int SY = kBiY + 2 * kT3R, SZ = kBiZ + 2 * kT3R;
   extern __shared__ __align__(16) uint32_t bi_smem[];
   uint32_t *sW = bi_smem;                   // label | I << 16 (0xffff: outside the lattice)
@@ -391,11 +395,12 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
   __shared__ int2 srow[(2 * kT3R + 1) * (2 * kT3R + 1)];  // per ball row: offsets of the two prefix entries
   __shared__ int nrow, s_pick;
   __shared__ long long sm[kLimbs];
-  const int ntx = gridDim.x, nty = gridDim.y, ntz = gridDim.z;
+  const int ntx = gridDim.x, nty = gridDim.y, ntz = ntz_all;
+  const int bz = (int)blockIdx.z + ztile0;
   if (tflag) {  // null: every tile (the full rebuild), every site written
     bool any = false;
     if (threadIdx.x < 27) {
-      const int tz = (int)blockIdx.z + (int)threadIdx.x / 9 - 1;
+      const int tz = bz + (int)threadIdx.x / 9 - 1;
       const int ty = (int)blockIdx.y + ((int)threadIdx.x / 3) % 3 - 1;
       const int tx = (int)blockIdx.x + (int)threadIdx.x % 3 - 1;
       if ((unsigned)tz < (unsigned)ntz && (unsigned)ty < (unsigned)nty && (unsigned)tx < (unsigned)ntx)
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
     if (!__syncthreads_or(any)) return;
   }
   const int tx = threadIdx.x % kBiX, ty = (threadIdx.x / kBiX) % kBiY, tz = threadIdx.x / (kBiX * kBiY);
-  const int x0 = blockIdx.x * kBiX, y0 = blockIdx.y * kBiY, z0 = blockIdx.z * kBiZ;
+  const int x0 = blockIdx.x * kBiX, y0 = blockIdx.y * kBiY, z0 = bz * kBiZ;
   const int x = x0 + tx, y = y0 + ty;
   const int hx = kBiX + 2 * R, hy = kBiY + 2 * R, hz = kBiZ + 2 * R;
   if (threadIdx.x == 0) {  // the ball as x-runs per (dz, dy): |o|^2 <= R^2
@@ -530,8 +535,11 @@ __global__ void __launch_bounds__(256) k_fields_band3d_int(
       }
     }
     if (band && changed) {
-      stage.add(sm, -oldr);
-      stage.add(sm, newr);
+      const int zz = z0 + tz + kBiZT * j;
+      if (zz >= own_z0 && zz < own_z1) {
+        stage.add(sm, -oldr);
+        stage.add(sm, newr);
+      }
     }
   }
   if (band) {  // every thread of the block reaches here (warp-uniform)
@@ -546,7 +554,8 @@ static size_t band3d_int_smem() {
 
 static int32_t launch_band3d_int(const int32_t *L, const uint16_t *I16, const Lat &lat, int R,
                                  const uint8_t *tflag, int32_t *Cown, double *Sown, double *rho0,
-                                 int poisson, long long *band, int4 *rec, cudaStream_t s) {
+                                 int poisson, long long *band, int4 *rec, cudaStream_t s,
+                                 const BandSlab *slab = nullptr) {
   static bool attr[64] = {};
   int dev = 0;
   RCB_CUDA(cudaGetDevice(&dev));
@@ -555,11 +564,22 @@ static int32_t launch_band3d_int(const int32_t *L, const uint16_t *I16, const La
                                   (int)band3d_int_smem()));
     attr[dev] = true;
   }
+  const int ntz = (int)((lat.nz + kBiZ - 1) / kBiZ);
+  int zt0 = 0, ztn = ntz, oz0 = 0, oz1 = (int)lat.nz;
+  if (slab) {  // tiles meeting planes [z0, z1), ledger over [own0, own1)
+    zt0 = (int)(std::max<int64_t>(slab->z0, 0) / kBiZ);
+    const int zt1 = (int)((std::min<int64_t>(slab->z1, lat.nz) + kBiZ - 1) / kBiZ);
+    ztn = zt1 > zt0 ? zt1 - zt0 : 0;
+    oz0 = (int)slab->own0;
+    oz1 = (int)slab->own1;
+    if (ztn == 0) return RCB_OK;
+  }
   dim3 grid((unsigned)((lat.nx + kBiX - 1) / kBiX), (unsigned)((lat.ny + kBiY - 1) / kBiY),
-            (unsigned)((lat.nz + kBiZ - 1) / kBiZ));
+            (unsigned)ztn);
   k_fields_band3d_int<<<grid, 256, band3d_int_smem(), s>>>(L, I16, (int)lat.nx, (int)lat.ny,
                                                            (int)lat.nz, R, tflag, Cown, Sown, rho0,
-                                                           poisson, band, rho0 ? rec : nullptr);
+                                                           poisson, band, rho0 ? rec : nullptr, zt0,
+                                                           ntz, oz0, oz1);
   RCB_CUDA(cudaGetLastError());
   return RCB_OK;
 }
@@ -600,12 +620,13 @@ int64_t band3d_tiles(const Lat &lat) {
 int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
                       const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
                       int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
-                      double *rho0, int poisson, long long *band, cudaStream_t s, int4 *rec) {
+                      double *rho0, int poisson, long long *band, cudaStream_t s, int4 *rec,
+                      const BandSlab *slab) {
   if (I16) {
     // integer image: prefix-sum ball runs on 16 x 8 x 8 tiles (the caller
     // checked the ranges); only the tile flags are marked, no per-site map
     k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 1, nullptr, tflag, kBiX, kBiY, kBiZ);
-    RCB_TRY(launch_band3d_int(L, I16, lat, R, tflag, Cown, Sown, rho0, poisson, band, rec, s));
+    RCB_TRY(launch_band3d_int(L, I16, lat, R, tflag, Cown, Sown, rho0, poisson, band, rec, s, slab));
     k_mark_flips<<<148 * 8, 256, 0, s>>>(acc, moves, lat, 0, nullptr, tflag, kBiX, kBiY, kBiZ);
     RCB_CUDA(cudaGetLastError());
     return RCB_OK;

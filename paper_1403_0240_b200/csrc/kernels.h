@@ -155,6 +155,11 @@ struct PendingChain {
   int32_t nl = 0;
 };
 
+// z-slab sharded runs (integer band refresh): refresh the tiles meeting planes
+// [z0, z1) and sum the band ledger over planes [own0, own1) only
+struct BandSlab {
+  int64_t z0, z1, own0, own1;
+};
 struct ParExtra {
   int64_t n_particles, budget;
   unsigned long long *hcount = nullptr;  // the engine's pinned word (candidate-list count)
@@ -173,6 +178,7 @@ struct ParExtra {
   const uint16_t *I16 = nullptr;   // integer image, 16 bits per site (integer band refresh), or null
   int4 *srec = nullptr;            // K5's packed site records, kept current by the integer band refresh
   bool *srec_current = nullptr;    // set when the band refresh left srec current
+  const BandSlab *band_slab = nullptr;  // slab-local band refresh; the ledger stays in band[] for the ranks' all-reduce
   int32_t *Cown;
   double *Sown;
   double *rho0;
@@ -255,11 +261,12 @@ int32_t fields_tile3d(const int32_t *L, const double *I, const Lat &lat, const O
                       double *rho0, int poisson, long long *band, cudaStream_t s);
 bool fields_tile3d_ok(const Lat &lat, int R, int nball_full);
 int64_t band3d_tiles(const Lat &lat);
+int32_t band_ledger_apply(const long long *band, double lam, double *energy, cudaStream_t s);
 int32_t fields_band3d(const int64_t *acc, const int64_t *moves, const int32_t *L, const double *I,
                       const uint16_t *I16, const Lat &lat, const Off *ball_full, int nball_full,
                       int R, uint8_t *flips, uint8_t *tflag, int32_t *Cown, double *Sown,
                       double *rho0, int poisson, long long *band, cudaStream_t s,
-                      int4 *rec = nullptr);
+                      int4 *rec = nullptr, const BandSlab *slab = nullptr);
 // integer image as 16-bit words (the integer band refresh reads 2 B per site)
 int32_t image_u16(const double *I, int64_t V, uint16_t *I16, cudaStream_t s);
 int32_t delta_ps_batch(const int32_t *L, const double *I, const int32_t *Cown, const double *Sown,

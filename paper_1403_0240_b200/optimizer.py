@@ -263,6 +263,10 @@ class RegionCompetition:
             self._exchange.gather(self._slab.buffers(info, self.device), self._slab.ranges(),
                                   stream=info.stream)
             rec = self._slab.finish()
+            limbs, st = self._slab.band_limbs(self.device)
+            if limbs is not None:  # slab-local band refresh: sum the ledger shares
+                self._exchange.reduce_limbs(limbs, stream=st)
+                rec = self._slab.band_apply(rec)
         return self._post_iterate(rec, t0)
 
     def attach_slab(self, slab, exchange) -> None:

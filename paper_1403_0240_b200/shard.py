@@ -81,7 +81,7 @@ class _CudaArray:
 
 def device_view(ptr: int, n: int, dtype, device: int):
     import torch
-    typestr = {np.float64: "<f8", np.int32: "<i4"}[np.dtype(dtype).type]
+    typestr = {np.float64: "<f8", np.int32: "<i4", np.int64: "<i8"}[np.dtype(dtype).type]
     return torch.as_tensor(_CudaArray(ptr, n, typestr), device=f"cuda:{device}")
 
 
@@ -129,6 +129,13 @@ class TorchExchange:
                     w = v.shape[1]
                     v[a:b] = recv[r][:b - a, col:col + w]
                     col += w
+
+    def reduce_limbs(self, limbs, stream=None) -> None:
+        """Sum the ranks' band-ledger limbs in place (int64: exact)."""
+        import torch
+        ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream)) if stream else _null()
+        with ctx:
+            self.dist.all_reduce(limbs, op=self.dist.ReduceOp.SUM, group=self.group)
 
     def _global(self, r: int) -> int:
         if self.group is None:
@@ -181,6 +188,25 @@ class SlabState:
         _lib.check(_lib.lib.rcb_engine_finish(self.engine._h, C.byref(rec)))
         return rec
 
+    def band_limbs(self, device: int):
+        """(limbs tensor, stream) when this iteration's band ledger is still
+        to be summed over the ranks (slab-local band refresh: 3-D PS runs on
+        integer images), else (None, stream)."""
+        ptr, n, pend, st = C.c_void_p(), C.c_int32(), C.c_int32(), C.c_void_p()
+        _lib.check(_lib.lib.rcb_engine_band_limbs(self.engine._h, C.byref(ptr), C.byref(n),
+                                                   C.byref(pend), C.byref(st)))
+        if not pend.value:
+            return None, st.value
+        return device_view(ptr.value, n.value, np.int64, device), st.value
+
+    def band_apply(self, rec):
+        """Round the (summed) limbs into the ledger; rec.energy becomes the
+        iteration's energy."""
+        e = C.c_double()
+        _lib.check(_lib.lib.rcb_engine_band_apply(self.engine._h, C.byref(e)))
+        rec.energy = e.value
+        return rec
+
 
 def slab_engine(image, init_labels, energy_config, sobolev_params=None, config=None, conn=None,
                 *, group=None, device=None):
@@ -228,4 +254,13 @@ class LocalSlabGroup:
                     for dst, src in zip(bufs[j], bufs[r]):
                         dst[a:b].copy_(src[a:b])
         torch.cuda.synchronize()
-        return [e._post_iterate(s.finish(), t) for e, s, t in zip(self.engines, self.slabs, t0)]
+        recs = [s.finish() for s in self.slabs]
+        limbs = [s.band_limbs(e.device)[0] for s, e in zip(self.slabs, self.engines)]
+        if any(l is not None for l in limbs):  # the ranks' all-reduce, in one process
+            torch.cuda.synchronize()
+            total = sum(l.clone() for l in limbs)
+            for l in limbs:
+                l.copy_(total)
+            torch.cuda.synchronize()
+            recs = [s.band_apply(r) for s, r in zip(self.slabs, recs)]
+        return [e._post_iterate(r, t) for e, r, t in zip(self.engines, recs, t0)]

@@ -79,3 +79,31 @@ def test_slab_engine_pairs_partition(P):
     group.iterate()
     assert sum(e.last_pairs for e in group.engines) == ref.last_pairs
     assert all(e.last_pairs < ref.last_pairs for e in group.engines)
+
+
+def test_slab_band_refresh_through_resync_and_l2_switch(P):
+    """3-D PS on integer data: each slab engine refreshes the own-label fields of
+    its slab plus halo only and sums the band ledger over its slab; the shares
+    are added exactly (int64 limbs) and rounded once.  Records must equal the
+    unsharded engine's through a resync (full rebuild, iteration 10) and after
+    the switch to l2 mode, whose acceptance reads the fields everywhere (the
+    engines rebuild them in full first)."""
+    from paper_1403_0240_b200.shard import LocalSlabGroup
+    sc = scenes.cfg4(n=64, n_obj=8, per_axis=2)
+    ref = _make(P, sc)
+    group = LocalSlabGroup([_make(P, sc) for _ in range(3)])
+    for it in range(14):
+        if it == 11:
+            ref.mode = "l2"
+            for e in group.engines:
+                e.mode = "l2"
+        want = ref.iterate()
+        got = group.iterate()
+        acc = ref.last_accepted
+        for g, eng in zip(got, group.engines):
+            assert (g.iteration, g.energy, g.moves, g.particles) == \
+                (want.iteration, want.energy, want.moves, want.particles), it
+            assert np.array_equal(eng.last_accepted, acc), it
+    lab = ref.labels
+    for eng in group.engines:
+        assert np.array_equal(eng.labels, lab)
