@@ -96,8 +96,16 @@ def _worker(rank, world, port, q):
         bufs[2][p0:p1] = sb0[p0:p1]
         tens = [torch.from_numpy(b) for b in bufs]
         TorchExchange().gather(tens, ranges)
+        # the band-ledger shares: int64 limbs (with negative parts) summed exactly
+        limb_rng = np.random.default_rng(100 + rank)
+        mine = limb_rng.integers(-2 ** 40, 2 ** 40, size=68).astype(np.int64)
+        want = sum(np.random.default_rng(100 + r).integers(-2 ** 40, 2 ** 40, size=68).astype(np.int64)
+                   for r in range(world))
+        limbs = torch.from_numpy(mine.copy())
+        TorchExchange().reduce_limbs(limbs)
+        ok_limbs = bool(np.array_equal(limbs.numpy(), want))
         q.put((rank, bool(np.array_equal(bufs[0], smooth) and np.array_equal(bufs[1], cb0)
-                          and np.array_equal(bufs[2], sb0)), ranges))
+                          and np.array_equal(bufs[2], sb0)) and ok_limbs, ranges))
     finally:
         dist.destroy_process_group()
 
