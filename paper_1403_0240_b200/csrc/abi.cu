@@ -1116,7 +1116,11 @@ static int32_t engine_finish(rcb_engine *e, rcb_iter_record *rec) {
       RCB_TRY(accept_seq(A, s));
   launches += 1;
     }
-    launches += 4 + 1 + 3 * 8;  // emit, dint, dE, rank, 2 radix sorts (~8 passes each)
+    // K1 emit, the energy kernel, k_rank, the 32-bit key sort (histogram,
+    // exclusive sum, four onesweep passes), k_tie_runs; + dE_int when lam != 0.
+    // (ncu launch lists: 35 launches per cfg4 iteration, 41 per cfg2 iteration;
+    // this count gives 39 and 38)
+    launches += 10 + (e->ecfg.lam != 0.0 ? 1 : 0);
   } else {
     cudaEventRecord(e->ev[4], s);
   }
