@@ -1687,16 +1687,19 @@ __device__ __forceinline__ void q_register(const ParArgs &A, int64_t f, int32_t 
   atomicAdd((unsigned long long *)(A.job + 41), 1ull);
 }
 
+// clear last run's registrations (grid-stride: up-front registration can list
+// every candidate of several labels) ...
 __global__ void k_q_reset(ParArgs A) {
-  // clear last run's registrations, then the job state (one block)
   const uint32_t n = (uint32_t)A.job[40];
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t y = A.qlist[i];
     const uint32_t l = (uint32_t)A.qmark[y];
     if (l != 0xffffffffu) A.qstate[2 * l] = 0;
     A.qmark[y] = ~0ull;
   }
-  __syncthreads();
+}
+// ... then the job state
+__global__ void k_q_reset_job(ParArgs A) {
   if (threadIdx.x < 8) A.job[40 + threadIdx.x] = 0;
 }
 
@@ -4630,7 +4633,8 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     // blocks.  (A plain launch measured 4.1 vs 3.9 images/s on batched cfg5.)
     RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(nblk), dim3(32 * kDfWarps),
                                          args, dsm, s));
-    k_q_reset<<<1, 1024, 0, s>>>(A);  // clear this run's deferred registry
+    k_q_reset<<<148, 1024, 0, s>>>(A);  // clear this run's deferred registry
+    k_q_reset_job<<<1, 32, 0, s>>>(A);
   }
   T.mark("decide");
   k_acc_flags<<<grid_for(N + 1, 256), 256, 0, s>>>(A.dec, A.nneg, X.slot);
