@@ -1938,7 +1938,10 @@ static constexpr int kBigLevels = 32;
 #ifndef RCB_BFS_U
 #define RCB_BFS_U 2
 #endif
-static constexpr int kBfsU = RCB_BFS_U;  // (site, neighbour) pairs in flight per lane (cfg4 accept phase: 1: 42.8, 2: 39.1, 3: 39.6, 4: 42.3, 6: 45.4 ms)
+#ifndef RCB_BFS_U2D
+#define RCB_BFS_U2D 2
+#endif
+static constexpr int kBfsU3 = RCB_BFS_U, kBfsU2 = RCB_BFS_U2D;  // (site, neighbour) pairs in flight per lane (cfg4 accept phase: 1: 42.8, 2: 39.1, 3: 39.6, 4: 42.3, 6: 45.4 ms)
 // kBig: the bounding-box map and the frontiers live in the warp's slot of
 // global memory (labels whose grown box exceeds the shared-memory map; run
 // after the hash tier overflowed, before deferring to an assist job).
@@ -1966,6 +1969,7 @@ __device__ RCB_BFS_INLINE int warp_bfs(const ParArgs &A, WarpBfs &S, int32_t pos
   const int fz = k3D ? (int)(f / nxy) : 0, frem = (int)(f - (int64_t)fz * nxy);
   const int fy = frem / nx, fx = frem - fy * nx;
   constexpr int kNb = k3D ? 26 : 8;
+  constexpr int kBfsU = k3D ? kBfsU3 : kBfsU2;
   uint32_t *nib = kBig ? A.bigmap + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) *
                                          (int64_t)A.big_words
                        : reinterpret_cast<uint32_t *>(S.key);
@@ -2884,6 +2888,10 @@ __device__ __noinline__ int warp_window5(const ParArgs &A, int32_t pos, int z, i
 }
 
 
+// Two instantiations, one per lattice dimension: `is3` folds at compile time, so
+// the 2-D kernel carries no 3-D window / flood code and vice versa (separate
+// register allocations; the 2-D floods take wider load batches, see kBfsU).
+template <bool K3D>
 __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_constant__ ParArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpBfs &S = reinterpret_cast<WarpBfs *>(smem_raw)[threadIdx.x >> 5];
@@ -2901,7 +2909,7 @@ __global__ void __launch_bounds__(32 * kDfWarps, 1) k_accept_df(const __grid_con
   // a position held behind a warp stuck in a long BFS stalls its dependants.
   int32_t pos = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(ctl + 12, 1) : 0, 0);
   int4 rc = pos < M ? __ldg(A.rec + pos) : make_int4(0, 0, 0, 0);
-  const bool is3 = lat.ndim == 3;
+  constexpr bool is3 = K3D;
   // The box of the NEXT position is loaded while the current decision is
   // published (its labels L are static, and a site word that already shows
   // pend >= next position is final): the ~1 us box round trip leaves the
@@ -4523,11 +4531,16 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     int &df_blocks = df_blocks_dev[cur_dev];
     const size_t dsm = sizeof(WarpBfs) * kDfWarps;
     if (df_blocks == 0) {
-      RCB_CUDA(cudaFuncSetAttribute(k_accept_df, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      RCB_CUDA(cudaFuncSetAttribute(k_accept_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)dsm));
-      int per_sm = 0, dev = 0, sms = 0;
-      RCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accept_df, 32 * kDfWarps,
-                                                             dsm));
+      RCB_CUDA(cudaFuncSetAttribute(k_accept_df<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      int per_sm = 0, per_sm2 = 0, dev = 0, sms = 0;
+      RCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accept_df<true>,
+                                                             32 * kDfWarps, dsm));
+      RCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_accept_df<false>,
+                                                             32 * kDfWarps, dsm));
+      per_sm = std::min(per_sm, per_sm2);
       RCB_CUDA(cudaGetDevice(&dev));
       RCB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       if (per_sm < 1) return fail(RCB_ERR_CUDA, "k_accept_df does not fit on an SM");
@@ -4631,8 +4644,9 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
     // of the grid (warp_idle_help), so with a plain launch several engines
     // whose blocks do not all fit could wait on one another's unscheduled
     // blocks.  (A plain launch measured 4.1 vs 3.9 images/s on batched cfg5.)
-    RCB_CUDA(cudaLaunchCooperativeKernel((void *)k_accept_df, dim3(nblk), dim3(32 * kDfWarps),
-                                         args, dsm, s));
+    RCB_CUDA(cudaLaunchCooperativeKernel(
+        A.lat.ndim == 3 ? (void *)k_accept_df<true> : (void *)k_accept_df<false>, dim3(nblk),
+        dim3(32 * kDfWarps), args, dsm, s));
     k_q_reset<<<148, 1024, 0, s>>>(A);  // clear this run's deferred registry
     k_q_reset_job<<<1, 32, 0, s>>>(A);
   }
