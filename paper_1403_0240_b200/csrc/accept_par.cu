@@ -1688,7 +1688,8 @@ __device__ __forceinline__ void q_register(const ParArgs &A, int64_t f, int32_t 
 }
 
 // clear last run's registrations (grid-stride: up-front registration can list
-// every candidate of several labels) ...
+// every candidate of several labels); the last block to finish clears the
+// job state (job[44] counts finished blocks and is cleared with it)
 __global__ void k_q_reset(ParArgs A) {
   const uint32_t n = (uint32_t)A.job[40];
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -1697,10 +1698,14 @@ __global__ void k_q_reset(ParArgs A) {
     if (l != 0xffffffffu) A.qstate[2 * l] = 0;
     A.qmark[y] = ~0ull;
   }
-}
-// ... then the job state
-__global__ void k_q_reset_job(ParArgs A) {
-  if (threadIdx.x < 8) A.job[40 + threadIdx.x] = 0;
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(A.job + 44, 1ull) == (unsigned long long)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 8) A.job[40 + threadIdx.x] = 0;
 }
 
 // Warp-level wait until every lane's site g (or -1) is settled for V_pos (no
@@ -4648,7 +4653,6 @@ int32_t accept_par(ParArgs A, const ParExtra &X, cudaStream_t s, int *launches) 
         A.lat.ndim == 3 ? (void *)k_accept_df<true> : (void *)k_accept_df<false>, dim3(nblk),
         dim3(32 * kDfWarps), args, dsm, s));
     k_q_reset<<<148, 1024, 0, s>>>(A);  // clear this run's deferred registry
-    k_q_reset_job<<<1, 32, 0, s>>>(A);
   }
   T.mark("decide");
   k_acc_flags<<<grid_for(N + 1, 256), 256, 0, s>>>(A.dec, A.nneg, X.slot);
